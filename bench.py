@@ -1,0 +1,294 @@
+"""Benchmark: MSC d=5 (proxy) shots/s on 1..8 B200, p=1e-3, post-selection.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step = one persistent-kernel launch that samples ``--shots-per-step`` shots
+per GPU (weak scaling: rank r takes global shots [step*N*S + r*S, +S)).
+Timing: barrier + synchronize on both sides of the K timed steps; every step
+is bracketed by CUDA events on the launching stream; L2 is flushed (256 MiB
+write) between steps outside the events; the max over ranks is reported.
+
+Extra keys: ``roofline`` (state-touch model bytes counted on device / kernel
+time vs measured HBM copy bandwidth), ``cpu_baseline`` (the CPU oracle port
+timed on this host's cores, rank 0, bounded sample), ``e2e`` (the public
+C-ABI path with host buffers: program upload + launch + counter readback),
+``clocks`` (nvidia-smi sampled during the timed region) and
+``gpu_launches``.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MSC d=5 shots/sec at 1/2/4/8 B200 (vs CPU ref); achieved HBM GB/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def _peaks():
+    try:
+        with open(PEAKS) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _workload(d: int, p: float):
+    from paper_2512_23037_b200.msc import msc_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    from paper_2512_23037_b200.circuit import compute_stats
+    base = msc_circuit(d)
+    return apply_noise_model(base, p), compute_stats(base).as_dict()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = sorted(float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit())
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(self.rows), "reasons": sorted(reasons)}
+
+
+def cpu_baseline(prog, seconds: float, mode: str, p_noise: float):
+    """Time the CPU oracle port on all host cores for a bounded sample."""
+    from oracle import gstab_oracle as orc
+    cores = os.cpu_count() or 1
+    # calibrate on one core, then size the parallel sample to ~`seconds`
+    t0 = time.perf_counter()
+    orc.run_counters(prog, 16, 1, mode=mode, postselect=True)
+    per_shot = max((time.perf_counter() - t0) / 16, 1e-5)
+    shots = max(cores * 8, int(seconds * cores / per_shot))
+    t0 = time.perf_counter()
+    c = orc.run_counters_parallel(prog, shots, cores, master_seed=1, mode=mode,
+                                  postselect=True)
+    dt = time.perf_counter() - t0
+    return {"value": c["total"] / dt, "unit": "shots/s", "cores": cores,
+            "kind": "port",
+            "sample": "%d shots of the same workload (oracle/gstab_oracle.py, "
+                      "%d processes, %.1f s)" % (c["total"], cores, dt),
+            "discard_rate": c["discarded"] / max(c["total"], 1)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--shots-per-step", type=int, default=1 << 22)
+    ap.add_argument("--d", type=int, default=5)
+    ap.add_argument("--p", type=float, default=1e-3)
+    ap.add_argument("--rng", default="philox", choices=["philox", "splitmix"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--chi-global", action="store_true")
+    ap.add_argument("--wpb", type=int, default=0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    prog, stats = _workload(args.d, args.p)
+    workload = "msc_d%d_proxy" % args.d
+    config = {"workload": workload, "noise_p": args.p, "postselect": True,
+              "rng": args.rng, "shots_per_step_per_gpu": args.shots_per_step,
+              "circuit": stats, "parallelism": "shot-dp%d" % world,
+              "l2": "flushed between steps (256 MiB write, untimed)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        vals = []
+        samples = []
+        for _ in range(args.warmup + args.steps):
+            cb = cpu_baseline(prog, max(2.0, args.cpu_seconds / 3), args.rng, args.p)
+            vals.append(cb["value"])
+            samples.append(cb)
+        v = sorted(vals[args.warmup:])[len(vals[args.warmup:]) // 2]
+        cb = samples[-1]
+        cb["value"] = v
+        line = {"metric": METRIC, "value": v, "unit": "shots/s", "impl": "reference",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000.0 / v if v else None, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded Philox noise on the generated MSC proxy)",
+                "config": config, "cpu_baseline": cb,
+                "e2e": {"value": v, "unit": "shots/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2512_23037_b200 import _lib
+    from paper_2512_23037_b200.compiler import compile_program
+    from paper_2512_23037_b200.engine import Engine, Program
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dp = compile_program(prog)
+    P = Program(dp)
+    eng = Engine(local)
+    flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if args.rng == "philox" else 0)
+    if args.chi_global:
+        flags |= _lib.GS_CHI_GLOBAL
+    S = args.shots_per_step
+    nc = P.num_counters
+    stream = torch.cuda.current_stream()
+    counters = torch.zeros(nc, dtype=torch.int64, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def launch(step):
+        base = step * world * S + rank * S
+        par = Engine.params(12345, base, S, 32768, flags, warps_per_block=args.wpb)
+        eng.run_counters_async(P, par, counters.data_ptr(), stream.cuda_stream)
+
+    for w in range(args.warmup):
+        launch(w)
+    torch.cuda.synchronize()
+    counters.zero_()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = eng.launches
+    t_wall = time.perf_counter()
+    for s in range(args.steps):
+        flush.zero_()
+        ev[s][0].record(stream)
+        launch(args.warmup + s)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall = time.perf_counter() - t_wall
+    ck = clocks.stop()
+    kernel_ms = [a.elapsed_time(b) for a, b in ev]
+    my_ms = sum(kernel_ms)
+    launches = eng.launches - launches0
+    if world > 1:
+        t = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.all_reduce(counters)            # the one data-path collective
+    else:
+        tot_ms = my_ms
+    c = counters.cpu().numpy()
+    total_shots = int(c[_lib.GS_C_TOTAL])
+    value = total_shots / (tot_ms * 1e-3)
+    model_bytes = int(c[_lib.GS_C_MODEL_BYTES])
+    peak, peak_src = _peaks()
+    # roofline of the (only) kernel: algorithmic state-touch bytes / time,
+    # per GPU (each rank's kernel sees its own shots)
+    achieved = (model_bytes / world) / (my_ms * 1e-3) / 1e9
+
+    e2e = None
+    cb = None
+    if rank == 0:
+        # e2e through the public C ABI with host buffers: every step creates
+        # the program (host->device upload of the op stream) and reads the
+        # counters back (device->host) inside the timed region
+        h2d = int(dp.ops.nbytes + dp.tables.nbytes + dp.locs.nbytes)
+        d2h = nc * 8
+        times = []
+        for s in range(max(2, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            Pe = Program(dp)
+            par = Engine.params(777, s * S, S, 32768, flags, warps_per_block=args.wpb)
+            out = eng.run_counters(Pe, par)
+            times.append(time.perf_counter() - t0)
+            del Pe
+        e2e = {"value": S / (sorted(times)[len(times) // 2]), "unit": "shots/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "gs_program_create + gs_run_counters (host buffers)"}
+        if not args.no_cpu_baseline:
+            cb = cpu_baseline(prog, args.cpu_seconds, args.rng, args.p)
+        line = {
+            "metric": METRIC, "value": value, "unit": "shots/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded %s noise on the generated MSC proxy)" % args.rng,
+            "config": config,
+            "discard_rate": int(c[_lib.GS_C_DISCARDED]) / max(total_shots, 1),
+            "logical_error_shots": int(c[_lib.GS_C_ERROR_SHOTS]),
+            "preserved": int(c[_lib.GS_C_PRESERVED]),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_src,
+                         "model_bytes_per_shot": model_bytes / max(total_shots, 1),
+                         "note": "SURVEY 8(d) state-touch model; chi is SM-resident"},
+            "cpu_baseline": cb, "e2e": e2e, "clocks": ck,
+            "gpu_launches": int(launches), "kernel_ms": kernel_ms,
+            "wall_s": t_wall,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

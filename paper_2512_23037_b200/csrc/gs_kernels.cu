@@ -1,0 +1,1257 @@
+// gs_kernels.cu -- B200 (sm_100a) shot-parallel generalized-stabilizer sampler.
+//
+// One warp simulates one shot at a time (persistent grid, atomic shot queue).
+// The per-shot state is the static-frame state of compiler.py:
+//   sig  : 2n tableau sign bits (destab word, stab word)    [ref tableau.py]
+//   c    : u64 coset offset of the amplitude support        [ref state.py]
+//   A    : dense complex128 amplitudes over 2^k coordinates [ref state.py]
+//   rec  : measurement record bits (shared memory)
+// Everything shot-invariant (x/z tableau trajectory, pivot rows, coordinate
+// basis, draw offsets) was folded into the op stream on the host.
+//
+// Per-element arithmetic mirrors the reference's numpy forms:
+//   complex product  (fma(ar,br,-(ai*bi)), fma(ar,bi,ai*br))
+//   |v|^2            hypot(re,im)^2                              np.abs()**2
+//   prune            hypot > 1e-12                        ref state.py:298
+//   renormalise      v * (1/sqrt(sum |v|^2))                ref state.py:311
+// so amplitudes agree with the reference to rounding of the (differently
+// ordered) sums only.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <math.h>
+#include <string>
+#include <vector>
+
+#include "../../include/gstab_sm100.h"
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+typedef unsigned char u8;
+
+#define FULL 0xffffffffu
+
+namespace gs {
+
+enum { OP_END = 0, OP_T = 1, OP_MEAS = 2, OP_NOISE = 3, OP_FEEDBACK = 4,
+       OP_DETECTOR = 5, OP_OBSERVABLE = 6, OP_GROW_LIMIT = 7 };
+enum { T_DIAG = 0, T_BUTTERFLY = 1, T_GROW = 2 };
+enum { M_DET = 0, M_PIVOT_SPAN = 1, M_PIVOT_NOSPAN = 2 };
+enum { MF_RECORD = 16, MF_FLIP = 32, MF_RESET = 64, MF_COMPACT = 128 };
+enum { NK_DEP1 = 0, NK_DEP2 = 1, NK_XERR = 2, NK_ZERR = 3 };
+enum { ST_RUNNING = 0, ST_PRESERVED = 1, ST_DISCARDED = 2, ST_OVERFLOW = 3,
+       ST_CORRUPT = 4, ST_UNSUPPORTED = 5 };
+enum { MODE_COUNTERS = 0, MODE_RECORDS = 1, MODE_DUMP = 2 };
+
+constexpr int kWinWords = 64;          // noise fire window: 2048 locations
+constexpr int kWinBytes = kWinWords * 4;
+constexpr double kPrune = 1e-12;
+constexpr int kEntryBytes = 24;        // SURVEY §8(d) state-touch model
+
+struct DevProg {
+  const u64 *ops, *tables, *locs;
+  u32 n, nmeas, max_dim, nobs, rec_words32, nlocs;
+};
+
+struct DevRun {
+  u64 master, shot_begin, shot_count, cap;
+  u32 flags;
+  const u64 *seeds;
+};
+
+struct DevOut {
+  long long *counters;
+  u64 *next_shot;
+  u8 *status;
+  int *aux;
+  u64 *rec;
+  u64 *obs;
+  u64 *sig;
+  u64 *cvec;
+  double2 *amps;
+  u32 *dim;
+  double2 *gchi;        // global chi scratch (per warp) when not in smem
+  u32 *grec;            // global record scratch (per warp) when not in smem
+  u32 mode;
+  u32 warp_bytes;       // dynamic smem bytes per warp
+  u32 rec_in_smem;
+  u32 chi_off;          // byte offset of chi inside the warp's smem slice
+};
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)),
+                      __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double r) {
+  return make_double2(__dmul_rn(a.x, r), __dmul_rn(a.y, r));
+}
+__device__ __forceinline__ double habs(double2 v) { return hypot(v.x, v.y); }
+__device__ __forceinline__ double abs2(double2 v) {
+  double h = hypot(v.x, v.y);
+  return __dmul_rn(h, h);
+}
+__device__ __forceinline__ double2 prune(double2 v) {
+  return habs(v) > kPrune ? v : make_double2(0.0, 0.0);
+}
+__device__ __forceinline__ u32 par64(u64 x) { return __popcll(x) & 1u; }
+__device__ __forceinline__ u32 par32(u32 x) { return __popc(x) & 1u; }
+__device__ __forceinline__ double dbits(u64 w) { return __longlong_as_double((long long)w); }
+// _I_POWERS of ref state.py:28 (signed zeros included)
+__device__ __forceinline__ double2 ipow(u32 e) {
+  switch (e & 3u) {
+    case 0: return make_double2(1.0, 0.0);
+    case 1: return make_double2(0.0, 1.0);
+    case 2: return make_double2(-1.0, 0.0);
+    default: return make_double2(-0.0, -1.0);
+  }
+}
+// insert `bit` at position pos of jp
+__device__ __forceinline__ u32 ins_bit(u32 jp, u32 pos, u32 bit) {
+  u32 low = jp & ((1u << pos) - 1u);
+  return ((jp >> pos) << (pos + 1)) | (bit << pos) | low;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(FULL, v); }
+__device__ __forceinline__ u64 warp_or64(u64 v) {
+  u32 lo = __reduce_or_sync(FULL, (u32)v);
+  u32 hi = __reduce_or_sync(FULL, (u32)(v >> 32));
+  return ((u64)hi << 32) | lo;
+}
+
+// ---------------------------------------------------------------- RNG
+
+__device__ __forceinline__ u32 bswap32(u32 x) { return __byte_perm(x, 0, 0x0123); }
+__device__ __forceinline__ u32 rotl(u32 x, int r) { return __funnelshift_l(x, x, r); }
+
+// derive_seed: first 8 bytes (LE) of SHA-1(LE64 master || LE64 shot)
+// (ref sampler.py:37-42); single 64-byte block.
+__device__ u64 sha1_seed(u64 master, u64 shot) {
+  u32 w[16];
+  w[0] = bswap32((u32)master);
+  w[1] = bswap32((u32)(master >> 32));
+  w[2] = bswap32((u32)shot);
+  w[3] = bswap32((u32)(shot >> 32));
+  w[4] = 0x80000000u;
+#pragma unroll
+  for (int i = 5; i < 15; ++i) w[i] = 0;
+  w[15] = 128;
+  u32 a = 0x67452301u, b = 0xEFCDAB89u, c = 0x98BADCFEu, d = 0x10325476u,
+      e = 0xC3D2E1F0u;
+#pragma unroll
+  for (int i = 0; i < 80; ++i) {
+    u32 wi;
+    if (i < 16) {
+      wi = w[i];
+    } else {
+      wi = rotl(w[(i - 3) & 15] ^ w[(i - 8) & 15] ^ w[(i - 14) & 15] ^ w[i & 15], 1);
+      w[i & 15] = wi;
+    }
+    u32 f, k;
+    if (i < 20) { f = (b & c) | (~b & d); k = 0x5A827999u; }
+    else if (i < 40) { f = b ^ c ^ d; k = 0x6ED9EBA1u; }
+    else if (i < 60) { f = (b & c) | (b & d) | (c & d); k = 0x8F1BBCDCu; }
+    else { f = b ^ c ^ d; k = 0xCA62C1D6u; }
+    u32 t = rotl(a, 5) + f + e + k + wi;
+    e = d; d = c; c = rotl(b, 30); b = a; a = t;
+  }
+  u32 h0 = 0x67452301u + a, h1 = 0xEFCDAB89u + b;
+  return ((u64)bswap32(h1) << 32) | bswap32(h0);
+}
+
+__device__ __forceinline__ u64 splitmix(u64 seed, u32 k) {
+  u64 z = seed + (u64)(k + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ u64 philox_u64(u64 master, u64 shot, u32 k) {
+  u32 c0 = k >> 1, c1 = 0, c2 = (u32)shot, c3 = (u32)(shot >> 32);
+  u32 k0 = (u32)master, k1 = (u32)(master >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    u32 lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    u32 lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    u32 n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return (k & 1u) ? (((u64)c3 << 32) | c2) : (((u64)c1 << 32) | c0);
+}
+
+struct Rng {
+  u64 seed, master, shot;
+  bool philox;
+  __device__ __forceinline__ u64 m53(u32 k) const {
+    return (philox ? philox_u64(master, shot, k) : splitmix(seed, k)) >> 11;
+  }
+  __device__ __forceinline__ double uniform(u32 k) const {
+    return (double)m53(k) * 0x1.0p-53;
+  }
+};
+
+// ---------------------------------------------------------------- kernel
+
+template <bool kSmemChi>
+__global__ void __launch_bounds__(256)
+sample_kernel(DevProg P, DevRun R, DevOut O) {
+  extern __shared__ __align__(16) u8 smem[];
+  const u32 lane = threadIdx.x & 31u;
+  const u32 wib = threadIdx.x >> 5;
+  const u32 wpb = blockDim.x >> 5;
+  const u64 gw = (u64)blockIdx.x * wpb + wib;
+  u8 *mine = smem + (size_t)wib * O.warp_bytes;
+  u32 *win = reinterpret_cast<u32 *>(mine);
+  u32 *rec = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kWinBytes)
+                           : O.grec + gw * P.rec_words32;
+  double2 *A = kSmemChi ? reinterpret_cast<double2 *>(mine + O.chi_off)
+                        : O.gchi + gw * ((u64)1 << P.max_dim);
+  const u32 n = P.n;
+  const u64 *__restrict__ ops = P.ops;
+  const u64 *__restrict__ tables = P.tables;
+  const u64 *__restrict__ locs = P.locs;
+  const double2 Z = make_double2(0.0, 0.0);
+
+  long long n_tot = 0, n_pres = 0, n_disc = 0, n_ovf = 0, n_cor = 0, n_uns = 0,
+            n_err = 0;
+  unsigned long long mbytes_all = 0;
+
+  for (;;) {
+    u64 sl = 0;
+    if (lane == 0) sl = atomicAdd(O.next_shot, 1ull);
+    sl = __shfl_sync(FULL, sl, 0);
+    if (sl >= R.shot_count) break;
+    const u64 shot = R.shot_begin + sl;
+    Rng rng;
+    rng.philox = (R.flags & GS_RNG_PHILOX) != 0;
+    rng.master = R.master;
+    rng.shot = shot;
+    rng.seed = 0;
+    if (!rng.philox) rng.seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
+
+    for (u32 w = lane; w < P.rec_words32; w += 32) rec[w] = 0;
+    if (lane == 0) A[0] = make_double2(1.0, 0.0);
+    __syncwarp();
+
+    u64 sig_lo = 0, sig_hi = 0, c = 0, obs = 0, mbytes = 0;
+    u32 cnt = 1, kcur = 0, pc = 0;
+    int status = ST_RUNNING, aux = -1;
+    u32 win_base = 0xFFFFFFFFu;
+
+    while (status == ST_RUNNING) {
+      const u64 *op = ops + pc;
+      const u64 h = __ldg(op);
+      const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
+      const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
+      const u32 instr = (u32)(h >> 32);
+      pc += len;
+      kcur = k;
+      const u32 size = 1u << k;
+
+      if (kind == OP_NOISE) {
+        const u64 w1 = __ldg(op + 1);
+        const u32 loc0 = (u32)w1, nloc = (u32)(w1 >> 32);
+        if (loc0 < win_base || loc0 + nloc > win_base + 32u * kWinWords) {
+          // rescan the fire window: one fire-draw per location, one lane each
+          win_base = loc0 & ~31u;
+          for (u32 wd = 0; wd < (u32)kWinWords; ++wd) {
+            const u32 l = win_base + wd * 32u + lane;
+            bool fire = false;
+            if (l < P.nlocs) {
+              const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+              fire = rng.m53((u32)lw) < thr;
+            }
+            const u32 bits = __ballot_sync(FULL, fire);
+            if (lane == 0) win[wd] = bits;
+            if (win_base + wd * 32u + 32u >= P.nlocs) break;
+          }
+          __syncwarp();
+        }
+        const u32 rel0 = loc0 - win_base, rel1 = rel0 + nloc;  // [rel0, rel1)
+        const u32 wfirst = rel0 >> 5, wlast = (rel1 - 1) >> 5;
+        bool any = false;
+        for (u32 wd = wfirst + lane; wd <= wlast; wd += 32) {
+          u32 m = win[wd];
+          if (wd == wfirst) m &= ~0u << (rel0 & 31);
+          if (wd == wlast && (rel1 & 31)) m &= (1u << (rel1 & 31)) - 1u;
+          any |= m != 0;
+        }
+        if (!__any_sync(FULL, any)) continue;
+        // build E = OR of fired letters (ref noise.py:68-100)
+        u64 ex = 0, ez = 0;
+        for (u32 i = lane; i < nloc; i += 32) {
+          const u32 rel = rel0 + i;
+          if (!((win[rel >> 5] >> (rel & 31)) & 1u)) continue;
+          const u64 lw = __ldg(locs + 2ull * (loc0 + i));
+          const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
+                    qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
+          if (nk == NK_DEP1) {
+            int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
+            code = code > 3 ? 3 : code;
+            ex |= (u64)(code != 3) << qa;
+            ez |= (u64)(code != 1) << qa;
+          } else if (nk == NK_DEP2) {
+            int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
+            pick = pick > 15 ? 15 : pick;
+            const int ca = pick & 3, cbq = pick >> 2;
+            if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+            if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+          } else if (nk == NK_XERR) {
+            ex |= 1ull << qa;
+          } else {
+            ez |= 1ull << qa;
+          }
+        }
+        ex = warp_or64(ex);
+        ez = warp_or64(ez);
+        const u64 eall = ex | ez;
+        if (!eall) continue;
+        // compose the action of E letter by letter
+        const u64 qmask = __ldg(op + 2);
+        const u64 off = __ldg(op + 3);
+        u64 beta = 0, delt = 0;
+        u32 xi = 0, dm = 0;
+        for (u64 rem = eall; rem; rem &= rem - 1) {
+          const u32 q = __ffsll((long long)rem) - 1;
+          const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
+          const u64 *tb = tables + off + 10ull * slot;
+          const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
+          const u32 xw = (u32)__ldg(tb + 4);
+          const u32 xx = ((xw & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
+          const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
+          const u64 zw64 = __ldg(tb + 9);
+          const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
+          const u32 xdm = (u32)(__ldg(tb + 4) >> 8), zdm = (u32)(zw64 >> 8);
+          const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
+          u64 lb, ld; u32 lxi, ldm;
+          if (hx && hz) {
+            lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
+            lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
+          } else if (hx) {
+            lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
+          } else {
+            lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
+          }
+          xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
+          beta ^= lb; delt ^= ld; dm ^= ldm;
+        }
+        // apply: v <- i^xi (-1)^{delta.alpha} v ; alpha ^= beta (ref state.py:88-102)
+        const double2 I = ipow(xi);
+        const double2 php = cmul(I, make_double2(1.0, 0.0));
+        const double2 phm = cmul(I, make_double2(-1.0, 0.0));
+        const u32 dc = par64(delt & c);
+        for (u32 j = lane; j < size; j += 32) {
+          const u32 s = dc ^ par32(j & dm);
+          A[j] = cmul(A[j], s ? phm : php);
+        }
+        __syncwarp();
+        c ^= beta;
+        mbytes += 2ull * kEntryBytes * cnt + 2ull * ((2 * n + 7) / 8);
+        continue;
+      }
+
+      if (kind == OP_T || kind == OP_GROW_LIMIT) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6);
+        const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
+        const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
+        const double2 b = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
+        mbytes += __ldg(op + 11);
+        const double2 I = ipow(xi0);
+        const double2 bx0 = cmul(b, cmul(I, make_double2(1.0, 0.0)));
+        const double2 bx1 = cmul(b, cmul(I, make_double2(-1.0, 0.0)));
+        const u32 dc = par64(delta & c);
+        const u32 tcase = fl & 3u;
+        if (tcase == T_DIAG) {
+          const double2 f0 = cadd(a, bx0), f1 = cadd(a, bx1);
+          for (u32 j = lane; j < size; j += 32) {
+            const u32 s = dc ^ par32(j & dmask);
+            A[j] = cmul(A[j], s ? f1 : f0);
+          }
+          __syncwarp();
+          mbytes += 32ull * cnt;
+          continue;
+        }
+        const u32 cin = cnt;
+        u32 nz = 0;
+        if (kind == OP_GROW_LIMIT) {
+          for (u32 j = lane; j < size; j += 32) {
+            const double2 v = A[j];
+            const u32 s = dc ^ par32(j & dmask);
+            nz += habs(cadd(Z, cmul(a, v))) > kPrune;
+            nz += habs(cadd(Z, cmul(s ? bx1 : bx0, v))) > kPrune;
+          }
+          nz = warp_sum_u32(nz);
+          status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
+          aux = (int)instr;
+          break;
+        }
+        if (tcase == T_BUTTERFLY) {
+          const u32 hb = 31 - __clz(cb);
+          const u32 half = size >> 1;
+          for (u32 m = lane; m < half; m += 32) {
+            const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+            const double2 v0 = A[j0], v1 = A[j1];
+            const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+            const double2 n0 = prune(cadd(cadd(Z, cmul(a, v0)), cmul(s1 ? bx1 : bx0, v1)));
+            const double2 n1 = prune(cadd(cadd(Z, cmul(a, v1)), cmul(s0 ? bx1 : bx0, v0)));
+            A[j0] = n0;
+            A[j1] = n1;
+            nz += (n0.x != 0.0 || n0.y != 0.0) + (n1.x != 0.0 || n1.y != 0.0);
+          }
+        } else {  // T_GROW: beta becomes coordinate k
+          for (u32 j = lane; j < size; j += 32) {
+            const double2 v = A[j];
+            const u32 s = dc ^ par32(j & dmask);
+            const double2 n0 = prune(cadd(Z, cmul(a, v)));
+            const double2 n1 = prune(cadd(Z, cmul(s ? bx1 : bx0, v)));
+            A[j] = n0;
+            A[size + j] = n1;
+            nz += (n0.x != 0.0 || n0.y != 0.0) + (n1.x != 0.0 || n1.y != 0.0);
+          }
+          kcur = k + 1;
+        }
+        __syncwarp();
+        cnt = warp_sum_u32(nz);
+        mbytes += (u64)kEntryBytes * (cin + cnt);
+        if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr; break; }
+        if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+        continue;
+      }
+
+      if (kind == OP_MEAS) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        const u32 mcase = fl & 3u;
+        const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
+        const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
+        const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
+        const u64 vec = __ldg(op + 8);
+        const u64 w13 = __ldg(op + 13);
+        const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
+        mbytes += __ldg(op + 17);
+        const u32 dc = par64(delta & c);
+        const double u = rng.uniform(udraw);
+        const u32 cin = cnt;
+        bool plus;
+        if (mcase == M_DET) {
+          // beta == 0: filter by eigenvalue (ref state.py:162-176)
+          const u32 neg0 = (xi0 >> 1) ^ dc;
+          double sp = 0.0, sm = 0.0;
+          for (u32 j = lane; j < size; j += 32) {
+            const double a2 = abs2(A[j]);
+            if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
+            else sp = __dadd_rn(sp, a2);
+          }
+          sp = warp_sum(sp);
+          sm = warp_sum(sm);
+          plus = u < sp;
+          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+          const u32 want_neg = plus ? 0u : 1u;
+          const double r = 1.0 / sqrt(plus ? sp : sm);
+          u32 nz = 0;
+          if (fl & MF_COMPACT) {
+            const u32 tau = want_neg ^ neg0;
+            const u32 half = size >> 1;
+            for (u32 base = 0; base < half; base += 32) {
+              const u32 jp = base + lane;
+              double2 v = Z;
+              if (jp < half) {
+                const u32 j0 = ins_bit(jp, isq, 0);
+                v = A[j0 | ((tau ^ par32(j0 & dmask)) << isq)];
+              }
+              __syncwarp();
+              if (jp < half) {
+                v = cscale(v, r);
+                A[jp] = v;
+                nz += (v.x != 0.0 || v.y != 0.0);
+              }
+              __syncwarp();
+            }
+            if (tau) c ^= vec;
+            kcur = k - 1;
+          } else {
+            for (u32 j = lane; j < size; j += 32) {
+              const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
+              const double2 v = keep ? cscale(A[j], r) : Z;
+              A[j] = v;
+              nz += (v.x != 0.0 || v.y != 0.0);
+            }
+            __syncwarp();
+          }
+          cnt = warp_sum_u32(nz);
+        } else {
+          // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
+          const double2 I = ipow(xi0);
+          const double2 xpp = cmul(I, make_double2(1.0, 0.0));
+          const double2 xpm = cmul(I, make_double2(-1.0, 0.0));
+          const u32 ct = (u32)(c >> t) & 1u;
+          double sp = 0.0;
+          const bool span = mcase == M_PIVOT_SPAN;
+          const u32 npairs = span ? (size >> 1) : size;
+          for (u32 m = lane; m < npairs; m += 32) {
+            double2 wpv;
+            if (span) {
+              const u32 j0 = ins_bit(m, isq, 0);
+              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+              const u32 part = rep ^ cb;
+              const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
+              wpv = cadd(A[rep], prod);
+            } else {
+              const double2 v = A[m];
+              if (ct ^ par32(m & tmask)) {
+                wpv = cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v));
+              } else {
+                wpv = v;
+              }
+            }
+            sp = __dadd_rn(sp, abs2(wpv));
+          }
+          sp = warp_sum(sp);
+          const double pp = __dmul_rn(0.5, sp);
+          plus = u < pp;
+          const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+          double sk = 0.0;
+          u32 nz = 0;
+          for (u32 m = lane; m < npairs; m += 32) {
+            double2 w;
+            u32 dst;
+            if (span) {
+              const u32 j0 = ins_bit(m, isq, 0);
+              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+              const u32 part = rep ^ cb;
+              const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
+              w = plus ? cadd(A[rep], prod) : csub(A[rep], prod);
+              dst = rep;
+            } else {
+              const double2 v = A[m];
+              if (ct ^ par32(m & tmask)) {
+                const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
+                w = plus ? cadd(Z, prod) : csub(Z, prod);
+              } else {
+                w = v;
+              }
+              dst = m;
+            }
+            w = prune(w);
+            A[dst] = w;
+            sk = __dadd_rn(sk, abs2(w));
+            nz += (w.x != 0.0 || w.y != 0.0);
+          }
+          __syncwarp();
+          sk = warp_sum(sk);
+          nz = warp_sum_u32(nz);
+          if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+          const double r = 1.0 / sqrt(sk);
+          if (span) {
+            const u32 half = size >> 1;
+            for (u32 base = 0; base < half; base += 32) {
+              const u32 jp = base + lane;
+              double2 v = Z;
+              if (jp < half) {
+                const u32 j0 = ins_bit(jp, isq, 0);
+                v = A[j0 | ((ct ^ par32(j0 & tmask)) << isq)];
+              }
+              __syncwarp();
+              if (jp < half) A[jp] = cscale(v, r);
+              __syncwarp();
+            }
+            kcur = k - 1;
+          } else {
+            for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], r);
+            __syncwarp();
+          }
+          if (ct) c ^= vec;
+          cnt = nz;
+          // tableau sign update of the pivot (ref tableau.py:176-200)
+          const u32 v = (u32)(sig_hi >> t) & 1u;
+          if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
+          sig_lo ^= __ldg(op + 11);
+          sig_hi ^= __ldg(op + 12);
+          sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
+          sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
+        }
+        mbytes += (u64)kEntryBytes * (cin + cnt);
+        const u32 bout = plus ? 0u : 1u;
+        u32 rb = bout;
+        if ((fl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
+        if (fl & MF_RECORD) {
+          if (lane == 0 && rb) rec[slot >> 5] |= 1u << (slot & 31);
+          __syncwarp();
+        }
+        if ((fl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
+        continue;
+      }
+
+      if (kind == OP_FEEDBACK) {
+        const u32 idx = (u32)__ldg(op + 1);
+        if ((rec[idx >> 5] >> (idx & 31)) & 1u) {
+          sig_lo ^= __ldg(op + 2);
+          sig_hi ^= __ldg(op + 3);
+          mbytes += __ldg(op + 4);
+        }
+        continue;
+      }
+
+      if (kind == OP_DETECTOR || kind == OP_OBSERVABLE) {
+        const u64 w1 = __ldg(op + 1);
+        const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
+        const u64 off = __ldg(op + 2);
+        u32 b = 0;
+        for (u32 i = lane; i < nidx; i += 32) {
+          const u32 idx = (u32)__ldg(tables + off + i);
+          b ^= (rec[idx >> 5] >> (idx & 31)) & 1u;
+        }
+        const u32 parity = __popc(__ballot_sync(FULL, b)) & 1u;
+        if (kind == OP_DETECTOR) {
+          if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
+        } else {
+          obs ^= (u64)parity << id;
+        }
+        continue;
+      }
+
+      if (kind == OP_END) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        mbytes += __ldg(op + 3);
+        status = ST_PRESERVED;
+        break;
+      }
+      status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
+      aux = -2;
+    }
+
+    // -------------------------------------------------------- shot outputs
+    n_tot += 1;
+    mbytes_all += mbytes;
+    if (status == ST_PRESERVED) {
+      n_pres += 1;
+      if (obs) {
+        n_err += 1;
+        if (lane == 0)
+          for (u64 o = obs; o; o &= o - 1)
+            atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
+      }
+    } else if (status == ST_DISCARDED) n_disc += 1;
+    else if (status == ST_OVERFLOW) n_ovf += 1;
+    else if (status == ST_CORRUPT) n_cor += 1;
+    else n_uns += 1;
+    if (O.mode != MODE_COUNTERS) {
+      if (lane == 0) {
+        O.status[sl] = (u8)status;
+        O.aux[sl] = aux;
+        O.obs[sl] = obs;
+      }
+      const u32 rw64 = (P.nmeas + 63) / 64;
+      for (u32 w = lane; w < rw64; w += 32) {
+        const u32 lo = rec[2 * w];
+        const u32 hi = (2 * w + 1 < P.rec_words32) ? rec[2 * w + 1] : 0u;
+        O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
+      }
+      if (O.mode == MODE_DUMP) {
+        if (lane == 0) {
+          O.sig[2 * sl] = sig_lo;
+          O.sig[2 * sl + 1] = sig_hi;
+          O.cvec[sl] = c;
+          O.dim[sl] = kcur;
+        }
+        const u64 stride = 1ull << P.max_dim;
+        for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = A[j];
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    unsigned long long *C = (unsigned long long *)O.counters;
+    if (n_tot) atomicAdd(C + GS_C_TOTAL, (unsigned long long)n_tot);
+    if (n_pres) atomicAdd(C + GS_C_PRESERVED, (unsigned long long)n_pres);
+    if (n_disc) atomicAdd(C + GS_C_DISCARDED, (unsigned long long)n_disc);
+    if (n_ovf) atomicAdd(C + GS_C_OVERFLOW, (unsigned long long)n_ovf);
+    if (n_cor) atomicAdd(C + GS_C_CORRUPT, (unsigned long long)n_cor);
+    if (n_uns) atomicAdd(C + GS_C_UNSUPPORTED, (unsigned long long)n_uns);
+    if (n_err) atomicAdd(C + GS_C_ERROR_SHOTS, (unsigned long long)n_err);
+    if (mbytes_all) atomicAdd(C + GS_C_MODEL_BYTES, mbytes_all);
+  }
+}
+
+// ------------------------------------------------ kernel plugin API kernels
+// batched equivalents of ref _kernels.pyx / _kernels_py.py
+
+__global__ void anticommute_kernel(const u64 *xs, const u64 *zs, u32 rows, u32 batch,
+                                   const u64 *qx, const u64 *qz, u64 *out) {
+  const u32 lane = threadIdx.x & 31u;
+  const u64 b = (u64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= batch) return;
+  const u64 X = qx[b], Zq = qz[b];
+  u64 lo = 0, hi = 0;
+  for (u32 base = 0; base < rows; base += 32) {
+    const u32 r = base + lane;
+    bool a = false;
+    if (r < rows) a = ((__popcll(xs[b * rows + r] & Zq) + __popcll(zs[b * rows + r] & X)) & 1) != 0;
+    const u32 bits = __ballot_sync(FULL, a);
+    if (base < 64) lo |= (u64)bits << base;
+    else hi |= (u64)bits << (base - 64);
+  }
+  if (lane == 0) { out[2 * b] = lo; out[2 * b + 1] = hi; }
+}
+
+__global__ void conj_gate_kernel(u64 *xs, u64 *zs, u8 *ph, u32 rows, u32 batch,
+                                 const u32 *code, const u64 *m1s, const u64 *m2s) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (u64)rows * batch) return;
+  const u64 b = i / rows;
+  const u64 m1 = m1s[b], m2 = m2s[b];
+  u64 x = xs[i], z = zs[i];
+  const bool x1 = (x & m1) != 0, z1 = (z & m1) != 0;
+  const bool x2 = (x & m2) != 0, z2 = (z & m2) != 0;
+  bool flip = false;
+  switch (code[b]) {
+    case 0: return;
+    case 1: flip = z1; break;
+    case 2: flip = x1 ^ z1; break;
+    case 3: flip = x1; break;
+    case 4: flip = x1 && z1; if (x1 != z1) { x ^= m1; z ^= m1; } break;
+    case 5: flip = x1 && z1; if (x1) z ^= m1; break;
+    case 6: flip = x1 && !z1; if (x1) z ^= m1; break;
+    case 7: flip = z1 && !x1; if (x1) z ^= m1; break;
+    case 8: flip = x1 || z1; if (x1) z ^= m1; break;
+    case 9: flip = x1 && z2 && !(x2 ^ z1); if (x1) x ^= m2; if (z2) z ^= m1; break;
+    case 10: flip = x1 && x2 && (z1 ^ z2); if (x1) z ^= m2; if (x2) z ^= m1; break;
+    case 11: if (x1 != x2) x ^= (m1 | m2); if (z1 != z2) z ^= (m1 | m2); break;
+    default: return;
+  }
+  xs[i] = x; zs[i] = z;
+  if (flip) ph[i] ^= 2;
+}
+
+__global__ void mul_rows_kernel(u64 *xs, u64 *zs, u8 *ph, u32 rows, u32 batch, const u8 *sel,
+                                const u64 *pxs, const u64 *pzs, const u32 *pes) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (u64)rows * batch || !sel[i]) return;
+  const u64 b = i / rows;
+  const u64 px = pxs[b], pz = pzs[b];
+  const u64 xj = xs[i], zj = zs[i], x3 = xj ^ px, z3 = zj ^ pz;
+  const long long e = (long long)ph[i] + pes[b] + __popcll(px & pz) + 2 * __popcll(zj & px) +
+                      __popcll(xj & zj) - __popcll(x3 & z3);
+  xs[i] = x3; zs[i] = z3;
+  ph[i] = (u8)(e & 3);
+}
+
+__global__ void parity_pm_kernel(const u64 *idx, size_t count, u64 mask, double *out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = 1.0 - 2.0 * (double)(__popcll(idx[i] & mask) & 1);
+}
+
+}  // namespace gs
+
+// =================================================================== host
+
+struct gs_program {
+  gs_program_info info;
+  std::vector<u64> ops, tables, locs;
+  int dev = -1;
+  u64 *d_ops = nullptr, *d_tables = nullptr, *d_locs = nullptr;
+};
+
+struct gs_engine {
+  int device = 0;
+  int num_sms = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long long *d_counters = nullptr;
+  size_t counters_cap = 0;
+  u64 *d_next = nullptr;
+  double2 *d_chi = nullptr;
+  size_t chi_bytes = 0;
+  u32 *d_rec = nullptr;
+  size_t rec_bytes = 0;
+  u64 launches = 0;
+  double last_ms = 0.0;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                            \
+  do {                                                                         \
+    cudaError_t e_ = (x);                                                      \
+    if (e_ != cudaSuccess)                                                     \
+      return fail(GS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" {
+
+const char *gs_last_error(void) { return g_err.c_str(); }
+int gs_abi_version(void) { return GS_ABI_VERSION; }
+
+int gs_program_create(const gs_program_info *info, const uint64_t *ops, size_t n_ops,
+                      const uint64_t *tables, size_t n_tables, const uint64_t *locs,
+                      size_t n_locs, gs_program **out) {
+  if (!info || !ops || !out || n_ops == 0) return fail(GS_ERR_ARG, "null argument");
+  if (info->num_qubits < 1 || info->num_qubits > 64)
+    return fail(GS_ERR_ARG, "num_qubits must be in 1..64");
+  if (info->max_dim > 30) return fail(GS_ERR_ARG, "max_dim must be <= 30");
+  if (info->num_obs > 64) return fail(GS_ERR_ARG, "at most 64 observables");
+  gs_program *p = new (std::nothrow) gs_program();
+  if (!p) return fail(GS_ERR_NOMEM, "out of host memory");
+  p->info = *info;
+  p->ops.assign(ops, ops + n_ops);
+  if (tables && n_tables) p->tables.assign(tables, tables + n_tables);
+  else p->tables.assign(1, 0);
+  if (locs && n_locs) p->locs.assign(locs, locs + n_locs);
+  else p->locs.assign(2, 0);
+  *out = p;
+  return GS_OK;
+}
+
+int gs_program_destroy(gs_program *p) {
+  if (!p) return GS_OK;
+  if (p->dev >= 0) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->dev);
+    cudaFree(p->d_ops);
+    cudaFree(p->d_tables);
+    cudaFree(p->d_locs);
+    cudaSetDevice(cur);
+  }
+  delete p;
+  return GS_OK;
+}
+
+int gs_engine_create(int device, gs_engine **out) {
+  if (!out) return fail(GS_ERR_ARG, "null argument");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(GS_ERR_ARG, "bad device index");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(GS_ERR_UNSUPPORTED, "libgstab_sm100a requires an sm_100 (B200) device");
+  gs_engine *e = new (std::nothrow) gs_engine();
+  if (!e) return fail(GS_ERR_NOMEM, "out of host memory");
+  e->device = device;
+  e->num_sms = prop.multiProcessorCount;
+  e->smem_optin = prop.sharedMemPerBlockOptin;
+  CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreate(&e->ev0));
+  CUDA_TRY(cudaEventCreate(&e->ev1));
+  CUDA_TRY(cudaMalloc(&e->d_next, sizeof(u64)));
+  *out = e;
+  return GS_OK;
+}
+
+int gs_engine_destroy(gs_engine *e) {
+  if (!e) return GS_OK;
+  cudaSetDevice(e->device);
+  cudaFree(e->d_counters);
+  cudaFree(e->d_next);
+  cudaFree(e->d_chi);
+  cudaFree(e->d_rec);
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+  return GS_OK;
+}
+
+uint64_t gs_engine_launches(gs_engine *e) { return e ? e->launches : 0; }
+double gs_engine_last_kernel_ms(gs_engine *e) { return e ? e->last_ms : 0.0; }
+
+static int upload(gs_engine *e, gs_program *p) {
+  if (p->dev == e->device) return GS_OK;
+  if (p->dev >= 0) return fail(GS_ERR_ARG, "program already bound to another device");
+  CUDA_TRY(cudaMalloc(&p->d_ops, p->ops.size() * 8));
+  CUDA_TRY(cudaMalloc(&p->d_tables, p->tables.size() * 8));
+  CUDA_TRY(cudaMalloc(&p->d_locs, p->locs.size() * 8));
+  CUDA_TRY(cudaMemcpy(p->d_ops, p->ops.data(), p->ops.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_tables, p->tables.data(), p->tables.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_locs, p->locs.data(), p->locs.size() * 8, cudaMemcpyHostToDevice));
+  p->dev = e->device;
+  return GS_OK;
+}
+
+struct LaunchCfg {
+  bool smem_chi;
+  u32 wpb, blocks, warp_bytes, chi_off, rec_in_smem, rec_words32;
+  size_t smem;
+};
+
+static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &L) {
+  const u32 K = p->info.max_dim;
+  const size_t chi = (size_t)16 << K;
+  L.rec_words32 = ((p->info.num_measurements + 63) / 64) * 2;
+  if (L.rec_words32 == 0) L.rec_words32 = 2;
+  const size_t rec_b = (size_t)L.rec_words32 * 4;
+  L.rec_in_smem = rec_b <= 2048;
+  size_t base = gs::kWinBytes + (L.rec_in_smem ? rec_b : 0);
+  base = (base + 15) & ~(size_t)15;
+  L.smem_chi = !(r->flags & GS_CHI_GLOBAL) && chi <= 48 * 1024;
+  L.chi_off = (u32)base;
+  L.warp_bytes = (u32)(base + (L.smem_chi ? chi : 0));
+  u32 wpb = r->warps_per_block ? r->warps_per_block : 4;
+  if (wpb > 8) wpb = 8;
+  while (wpb > 1 && (size_t)wpb * L.warp_bytes > e->smem_optin) --wpb;
+  if ((size_t)wpb * L.warp_bytes > e->smem_optin)
+    return fail(GS_ERR_UNSUPPORTED, "per-warp state exceeds shared memory");
+  L.wpb = wpb;
+  L.smem = (size_t)wpb * L.warp_bytes;
+  if (L.smem_chi) {
+    CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+  } else {
+    CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+  }
+  int per_sm = 0;
+  if (L.smem_chi) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::sample_kernel<true>,
+                                                           wpb * 32, L.smem));
+  } else {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::sample_kernel<false>,
+                                                           wpb * 32, L.smem));
+  }
+  if (per_sm < 1) return fail(GS_ERR_UNSUPPORTED, "kernel does not fit on an SM");
+  u64 blocks = r->blocks ? r->blocks : (u64)e->num_sms * per_sm;
+  const u64 need = (r->shot_count + wpb - 1) / wpb;
+  if (blocks > need) blocks = need ? need : 1;
+  L.blocks = (u32)blocks;
+  const u64 warps = (u64)L.blocks * wpb;
+  if (!L.smem_chi) {
+    const size_t want = (size_t)warps * chi;
+    if (want > e->chi_bytes) {
+      cudaFree(e->d_chi);
+      e->d_chi = nullptr;
+      e->chi_bytes = 0;
+      CUDA_TRY(cudaMalloc(&e->d_chi, want));
+      e->chi_bytes = want;
+    }
+  }
+  if (!L.rec_in_smem) {
+    const size_t want = (size_t)warps * rec_b;
+    if (want > e->rec_bytes) {
+      cudaFree(e->d_rec);
+      e->d_rec = nullptr;
+      e->rec_bytes = 0;
+      CUDA_TRY(cudaMalloc(&e->d_rec, want));
+      e->rec_bytes = want;
+    }
+  }
+  return GS_OK;
+}
+
+static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOut O,
+                  cudaStream_t st, bool timed) {
+  if (!e || !p || !r) return fail(GS_ERR_ARG, "null argument");
+  if (r->capacity < 1) return fail(GS_ERR_ARG, "capacity must be >= 1");
+  if ((r->flags & GS_RNG_PHILOX) && r->seeds)
+    return fail(GS_ERR_ARG, "explicit seeds require the SplitMix RNG");
+  CUDA_TRY(cudaSetDevice(e->device));
+  int rc = upload(e, p);
+  if (rc) return rc;
+  LaunchCfg L;
+  rc = plan(e, p, r, L);
+  if (rc) return rc;
+  gs::DevProg P;
+  P.ops = p->d_ops;
+  P.tables = p->d_tables;
+  P.locs = p->d_locs;
+  P.n = p->info.num_qubits;
+  P.nmeas = p->info.num_measurements;
+  P.max_dim = p->info.max_dim;
+  P.nobs = p->info.num_obs;
+  P.rec_words32 = L.rec_words32;
+  P.nlocs = p->info.num_locations;
+  gs::DevRun R;
+  R.master = r->master_seed;
+  R.shot_begin = r->shot_begin;
+  R.shot_count = r->shot_count;
+  R.cap = r->capacity;
+  R.flags = r->flags;
+  R.seeds = nullptr;
+  u64 *d_seeds = nullptr;
+  if (r->seeds && r->shot_count) {
+    CUDA_TRY(cudaMallocAsync(&d_seeds, r->shot_count * 8, st));
+    CUDA_TRY(cudaMemcpyAsync(d_seeds, r->seeds, r->shot_count * 8, cudaMemcpyHostToDevice, st));
+    R.seeds = d_seeds;
+  }
+  O.next_shot = e->d_next;
+  O.gchi = e->d_chi;
+  O.grec = e->d_rec;
+  O.warp_bytes = L.warp_bytes;
+  O.rec_in_smem = L.rec_in_smem;
+  O.chi_off = L.chi_off;
+  CUDA_TRY(cudaMemsetAsync(e->d_next, 0, sizeof(u64), st));
+  if (r->shot_count) {
+    if (timed) CUDA_TRY(cudaEventRecord(e->ev0, st));
+    if (L.smem_chi)
+      gs::sample_kernel<true><<<L.blocks, L.wpb * 32, L.smem, st>>>(P, R, O);
+    else
+      gs::sample_kernel<false><<<L.blocks, L.wpb * 32, L.smem, st>>>(P, R, O);
+    CUDA_TRY(cudaGetLastError());
+    if (timed) CUDA_TRY(cudaEventRecord(e->ev1, st));
+    e->launches += 1;
+  }
+  if (d_seeds) CUDA_TRY(cudaFreeAsync(d_seeds, st));
+  return GS_OK;
+}
+
+static int ensure_counters(gs_engine *e, size_t n) {
+  if (n <= e->counters_cap) return GS_OK;
+  cudaFree(e->d_counters);
+  e->d_counters = nullptr;
+  e->counters_cap = 0;
+  CUDA_TRY(cudaMalloc(&e->d_counters, n * 8));
+  e->counters_cap = n;
+  return GS_OK;
+}
+
+int gs_run_counters(gs_engine *e, gs_program *p, const gs_run_params *r, int64_t *counters) {
+  if (!e || !p || !r || !counters) return fail(GS_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  const size_t nc = GS_C_PER_OBS + p->info.num_obs;
+  int rc = ensure_counters(e, nc);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemsetAsync(e->d_counters, 0, nc * 8, e->stream));
+  gs::DevOut O;
+  memset(&O, 0, sizeof(O));
+  O.counters = e->d_counters;
+  O.mode = gs::MODE_COUNTERS;
+  rc = launch(e, p, r, O, e->stream, true);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(counters, e->d_counters, nc * 8, cudaMemcpyDeviceToHost, e->stream));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  float ms = 0.f;
+  if (r->shot_count) CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  e->last_ms = ms;
+  return GS_OK;
+}
+
+int gs_run_counters_async(gs_engine *e, gs_program *p, const gs_run_params *r,
+                          int64_t *counters_dev, void *stream) {
+  if (!e || !p || !r || !counters_dev) return fail(GS_ERR_ARG, "null argument");
+  gs::DevOut O;
+  memset(&O, 0, sizeof(O));
+  O.counters = (long long *)counters_dev;
+  O.mode = gs::MODE_COUNTERS;
+  return launch(e, p, r, O, (cudaStream_t)stream, false);
+}
+
+static int run_out(gs_engine *e, gs_program *p, const gs_run_params *r, uint8_t *status,
+                   int32_t *aux, uint64_t *record_bits, uint64_t *obs_bits, uint64_t *sig,
+                   uint64_t *cv, double *amps, uint32_t *dim, u32 mode) {
+  if (!e || !p || !r || !status || !aux || !record_bits || !obs_bits)
+    return fail(GS_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  const size_t nc = GS_C_PER_OBS + p->info.num_obs;
+  int rc = ensure_counters(e, nc);
+  if (rc) return rc;
+  const u64 S = r->shot_count;
+  const u64 rw = (p->info.num_measurements + 63) / 64;
+  const u64 stride = 1ull << p->info.max_dim;
+  gs::DevOut O;
+  memset(&O, 0, sizeof(O));
+  O.counters = e->d_counters;
+  O.mode = mode;
+  cudaStream_t st = e->stream;
+  CUDA_TRY(cudaMemsetAsync(e->d_counters, 0, nc * 8, st));
+  const size_t bytes_rec = (size_t)S * (rw ? rw : 1) * 8;
+  CUDA_TRY(cudaMallocAsync(&O.status, S ? S : 1, st));
+  CUDA_TRY(cudaMallocAsync(&O.aux, (S ? S : 1) * 4, st));
+  CUDA_TRY(cudaMallocAsync(&O.rec, bytes_rec ? bytes_rec : 8, st));
+  CUDA_TRY(cudaMallocAsync(&O.obs, (S ? S : 1) * 8, st));
+  if (bytes_rec) CUDA_TRY(cudaMemsetAsync(O.rec, 0, bytes_rec, st));
+  if (mode == gs::MODE_DUMP) {
+    CUDA_TRY(cudaMallocAsync(&O.sig, (S ? S : 1) * 16, st));
+    CUDA_TRY(cudaMallocAsync(&O.cvec, (S ? S : 1) * 8, st));
+    CUDA_TRY(cudaMallocAsync(&O.dim, (S ? S : 1) * 4, st));
+    CUDA_TRY(cudaMallocAsync(&O.amps, (S ? S : 1) * stride * 16, st));
+    CUDA_TRY(cudaMemsetAsync(O.amps, 0, (S ? S : 1) * stride * 16, st));
+  }
+  rc = launch(e, p, r, O, st, true);
+  if (rc) return rc;
+  if (S) {
+    CUDA_TRY(cudaMemcpyAsync(status, O.status, S, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(aux, O.aux, S * 4, cudaMemcpyDeviceToHost, st));
+    if (rw) CUDA_TRY(cudaMemcpyAsync(record_bits, O.rec, bytes_rec, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(obs_bits, O.obs, S * 8, cudaMemcpyDeviceToHost, st));
+    if (mode == gs::MODE_DUMP) {
+      CUDA_TRY(cudaMemcpyAsync(sig, O.sig, S * 16, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(cv, O.cvec, S * 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(dim, O.dim, S * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(amps, O.amps, S * stride * 16, cudaMemcpyDeviceToHost, st));
+    }
+  }
+  cudaFreeAsync(O.status, st);
+  cudaFreeAsync(O.aux, st);
+  cudaFreeAsync(O.rec, st);
+  cudaFreeAsync(O.obs, st);
+  if (mode == gs::MODE_DUMP) {
+    cudaFreeAsync(O.sig, st);
+    cudaFreeAsync(O.cvec, st);
+    cudaFreeAsync(O.dim, st);
+    cudaFreeAsync(O.amps, st);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  if (S) CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  e->last_ms = ms;
+  return GS_OK;
+}
+
+int gs_run_records(gs_engine *e, gs_program *p, const gs_run_params *r, uint8_t *status,
+                   int32_t *aux, uint64_t *record_bits, uint64_t *obs_bits) {
+  return run_out(e, p, r, status, aux, record_bits, obs_bits, nullptr, nullptr, nullptr,
+                 nullptr, gs::MODE_RECORDS);
+}
+
+int gs_dump_shots(gs_engine *e, gs_program *p, const gs_run_params *r, uint8_t *status,
+                  int32_t *aux, uint64_t *record_bits, uint64_t *obs_bits, uint64_t *sig,
+                  uint64_t *c, double *amps, uint32_t *dim) {
+  if (!sig || !c || !amps || !dim) return fail(GS_ERR_ARG, "null argument");
+  return run_out(e, p, r, status, aux, record_bits, obs_bits, sig, c, amps, dim,
+                 gs::MODE_DUMP);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------ kernel plugin API (host)
+
+template <typename T>
+static int to_dev(T **d, const void *h, size_t n, cudaStream_t st) {
+  CUDA_TRY(cudaMallocAsync((void **)d, (n ? n : 1) * sizeof(T), st));
+  if (n && h) CUDA_TRY(cudaMemcpyAsync(*d, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+  return GS_OK;
+}
+
+extern "C" {
+
+int gs_anticommute_mask(gs_engine *e, const uint64_t *xs, const uint64_t *zs, uint32_t rows,
+                        uint32_t batch, const uint64_t *qx, const uint64_t *qz,
+                        uint64_t *out_mask) {
+  if (!e || !xs || !zs || !qx || !qz || !out_mask) return fail(GS_ERR_ARG, "null argument");
+  if (rows > 128) return fail(GS_ERR_ARG, "rows must be <= 128");
+  CUDA_TRY(cudaSetDevice(e->device));
+  cudaStream_t st = e->stream;
+  u64 *dx, *dz, *dqx, *dqz, *dout;
+  const size_t nr = (size_t)rows * batch;
+  if (to_dev(&dx, xs, nr, st) || to_dev(&dz, zs, nr, st) || to_dev(&dqx, qx, batch, st) ||
+      to_dev(&dqz, qz, batch, st) || to_dev(&dout, nullptr, 2 * (size_t)batch, st))
+    return GS_ERR_CUDA;
+  if (batch) {
+    gs::anticommute_kernel<<<(batch + 3) / 4, 128, 0, st>>>(dx, dz, rows, batch, dqx, dqz, dout);
+    CUDA_TRY(cudaGetLastError());
+    e->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync((void *)out_mask, dout, 16 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  }
+  cudaFreeAsync(dx, st); cudaFreeAsync(dz, st); cudaFreeAsync(dqx, st);
+  cudaFreeAsync(dqz, st); cudaFreeAsync(dout, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
+int gs_conj_gate_rows(gs_engine *e, uint64_t *xs, uint64_t *zs, uint8_t *ph, uint32_t rows,
+                      uint32_t batch, const uint32_t *code, const uint64_t *m1,
+                      const uint64_t *m2) {
+  if (!e || !xs || !zs || !ph || !code || !m1 || !m2) return fail(GS_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  cudaStream_t st = e->stream;
+  const size_t nr = (size_t)rows * batch;
+  u64 *dx, *dz, *dm1, *dm2;
+  u8 *dph;
+  u32 *dcode;
+  if (to_dev(&dx, xs, nr, st) || to_dev(&dz, zs, nr, st) ||
+      to_dev(&dph, ph, nr, st) || to_dev(&dcode, code, batch, st) ||
+      to_dev(&dm1, m1, batch, st) || to_dev(&dm2, m2, batch, st))
+    return GS_ERR_CUDA;
+  if (nr) {
+    gs::conj_gate_kernel<<<(u32)((nr + 255) / 256), 256, 0, st>>>(dx, dz, dph, rows, batch, dcode, dm1, dm2);
+    CUDA_TRY(cudaGetLastError());
+    e->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync(xs, dx, nr * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(zs, dz, nr * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ph, dph, nr, cudaMemcpyDeviceToHost, st));
+  }
+  cudaFreeAsync(dx, st); cudaFreeAsync(dz, st); cudaFreeAsync(dph, st);
+  cudaFreeAsync(dcode, st); cudaFreeAsync(dm1, st); cudaFreeAsync(dm2, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
+int gs_mul_rows(gs_engine *e, uint64_t *xs, uint64_t *zs, uint8_t *ph, uint32_t rows,
+                uint32_t batch, const uint8_t *sel, const uint64_t *px, const uint64_t *pz,
+                const uint32_t *pe) {
+  if (!e || !xs || !zs || !ph || !sel || !px || !pz || !pe) return fail(GS_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  cudaStream_t st = e->stream;
+  const size_t nr = (size_t)rows * batch;
+  u64 *dx, *dz, *dpx, *dpz;
+  u8 *dph, *dsel;
+  u32 *dpe;
+  if (to_dev(&dx, xs, nr, st) || to_dev(&dz, zs, nr, st) ||
+      to_dev(&dph, ph, nr, st) || to_dev(&dsel, sel, nr, st) ||
+      to_dev(&dpx, px, batch, st) || to_dev(&dpz, pz, batch, st) || to_dev(&dpe, pe, batch, st))
+    return GS_ERR_CUDA;
+  if (nr) {
+    gs::mul_rows_kernel<<<(u32)((nr + 255) / 256), 256, 0, st>>>(dx, dz, dph, rows, batch, dsel, dpx, dpz, dpe);
+    CUDA_TRY(cudaGetLastError());
+    e->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync(xs, dx, nr * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(zs, dz, nr * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ph, dph, nr, cudaMemcpyDeviceToHost, st));
+  }
+  cudaFreeAsync(dx, st); cudaFreeAsync(dz, st); cudaFreeAsync(dph, st); cudaFreeAsync(dsel, st);
+  cudaFreeAsync(dpx, st); cudaFreeAsync(dpz, st); cudaFreeAsync(dpe, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
+int gs_parity_pm(gs_engine *e, const uint64_t *idx, size_t count, uint64_t mask, double *out) {
+  if (!e || (count && (!idx || !out))) return fail(GS_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  cudaStream_t st = e->stream;
+  u64 *di;
+  double *dout;
+  if (to_dev(&di, idx, count, st) || to_dev(&dout, nullptr, count, st))
+    return GS_ERR_CUDA;
+  if (count) {
+    gs::parity_pm_kernel<<<(u32)((count + 255) / 256), 256, 0, st>>>(di, count, mask, dout);
+    CUDA_TRY(cudaGetLastError());
+    e->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync(out, dout, count * 8, cudaMemcpyDeviceToHost, st));
+  }
+  cudaFreeAsync(di, st);
+  cudaFreeAsync(dout, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
+}  // extern "C"

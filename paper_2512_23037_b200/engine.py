@@ -1,0 +1,166 @@
+"""Thin owner objects over the C ABI: ``Engine`` (one per device) and
+``Program`` (a compiled op stream bound to the library).
+
+All sampling goes through ``libgstab_sm100a.so``; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+import threading
+
+import numpy as np
+
+from . import _lib
+from .compiler import DeviceProgram, compile_program
+
+
+def _u64p(a: np.ndarray):
+    return a.ctypes.data_as(ct.POINTER(ct.c_uint64))
+
+
+class Program:
+    """A ``DeviceProgram`` registered with the library (host copy; uploaded
+    to an engine's device on first use)."""
+
+    def __init__(self, dp: DeviceProgram):
+        self.dp = dp
+        lib = _lib.load()
+        info = _lib.GsProgramInfo(dp.num_qubits, dp.num_measurements,
+                                  dp.num_detectors, len(dp.obs_keys),
+                                  dp.max_dim, dp.num_locations)
+        self._ops = np.ascontiguousarray(dp.ops, dtype=np.uint64)
+        self._tables = np.ascontiguousarray(dp.tables, dtype=np.uint64)
+        self._locs = np.ascontiguousarray(dp.locs, dtype=np.uint64)
+        h = ct.c_void_p()
+        _lib.check(lib.gs_program_create(ct.byref(info), _u64p(self._ops),
+                                         self._ops.size, _u64p(self._tables),
+                                         self._tables.size, _u64p(self._locs),
+                                         self._locs.size, ct.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def compile(cls, prog, **kw) -> "Program":
+        return cls(compile_program(prog, **kw))
+
+    @property
+    def num_counters(self) -> int:
+        return _lib.GS_C_PER_OBS + len(self.dp.obs_keys)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().gs_program_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class Engine:
+    """A device context of the sampler (streams, scratch, counters)."""
+
+    def __init__(self, device: int = 0):
+        lib = _lib.load()
+        h = ct.c_void_p()
+        _lib.check(lib.gs_engine_create(int(device), ct.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().gs_engine_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    @staticmethod
+    def params(master_seed=0, shot_begin=0, shot_count=0, capacity=4096,
+               flags=0, warps_per_block=0, blocks=0, seeds=None):
+        p = _lib.GsRunParams()
+        p.master_seed = master_seed & 0xFFFFFFFFFFFFFFFF
+        p.shot_begin = shot_begin
+        p.shot_count = shot_count
+        p.capacity = capacity
+        p.flags = flags
+        p.warps_per_block = warps_per_block
+        p.blocks = blocks
+        p._seeds_keep = None
+        if seeds is not None:
+            s = np.ascontiguousarray(seeds, dtype=np.uint64)
+            p._seeds_keep = s
+            p.seeds = _u64p(s)
+        return p
+
+    # -- sampling -----------------------------------------------------
+
+    def run_counters(self, prog: Program, params) -> np.ndarray:
+        out = np.zeros(prog.num_counters, dtype=np.int64)
+        _lib.check(_lib.load().gs_run_counters(
+            self.handle, prog.handle, ct.byref(params),
+            out.ctypes.data_as(ct.POINTER(ct.c_int64))))
+        return out
+
+    def run_counters_async(self, prog: Program, params, counters_dev_ptr: int,
+                           stream_ptr: int) -> None:
+        _lib.check(_lib.load().gs_run_counters_async(
+            self.handle, prog.handle, ct.byref(params),
+            ct.c_void_p(counters_dev_ptr), ct.c_void_p(stream_ptr)))
+
+    def run_records(self, prog: Program, params):
+        S = params.shot_count
+        rw = (prog.dp.num_measurements + 63) // 64
+        status = np.zeros(max(S, 1), dtype=np.uint8)
+        aux = np.zeros(max(S, 1), dtype=np.int32)
+        rec = np.zeros((max(S, 1), max(rw, 1)), dtype=np.uint64)
+        obs = np.zeros(max(S, 1), dtype=np.uint64)
+        _lib.check(_lib.load().gs_run_records(
+            self.handle, prog.handle, ct.byref(params), status.ctypes.data,
+            aux.ctypes.data, rec.ctypes.data, obs.ctypes.data))
+        return status[:S], aux[:S], rec[:S, :rw], obs[:S]
+
+    def dump(self, prog: Program, params):
+        S = params.shot_count
+        rw = (prog.dp.num_measurements + 63) // 64
+        stride = 1 << prog.dp.max_dim
+        status = np.zeros(max(S, 1), dtype=np.uint8)
+        aux = np.zeros(max(S, 1), dtype=np.int32)
+        rec = np.zeros((max(S, 1), max(rw, 1)), dtype=np.uint64)
+        obs = np.zeros(max(S, 1), dtype=np.uint64)
+        sig = np.zeros((max(S, 1), 2), dtype=np.uint64)
+        cv = np.zeros(max(S, 1), dtype=np.uint64)
+        amps = np.zeros((max(S, 1), stride, 2), dtype=np.float64)
+        dim = np.zeros(max(S, 1), dtype=np.uint32)
+        _lib.check(_lib.load().gs_dump_shots(
+            self.handle, prog.handle, ct.byref(params), status.ctypes.data,
+            aux.ctypes.data, rec.ctypes.data, obs.ctypes.data, sig.ctypes.data,
+            cv.ctypes.data, amps.ctypes.data, dim.ctypes.data))
+        return {"status": status[:S], "aux": aux[:S], "rec": rec[:S, :rw],
+                "obs": obs[:S], "sig": sig[:S], "c": cv[:S],
+                "amps": amps[:S, :, 0] + 1j * amps[:S, :, 1], "dim": dim[:S]}
+
+    # -- diagnostics --------------------------------------------------
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.load().gs_engine_launches(self.handle))
+
+    @property
+    def last_kernel_ms(self) -> float:
+        return float(_lib.load().gs_engine_last_kernel_ms(self.handle))
+
+
+_engines: dict[int, Engine] = {}
+_engines_lock = threading.Lock()
+
+
+def get_engine(device: int = 0) -> Engine:
+    """Process-wide engine per device (created on first use)."""
+    with _engines_lock:
+        eng = _engines.get(device)
+        if eng is None:
+            eng = Engine(device)
+            _engines[device] = eng
+        return eng

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA sampler (through the C ABI) against the reference's
+golden fixtures and the CPU oracle.
+
+Bars (north star): records / statuses / counters bit-exact; tableau x/z/sign
+bits and amplitude indices exact; amplitudes within 1e-12 absolute (fp64,
+only the summation order differs from numpy).
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import gstab_oracle as orc
+from paper_2512_23037_b200 import (SamplerConfig, ShotContext, compile_program,
+                                   derive_seed, parse_circuit, run_batch,
+                                   run_shot, sample)
+from paper_2512_23037_b200 import _lib
+from paper_2512_23037_b200.engine import Engine, Program, get_engine
+from paper_2512_23037_b200.frames import reconstruct_state
+from paper_2512_23037_b200.sampler import _records_before
+
+AMP_TOL = 1e-12
+
+
+def _gpu_results(prog, master, shots, capacity, postselect, rng="splitmix",
+                 shot_begin=0, flags_extra=0):
+    dp = compile_program(prog)
+    p = Program(dp)
+    eng = get_engine(0)
+    flags = (_lib.GS_POSTSELECT if postselect else 0) | flags_extra
+    if rng == "philox":
+        flags |= _lib.GS_RNG_PHILOX
+    par = Engine.params(master, shot_begin, shots, capacity, flags)
+    status, aux, rec, obs = eng.run_records(p, par)
+    from paper_2512_23037_b200.sampler import ShotBatch
+    b = ShotBatch(status, aux, rec, obs, list(dp.obs_keys), dp.num_measurements)
+    out = []
+    for i in range(shots):
+        r = b.result(i, measured=_records_before(prog, b, i))
+        out.append({"status": r.status.value,
+                    "observables": {str(k): v for k, v in sorted(r.observables.items())},
+                    "discarded_detector": r.discarded_detector,
+                    "overflow_instruction": r.overflow_instruction,
+                    "record": r.record})
+    return out
+
+
+def _oracle_results(prog, master, shots, capacity, postselect, mode="splitmix",
+                    shot_begin=0):
+    flat = list(prog.flat())
+    out = []
+    for s in range(shot_begin, shot_begin + shots):
+        r = orc.run_one_shot(flat, prog.num_qubits,
+                             orc.DrawStream(mode, master, s), capacity, postselect)
+        out.append({"status": r["status"],
+                    "observables": {str(k): v for k, v in sorted(r["observables"].items())},
+                    "discarded_detector": r["discarded_detector"],
+                    "overflow_instruction": r["overflow_instruction"],
+                    "record": r["record"]})
+    return out
+
+
+def test_golden_shot_results_bit_exact(golden_shots):
+    for fx in golden_shots:
+        prog = parse_circuit(fx["text"])
+        got = _gpu_results(prog, fx["master"], len(fx["shots"]), fx["capacity"],
+                           fx["postselect"])
+        assert got == fx["shots"], fx["name"]
+
+
+def test_golden_shot_results_chi_in_global_memory(golden_shots):
+    for fx in golden_shots[::3]:
+        prog = parse_circuit(fx["text"])
+        got = _gpu_results(prog, fx["master"], len(fx["shots"]), fx["capacity"],
+                           fx["postselect"], flags_extra=_lib.GS_CHI_GLOBAL)
+        assert got == fx["shots"], fx["name"]
+
+
+def test_golden_state_snapshots(golden_states):
+    eng = get_engine(0)
+    for fx in golden_states:
+        prog = parse_circuit(fx["text"])
+        for snap in fx["snaps"]:
+            dp = compile_program(prog, stop_after=snap["i"], keep_frames=True)
+            p = Program(dp)
+            seeds = np.array([derive_seed(fx["master"], fx["shot"])], dtype=np.uint64)
+            d = eng.dump(p, Engine.params(fx["master"], 0, 1, 4096, 0, seeds=seeds))
+            assert int(d["status"][0]) == 1
+            st = reconstruct_state(dp, snap["i"], int(d["sig"][0][0]) |
+                                   (int(d["sig"][0][1]) << prog.num_qubits),
+                                   int(d["c"][0]), d["amps"][0])
+            assert st["xs"] == snap["xs"] and st["zs"] == snap["zs"]
+            assert st["ph"] == snap["ph"], (fx["text"], snap["i"])
+            assert st["idx"] == snap["idx"], (fx["text"], snap["i"])
+            np.testing.assert_allclose(np.array(st["amp"]), np.array(snap["amp"]),
+                                       rtol=0, atol=AMP_TOL)
+
+
+def test_golden_counters(golden_counters):
+    for fx in golden_counters:
+        kw = dict(fx["config"])
+        cfg = SamplerConfig(**kw)
+        st = run_batch(parse_circuit(fx["text"]), cfg)
+        want = fx["counters"]
+        assert st.total_shots == want["total"]
+        assert st.preserved_shots == want["preserved"]
+        assert st.discarded_shots == want["discarded"]
+        assert st.overflow_count == want["overflow"]
+        assert st.logical_error_shots == want["error_shots"]
+        assert {str(k): v for k, v in st.logical_errors.items()} == want["per_observable"]
+
+
+def _random_program(rng, n, gates, tcount, noise_p, mpp=True):
+    lines = ["H %d" % rng.randrange(n)]
+    meas = 0
+    one = ("I", "X", "Y", "Z", "H", "S", "S_DAG", "H_XY", "H_NXY")
+    for _ in range(gates):
+        r = rng.random()
+        if r < 0.12 and tcount > 0:
+            tcount -= 1
+            lines.append("%s %d" % (rng.choice(("T", "T_DAG")), rng.randrange(n)))
+        elif r < 0.40:
+            lines.append("%s %d" % (rng.choice(one), rng.randrange(n)))
+        elif r < 0.62 and n >= 2:
+            a, b = rng.sample(range(n), 2)
+            lines.append("%s %d %d" % (rng.choice(("CX", "CZ", "SWAP")), a, b))
+        elif r < 0.70:
+            lines.append("%s %d" % (rng.choice(("M", "MR", "R")), rng.randrange(n)))
+            meas += lines[-1][0] == "M"
+        elif r < 0.75 and mpp:
+            qs = rng.sample(range(n), min(n, rng.randint(1, 3)))
+            prod = "*".join("%s%d" % (rng.choice("XYZ"), q) for q in qs)
+            arg = "(%g)" % noise_p if rng.random() < 0.3 else ""
+            lines.append("MPP%s %s" % (arg, prod))
+            meas += 1
+        elif r < 0.84:
+            kind = rng.choice(("X_ERROR", "Z_ERROR", "DEPOLARIZE1", "DEPOLARIZE2"))
+            if kind == "DEPOLARIZE2" and n >= 2:
+                a, b = rng.sample(range(n), 2)
+                lines.append("DEPOLARIZE2(%g) %d %d" % (noise_p, a, b))
+            else:
+                kind = "DEPOLARIZE1" if kind == "DEPOLARIZE2" else kind
+                qs = [rng.randrange(n) for _ in range(rng.randint(1, 3))]
+                lines.append("%s(%g) %s" % (kind, noise_p, " ".join(map(str, qs))))
+        elif r < 0.90 and meas:
+            g = rng.choice(("X", "Z", "CX", "CZ"))
+            lines.append("%s rec[-%d] %d" % (g, rng.randint(1, meas), rng.randrange(n)))
+        elif r < 0.95 and meas:
+            lines.append("DETECTOR rec[-%d]" % rng.randint(1, meas))
+        else:
+            lines.append("TICK")
+    lines.append("M %d" % rng.randrange(n))
+    lines.append("OBSERVABLE_INCLUDE(%d) rec[-1]" % rng.randrange(3))
+    return parse_circuit("\n".join(lines) + "\n")
+
+
+@pytest.mark.parametrize("mode", ["splitmix", "philox"])
+def test_random_programs_match_oracle(mode):
+    rng = random.Random(1234 if mode == "splitmix" else 99)
+    for it in range(60):
+        n = rng.choice((2, 5, 9, 17, 33, 64))
+        prog = _random_program(rng, n, rng.choice((30, 80)), rng.choice((4, 10, 16)),
+                               rng.choice((0.02, 0.2)))
+        post = it % 2 == 0
+        cap = rng.choice((4, 64, 4096))
+        got = _gpu_results(prog, 5 + it, 24, cap, post, rng=mode, shot_begin=1000)
+        ref = _oracle_results(prog, 5 + it, 24, cap, post, mode=mode, shot_begin=1000)
+        assert got == ref, (it, prog.serialize())
+
+
+def test_run_shot_api_matches_reference_examples():
+    prog = parse_circuit("H 0\nH 1\nT 0\nT 1\n")
+    ctx = ShotContext(prog.num_qubits, 2)
+    ctx.reset(derive_seed(0, 0))
+    res = run_shot(prog, ctx)
+    assert res.status.value == "overflow" and res.overflow_instruction == 3
+    for shot in range(20):
+        ctx = ShotContext(2, 4096)
+        ctx.reset(derive_seed(0, shot))
+        res = run_shot(parse_circuit("H 0\nM 0\nX rec[-1] 0\nM 0\n"), ctx,
+                       keep_record=True)
+        assert res.record[1] == 0
+
+
+def test_shard_and_launch_shape_invariance():
+    from paper_2512_23037_b200.msc import msc_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(msc_circuit(3), 2e-3)
+    p = Program(compile_program(prog))
+    eng = get_engine(0)
+    flags = _lib.GS_POSTSELECT | _lib.GS_RNG_PHILOX
+    whole = eng.run_counters(p, Engine.params(7, 0, 20000, 32768, flags))
+    parts = sum(eng.run_counters(p, Engine.params(7, a, 5000, 32768, flags))
+                for a in range(0, 20000, 5000))
+    odd = eng.run_counters(p, Engine.params(7, 0, 20000, 32768, flags,
+                                            warps_per_block=3, blocks=17))
+    assert np.array_equal(whole, parts)
+    assert np.array_equal(whole, odd)
+
+
+@pytest.mark.parametrize("d", [3, 5])
+def test_msc_noiseless_is_deterministic(d):
+    from paper_2512_23037_b200.msc import msc_circuit
+    prog = msc_circuit(d)
+    st = run_batch(prog, SamplerConfig(shots=4096, postselect=True, rng="philox"))
+    assert st.discarded_shots == 0 and st.logical_error_shots == 0
+    assert st.preserved_shots == 4096
