@@ -48,6 +48,7 @@ extern "C" {
 #define GS_POSTSELECT 1u   /* discard on the first firing detector      */
 #define GS_RNG_PHILOX 2u   /* Philox4x32-10 streams (else SHA-1+SplitMix) */
 #define GS_CHI_GLOBAL 4u   /* force chi buffers into global memory (test) */
+#define GS_DENSE_ONLY 8u   /* disable the sparse occupancy list (test)   */
 
 /* per-shot status codes (gs_run_records) */
 #define GS_ST_PRESERVED 1
@@ -87,7 +88,7 @@ typedef struct {
   uint32_t flags;            /* GS_POSTSELECT | GS_RNG_PHILOX | ...      */
   uint32_t warps_per_block;  /* 0 = auto                                 */
   uint32_t blocks;           /* 0 = auto (persistent grid)               */
-  uint32_t reserved;
+  uint32_t list_cap;         /* occupancy-list capacity, 0 = default 128 */
   const uint64_t *seeds;     /* optional host per-shot seeds (SplitMix)  */
 } gs_run_params;
 

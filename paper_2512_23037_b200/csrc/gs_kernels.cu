@@ -47,7 +47,7 @@ enum { MODE_COUNTERS = 0, MODE_RECORDS = 1, MODE_DUMP = 2 };
 
 constexpr int kWinWords = 64;          // noise fire window: 2048 locations
 constexpr int kWinBytes = kWinWords * 4;
-constexpr double kPrune = 1e-12;
+constexpr double kPrune2 = 1e-24;   // (1e-12)^2, ref state.py:24
 constexpr int kEntryBytes = 24;        // SURVEY §8(d) state-touch model
 
 struct DevProg {
@@ -78,6 +78,7 @@ struct DevOut {
   u32 warp_bytes;       // dynamic smem bytes per warp
   u32 rec_in_smem;
   u32 chi_off;          // byte offset of chi inside the warp's smem slice
+  u32 lcap;             // occupancy-list capacity (<= kLcapMax; 0 = dense only)
 };
 
 // ---------------------------------------------------------------- helpers
@@ -95,13 +96,13 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) {
 __device__ __forceinline__ double2 cscale(double2 a, double r) {
   return make_double2(__dmul_rn(a.x, r), __dmul_rn(a.y, r));
 }
-__device__ __forceinline__ double habs(double2 v) { return hypot(v.x, v.y); }
+// |v|^2 as one fma; the reference's hypot(v)^2 and hypot(v) > 1e-12 agree
+// with these except within an ulp of the threshold
 __device__ __forceinline__ double abs2(double2 v) {
-  double h = hypot(v.x, v.y);
-  return __dmul_rn(h, h);
+  return __fma_rn(v.x, v.x, __dmul_rn(v.y, v.y));
 }
 __device__ __forceinline__ double2 prune(double2 v) {
-  return habs(v) > kPrune ? v : make_double2(0.0, 0.0);
+  return abs2(v) > kPrune2 ? v : make_double2(0.0, 0.0);
 }
 __device__ __forceinline__ u32 par64(u64 x) { return __popcll(x) & 1u; }
 __device__ __forceinline__ u32 par32(u32 x) { return __popc(x) & 1u; }
@@ -204,10 +205,44 @@ struct Rng {
   }
 };
 
+// ---------------------------------------------------------------- chi views
+//
+// The dense array A[0, 2^k) is always the storage (zero = absent entry, so
+// partner lookups are O(1)).  When at most `lcap` entries are nonzero the
+// warp also keeps their coordinates in the occupancy list L and iterates
+// only over those (sparse mode); otherwise it sweeps all 2^k coordinates
+// (dense mode).  Invariant: inside [0, 2^k) an entry is nonzero iff it is in
+// the support; positions >= 2^k are don't-care until a GROW initialises them.
+
+constexpr u32 kLcapMax = 128;
+constexpr u32 kR = kLcapMax / 32;
+
+__device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y != 0.0; }
+
+__device__ __forceinline__ u32 lanemask_lt(u32 lane) { return (1u << lane) - 1u; }
+
+// append `pos` for every lane with `flag`, preserving lane order
+__device__ __forceinline__ void list_push(u32 *L, u32 &base, bool flag, u32 pos, u32 lane) {
+  const u32 bal = __ballot_sync(FULL, flag);
+  if (flag) L[base + __popc(bal & lanemask_lt(lane))] = pos;
+  base += __popc(bal);
+}
+
+// rebuild the occupancy list from a dense scan (only when cnt <= lcap)
+__device__ void build_list(const double2 *A, u32 *L, u32 size, u32 lane) {
+  u32 base = 0;
+  for (u32 b = 0; b < size; b += 32) {
+    const u32 j = b + lane;
+    const bool nz = j < size && nonzero(A[j]);
+    list_push(L, base, nz, j, lane);
+  }
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------- kernel
 
 template <bool kSmemChi>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 sample_kernel(DevProg P, DevRun R, DevOut O) {
   extern __shared__ __align__(16) u8 smem[];
   const u32 lane = threadIdx.x & 31u;
@@ -216,7 +251,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
   const u64 gw = (u64)blockIdx.x * wpb + wib;
   u8 *mine = smem + (size_t)wib * O.warp_bytes;
   u32 *win = reinterpret_cast<u32 *>(mine);
-  u32 *rec = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kWinBytes)
+  u32 *L = reinterpret_cast<u32 *>(mine + kWinBytes);
+  u32 *rec = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kWinBytes + 4 * kLcapMax)
                            : O.grec + gw * P.rec_words32;
   double2 *A = kSmemChi ? reinterpret_cast<double2 *>(mine + O.chi_off)
                         : O.gchi + gw * ((u64)1 << P.max_dim);
@@ -225,6 +261,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
   const u64 *__restrict__ tables = P.tables;
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
+  const u32 lcap = O.lcap;
 
   long long n_tot = 0, n_pres = 0, n_disc = 0, n_ovf = 0, n_cor = 0, n_uns = 0,
             n_err = 0;
@@ -244,21 +281,27 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
     if (!rng.philox) rng.seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
 
     for (u32 w = lane; w < P.rec_words32; w += 32) rec[w] = 0;
-    if (lane == 0) A[0] = make_double2(1.0, 0.0);
+    if (lane == 0) {
+      A[0] = make_double2(1.0, 0.0);
+      L[0] = 0;
+    }
     __syncwarp();
 
     u64 sig_lo = 0, sig_hi = 0, c = 0, obs = 0, mbytes = 0;
     u32 cnt = 1, kcur = 0, pc = 0;
+    bool lst = lcap >= 1;          // occupancy list valid
     int status = ST_RUNNING, aux = -1;
     u32 win_base = 0xFFFFFFFFu;
+    u64 hnext = __ldg(ops);
 
     while (status == ST_RUNNING) {
       const u64 *op = ops + pc;
-      const u64 h = __ldg(op);
+      const u64 h = hnext;
       const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
       const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
       const u32 instr = (u32)(h >> 32);
       pc += len;
+      hnext = __ldg(ops + pc);       // prefetch the next header
       kcur = k;
       const u32 size = 1u << k;
 
@@ -330,12 +373,12 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
           const u64 *tb = tables + off + 10ull * slot;
           const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
-          const u32 xw = (u32)__ldg(tb + 4);
-          const u32 xx = ((xw & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
+          const u64 xw64 = __ldg(tb + 4);
+          const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
           const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
           const u64 zw64 = __ldg(tb + 9);
           const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
-          const u32 xdm = (u32)(__ldg(tb + 4) >> 8), zdm = (u32)(zw64 >> 8);
+          const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
           const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
           u64 lb, ld; u32 lxi, ldm;
           if (hx && hz) {
@@ -354,9 +397,14 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const double2 php = cmul(I, make_double2(1.0, 0.0));
         const double2 phm = cmul(I, make_double2(-1.0, 0.0));
         const u32 dc = par64(delt & c);
-        for (u32 j = lane; j < size; j += 32) {
-          const u32 s = dc ^ par32(j & dm);
-          A[j] = cmul(A[j], s ? phm : php);
+        if (lst) {
+          for (u32 i = lane; i < cnt; i += 32) {
+            const u32 j = L[i];
+            A[j] = cmul(A[j], (dc ^ par32(j & dm)) ? phm : php);
+          }
+        } else {
+          for (u32 j = lane; j < size; j += 32)
+            A[j] = cmul(A[j], (dc ^ par32(j & dm)) ? phm : php);
         }
         __syncwarp();
         c ^= beta;
@@ -380,56 +428,135 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u32 dc = par64(delta & c);
         const u32 tcase = fl & 3u;
         if (tcase == T_DIAG) {
+          // beta == 0: pure phase per entry (ref state.py:120-126)
           const double2 f0 = cadd(a, bx0), f1 = cadd(a, bx1);
-          for (u32 j = lane; j < size; j += 32) {
-            const u32 s = dc ^ par32(j & dmask);
-            A[j] = cmul(A[j], s ? f1 : f0);
+          if (lst) {
+            for (u32 i = lane; i < cnt; i += 32) {
+              const u32 j = L[i];
+              A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
+            }
+          } else {
+            for (u32 j = lane; j < size; j += 32)
+              A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
           }
           __syncwarp();
           mbytes += 32ull * cnt;
           continue;
         }
         const u32 cin = cnt;
-        u32 nz = 0;
         if (kind == OP_GROW_LIMIT) {
+          u32 nz = 0;
           for (u32 j = lane; j < size; j += 32) {
             const double2 v = A[j];
             const u32 s = dc ^ par32(j & dmask);
-            nz += habs(cadd(Z, cmul(a, v))) > kPrune;
-            nz += habs(cadd(Z, cmul(s ? bx1 : bx0, v))) > kPrune;
+            nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
+            nz += abs2(cadd(Z, cmul(s ? bx1 : bx0, v))) > kPrune2;
           }
           nz = warp_sum_u32(nz);
           status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
           aux = (int)instr;
           break;
         }
-        if (tcase == T_BUTTERFLY) {
-          const u32 hb = 31 - __clz(cb);
-          const u32 half = size >> 1;
-          for (u32 m = lane; m < half; m += 32) {
-            const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
-            const double2 v0 = A[j0], v1 = A[j1];
-            const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
-            const double2 n0 = prune(cadd(cadd(Z, cmul(a, v0)), cmul(s1 ? bx1 : bx0, v1)));
-            const double2 n1 = prune(cadd(cadd(Z, cmul(a, v1)), cmul(s0 ? bx1 : bx0, v0)));
-            A[j0] = n0;
-            A[j1] = n1;
-            nz += (n0.x != 0.0 || n0.y != 0.0) + (n1.x != 0.0 || n1.y != 0.0);
+        const bool grow = tcase == T_GROW;
+        u32 ncnt = 0;
+        if (lst && 2 * cnt <= lcap) {
+          // ---- sparse merge: each listed entry owns its pair unless its
+          // partner is a listed lower member (ref state.py:127-129, 294-306)
+          const u32 hb = grow ? 0u : 31 - __clz(cb);
+          if (grow) {
+            for (u32 m = lane; m < size; m += 32) A[size + m] = Z;
+            __syncwarp();
           }
-        } else {  // T_GROW: beta becomes coordinate k
-          for (u32 j = lane; j < size; j += 32) {
-            const double2 v = A[j];
-            const u32 s = dc ^ par32(j & dmask);
-            const double2 n0 = prune(cadd(Z, cmul(a, v)));
-            const double2 n1 = prune(cadd(Z, cmul(s ? bx1 : bx0, v)));
-            A[j] = n0;
-            A[size + j] = n1;
-            nz += (n0.x != 0.0 || n0.y != 0.0) + (n1.x != 0.0 || n1.y != 0.0);
+          u32 pj[kR], pp[kR];
+          double2 vj[kR], vp[kR];
+          bool proc[kR];
+#pragma unroll
+          for (u32 r = 0; r < kR; ++r) {
+            const u32 i = lane + 32 * r;
+            proc[r] = false;
+            pj[r] = pp[r] = 0;
+            vj[r] = vp[r] = Z;
+            if (i < cnt) {
+              const u32 j = L[i];
+              pj[r] = j;
+              vj[r] = A[j];
+              if (grow) {
+                pp[r] = j + size;
+                proc[r] = true;
+              } else {
+                const u32 p = j ^ cb;
+                pp[r] = p;
+                vp[r] = A[p];
+                proc[r] = !(((j >> hb) & 1u) && nonzero(vp[r]));
+              }
+            }
           }
-          kcur = k + 1;
+          __syncwarp();
+          bool nz0[kR], nz1[kR];
+#pragma unroll
+          for (u32 r = 0; r < kR; ++r) {
+            nz0[r] = nz1[r] = false;
+            if (proc[r]) {
+              const u32 j = pj[r], p = pp[r];
+              const double2 aterm = cadd(Z, cmul(a, vj[r]));
+              const u32 sj = dc ^ par32(j & dmask);
+              double2 n0, n1;
+              if (grow) {
+                n0 = prune(aterm);
+                n1 = prune(cadd(Z, cmul(sj ? bx1 : bx0, vj[r])));
+              } else {
+                const u32 sp = dc ^ par32(p & dmask);
+                n0 = prune(cadd(aterm, cmul(sp ? bx1 : bx0, vp[r])));
+                n1 = prune(cadd(cadd(Z, cmul(a, vp[r])), cmul(sj ? bx1 : bx0, vj[r])));
+              }
+              A[j] = n0;
+              A[p] = n1;
+              nz0[r] = nonzero(n0);
+              nz1[r] = nonzero(n1);
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (u32 r = 0; r < kR; ++r) {
+            list_push(L, ncnt, nz0[r], pj[r], lane);
+            list_push(L, ncnt, nz1[r], pp[r], lane);
+          }
+          __syncwarp();
+          lst = true;
+        } else {
+          // ---- dense merge over all coordinates
+          u32 nz = 0;
+          if (!grow) {
+            const u32 hb = 31 - __clz(cb);
+            const u32 half = size >> 1;
+            for (u32 m = lane; m < half; m += 32) {
+              const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+              const double2 v0 = A[j0], v1 = A[j1];
+              const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+              const double2 n0 = prune(cadd(cadd(Z, cmul(a, v0)), cmul(s1 ? bx1 : bx0, v1)));
+              const double2 n1 = prune(cadd(cadd(Z, cmul(a, v1)), cmul(s0 ? bx1 : bx0, v0)));
+              A[j0] = n0;
+              A[j1] = n1;
+              nz += nonzero(n0) + nonzero(n1);
+            }
+          } else {
+            for (u32 j = lane; j < size; j += 32) {
+              const double2 v = A[j];
+              const u32 s = dc ^ par32(j & dmask);
+              const double2 n0 = prune(cadd(Z, cmul(a, v)));
+              const double2 n1 = prune(cadd(Z, cmul(s ? bx1 : bx0, v)));
+              A[j] = n0;
+              A[size + j] = n1;
+              nz += nonzero(n0) + nonzero(n1);
+            }
+          }
+          __syncwarp();
+          ncnt = warp_sum_u32(nz);
+          lst = ncnt <= lcap;
+          if (lst) build_list(A, L, grow ? 2 * size : size, lane);
         }
-        __syncwarp();
-        cnt = warp_sum_u32(nz);
+        if (grow) kcur = k + 1;
+        cnt = ncnt;
         mbytes += (u64)kEntryBytes * (cin + cnt);
         if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr; break; }
         if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
@@ -452,138 +579,274 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u32 dc = par64(delta & c);
         const double u = rng.uniform(udraw);
         const u32 cin = cnt;
+        const bool compact = (fl & MF_COMPACT) != 0;
         bool plus;
         if (mcase == M_DET) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
           double sp = 0.0, sm = 0.0;
-          for (u32 j = lane; j < size; j += 32) {
-            const double a2 = abs2(A[j]);
-            if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
-            else sp = __dadd_rn(sp, a2);
-          }
-          sp = warp_sum(sp);
-          sm = warp_sum(sm);
-          plus = u < sp;
-          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-          const u32 want_neg = plus ? 0u : 1u;
-          const double r = 1.0 / sqrt(plus ? sp : sm);
-          u32 nz = 0;
-          if (fl & MF_COMPACT) {
-            const u32 tau = want_neg ^ neg0;
-            const u32 half = size >> 1;
-            for (u32 base = 0; base < half; base += 32) {
-              const u32 jp = base + lane;
-              double2 v = Z;
-              if (jp < half) {
-                const u32 j0 = ins_bit(jp, isq, 0);
-                v = A[j0 | ((tau ^ par32(j0 & dmask)) << isq)];
+          if (lst) {
+            u32 pj[kR];
+            double2 vj[kR];
+            bool ng[kR];
+#pragma unroll
+            for (u32 r = 0; r < kR; ++r) {
+              const u32 i = lane + 32 * r;
+              pj[r] = 0; vj[r] = Z; ng[r] = false;
+              if (i < cnt) {
+                pj[r] = L[i];
+                vj[r] = A[pj[r]];
+                ng[r] = (neg0 ^ par32(pj[r] & dmask)) != 0;
+                const double a2 = abs2(vj[r]);
+                if (ng[r]) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
               }
-              __syncwarp();
-              if (jp < half) {
-                v = cscale(v, r);
-                A[jp] = v;
-                nz += (v.x != 0.0 || v.y != 0.0);
-              }
+            }
+            sp = warp_sum(sp);
+            sm = warp_sum(sm);
+            plus = u < sp;
+            const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+            const bool want_neg = !plus;
+            const double rs = 1.0 / sqrt(plus ? sp : sm);
+            if (compact) {
+              const u32 tau = (want_neg ? 1u : 0u) ^ neg0;
+              if (tau) c ^= vec;
+#pragma unroll
+              for (u32 r = 0; r < kR; ++r)
+                if (lane + 32 * r < cnt) A[pj[r]] = Z;
               __syncwarp();
             }
-            if (tau) c ^= vec;
-            kcur = k - 1;
-          } else {
-            for (u32 j = lane; j < size; j += 32) {
-              const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
-              const double2 v = keep ? cscale(A[j], r) : Z;
-              A[j] = v;
-              nz += (v.x != 0.0 || v.y != 0.0);
+            u32 ncnt = 0;
+#pragma unroll
+            for (u32 r = 0; r < kR; ++r) {
+              const bool valid = lane + 32 * r < cnt;
+              const bool keep = valid && ng[r] == want_neg;
+              u32 dst = pj[r];
+              if (compact) {
+                const u32 low = dst & ((1u << isq) - 1u);
+                dst = ((dst >> (isq + 1)) << isq) | low;
+                if (keep) A[dst] = cscale(vj[r], rs);
+              } else if (valid) {
+                A[dst] = keep ? cscale(vj[r], rs) : Z;
+              }
+              list_push(L, ncnt, keep, dst, lane);
             }
             __syncwarp();
+            cnt = ncnt;
+            if (compact) kcur = k - 1;
+          } else {
+            for (u32 j = lane; j < size; j += 32) {
+              const double a2 = abs2(A[j]);
+              if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
+              else sp = __dadd_rn(sp, a2);
+            }
+            sp = warp_sum(sp);
+            sm = warp_sum(sm);
+            plus = u < sp;
+            const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+            const u32 want_neg = plus ? 0u : 1u;
+            const double rs = 1.0 / sqrt(plus ? sp : sm);
+            u32 nz = 0;
+            u32 nsize = size;
+            if (compact) {
+              const u32 tau = want_neg ^ neg0;
+              const u32 half = size >> 1;
+              for (u32 base = 0; base < half; base += 32) {
+                const u32 jp = base + lane;
+                double2 v = Z;
+                if (jp < half) {
+                  const u32 j0 = ins_bit(jp, isq, 0);
+                  v = A[j0 | ((tau ^ par32(j0 & dmask)) << isq)];
+                }
+                __syncwarp();
+                if (jp < half) {
+                  v = cscale(v, rs);
+                  A[jp] = v;
+                  nz += nonzero(v);
+                }
+                __syncwarp();
+              }
+              if (tau) c ^= vec;
+              kcur = k - 1;
+              nsize = half;
+            } else {
+              for (u32 j = lane; j < size; j += 32) {
+                const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
+                const double2 v = keep ? cscale(A[j], rs) : Z;
+                A[j] = v;
+                nz += nonzero(v);
+              }
+              __syncwarp();
+            }
+            cnt = warp_sum_u32(nz);
+            lst = cnt <= lcap;
+            if (lst) build_list(A, L, nsize, lane);
           }
-          cnt = warp_sum_u32(nz);
         } else {
           // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
           const double2 I = ipow(xi0);
           const double2 xpp = cmul(I, make_double2(1.0, 0.0));
           const double2 xpm = cmul(I, make_double2(-1.0, 0.0));
           const u32 ct = (u32)(c >> t) & 1u;
-          double sp = 0.0;
           const bool span = mcase == M_PIVOT_SPAN;
-          const u32 npairs = span ? (size >> 1) : size;
-          for (u32 m = lane; m < npairs; m += 32) {
-            double2 wpv;
-            if (span) {
-              const u32 j0 = ins_bit(m, isq, 0);
-              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-              const u32 part = rep ^ cb;
-              const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
-              wpv = cadd(A[rep], prod);
-            } else {
-              const double2 v = A[m];
-              if (ct ^ par32(m & tmask)) {
-                wpv = cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v));
-              } else {
-                wpv = v;
+          if (lst) {
+            u32 prep[kR];
+            double2 vr[kR], pr[kR];
+            bool proc[kR];
+            double sp = 0.0;
+#pragma unroll
+            for (u32 r = 0; r < kR; ++r) {
+              const u32 i = lane + 32 * r;
+              proc[r] = false; prep[r] = 0; vr[r] = pr[r] = Z;
+              if (i < cnt) {
+                const u32 j = L[i];
+                const bool is_part = (ct ^ par32(j & tmask)) != 0;
+                if (span) {
+                  const u32 other = j ^ cb;
+                  const u32 rep = is_part ? other : j, part = is_part ? j : other;
+                  const double2 v_rep = A[rep], v_part = A[part];
+                  proc[r] = !(is_part && nonzero(v_rep));
+                  prep[r] = rep;
+                  vr[r] = v_rep;
+                  pr[r] = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, v_part);
+                } else {
+                  proc[r] = true;
+                  prep[r] = j;
+                  if (is_part) {
+                    vr[r] = Z;      // representative alpha^beta is absent
+                    pr[r] = cmul((dc ^ par32(j & dmask)) ? xpm : xpp, A[j]);
+                  } else {
+                    vr[r] = A[j];
+                    pr[r] = Z;
+                  }
+                }
+                if (proc[r]) sp = __dadd_rn(sp, abs2(cadd(vr[r], pr[r])));
               }
             }
-            sp = __dadd_rn(sp, abs2(wpv));
-          }
-          sp = warp_sum(sp);
-          const double pp = __dmul_rn(0.5, sp);
-          plus = u < pp;
-          const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-          double sk = 0.0;
-          u32 nz = 0;
-          for (u32 m = lane; m < npairs; m += 32) {
-            double2 w;
-            u32 dst;
-            if (span) {
-              const u32 j0 = ins_bit(m, isq, 0);
-              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-              const u32 part = rep ^ cb;
-              const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
-              w = plus ? cadd(A[rep], prod) : csub(A[rep], prod);
-              dst = rep;
-            } else {
-              const double2 v = A[m];
-              if (ct ^ par32(m & tmask)) {
-                const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
-                w = plus ? cadd(Z, prod) : csub(Z, prod);
-              } else {
-                w = v;
+            sp = warp_sum(sp);
+            const double pp = __dmul_rn(0.5, sp);
+            plus = u < pp;
+            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+            double sk = 0.0;
+            double2 wv[kR];
+            bool wnz[kR];
+#pragma unroll
+            for (u32 r = 0; r < kR; ++r) {
+              wv[r] = Z; wnz[r] = false;
+              if (proc[r]) {
+                wv[r] = prune(plus ? cadd(vr[r], pr[r]) : csub(vr[r], pr[r]));
+                wnz[r] = nonzero(wv[r]);
+                sk = __dadd_rn(sk, abs2(wv[r]));
               }
-              dst = m;
             }
-            w = prune(w);
-            A[dst] = w;
-            sk = __dadd_rn(sk, abs2(w));
-            nz += (w.x != 0.0 || w.y != 0.0);
-          }
-          __syncwarp();
-          sk = warp_sum(sk);
-          nz = warp_sum_u32(nz);
-          if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-          const double r = 1.0 / sqrt(sk);
-          if (span) {
-            const u32 half = size >> 1;
-            for (u32 base = 0; base < half; base += 32) {
-              const u32 jp = base + lane;
-              double2 v = Z;
-              if (jp < half) {
-                const u32 j0 = ins_bit(jp, isq, 0);
-                v = A[j0 | ((ct ^ par32(j0 & tmask)) << isq)];
-              }
-              __syncwarp();
-              if (jp < half) A[jp] = cscale(v, r);
+            sk = warp_sum(sk);
+            u32 any = 0;
+#pragma unroll
+            for (u32 r = 0; r < kR; ++r) any |= wnz[r];
+            if (!__any_sync(FULL, any)) { status = ST_CORRUPT; aux = (int)instr; break; }
+            const double rs = 1.0 / sqrt(sk);
+            if (span) {
+              // clear both members of every processed pair, then write the
+              // squeezed representatives
+#pragma unroll
+              for (u32 r = 0; r < kR; ++r)
+                if (proc[r]) { A[prep[r]] = Z; A[prep[r] ^ cb] = Z; }
               __syncwarp();
             }
-            kcur = k - 1;
-          } else {
-            for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], r);
+            u32 ncnt = 0;
+#pragma unroll
+            for (u32 r = 0; r < kR; ++r) {
+              u32 dst = prep[r];
+              if (span) {
+                const u32 low = dst & ((1u << isq) - 1u);
+                dst = ((dst >> (isq + 1)) << isq) | low;
+              }
+              if (proc[r]) A[dst] = wnz[r] ? cscale(wv[r], rs) : Z;
+              list_push(L, ncnt, wnz[r], dst, lane);
+            }
             __syncwarp();
+            cnt = ncnt;
+            if (span) kcur = k - 1;
+          } else {
+            double sp = 0.0;
+            const u32 npairs = span ? (size >> 1) : size;
+            for (u32 m = lane; m < npairs; m += 32) {
+              double2 wpv;
+              if (span) {
+                const u32 j0 = ins_bit(m, isq, 0);
+                const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+                const u32 part = rep ^ cb;
+                wpv = cadd(A[rep], cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]));
+              } else {
+                const double2 v = A[m];
+                wpv = (ct ^ par32(m & tmask)) ? cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v)) : v;
+              }
+              sp = __dadd_rn(sp, abs2(wpv));
+            }
+            sp = warp_sum(sp);
+            const double pp = __dmul_rn(0.5, sp);
+            plus = u < pp;
+            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+            double sk = 0.0;
+            u32 nz = 0;
+            for (u32 m = lane; m < npairs; m += 32) {
+              double2 w;
+              u32 dst;
+              if (span) {
+                const u32 j0 = ins_bit(m, isq, 0);
+                const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+                const u32 part = rep ^ cb;
+                const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
+                w = plus ? cadd(A[rep], prod) : csub(A[rep], prod);
+                dst = rep;
+              } else {
+                const double2 v = A[m];
+                if (ct ^ par32(m & tmask)) {
+                  const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
+                  w = plus ? cadd(Z, prod) : csub(Z, prod);
+                } else {
+                  w = v;
+                }
+                dst = m;
+              }
+              w = prune(w);
+              A[dst] = w;
+              sk = __dadd_rn(sk, abs2(w));
+              nz += nonzero(w);
+            }
+            __syncwarp();
+            sk = warp_sum(sk);
+            nz = warp_sum_u32(nz);
+            if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+            const double rs = 1.0 / sqrt(sk);
+            u32 nsize = size;
+            if (span) {
+              const u32 half = size >> 1;
+              for (u32 base = 0; base < half; base += 32) {
+                const u32 jp = base + lane;
+                double2 v = Z;
+                if (jp < half) {
+                  const u32 j0 = ins_bit(jp, isq, 0);
+                  v = A[j0 | ((ct ^ par32(j0 & tmask)) << isq)];
+                }
+                __syncwarp();
+                if (jp < half) A[jp] = cscale(v, rs);
+                __syncwarp();
+              }
+              kcur = k - 1;
+              nsize = half;
+            } else {
+              for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], rs);
+              __syncwarp();
+            }
+            cnt = nz;
+            lst = cnt <= lcap;
+            if (lst) build_list(A, L, nsize, lane);
           }
           if (ct) c ^= vec;
-          cnt = nz;
           // tableau sign update of the pivot (ref tableau.py:176-200)
           const u32 v = (u32)(sig_hi >> t) & 1u;
           if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
@@ -618,12 +881,12 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u64 w1 = __ldg(op + 1);
         const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
         const u64 off = __ldg(op + 2);
-        u32 b = 0;
+        u32 bb = 0;
         for (u32 i = lane; i < nidx; i += 32) {
           const u32 idx = (u32)__ldg(tables + off + i);
-          b ^= (rec[idx >> 5] >> (idx & 31)) & 1u;
+          bb ^= (rec[idx >> 5] >> (idx & 31)) & 1u;
         }
-        const u32 parity = __popc(__ballot_sync(FULL, b)) & 1u;
+        const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
         if (kind == OP_DETECTOR) {
           if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
         } else {
@@ -912,13 +1175,13 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
   if (L.rec_words32 == 0) L.rec_words32 = 2;
   const size_t rec_b = (size_t)L.rec_words32 * 4;
   L.rec_in_smem = rec_b <= 2048;
-  size_t base = gs::kWinBytes + (L.rec_in_smem ? rec_b : 0);
+  size_t base = gs::kWinBytes + 4 * gs::kLcapMax + (L.rec_in_smem ? rec_b : 0);
   base = (base + 15) & ~(size_t)15;
   L.smem_chi = !(r->flags & GS_CHI_GLOBAL) && chi <= 48 * 1024;
   L.chi_off = (u32)base;
   L.warp_bytes = (u32)(base + (L.smem_chi ? chi : 0));
   u32 wpb = r->warps_per_block ? r->warps_per_block : 4;
-  if (wpb > 8) wpb = 8;
+  if (wpb > 4) wpb = 4;   // __launch_bounds__(128)
   while (wpb > 1 && (size_t)wpb * L.warp_bytes > e->smem_optin) --wpb;
   if ((size_t)wpb * L.warp_bytes > e->smem_optin)
     return fail(GS_ERR_UNSUPPORTED, "per-warp state exceeds shared memory");
@@ -1009,6 +1272,8 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   O.warp_bytes = L.warp_bytes;
   O.rec_in_smem = L.rec_in_smem;
   O.chi_off = L.chi_off;
+  O.lcap = (r->flags & GS_DENSE_ONLY) ? 0u
+           : (r->list_cap == 0 || r->list_cap > gs::kLcapMax ? gs::kLcapMax : r->list_cap);
   CUDA_TRY(cudaMemsetAsync(e->d_next, 0, sizeof(u64), st));
   if (r->shot_count) {
     if (timed) CUDA_TRY(cudaEventRecord(e->ev0, st));

@@ -208,3 +208,61 @@ def test_msc_noiseless_is_deterministic(d):
     st = run_batch(prog, SamplerConfig(shots=4096, postselect=True, rng="philox"))
     assert st.discarded_shots == 0 and st.logical_error_shots == 0
     assert st.preserved_shots == 4096
+
+
+@pytest.mark.parametrize("variant", ["dense_only", "lcap4", "lcap32", "chi_global"])
+def test_chi_storage_modes_match_oracle(variant):
+    """Sparse occupancy list / dense sweeps / global-memory chi must all give
+    the oracle's results (mode switches are exercised with tiny list caps)."""
+    rng = random.Random(7)
+    flags_extra, lcap = 0, 0
+    if variant == "dense_only":
+        flags_extra = _lib.GS_DENSE_ONLY
+    elif variant == "chi_global":
+        flags_extra = _lib.GS_CHI_GLOBAL
+    else:
+        lcap = int(variant[4:])
+    eng = get_engine(0)
+    for it in range(25):
+        n = rng.choice((4, 9, 20))
+        prog = _random_program(rng, n, 70, rng.choice((8, 14)), 0.1)
+        dp = compile_program(prog)
+        p = Program(dp)
+        flags = _lib.GS_POSTSELECT * (it % 2) | flags_extra
+        par = Engine.params(3 + it, 0, 16, 4096, flags, list_cap=lcap)
+        status, aux, rec, obs = eng.run_records(p, par)
+        from paper_2512_23037_b200.sampler import ShotBatch
+        b = ShotBatch(status, aux, rec, obs, list(dp.obs_keys), dp.num_measurements)
+        ref = _oracle_results(prog, 3 + it, 16, 4096, bool(it % 2))
+        for i in range(16):
+            r = b.result(i, measured=_records_before(prog, b, i))
+            assert r.status.value == ref[i]["status"], (variant, it, i)
+            assert r.record == ref[i]["record"], (variant, it, i)
+
+
+def test_msc_d5_dumps_match_oracle_through_t_layer():
+    """Full-size state check: the d=5 proxy with chi peaking at 1024
+    entries, dumped after the first T layer and after the undo layer."""
+    from paper_2512_23037_b200.msc import msc_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(msc_circuit(5), 2e-3)
+    flat = list(prog.flat())
+    t_idx = [i for i, ins in enumerate(flat) if ins.name in ("T", "T_DAG")]
+    eng = get_engine(0)
+    for stop in (t_idx[20], t_idx[40], t_idx[59] + 3):
+        dp = compile_program(prog, stop_after=stop, keep_frames=True)
+        p = Program(dp)
+        for shot in range(3):
+            seeds = np.array([derive_seed(4, shot)], dtype=np.uint64)
+            d = eng.dump(p, Engine.params(4, 0, 1, 1 << 20, 0, seeds=seeds))
+            ref = orc.run_one_shot(flat, prog.num_qubits,
+                                   orc.DrawStream("splitmix", 4, shot), 1 << 20,
+                                   False, stop_after=stop, snapshot=True)
+            assert int(d["status"][0]) == 1
+            st = reconstruct_state(dp, stop, int(d["sig"][0][0]) |
+                                   (int(d["sig"][0][1]) << prog.num_qubits),
+                                   int(d["c"][0]), d["amps"][0])
+            rs = ref["state"]
+            assert st["ph"] == rs["ph"] and st["idx"] == rs["idx"]
+            np.testing.assert_allclose(np.array(st["amp"]), np.array(rs["amp"]),
+                                       rtol=0, atol=AMP_TOL)
