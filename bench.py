@@ -139,6 +139,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chi-global", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
+    ap.add_argument("--dense-only", action="store_true")
+    ap.add_argument("--list-cap", type=int, default=0)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -190,6 +192,8 @@ def main():
     flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if args.rng == "philox" else 0)
     if args.chi_global:
         flags |= _lib.GS_CHI_GLOBAL
+    if args.dense_only:
+        flags |= _lib.GS_DENSE_ONLY
     S = args.shots_per_step
     nc = P.num_counters
     stream = torch.cuda.current_stream()
@@ -198,7 +202,8 @@ def main():
 
     def launch(step):
         base = step * world * S + rank * S
-        par = Engine.params(12345, base, S, 32768, flags, warps_per_block=args.wpb)
+        par = Engine.params(12345, base, S, 32768, flags, warps_per_block=args.wpb,
+                            list_cap=args.list_cap)
         eng.run_counters_async(P, par, counters.data_ptr(), stream.cuda_stream)
 
     for w in range(args.warmup):
