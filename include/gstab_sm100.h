@@ -78,6 +78,10 @@ typedef struct {
   uint32_t num_obs;          /* distinct observable keys (<= 64)         */
   uint32_t max_dim;          /* static chi dimension k_max (<= 30)       */
   uint32_t num_locations;    /* noise locations                          */
+  uint32_t num_noise;        /* noise instructions (tables[noise_off..]) */
+  uint32_t num_words;        /* ceil(num_locations / 32)                 */
+  uint64_t noise_off;        /* tables offset: 4 words per noise instr.  */
+  uint64_t wordpc_off;       /* tables offset: insertion pc per word     */
 } gs_program_info;
 
 typedef struct {

@@ -46,7 +46,9 @@ class EngineUnavailable(RuntimeError):
 class GsProgramInfo(ct.Structure):
     _fields_ = [("num_qubits", ct.c_uint32), ("num_measurements", ct.c_uint32),
                 ("num_detectors", ct.c_uint32), ("num_obs", ct.c_uint32),
-                ("max_dim", ct.c_uint32), ("num_locations", ct.c_uint32)]
+                ("max_dim", ct.c_uint32), ("num_locations", ct.c_uint32),
+                ("num_noise", ct.c_uint32), ("num_words", ct.c_uint32),
+                ("noise_off", ct.c_uint64), ("wordpc_off", ct.c_uint64)]
 
 
 class GsRunParams(ct.Structure):

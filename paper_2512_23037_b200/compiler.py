@@ -23,8 +23,11 @@ Why a static frame:
 
 Encoding: ``ops`` is a u64 stream of variable-length records
 ``[header, payload...]``; header = kind | len<<8 | k<<16 | flags<<24 |
-flat_instruction<<32.  ``tables`` holds noise letter tables and record index
-lists; ``locs`` holds two words per noise location.  The layout is mirrored
+flat_instruction<<32.  Noise instructions are *not* in the stream: the
+``tables`` array holds, besides letter tables and record index lists, a noise
+instruction table (insertion pc, location range, qubit mask, letter table)
+and the insertion pc of every 32-location word of the fire bitset; ``locs``
+holds two words (draw index | qubits | kind, threshold) per noise location.  The layout is mirrored
 by ``csrc/gs_kernels.cu`` and by the CPU frame model in tests.
 """
 
@@ -300,6 +303,10 @@ class DeviceProgram:
     xz_after: dict = field(default_factory=dict)
     truncated_at: int | None = None
     static_sign_bytes: int = 0
+    noise_off: int = 0       # tables offset of the noise instruction table
+    num_noise: int = 0
+    wordpc_off: int = 0      # tables offset of the per-word insertion pcs
+    num_words: int = 0
 
     @property
     def nbytes(self) -> int:
@@ -361,6 +368,7 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
     truncated = None
     sign_bytes = 2 * ((2 * n + 7) // 8)
     total_static_sign = 0
+    noise_ops: list = []
 
     def lohi(m):
         return m & nmask, (m >> n) & nmask
@@ -515,8 +523,10 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
                 words += [beta, delta, m_lo, m_hi,
                           xis | (span.dots(delta) << 8)]
         off = em.table(words)
-        em.op(OP_NOISE, len(span.vecs), kind, instr,
-              [loc0 | (nloc << 32), qmask, off])
+        # not an op-stream record: the device visits a noise instruction only
+        # if one of its locations fired; it is applied right before the op at
+        # `insert_pc` (the next op emitted)
+        noise_ops.append((len(em.ops), nloc, loc0, qmask, off, instr))
 
     flat = prog.flat()
     for i, ins in enumerate(flat):
@@ -593,6 +603,22 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
     pre_lo, pre_hi, cnt = flush_words()
     em.op(OP_END, len(span.vecs), 0, 0xFFFFFFFF,
           [pre_lo, pre_hi, cnt * sign_bytes])
+    # noise instruction table (4 words each) and, per 32-location word of the
+    # fire bitset, the insertion pc of the instruction owning its first
+    # location (the device scans a word only once execution reaches it)
+    nloc_total = len(em.locs) // 2
+    noise_off = len(em.tables)
+    word_owner = []
+    for rec_ in noise_ops:
+        ipc, nl, l0, qm, off, ins_i = rec_
+        em.tables += [ipc | (nl << 32), l0, qm, off]
+    wordpc_off = len(em.tables)
+    m = 0
+    for w in range((nloc_total + 31) // 32):
+        l = 32 * w
+        while noise_ops[m][2] + noise_ops[m][1] <= l:
+            m += 1
+        em.tables.append(noise_ops[m][0])
     return DeviceProgram(
         num_qubits=n, num_measurements=meas, num_detectors=det_ordinal,
         obs_keys=obs_keys, max_dim=max_k, num_locations=len(em.locs) // 2,
@@ -601,7 +627,9 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         tables=np.array(em.tables if em.tables else [0], dtype=np.uint64),
         locs=np.array(em.locs if em.locs else [0, 0], dtype=np.uint64),
         op_instr=em.op_instr, basis_after=basis_after, xz_after=xz_after,
-        truncated_at=truncated, static_sign_bytes=total_static_sign)
+        truncated_at=truncated, static_sign_bytes=total_static_sign,
+        noise_off=noise_off, num_noise=len(noise_ops), wordpc_off=wordpc_off,
+        num_words=(nloc_total + 31) // 32)
 
 
 def decode_header(w: int):

@@ -53,6 +53,8 @@ constexpr int kEntryBytes = 24;        // SURVEY §8(d) state-touch model
 struct DevProg {
   const u64 *ops, *tables, *locs;
   u32 n, nmeas, max_dim, nobs, rec_words32, nlocs;
+  u32 nnoise, nwords;
+  u64 noise_off, wordpc_off;
 };
 
 struct DevRun {
@@ -216,6 +218,7 @@ struct Rng {
 
 constexpr u32 kLcapMax = 128;
 constexpr u32 kR = kLcapMax / 32;
+constexpr u32 kSparseMin = 128;   // below this a dense sweep is <= 4 rounds
 
 __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y != 0.0; }
 
@@ -289,12 +292,134 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
 
     u64 sig_lo = 0, sig_hi = 0, c = 0, obs = 0, mbytes = 0;
     u32 cnt = 1, kcur = 0, pc = 0;
-    bool lst = lcap >= 1;          // occupancy list valid
+    bool lst = false;              // occupancy list valid
     int status = ST_RUNNING, aux = -1;
-    u32 win_base = 0xFFFFFFFFu;
+    // lazy noise scan state: words [0, scanned) of the fire bitset are in
+    // the ring `win`; locations < cursor are consumed
+    u32 scanned = 0, search_w = 0, cursor = 0, fire_pc = 0xFFFFFFFFu;
+    u32 next_word_pc = P.nwords ? (u32)__ldg(tables + P.wordpc_off) : 0xFFFFFFFFu;
     u64 hnext = __ldg(ops);
 
     while (status == ST_RUNNING) {
+      // ---- noise instructions inserted before this op (only fired ones)
+      if (pc >= next_word_pc || pc == fire_pc) {
+        while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= pc) {
+          // one fire draw per location of word `scanned`, one lane each
+          const u32 l = scanned * 32u + lane;
+          bool fire = false;
+          if (l < P.nlocs) {
+            const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+            fire = rng.m53((u32)lw) < thr;
+          }
+          const u32 bits = __ballot_sync(FULL, fire);
+          if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+          ++scanned;
+        }
+        __syncwarp();
+        next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
+        fire_pc = 0xFFFFFFFFu;
+        for (;;) {
+          // next fired location >= cursor among the scanned words
+          u32 fl_loc = 0xFFFFFFFFu;
+          u32 w = max(search_w, cursor >> 5);
+          for (; w < scanned; ++w) {
+            u32 bits = win[w & (kWinWords - 1)];
+            if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
+            if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+          }
+          search_w = w;
+          if (fl_loc == 0xFFFFFFFFu) break;
+          // owning noise instruction: last m with loc0(m) <= fl_loc
+          u32 lo = 0, hi = P.nnoise;
+          while (hi - lo > 1) {
+            const u32 mid = (lo + hi) >> 1;
+            if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= fl_loc) lo = mid; else hi = mid;
+          }
+          const u64 *nrec = tables + P.noise_off + 4ull * lo;
+          const u64 nw0 = __ldg(nrec);
+          const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+          if (ipc > pc) { fire_pc = ipc; break; }
+          const u32 loc0 = (u32)__ldg(nrec + 1);
+          const u64 qmask = __ldg(nrec + 2);
+          const u64 off = __ldg(nrec + 3);
+          cursor = loc0 + nloc;
+          // build E = OR of fired letters (ref noise.py:68-100)
+          u64 ex = 0, ez = 0;
+          for (u32 i = lane; i < nloc; i += 32) {
+            const u32 l = loc0 + i;
+            if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+            const u64 lw = __ldg(locs + 2ull * l);
+            const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
+                      qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
+            if (nk == NK_DEP1) {
+              int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
+              code = code > 3 ? 3 : code;
+              ex |= (u64)(code != 3) << qa;
+              ez |= (u64)(code != 1) << qa;
+            } else if (nk == NK_DEP2) {
+              int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
+              pick = pick > 15 ? 15 : pick;
+              const int ca = pick & 3, cbq = pick >> 2;
+              if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+              if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+            } else if (nk == NK_XERR) {
+              ex |= 1ull << qa;
+            } else {
+              ez |= 1ull << qa;
+            }
+          }
+          ex = warp_or64(ex);
+          ez = warp_or64(ez);
+          const u64 eall = ex | ez;
+          if (!eall) continue;
+          // compose the action of E letter by letter
+          u64 beta = 0, delt = 0;
+          u32 xi = 0, dm = 0;
+          for (u64 rem = eall; rem; rem &= rem - 1) {
+            const u32 q = __ffsll((long long)rem) - 1;
+            const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
+            const u64 *tb = tables + off + 10ull * slot;
+            const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
+            const u64 xw64 = __ldg(tb + 4);
+            const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
+            const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
+            const u64 zw64 = __ldg(tb + 9);
+            const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
+            const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
+            const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
+            u64 lb, ld; u32 lxi, ldm;
+            if (hx && hz) {
+              lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
+              lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
+            } else if (hx) {
+              lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
+            } else {
+              lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
+            }
+            xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
+            beta ^= lb; delt ^= ld; dm ^= ldm;
+          }
+          // apply: v <- i^xi (-1)^{delta.alpha} v ; alpha ^= beta (ref state.py:88-102)
+          const double2 I = ipow(xi);
+          const double2 php = cmul(I, make_double2(1.0, 0.0));
+          const double2 phm = cmul(I, make_double2(-1.0, 0.0));
+          const u32 dcn = par64(delt & c);
+          if (lst) {
+            for (u32 i = lane; i < cnt; i += 32) {
+              const u32 j = L[i];
+              A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
+            }
+          } else {
+            const u32 nsz = 1u << kcur;
+            for (u32 j = lane; j < nsz; j += 32)
+              A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
+          }
+          __syncwarp();
+          c ^= beta;
+          mbytes += 2ull * kEntryBytes * cnt + 2ull * ((2 * n + 7) / 8);
+        }
+      }
+
       const u64 *op = ops + pc;
       const u64 h = hnext;
       const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
@@ -304,113 +429,6 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
       hnext = __ldg(ops + pc);       // prefetch the next header
       kcur = k;
       const u32 size = 1u << k;
-
-      if (kind == OP_NOISE) {
-        const u64 w1 = __ldg(op + 1);
-        const u32 loc0 = (u32)w1, nloc = (u32)(w1 >> 32);
-        if (loc0 < win_base || loc0 + nloc > win_base + 32u * kWinWords) {
-          // rescan the fire window: one fire-draw per location, one lane each
-          win_base = loc0 & ~31u;
-          for (u32 wd = 0; wd < (u32)kWinWords; ++wd) {
-            const u32 l = win_base + wd * 32u + lane;
-            bool fire = false;
-            if (l < P.nlocs) {
-              const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
-              fire = rng.m53((u32)lw) < thr;
-            }
-            const u32 bits = __ballot_sync(FULL, fire);
-            if (lane == 0) win[wd] = bits;
-            if (win_base + wd * 32u + 32u >= P.nlocs) break;
-          }
-          __syncwarp();
-        }
-        const u32 rel0 = loc0 - win_base, rel1 = rel0 + nloc;  // [rel0, rel1)
-        const u32 wfirst = rel0 >> 5, wlast = (rel1 - 1) >> 5;
-        bool any = false;
-        for (u32 wd = wfirst + lane; wd <= wlast; wd += 32) {
-          u32 m = win[wd];
-          if (wd == wfirst) m &= ~0u << (rel0 & 31);
-          if (wd == wlast && (rel1 & 31)) m &= (1u << (rel1 & 31)) - 1u;
-          any |= m != 0;
-        }
-        if (!__any_sync(FULL, any)) continue;
-        // build E = OR of fired letters (ref noise.py:68-100)
-        u64 ex = 0, ez = 0;
-        for (u32 i = lane; i < nloc; i += 32) {
-          const u32 rel = rel0 + i;
-          if (!((win[rel >> 5] >> (rel & 31)) & 1u)) continue;
-          const u64 lw = __ldg(locs + 2ull * (loc0 + i));
-          const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
-                    qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
-          if (nk == NK_DEP1) {
-            int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
-            code = code > 3 ? 3 : code;
-            ex |= (u64)(code != 3) << qa;
-            ez |= (u64)(code != 1) << qa;
-          } else if (nk == NK_DEP2) {
-            int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
-            pick = pick > 15 ? 15 : pick;
-            const int ca = pick & 3, cbq = pick >> 2;
-            if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
-            if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
-          } else if (nk == NK_XERR) {
-            ex |= 1ull << qa;
-          } else {
-            ez |= 1ull << qa;
-          }
-        }
-        ex = warp_or64(ex);
-        ez = warp_or64(ez);
-        const u64 eall = ex | ez;
-        if (!eall) continue;
-        // compose the action of E letter by letter
-        const u64 qmask = __ldg(op + 2);
-        const u64 off = __ldg(op + 3);
-        u64 beta = 0, delt = 0;
-        u32 xi = 0, dm = 0;
-        for (u64 rem = eall; rem; rem &= rem - 1) {
-          const u32 q = __ffsll((long long)rem) - 1;
-          const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
-          const u64 *tb = tables + off + 10ull * slot;
-          const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
-          const u64 xw64 = __ldg(tb + 4);
-          const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
-          const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
-          const u64 zw64 = __ldg(tb + 9);
-          const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
-          const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
-          const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
-          u64 lb, ld; u32 lxi, ldm;
-          if (hx && hz) {
-            lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
-            lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
-          } else if (hx) {
-            lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
-          } else {
-            lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
-          }
-          xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
-          beta ^= lb; delt ^= ld; dm ^= ldm;
-        }
-        // apply: v <- i^xi (-1)^{delta.alpha} v ; alpha ^= beta (ref state.py:88-102)
-        const double2 I = ipow(xi);
-        const double2 php = cmul(I, make_double2(1.0, 0.0));
-        const double2 phm = cmul(I, make_double2(-1.0, 0.0));
-        const u32 dc = par64(delt & c);
-        if (lst) {
-          for (u32 i = lane; i < cnt; i += 32) {
-            const u32 j = L[i];
-            A[j] = cmul(A[j], (dc ^ par32(j & dm)) ? phm : php);
-          }
-        } else {
-          for (u32 j = lane; j < size; j += 32)
-            A[j] = cmul(A[j], (dc ^ par32(j & dm)) ? phm : php);
-        }
-        __syncwarp();
-        c ^= beta;
-        mbytes += 2ull * kEntryBytes * cnt + 2ull * ((2 * n + 7) / 8);
-        continue;
-      }
 
       if (kind == OP_T || kind == OP_GROW_LIMIT) {
         sig_lo ^= __ldg(op + 1);
@@ -459,7 +477,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         }
         const bool grow = tcase == T_GROW;
         u32 ncnt = 0;
-        if (lst && 2 * cnt <= lcap) {
+        if (lst && size >= kSparseMin && 2 * cnt <= lcap) {
           // ---- sparse merge: each listed entry owns its pair unless its
           // partner is a listed lower member (ref state.py:127-129, 294-306)
           const u32 hb = grow ? 0u : 31 - __clz(cb);
@@ -552,8 +570,9 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           }
           __syncwarp();
           ncnt = warp_sum_u32(nz);
-          lst = ncnt <= lcap;
-          if (lst) build_list(A, L, grow ? 2 * size : size, lane);
+          const u32 nsz = grow ? 2 * size : size;
+          lst = ncnt <= lcap && nsz >= kSparseMin;
+          if (lst) build_list(A, L, nsz, lane);
         }
         if (grow) kcur = k + 1;
         cnt = ncnt;
@@ -585,7 +604,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
           double sp = 0.0, sm = 0.0;
-          if (lst) {
+          if (lst && size >= kSparseMin) {
             u32 pj[kR];
             double2 vj[kR];
             bool ng[kR];
@@ -680,7 +699,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               __syncwarp();
             }
             cnt = warp_sum_u32(nz);
-            lst = cnt <= lcap;
+            lst = cnt <= lcap && nsize >= kSparseMin;
             if (lst) build_list(A, L, nsize, lane);
           }
         } else {
@@ -690,7 +709,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const double2 xpm = cmul(I, make_double2(-1.0, 0.0));
           const u32 ct = (u32)(c >> t) & 1u;
           const bool span = mcase == M_PIVOT_SPAN;
-          if (lst) {
+          if (lst && size >= kSparseMin) {
             u32 prep[kR];
             double2 vr[kR], pr[kR];
             bool proc[kR];
@@ -843,7 +862,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               __syncwarp();
             }
             cnt = nz;
-            lst = cnt <= lcap;
+            lst = cnt <= lcap && nsize >= kSparseMin;
             if (lst) build_list(A, L, nsize, lane);
           }
           if (ct) c ^= vec;
@@ -1082,6 +1101,13 @@ int gs_program_create(const gs_program_info *info, const uint64_t *ops, size_t n
     return fail(GS_ERR_ARG, "num_qubits must be in 1..64");
   if (info->max_dim > 30) return fail(GS_ERR_ARG, "max_dim must be <= 30");
   if (info->num_obs > 64) return fail(GS_ERR_ARG, "at most 64 observables");
+  if (info->num_noise && (!tables || info->noise_off + 4ull * info->num_noise > n_tables))
+    return fail(GS_ERR_ARG, "noise table out of range");
+  if (info->num_words && (!tables || info->wordpc_off + info->num_words > n_tables))
+    return fail(GS_ERR_ARG, "word table out of range");
+  if (info->num_words != (info->num_locations + 31) / 32)
+    return fail(GS_ERR_ARG, "num_words must be ceil(num_locations/32)");
+  if (n_locs < 2ull * info->num_locations) return fail(GS_ERR_ARG, "locs too short");
   gs_program *p = new (std::nothrow) gs_program();
   if (!p) return fail(GS_ERR_NOMEM, "out of host memory");
   p->info = *info;
@@ -1253,6 +1279,10 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   P.nobs = p->info.num_obs;
   P.rec_words32 = L.rec_words32;
   P.nlocs = p->info.num_locations;
+  P.nnoise = p->info.num_noise;
+  P.nwords = p->info.num_words;
+  P.noise_off = p->info.noise_off;
+  P.wordpc_off = p->info.wordpc_off;
   gs::DevRun R;
   R.master = r->master_seed;
   R.shot_begin = r->shot_begin;

@@ -28,7 +28,9 @@ class Program:
         lib = _lib.load()
         info = _lib.GsProgramInfo(dp.num_qubits, dp.num_measurements,
                                   dp.num_detectors, len(dp.obs_keys),
-                                  dp.max_dim, dp.num_locations)
+                                  dp.max_dim, dp.num_locations,
+                                  dp.num_noise, dp.num_words, dp.noise_off,
+                                  dp.wordpc_off)
         self._ops = np.ascontiguousarray(dp.ops, dtype=np.uint64)
         self._tables = np.ascontiguousarray(dp.tables, dtype=np.uint64)
         self._locs = np.ascontiguousarray(dp.locs, dtype=np.uint64)

@@ -68,6 +68,11 @@ def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
     n = dp.num_qubits
     nm = (1 << n) - 1
     rng = Draws(mode, master, shot, seed)
+    noise_at = {}
+    for m in range(dp.num_noise):
+        w = tables[dp.noise_off + 4 * m: dp.noise_off + 4 * m + 4]
+        noise_at.setdefault(w[0] & 0xFFFFFFFF, []).append(
+            (w[1], w[0] >> 32, w[2], w[3]))
     sig = 0                                   # bit j = row j
     c = 0
     A = np.zeros(1 << max(dp.max_dim, 0), dtype=np.complex128)
@@ -92,6 +97,10 @@ def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
     while status == RUNNING:
         hdr = ops[pc]
         kind, ln, k, flags, instr = C.decode_header(hdr)
+        for loc0, nloc, qmask, off in noise_at.get(pc, ()):
+            c, cnt_b = _apply_noise(A, 1 << k, rng, locs, tables, n, sig, c,
+                                    loc0, nloc, qmask, off, cnt)
+            model_bytes += cnt_b
         pay = ops[pc + 1: pc + ln]
         pc += ln
         size = 1 << k
@@ -281,64 +290,6 @@ def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
             if (flags & C.MF_RESET) and b_out:
                 sig ^= rst
             continue
-        if kind == C.OP_NOISE:
-            loc0 = pay[0] & 0xFFFFFFFF
-            nloc = pay[0] >> 32
-            qmask = pay[1]
-            off = pay[2]
-            ex = ez = 0
-            for l in range(loc0, loc0 + nloc):
-                w0, thr = locs[2 * l], locs[2 * l + 1]
-                d = w0 & 0xFFFFFFFF
-                qa = (w0 >> 32) & 0xFF
-                qb = (w0 >> 40) & 0xFF
-                nk = (w0 >> 48) & 3
-                if rng.m53(d) >= thr:
-                    continue
-                if nk == C.NK_DEP1:
-                    code = min(1 + int(rng.uniform(d + 1) * 3), 3)
-                    ex |= (code in (1, 2)) << qa
-                    ez |= (code in (2, 3)) << qa
-                elif nk == C.NK_DEP2:
-                    pick = min(1 + int(rng.uniform(d + 1) * 15), 15)
-                    for qq, code in ((qa, pick & 3), (qb, pick >> 2)):
-                        ex |= (code in (1, 2)) << qq
-                        ez |= (code in (2, 3)) << qq
-                elif nk == C.NK_XERR:
-                    ex |= 1 << qa
-                else:
-                    ez |= 1 << qa
-            if not (ex | ez):
-                continue
-            beta = delt = xi = dm = 0
-            for q in C._iter_bits(ex | ez):
-                slot = ((qmask & ((1 << q) - 1))).bit_count()
-                lets = []
-                for li in range(2):
-                    base = off + 10 * slot + 5 * li
-                    lb, ld, mlo, mhi, xd = tables[base: base + 5]
-                    lx = ((xd & 3) + 2 * par(sig & (mlo | (mhi << n)))) & 3
-                    lets.append((lb, ld, lx, xd >> 8))
-                X, Z = lets
-                xb, zb = (ex >> q) & 1, (ez >> q) & 1
-                if xb and zb:
-                    L = (X[0] ^ Z[0], X[1] ^ Z[1],
-                         (1 + X[2] + Z[2] + 2 * par(X[1] & Z[0])) & 3, X[3] ^ Z[3])
-                elif xb:
-                    L = X
-                else:
-                    L = Z
-                xi = (xi + L[2] + 2 * par(delt & L[0])) & 3
-                beta ^= L[0]
-                delt ^= L[1]
-                dm ^= L[3]
-            I = I_POW[xi]
-            dc = par(delt & c)
-            for j in range(size):
-                A[j] = A[j] * (I * (-1.0 if dc ^ par(j & dm) else 1.0))
-            c ^= beta
-            model_bytes += 2 * C.CHI_ENTRY_BYTES * cnt + 2 * ((2 * n + 7) // 8)
-            continue
         if kind == C.OP_FEEDBACK:
             if rec[pay[0]]:
                 sig_xor(pay[1], pay[2])
@@ -370,6 +321,63 @@ def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
         out["c"] = c
         out["A"] = A[: 1 << k_final].copy()
     return out
+
+
+def _apply_noise(A, size, rng, locs, tables, n, sig, c, loc0, nloc, qmask,
+                 off, cnt):
+    """Sample one noise instruction's error and apply it (returns the new
+    coset offset and the model bytes)."""
+    ex = ez = 0
+    for l in range(loc0, loc0 + nloc):
+        w0, thr = locs[2 * l], locs[2 * l + 1]
+        d = w0 & 0xFFFFFFFF
+        qa = (w0 >> 32) & 0xFF
+        qb = (w0 >> 40) & 0xFF
+        nk = (w0 >> 48) & 3
+        if rng.m53(d) >= thr:
+            continue
+        if nk == C.NK_DEP1:
+            code = min(1 + int(rng.uniform(d + 1) * 3), 3)
+            ex |= (code in (1, 2)) << qa
+            ez |= (code in (2, 3)) << qa
+        elif nk == C.NK_DEP2:
+            pick = min(1 + int(rng.uniform(d + 1) * 15), 15)
+            for qq, code in ((qa, pick & 3), (qb, pick >> 2)):
+                ex |= (code in (1, 2)) << qq
+                ez |= (code in (2, 3)) << qq
+        elif nk == C.NK_XERR:
+            ex |= 1 << qa
+        else:
+            ez |= 1 << qa
+    if not (ex | ez):
+        return c, 0
+    beta = delt = xi = dm = 0
+    for q in C._iter_bits(ex | ez):
+        slot = ((qmask & ((1 << q) - 1))).bit_count()
+        lets = []
+        for li in range(2):
+            base = off + 10 * slot + 5 * li
+            lb, ld, mlo, mhi, xd = tables[base: base + 5]
+            lx = ((xd & 3) + 2 * par(sig & (mlo | (mhi << n)))) & 3
+            lets.append((lb, ld, lx, xd >> 8))
+        X, Z = lets
+        xb, zb = (ex >> q) & 1, (ez >> q) & 1
+        if xb and zb:
+            L = (X[0] ^ Z[0], X[1] ^ Z[1],
+                 (1 + X[2] + Z[2] + 2 * par(X[1] & Z[0])) & 3, X[3] ^ Z[3])
+        elif xb:
+            L = X
+        else:
+            L = Z
+        xi = (xi + L[2] + 2 * par(delt & L[0])) & 3
+        beta ^= L[0]
+        delt ^= L[1]
+        dm ^= L[3]
+    I = I_POW[xi]
+    dc = par(delt & c)
+    for j in range(size):
+        A[j] = A[j] * (I * (-1.0 if dc ^ par(j & dm) else 1.0))
+    return c ^ beta, 2 * C.CHI_ENTRY_BYTES * cnt + 2 * ((2 * n + 7) // 8)
 
 
 def as_shot_result(dp, res):

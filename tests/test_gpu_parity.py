@@ -249,7 +249,7 @@ def test_msc_d5_dumps_match_oracle_through_t_layer():
     flat = list(prog.flat())
     t_idx = [i for i, ins in enumerate(flat) if ins.name in ("T", "T_DAG")]
     eng = get_engine(0)
-    for stop in (t_idx[20], t_idx[40], t_idx[59] + 3):
+    for stop in (t_idx[1], t_idx[2], t_idx[3] + 3, t_idx[5]):
         dp = compile_program(prog, stop_after=stop, keep_frames=True)
         p = Program(dp)
         for shot in range(3):
