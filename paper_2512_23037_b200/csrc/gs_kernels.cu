@@ -142,7 +142,7 @@ __device__ __forceinline__ u32 rotl(u32 x, int r) { return __funnelshift_l(x, x,
 
 // derive_seed: first 8 bytes (LE) of SHA-1(LE64 master || LE64 shot)
 // (ref sampler.py:37-42); single 64-byte block.
-__device__ u64 sha1_seed(u64 master, u64 shot) {
+__device__ __noinline__ u64 sha1_seed(u64 master, u64 shot) {
   u32 w[16];
   w[0] = bswap32((u32)master);
   w[1] = bswap32((u32)(master >> 32));
@@ -196,11 +196,15 @@ __device__ __forceinline__ u64 philox_u64(u64 master, u64 shot, u32 k) {
   return (k & 1u) ? (((u64)c3 << 32) | c2) : (((u64)c1 << 32) | c0);
 }
 
+__device__ __noinline__ u64 draw53(u64 seed, u64 master, u64 shot, u32 k, bool philox) {
+  return (philox ? philox_u64(master, shot, k) : splitmix(seed, k)) >> 11;
+}
+
 struct Rng {
   u64 seed, master, shot;
   bool philox;
   __device__ __forceinline__ u64 m53(u32 k) const {
-    return (philox ? philox_u64(master, shot, k) : splitmix(seed, k)) >> 11;
+    return draw53(seed, master, shot, k, philox);
   }
   __device__ __forceinline__ double uniform(u32 k) const {
     return (double)m53(k) * 0x1.0p-53;
@@ -216,9 +220,8 @@ struct Rng {
 // (dense mode).  Invariant: inside [0, 2^k) an entry is nonzero iff it is in
 // the support; positions >= 2^k are don't-care until a GROW initialises them.
 
-constexpr u32 kLcapMax = 128;
-constexpr u32 kR = kLcapMax / 32;
-constexpr u32 kSparseMin = 128;   // below this a dense sweep is <= 4 rounds
+constexpr u32 kLcapMax = 64;    // list storage; sparse ops need cnt <= 32
+constexpr u32 kSparseMin = 64;    // below this a dense sweep is <= 2 rounds
 
 __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y != 0.0; }
 
@@ -264,7 +267,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
   const u64 *__restrict__ tables = P.tables;
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
-  const u32 lcap = O.lcap;
+  const u32 scap = O.lcap < 32u ? O.lcap : 32u;   // sparse ops: <= 1 entry per lane
 
   long long n_tot = 0, n_pres = 0, n_disc = 0, n_ovf = 0, n_cor = 0, n_uns = 0,
             n_err = 0;
@@ -477,68 +480,42 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         }
         const bool grow = tcase == T_GROW;
         u32 ncnt = 0;
-        if (lst && size >= kSparseMin && 2 * cnt <= lcap) {
-          // ---- sparse merge: each listed entry owns its pair unless its
-          // partner is a listed lower member (ref state.py:127-129, 294-306)
-          const u32 hb = grow ? 0u : 31 - __clz(cb);
+        if (lst && cnt <= scap && size >= kSparseMin) {
+          // ---- sparse merge (<= 32 entries, one per lane): each listed
+          // entry owns its pair unless it is the upper member of a pair whose
+          // lower member is listed too (ref state.py:127-129, 294-306)
+          const bool valid = lane < cnt;
           if (grow) {
             for (u32 m = lane; m < size; m += 32) A[size + m] = Z;
             __syncwarp();
           }
-          u32 pj[kR], pp[kR];
-          double2 vj[kR], vp[kR];
-          bool proc[kR];
-#pragma unroll
-          for (u32 r = 0; r < kR; ++r) {
-            const u32 i = lane + 32 * r;
-            proc[r] = false;
-            pj[r] = pp[r] = 0;
-            vj[r] = vp[r] = Z;
-            if (i < cnt) {
-              const u32 j = L[i];
-              pj[r] = j;
-              vj[r] = A[j];
-              if (grow) {
-                pp[r] = j + size;
-                proc[r] = true;
-              } else {
-                const u32 p = j ^ cb;
-                pp[r] = p;
-                vp[r] = A[p];
-                proc[r] = !(((j >> hb) & 1u) && nonzero(vp[r]));
-              }
+          const u32 j = valid ? L[lane] : 0u;
+          const double2 vj = valid ? A[j] : Z;
+          const u32 p = grow ? j + size : (j ^ cb);
+          const double2 vp = (valid && !grow) ? A[p] : Z;
+          const bool proc = valid && (grow || !(((j >> (31 - __clz(cb))) & 1u) && nonzero(vp)));
+          __syncwarp();
+          bool nz0 = false, nz1 = false;
+          if (proc) {
+            const double2 aterm = cadd(Z, cmul(a, vj));
+            const u32 sj = dc ^ par32(j & dmask);
+            double2 n0, n1;
+            if (grow) {
+              n0 = prune(aterm);
+              n1 = prune(cadd(Z, cmul(sj ? bx1 : bx0, vj)));
+            } else {
+              const u32 sp = dc ^ par32(p & dmask);
+              n0 = prune(cadd(aterm, cmul(sp ? bx1 : bx0, vp)));
+              n1 = prune(cadd(cadd(Z, cmul(a, vp)), cmul(sj ? bx1 : bx0, vj)));
             }
+            A[j] = n0;
+            A[p] = n1;
+            nz0 = nonzero(n0);
+            nz1 = nonzero(n1);
           }
           __syncwarp();
-          bool nz0[kR], nz1[kR];
-#pragma unroll
-          for (u32 r = 0; r < kR; ++r) {
-            nz0[r] = nz1[r] = false;
-            if (proc[r]) {
-              const u32 j = pj[r], p = pp[r];
-              const double2 aterm = cadd(Z, cmul(a, vj[r]));
-              const u32 sj = dc ^ par32(j & dmask);
-              double2 n0, n1;
-              if (grow) {
-                n0 = prune(aterm);
-                n1 = prune(cadd(Z, cmul(sj ? bx1 : bx0, vj[r])));
-              } else {
-                const u32 sp = dc ^ par32(p & dmask);
-                n0 = prune(cadd(aterm, cmul(sp ? bx1 : bx0, vp[r])));
-                n1 = prune(cadd(cadd(Z, cmul(a, vp[r])), cmul(sj ? bx1 : bx0, vj[r])));
-              }
-              A[j] = n0;
-              A[p] = n1;
-              nz0[r] = nonzero(n0);
-              nz1[r] = nonzero(n1);
-            }
-          }
-          __syncwarp();
-#pragma unroll
-          for (u32 r = 0; r < kR; ++r) {
-            list_push(L, ncnt, nz0[r], pj[r], lane);
-            list_push(L, ncnt, nz1[r], pp[r], lane);
-          }
+          list_push(L, ncnt, nz0, j, lane);
+          list_push(L, ncnt, nz1, p, lane);
           __syncwarp();
           lst = true;
         } else {
@@ -571,7 +548,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           __syncwarp();
           ncnt = warp_sum_u32(nz);
           const u32 nsz = grow ? 2 * size : size;
-          lst = ncnt <= lcap && nsz >= kSparseMin;
+          lst = ncnt <= scap && nsz >= kSparseMin;
           if (lst) build_list(A, L, nsz, lane);
         }
         if (grow) kcur = k + 1;
@@ -604,56 +581,39 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
           double sp = 0.0, sm = 0.0;
-          if (lst && size >= kSparseMin) {
-            u32 pj[kR];
-            double2 vj[kR];
-            bool ng[kR];
-#pragma unroll
-            for (u32 r = 0; r < kR; ++r) {
-              const u32 i = lane + 32 * r;
-              pj[r] = 0; vj[r] = Z; ng[r] = false;
-              if (i < cnt) {
-                pj[r] = L[i];
-                vj[r] = A[pj[r]];
-                ng[r] = (neg0 ^ par32(pj[r] & dmask)) != 0;
-                const double a2 = abs2(vj[r]);
-                if (ng[r]) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
-              }
+          if (lst && cnt <= scap && size >= kSparseMin) {
+            const bool valid = lane < cnt;
+            const u32 j = valid ? L[lane] : 0u;
+            const double2 v = valid ? A[j] : Z;
+            const bool ng = (neg0 ^ par32(j & dmask)) != 0;
+            const double a2 = abs2(v);
+            if (valid) {
+              if (ng) sm = a2; else sp = a2;
             }
             sp = warp_sum(sp);
             sm = warp_sum(sm);
             plus = u < sp;
             const double chosen = plus ? sp : __dsub_rn(1.0, sp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const bool want_neg = !plus;
+            const bool keep = valid && (ng == !plus);
             const double rs = 1.0 / sqrt(plus ? sp : sm);
+            u32 dst = j;
             if (compact) {
-              const u32 tau = (want_neg ? 1u : 0u) ^ neg0;
+              const u32 tau = (plus ? 0u : 1u) ^ neg0;
               if (tau) c ^= vec;
-#pragma unroll
-              for (u32 r = 0; r < kR; ++r)
-                if (lane + 32 * r < cnt) A[pj[r]] = Z;
+              if (valid) A[j] = Z;
               __syncwarp();
+              dst = ((j >> (isq + 1)) << isq) | (j & ((1u << isq) - 1u));
+              if (keep) A[dst] = cscale(v, rs);
+              kcur = k - 1;
+            } else if (valid) {
+              A[j] = keep ? cscale(v, rs) : Z;
             }
             u32 ncnt = 0;
-#pragma unroll
-            for (u32 r = 0; r < kR; ++r) {
-              const bool valid = lane + 32 * r < cnt;
-              const bool keep = valid && ng[r] == want_neg;
-              u32 dst = pj[r];
-              if (compact) {
-                const u32 low = dst & ((1u << isq) - 1u);
-                dst = ((dst >> (isq + 1)) << isq) | low;
-                if (keep) A[dst] = cscale(vj[r], rs);
-              } else if (valid) {
-                A[dst] = keep ? cscale(vj[r], rs) : Z;
-              }
-              list_push(L, ncnt, keep, dst, lane);
-            }
+            list_push(L, ncnt, keep, dst, lane);
             __syncwarp();
             cnt = ncnt;
-            if (compact) kcur = k - 1;
-          } else {
+        } else {
             for (u32 j = lane; j < size; j += 32) {
               const double a2 = abs2(A[j]);
               if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
@@ -699,7 +659,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               __syncwarp();
             }
             cnt = warp_sum_u32(nz);
-            lst = cnt <= lcap && nsize >= kSparseMin;
+            lst = cnt <= scap && nsize >= kSparseMin;
             if (lst) build_list(A, L, nsize, lane);
           }
         } else {
@@ -709,86 +669,52 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const double2 xpm = cmul(I, make_double2(-1.0, 0.0));
           const u32 ct = (u32)(c >> t) & 1u;
           const bool span = mcase == M_PIVOT_SPAN;
-          if (lst && size >= kSparseMin) {
-            u32 prep[kR];
-            double2 vr[kR], pr[kR];
-            bool proc[kR];
-            double sp = 0.0;
-#pragma unroll
-            for (u32 r = 0; r < kR; ++r) {
-              const u32 i = lane + 32 * r;
-              proc[r] = false; prep[r] = 0; vr[r] = pr[r] = Z;
-              if (i < cnt) {
-                const u32 j = L[i];
-                const bool is_part = (ct ^ par32(j & tmask)) != 0;
-                if (span) {
-                  const u32 other = j ^ cb;
-                  const u32 rep = is_part ? other : j, part = is_part ? j : other;
-                  const double2 v_rep = A[rep], v_part = A[part];
-                  proc[r] = !(is_part && nonzero(v_rep));
-                  prep[r] = rep;
-                  vr[r] = v_rep;
-                  pr[r] = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, v_part);
-                } else {
-                  proc[r] = true;
-                  prep[r] = j;
-                  if (is_part) {
-                    vr[r] = Z;      // representative alpha^beta is absent
-                    pr[r] = cmul((dc ^ par32(j & dmask)) ? xpm : xpp, A[j]);
-                  } else {
-                    vr[r] = A[j];
-                    pr[r] = Z;
-                  }
-                }
-                if (proc[r]) sp = __dadd_rn(sp, abs2(cadd(vr[r], pr[r])));
+          if (lst && cnt <= scap && size >= kSparseMin) {
+            const bool valid = lane < cnt;
+            const u32 j = valid ? L[lane] : 0u;
+            const bool is_part = (ct ^ par32(j & tmask)) != 0;
+            u32 rep = j;
+            double2 vr = Z, pr = Z;
+            bool proc = valid;
+            if (valid) {
+              if (span) {
+                const u32 other = j ^ cb;
+                rep = is_part ? other : j;
+                const u32 part = is_part ? j : other;
+                vr = A[rep];
+                proc = !(is_part && nonzero(vr));
+                pr = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
+              } else if (is_part) {
+                pr = cmul((dc ^ par32(j & dmask)) ? xpm : xpp, A[j]);  // rep absent
+              } else {
+                vr = A[j];
               }
             }
-            sp = warp_sum(sp);
+            const double sp = warp_sum(proc ? abs2(cadd(vr, pr)) : 0.0);
             const double pp = __dmul_rn(0.5, sp);
             plus = u < pp;
             const double chosen = plus ? pp : __dsub_rn(1.0, pp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-            double sk = 0.0;
-            double2 wv[kR];
-            bool wnz[kR];
-#pragma unroll
-            for (u32 r = 0; r < kR; ++r) {
-              wv[r] = Z; wnz[r] = false;
-              if (proc[r]) {
-                wv[r] = prune(plus ? cadd(vr[r], pr[r]) : csub(vr[r], pr[r]));
-                wnz[r] = nonzero(wv[r]);
-                sk = __dadd_rn(sk, abs2(wv[r]));
-              }
-            }
-            sk = warp_sum(sk);
-            u32 any = 0;
-#pragma unroll
-            for (u32 r = 0; r < kR; ++r) any |= wnz[r];
-            if (!__any_sync(FULL, any)) { status = ST_CORRUPT; aux = (int)instr; break; }
+            double2 w = Z;
+            if (proc) w = prune(plus ? cadd(vr, pr) : csub(vr, pr));
+            const bool wnz = nonzero(w);
+            const double sk = warp_sum(abs2(w));
+            if (!__any_sync(FULL, wnz)) { status = ST_CORRUPT; aux = (int)instr; break; }
             const double rs = 1.0 / sqrt(sk);
+            u32 dst = rep;
             if (span) {
-              // clear both members of every processed pair, then write the
-              // squeezed representatives
-#pragma unroll
-              for (u32 r = 0; r < kR; ++r)
-                if (proc[r]) { A[prep[r]] = Z; A[prep[r] ^ cb] = Z; }
               __syncwarp();
+              if (proc) { A[rep] = Z; A[rep ^ cb] = Z; }
+              __syncwarp();
+              dst = ((rep >> (isq + 1)) << isq) | (rep & ((1u << isq) - 1u));
+              kcur = k - 1;
             }
+            if (proc) A[dst] = wnz ? cscale(w, rs) : Z;
             u32 ncnt = 0;
-#pragma unroll
-            for (u32 r = 0; r < kR; ++r) {
-              u32 dst = prep[r];
-              if (span) {
-                const u32 low = dst & ((1u << isq) - 1u);
-                dst = ((dst >> (isq + 1)) << isq) | low;
-              }
-              if (proc[r]) A[dst] = wnz[r] ? cscale(wv[r], rs) : Z;
-              list_push(L, ncnt, wnz[r], dst, lane);
-            }
+            list_push(L, ncnt, wnz, dst, lane);
             __syncwarp();
             cnt = ncnt;
-            if (span) kcur = k - 1;
-          } else {
+        } else {
             double sp = 0.0;
             const u32 npairs = span ? (size >> 1) : size;
             for (u32 m = lane; m < npairs; m += 32) {
@@ -862,7 +788,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               __syncwarp();
             }
             cnt = nz;
-            lst = cnt <= lcap && nsize >= kSparseMin;
+            lst = cnt <= scap && nsize >= kSparseMin;
             if (lst) build_list(A, L, nsize, lane);
           }
           if (ct) c ^= vec;
