@@ -138,6 +138,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chi-global", action="store_true")
+    ap.add_argument("--chi-smem", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
     ap.add_argument("--dense-only", action="store_true")
     ap.add_argument("--list-cap", type=int, default=0)
@@ -192,6 +193,8 @@ def main():
     flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if args.rng == "philox" else 0)
     if args.chi_global:
         flags |= _lib.GS_CHI_GLOBAL
+    if args.chi_smem:
+        flags |= _lib.GS_CHI_SMEM
     if args.dense_only:
         flags |= _lib.GS_DENSE_ONLY
     S = args.shots_per_step

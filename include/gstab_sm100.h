@@ -49,6 +49,7 @@ extern "C" {
 #define GS_RNG_PHILOX 2u   /* Philox4x32-10 streams (else SHA-1+SplitMix) */
 #define GS_CHI_GLOBAL 4u   /* force chi buffers into global memory (test) */
 #define GS_DENSE_ONLY 8u   /* disable the sparse occupancy list (test)   */
+#define GS_CHI_SMEM 16u    /* force chi buffers into shared memory (test) */
 
 /* per-shot status codes (gs_run_records) */
 #define GS_ST_PRESERVED 1

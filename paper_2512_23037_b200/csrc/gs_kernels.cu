@@ -1129,7 +1129,13 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
   L.rec_in_smem = rec_b <= 2048;
   size_t base = gs::kWinBytes + 4 * gs::kLcapMax + (L.rec_in_smem ? rec_b : 0);
   base = (base + 15) & ~(size_t)15;
-  L.smem_chi = !(r->flags & GS_CHI_GLOBAL) && chi <= 48 * 1024;
+  // chi in shared memory only when it is small: large chi buffers cap the
+  // resident warps per SM, while the global (L1/L2-cached) placement keeps
+  // occupancy register-bound and leaves L1 to the program stream (measured:
+  // d=5 proxy 5.9M vs 5.1M shots/s, profiles/README.md)
+  if (r->flags & GS_CHI_SMEM) L.smem_chi = chi <= 48 * 1024;
+  else if (r->flags & GS_CHI_GLOBAL) L.smem_chi = false;
+  else L.smem_chi = chi <= 4 * 1024;
   L.chi_off = (u32)base;
   L.warp_bytes = (u32)(base + (L.smem_chi ? chi : 0));
   u32 wpb = r->warps_per_block ? r->warps_per_block : 4;

@@ -10,6 +10,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 600 python bench.py --steps 3 --warmup 3 --cpu-seconds 10 > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench rc=$?" >> gpurun_out/bench.err
-for v in "--chi-global" "--dense-only" "--wpb 2" "--rng splitmix"; do
+for v in "--chi-smem" "--dense-only" "--rng splitmix"; do
   timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline $v > "gpurun_out/bench_var_${v// /_}.json" 2>> gpurun_out/bench.err
 done

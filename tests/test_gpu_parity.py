@@ -71,11 +71,13 @@ def test_golden_shot_results_bit_exact(golden_shots):
         assert got == fx["shots"], fx["name"]
 
 
-def test_golden_shot_results_chi_in_global_memory(golden_shots):
+@pytest.mark.parametrize("flag", [_lib.GS_CHI_GLOBAL, _lib.GS_CHI_SMEM,
+                                  _lib.GS_DENSE_ONLY])
+def test_golden_shot_results_storage_variants(golden_shots, flag):
     for fx in golden_shots[::3]:
         prog = parse_circuit(fx["text"])
         got = _gpu_results(prog, fx["master"], len(fx["shots"]), fx["capacity"],
-                           fx["postselect"], flags_extra=_lib.GS_CHI_GLOBAL)
+                           fx["postselect"], flags_extra=flag)
         assert got == fx["shots"], fx["name"]
 
 
@@ -210,7 +212,8 @@ def test_msc_noiseless_is_deterministic(d):
     assert st.preserved_shots == 4096
 
 
-@pytest.mark.parametrize("variant", ["dense_only", "lcap4", "lcap32", "chi_global"])
+@pytest.mark.parametrize("variant", ["dense_only", "lcap4", "lcap32", "chi_global",
+                                     "chi_smem"])
 def test_chi_storage_modes_match_oracle(variant):
     """Sparse occupancy list / dense sweeps / global-memory chi must all give
     the oracle's results (mode switches are exercised with tiny list caps)."""
@@ -220,6 +223,8 @@ def test_chi_storage_modes_match_oracle(variant):
         flags_extra = _lib.GS_DENSE_ONLY
     elif variant == "chi_global":
         flags_extra = _lib.GS_CHI_GLOBAL
+    elif variant == "chi_smem":
+        flags_extra = _lib.GS_CHI_SMEM
     else:
         lcap = int(variant[4:])
     eng = get_engine(0)
