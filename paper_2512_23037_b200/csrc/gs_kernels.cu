@@ -107,6 +107,10 @@ __device__ __forceinline__ double2 prune(double2 v) {
   return abs2(v) > kPrune2 ? v : make_double2(0.0, 0.0);
 }
 __device__ __forceinline__ u32 par64(u64 x) { return __popcll(x) & 1u; }
+// 1/sqrt(sum |v|^2) of ref state.py:311; exactly 1 when the sum is 1
+__device__ __forceinline__ double inv_sqrt_norm(double s) {
+  return s == 1.0 ? 1.0 : 1.0 / sqrt(s);
+}
 __device__ __forceinline__ u32 par32(u32 x) { return __popc(x) & 1u; }
 __device__ __forceinline__ double dbits(u64 w) { return __longlong_as_double((long long)w); }
 // _I_POWERS of ref state.py:28 (signed zeros included)
@@ -497,16 +501,16 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           __syncwarp();
           bool nz0 = false, nz1 = false;
           if (proc) {
-            const double2 aterm = cadd(Z, cmul(a, vj));
+            const double2 aterm = cmul(a, vj);
             const u32 sj = dc ^ par32(j & dmask);
             double2 n0, n1;
             if (grow) {
               n0 = prune(aterm);
-              n1 = prune(cadd(Z, cmul(sj ? bx1 : bx0, vj)));
+              n1 = prune(cmul(sj ? bx1 : bx0, vj));
             } else {
               const u32 sp = dc ^ par32(p & dmask);
               n0 = prune(cadd(aterm, cmul(sp ? bx1 : bx0, vp)));
-              n1 = prune(cadd(cadd(Z, cmul(a, vp)), cmul(sj ? bx1 : bx0, vj)));
+              n1 = prune(cadd(cmul(a, vp), cmul(sj ? bx1 : bx0, vj)));
             }
             A[j] = n0;
             A[p] = n1;
@@ -528,8 +532,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
               const double2 v0 = A[j0], v1 = A[j1];
               const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
-              const double2 n0 = prune(cadd(cadd(Z, cmul(a, v0)), cmul(s1 ? bx1 : bx0, v1)));
-              const double2 n1 = prune(cadd(cadd(Z, cmul(a, v1)), cmul(s0 ? bx1 : bx0, v0)));
+              const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
+              const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
               A[j0] = n0;
               A[j1] = n1;
               nz += nonzero(n0) + nonzero(n1);
@@ -538,8 +542,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             for (u32 j = lane; j < size; j += 32) {
               const double2 v = A[j];
               const u32 s = dc ^ par32(j & dmask);
-              const double2 n0 = prune(cadd(Z, cmul(a, v)));
-              const double2 n1 = prune(cadd(Z, cmul(s ? bx1 : bx0, v)));
+              const double2 n0 = prune(cmul(a, v));
+              const double2 n1 = prune(cmul(s ? bx1 : bx0, v));
               A[j] = n0;
               A[size + j] = n1;
               nz += nonzero(n0) + nonzero(n1);
@@ -573,11 +577,31 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
         mbytes += __ldg(op + 17);
         const u32 dc = par64(delta & c);
-        const double u = rng.uniform(udraw);
+        // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
+        // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
+        auto pick_plus = [&](double pplus) -> bool {
+          if (pplus >= 1.0) return true;
+          if (pplus <= 0.0) return false;
+          return rng.uniform(udraw) < pplus;
+        };
         const u32 cin = cnt;
         const bool compact = (fl & MF_COMPACT) != 0;
         bool plus;
-        if (mcase == M_DET) {
+        if (mcase == M_DET && size == 1u) {
+          // one amplitude: every lane evaluates it, no reductions
+          const u32 neg0 = (xi0 >> 1) ^ dc;
+          const double2 v = A[0];
+          const double a2 = abs2(v);
+          plus = pick_plus(neg0 ? 0.0 : a2);
+          if (plus == (neg0 != 0)) { status = ST_CORRUPT; aux = (int)instr; break; }
+          const double chosen = plus ? a2 : __dsub_rn(1.0, neg0 ? 0.0 : a2);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+          if (a2 != 1.0) {
+            __syncwarp();
+            if (lane == 0) A[0] = cscale(v, 1.0 / sqrt(a2));
+            __syncwarp();
+          }
+        } else if (mcase == M_DET) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
           double sp = 0.0, sm = 0.0;
@@ -592,11 +616,11 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             }
             sp = warp_sum(sp);
             sm = warp_sum(sm);
-            plus = u < sp;
+            plus = pick_plus(sp);
             const double chosen = plus ? sp : __dsub_rn(1.0, sp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
             const bool keep = valid && (ng == !plus);
-            const double rs = 1.0 / sqrt(plus ? sp : sm);
+            const double rs = inv_sqrt_norm(plus ? sp : sm);
             u32 dst = j;
             if (compact) {
               const u32 tau = (plus ? 0u : 1u) ^ neg0;
@@ -621,11 +645,11 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             }
             sp = warp_sum(sp);
             sm = warp_sum(sm);
-            plus = u < sp;
+            plus = pick_plus(sp);
             const double chosen = plus ? sp : __dsub_rn(1.0, sp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
             const u32 want_neg = plus ? 0u : 1u;
-            const double rs = 1.0 / sqrt(plus ? sp : sm);
+            const double rs = inv_sqrt_norm(plus ? sp : sm);
             u32 nz = 0;
             u32 nsize = size;
             if (compact) {
@@ -692,7 +716,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             }
             const double sp = warp_sum(proc ? abs2(cadd(vr, pr)) : 0.0);
             const double pp = __dmul_rn(0.5, sp);
-            plus = u < pp;
+            plus = pick_plus(pp);
             const double chosen = plus ? pp : __dsub_rn(1.0, pp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
             double2 w = Z;
@@ -700,7 +724,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             const bool wnz = nonzero(w);
             const double sk = warp_sum(abs2(w));
             if (!__any_sync(FULL, wnz)) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const double rs = 1.0 / sqrt(sk);
+            const double rs = inv_sqrt_norm(sk);
             u32 dst = rep;
             if (span) {
               __syncwarp();
@@ -732,7 +756,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             }
             sp = warp_sum(sp);
             const double pp = __dmul_rn(0.5, sp);
-            plus = u < pp;
+            plus = pick_plus(pp);
             const double chosen = plus ? pp : __dsub_rn(1.0, pp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
             double sk = 0.0;
@@ -766,7 +790,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             sk = warp_sum(sk);
             nz = warp_sum_u32(nz);
             if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const double rs = 1.0 / sqrt(sk);
+            const double rs = inv_sqrt_norm(sk);
             u32 nsize = size;
             if (span) {
               const u32 half = size >> 1;
