@@ -1188,6 +1188,11 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
   u64 blocks = r->blocks ? r->blocks : (u64)e->num_sms * per_sm;
   const u64 need = (r->shot_count + wpb - 1) / wpb;
   if (blocks > need) blocks = need ? need : 1;
+  // bound the global chi scratch (large-k programs run fewer resident shots)
+  if (!L.smem_chi) {
+    const u64 max_warps = ((u64)8 << 30) / chi;
+    if (blocks * wpb > max_warps) blocks = max_warps / wpb ? max_warps / wpb : 1;
+  }
   L.blocks = (u32)blocks;
   const u64 warps = (u64)L.blocks * wpb;
   if (!L.smem_chi) {

@@ -33,7 +33,7 @@ def _gpu_shard_counters(prog, cfg: SamplerConfig, begin: int, count: int):
     """Run one rank's shard on its GPU; counters stay on the device."""
     import torch
     from .engine import Engine, get_engine
-    p = _program_for(prog, cfg.max_dim)
+    p = _program_for(prog, cfg.dim_limit)
     dev = torch.cuda.current_device()
     eng = get_engine(dev)
     counters = torch.zeros(p.num_counters, dtype=torch.int64, device="cuda")

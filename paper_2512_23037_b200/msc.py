@@ -106,7 +106,7 @@ class _Builder:
 
 
 def msc_circuit(d: int = 5, *, checks: int | None = None, flags: int | None = None,
-                final_observable: bool = True):
+                final_observable: bool = True, rounds_after_injection: int = 1):
     """Noiseless MSC-like cultivation proxy of distance ``d`` (3 or 5).
 
     Defaults: d=3 -> 1 full check + final half-check on 15 qubits
@@ -238,8 +238,9 @@ def msc_circuit(d: int = 5, *, checks: int | None = None, flags: int | None = No
     im = b.measure("MR", [inj])
     b.tick()
     b.op("DETECTOR " + b.rec(im[0]))
-    z_round(detect=True)
-    x_round(detect=True)
+    for _ in range(rounds_after_injection):
+        z_round(detect=True)
+        x_round(detect=True)
     # --- cultivation checks
     for _ in range(checks):
         t_layer(undo=False)
@@ -255,7 +256,7 @@ def msc_circuit(d: int = 5, *, checks: int | None = None, flags: int | None = No
 
 
 def random_clifford_t(n: int, gates: int, t_count: int, mid_measurements: int,
-                      seed: int, *, tick: bool = True):
+                      seed: int, *, tick: bool = True, plus_start: bool = False):
     """Random Clifford+T circuit (BASELINE configs 1 and 4): ``gates``
     Cliffords from {H,S,S_DAG,X,Y,Z,H_XY,H_NXY,CX,CZ,SWAP}, ``t_count``
     T/T_DAG and ``mid_measurements`` M at random positions, TICK after each
@@ -277,7 +278,7 @@ def random_clifford_t(n: int, gates: int, t_count: int, mid_measurements: int,
     for _ in range(mid_measurements):
         ops.insert(rng.randrange(len(ops) // 2, len(ops) + 1),
                    "M %d" % rng.randrange(n))
-    lines = []
+    lines = ["H " + " ".join(str(q) for q in range(n)), "TICK"] if plus_start else []
     for o in ops:
         lines.append(o)
         if tick:
@@ -287,3 +288,23 @@ def random_clifford_t(n: int, gates: int, t_count: int, mid_measurements: int,
         lines.append("DETECTOR rec[-%d]" % (n + mid_measurements))
     lines.append("OBSERVABLE_INCLUDE(0) rec[-1]")
     return parse_circuit("\n".join(lines) + "\n")
+
+
+def injection_circuit(d: int = 3, rounds: int = 3):
+    """BASELINE config 3: color-code T-state injection followed by ``rounds``
+    Z+X syndrome rounds with detectors and a final T-check whose X^n parity
+    is the observable (post-selection on every detector)."""
+    return msc_circuit(d, checks=0, flags=0, rounds_after_injection=rounds)
+
+
+def config1_circuit(seed: int = 1):
+    """BASELINE config 1: random Clifford+T on 8 qubits, 40 Cliffords, 4 T,
+    2 mid-circuit M (noise is added with apply_noise_model(p=1e-3))."""
+    return random_clifford_t(8, 40, 4, 2, seed)
+
+
+def config4_circuit(n: int, t_count: int, seed: int = 0):
+    """BASELINE config 4: chi-growth stress, random Clifford+T with n qubits
+    and ``t_count`` T gates, 3n Cliffords and n//8 mid-circuit M."""
+    return random_clifford_t(n, 3 * n, t_count, max(1, n // 8), seed,
+                             plus_start=True)

@@ -88,7 +88,7 @@ class SamplerConfig:
     max_capacity_doublings: int = 3
     rng: str = "splitmix"
     device: int = 0
-    max_dim: int = 20
+    max_dim: int | None = None   # chi dimension limit (auto from capacity)
 
     def __post_init__(self):
         if self.shots < 0:
@@ -101,6 +101,15 @@ class SamplerConfig:
             raise ValueError("threads must be >= 1")
         if self.rng not in ("splitmix", "philox"):
             raise ValueError("rng must be 'splitmix' or 'philox'")
+
+    @property
+    def dim_limit(self) -> int:
+        """Largest chi dimension the device buffers hold: a shot whose
+        support needs more coordinates than 2^limit while staying within the
+        entry capacity reports UNSUPPORTED (never silently wrong)."""
+        if self.max_dim is not None:
+            return self.max_dim
+        return min(24, max(1, (self.effective_capacity - 1).bit_length() + 2))
 
     @property
     def effective_capacity(self) -> int:
@@ -226,7 +235,7 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     """Counters of shots [shot_begin, shot_begin + cfg.shots) (global shot
     indices, so shards of one run combine exactly)."""
     t0 = time.perf_counter()
-    p = _program_for(prog, cfg.max_dim)
+    p = _program_for(prog, cfg.dim_limit)
     eng = engine or get_engine(cfg.device)
     total = np.zeros(p.num_counters, dtype=np.int64)
     dev_s = 0.0
@@ -282,7 +291,7 @@ class ShotBatch:
 def sample(prog, cfg: SamplerConfig, *, shot_begin: int = 0, seeds=None,
            engine: Engine | None = None) -> ShotBatch:
     """Per-shot statuses, measurement records and observables."""
-    p = _program_for(prog, cfg.max_dim)
+    p = _program_for(prog, cfg.dim_limit)
     eng = engine or get_engine(cfg.device)
     par = Engine.params(cfg.master_seed, shot_begin, cfg.shots,
                         cfg.effective_capacity, cfg.run_flags(), seeds=seeds)

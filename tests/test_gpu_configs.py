@@ -1,0 +1,101 @@
+"""GPU parity at BASELINE sizes: config 1 (all 1e5 shots bit-exact against
+reference-generated records), config 4 chi-growth stress with capacity tiers
+(overflow statuses bit-exact vs the oracle), and statistical parity of
+discard / logical-error rates on the d=3 and d=5 MSC proxies
+(Philox GPU stream vs SplitMix oracle stream, binomial CIs)."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import gstab_oracle as orc
+from paper_2512_23037_b200 import SamplerConfig, parse_circuit, run_batch, sample
+from paper_2512_23037_b200.msc import config4_circuit, msc_circuit, injection_circuit
+from paper_2512_23037_b200.noise import apply_noise_model
+from paper_2512_23037_b200.sampler import _records_before
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "config1_records.npz")
+
+
+def test_config1_all_1e5_shots_bit_exact():
+    g = np.load(GOLDEN)
+    prog = parse_circuit(str(g["text"]))
+    shots = len(g["status"])
+    assert shots == 100_000
+    b = sample(prog, SamplerConfig(shots=shots, master_seed=int(g["master"]),
+                                   postselect=True))
+    assert np.array_equal(b.status, g["status"])
+    m = int(g["num_measurements"])
+    want = np.unpackbits(g["records"], axis=1, bitorder="little")[:, :m]
+    assert np.array_equal(b.record_bits(), want)
+
+
+@pytest.mark.parametrize("n,t", [(20, 8), (24, 16), (32, 24), (64, 32)])
+@pytest.mark.parametrize("cap,rerun", [(64, False), (256, True), (4096, True)])
+def test_config4_overflow_parity(n, t, cap, rerun):
+    prog = apply_noise_model(config4_circuit(n, t, seed=n + t), 2e-3)
+    cfg = SamplerConfig(shots=6, master_seed=n * t, entry_capacity=cap,
+                        rerun_on_overflow=rerun, postselect=False)
+    b = sample(prog, cfg)
+    flat = list(prog.flat())
+    for s in range(6):
+        ref = orc.run_shot_with_reruns(flat, prog.num_qubits, "splitmix",
+                                       cfg.master_seed, s, cap, 3, rerun, False)
+        got = b.result(s, measured=_records_before(prog, b, s))
+        assert got.status.value == ref["status"], (n, t, cap, s)
+        assert got.overflow_instruction == ref["overflow_instruction"]
+        assert got.record == ref["record"]
+
+
+def _z(k1, n1, k2, n2):
+    p = (k1 + k2) / (n1 + n2)
+    se = math.sqrt(max(p * (1 - p), 1e-12) * (1 / n1 + 1 / n2))
+    return abs(k1 / n1 - k2 / n2) / se
+
+
+@pytest.mark.parametrize("d,cpu_shots", [(3, 4000), (5, 800)])
+def test_msc_statistics_match_oracle(d, cpu_shots):
+    prog = apply_noise_model(msc_circuit(d), 1e-3)
+    gpu = run_batch(prog, SamplerConfig(shots=1 << 20, master_seed=3,
+                                        postselect=True, rng="philox"))
+    cpu = orc.run_counters_parallel(prog, cpu_shots, os.cpu_count() or 1,
+                                    master_seed=11, mode="splitmix",
+                                    postselect=True)
+    assert _z(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
+              cpu["total"]) < 4.5
+    assert _z(gpu.logical_error_shots, gpu.preserved_shots,
+              cpu["error_shots"], max(cpu["preserved"], 1)) < 4.5
+
+
+def test_config3_injection_rounds_statistics():
+    prog = apply_noise_model(injection_circuit(3, 3), 5e-4)
+    gpu = run_batch(prog, SamplerConfig(shots=1 << 20, master_seed=5,
+                                        postselect=True, rng="philox"))
+    cpu = orc.run_counters_parallel(prog, 3000, os.cpu_count() or 1,
+                                    master_seed=2, mode="splitmix", postselect=True)
+    assert _z(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
+              cpu["total"]) < 4.5
+
+
+def test_d5_full_size_properties():
+    """1e7 shots of the d=5 workload: conservation, no corrupt/unsupported
+    shots, and identical counters from two different launch shapes."""
+    prog = apply_noise_model(msc_circuit(5), 1e-3)
+    a = run_batch(prog, SamplerConfig(shots=10**7, master_seed=9,
+                                      postselect=True, rng="philox"))
+    assert a.preserved_shots + a.discarded_shots + a.overflow_count == a.total_shots
+    assert a.overflow_count == 0
+    from paper_2512_23037_b200 import _lib
+    from paper_2512_23037_b200.engine import Engine, get_engine
+    from paper_2512_23037_b200.sampler import _program_for
+    cfg = SamplerConfig(shots=10**7, master_seed=9, postselect=True, rng="philox")
+    p = _program_for(prog, cfg.dim_limit)
+    c = get_engine(0).run_counters(p, Engine.params(
+        9, 0, 10**7, cfg.effective_capacity, cfg.run_flags(),
+        warps_per_block=2, blocks=300))
+    assert int(c[_lib.GS_C_PRESERVED]) == a.preserved_shots
+    assert int(c[_lib.GS_C_ERROR_SHOTS]) == a.logical_error_shots

@@ -63,3 +63,23 @@ def test_oracle_counters(golden_counters):
             assert got[k] == fx["counters"][k], k
         assert {str(k): v for k, v in got["per_observable"].items()} == \
             fx["counters"]["per_observable"]
+
+
+def test_oracle_config1_golden_prefix():
+    """The oracle reproduces the reference's config-1 records (first 1500 of
+    the 1e5 golden shots; the GPU test checks all of them)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden",
+                             "config1_records.npz"))
+    prog = parse_circuit(str(g["text"]))
+    flat = list(prog.flat())
+    m = int(g["num_measurements"])
+    want = np.unpackbits(g["records"][:1500], axis=1, bitorder="little")[:, :m]
+    code = {"preserved": 1, "discarded": 2, "overflow": 3}
+    for s in range(1500):
+        r = orc.run_one_shot(flat, prog.num_qubits,
+                             orc.DrawStream("splitmix", int(g["master"]), s), 4096, True)
+        assert code[r["status"]] == g["status"][s]
+        rec = np.zeros(m, dtype=np.uint8)
+        rec[:len(r["record"])] = r["record"]
+        assert np.array_equal(rec, want[s]), s
