@@ -109,7 +109,7 @@ class SamplerConfig:
         entry capacity reports UNSUPPORTED (never silently wrong)."""
         if self.max_dim is not None:
             return self.max_dim
-        return min(24, max(1, (self.effective_capacity - 1).bit_length() + 2))
+        return min(24, max(1, (self.effective_capacity - 1).bit_length() + 5))
 
     @property
     def effective_capacity(self) -> int:
