@@ -34,9 +34,10 @@ def anticommute_mask_batch(xs, zs, qx, qz, device: int = 0):
     zs = np.atleast_2d(_u64(zs))
     b, rows = xs.shape
     out = np.zeros((b, 2), dtype=np.uint64)
+    qx, qz = _u64(qx), _u64(qz)          # keep the buffers alive across the call
     _lib.check(_lib.load().gs_anticommute_mask(
         get_engine(device).handle, xs.ctypes.data, zs.ctypes.data, rows, b,
-        _u64(qx).ctypes.data, _u64(qz).ctypes.data, out.ctypes.data))
+        qx.ctypes.data, qz.ctypes.data, out.ctypes.data))
     return [int(lo) | (int(hi) << 64) for lo, hi in out]
 
 
@@ -52,11 +53,12 @@ def anticommute_mask(xs, zs, qx: int, qz: int) -> int:
 def conj_gate_rows_batch(xs, zs, ph, code, m1, m2, device: int = 0):
     """In-place batched Clifford conjugation; arrays shaped (batch, rows)."""
     b, rows = xs.shape
+    code = np.ascontiguousarray(code, dtype=np.uint32)
+    m1, m2 = _u64(m1), _u64(m2)
     _lib.check(_lib.load().gs_conj_gate_rows(
         get_engine(device).handle, xs.ctypes.data, zs.ctypes.data,
-        ph.ctypes.data, rows, b,
-        np.ascontiguousarray(code, dtype=np.uint32).ctypes.data,
-        _u64(m1).ctypes.data, _u64(m2).ctypes.data))
+        ph.ctypes.data, rows, b, code.ctypes.data, m1.ctypes.data,
+        m2.ctypes.data))
 
 
 def conj_gate_rows(xs, zs, ph, code: int, m1: int, m2: int) -> None:
@@ -72,12 +74,13 @@ def conj_gate_rows(xs, zs, ph, code: int, m1: int, m2: int) -> None:
 
 def mul_rows_batch(xs, zs, ph, sel, px, pz, pe, device: int = 0):
     b, rows = xs.shape
+    sel = np.ascontiguousarray(sel, dtype=np.uint8)
+    px, pz = _u64(px), _u64(pz)
+    pe = np.ascontiguousarray(pe, dtype=np.uint32)
     _lib.check(_lib.load().gs_mul_rows(
         get_engine(device).handle, xs.ctypes.data, zs.ctypes.data,
-        ph.ctypes.data, rows, b,
-        np.ascontiguousarray(sel, dtype=np.uint8).ctypes.data,
-        _u64(px).ctypes.data, _u64(pz).ctypes.data,
-        np.ascontiguousarray(pe, dtype=np.uint32).ctypes.data))
+        ph.ctypes.data, rows, b, sel.ctypes.data, px.ctypes.data,
+        pz.ctypes.data, pe.ctypes.data))
 
 
 def mul_rows(xs, zs, ph, sel, px: int, pz: int, pe: int) -> None:
