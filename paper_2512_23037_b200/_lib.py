@@ -68,7 +68,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("GSTAB_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise EngineUnavailable(
             "%s not built; run __graft_entry__.build() (nvcc sm_100a)" % p)
