@@ -252,7 +252,7 @@ __device__ void build_list(const double2 *A, u32 *L, u32 size, u32 lane) {
 // ---------------------------------------------------------------- kernel
 
 #ifndef GS_MIN_BLOCKS
-#define GS_MIN_BLOCKS 1
+#define GS_MIN_BLOCKS 4   // 128 registers: 16 resident warps/SM (measured best)
 #endif
 
 template <bool kSmemChi>
@@ -532,27 +532,15 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           if (!grow) {
             const u32 hb = 31 - __clz(cb);
             const u32 half = size >> 1;
-            // two pairs per lane per round: four independent loads in flight
-            for (u32 m = lane; m < half; m += 64) {
-              const bool two = m + 32 < half;
+            for (u32 m = lane; m < half; m += 32) {
               const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
-              const u32 k0 = two ? ins_bit(m + 32, hb, 0) : j0, k1 = k0 ^ cb;
               const double2 v0 = A[j0], v1 = A[j1];
-              const double2 w0 = A[k0], w1 = A[k1];
               const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
-              const u32 t0 = dc ^ par32(k0 & dmask), t1 = dc ^ par32(k1 & dmask);
               const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
               const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
-              const double2 o0 = prune(cadd(cmul(a, w0), cmul(t1 ? bx1 : bx0, w1)));
-              const double2 o1 = prune(cadd(cmul(a, w1), cmul(t0 ? bx1 : bx0, w0)));
               A[j0] = n0;
               A[j1] = n1;
               nz += nonzero(n0) + nonzero(n1);
-              if (two) {
-                A[k0] = o0;
-                A[k1] = o1;
-                nz += nonzero(o0) + nonzero(o1);
-              }
             }
           } else {
             for (u32 j = lane; j < size; j += 32) {
