@@ -132,6 +132,16 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
   return v;
 }
+// Sum over lanes when only lanes < live can be nonzero: the butterfly levels
+// above live only add exact zeros, so this is bit-identical to warp_sum with
+// log2(live) shuffle levels instead of 5 (most measurements see 1-4 lanes).
+__device__ __forceinline__ double warp_sum_live(double v, u32 live) {
+  if (live >= 32u) return warp_sum(v);
+  if (live <= 1u) return __shfl_sync(FULL, v, 0);
+  for (u32 o = 1u << (31 - __clz(live - 1)); o > 0; o >>= 1)
+    v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+  return __shfl_sync(FULL, v, 0);
+}
 __device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(FULL, v); }
 __device__ __forceinline__ u64 warp_or64(u64 v) {
   u32 lo = __reduce_or_sync(FULL, (u32)v);
@@ -618,8 +628,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             if (valid) {
               if (ng) sm = a2; else sp = a2;
             }
-            sp = warp_sum(sp);
-            sm = warp_sum(sm);
+            sp = warp_sum_live(sp, cnt);
+            sm = warp_sum_live(sm, cnt);
             plus = pick_plus(sp);
             const double chosen = plus ? sp : __dsub_rn(1.0, sp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
@@ -647,8 +657,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
               else sp = __dadd_rn(sp, a2);
             }
-            sp = warp_sum(sp);
-            sm = warp_sum(sm);
+            sp = warp_sum_live(sp, size);
+            sm = warp_sum_live(sm, size);
             plus = pick_plus(sp);
             const double chosen = plus ? sp : __dsub_rn(1.0, sp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
@@ -718,7 +728,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
                 vr = A[j];
               }
             }
-            const double sp = warp_sum(proc ? abs2(cadd(vr, pr)) : 0.0);
+            const double sp = warp_sum_live(proc ? abs2(cadd(vr, pr)) : 0.0, cnt);
             const double pp = __dmul_rn(0.5, sp);
             plus = pick_plus(pp);
             const double chosen = plus ? pp : __dsub_rn(1.0, pp);
@@ -726,7 +736,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             double2 w = Z;
             if (proc) w = prune(plus ? cadd(vr, pr) : csub(vr, pr));
             const bool wnz = nonzero(w);
-            const double sk = warp_sum(abs2(w));
+            const double sk = warp_sum_live(abs2(w), cnt);
             if (!__any_sync(FULL, wnz)) { status = ST_CORRUPT; aux = (int)instr; break; }
             const double rs = inv_sqrt_norm(sk);
             u32 dst = rep;
@@ -758,7 +768,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               }
               sp = __dadd_rn(sp, abs2(wpv));
             }
-            sp = warp_sum(sp);
+            sp = warp_sum_live(sp, npairs);
             const double pp = __dmul_rn(0.5, sp);
             plus = pick_plus(pp);
             const double chosen = plus ? pp : __dsub_rn(1.0, pp);
@@ -791,7 +801,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               nz += nonzero(w);
             }
             __syncwarp();
-            sk = warp_sum(sk);
+            sk = warp_sum_live(sk, npairs);
             nz = warp_sum_u32(nz);
             if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
             const double rs = inv_sqrt_norm(sk);
