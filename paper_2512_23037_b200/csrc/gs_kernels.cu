@@ -136,6 +136,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 // above live only add exact zeros, so this is bit-identical to warp_sum with
 // log2(live) shuffle levels instead of 5 (most measurements see 1-4 lanes).
 __device__ __forceinline__ double warp_sum_live(double v, u32 live) {
+#ifdef GS_FULL_SUMS
+  return warp_sum(v);
+#endif
   if (live >= 32u) return warp_sum(v);
   if (live <= 1u) return __shfl_sync(FULL, v, 0);
   for (u32 o = 1u << (31 - __clz(live - 1)); o > 0; o >>= 1)
