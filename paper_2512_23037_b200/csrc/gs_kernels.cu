@@ -132,18 +132,13 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
   return v;
 }
-// Sum over lanes when only lanes < live can be nonzero: the butterfly levels
-// above live only add exact zeros, so this is bit-identical to warp_sum with
-// log2(live) shuffle levels instead of 5 (most measurements see 1-4 lanes).
+// Sum over lanes where only lanes < live can be nonzero.  A shortened
+// log2(live)-level tree would be bit-identical, but measured slower than the
+// branch-free 5-level tree (A/B on one B200: 5.70M vs 6.35M shots/s, d=5), so
+// the full tree is used.
 __device__ __forceinline__ double warp_sum_live(double v, u32 live) {
-#ifdef GS_FULL_SUMS
+  (void)live;
   return warp_sum(v);
-#endif
-  if (live >= 32u) return warp_sum(v);
-  if (live <= 1u) return __shfl_sync(FULL, v, 0);
-  for (u32 o = 1u << (31 - __clz(live - 1)); o > 0; o >>= 1)
-    v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
-  return __shfl_sync(FULL, v, 0);
 }
 __device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(FULL, v); }
 __device__ __forceinline__ u64 warp_or64(u64 v) {
