@@ -184,12 +184,17 @@ def main():
     from paper_2512_23037_b200.compiler import compile_program
     from paper_2512_23037_b200.engine import Engine, Program
 
-    torch.cuda.set_device(local)
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GS_DIST_BACKEND", "nccl")   # gloo: CI on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     dp = compile_program(prog)
     P = Program(dp)
-    eng = Engine(local)
+    eng = Engine(dev)
     flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if args.rng == "philox" else 0)
     if args.chi_global:
         flags |= _lib.GS_CHI_GLOBAL
@@ -215,7 +220,7 @@ def main():
     counters.zero_()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     clocks.start()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
