@@ -39,3 +39,29 @@ def test_frame_model_states(golden_states):
             assert st["idx"] == snap["idx"], (fx["text"], snap["i"])
             np.testing.assert_allclose(np.array(st["amp"]), np.array(snap["amp"]),
                                        rtol=0, atol=1e-12)
+
+
+def test_frame_model_random_programs_vs_oracle():
+    """Compiler check on programs with MPP flips, R/MR, SWAP-controlled
+    feedback, repeated noise targets, both RNG modes and tiny capacities."""
+    import random
+    from oracle import gstab_oracle as orc
+    from tests_helpers import random_program
+    rng = random.Random(11)
+    for it in range(40):
+        prog = random_program(rng)
+        flat = list(prog.flat())
+        dp = C.compile_program(prog)
+        mode = "philox" if it % 2 else "splitmix"
+        cap = rng.choice((2, 8, 4096))
+        for shot in range(4):
+            post = shot % 2 == 0
+            ref = orc.run_one_shot(flat, prog.num_qubits,
+                                   orc.DrawStream(mode, 5, shot), cap, post)
+            got = FM.as_shot_result(dp, FM.run_shot(dp, mode, 5, shot, cap, post))
+            want = {"status": ref["status"],
+                    "observables": {str(k): v for k, v in sorted(ref["observables"].items())},
+                    "discarded_detector": ref["discarded_detector"],
+                    "overflow_instruction": ref["overflow_instruction"],
+                    "record": ref["record"]}
+            assert got == want, (it, shot, prog.serialize())
