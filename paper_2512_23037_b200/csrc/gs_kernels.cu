@@ -259,6 +259,9 @@ __device__ void build_list(const double2 *A, u32 *L, u32 size, u32 lane) {
 
 // ---------------------------------------------------------------- kernel
 
+#ifndef GS_SMALL_MAX
+#define GS_SMALL_MAX 4u   // chi sizes handled by the redundant per-lane path
+#endif
 #ifndef GS_MIN_BLOCKS
 #define GS_MIN_BLOCKS 4   // 128 registers: 16 resident warps/SM (measured best)
 #endif
@@ -599,20 +602,47 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u32 cin = cnt;
         const bool compact = (fl & MF_COMPACT) != 0;
         bool plus;
-        if (mcase == M_DET && size == 1u) {
-          // one amplitude: every lane evaluates it, no reductions
+        if (mcase == M_DET && size <= GS_SMALL_MAX) {
+          // <= 4 amplitudes: every lane evaluates the whole measurement from
+          // broadcast loads -- no cross-lane reductions (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
-          const double2 v = A[0];
-          const double a2 = abs2(v);
-          plus = pick_plus(neg0 ? 0.0 : a2);
-          if (plus == (neg0 != 0)) { status = ST_CORRUPT; aux = (int)instr; break; }
-          const double chosen = plus ? a2 : __dsub_rn(1.0, neg0 ? 0.0 : a2);
-          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-          if (a2 != 1.0) {
-            __syncwarp();
-            if (lane == 0) A[0] = cscale(v, 1.0 / sqrt(a2));
-            __syncwarp();
+          double2 v[4];
+          double sp = 0.0, sm = 0.0;
+#pragma unroll
+          for (u32 e = 0; e < 4; ++e) {
+            v[e] = e < size ? A[e] : Z;
+            if (e < size) {
+              const double a2 = abs2(v[e]);
+              if (neg0 ^ par32(e & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+            }
           }
+          plus = pick_plus(sp);
+          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+          const u32 want_neg = plus ? 0u : 1u;
+          u32 nk = 0;
+#pragma unroll
+          for (u32 e = 0; e < 4; ++e)
+            nk += (e < size) && ((neg0 ^ par32(e & dmask)) == want_neg) && nonzero(v[e]);
+          if (nk == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+          const double rs = inv_sqrt_norm(plus ? sp : sm);
+          __syncwarp();
+          if (compact) {
+            const u32 tau = want_neg ^ neg0;
+            if (tau) c ^= vec;
+            if (lane < (size >> 1)) {
+              const u32 j0 = ins_bit(lane, isq, 0);
+              const u32 src = j0 | ((tau ^ par32(j0 & dmask)) << isq);
+              const double2 vs = src == 0 ? v[0] : src == 1 ? v[1] : src == 2 ? v[2] : v[3];
+              A[lane] = cscale(vs, rs);
+            }
+            kcur = k - 1;
+          } else if (lane < size) {
+            const double2 vl = lane == 0 ? v[0] : lane == 1 ? v[1] : lane == 2 ? v[2] : v[3];
+            A[lane] = ((neg0 ^ par32(lane & dmask)) == want_neg) ? cscale(vl, rs) : Z;
+          }
+          __syncwarp();
+          cnt = nk;
         } else if (mcase == M_DET) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
@@ -705,7 +735,58 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const double2 xpm = cmul(I, make_double2(-1.0, 0.0));
           const u32 ct = (u32)(c >> t) & 1u;
           const bool span = mcase == M_PIVOT_SPAN;
-          if (lst && cnt <= scap && size >= kSparseMin) {
+          if (size <= GS_SMALL_MAX) {
+            // <= 4 amplitudes: redundant per-lane evaluation, no reductions
+            double2 v[4];
+#pragma unroll
+            for (u32 e = 0; e < 4; ++e) v[e] = e < size ? A[e] : Z;
+            const u32 npairs = span ? (size >> 1) : size;
+            // w(m, sign) for pair / entry m: rep + sign * xi_part * part
+            auto pair_w = [&](u32 m, bool plus_branch) -> double2 {
+              if (span) {
+                const u32 j0 = ins_bit(m, isq, 0);
+                const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+                const u32 part = rep ^ cb;
+                const double2 vr = rep == 0 ? v[0] : rep == 1 ? v[1] : rep == 2 ? v[2] : v[3];
+                const double2 vp = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
+                const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, vp);
+                return plus_branch ? cadd(vr, prod) : csub(vr, prod);
+              }
+              const double2 vm = m == 0 ? v[0] : m == 1 ? v[1] : m == 2 ? v[2] : v[3];
+              if (ct ^ par32(m & tmask)) {
+                const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, vm);
+                return plus_branch ? cadd(Z, prod) : csub(Z, prod);
+              }
+              return vm;
+            };
+            double sp = 0.0;
+#pragma unroll
+            for (u32 m = 0; m < 4; ++m)
+              if (m < npairs) sp = __dadd_rn(sp, abs2(pair_w(m, true)));
+            const double pp = __dmul_rn(0.5, sp);
+            plus = pick_plus(pp);
+            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+            double sk = 0.0;
+            u32 nz = 0;
+            double2 wp[4];
+#pragma unroll
+            for (u32 m = 0; m < 4; ++m) {
+              wp[m] = m < npairs ? prune(pair_w(m, plus)) : Z;
+              sk = __dadd_rn(sk, abs2(wp[m]));
+              nz += nonzero(wp[m]);
+            }
+            if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+            const double rs = inv_sqrt_norm(sk);
+            __syncwarp();
+            if (lane < npairs) {
+              const double2 wl = lane == 0 ? wp[0] : lane == 1 ? wp[1] : lane == 2 ? wp[2] : wp[3];
+              A[lane] = cscale(wl, rs);
+            }
+            __syncwarp();
+            if (span) kcur = k - 1;
+            cnt = nz;
+          } else if (lst && cnt <= scap && size >= kSparseMin) {
             const bool valid = lane < cnt;
             const u32 j = valid ? L[lane] : 0u;
             const bool is_part = (ct ^ par32(j & tmask)) != 0;
