@@ -406,10 +406,14 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
             kind = OP_GROW_LIMIT
         pre_lo, pre_hi, cnt = flush_words()
         m_lo, m_hi = lohi(msig)
+        # b * i^{xi_s}: multiplying by +-1 / +-i only swaps and negates the
+        # components, so this host constant is exact; the device negates it
+        # when the per-shot sign parity adds 2 to xi0
+        bxs = b * (1.0 + 0.0j, 1.0j, -1.0 + 0.0j, -1.0j)[xis]
         em.op(kind, k, case | (xis << 2), instr,
               [pre_lo, pre_hi, m_lo, m_hi, delta, cb | (dmask << 32),
-               _dbl_bits(a.real), _dbl_bits(a.imag), _dbl_bits(b.real),
-               _dbl_bits(b.imag), (cnt + 1) * sign_bytes])
+               _dbl_bits(a.real), _dbl_bits(a.imag), _dbl_bits(bxs.real),
+               _dbl_bits(bxs.imag), (cnt + 1) * sign_bytes])
         if kind == OP_GROW_LIMIT:
             truncated = instr
             return False

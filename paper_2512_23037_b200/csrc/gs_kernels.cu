@@ -95,6 +95,7 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
 __device__ __forceinline__ double2 csub(double2 a, double2 b) {
   return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
 }
+__device__ __forceinline__ double2 cneg(double2 a) { return make_double2(-a.x, -a.y); }
 __device__ __forceinline__ double2 cscale(double2 a, double r) {
   return make_double2(__dmul_rn(a.x, r), __dmul_rn(a.y, r));
 }
@@ -423,8 +424,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           }
           // apply: v <- i^xi (-1)^{delta.alpha} v ; alpha ^= beta (ref state.py:88-102)
           const double2 I = ipow(xi);
-          const double2 php = cmul(I, make_double2(1.0, 0.0));
-          const double2 phm = cmul(I, make_double2(-1.0, 0.0));
+          const double2 php = I;            // i^xi * (+1), exact
+          const double2 phm = cneg(I);
           const u32 dcn = par64(delt & c);
           if (lst) {
             for (u32 i = lane; i < cnt; i += 32) {
@@ -455,16 +456,17 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
       if (kind == OP_T || kind == OP_GROW_LIMIT) {
         sig_lo ^= __ldg(op + 1);
         sig_hi ^= __ldg(op + 2);
-        const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+        // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
+        // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
+        const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
         const u64 delta = __ldg(op + 5);
         const u64 w6 = __ldg(op + 6);
         const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
         const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
-        const double2 b = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
+        const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
         mbytes += __ldg(op + 11);
-        const double2 I = ipow(xi0);
-        const double2 bx0 = cmul(b, cmul(I, make_double2(1.0, 0.0)));
-        const double2 bx1 = cmul(b, cmul(I, make_double2(-1.0, 0.0)));
+        const double2 bx0 = flip ? cneg(bxs) : bxs;
+        const double2 bx1 = cneg(bx0);
         const u32 dc = par64(delta & c);
         const u32 tcase = fl & 3u;
         if (tcase == T_DIAG) {
@@ -731,8 +733,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         } else {
           // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
           const double2 I = ipow(xi0);
-          const double2 xpp = cmul(I, make_double2(1.0, 0.0));
-          const double2 xpm = cmul(I, make_double2(-1.0, 0.0));
+          const double2 xpp = I;            // i^xi0 * (+1), exact
+          const double2 xpm = cneg(I);
           const u32 ct = (u32)(c >> t) & 1u;
           const bool span = mcase == M_PIVOT_SPAN;
           if (size <= GS_SMALL_MAX) {

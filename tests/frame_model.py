@@ -117,12 +117,12 @@ def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
             cb = pay[5] & 0xFFFFFFFF
             dmask = pay[5] >> 32
             a = complex(_f64(pay[6]), _f64(pay[7]))
-            b = complex(_f64(pay[8]), _f64(pay[9]))
+            bxs = complex(_f64(pay[8]), _f64(pay[9]))     # b * i^{xi_s}
             model_bytes += pay[10]
             case = flags & 3
-            xi0 = ((flags >> 2) + 2 * par(sig & M)) & 3
-            I = I_POW[xi0]
-            bx = (b * I, b * (-I))
+            flip = par(sig & M)
+            bx0 = -bxs if flip else bxs
+            bx = (bx0, -bx0)
             dc = par(delta & c)
 
             def s(j):
