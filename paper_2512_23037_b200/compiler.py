@@ -53,7 +53,6 @@ OP_FEEDBACK = 4
 OP_DETECTOR = 5
 OP_OBSERVABLE = 6
 OP_GROW_LIMIT = 7
-OP_FUSE2 = 8       # marker: the next two T BUTTERFLY ops may run as one pass
 
 # T cases
 T_DIAG, T_BUTTERFLY, T_GROW = 0, 1, 2
@@ -338,37 +337,9 @@ class _Emitter:
         return off
 
 
-def _insert_fuse_markers(em, t_ops) -> None:
-    """Pair consecutive BUTTERFLY T ops of one instruction (same k,
-    independent coordinate masks) behind an OP_FUSE2 marker.  The device
-    runs a marked pair as one dense pass over 4-entry blocks
-    {base, base^e1, base^e2, base^e1^e2}, applying both merges in registers;
-    in sparse mode it ignores the marker.  Payload: h1 | h2<<8 | c21<<16,
-    e2 (e1 = cb1; e2 = cb2 reduced by e1 at pivot h1)."""
-    pairs = []
-    i = 0
-    while i + 1 < len(t_ops):
-        o1, k1, c1, kk1, cb1, _ = t_ops[i]
-        o2, k2, c2, kk2, cb2, _ = t_ops[i + 1]
-        if (k1 == k2 == OP_T and c1 == c2 == T_BUTTERFLY and kk1 == kk2
-                and kk1 >= 2 and cb1 and cb2 and cb1 != cb2):
-            h1 = cb1.bit_length() - 1
-            e2 = cb2 ^ cb1 if (cb2 >> h1) & 1 else cb2
-            h2 = e2.bit_length() - 1
-            c21 = (cb2 >> h1) & 1
-            pairs.append((o1, kk1, h1 | (h2 << 8) | (c21 << 16), e2))
-            i += 2
-        else:
-            i += 1
-    # insert back to front so earlier offsets stay valid
-    for off, kk, w0, e2 in reversed(pairs):
-        hdr = OP_FUSE2 | (3 << 8) | ((kk & 0xFF) << 16) | (0xFFFFFFFF << 32)
-        em.ops[off:off] = [hdr, w0, e2]
-
-
 def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
                     stop_after: int | None = None,
-                    keep_frames: bool = False, fuse: bool = True) -> DeviceProgram:
+                    keep_frames: bool = False) -> DeviceProgram:
     """Lower a parsed program (this package's or the reference's
     ``CircuitProgram``) to the device op stream.
 
@@ -398,7 +369,6 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
     sign_bytes = 2 * ((2 * n + 7) // 8)
     total_static_sign = 0
     noise_ops: list = []
-    t_ops: list = []
 
     def lohi(m):
         return m & nmask, (m >> n) & nmask
@@ -440,7 +410,6 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         # components, so this host constant is exact; the device negates it
         # when the per-shot sign parity adds 2 to xi0
         bxs = b * (1.0 + 0.0j, 1.0j, -1.0 + 0.0j, -1.0j)[xis]
-        t_ops.append((len(em.ops), kind, case, k, cb, instr))
         em.op(kind, k, case | (xis << 2), instr,
               [pre_lo, pre_hi, m_lo, m_hi, delta, cb | (dmask << 32),
                _dbl_bits(a.real), _dbl_bits(a.imag), _dbl_bits(bxs.real),
@@ -572,13 +541,10 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
             emit_noise(name, tuple(ins.targets), float(ins.args[0]), i)
         elif name in ("T", "T_DAG"):
             ok = True
-            t_ops = []
             for q in ins.targets:
                 if not emit_t(q, name == "T_DAG", i):
                     ok = False
                     break
-            if fuse:
-                _insert_fuse_markers(em, t_ops)
             if not ok:
                 break
         elif name in GATES_2Q:

@@ -36,7 +36,7 @@ typedef unsigned char u8;
 namespace gs {
 
 enum { OP_END = 0, OP_T = 1, OP_MEAS = 2, OP_NOISE = 3, OP_FEEDBACK = 4,
-       OP_DETECTOR = 5, OP_OBSERVABLE = 6, OP_GROW_LIMIT = 7, OP_FUSE2 = 8 };
+       OP_DETECTOR = 5, OP_OBSERVABLE = 6, OP_GROW_LIMIT = 7 };
 enum { T_DIAG = 0, T_BUTTERFLY = 1, T_GROW = 2 };
 enum { M_DET = 0, M_PIVOT_SPAN = 1, M_PIVOT_NOSPAN = 2 };
 enum { MF_RECORD = 16, MF_FLIP = 32, MF_RESET = 64, MF_COMPACT = 128 };
@@ -452,80 +452,6 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
       hnext = __ldg(ops + pc);       // prefetch the next header
       kcur = k;
       const u32 size = 1u << k;
-
-      if (kind == OP_FUSE2) {
-        // two BUTTERFLY T ops of one instruction in one dense pass over
-        // 4-entry blocks {base, base^e1, base^e2, base^e1^e2}; identical
-        // arithmetic, prune and capacity checks per gate (ref state.py:104-129)
-#ifdef GS_NO_FUSE
-        continue;
-#endif
-        if (lst && cnt <= scap && size >= kSparseMin) continue;   // sparse: run singly
-        const u64 *o1 = ops + pc;
-        const u64 h1w = __ldg(o1);
-        const u32 len1 = (u32)((h1w >> 8) & 0xff);
-        const u64 *o2 = o1 + len1;
-        const u64 h2w = __ldg(o2);
-        const u32 len2 = (u32)((h2w >> 8) & 0xff);
-        const u64 mw = __ldg(op + 1);
-        const u32 p1 = (u32)mw & 0xff, p2 = (u32)(mw >> 8) & 0xff, c21 = (u32)(mw >> 16) & 1u;
-        const u32 e2 = (u32)__ldg(op + 2);
-        sig_lo ^= __ldg(o1 + 1);
-        sig_hi ^= __ldg(o1 + 2);
-        const u32 f1 = par64(sig_lo & __ldg(o1 + 3)) ^ par64(sig_hi & __ldg(o1 + 4));
-        sig_lo ^= __ldg(o2 + 1);
-        sig_hi ^= __ldg(o2 + 2);
-        const u32 f2 = par64(sig_lo & __ldg(o2 + 3)) ^ par64(sig_hi & __ldg(o2 + 4));
-        const u32 dc1 = par64(__ldg(o1 + 5) & c), dc2 = par64(__ldg(o2 + 5) & c);
-        const u64 q1 = __ldg(o1 + 6), q2 = __ldg(o2 + 6);
-        const u32 cb1 = (u32)q1, dm1 = (u32)(q1 >> 32), dm2 = (u32)(q2 >> 32);
-        const double2 a1 = make_double2(dbits(__ldg(o1 + 7)), dbits(__ldg(o1 + 8)));
-        const double2 a2 = make_double2(dbits(__ldg(o2 + 7)), dbits(__ldg(o2 + 8)));
-        const double2 bs1 = make_double2(dbits(__ldg(o1 + 9)), dbits(__ldg(o1 + 10)));
-        const double2 bs2 = make_double2(dbits(__ldg(o2 + 9)), dbits(__ldg(o2 + 10)));
-        const double2 b10 = f1 ? cneg(bs1) : bs1, b11 = cneg(b10);
-        const double2 b20 = f2 ? cneg(bs2) : bs2, b21 = cneg(b20);
-        const u32 lo_p = p1 < p2 ? p1 : p2, hi_p = p1 < p2 ? p2 : p1;
-        u32 nz1 = 0, nz2 = 0;
-        for (u32 m = lane; m < (size >> 2); m += 32) {
-          const u32 i0 = ins_bit(ins_bit(m, lo_p, 0), hi_p, 0);
-          const u32 i1 = i0 ^ cb1, i2 = i0 ^ e2, i3 = i1 ^ e2;
-          const double2 v0 = A[i0], v1 = A[i1], v2 = A[i2], v3 = A[i3];
-          // gate 1: pairs (i0,i1), (i2,i3)
-          const double2 n0 = prune(cadd(cmul(a1, v0), cmul((dc1 ^ par32(i1 & dm1)) ? b11 : b10, v1)));
-          const double2 n1 = prune(cadd(cmul(a1, v1), cmul((dc1 ^ par32(i0 & dm1)) ? b11 : b10, v0)));
-          const double2 n2 = prune(cadd(cmul(a1, v2), cmul((dc1 ^ par32(i3 & dm1)) ? b11 : b10, v3)));
-          const double2 n3 = prune(cadd(cmul(a1, v3), cmul((dc1 ^ par32(i2 & dm1)) ? b11 : b10, v2)));
-          nz1 += nonzero(n0) + nonzero(n1) + nonzero(n2) + nonzero(n3);
-          // gate 2: partner = x ^ (e2 ^ c21*e1)
-          const u32 ja = c21 ? i3 : i2, jb = c21 ? i2 : i3;      // partners of i0, i1
-          const double2 va = c21 ? n3 : n2, vb = c21 ? n2 : n3;
-          const double2 r0 = prune(cadd(cmul(a2, n0), cmul((dc2 ^ par32(ja & dm2)) ? b21 : b20, va)));
-          const double2 ra = prune(cadd(cmul(a2, va), cmul((dc2 ^ par32(i0 & dm2)) ? b21 : b20, n0)));
-          const double2 r1 = prune(cadd(cmul(a2, n1), cmul((dc2 ^ par32(jb & dm2)) ? b21 : b20, vb)));
-          const double2 rb = prune(cadd(cmul(a2, vb), cmul((dc2 ^ par32(i1 & dm2)) ? b21 : b20, n1)));
-          nz2 += nonzero(r0) + nonzero(ra) + nonzero(r1) + nonzero(rb);
-          A[i0] = r0;
-          A[i1] = r1;
-          A[ja] = ra;
-          A[jb] = rb;
-        }
-        __syncwarp();
-        const u32 cin = cnt;
-        const u32 cnt1 = warp_sum_u32(nz1), cnt2 = warp_sum_u32(nz2);
-        mbytes += __ldg(o1 + 11) + __ldg(o2 + 11) +
-                  (u64)kEntryBytes * (cin + 2ull * cnt1 + cnt2);
-        pc += len1 + len2;
-        hnext = __ldg(ops + pc);
-        if ((u64)cnt1 > R.cap) { status = ST_OVERFLOW; aux = (int)(h1w >> 32); break; }
-        if (cnt1 == 0) { status = ST_CORRUPT; aux = (int)(h1w >> 32); break; }
-        cnt = cnt2;
-        if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)(h2w >> 32); break; }
-        if (cnt == 0) { status = ST_CORRUPT; aux = (int)(h2w >> 32); break; }
-        lst = cnt <= scap && size >= kSparseMin;
-        if (lst) build_list(A, L, size, lane);
-        continue;
-      }
 
       if (kind == OP_T || kind == OP_GROW_LIMIT) {
         sig_lo ^= __ldg(op + 1);

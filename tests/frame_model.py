@@ -105,8 +105,6 @@ def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
         pc += ln
         size = 1 << k
         k_final = k
-        if kind == C.OP_FUSE2:
-            continue        # device-side fusion hint; semantics = the two ops
         if kind == C.OP_END:
             sig_xor(pay[0], pay[1])
             model_bytes += pay[2]
