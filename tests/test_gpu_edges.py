@@ -1,0 +1,74 @@
+"""GPU edge cases: empty runs, Clifford-only programs, records larger than
+the shared-memory slot (global record path), REPEAT-heavy programs, the
+chi-dimension limit (OVERFLOW vs UNSUPPORTED), 64-qubit masks."""
+
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import gstab_oracle as orc
+from paper_2512_23037_b200 import SamplerConfig, parse_circuit, run_batch, sample
+from paper_2512_23037_b200.sampler import _records_before
+
+
+def _oracle(prog, master, shots, cap, post, mode="splitmix"):
+    flat = list(prog.flat())
+    return [orc.run_one_shot(flat, prog.num_qubits, orc.DrawStream(mode, master, s),
+                             cap, post) for s in range(shots)]
+
+
+def _check(prog, master, shots, cfg_kw, cap):
+    cfg = SamplerConfig(shots=shots, master_seed=master, **cfg_kw)
+    b = sample(prog, cfg)
+    ref = _oracle(prog, master, shots, cap, cfg.postselect, cfg.rng)
+    for s in range(shots):
+        got = b.result(s, measured=_records_before(prog, b, s))
+        assert got.status.value == ref[s]["status"], s
+        assert got.record == ref[s]["record"], s
+
+
+def test_zero_shots_and_empty_program():
+    st = run_batch(parse_circuit("M 0\n"), SamplerConfig(shots=0))
+    assert st.total_shots == 0 and st.discard_rate == 0.0
+    st = run_batch(parse_circuit("H 0\n"), SamplerConfig(shots=100))
+    assert st.preserved_shots == 100 and st.logical_error_shots == 0
+
+
+def test_clifford_only_program():
+    prog = parse_circuit("H 0\nCX 0 1\nS 1\nDEPOLARIZE1(0.2) 0 1\nM 0 1\n"
+                         "DETECTOR rec[-1] rec[-2]\nOBSERVABLE_INCLUDE(0) rec[-1]\n")
+    _check(prog, 4, 64, dict(postselect=True), 4096)
+
+
+def test_records_beyond_shared_memory_slot():
+    # 20000 measurements -> 2.5 KB of record bits per shot (global path)
+    text = "H 0\nREPEAT 10000 {\n  X_ERROR(0.01) 0 1\n  M 0 1\n  DETECTOR rec[-2] rec[-4]\n}\n"
+    prog = parse_circuit("M 0 1\n" + text)
+    _check(prog, 2, 8, dict(postselect=False), 4096)
+    b = sample(prog, SamplerConfig(shots=16, master_seed=3, postselect=True))
+    assert b.records.shape[1] == (prog.num_measurements + 63) // 64
+
+
+def test_dimension_limit_overflow_and_unsupported():
+    prog = parse_circuit("H 0 1 2 3 4 5\nT 0 1 2 3 4 5\nM 0\n")   # k reaches 6
+    # capacity 8 < 2^4: the reference overflows at the 4th T -> OVERFLOW
+    _check(prog, 1, 4, dict(entry_capacity=8, rerun_on_overflow=False, max_dim=3), 8)
+    # capacity large, dimension limit 3: not representable -> loud error
+    with pytest.raises(RuntimeError):
+        run_batch(prog, SamplerConfig(shots=4, max_dim=3))
+
+
+def test_64_qubit_masks():
+    rng = random.Random(64)
+    lines = ["H " + " ".join(str(q) for q in range(64))]
+    for _ in range(60):
+        a, b = rng.sample(range(64), 2)
+        lines.append("CX %d %d" % (a, b))
+    lines += ["T 63", "T_DAG 0", "DEPOLARIZE1(0.05) 63 0 31", "M 63 0 32",
+              "MPP X63*Z0*Y31", "DETECTOR rec[-1]", "OBSERVABLE_INCLUDE(5) rec[-2]"]
+    prog = parse_circuit("\n".join(lines) + "\n")
+    assert prog.num_qubits == 64
+    _check(prog, 9, 48, dict(postselect=True), 4096)
