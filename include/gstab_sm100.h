@@ -109,6 +109,14 @@ int gs_engine_destroy(gs_engine *eng);
 /* counters: host vector of GS_C_PER_OBS + num_obs int64 (overwritten) */
 int gs_run_counters(gs_engine *eng, gs_program *prog, const gs_run_params *p,
                     int64_t *counters);
+/* counters plus up to witness_cap global shot indices of preserved shots
+   whose observables flipped (logical-error witnesses, paper §V-B); the
+   total number found is returned in *witness_count (may exceed the cap).
+   Order is nondeterministic; callers sort. */
+int gs_run_counters_witness(gs_engine *eng, gs_program *prog,
+                            const gs_run_params *p, int64_t *counters,
+                            uint64_t *witness, uint32_t witness_cap,
+                            uint32_t *witness_count);
 /* async variant: accumulates (+=) into a DEVICE int64 vector on `stream`
    (cudaStream_t); lets NCCL reduce the counters in place */
 int gs_run_counters_async(gs_engine *eng, gs_program *prog,

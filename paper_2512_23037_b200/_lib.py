@@ -33,7 +33,8 @@ GS_C_PER_OBS = 8
 
 EXPORTED = (
     "gs_program_create", "gs_program_destroy", "gs_engine_create",
-    "gs_engine_destroy", "gs_run_counters", "gs_run_counters_async",
+    "gs_engine_destroy", "gs_run_counters", "gs_run_counters_witness",
+    "gs_run_counters_async",
     "gs_run_records", "gs_dump_shots", "gs_anticommute_mask",
     "gs_conj_gate_rows", "gs_mul_rows", "gs_parity_pm", "gs_last_error",
     "gs_abi_version", "gs_engine_launches", "gs_engine_last_kernel_ms",
@@ -85,6 +86,9 @@ def load(path: str | None = None):
     lib.gs_engine_destroy.argtypes = [vp]
     lib.gs_run_counters.argtypes = [vp, vp, ct.POINTER(GsRunParams),
                                     ct.POINTER(ct.c_int64)]
+    lib.gs_run_counters_witness.argtypes = [vp, vp, ct.POINTER(GsRunParams),
+                                            ct.POINTER(ct.c_int64), vp, ct.c_uint32,
+                                            ct.POINTER(ct.c_uint32)]
     lib.gs_run_counters_async.argtypes = [vp, vp, ct.POINTER(GsRunParams),
                                           vp, vp]
     lib.gs_run_records.argtypes = [vp, vp, ct.POINTER(GsRunParams), vp, vp,

@@ -81,6 +81,9 @@ struct DevOut {
   u32 rec_in_smem;
   u32 chi_off;          // byte offset of chi inside the warp's smem slice
   u32 lcap;             // occupancy-list capacity (<= kLcapMax; 0 = dense only)
+  u64 *witness;         // optional: global indices of preserved shots with a
+  u32 *witness_count;   //   flipped observable (paper §V-B witnesses)
+  u32 witness_cap;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -977,9 +980,14 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
       n_pres += 1;
       if (obs) {
         n_err += 1;
-        if (lane == 0)
+        if (lane == 0) {
           for (u64 o = obs; o; o &= o - 1)
             atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
+          if (O.witness) {
+            const u32 wi = atomicAdd(O.witness_count, 1u);
+            if (wi < O.witness_cap) O.witness[wi] = shot;
+          }
+        }
       }
     } else if (status == ST_DISCARDED) n_disc += 1;
     else if (status == ST_OVERFLOW) n_ovf += 1;
@@ -1385,7 +1393,24 @@ static int ensure_counters(gs_engine *e, size_t n) {
   return GS_OK;
 }
 
+static int run_counters_impl(gs_engine *e, gs_program *p, const gs_run_params *r,
+                             int64_t *counters, uint64_t *witness, uint32_t witness_cap,
+                             uint32_t *witness_count);
+
 int gs_run_counters(gs_engine *e, gs_program *p, const gs_run_params *r, int64_t *counters) {
+  return run_counters_impl(e, p, r, counters, nullptr, 0, nullptr);
+}
+
+int gs_run_counters_witness(gs_engine *e, gs_program *p, const gs_run_params *r,
+                            int64_t *counters, uint64_t *witness, uint32_t witness_cap,
+                            uint32_t *witness_count) {
+  if (!witness || !witness_count) return fail(GS_ERR_ARG, "null argument");
+  return run_counters_impl(e, p, r, counters, witness, witness_cap, witness_count);
+}
+
+static int run_counters_impl(gs_engine *e, gs_program *p, const gs_run_params *r,
+                             int64_t *counters, uint64_t *witness, uint32_t witness_cap,
+                             uint32_t *witness_count) {
   if (!e || !p || !r || !counters) return fail(GS_ERR_ARG, "null argument");
   CUDA_TRY(cudaSetDevice(e->device));
   const size_t nc = GS_C_PER_OBS + p->info.num_obs;
@@ -1396,9 +1421,26 @@ int gs_run_counters(gs_engine *e, gs_program *p, const gs_run_params *r, int64_t
   memset(&O, 0, sizeof(O));
   O.counters = e->d_counters;
   O.mode = gs::MODE_COUNTERS;
+  u64 *d_w = nullptr;
+  u32 *d_wc = nullptr;
+  if (witness) {
+    CUDA_TRY(cudaMallocAsync(&d_w, (witness_cap ? witness_cap : 1) * 8ull, e->stream));
+    CUDA_TRY(cudaMallocAsync(&d_wc, 4, e->stream));
+    CUDA_TRY(cudaMemsetAsync(d_wc, 0, 4, e->stream));
+    O.witness = d_w;
+    O.witness_count = d_wc;
+    O.witness_cap = witness_cap;
+  }
   rc = launch(e, p, r, O, e->stream, true);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(counters, e->d_counters, nc * 8, cudaMemcpyDeviceToHost, e->stream));
+  if (witness) {
+    CUDA_TRY(cudaMemcpyAsync(witness_count, d_wc, 4, cudaMemcpyDeviceToHost, e->stream));
+    if (witness_cap)
+      CUDA_TRY(cudaMemcpyAsync(witness, d_w, witness_cap * 8ull, cudaMemcpyDeviceToHost, e->stream));
+    cudaFreeAsync(d_w, e->stream);
+    cudaFreeAsync(d_wc, e->stream);
+  }
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   float ms = 0.f;
   if (r->shot_count) CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));

@@ -106,6 +106,18 @@ class Engine:
             out.ctypes.data_as(ct.POINTER(ct.c_int64))))
         return out
 
+    def run_counters_witness(self, prog: Program, params, cap: int):
+        """Counters plus the global indices of (up to ``cap``) preserved
+        shots with a flipped observable, sorted."""
+        out = np.zeros(prog.num_counters, dtype=np.int64)
+        wit = np.zeros(max(cap, 1), dtype=np.uint64)
+        found = ct.c_uint32(0)
+        _lib.check(_lib.load().gs_run_counters_witness(
+            self.handle, prog.handle, ct.byref(params),
+            out.ctypes.data_as(ct.POINTER(ct.c_int64)), wit.ctypes.data, cap,
+            ct.byref(found)))
+        return out, np.sort(wit[:min(cap, found.value)]), int(found.value)
+
     def run_counters_async(self, prog: Program, params, counters_dev_ptr: int,
                            stream_ptr: int) -> None:
         _lib.check(_lib.load().gs_run_counters_async(

@@ -138,6 +138,7 @@ class RunStats:
     # B200 extras (not in as_dict, which keeps the reference schema)
     device_time_s: float = 0.0
     model_bytes: int = 0
+    witnesses: list = field(default_factory=list)   # shot indices (see run_batch)
 
     @property
     def discard_rate(self) -> float:
@@ -231,24 +232,38 @@ def counters_to_stats(c: np.ndarray, obs_keys, wall: float,
 
 
 def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
-              engine: Engine | None = None) -> RunStats:
+              engine: Engine | None = None, witnesses: int = 0) -> RunStats:
     """Counters of shots [shot_begin, shot_begin + cfg.shots) (global shot
-    indices, so shards of one run combine exactly)."""
+    indices, so shards of one run combine exactly).
+
+    ``witnesses > 0`` also collects the global indices of up to that many
+    preserved shots whose observables flipped ("rare-failure witnesses",
+    paper §V-B); replay one with ``run_shot`` and
+    ``ShotContext.reset(derive_seed(master_seed, index))``.
+    """
     t0 = time.perf_counter()
     p = _program_for(prog, cfg.dim_limit)
     eng = engine or get_engine(cfg.device)
     total = np.zeros(p.num_counters, dtype=np.int64)
+    wit: list = []
     dev_s = 0.0
     done = 0
     while done < cfg.shots:
         cnt = min(_CHUNK, cfg.shots - done)
         par = Engine.params(cfg.master_seed, shot_begin + done, cnt,
                             cfg.effective_capacity, cfg.run_flags())
-        total += eng.run_counters(p, par)
+        if witnesses > len(wit):
+            c, w, _ = eng.run_counters_witness(p, par, witnesses - len(wit))
+            total += c
+            wit.extend(int(x) for x in w)
+        else:
+            total += eng.run_counters(p, par)
         dev_s += eng.last_kernel_ms * 1e-3
         done += cnt
-    return counters_to_stats(total, p.dp.obs_keys, time.perf_counter() - t0,
-                             dev_s)
+    st = counters_to_stats(total, p.dp.obs_keys, time.perf_counter() - t0,
+                           dev_s)
+    st.witnesses = sorted(wit)
+    return st
 
 
 @dataclass

@@ -72,3 +72,33 @@ def test_64_qubit_masks():
     prog = parse_circuit("\n".join(lines) + "\n")
     assert prog.num_qubits == 64
     _check(prog, 9, 48, dict(postselect=True), 4096)
+
+
+def test_witnesses_replay_to_logical_errors():
+    """Witness shot indices (preserved shots with a flipped observable) must
+    replay through run_shot to an error, and their count equals the counter."""
+    from paper_2512_23037_b200 import ShotContext, derive_seed, run_shot
+    from paper_2512_23037_b200.msc import msc_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(msc_circuit(3), 2e-3)
+    st = run_batch(prog, SamplerConfig(shots=20000, master_seed=6, postselect=True),
+                   witnesses=64)
+    assert len(st.witnesses) == min(64, st.logical_error_shots)
+    for w in st.witnesses[:8]:
+        ctx = ShotContext(prog.num_qubits, 4096 * 8)
+        ctx.reset(derive_seed(6, w))
+        r = run_shot(prog, ctx, postselect=True)
+        assert r.status.value == "preserved" and any(r.observables.values())
+
+
+def test_cli_sample_json_schema(tmp_path):
+    import json
+    from paper_2512_23037_b200.cli import main
+    path = tmp_path / "c.stim"
+    path.write_text("H 0\nCX 0 1\nM 0 1\nDETECTOR rec[-1] rec[-2]\nOBSERVABLE_INCLUDE(0) rec[-1]\n")
+    out = tmp_path / "o.json"
+    assert main(["sample", str(path), "--shots", "1000", "--noise", "0.01",
+                 "--postselect", "--out", str(out)]) == 0
+    d = json.loads(out.read_text())
+    assert d["total_shots"] == 1000
+    assert set(d) >= {"preserved_shots", "discard_rate", "bayes_lo", "throughput"}

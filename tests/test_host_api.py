@@ -209,3 +209,25 @@ def test_bayes_interval_brackets_mle_everywhere():
                 target = ll(k / n) - math.log(1000)
                 for p in (lo, hi):
                     assert ll(p) == pytest.approx(target, abs=1e-6)
+
+
+# -- CLI (host-only commands; `sample` runs on the GPU tests) ---------------
+
+def test_cli_stats_and_msc(tmp_path):
+    from paper_2512_23037_b200.cli import main
+    path = tmp_path / "d3.stim"
+    assert main(["msc", "--d", "3", "--out", str(path)]) == 0
+    out = tmp_path / "s.json"
+    assert main(["stats", str(path), "--out", str(out)]) == 0
+    import json
+    d = json.loads(out.read_text())
+    assert d["total_qubits"] == 15 and d["t_count"] == 22
+
+
+def test_cli_parse_error_exit_code(tmp_path):
+    from paper_2512_23037_b200.cli import main
+    bad = tmp_path / "bad.stim"
+    bad.write_text("FOO 0\n")
+    with pytest.raises(SystemExit) as ei:
+        main(["stats", str(bad)])
+    assert ei.value.code == 3
