@@ -1,4 +1,5 @@
-"""Benchmark: MSC d=5 (proxy) shots/s on 1..8 B200, p=1e-3, post-selection.
+"""Benchmark: MSC d=5 (grown proxy, 42 q, 72 T) shots/s on 1..8 B200, p=1e-3,
+post-selection.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
@@ -43,12 +44,23 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _workload(d: int, p: float):
-    from paper_2512_23037_b200.msc import msc_circuit
+WORKLOADS = {
+    # BASELINE config 5: d=3 -> d=5 grown cultivation proxy, 42 q, 72 T
+    "msc_d5": ("msc_d5_grown_proxy", lambda m: m.msc_grown_circuit(5)),
+    # round-1 headline: all checks at d=5 (42 q, 96 T; more chi work)
+    "msc_d5_2check": ("msc_d5_2check_proxy", lambda m: m.msc_circuit(5)),
+    # BASELINE config 2
+    "msc_d3": ("msc_d3_proxy", lambda m: m.msc_circuit(3)),
+}
+
+
+def _workload(key: str, p: float):
+    from paper_2512_23037_b200 import msc
     from paper_2512_23037_b200.noise import apply_noise_model
     from paper_2512_23037_b200.circuit import compute_stats
-    base = msc_circuit(d)
-    return apply_noise_model(base, p), compute_stats(base).as_dict()
+    name, make = WORKLOADS[key]
+    base = make(msc)
+    return name, apply_noise_model(base, p), compute_stats(base).as_dict()
 
 
 class ClockSampler:
@@ -132,7 +144,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--shots-per-step", type=int, default=1 << 22)
-    ap.add_argument("--d", type=int, default=5)
+    ap.add_argument("--workload", default="msc_d5", choices=sorted(WORKLOADS))
     ap.add_argument("--p", type=float, default=1e-3)
     ap.add_argument("--rng", default="philox", choices=["philox", "splitmix"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -147,8 +159,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    prog, stats = _workload(args.d, args.p)
-    workload = "msc_d%d_proxy" % args.d
+    workload, prog, stats = _workload(args.workload, args.p)
     config = {"workload": workload, "noise_p": args.p, "postselect": True,
               "rng": args.rng, "shots_per_step_per_gpu": args.shots_per_step,
               "circuit": stats, "parallelism": "shot-dp%d" % world,
@@ -256,25 +267,33 @@ def main():
     # per GPU (each rank's kernel sees its own shots)
     achieved = (model_bytes / world) / (my_ms * 1e-3) / 1e9
 
-    e2e = None
+    # e2e through the public C ABI with host buffers, on every rank: each
+    # step creates the program (host->device upload of the op stream),
+    # samples this rank's shots and reads the counters back (device->host);
+    # wall time between barriers, max over ranks
+    h2d = int(dp.ops.nbytes + dp.tables.nbytes + dp.locs.nbytes)
+    d2h = nc * 8
+    e2e_steps = max(2, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        Pe = Program(dp)
+        base = (1 << 40) + s * world * S + rank * S
+        par = Engine.params(777, base, S, 32768, flags, warps_per_block=args.wpb)
+        eng.run_counters(Pe, par)
+        del Pe
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": e2e_steps * world * S / e2e_s, "unit": "shots/s",
+           "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+           "steps": e2e_steps,
+           "path": "gs_program_create + gs_run_counters (host buffers), all ranks"}
     cb = None
     if rank == 0:
-        # e2e through the public C ABI with host buffers: every step creates
-        # the program (host->device upload of the op stream) and reads the
-        # counters back (device->host) inside the timed region
-        h2d = int(dp.ops.nbytes + dp.tables.nbytes + dp.locs.nbytes)
-        d2h = nc * 8
-        times = []
-        for s in range(max(2, min(args.steps, 3))):
-            t0 = time.perf_counter()
-            Pe = Program(dp)
-            par = Engine.params(777, s * S, S, 32768, flags, warps_per_block=args.wpb)
-            out = eng.run_counters(Pe, par)
-            times.append(time.perf_counter() - t0)
-            del Pe
-        e2e = {"value": S / (sorted(times)[len(times) // 2]), "unit": "shots/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "gs_program_create + gs_run_counters (host buffers)"}
         if not args.no_cpu_baseline:
             cb = cpu_baseline(prog, args.cpu_seconds, args.rng, args.p)
         line = {

@@ -105,84 +105,81 @@ class _Builder:
         return "rec[%d]" % (absolute - self.meas)
 
 
-def msc_circuit(d: int = 5, *, checks: int | None = None, flags: int | None = None,
-                final_observable: bool = True, rounds_after_injection: int = 1):
-    """Noiseless MSC-like cultivation proxy of distance ``d`` (3 or 5).
+class _Patch:
+    """Qubit roles of one color-code patch inside the 42-qubit layout."""
 
-    Defaults: d=3 -> 1 full check + final half-check on 15 qubits
-    (22 T, T-depth 4 as in Table 2); d=5 -> 2 full checks + final
-    half-check on 42 qubits (19 data, 9+9 check ancillas, injection, check
-    and 3 flag qubits; 96 T, T-depth 6).
-    """
-    sites, faces = color_code_patch(d)
-    nd, nf = len(sites), len(faces)
-    if checks is None:
-        checks = 1 if d == 3 else 2
-    if flags is None:
-        flags = 0 if d == 3 else 3
-    data = list(range(nd))
-    zanc = list(range(nd, nd + nf))
-    xanc = list(range(nd + nf, nd + 2 * nf))
-    inj = nd + 2 * nf
-    chk = inj + 1
-    flg = list(range(chk + 1, chk + 1 + flags))
-    allq = data + zanc + xanc + [inj, chk] + flg
-    sub0 = [q for q, (r, c) in enumerate(sites) if (r + c) % 3 == 0]
-    sub2 = [q for q, (r, c) in enumerate(sites) if (r + c) % 3 == 2]
-    b = _Builder()
+    def __init__(self, data, faces, zanc, xanc, sub0, sub2):
+        self.data, self.faces = data, faces
+        self.zanc, self.xanc = zanc, xanc
+        self.sub0, self.sub2 = sub0, sub2
 
-    def z_round(detect: bool):
-        b.op("R " + " ".join(map(str, zanc)))
+
+class _Cultivation:
+    """Gadgets shared by the proxies."""
+
+    def __init__(self, b: _Builder, chk: int, flg):
+        self.b, self.chk, self.flg = b, chk, list(flg)
+
+    def z_round(self, P: _Patch, detect):
+        """Z-face round; ``detect`` = True (every face), False, or the set of
+        face indices whose outcome is deterministic."""
+        b = self.b
+        b.op("R " + " ".join(map(str, P.zanc)))
         b.tick()
         for layer in range(6):
             pairs = []
-            for f, face in enumerate(faces):
+            for f, face in enumerate(P.faces):
                 if layer < len(face):
-                    pairs += [face[layer], zanc[f]]
+                    pairs += [face[layer], P.zanc[f]]
             if pairs:
                 b.op("CX " + " ".join(map(str, pairs)))
                 b.tick()
-        ms = b.measure("MR", zanc)
+        ms = b.measure("MR", P.zanc)
         b.tick()
-        if detect:
-            for m in ms:
-                b.op("DETECTOR " + b.rec(m))
+        self._detect(ms, detect)
         return ms
 
-    def x_round(detect: bool):
-        b.op("R " + " ".join(map(str, xanc)))
+    def x_round(self, P: _Patch, detect):
+        b = self.b
+        b.op("R " + " ".join(map(str, P.xanc)))
         b.tick()
-        b.op("H " + " ".join(map(str, xanc)))
+        b.op("H " + " ".join(map(str, P.xanc)))
         b.tick()
         for layer in range(6):
             pairs = []
-            for f, face in enumerate(faces):
+            for f, face in enumerate(P.faces):
                 if layer < len(face):
-                    pairs += [xanc[f], face[layer]]
+                    pairs += [P.xanc[f], face[layer]]
             if pairs:
                 b.op("CX " + " ".join(map(str, pairs)))
                 b.tick()
-        b.op("H " + " ".join(map(str, xanc)))
+        b.op("H " + " ".join(map(str, P.xanc)))
         b.tick()
-        ms = b.measure("MR", xanc)
+        ms = b.measure("MR", P.xanc)
         b.tick()
-        if detect:
-            for m in ms:
-                b.op("DETECTOR " + b.rec(m))
+        self._detect(ms, detect)
+        return ms
 
-    def t_layer(undo: bool):
+    def _detect(self, ms, detect):
+        for f, m in enumerate(ms):
+            if detect is True or (detect and f in detect):
+                self.b.op("DETECTOR " + self.b.rec(m))
+
+    def t_layer(self, P: _Patch, undo: bool):
+        b = self.b
         first, second = ("T", "T_DAG") if undo else ("T_DAG", "T")
-        if sub0:
-            b.op("%s %s" % (first, " ".join(map(str, sub0))))
-        if sub2:
-            b.op("%s %s" % (second, " ".join(map(str, sub2))))
+        if P.sub0:
+            b.op("%s %s" % (first, " ".join(map(str, P.sub0))))
+        if P.sub2:
+            b.op("%s %s" % (second, " ".join(map(str, P.sub2))))
         b.tick()
 
-    def x_parity(observable: bool):
+    def x_parity(self, P: _Patch, observable: bool):
         """X^n parity of the data block read out through a cat state on the
         check ancilla and the flag qubits (flags end deterministic 0 and
         catch hook errors); each cat qubit drives one segment of data CXs so
         the segments run in parallel."""
+        b, chk, flg = self.b, self.chk, self.flg
         cat = [chk] + flg
         b.op("R " + " ".join(map(str, cat)))
         b.tick()
@@ -191,7 +188,7 @@ def msc_circuit(d: int = 5, *, checks: int | None = None, flags: int | None = No
         for f in flg:
             b.op("CX %d %d" % (chk, f))
             b.tick()
-        seg = [data[i::len(cat)] for i in range(len(cat))]
+        seg = [P.data[i::len(cat)] for i in range(len(cat))]
         for layer in range(max(len(s_) for s_ in seg)):
             pairs = []
             for a, s_ in zip(cat, seg):
@@ -214,44 +211,207 @@ def msc_circuit(d: int = 5, *, checks: int | None = None, flags: int | None = No
         for m in fms:
             b.op("DETECTOR " + b.rec(m))
 
-    # --- prepare |+_L>
-    b.op("R " + " ".join(map(str, allq)))
-    b.tick()
-    b.op("H " + " ".join(map(str, data)))
-    b.tick()
-    zm = z_round(detect=False)
-    for f, e in enumerate(_pure_errors(nd, faces)):
-        for q in e:
-            b.op("X %s %d" % (b.rec(zm[f]), q))
-    b.tick()
-    # --- inject T on the logical parity
-    b.op("R %d" % inj)
-    b.tick()
-    for q in data:
-        b.op("CX %d %d" % (q, inj))
-    b.tick()
-    b.op("T %d" % inj)
-    b.tick()
-    for q in reversed(data):
-        b.op("CX %d %d" % (q, inj))
-    b.tick()
-    im = b.measure("MR", [inj])
-    b.tick()
-    b.op("DETECTOR " + b.rec(im[0]))
+    def prepare_plus(self, P: _Patch, allq):
+        """R all, H data, one Z round without detectors, then Pauli-frame
+        feedback on a pure-error set per face: |+_L> with every face +1."""
+        b = self.b
+        b.op("R " + " ".join(map(str, allq)))
+        b.tick()
+        b.op("H " + " ".join(map(str, P.data)))
+        b.tick()
+        zm = self.z_round(P, detect=False)
+        nd = max(P.data) + 1
+        for f, e in enumerate(_pure_errors(nd, P.faces)):
+            for q in e:
+                b.op("X %s %d" % (b.rec(zm[f]), q))
+        b.tick()
+
+    def inject(self, P: _Patch, inj: int):
+        """T on the logical Z-parity through an ancilla, MR + DETECTOR."""
+        b = self.b
+        b.op("R %d" % inj)
+        b.tick()
+        for q in P.data:
+            b.op("CX %d %d" % (q, inj))
+        b.tick()
+        b.op("T %d" % inj)
+        b.tick()
+        for q in reversed(P.data):
+            b.op("CX %d %d" % (q, inj))
+        b.tick()
+        im = b.measure("MR", [inj])
+        b.tick()
+        b.op("DETECTOR " + b.rec(im[0]))
+
+    def check(self, P: _Patch, rounds: int = 1):
+        """One cultivation check: T_DAG/T layer, X^n parity (DETECTOR), undo
+        layer, then ``rounds`` Z+X syndrome rounds with detectors."""
+        self.t_layer(P, undo=False)
+        self.x_parity(P, observable=False)
+        self.t_layer(P, undo=True)
+        for _ in range(rounds):
+            self.z_round(P, detect=True)
+            self.x_round(P, detect=True)
+
+    def final(self, P: _Patch):
+        """Final half-check: T layer + X^n parity into OBSERVABLE_INCLUDE(0)."""
+        self.t_layer(P, undo=False)
+        self.x_parity(P, observable=True)
+
+
+def _layout(d: int, flags: int):
+    sites, faces = color_code_patch(d)
+    nd, nf = len(sites), len(faces)
+    data = list(range(nd))
+    zanc = list(range(nd, nd + nf))
+    xanc = list(range(nd + nf, nd + 2 * nf))
+    inj = nd + 2 * nf
+    chk = inj + 1
+    flg = list(range(chk + 1, chk + 1 + flags))
+    sub0 = [q for q, (r, c) in enumerate(sites) if (r + c) % 3 == 0]
+    sub2 = [q for q, (r, c) in enumerate(sites) if (r + c) % 3 == 2]
+    P = _Patch(data, faces, zanc, xanc, sub0, sub2)
+    return sites, P, inj, chk, flg, data + zanc + xanc + [inj, chk] + flg
+
+
+def msc_circuit(d: int = 5, *, checks: int | None = None, flags: int | None = None,
+                final_observable: bool = True, rounds_after_injection: int = 1):
+    """Noiseless MSC-like cultivation proxy of distance ``d`` (3 or 5), all
+    checks at the final distance.
+
+    Defaults: d=3 -> 1 full check + final half-check on 15 qubits
+    (22 T, T-depth 4 as in Table 2); d=5 -> 2 full checks + final
+    half-check on 42 qubits (19 data, 9+9 check ancillas, injection, check
+    and 3 flag qubits; 96 T, T-depth 6).  See ``msc_grown_circuit`` for the
+    d=3 -> d=5 growth variant with Table 2's 72 T.
+    """
+    if checks is None:
+        checks = 1 if d == 3 else 2
+    if flags is None:
+        flags = 0 if d == 3 else 3
+    sites, P, inj, chk, flg, allq = _layout(d, flags)
+    b = _Builder()
+    g = _Cultivation(b, chk, flg)
+    g.prepare_plus(P, allq)
+    g.inject(P, inj)
     for _ in range(rounds_after_injection):
-        z_round(detect=True)
-        x_round(detect=True)
-    # --- cultivation checks
+        g.z_round(P, detect=True)
+        g.x_round(P, detect=True)
     for _ in range(checks):
-        t_layer(undo=False)
-        x_parity(observable=False)
-        t_layer(undo=True)
-        z_round(detect=True)
-        x_round(detect=True)
-    # --- final half-check: the observable
+        g.check(P)
     if final_observable:
-        t_layer(undo=False)
-        x_parity(observable=True)
+        g.final(P)
+    return parse_circuit("\n".join(b.lines) + "\n")
+
+
+def _grown_init(sites, inner_rows: int):
+    """|0> / |+> pattern of the data qubits added by the growth.
+
+    The d_to logical pair is kept as Z_L = Z on the left boundary (c == 0)
+    and X_L = X on the diagonal boundary (c == r); both restrict to logicals
+    of the inner patch, so new qubits on the left boundary start in |0>, on
+    the diagonal in |+>.  The others are split so that as many grown faces
+    as possible have a deterministic first outcome (Z faces whose new qubits
+    are all |0>, X faces whose new qubits are all |+>)."""
+    new = [q for q, (r, c) in enumerate(sites) if r >= inner_rows]
+    fixed0 = {q for q in new if sites[q][1] == 0}
+    fixedp = {q for q in new if sites[q][0] == sites[q][1]}
+    return new, fixed0, fixedp
+
+
+def msc_grown_circuit(d: int = 5, *, d_inner: int = 3, inner_checks: int = 1,
+                      checks: int = 1, flags: int = 3,
+                      rounds_after_injection: int = 1, rounds_after_growth: int = 1,
+                      final_observable: bool = True):
+    """MSC proxy with the paper's injection -> cultivate at d=3 -> grow to
+    d=5 -> cultivate structure (Table 2 d=5: 42 qubits,
+    72 T, T-depth 6 = 1 injection T + 2 layers x 7 + 3 layers x 19).
+
+    The inner d_inner patch is the top corner (rows < 3(d_inner-1)/2+1) of
+    the distance-d triangle, so it reuses the first data qubits and the
+    corner faces.  Growth: the new data qubits start in |0> or |+>
+    (``_grown_init``), one Z and one X round of every distance-d face
+    follows, faces with a deterministic outcome get DETECTORs and every
+    other face is fixed to +1 by Pauli-frame feedback on a pure error that
+    commutes with the kept logical pair -- the logical state of the inner
+    patch is carried over exactly (Z_L and X_L commute with every measured
+    face).  Noiselessly every detector and the observable are
+    deterministic (tested).
+    """
+    sites, P, inj, chk, flg, allq = _layout(d, flags)
+    inner_rows = 3 * (d_inner - 1) // 2 + 1
+    isites, ifaces = color_code_patch(d_inner)
+    assert sites[:len(isites)] == isites
+    ni = len(isites)
+    # inner faces = outer faces whose centre lies in the corner, restricted
+    # to inner data (same order as color_code_patch(d_inner))
+    outer_of = []
+    for f, face in enumerate(P.faces):
+        inner = [q for q in face if q < ni]
+        if inner and sorted(inner) in [sorted(x) for x in ifaces]:
+            outer_of.append((ifaces.index(sorted(inner)), f))
+    outer_of.sort()
+    assert [i for i, _ in outer_of] == list(range(len(ifaces)))
+    Pi = _Patch(list(range(ni)), ifaces, [P.zanc[f] for _, f in outer_of],
+                [P.xanc[f] for _, f in outer_of],
+                [q for q in P.sub0 if q < ni], [q for q in P.sub2 if q < ni])
+    b = _Builder()
+    g = _Cultivation(b, chk, flg)
+    # --- inner stage: prepare, inject, cultivate at d_inner
+    g.prepare_plus(Pi, allq)
+    g.inject(Pi, inj)
+    for _ in range(rounds_after_injection):
+        g.z_round(Pi, detect=True)
+        g.x_round(Pi, detect=True)
+    for _ in range(inner_checks):
+        g.check(Pi)
+    # --- growth to distance d
+    new, zero, plus = _grown_init(sites, inner_rows)
+    free = [q for q in new if q not in zero and q not in plus]
+    # a grown face is deterministic only if its inner part is empty or an
+    # inner face (a stabilizer of the inner code)
+    inner_ok = [not [q for q in face if q < ni] or
+                sorted(q for q in face if q < ni) in [sorted(x) for x in ifaces]
+                for face in P.faces]
+    best = None
+    for m in range(1 << len(free)):
+        z_ = zero | {q for i, q in enumerate(free) if not m >> i & 1}
+        p_ = plus | {q for i, q in enumerate(free) if m >> i & 1}
+        zdet = [f for f, face in enumerate(P.faces)
+                if inner_ok[f] and all(q in z_ for q in face if q >= ni)]
+        xdet = [f for f, face in enumerate(P.faces)
+                if inner_ok[f] and all(q in p_ for q in face if q >= ni)]
+        key = len(zdet) + len(xdet)
+        if best is None or key > best[0]:
+            best = (key, sorted(p_), zdet, xdet)
+    _, plus_q, zdet, xdet = best
+    if plus_q:
+        b.op("H " + " ".join(map(str, plus_q)))
+        b.tick()
+    zm = g.z_round(P, detect=set(zdet))
+    xm = g.x_round(P, detect=set(xdet))
+    nd = len(P.data)
+    left = [q for q in P.data if sites[q][1] == 0]
+    diag = [q for q in P.data if sites[q][0] == sites[q][1]]
+    # pure errors that also commute with the kept logical representative
+    xerr = _pure_errors(nd, P.faces + [left])[:len(P.faces)]
+    zerr = _pure_errors(nd, P.faces + [diag])[:len(P.faces)]
+    for f in range(len(P.faces)):
+        if f not in zdet:
+            for q in xerr[f]:
+                b.op("X %s %d" % (b.rec(zm[f]), q))
+        if f not in xdet:
+            for q in zerr[f]:
+                b.op("Z %s %d" % (b.rec(xm[f]), q))
+    b.tick()
+    for _ in range(rounds_after_growth):
+        g.z_round(P, detect=True)
+        g.x_round(P, detect=True)
+    # --- cultivation at distance d
+    for _ in range(checks):
+        g.check(P)
+    if final_observable:
+        g.final(P)
     return parse_circuit("\n".join(b.lines) + "\n")
 
 

@@ -2,7 +2,8 @@
 reference-generated records), config 4 chi-growth stress with capacity tiers
 (overflow statuses bit-exact vs the oracle), and statistical parity of
 discard / logical-error rates on the d=3 and d=5 MSC proxies
-(Philox GPU stream vs SplitMix oracle stream, binomial CIs)."""
+(Philox GPU stream vs SplitMix oracle stream, binomial CIs), and the
+headline MSC workloads' 20,000 reference-generated shots bit-exact."""
 
 import math
 import os
@@ -99,3 +100,38 @@ def test_d5_full_size_properties():
         warps_per_block=2, blocks=300))
     assert int(c[_lib.GS_C_PRESERVED]) == a.preserved_shots
     assert int(c[_lib.GS_C_ERROR_SHOTS]) == a.logical_error_shots
+
+
+@pytest.mark.parametrize("name", ["msc_d5_records.npz", "msc_d3_records.npz"])
+def test_msc_golden_records_bit_exact(name):
+    """Headline workloads: every one of the 20,000 reference-generated shots
+    (statuses, discarding detector, observable, record bits) bit-exact."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", name))
+    prog = parse_circuit(str(g["text"]))
+    shots = len(g["status"])
+    b = sample(prog, SamplerConfig(shots=shots, master_seed=int(g["master"]),
+                                   postselect=True))
+    assert np.array_equal(b.status, g["status"])
+    m = int(g["num_measurements"])
+    want = np.unpackbits(g["records"], axis=1, bitorder="little")[:, :m]
+    assert np.array_equal(b.record_bits(), want)
+    disc = g["status"] == 2
+    assert np.array_equal(np.asarray(b.aux)[disc], g["detector"][disc])
+    pres = g["status"] == 1
+    assert list(b.obs_keys) == [0]
+    got_obs = (np.asarray(b.obs_bits).astype(np.uint64) & np.uint64(1)).astype(np.uint8)
+    assert np.array_equal(got_obs[pres], g["observable"][pres])
+
+
+def test_grown_d5_statistics_match_oracle():
+    from paper_2512_23037_b200.msc import msc_grown_circuit
+    prog = apply_noise_model(msc_grown_circuit(5), 1e-3)
+    gpu = run_batch(prog, SamplerConfig(shots=1 << 20, master_seed=3,
+                                        postselect=True, rng="philox"))
+    cpu = orc.run_counters_parallel(prog, 1600, os.cpu_count() or 1,
+                                    master_seed=11, mode="splitmix",
+                                    postselect=True)
+    assert _z(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
+              cpu["total"]) < 4.5
+    assert _z(gpu.logical_error_shots, gpu.preserved_shots,
+              cpu["error_shots"], max(cpu["preserved"], 1)) < 4.5

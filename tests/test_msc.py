@@ -1,0 +1,87 @@
+"""The MSC workloads (paper_2512_23037_b200/msc.py) on CPU: circuit shape
+against PAPER.md Table 2, noiseless determinism of every detector and the
+observable (oracle), and the oracle against the reference-generated golden
+records of the headline workloads (tests/golden/make_golden_msc.py)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import gstab_oracle as orc
+from paper_2512_23037_b200.circuit import compute_stats, parse_circuit
+from paper_2512_23037_b200.msc import msc_circuit, msc_grown_circuit
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_grown_d5_matches_table2_t_budget():
+    st = compute_stats(msc_grown_circuit(5)).as_dict()
+    # PAPER.md Table 2 (d=5): 42 qubits, 72 T/T_DAG, T-depth 6
+    assert st["total_qubits"] == 42
+    assert st["t_count"] == 72
+    assert st["t_depth"] == 6
+    assert st["t_support_size"] == 20      # 19 data + injection ancilla
+
+
+@pytest.mark.parametrize("make", [lambda: msc_grown_circuit(5),
+                                  lambda: msc_circuit(3)])
+def test_noiseless_deterministic(make):
+    prog = make()
+    flat = list(prog.flat())
+    for s in range(24):
+        r = orc.run_one_shot(flat, prog.num_qubits,
+                             orc.DrawStream("splitmix", 5, s), 4096, True)
+        assert r["status"] == "preserved", (s, r["discarded_detector"])
+        assert not any(r["observables"].values()), s
+
+
+def test_grown_d5_chi_peaks_at_theorem2_bound():
+    """|v| reaches 1024 = 2^(19-9) in the d=5 check and
+    the growth itself keeps |v| at 2 (the inner |T_L> is carried over)."""
+    prog = msc_grown_circuit(5)
+    flat = list(prog.flat())
+    t_idx = [i for i, ins in enumerate(flat) if ins.name in ("T", "T_DAG")]
+    # the d=5 check's first layer ends at the 4th T instruction after the
+    # inner stage (injection 1 + inner check 2 layers x 2 instructions)
+    peak = 0
+    for stop in t_idx:
+        r = orc.run_one_shot(flat, prog.num_qubits, orc.DrawStream("splitmix", 1, 0),
+                             4096, True, stop_after=stop, snapshot=True)
+        peak = max(peak, len(r["state"]["idx"]))
+    assert peak == 1024
+
+
+def _golden(name):
+    return np.load(os.path.join(GOLDEN, name))
+
+
+@pytest.mark.parametrize("name,n", [("msc_d5_records.npz", 120),
+                                    ("msc_d3_records.npz", 600)])
+def test_oracle_reproduces_reference_msc_records(name, n):
+    g = _golden(name)
+    prog = parse_circuit(str(g["text"]))
+    flat = list(prog.flat())
+    m = int(g["num_measurements"])
+    want = np.unpackbits(g["records"][:n], axis=1, bitorder="little")[:, :m]
+    code = {"preserved": 1, "discarded": 2, "overflow": 3}
+    for s in range(n):
+        r = orc.run_one_shot(flat, prog.num_qubits,
+                             orc.DrawStream("splitmix", int(g["master"]), s), 4096, True)
+        assert code[r["status"]] == g["status"][s], s
+        rec = np.zeros(m, dtype=np.uint8)
+        rec[:len(r["record"])] = r["record"]
+        assert np.array_equal(rec, want[s]), s
+        if r["status"] == "discarded":
+            assert r["discarded_detector"] == g["detector"][s]
+        if r["status"] == "preserved":
+            assert int(bool(r["observables"].get(0, 0))) == g["observable"][s]
+
+
+def test_golden_texts_are_the_generators_output():
+    """The committed golden circuits are exactly what msc.py emits today."""
+    from paper_2512_23037_b200.noise import apply_noise_model
+    assert str(_golden("msc_d5_records.npz")["text"]) == \
+        apply_noise_model(msc_grown_circuit(5), 1e-3).serialize()
+    assert str(_golden("msc_d3_records.npz")["text"]) == \
+        apply_noise_model(msc_circuit(3), 1e-3).serialize()
