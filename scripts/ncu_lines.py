@@ -1,0 +1,103 @@
+"""Attribute ncu SASS-level samples / executed instructions to CUDA source
+lines: ncu's source page (SASS view, csv) of the captured kernel is matched
+by instruction offset against ``nvdisasm -g`` of the locally built cubin
+(same source + nvcc => same SASS; checked by comparing opcodes).
+
+    ncu -i prof.ncu-rep --page source --csv --print-source sass > sass.csv
+    python scripts/ncu_lines.py sass.csv [lib.so] [top]
+"""
+import csv
+import os
+import re
+import subprocess
+import sys
+import tempfile
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def disasm(lib, kernel_regex):
+    tmp = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, check=True,
+                   capture_output=True)
+    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
+    out = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)],
+                         capture_output=True, text=True).stdout
+    lines = out.splitlines()
+    m = {}
+    cur_line = None
+    inside = False
+    for ln in lines:
+        if ln.startswith("//---") and ".text." in ln:
+            inside = re.search(kernel_regex, ln) is not None
+            continue
+        if not inside:
+            continue
+        if ln.strip().startswith("//##"):
+            # innermost-first chain "line A inlined at ... line B": keep the
+            # outermost call site (the kernel body line)
+            nums = re.findall(r'line (\d+)', ln)
+            if nums:
+                cur_line = int(nums[-1])
+            continue
+        g = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
+        if g:
+            m[int(g.group(1), 16)] = (cur_line, g.group(2).split()[0] if g.group(2) else "")
+    return m
+
+
+def main():
+    path = sys.argv[1]
+    lib = os.path.abspath(sys.argv[2]) if len(sys.argv) > 2 else os.path.join(
+        ROOT, "paper_2512_23037_b200", "libgstab_sm100a.so")
+    top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    h = rows[hi]
+    data = [r for r in rows[hi + 1:] if len(r) == len(h)]
+    iA, iS, iE = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), \
+        h.index("Instructions Executed")
+    base = int(data[0][iA], 16)
+    m = disasm(lib, r"sample_kernelILb0E")
+    by_line_s, by_line_e = defaultdict(float), defaultdict(float)
+    mism = 0
+    for r in data:
+        off = int(r[iA], 16) - base
+        line, op = m.get(off, (None, None))
+        src_op = r[h.index("Source")].split()[0] if r[h.index("Source")].split() else ""
+        if op and src_op and op.split(".")[0] != src_op.split(".")[0] and not src_op.startswith("@"):
+            mism += 1
+        by_line_s[line] += float(r[iS] or 0)
+        by_line_e[line] += float(r[iE] or 0)
+    ts, te = sum(by_line_s.values()), sum(by_line_e.values())
+    print("instructions %d, opcode mismatches %d, samples %.0f, warp-instr %.3g" %
+          (len(data), mism, ts, te))
+    regions = [(1, 299, "prologue/helpers"), (300, 328, "shot setup"),
+               (329, 330, "op loop"), (331, 447, "noise scan+apply"),
+               (448, 458, "op dispatch"), (459, 490, "T diag/preamble"),
+               (491, 545, "T grow-limit/sparse"), (546, 584, "T dense merge"),
+               (586, 609, "meas preamble"), (610, 650, "meas det small"),
+               (651, 687, "meas det sparse"), (688, 735, "meas det dense"),
+               (736, 793, "meas pivot small"), (794, 838, "meas pivot sparse"),
+               (839, 915, "meas pivot dense"), (916, 934, "meas epilogue"),
+               (935, 975, "feedback/detector/obs/end"), (976, 1032, "shot outputs")]
+    agg_s, agg_e = defaultdict(float), defaultdict(float)
+    for line in by_line_s:
+        name = "?"
+        for a, b, nm in regions:
+            if line and a <= line <= b:
+                name = nm
+        agg_s[name] += by_line_s[line]
+        agg_e[name] += by_line_e[line]
+    for nm in sorted(agg_s, key=lambda k: -agg_s[k]):
+        print("%-28s %6.2f%% samp %6.2f%% inst" % (nm, 100 * agg_s[nm] / ts, 100 * agg_e[nm] / te))
+    src = open(os.path.join(ROOT, "paper_2512_23037_b200", "csrc", "gs_kernels.cu")).read().splitlines()
+    for line in sorted(by_line_s, key=lambda k: -by_line_s[k])[:top]:
+        txt = src[line - 1].strip()[:80] if line else "?"
+        print("%5s %6.2f%% samp %6.2f%% inst  %s" % (line, 100 * by_line_s[line] / ts,
+                                                     100 * by_line_e[line] / te, txt))
+
+
+if __name__ == "__main__":
+    main()
