@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 /* error codes */
 #define GS_OK 0
@@ -83,6 +83,13 @@ typedef struct {
   uint32_t num_words;        /* ceil(num_locations / 32)                 */
   uint64_t noise_off;        /* tables offset: 4 words per noise instr.  */
   uint64_t wordpc_off;       /* tables offset: insertion pc per word     */
+  /* Philox mode: fired noise locations come from geometric skipping over a
+     Bernoulli(p_max) candidate process (thinned to each location's p) */
+  uint64_t geo_off;          /* tables offset: gap table T[0..geo_len)   */
+  uint32_t geo_len;          /* num_locations of the full program + 1    */
+  uint32_t noise_uniform;    /* 1: every location has p == p_max        */
+  uint64_t acc_off;          /* tables offset: per-location thinning
+                                thresholds (used when !noise_uniform)    */
 } gs_program_info;
 
 typedef struct {

@@ -50,7 +50,9 @@ class GsProgramInfo(ct.Structure):
                 ("num_detectors", ct.c_uint32), ("num_obs", ct.c_uint32),
                 ("max_dim", ct.c_uint32), ("num_locations", ct.c_uint32),
                 ("num_noise", ct.c_uint32), ("num_words", ct.c_uint32),
-                ("noise_off", ct.c_uint64), ("wordpc_off", ct.c_uint64)]
+                ("noise_off", ct.c_uint64), ("wordpc_off", ct.c_uint64),
+                ("geo_off", ct.c_uint64), ("geo_len", ct.c_uint32),
+                ("noise_uniform", ct.c_uint32), ("acc_off", ct.c_uint64)]
 
 
 class GsRunParams(ct.Structure):

@@ -93,6 +93,19 @@ def _threshold(p: float) -> int:
     return int(math.ceil(x))
 
 
+def geo_table(p_max: float, nlocs: int):
+    """T[g] = ceil((1-p_max)^g * 2^53), g = 0..nlocs.  In Philox mode the gap
+    between consecutive candidate noise locations is max{g : m < T[g]} for a
+    53-bit draw m, i.e. P(gap >= g) = (1-p_max)^g (geometric skipping of a
+    Bernoulli(p_max) process over the locations)."""
+    q = 1.0 - p_max
+    out = []
+    for g in range(nlocs + 1):
+        x = (q ** g) * 9007199254740992.0
+        out.append(1 << 53 if x >= 9007199254740992.0 else int(math.ceil(x)))
+    return out
+
+
 def t_coefficients(dagger: bool):
     """T = a*I + b*Z on the branch basis, built with the reference's exact
     Python expressions so the constants are bit-identical
@@ -307,6 +320,11 @@ class DeviceProgram:
     num_noise: int = 0
     wordpc_off: int = 0      # tables offset of the per-word insertion pcs
     num_words: int = 0
+    geo_off: int = 0         # tables offset of the geometric gap table
+    geo_len: int = 1         # its length (locations of the whole program + 1)
+    noise_uniform: int = 1   # every location has p == p_max (no thinning)
+    acc_off: int = 0         # tables offset of per-location p/p_max thresholds
+    p_max: float = 0.0
 
     @property
     def nbytes(self) -> int:
@@ -532,7 +550,16 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         # `insert_pc` (the next op emitted)
         noise_ops.append((len(em.ops), nloc, loc0, qmask, off, instr))
 
-    flat = prog.flat()
+    flat = list(prog.flat())
+    # Philox-mode fire schedule constants over the WHOLE program (a
+    # truncated compile must draw the same schedule): p_max and the number
+    # of noise locations fix the geometric gap table
+    loc_ps = []
+    for ins in flat:
+        if ins.name in NOISE_OPS:
+            cnt_ = len(ins.targets) // 2 if ins.name == "DEPOLARIZE2" else len(ins.targets)
+            loc_ps += [float(ins.args[0])] * cnt_
+    p_max = max(loc_ps) if loc_ps else 0.0
     for i, ins in enumerate(flat):
         name = ins.name
         if name in ("TICK", "QUBIT_COORDS", "SHIFT_COORDS"):
@@ -623,6 +650,16 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         while noise_ops[m][2] + noise_ops[m][1] <= l:
             m += 1
         em.tables.append(noise_ops[m][0])
+    # geometric gap table for p_max (Philox mode) and, when the locations'
+    # probabilities differ, per-location thinning thresholds p / p_max
+    geo_off = len(em.tables)
+    geo = geo_table(p_max, len(loc_ps)) if p_max > 0.0 else [1 << 53]
+    em.tables += geo
+    noise_uniform = int(all(q == p_max for q in loc_ps))
+    acc_off = 0
+    if not noise_uniform:
+        acc_off = len(em.tables)
+        em.tables += [_threshold(q / p_max) for q in loc_ps[:nloc_total]]
     return DeviceProgram(
         num_qubits=n, num_measurements=meas, num_detectors=det_ordinal,
         obs_keys=obs_keys, max_dim=max_k, num_locations=len(em.locs) // 2,
@@ -633,7 +670,8 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         op_instr=em.op_instr, basis_after=basis_after, xz_after=xz_after,
         truncated_at=truncated, static_sign_bytes=total_static_sign,
         noise_off=noise_off, num_noise=len(noise_ops), wordpc_off=wordpc_off,
-        num_words=(nloc_total + 31) // 32)
+        num_words=(nloc_total + 31) // 32, geo_off=geo_off, geo_len=len(geo),
+        noise_uniform=noise_uniform, acc_off=acc_off, p_max=p_max)
 
 
 def decode_header(w: int):

@@ -55,6 +55,8 @@ struct DevProg {
   u32 n, nmeas, max_dim, nobs, rec_words32, nlocs;
   u32 nnoise, nwords;
   u64 noise_off, wordpc_off;
+  u64 geo_off, acc_off;   // Philox fire schedule: gap table, thinning table
+  u32 geo_len, noise_uniform;
 };
 
 struct DevRun {
@@ -198,8 +200,9 @@ __device__ __forceinline__ u64 splitmix(u64 seed, u32 k) {
   return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ u64 philox_u64(u64 master, u64 shot, u32 k) {
-  u32 c0 = k >> 1, c1 = 0, c2 = (u32)shot, c3 = (u32)(shot >> 32);
+// Philox4x32-10, key = master seed, counter = (c0, c1, shot lo, shot hi)
+__device__ __forceinline__ uint4 philox4(u32 c0, u32 c1, u64 shot, u64 master) {
+  u32 c2 = (u32)shot, c3 = (u32)(shot >> 32);
   u32 k0 = (u32)master, k1 = (u32)(master >> 32);
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
@@ -209,7 +212,42 @@ __device__ __forceinline__ u64 philox_u64(u64 master, u64 shot, u32 k) {
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
     k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
   }
-  return (k & 1u) ? (((u64)c3 << 32) | c2) : (((u64)c1 << 32) | c0);
+  return make_uint4(c0, c1, c2, c3);
+}
+
+// static draw k (measurements, MPP flips): block (k>>1, 0, shot), even k
+// takes words (0,1), odd k words (2,3)
+__device__ __forceinline__ u64 philox_u64(u64 master, u64 shot, u32 k) {
+  const uint4 x = philox4(k >> 1, 0u, shot, master);
+  return (k & 1u) ? (((u64)x.w << 32) | x.z) : (((u64)x.y << 32) | x.x);
+}
+
+// Philox-mode noise: candidate j of the shot's Bernoulli(p_max) location
+// process (oracle GeoNoise).  Block (j, 1, shot): words 0-1 >> 11 = gap draw
+// m, words 2-3 >> 11 = letter pick; gap = max{g : m < T[g]} (binary search
+// of the host gap table); the candidate sits at start + gap.
+struct GeoCand {
+  u64 pick;
+  u32 pos;
+};
+__device__ __noinline__ GeoCand geo_candidate(const u64 *__restrict__ T, u32 tlen,
+                                              u64 master, u64 shot, u32 j, u32 start) {
+  const uint4 x = philox4(j, 1u, shot, master);
+  const u64 m = ((((u64)x.y) << 32) | x.x) >> 11;
+  GeoCand c;
+  c.pick = ((((u64)x.w) << 32) | x.z) >> 11;
+  u32 lo = 0, hi = tlen - 1;
+  while (lo < hi) {
+    const u32 mid = (lo + hi + 1) >> 1;
+    if (m < __ldg(T + mid)) lo = mid; else hi = mid - 1;
+  }
+  c.pos = start + lo;
+  return c;
+}
+// thinning of candidate j at a location with p < p_max: block (j, 2, shot)
+__device__ __noinline__ bool geo_accept(u64 master, u64 shot, u32 j, u64 thr) {
+  const uint4 x = philox4(j, 2u, shot, master);
+  return (((((u64)x.y) << 32) | x.x) >> 11) < thr;
 }
 
 __device__ __noinline__ u64 draw53(u64 seed, u64 master, u64 shot, u32 k, bool philox) {
@@ -324,80 +362,30 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
     // the ring `win`; locations < cursor are consumed
     u32 scanned = 0, search_w = 0, cursor = 0, fire_pc = 0xFFFFFFFFu;
     u32 next_word_pc = P.nwords ? (u32)__ldg(tables + P.wordpc_off) : 0xFFFFFFFFu;
+    // Philox mode: geometric fire schedule instead of the per-word scan
+    const bool geo = rng.philox;
+    u32 gj = 0, gpos = 0xFFFFFFFFu;
+    u64 gpick = 0;
+    if (geo) {
+      next_word_pc = 0xFFFFFFFFu;
+      if (P.geo_len > 1 && P.nlocs) {
+        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, rng.master, shot, 0u, 0u);
+        gpos = gc.pos;
+        gpick = gc.pick;
+        gj = 1;
+      }
+      fire_pc = gpos < P.nlocs ? 0u : 0xFFFFFFFFu;   // resolved at the first op
+    }
     u64 hnext = __ldg(ops);
 
     while (status == ST_RUNNING) {
       // ---- noise instructions inserted before this op (only fired ones)
-      if (pc >= next_word_pc || pc == fire_pc) {
-        while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= pc) {
-          // one fire draw per location of word `scanned`, one lane each
-          const u32 l = scanned * 32u + lane;
-          bool fire = false;
-          if (l < P.nlocs) {
-            const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
-            fire = rng.m53((u32)lw) < thr;
-          }
-          const u32 bits = __ballot_sync(FULL, fire);
-          if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
-          ++scanned;
-        }
-        __syncwarp();
-        next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
-        fire_pc = 0xFFFFFFFFu;
-        for (;;) {
-          // next fired location >= cursor among the scanned words
-          u32 fl_loc = 0xFFFFFFFFu;
-          u32 w = max(search_w, cursor >> 5);
-          for (; w < scanned; ++w) {
-            u32 bits = win[w & (kWinWords - 1)];
-            if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
-            if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
-          }
-          search_w = w;
-          if (fl_loc == 0xFFFFFFFFu) break;
-          // owning noise instruction: last m with loc0(m) <= fl_loc
-          u32 lo = 0, hi = P.nnoise;
-          while (hi - lo > 1) {
-            const u32 mid = (lo + hi) >> 1;
-            if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= fl_loc) lo = mid; else hi = mid;
-          }
-          const u64 *nrec = tables + P.noise_off + 4ull * lo;
-          const u64 nw0 = __ldg(nrec);
-          const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-          if (ipc > pc) { fire_pc = ipc; break; }
-          const u32 loc0 = (u32)__ldg(nrec + 1);
-          const u64 qmask = __ldg(nrec + 2);
-          const u64 off = __ldg(nrec + 3);
-          cursor = loc0 + nloc;
-          // build E = OR of fired letters (ref noise.py:68-100)
-          u64 ex = 0, ez = 0;
-          for (u32 i = lane; i < nloc; i += 32) {
-            const u32 l = loc0 + i;
-            if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
-            const u64 lw = __ldg(locs + 2ull * l);
-            const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
-                      qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
-            if (nk == NK_DEP1) {
-              int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
-              code = code > 3 ? 3 : code;
-              ex |= (u64)(code != 3) << qa;
-              ez |= (u64)(code != 1) << qa;
-            } else if (nk == NK_DEP2) {
-              int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
-              pick = pick > 15 ? 15 : pick;
-              const int ca = pick & 3, cbq = pick >> 2;
-              if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
-              if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
-            } else if (nk == NK_XERR) {
-              ex |= 1ull << qa;
-            } else {
-              ez |= 1ull << qa;
-            }
-          }
-          ex = warp_or64(ex);
-          ez = warp_or64(ez);
+      if (pc >= next_word_pc || pc >= fire_pc) {
+        // E = OR of the fired letters of one noise instruction applied to the
+        // state (ref noise.py:68-100, state.py:88-102)
+        auto apply_error = [&](u64 ex, u64 ez, u64 qmask, u64 off) {
           const u64 eall = ex | ez;
-          if (!eall) continue;
+          if (!eall) return;
           // compose the action of E letter by letter
           u64 beta = 0, delt = 0;
           u32 xi = 0, dm = 0;
@@ -443,6 +431,121 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           __syncwarp();
           c ^= beta;
           mbytes += 2ull * kEntryBytes * cnt + 2ull * ((2 * n + 7) / 8);
+        };
+        // owning noise instruction of location l: last m with loc0(m) <= l
+        auto owner = [&](u32 l) -> const u64 * {
+          u32 lo = 0, hi = P.nnoise;
+          while (hi - lo > 1) {
+            const u32 mid = (lo + hi) >> 1;
+            if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= l) lo = mid; else hi = mid;
+          }
+          return tables + P.noise_off + 4ull * lo;
+        };
+        if (geo) {
+          // Philox: walk the candidate schedule (lane-uniform, rare)
+          fire_pc = 0xFFFFFFFFu;
+          while (gpos < P.nlocs) {
+            const u64 *nrec = owner(gpos);
+            const u64 nw0 = __ldg(nrec);
+            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+            if (ipc > pc) { fire_pc = ipc; break; }
+            const u32 loc0 = (u32)__ldg(nrec + 1);
+            u64 ex = 0, ez = 0;
+            while (gpos < loc0 + nloc) {
+              const u32 l = gpos;
+              bool ok = true;
+              if (!P.noise_uniform) ok = geo_accept(rng.master, shot, gj - 1, __ldg(tables + P.acc_off + l));
+              if (ok) {
+                const u64 lw = __ldg(locs + 2ull * l);
+                const u32 qa = (u32)(lw >> 32) & 0xff, qb = (u32)(lw >> 40) & 0xff,
+                          nk = (u32)(lw >> 48) & 3;
+                const double u = (double)gpick * 0x1.0p-53;
+                if (nk == NK_DEP1) {
+                  int code = 1 + (int)(u * 3.0);
+                  code = code > 3 ? 3 : code;
+                  ex |= (u64)(code != 3) << qa;
+                  ez |= (u64)(code != 1) << qa;
+                } else if (nk == NK_DEP2) {
+                  int pick = 1 + (int)(u * 15.0);
+                  pick = pick > 15 ? 15 : pick;
+                  const int ca = pick & 3, cbq = pick >> 2;
+                  if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+                  if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+                } else if (nk == NK_XERR) {
+                  ex |= 1ull << qa;
+                } else {
+                  ez |= 1ull << qa;
+                }
+              }
+              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, rng.master, shot, gj, l + 1);
+              gpos = gc.pos;
+              gpick = gc.pick;
+              ++gj;
+            }
+            apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
+          }
+        } else {
+        while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= pc) {
+          // one fire draw per location of word `scanned`, one lane each
+          const u32 l = scanned * 32u + lane;
+          bool fire = false;
+          if (l < P.nlocs) {
+            const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+            fire = rng.m53((u32)lw) < thr;
+          }
+          const u32 bits = __ballot_sync(FULL, fire);
+          if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+          ++scanned;
+        }
+        __syncwarp();
+        next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
+        fire_pc = 0xFFFFFFFFu;
+        for (;;) {
+          // next fired location >= cursor among the scanned words
+          u32 fl_loc = 0xFFFFFFFFu;
+          u32 w = max(search_w, cursor >> 5);
+          for (; w < scanned; ++w) {
+            u32 bits = win[w & (kWinWords - 1)];
+            if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
+            if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+          }
+          search_w = w;
+          if (fl_loc == 0xFFFFFFFFu) break;
+          const u64 *nrec = owner(fl_loc);
+          const u64 nw0 = __ldg(nrec);
+          const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+          if (ipc > pc) { fire_pc = ipc; break; }
+          const u32 loc0 = (u32)__ldg(nrec + 1);
+          cursor = loc0 + nloc;
+          // build E = OR of fired letters (ref noise.py:68-100)
+          u64 ex = 0, ez = 0;
+          for (u32 i = lane; i < nloc; i += 32) {
+            const u32 l = loc0 + i;
+            if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+            const u64 lw = __ldg(locs + 2ull * l);
+            const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
+                      qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
+            if (nk == NK_DEP1) {
+              int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
+              code = code > 3 ? 3 : code;
+              ex |= (u64)(code != 3) << qa;
+              ez |= (u64)(code != 1) << qa;
+            } else if (nk == NK_DEP2) {
+              int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
+              pick = pick > 15 ? 15 : pick;
+              const int ca = pick & 3, cbq = pick >> 2;
+              if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+              if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+            } else if (nk == NK_XERR) {
+              ex |= 1ull << qa;
+            } else {
+              ez |= 1ull << qa;
+            }
+          }
+          ex = warp_or64(ex);
+          ez = warp_or64(ez);
+          apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
+        }
         }
       }
 
@@ -1158,6 +1261,11 @@ int gs_program_create(const gs_program_info *info, const uint64_t *ops, size_t n
     return fail(GS_ERR_ARG, "noise table out of range");
   if (info->num_words && (!tables || info->wordpc_off + info->num_words > n_tables))
     return fail(GS_ERR_ARG, "word table out of range");
+  if (info->geo_len < 1 || !tables || info->geo_off + info->geo_len > n_tables)
+    return fail(GS_ERR_ARG, "geometric gap table out of range");
+  if (!info->noise_uniform && info->num_locations &&
+      info->acc_off + info->num_locations > n_tables)
+    return fail(GS_ERR_ARG, "thinning table out of range");
   if (info->num_words != (info->num_locations + 31) / 32)
     return fail(GS_ERR_ARG, "num_words must be ceil(num_locations/32)");
   if (n_locs < 2ull * info->num_locations) return fail(GS_ERR_ARG, "locs too short");
@@ -1347,6 +1455,10 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   P.nwords = p->info.num_words;
   P.noise_off = p->info.noise_off;
   P.wordpc_off = p->info.wordpc_off;
+  P.geo_off = p->info.geo_off;
+  P.geo_len = p->info.geo_len;
+  P.acc_off = p->info.acc_off;
+  P.noise_uniform = p->info.noise_uniform;
   gs::DevRun R;
   R.master = r->master_seed;
   R.shot_begin = r->shot_begin;

@@ -30,7 +30,8 @@ class Program:
                                   dp.num_detectors, len(dp.obs_keys),
                                   dp.max_dim, dp.num_locations,
                                   dp.num_noise, dp.num_words, dp.noise_off,
-                                  dp.wordpc_off)
+                                  dp.wordpc_off, dp.geo_off, dp.geo_len,
+                                  dp.noise_uniform, dp.acc_off)
         self._ops = np.ascontiguousarray(dp.ops, dtype=np.uint64)
         self._tables = np.ascontiguousarray(dp.tables, dtype=np.uint64)
         self._locs = np.ascontiguousarray(dp.locs, dtype=np.uint64)

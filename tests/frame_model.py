@@ -12,7 +12,7 @@ import math
 
 import numpy as np
 
-from oracle.gstab_oracle import M64, philox_u64, sha1_seed, splitmix_u64
+from oracle.gstab_oracle import M64, philox4x32_10, philox_u64, sha1_seed, splitmix_u64
 from paper_2512_23037_b200 import compiler as C
 
 I_POW = (1.0 + 0.0j, 1.0j, -1.0 + 0.0j, -1.0j)
@@ -45,11 +45,14 @@ def _f64(w: int) -> float:
 
 
 class Draws:
-    def __init__(self, mode, master, shot, seed=None):
+    def __init__(self, mode, master, shot, seed=None, dp=None):
         self.mode = mode
         self.master = master & M64
         self.shot = shot & M64
         self.seed = sha1_seed(master, shot) if seed is None else seed
+        self.geo = None
+        if mode == "philox" and dp is not None:
+            self.geo = _Geo(dp, self.master, self.shot)
 
     def m53(self, k: int) -> int:
         if self.mode == "philox":
@@ -60,6 +63,54 @@ class Draws:
         return self.m53(k) * (2.0 ** -53)
 
 
+class _Geo:
+    """Philox-mode fire schedule read from the compiled tables (gap table
+    at geo_off, thinning thresholds at acc_off) -- the device's algorithm."""
+
+    def __init__(self, dp, master, shot):
+        t = dp.tables
+        self.T = [int(w) for w in t[dp.geo_off: dp.geo_off + dp.geo_len]]
+        self.acc = None if dp.noise_uniform else [int(w) for w in t[dp.acc_off: dp.acc_off + dp.num_locations]]
+        self.key = (master & 0xFFFFFFFF, master >> 32)
+        self.shot = shot
+        self.j = 0
+        self.pos = -1
+        self.on = dp.p_max > 0.0
+        self._adv(-1)
+
+    def _blk(self, j, s):
+        return philox4x32_10((j & 0xFFFFFFFF, s, self.shot & 0xFFFFFFFF, self.shot >> 32), self.key)
+
+    def _adv(self, prev):
+        if not self.on:
+            self.pos = 1 << 62
+            return
+        x = self._blk(self.j, 1)
+        m = (x[0] | (x[1] << 32)) >> 11
+        self.pick = (x[2] | (x[3] << 32)) >> 11
+        lo, hi = 0, len(self.T) - 1
+        while lo < hi:
+            mid = (lo + hi + 1) >> 1
+            if m < self.T[mid]:
+                lo = mid
+            else:
+                hi = mid - 1
+        self.cand = self.j
+        self.j += 1
+        self.pos = prev + 1 + lo
+
+    def at(self, loc):
+        if self.pos != loc:
+            return False, 0
+        j, pick = self.cand, self.pick
+        self._adv(loc)
+        if self.acc is not None:
+            x = self._blk(j, 2)
+            if ((x[0] | (x[1] << 32)) >> 11) >= self.acc[loc]:
+                return False, 0
+        return True, pick
+
+
 def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
              want_state=False):
     ops = [int(w) for w in dp.ops]
@@ -67,7 +118,7 @@ def run_shot(dp, mode, master, shot, capacity, postselect, seed=None,
     locs = [int(w) for w in dp.locs]
     n = dp.num_qubits
     nm = (1 << n) - 1
-    rng = Draws(mode, master, shot, seed)
+    rng = Draws(mode, master, shot, seed, dp)
     noise_at = {}
     for m in range(dp.num_noise):
         w = tables[dp.noise_off + 4 * m: dp.noise_off + 4 * m + 4]
@@ -334,14 +385,21 @@ def _apply_noise(A, size, rng, locs, tables, n, sig, c, loc0, nloc, qmask,
         qa = (w0 >> 32) & 0xFF
         qb = (w0 >> 40) & 0xFF
         nk = (w0 >> 48) & 3
-        if rng.m53(d) >= thr:
-            continue
+        if rng.geo is not None:
+            fired, pick53 = rng.geo.at(l)
+            if not fired:
+                continue
+            u2 = pick53 * (2.0 ** -53)
+        else:
+            if rng.m53(d) >= thr:
+                continue
+            u2 = rng.uniform(d + 1) if nk in (C.NK_DEP1, C.NK_DEP2) else 0.0
         if nk == C.NK_DEP1:
-            code = min(1 + int(rng.uniform(d + 1) * 3), 3)
+            code = min(1 + int(u2 * 3), 3)
             ex |= (code in (1, 2)) << qa
             ez |= (code in (2, 3)) << qa
         elif nk == C.NK_DEP2:
-            pick = min(1 + int(rng.uniform(d + 1) * 15), 15)
+            pick = min(1 + int(u2 * 15), 15)
             for qq, code in ((qa, pick & 3), (qb, pick >> 2)):
                 ex |= (code in (1, 2)) << qq
                 ez |= (code in (2, 3)) << qq
