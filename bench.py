@@ -153,6 +153,7 @@ def main():
     ap.add_argument("--chi-smem", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
     ap.add_argument("--dense-only", action="store_true")
+    ap.add_argument("--wide-only", action="store_true")
     ap.add_argument("--list-cap", type=int, default=0)
     args = ap.parse_args()
 
@@ -213,6 +214,8 @@ def main():
         flags |= _lib.GS_CHI_SMEM
     if args.dense_only:
         flags |= _lib.GS_DENSE_ONLY
+    if args.wide_only:
+        flags |= _lib.GS_WIDE_ONLY
     S = args.shots_per_step
     nc = P.num_counters
     stream = torch.cuda.current_stream()

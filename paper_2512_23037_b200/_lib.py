@@ -20,6 +20,7 @@ GS_RNG_PHILOX = 2
 GS_CHI_GLOBAL = 4
 GS_DENSE_ONLY = 8
 GS_CHI_SMEM = 16
+GS_WIDE_ONLY = 32
 
 GS_C_TOTAL = 0
 GS_C_PRESERVED = 1

@@ -275,6 +275,10 @@ struct Rng {
 // the support; positions >= 2^k are don't-care until a GROW initialises them.
 
 constexpr u32 kLcapMax = 64;    // list storage; sparse ops need cnt <= 32
+#ifndef GS_KN
+#define GS_KN 4u                // narrow (lane-per-shot) chi dimension limit
+#endif
+constexpr u32 kNarrowBytes = (1u << GS_KN) * 32u * 16u;   // An[2^KN][32] double2
 constexpr u32 kSparseMin = 64;    // below this a dense sweep is <= 2 rounds
 
 __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y != 0.0; }
@@ -300,6 +304,24 @@ __device__ void build_list(const double2 *A, u32 *L, u32 size, u32 lane) {
 }
 
 // ---------------------------------------------------------------- kernel
+//
+// Execution model.  A warp takes a BATCH of 32 consecutive shots (one per
+// lane) and walks the static op stream with all lanes at the same pc:
+//
+//  * narrow ops (chi dimension k <= GS_KN before and after the op) run
+//    lane-per-shot: every lane applies the op to its own shot, chi lives in
+//    shared memory as An[j * 32 + lane] (row j uniform across lanes, so
+//    accesses are bank-conflict free) -- the fixed per-op cost (decode,
+//    sign-mask parities, draws) is paid once for 32 shots;
+//  * wide ops (k > GS_KN, and GROW_LIMIT) run warp-per-shot: the warp takes
+//    the live lanes' shots one at a time through the whole wide section
+//    (lanes split the 2^k coordinates, chi in a per-warp buffer) and hands
+//    each surviving shot back at the first narrow op after it.
+//
+// k is static per op (shot-invariant basis, compiler.py), so every shot of
+// the batch enters and leaves a wide section at the same pc.  Shots that
+// end (discarded / preserved / overflow) leave their lane idle until the
+// batch finishes.  GS_WIDE_ONLY runs every op warp-per-shot (A/B, tests).
 
 #ifndef GS_SMALL_MAX
 #define GS_SMALL_MAX 1u   // redundant per-lane path only for one amplitude (A/B: 6.62M vs 5.99M at <=2, 5.73M at <=4)
@@ -307,6 +329,11 @@ __device__ void build_list(const double2 *A, u32 *L, u32 size, u32 lane) {
 #ifndef GS_MIN_BLOCKS
 #define GS_MIN_BLOCKS 4   // 128 registers: 16 resident warps/SM (measured best)
 #endif
+
+__device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
+  return kind == OP_GROW_LIMIT || k > GS_KN ||
+         (kind == OP_T && (fl & 3u) == T_GROW && k + 1 > GS_KN);
+}
 
 template <bool kSmemChi>
 __global__ void __launch_bounds__(128, GS_MIN_BLOCKS)
@@ -319,8 +346,10 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
   u8 *mine = smem + (size_t)wib * O.warp_bytes;
   u32 *win = reinterpret_cast<u32 *>(mine);
   u32 *L = reinterpret_cast<u32 *>(mine + kWinBytes);
-  u32 *rec = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kWinBytes + 4 * kLcapMax)
-                           : O.grec + gw * P.rec_words32;
+  double2 *An = reinterpret_cast<double2 *>(mine + kWinBytes + 4 * kLcapMax);
+  // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
+  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kWinBytes + 4 * kLcapMax + kNarrowBytes)
+                            : O.grec + gw * (u64)P.rec_words32 * 32u;
   double2 *A = kSmemChi ? reinterpret_cast<double2 *>(mine + O.chi_off)
                         : O.gchi + gw * ((u64)1 << P.max_dim);
   const u32 n = P.n;
@@ -329,368 +358,1004 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
   const u32 scap = O.lcap < 32u ? O.lcap : 32u;   // sparse ops: <= 1 entry per lane
+  const bool philox = (R.flags & GS_RNG_PHILOX) != 0;
+  const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
+  const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
+#define AN(j) An[(j) * 32u + lane]
 
   long long n_tot = 0, n_pres = 0, n_disc = 0, n_ovf = 0, n_cor = 0, n_uns = 0,
             n_err = 0;
   unsigned long long mbytes_all = 0;
 
   for (;;) {
-    u64 sl = 0;
-    if (lane == 0) sl = atomicAdd(O.next_shot, 1ull);
-    sl = __shfl_sync(FULL, sl, 0);
-    if (sl >= R.shot_count) break;
+    u64 base = 0;
+    if (lane == 0) base = atomicAdd(O.next_shot, 32ull);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= R.shot_count) break;
+    const u64 sl = base + lane;
+    const bool valid = sl < R.shot_count;
     const u64 shot = R.shot_begin + sl;
-    Rng rng;
-    rng.philox = (R.flags & GS_RNG_PHILOX) != 0;
-    rng.master = R.master;
-    rng.shot = shot;
-    rng.seed = 0;
-    if (!rng.philox) rng.seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
+    u64 seed = 0;
+    if (valid && !philox) seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
+    for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
+    AN(0) = make_double2(1.0, 0.0);
 
-    for (u32 w = lane; w < P.rec_words32; w += 32) rec[w] = 0;
-    if (lane == 0) {
-      A[0] = make_double2(1.0, 0.0);
-      L[0] = 0;
+    // this lane's shot (ref sampler.py:169-255 state: tableau signs, coset
+    // offset, record, observables)
+    u64 s_lo = 0, s_hi = 0, sc = 0, sobs = 0, smb = 0;
+    u32 scnt = 1, sk = 0;
+    int sst = valid ? ST_RUNNING : ST_PRESERVED, saux = -1;
+    bool dumped = false;
+    // Philox fire schedule of this shot
+    u32 sgj = 0, sgpos = 0xFFFFFFFFu, sfire = 0xFFFFFFFFu;
+    u64 sgpick = 0;
+    if (philox && valid && P.geo_len > 1 && P.nlocs) {
+      const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, shot, 0u, 0u);
+      sgpos = gc.pos;
+      sgpick = gc.pick;
+      sgj = 1;
+      sfire = sgpos < P.nlocs ? 0u : 0xFFFFFFFFu;
     }
     __syncwarp();
 
-    u64 sig_lo = 0, sig_hi = 0, c = 0, obs = 0, mbytes = 0;
-    u32 cnt = 1, kcur = 0, pc = 0;
-    bool lst = false;              // occupancy list valid
-    int status = ST_RUNNING, aux = -1;
-    // lazy noise scan state: words [0, scanned) of the fire bitset are in
-    // the ring `win`; locations < cursor are consumed
-    u32 scanned = 0, search_w = 0, cursor = 0, fire_pc = 0xFFFFFFFFu;
-    u32 next_word_pc = P.nwords ? (u32)__ldg(tables + P.wordpc_off) : 0xFFFFFFFFu;
-    // Philox mode: geometric fire schedule instead of the per-word scan
-    const bool geo = rng.philox;
-    u32 gj = 0, gpos = 0xFFFFFFFFu;
-    u64 gpick = 0;
-    if (geo) {
-      next_word_pc = 0xFFFFFFFFu;
-      if (P.geo_len > 1 && P.nlocs) {
-        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, rng.master, shot, 0u, 0u);
-        gpos = gc.pos;
-        gpick = gc.pick;
-        gj = 1;
-      }
-      fire_pc = gpos < P.nlocs ? 0u : 0xFFFFFFFFu;   // resolved at the first op
-    }
-    u64 hnext = __ldg(ops);
-
-    while (status == ST_RUNNING) {
-      // ---- noise instructions inserted before this op (only fired ones)
-      if (pc >= next_word_pc || pc >= fire_pc) {
-        // E = OR of the fired letters of one noise instruction applied to the
-        // state (ref noise.py:68-100, state.py:88-102)
-        auto apply_error = [&](u64 ex, u64 ez, u64 qmask, u64 off) {
-          const u64 eall = ex | ez;
-          if (!eall) return;
-          // compose the action of E letter by letter
-          u64 beta = 0, delt = 0;
-          u32 xi = 0, dm = 0;
-          for (u64 rem = eall; rem; rem &= rem - 1) {
-            const u32 q = __ffsll((long long)rem) - 1;
-            const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
-            const u64 *tb = tables + off + 10ull * slot;
-            const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
-            const u64 xw64 = __ldg(tb + 4);
-            const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
-            const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
-            const u64 zw64 = __ldg(tb + 9);
-            const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
-            const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
-            const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
-            u64 lb, ld; u32 lxi, ldm;
-            if (hx && hz) {
-              lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
-              lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
-            } else if (hx) {
-              lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
-            } else {
-              lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
-            }
-            xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
-            beta ^= lb; delt ^= ld; dm ^= ldm;
-          }
-          // apply: v <- i^xi (-1)^{delta.alpha} v ; alpha ^= beta (ref state.py:88-102)
-          const double2 I = ipow(xi);
-          const double2 php = I;            // i^xi * (+1), exact
-          const double2 phm = cneg(I);
-          const u32 dcn = par64(delt & c);
-          if (lst) {
-            for (u32 i = lane; i < cnt; i += 32) {
-              const u32 j = L[i];
-              A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
-            }
-          } else {
-            const u32 nsz = 1u << kcur;
-            for (u32 j = lane; j < nsz; j += 32)
-              A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
-          }
-          __syncwarp();
-          c ^= beta;
-          mbytes += 2ull * kEntryBytes * cnt + 2ull * ((2 * n + 7) / 8);
-        };
-        // owning noise instruction of location l: last m with loc0(m) <= l
-        auto owner = [&](u32 l) -> const u64 * {
-          u32 lo = 0, hi = P.nnoise;
-          while (hi - lo > 1) {
-            const u32 mid = (lo + hi) >> 1;
-            if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= l) lo = mid; else hi = mid;
-          }
-          return tables + P.noise_off + 4ull * lo;
-        };
-        if (geo) {
-          // Philox: walk the candidate schedule (lane-uniform, rare)
-          fire_pc = 0xFFFFFFFFu;
-          while (gpos < P.nlocs) {
-            const u64 *nrec = owner(gpos);
-            const u64 nw0 = __ldg(nrec);
-            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-            if (ipc > pc) { fire_pc = ipc; break; }
-            const u32 loc0 = (u32)__ldg(nrec + 1);
-            u64 ex = 0, ez = 0;
-            while (gpos < loc0 + nloc) {
-              const u32 l = gpos;
-              bool ok = true;
-              if (!P.noise_uniform) ok = geo_accept(rng.master, shot, gj - 1, __ldg(tables + P.acc_off + l));
-              if (ok) {
-                const u64 lw = __ldg(locs + 2ull * l);
-                const u32 qa = (u32)(lw >> 32) & 0xff, qb = (u32)(lw >> 40) & 0xff,
-                          nk = (u32)(lw >> 48) & 3;
-                const double u = (double)gpick * 0x1.0p-53;
-                if (nk == NK_DEP1) {
-                  int code = 1 + (int)(u * 3.0);
-                  code = code > 3 ? 3 : code;
-                  ex |= (u64)(code != 3) << qa;
-                  ez |= (u64)(code != 1) << qa;
-                } else if (nk == NK_DEP2) {
-                  int pick = 1 + (int)(u * 15.0);
-                  pick = pick > 15 ? 15 : pick;
-                  const int ca = pick & 3, cbq = pick >> 2;
-                  if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
-                  if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
-                } else if (nk == NK_XERR) {
-                  ex |= 1ull << qa;
-                } else {
-                  ez |= 1ull << qa;
-                }
-              }
-              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, rng.master, shot, gj, l + 1);
-              gpos = gc.pos;
-              gpick = gc.pick;
-              ++gj;
-            }
-            apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
-          }
+    // apply E = OR of fired letters of one noise instruction to this lane's
+    // shot (ref noise.py:68-100, state.py:88-102)
+    auto lane_error = [&](u64 ex, u64 ez, u64 qmask, u64 off, u32 size) {
+      u64 beta = 0, delt = 0;
+      u32 xi = 0, dm = 0;
+      for (u64 rem = ex | ez; rem; rem &= rem - 1) {
+        const u32 q = __ffsll((long long)rem) - 1;
+        const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
+        const u64 *tb = tables + off + 10ull * slot;
+        const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
+        const u64 xw64 = __ldg(tb + 4);
+        const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(s_lo & __ldg(tb + 2)) ^ par64(s_hi & __ldg(tb + 3)))) & 3u;
+        const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
+        const u64 zw64 = __ldg(tb + 9);
+        const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(s_lo & __ldg(tb + 7)) ^ par64(s_hi & __ldg(tb + 8)))) & 3u;
+        const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
+        const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
+        u64 lb, ld; u32 lxi, ldm;
+        if (hx && hz) {
+          lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
+          lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
+        } else if (hx) {
+          lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
         } else {
-        while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= pc) {
-          // one fire draw per location of word `scanned`, one lane each
-          const u32 l = scanned * 32u + lane;
-          bool fire = false;
-          if (l < P.nlocs) {
-            const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
-            fire = rng.m53((u32)lw) < thr;
-          }
-          const u32 bits = __ballot_sync(FULL, fire);
-          if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
-          ++scanned;
+          lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
         }
-        __syncwarp();
-        next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
-        fire_pc = 0xFFFFFFFFu;
-        for (;;) {
-          // next fired location >= cursor among the scanned words
-          u32 fl_loc = 0xFFFFFFFFu;
-          u32 w = max(search_w, cursor >> 5);
-          for (; w < scanned; ++w) {
-            u32 bits = win[w & (kWinWords - 1)];
-            if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
-            if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
-          }
-          search_w = w;
-          if (fl_loc == 0xFFFFFFFFu) break;
-          const u64 *nrec = owner(fl_loc);
-          const u64 nw0 = __ldg(nrec);
-          const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-          if (ipc > pc) { fire_pc = ipc; break; }
-          const u32 loc0 = (u32)__ldg(nrec + 1);
-          cursor = loc0 + nloc;
-          // build E = OR of fired letters (ref noise.py:68-100)
-          u64 ex = 0, ez = 0;
-          for (u32 i = lane; i < nloc; i += 32) {
-            const u32 l = loc0 + i;
-            if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
-            const u64 lw = __ldg(locs + 2ull * l);
-            const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
-                      qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
-            if (nk == NK_DEP1) {
-              int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
-              code = code > 3 ? 3 : code;
-              ex |= (u64)(code != 3) << qa;
-              ez |= (u64)(code != 1) << qa;
-            } else if (nk == NK_DEP2) {
-              int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
-              pick = pick > 15 ? 15 : pick;
-              const int ca = pick & 3, cbq = pick >> 2;
-              if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
-              if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
-            } else if (nk == NK_XERR) {
-              ex |= 1ull << qa;
-            } else {
-              ez |= 1ull << qa;
-            }
-          }
-          ex = warp_or64(ex);
-          ez = warp_or64(ez);
-          apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
-        }
-        }
+        xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
+        beta ^= lb; delt ^= ld; dm ^= ldm;
       }
+      const double2 php = ipow(xi);
+      const double2 phm = cneg(php);
+      const u32 dcn = par64(delt & sc);
+      for (u32 j = 0; j < size; ++j) AN(j) = cmul(AN(j), (dcn ^ par32(j & dm)) ? phm : php);
+      sc ^= beta;
+      smb += 2ull * kEntryBytes * scnt + sign_bytes;
+    };
+    // letter of a fired location from its pick draw u (ref noise.py:68-100)
+    auto letter = [&](u32 nk, u32 qa, u32 qb, double u, u64 &ex, u64 &ez) {
+      if (nk == NK_DEP1) {
+        int code = 1 + (int)(u * 3.0);
+        code = code > 3 ? 3 : code;
+        ex |= (u64)(code != 3) << qa;
+        ez |= (u64)(code != 1) << qa;
+      } else if (nk == NK_DEP2) {
+        int pick = 1 + (int)(u * 15.0);
+        pick = pick > 15 ? 15 : pick;
+        const int ca = pick & 3, cbq = pick >> 2;
+        if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+        if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+      } else if (nk == NK_XERR) {
+        ex |= 1ull << qa;
+      } else {
+        ez |= 1ull << qa;
+      }
+    };
 
-      const u64 *op = ops + pc;
-      const u64 h = hnext;
+    u32 pc = 0, nm = 0;
+    for (;;) {
+      if (!__any_sync(FULL, sst == ST_RUNNING)) break;
+      const u64 h = __ldg(ops + pc);
       const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
       const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
       const u32 instr = (u32)(h >> 32);
-      pc += len;
-      hnext = __ldg(ops + pc);       // prefetch the next header
-      kcur = k;
-      const u32 size = 1u << k;
 
-      if (kind == OP_T || kind == OP_GROW_LIMIT) {
-        sig_lo ^= __ldg(op + 1);
-        sig_hi ^= __ldg(op + 2);
-        // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
-        // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
-        const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
+      if (wide_only || op_is_wide(kind, k, fl)) {
+        // ============================== wide section, warp per shot
+        __syncwarp();
+        u32 live = __ballot_sync(FULL, sst == ST_RUNNING);
+        u32 exit_pc = 0xFFFFFFFFu;
+        while (live) {
+          const u32 s = __ffs(live) - 1;
+          live &= live - 1;
+          u32 *recw = recb + s;
+          Rng rng;
+          rng.philox = philox;
+          rng.master = R.master;
+          rng.shot = __shfl_sync(FULL, shot, s);
+          rng.seed = __shfl_sync(FULL, seed, s);
+          const u64 wshot = rng.shot;
+          u64 sig_lo = __shfl_sync(FULL, s_lo, s), sig_hi = __shfl_sync(FULL, s_hi, s);
+          u64 c = __shfl_sync(FULL, sc, s), obs = __shfl_sync(FULL, sobs, s);
+          u64 mbytes = __shfl_sync(FULL, smb, s);
+          u32 cnt = __shfl_sync(FULL, scnt, s), kcur = k;
+          int status = ST_RUNNING, aux = -1;
+          bool lst = false;
+          // noise scan state: everything inserted before `pc` is applied
+          u32 cursor = P.nlocs;
+          if (nm < P.nnoise) cursor = (u32)__ldg(tables + P.noise_off + 4ull * nm + 1);
+          u32 scanned = cursor >> 5, search_w = scanned;
+          u32 next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
+          u32 fire_pc = 0xFFFFFFFFu;
+          const bool geo = philox;
+          u32 gj = __shfl_sync(FULL, sgj, s), gpos = __shfl_sync(FULL, sgpos, s);
+          u64 gpick = __shfl_sync(FULL, sgpick, s);
+          if (geo) {
+            next_word_pc = 0xFFFFFFFFu;
+            fire_pc = __shfl_sync(FULL, sfire, s);
+          }
+          const u32 size0 = 1u << k;
+          for (u32 j = lane; j < size0; j += 32) A[j] = An[j * 32u + s];
+          __syncwarp();
+          u32 wpc = pc;
+          u64 hnext = h;
+          {
+            u32 pc = wpc;
+            while (status == ST_RUNNING) {
+              if (!wide_only) {
+                const u32 kind_ = (u32)(hnext & 0xff), k_ = (u32)((hnext >> 16) & 0xff),
+                          fl_ = (u32)((hnext >> 24) & 0xff);
+                if (!op_is_wide(kind_, k_, fl_)) { exit_pc = pc; break; }
+              }
+            // ---- noise instructions inserted before this op (only fired ones)
+            if (pc >= next_word_pc || pc >= fire_pc) {
+              // E = OR of the fired letters of one noise instruction applied to the
+              // state (ref noise.py:68-100, state.py:88-102)
+              auto apply_error = [&](u64 ex, u64 ez, u64 qmask, u64 off) {
+                const u64 eall = ex | ez;
+                if (!eall) return;
+                // compose the action of E letter by letter
+                u64 beta = 0, delt = 0;
+                u32 xi = 0, dm = 0;
+                for (u64 rem = eall; rem; rem &= rem - 1) {
+                  const u32 q = __ffsll((long long)rem) - 1;
+                  const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
+                  const u64 *tb = tables + off + 10ull * slot;
+                  const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
+                  const u64 xw64 = __ldg(tb + 4);
+                  const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
+                  const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
+                  const u64 zw64 = __ldg(tb + 9);
+                  const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
+                  const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
+                  const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
+                  u64 lb, ld; u32 lxi, ldm;
+                  if (hx && hz) {
+                    lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
+                    lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
+                  } else if (hx) {
+                    lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
+                  } else {
+                    lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
+                  }
+                  xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
+                  beta ^= lb; delt ^= ld; dm ^= ldm;
+                }
+                // apply: v <- i^xi (-1)^{delta.alpha} v ; alpha ^= beta (ref state.py:88-102)
+                const double2 I = ipow(xi);
+                const double2 php = I;            // i^xi * (+1), exact
+                const double2 phm = cneg(I);
+                const u32 dcn = par64(delt & c);
+                if (lst) {
+                  for (u32 i = lane; i < cnt; i += 32) {
+                    const u32 j = L[i];
+                    A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
+                  }
+                } else {
+                  const u32 nsz = 1u << kcur;
+                  for (u32 j = lane; j < nsz; j += 32)
+                    A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
+                }
+                __syncwarp();
+                c ^= beta;
+                mbytes += 2ull * kEntryBytes * cnt + 2ull * ((2 * n + 7) / 8);
+              };
+              // owning noise instruction of location l: last m with loc0(m) <= l
+              auto owner = [&](u32 l) -> const u64 * {
+                u32 lo = 0, hi = P.nnoise;
+                while (hi - lo > 1) {
+                  const u32 mid = (lo + hi) >> 1;
+                  if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= l) lo = mid; else hi = mid;
+                }
+                return tables + P.noise_off + 4ull * lo;
+              };
+              if (geo) {
+                // Philox: walk the candidate schedule (lane-uniform, rare)
+                fire_pc = 0xFFFFFFFFu;
+                while (gpos < P.nlocs) {
+                  const u64 *nrec = owner(gpos);
+                  const u64 nw0 = __ldg(nrec);
+                  const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+                  if (ipc > pc) { fire_pc = ipc; break; }
+                  const u32 loc0 = (u32)__ldg(nrec + 1);
+                  u64 ex = 0, ez = 0;
+                  while (gpos < loc0 + nloc) {
+                    const u32 l = gpos;
+                    bool ok = true;
+                    if (!P.noise_uniform) ok = geo_accept(rng.master, wshot, gj - 1, __ldg(tables + P.acc_off + l));
+                    if (ok) {
+                      const u64 lw = __ldg(locs + 2ull * l);
+                      const u32 qa = (u32)(lw >> 32) & 0xff, qb = (u32)(lw >> 40) & 0xff,
+                                nk = (u32)(lw >> 48) & 3;
+                      const double u = (double)gpick * 0x1.0p-53;
+                      if (nk == NK_DEP1) {
+                        int code = 1 + (int)(u * 3.0);
+                        code = code > 3 ? 3 : code;
+                        ex |= (u64)(code != 3) << qa;
+                        ez |= (u64)(code != 1) << qa;
+                      } else if (nk == NK_DEP2) {
+                        int pick = 1 + (int)(u * 15.0);
+                        pick = pick > 15 ? 15 : pick;
+                        const int ca = pick & 3, cbq = pick >> 2;
+                        if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+                        if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+                      } else if (nk == NK_XERR) {
+                        ex |= 1ull << qa;
+                      } else {
+                        ez |= 1ull << qa;
+                      }
+                    }
+                    const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, rng.master, wshot, gj, l + 1);
+                    gpos = gc.pos;
+                    gpick = gc.pick;
+                    ++gj;
+                  }
+                  apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
+                }
+              } else {
+              while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= pc) {
+                // one fire draw per location of word `scanned`, one lane each
+                const u32 l = scanned * 32u + lane;
+                bool fire = false;
+                if (l < P.nlocs) {
+                  const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+                  fire = rng.m53((u32)lw) < thr;
+                }
+                const u32 bits = __ballot_sync(FULL, fire);
+                if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+                ++scanned;
+              }
+              __syncwarp();
+              next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
+              fire_pc = 0xFFFFFFFFu;
+              for (;;) {
+                // next fired location >= cursor among the scanned words
+                u32 fl_loc = 0xFFFFFFFFu;
+                u32 w = max(search_w, cursor >> 5);
+                for (; w < scanned; ++w) {
+                  u32 bits = win[w & (kWinWords - 1)];
+                  if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
+                  if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+                }
+                search_w = w;
+                if (fl_loc == 0xFFFFFFFFu) break;
+                const u64 *nrec = owner(fl_loc);
+                const u64 nw0 = __ldg(nrec);
+                const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+                if (ipc > pc) { fire_pc = ipc; break; }
+                const u32 loc0 = (u32)__ldg(nrec + 1);
+                cursor = loc0 + nloc;
+                // build E = OR of fired letters (ref noise.py:68-100)
+                u64 ex = 0, ez = 0;
+                for (u32 i = lane; i < nloc; i += 32) {
+                  const u32 l = loc0 + i;
+                  if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+                  const u64 lw = __ldg(locs + 2ull * l);
+                  const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
+                            qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
+                  if (nk == NK_DEP1) {
+                    int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
+                    code = code > 3 ? 3 : code;
+                    ex |= (u64)(code != 3) << qa;
+                    ez |= (u64)(code != 1) << qa;
+                  } else if (nk == NK_DEP2) {
+                    int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
+                    pick = pick > 15 ? 15 : pick;
+                    const int ca = pick & 3, cbq = pick >> 2;
+                    if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+                    if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+                  } else if (nk == NK_XERR) {
+                    ex |= 1ull << qa;
+                  } else {
+                    ez |= 1ull << qa;
+                  }
+                }
+                ex = warp_or64(ex);
+                ez = warp_or64(ez);
+                apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
+              }
+              }
+            }
+
+            const u64 *op = ops + pc;
+            const u64 h = hnext;
+            const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
+            const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
+            const u32 instr = (u32)(h >> 32);
+            pc += len;
+            hnext = __ldg(ops + pc);       // prefetch the next header
+            kcur = k;
+            const u32 size = 1u << k;
+
+            if (kind == OP_T || kind == OP_GROW_LIMIT) {
+              sig_lo ^= __ldg(op + 1);
+              sig_hi ^= __ldg(op + 2);
+              // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
+              // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
+              const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
+              const u64 delta = __ldg(op + 5);
+              const u64 w6 = __ldg(op + 6);
+              const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
+              const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
+              const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
+              mbytes += __ldg(op + 11);
+              const double2 bx0 = flip ? cneg(bxs) : bxs;
+              const double2 bx1 = cneg(bx0);
+              const u32 dc = par64(delta & c);
+              const u32 tcase = fl & 3u;
+              if (tcase == T_DIAG) {
+                // beta == 0: pure phase per entry (ref state.py:120-126)
+                const double2 f0 = cadd(a, bx0), f1 = cadd(a, bx1);
+                if (lst) {
+                  for (u32 i = lane; i < cnt; i += 32) {
+                    const u32 j = L[i];
+                    A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
+                  }
+                } else {
+                  for (u32 j = lane; j < size; j += 32)
+                    A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
+                }
+                __syncwarp();
+                mbytes += 32ull * cnt;
+                continue;
+              }
+              const u32 cin = cnt;
+              if (kind == OP_GROW_LIMIT) {
+                u32 nz = 0;
+                for (u32 j = lane; j < size; j += 32) {
+                  const double2 v = A[j];
+                  const u32 s = dc ^ par32(j & dmask);
+                  nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
+                  nz += abs2(cadd(Z, cmul(s ? bx1 : bx0, v))) > kPrune2;
+                }
+                nz = warp_sum_u32(nz);
+                status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
+                aux = (int)instr;
+                break;
+              }
+              const bool grow = tcase == T_GROW;
+              u32 ncnt = 0;
+              if (lst && cnt <= scap && size >= kSparseMin) {
+                // ---- sparse merge (<= 32 entries, one per lane): each listed
+                // entry owns its pair unless it is the upper member of a pair whose
+                // lower member is listed too (ref state.py:127-129, 294-306)
+                const bool valid = lane < cnt;
+                if (grow) {
+                  for (u32 m = lane; m < size; m += 32) A[size + m] = Z;
+                  __syncwarp();
+                }
+                const u32 j = valid ? L[lane] : 0u;
+                const double2 vj = valid ? A[j] : Z;
+                const u32 p = grow ? j + size : (j ^ cb);
+                const double2 vp = (valid && !grow) ? A[p] : Z;
+                const bool proc = valid && (grow || !(((j >> (31 - __clz(cb))) & 1u) && nonzero(vp)));
+                __syncwarp();
+                bool nz0 = false, nz1 = false;
+                if (proc) {
+                  const double2 aterm = cmul(a, vj);
+                  const u32 sj = dc ^ par32(j & dmask);
+                  double2 n0, n1;
+                  if (grow) {
+                    n0 = prune(aterm);
+                    n1 = prune(cmul(sj ? bx1 : bx0, vj));
+                  } else {
+                    const u32 sp = dc ^ par32(p & dmask);
+                    n0 = prune(cadd(aterm, cmul(sp ? bx1 : bx0, vp)));
+                    n1 = prune(cadd(cmul(a, vp), cmul(sj ? bx1 : bx0, vj)));
+                  }
+                  A[j] = n0;
+                  A[p] = n1;
+                  nz0 = nonzero(n0);
+                  nz1 = nonzero(n1);
+                }
+                __syncwarp();
+                list_push(L, ncnt, nz0, j, lane);
+                list_push(L, ncnt, nz1, p, lane);
+                __syncwarp();
+                lst = true;
+              } else {
+                // ---- dense merge over all coordinates
+                u32 nz = 0;
+                if (!grow) {
+                  const u32 hb = 31 - __clz(cb);
+                  const u32 half = size >> 1;
+                  for (u32 m = lane; m < half; m += 32) {
+                    const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+                    const double2 v0 = A[j0], v1 = A[j1];
+                    const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+                    const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
+                    const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
+                    A[j0] = n0;
+                    A[j1] = n1;
+                    nz += nonzero(n0) + nonzero(n1);
+                  }
+                } else {
+                  for (u32 j = lane; j < size; j += 32) {
+                    const double2 v = A[j];
+                    const u32 s = dc ^ par32(j & dmask);
+                    const double2 n0 = prune(cmul(a, v));
+                    const double2 n1 = prune(cmul(s ? bx1 : bx0, v));
+                    A[j] = n0;
+                    A[size + j] = n1;
+                    nz += nonzero(n0) + nonzero(n1);
+                  }
+                }
+                __syncwarp();
+                ncnt = warp_sum_u32(nz);
+                const u32 nsz = grow ? 2 * size : size;
+                lst = ncnt <= scap && nsz >= kSparseMin;
+                if (lst) build_list(A, L, nsz, lane);
+              }
+              if (grow) kcur = k + 1;
+              cnt = ncnt;
+              mbytes += (u64)kEntryBytes * (cin + cnt);
+              if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr; break; }
+              if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+              continue;
+            }
+
+            if (kind == OP_MEAS) {
+              sig_lo ^= __ldg(op + 1);
+              sig_hi ^= __ldg(op + 2);
+              const u32 mcase = fl & 3u;
+              const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+              const u64 delta = __ldg(op + 5);
+              const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
+              const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
+              const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
+              const u64 vec = __ldg(op + 8);
+              const u64 w13 = __ldg(op + 13);
+              const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
+              mbytes += __ldg(op + 17);
+              const u32 dc = par64(delta & c);
+              // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
+              // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
+              auto pick_plus = [&](double pplus) -> bool {
+                if (pplus >= 1.0) return true;
+                if (pplus <= 0.0) return false;
+                return rng.uniform(udraw) < pplus;
+              };
+              const u32 cin = cnt;
+              const bool compact = (fl & MF_COMPACT) != 0;
+              bool plus;
+              if (mcase == M_DET && size <= GS_SMALL_MAX) {
+                // <= 4 amplitudes: every lane evaluates the whole measurement from
+                // broadcast loads -- no cross-lane reductions (ref state.py:162-176)
+                const u32 neg0 = (xi0 >> 1) ^ dc;
+                double2 v[4];
+                double sp = 0.0, sm = 0.0;
+      #pragma unroll
+                for (u32 e = 0; e < 4; ++e) {
+                  v[e] = e < size ? A[e] : Z;
+                  if (e < size) {
+                    const double a2 = abs2(v[e]);
+                    if (neg0 ^ par32(e & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+                  }
+                }
+                plus = pick_plus(sp);
+                const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+                if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+                const u32 want_neg = plus ? 0u : 1u;
+                u32 nk = 0;
+      #pragma unroll
+                for (u32 e = 0; e < 4; ++e)
+                  nk += (e < size) && ((neg0 ^ par32(e & dmask)) == want_neg) && nonzero(v[e]);
+                if (nk == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+                const double rs = inv_sqrt_norm(plus ? sp : sm);
+                __syncwarp();
+                if (compact) {
+                  const u32 tau = want_neg ^ neg0;
+                  if (tau) c ^= vec;
+                  if (lane < (size >> 1)) {
+                    const u32 j0 = ins_bit(lane, isq, 0);
+                    const u32 src = j0 | ((tau ^ par32(j0 & dmask)) << isq);
+                    const double2 vs = src == 0 ? v[0] : src == 1 ? v[1] : src == 2 ? v[2] : v[3];
+                    A[lane] = cscale(vs, rs);
+                  }
+                  kcur = k - 1;
+                } else if (lane < size) {
+                  const double2 vl = lane == 0 ? v[0] : lane == 1 ? v[1] : lane == 2 ? v[2] : v[3];
+                  A[lane] = ((neg0 ^ par32(lane & dmask)) == want_neg) ? cscale(vl, rs) : Z;
+                }
+                __syncwarp();
+                cnt = nk;
+              } else if (mcase == M_DET) {
+                // beta == 0: filter by eigenvalue (ref state.py:162-176)
+                const u32 neg0 = (xi0 >> 1) ^ dc;
+                double sp = 0.0, sm = 0.0;
+                if (lst && cnt <= scap && size >= kSparseMin) {
+                  const bool valid = lane < cnt;
+                  const u32 j = valid ? L[lane] : 0u;
+                  const double2 v = valid ? A[j] : Z;
+                  const bool ng = (neg0 ^ par32(j & dmask)) != 0;
+                  const double a2 = abs2(v);
+                  if (valid) {
+                    if (ng) sm = a2; else sp = a2;
+                  }
+                  sp = warp_sum_live(sp, cnt);
+                  sm = warp_sum_live(sm, cnt);
+                  plus = pick_plus(sp);
+                  const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  const bool keep = valid && (ng == !plus);
+                  const double rs = inv_sqrt_norm(plus ? sp : sm);
+                  u32 dst = j;
+                  if (compact) {
+                    const u32 tau = (plus ? 0u : 1u) ^ neg0;
+                    if (tau) c ^= vec;
+                    if (valid) A[j] = Z;
+                    __syncwarp();
+                    dst = ((j >> (isq + 1)) << isq) | (j & ((1u << isq) - 1u));
+                    if (keep) A[dst] = cscale(v, rs);
+                    kcur = k - 1;
+                  } else if (valid) {
+                    A[j] = keep ? cscale(v, rs) : Z;
+                  }
+                  u32 ncnt = 0;
+                  list_push(L, ncnt, keep, dst, lane);
+                  __syncwarp();
+                  cnt = ncnt;
+              } else {
+                  for (u32 j = lane; j < size; j += 32) {
+                    const double a2 = abs2(A[j]);
+                    if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
+                    else sp = __dadd_rn(sp, a2);
+                  }
+                  sp = warp_sum_live(sp, size);
+                  sm = warp_sum_live(sm, size);
+                  plus = pick_plus(sp);
+                  const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  const u32 want_neg = plus ? 0u : 1u;
+                  const double rs = inv_sqrt_norm(plus ? sp : sm);
+                  u32 nz = 0;
+                  u32 nsize = size;
+                  if (compact) {
+                    const u32 tau = want_neg ^ neg0;
+                    const u32 half = size >> 1;
+                    for (u32 base = 0; base < half; base += 32) {
+                      const u32 jp = base + lane;
+                      double2 v = Z;
+                      if (jp < half) {
+                        const u32 j0 = ins_bit(jp, isq, 0);
+                        v = A[j0 | ((tau ^ par32(j0 & dmask)) << isq)];
+                      }
+                      __syncwarp();
+                      if (jp < half) {
+                        v = cscale(v, rs);
+                        A[jp] = v;
+                        nz += nonzero(v);
+                      }
+                      __syncwarp();
+                    }
+                    if (tau) c ^= vec;
+                    kcur = k - 1;
+                    nsize = half;
+                  } else {
+                    for (u32 j = lane; j < size; j += 32) {
+                      const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
+                      const double2 v = keep ? cscale(A[j], rs) : Z;
+                      A[j] = v;
+                      nz += nonzero(v);
+                    }
+                    __syncwarp();
+                  }
+                  cnt = warp_sum_u32(nz);
+                  lst = cnt <= scap && nsize >= kSparseMin;
+                  if (lst) build_list(A, L, nsize, lane);
+                }
+              } else {
+                // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
+                const double2 I = ipow(xi0);
+                const double2 xpp = I;            // i^xi0 * (+1), exact
+                const double2 xpm = cneg(I);
+                const u32 ct = (u32)(c >> t) & 1u;
+                const bool span = mcase == M_PIVOT_SPAN;
+                if (size <= GS_SMALL_MAX) {
+                  // <= 4 amplitudes: redundant per-lane evaluation, no reductions
+                  double2 v[4];
+      #pragma unroll
+                  for (u32 e = 0; e < 4; ++e) v[e] = e < size ? A[e] : Z;
+                  const u32 npairs = span ? (size >> 1) : size;
+                  // w(m, sign) for pair / entry m: rep + sign * xi_part * part
+                  auto pair_w = [&](u32 m, bool plus_branch) -> double2 {
+                    if (span) {
+                      const u32 j0 = ins_bit(m, isq, 0);
+                      const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+                      const u32 part = rep ^ cb;
+                      const double2 vr = rep == 0 ? v[0] : rep == 1 ? v[1] : rep == 2 ? v[2] : v[3];
+                      const double2 vp = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
+                      const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, vp);
+                      return plus_branch ? cadd(vr, prod) : csub(vr, prod);
+                    }
+                    const double2 vm = m == 0 ? v[0] : m == 1 ? v[1] : m == 2 ? v[2] : v[3];
+                    if (ct ^ par32(m & tmask)) {
+                      const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, vm);
+                      return plus_branch ? cadd(Z, prod) : csub(Z, prod);
+                    }
+                    return vm;
+                  };
+                  double sp = 0.0;
+      #pragma unroll
+                  for (u32 m = 0; m < 4; ++m)
+                    if (m < npairs) sp = __dadd_rn(sp, abs2(pair_w(m, true)));
+                  const double pp = __dmul_rn(0.5, sp);
+                  plus = pick_plus(pp);
+                  const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  double sk = 0.0;
+                  u32 nz = 0;
+                  double2 wp[4];
+      #pragma unroll
+                  for (u32 m = 0; m < 4; ++m) {
+                    wp[m] = m < npairs ? prune(pair_w(m, plus)) : Z;
+                    sk = __dadd_rn(sk, abs2(wp[m]));
+                    nz += nonzero(wp[m]);
+                  }
+                  if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  const double rs = inv_sqrt_norm(sk);
+                  __syncwarp();
+                  if (lane < npairs) {
+                    const double2 wl = lane == 0 ? wp[0] : lane == 1 ? wp[1] : lane == 2 ? wp[2] : wp[3];
+                    A[lane] = cscale(wl, rs);
+                  }
+                  __syncwarp();
+                  if (span) kcur = k - 1;
+                  cnt = nz;
+                } else if (lst && cnt <= scap && size >= kSparseMin) {
+                  const bool valid = lane < cnt;
+                  const u32 j = valid ? L[lane] : 0u;
+                  const bool is_part = (ct ^ par32(j & tmask)) != 0;
+                  u32 rep = j;
+                  double2 vr = Z, pr = Z;
+                  bool proc = valid;
+                  if (valid) {
+                    if (span) {
+                      const u32 other = j ^ cb;
+                      rep = is_part ? other : j;
+                      const u32 part = is_part ? j : other;
+                      vr = A[rep];
+                      proc = !(is_part && nonzero(vr));
+                      pr = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
+                    } else if (is_part) {
+                      pr = cmul((dc ^ par32(j & dmask)) ? xpm : xpp, A[j]);  // rep absent
+                    } else {
+                      vr = A[j];
+                    }
+                  }
+                  const double sp = warp_sum_live(proc ? abs2(cadd(vr, pr)) : 0.0, cnt);
+                  const double pp = __dmul_rn(0.5, sp);
+                  plus = pick_plus(pp);
+                  const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  double2 w = Z;
+                  if (proc) w = prune(plus ? cadd(vr, pr) : csub(vr, pr));
+                  const bool wnz = nonzero(w);
+                  const double sk = warp_sum_live(abs2(w), cnt);
+                  if (!__any_sync(FULL, wnz)) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  const double rs = inv_sqrt_norm(sk);
+                  u32 dst = rep;
+                  if (span) {
+                    __syncwarp();
+                    if (proc) { A[rep] = Z; A[rep ^ cb] = Z; }
+                    __syncwarp();
+                    dst = ((rep >> (isq + 1)) << isq) | (rep & ((1u << isq) - 1u));
+                    kcur = k - 1;
+                  }
+                  if (proc) A[dst] = wnz ? cscale(w, rs) : Z;
+                  u32 ncnt = 0;
+                  list_push(L, ncnt, wnz, dst, lane);
+                  __syncwarp();
+                  cnt = ncnt;
+              } else {
+                  double sp = 0.0;
+                  const u32 npairs = span ? (size >> 1) : size;
+                  for (u32 m = lane; m < npairs; m += 32) {
+                    double2 wpv;
+                    if (span) {
+                      const u32 j0 = ins_bit(m, isq, 0);
+                      const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+                      const u32 part = rep ^ cb;
+                      wpv = cadd(A[rep], cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]));
+                    } else {
+                      const double2 v = A[m];
+                      wpv = (ct ^ par32(m & tmask)) ? cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v)) : v;
+                    }
+                    sp = __dadd_rn(sp, abs2(wpv));
+                  }
+                  sp = warp_sum_live(sp, npairs);
+                  const double pp = __dmul_rn(0.5, sp);
+                  plus = pick_plus(pp);
+                  const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  double sk = 0.0;
+                  u32 nz = 0;
+                  for (u32 m = lane; m < npairs; m += 32) {
+                    double2 w;
+                    u32 dst;
+                    if (span) {
+                      const u32 j0 = ins_bit(m, isq, 0);
+                      const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+                      const u32 part = rep ^ cb;
+                      const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
+                      w = plus ? cadd(A[rep], prod) : csub(A[rep], prod);
+                      dst = rep;
+                    } else {
+                      const double2 v = A[m];
+                      if (ct ^ par32(m & tmask)) {
+                        const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
+                        w = plus ? cadd(Z, prod) : csub(Z, prod);
+                      } else {
+                        w = v;
+                      }
+                      dst = m;
+                    }
+                    w = prune(w);
+                    A[dst] = w;
+                    sk = __dadd_rn(sk, abs2(w));
+                    nz += nonzero(w);
+                  }
+                  __syncwarp();
+                  sk = warp_sum_live(sk, npairs);
+                  nz = warp_sum_u32(nz);
+                  if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+                  const double rs = inv_sqrt_norm(sk);
+                  u32 nsize = size;
+                  if (span) {
+                    const u32 half = size >> 1;
+                    for (u32 base = 0; base < half; base += 32) {
+                      const u32 jp = base + lane;
+                      double2 v = Z;
+                      if (jp < half) {
+                        const u32 j0 = ins_bit(jp, isq, 0);
+                        v = A[j0 | ((ct ^ par32(j0 & tmask)) << isq)];
+                      }
+                      __syncwarp();
+                      if (jp < half) A[jp] = cscale(v, rs);
+                      __syncwarp();
+                    }
+                    kcur = k - 1;
+                    nsize = half;
+                  } else {
+                    for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], rs);
+                    __syncwarp();
+                  }
+                  cnt = nz;
+                  lst = cnt <= scap && nsize >= kSparseMin;
+                  if (lst) build_list(A, L, nsize, lane);
+                }
+                if (ct) c ^= vec;
+                // tableau sign update of the pivot (ref tableau.py:176-200)
+                const u32 v = (u32)(sig_hi >> t) & 1u;
+                if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
+                sig_lo ^= __ldg(op + 11);
+                sig_hi ^= __ldg(op + 12);
+                sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
+                sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
+              }
+              mbytes += (u64)kEntryBytes * (cin + cnt);
+              const u32 bout = plus ? 0u : 1u;
+              u32 rb = bout;
+              if ((fl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
+              if (fl & MF_RECORD) {
+                if (lane == 0 && rb) recw[(slot >> 5) * 32u] |= 1u << (slot & 31);
+                __syncwarp();
+              }
+              if ((fl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
+              continue;
+            }
+
+            if (kind == OP_FEEDBACK) {
+              const u32 idx = (u32)__ldg(op + 1);
+              if ((recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u) {
+                sig_lo ^= __ldg(op + 2);
+                sig_hi ^= __ldg(op + 3);
+                mbytes += __ldg(op + 4);
+              }
+              continue;
+            }
+
+            if (kind == OP_DETECTOR || kind == OP_OBSERVABLE) {
+              const u64 w1 = __ldg(op + 1);
+              const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
+              const u64 off = __ldg(op + 2);
+              u32 bb = 0;
+              for (u32 i = lane; i < nidx; i += 32) {
+                const u32 idx = (u32)__ldg(tables + off + i);
+                bb ^= (recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u;
+              }
+              const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
+              if (kind == OP_DETECTOR) {
+                if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
+              } else {
+                obs ^= (u64)parity << id;
+              }
+              continue;
+            }
+
+            if (kind == OP_END) {
+              sig_lo ^= __ldg(op + 1);
+              sig_hi ^= __ldg(op + 2);
+              mbytes += __ldg(op + 3);
+              status = ST_PRESERVED;
+              break;
+            }
+            status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
+            aux = -2;
+            }
+          }
+          // hand the shot back to its lane
+          __syncwarp();
+          if (lane == s) {
+            s_lo = sig_lo; s_hi = sig_hi; sc = c; sobs = obs; smb = mbytes;
+            scnt = cnt; sk = kcur; sst = status; saux = aux;
+            sgj = gj; sgpos = gpos; sgpick = gpick; sfire = fire_pc;
+          }
+          if (status == ST_RUNNING) {
+            for (u32 j = lane; j < (1u << kcur); j += 32) An[j * 32u + s] = A[j];
+          } else if (O.mode == MODE_DUMP) {
+            const u64 ssl = base + s;
+            if (lane == 0) {
+              O.sig[2 * ssl] = sig_lo;
+              O.sig[2 * ssl + 1] = sig_hi;
+              O.cvec[ssl] = c;
+              O.dim[ssl] = kcur;
+            }
+            const u64 stride = 1ull << P.max_dim;
+            for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[ssl * stride + j] = A[j];
+            if (lane == s) dumped = true;
+          }
+          __syncwarp();
+        }
+        if (exit_pc == 0xFFFFFFFFu) break;   // no shot survived the section
+        pc = exit_pc;
+        while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) < pc) ++nm;
+        continue;
+      }
+
+      // ============================== narrow op, lane per shot
+      const u64 *op = ops + pc;
+      const u32 size = 1u << k;
+      // ---- noise instructions inserted before this op
+      if (!philox) {
+        for (; nm < P.nnoise; ++nm) {
+          const u64 *nrec = tables + P.noise_off + 4ull * nm;
+          const u64 nw0 = __ldg(nrec);
+          if ((u32)nw0 > pc) break;
+          if (sst != ST_RUNNING) continue;
+          const u32 nloc = (u32)(nw0 >> 32), loc0 = (u32)__ldg(nrec + 1);
+          u64 ex = 0, ez = 0;
+          for (u32 l = loc0; l < loc0 + nloc; ++l) {
+            const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+            const u32 d = (u32)lw;
+            if ((splitmix(seed, d) >> 11) < thr) {
+              const u32 nk = (u32)(lw >> 48) & 3;
+              const double u = nk <= NK_DEP2 ? (double)(splitmix(seed, d + 1) >> 11) * 0x1.0p-53 : 0.0;
+              letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+            }
+          }
+          if (ex | ez) lane_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3), size);
+        }
+      } else {
+        while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) <= pc) ++nm;
+        if (sst == ST_RUNNING && pc >= sfire) {
+          sfire = 0xFFFFFFFFu;
+          while (sgpos < P.nlocs) {
+            u32 lo = 0, hi = P.nnoise;
+            while (hi - lo > 1) {
+              const u32 mid = (lo + hi) >> 1;
+              if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= sgpos) lo = mid; else hi = mid;
+            }
+            const u64 *nrec = tables + P.noise_off + 4ull * lo;
+            const u64 nw0 = __ldg(nrec);
+            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+            if (ipc > pc) { sfire = ipc; break; }
+            const u32 loc0 = (u32)__ldg(nrec + 1);
+            u64 ex = 0, ez = 0;
+            while (sgpos < loc0 + nloc) {
+              const u32 l = sgpos;
+              bool ok = true;
+              if (!P.noise_uniform) ok = geo_accept(R.master, shot, sgj - 1, __ldg(tables + P.acc_off + l));
+              if (ok) {
+                const u64 lw = __ldg(locs + 2ull * l);
+                letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
+                       (double)sgpick * 0x1.0p-53, ex, ez);
+              }
+              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, shot, sgj, l + 1);
+              sgpos = gc.pos;
+              sgpick = gc.pick;
+              ++sgj;
+            }
+            if (ex | ez) lane_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3), size);
+          }
+        }
+      }
+      pc += len;
+      if (sst != ST_RUNNING) continue;
+      sk = k;
+
+      if (kind == OP_T) {
+        s_lo ^= __ldg(op + 1);
+        s_hi ^= __ldg(op + 2);
+        const u32 flip = par64(s_lo & __ldg(op + 3)) ^ par64(s_hi & __ldg(op + 4));
         const u64 delta = __ldg(op + 5);
         const u64 w6 = __ldg(op + 6);
         const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
         const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
         const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
-        mbytes += __ldg(op + 11);
+        smb += __ldg(op + 11);
         const double2 bx0 = flip ? cneg(bxs) : bxs;
         const double2 bx1 = cneg(bx0);
-        const u32 dc = par64(delta & c);
+        const u32 dc = par64(delta & sc);
         const u32 tcase = fl & 3u;
         if (tcase == T_DIAG) {
           // beta == 0: pure phase per entry (ref state.py:120-126)
           const double2 f0 = cadd(a, bx0), f1 = cadd(a, bx1);
-          if (lst) {
-            for (u32 i = lane; i < cnt; i += 32) {
-              const u32 j = L[i];
-              A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
-            }
-          } else {
-            for (u32 j = lane; j < size; j += 32)
-              A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
-          }
-          __syncwarp();
-          mbytes += 32ull * cnt;
+          for (u32 j = 0; j < size; ++j) AN(j) = cmul(AN(j), (dc ^ par32(j & dmask)) ? f1 : f0);
+          smb += 32ull * scnt;
           continue;
         }
-        const u32 cin = cnt;
-        if (kind == OP_GROW_LIMIT) {
-          u32 nz = 0;
-          for (u32 j = lane; j < size; j += 32) {
-            const double2 v = A[j];
-            const u32 s = dc ^ par32(j & dmask);
-            nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
-            nz += abs2(cadd(Z, cmul(s ? bx1 : bx0, v))) > kPrune2;
+        // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
+        const u32 cin = scnt;
+        u32 nz = 0;
+        if (tcase == T_BUTTERFLY) {
+          const u32 hb = 31 - __clz(cb);
+          for (u32 m = 0; m < (size >> 1); ++m) {
+            const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+            const double2 v0 = AN(j0), v1 = AN(j1);
+            const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+            const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
+            const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
+            AN(j0) = n0;
+            AN(j1) = n1;
+            nz += nonzero(n0) + nonzero(n1);
           }
-          nz = warp_sum_u32(nz);
-          status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
-          aux = (int)instr;
-          break;
-        }
-        const bool grow = tcase == T_GROW;
-        u32 ncnt = 0;
-        if (lst && cnt <= scap && size >= kSparseMin) {
-          // ---- sparse merge (<= 32 entries, one per lane): each listed
-          // entry owns its pair unless it is the upper member of a pair whose
-          // lower member is listed too (ref state.py:127-129, 294-306)
-          const bool valid = lane < cnt;
-          if (grow) {
-            for (u32 m = lane; m < size; m += 32) A[size + m] = Z;
-            __syncwarp();
-          }
-          const u32 j = valid ? L[lane] : 0u;
-          const double2 vj = valid ? A[j] : Z;
-          const u32 p = grow ? j + size : (j ^ cb);
-          const double2 vp = (valid && !grow) ? A[p] : Z;
-          const bool proc = valid && (grow || !(((j >> (31 - __clz(cb))) & 1u) && nonzero(vp)));
-          __syncwarp();
-          bool nz0 = false, nz1 = false;
-          if (proc) {
-            const double2 aterm = cmul(a, vj);
-            const u32 sj = dc ^ par32(j & dmask);
-            double2 n0, n1;
-            if (grow) {
-              n0 = prune(aterm);
-              n1 = prune(cmul(sj ? bx1 : bx0, vj));
-            } else {
-              const u32 sp = dc ^ par32(p & dmask);
-              n0 = prune(cadd(aterm, cmul(sp ? bx1 : bx0, vp)));
-              n1 = prune(cadd(cmul(a, vp), cmul(sj ? bx1 : bx0, vj)));
-            }
-            A[j] = n0;
-            A[p] = n1;
-            nz0 = nonzero(n0);
-            nz1 = nonzero(n1);
-          }
-          __syncwarp();
-          list_push(L, ncnt, nz0, j, lane);
-          list_push(L, ncnt, nz1, p, lane);
-          __syncwarp();
-          lst = true;
         } else {
-          // ---- dense merge over all coordinates
-          u32 nz = 0;
-          if (!grow) {
-            const u32 hb = 31 - __clz(cb);
-            const u32 half = size >> 1;
-            for (u32 m = lane; m < half; m += 32) {
-              const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
-              const double2 v0 = A[j0], v1 = A[j1];
-              const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
-              const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
-              const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
-              A[j0] = n0;
-              A[j1] = n1;
-              nz += nonzero(n0) + nonzero(n1);
-            }
-          } else {
-            for (u32 j = lane; j < size; j += 32) {
-              const double2 v = A[j];
-              const u32 s = dc ^ par32(j & dmask);
-              const double2 n0 = prune(cmul(a, v));
-              const double2 n1 = prune(cmul(s ? bx1 : bx0, v));
-              A[j] = n0;
-              A[size + j] = n1;
-              nz += nonzero(n0) + nonzero(n1);
-            }
+          for (u32 j = 0; j < size; ++j) {
+            const double2 v = AN(j);
+            const u32 sj = dc ^ par32(j & dmask);
+            const double2 n0 = prune(cmul(a, v));
+            const double2 n1 = prune(cmul(sj ? bx1 : bx0, v));
+            AN(j) = n0;
+            AN(size + j) = n1;
+            nz += nonzero(n0) + nonzero(n1);
           }
-          __syncwarp();
-          ncnt = warp_sum_u32(nz);
-          const u32 nsz = grow ? 2 * size : size;
-          lst = ncnt <= scap && nsz >= kSparseMin;
-          if (lst) build_list(A, L, nsz, lane);
+          sk = k + 1;
         }
-        if (grow) kcur = k + 1;
-        cnt = ncnt;
-        mbytes += (u64)kEntryBytes * (cin + cnt);
-        if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr; break; }
-        if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
+        scnt = nz;
+        smb += (u64)kEntryBytes * (cin + nz);
+        if ((u64)nz > R.cap) { sst = ST_OVERFLOW; saux = (int)instr; }
+        else if (nz == 0) { sst = ST_CORRUPT; saux = (int)instr; }
         continue;
       }
 
       if (kind == OP_MEAS) {
-        sig_lo ^= __ldg(op + 1);
-        sig_hi ^= __ldg(op + 2);
+        s_lo ^= __ldg(op + 1);
+        s_hi ^= __ldg(op + 2);
         const u32 mcase = fl & 3u;
-        const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+        const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(s_lo & __ldg(op + 3)) ^ par64(s_hi & __ldg(op + 4)))) & 3u;
         const u64 delta = __ldg(op + 5);
         const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
         const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
@@ -698,351 +1363,136 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u64 vec = __ldg(op + 8);
         const u64 w13 = __ldg(op + 13);
         const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
-        mbytes += __ldg(op + 17);
-        const u32 dc = par64(delta & c);
+        smb += __ldg(op + 17);
+        const u32 dc = par64(delta & sc);
         // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
         // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
         auto pick_plus = [&](double pplus) -> bool {
           if (pplus >= 1.0) return true;
           if (pplus <= 0.0) return false;
-          return rng.uniform(udraw) < pplus;
+          return (double)draw53(seed, R.master, shot, udraw, philox) * 0x1.0p-53 < pplus;
         };
-        const u32 cin = cnt;
-        const bool compact = (fl & MF_COMPACT) != 0;
+        const u32 cin = scnt;
         bool plus;
-        if (mcase == M_DET && size <= GS_SMALL_MAX) {
-          // <= 4 amplitudes: every lane evaluates the whole measurement from
-          // broadcast loads -- no cross-lane reductions (ref state.py:162-176)
-          const u32 neg0 = (xi0 >> 1) ^ dc;
-          double2 v[4];
-          double sp = 0.0, sm = 0.0;
-#pragma unroll
-          for (u32 e = 0; e < 4; ++e) {
-            v[e] = e < size ? A[e] : Z;
-            if (e < size) {
-              const double a2 = abs2(v[e]);
-              if (neg0 ^ par32(e & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
-            }
-          }
-          plus = pick_plus(sp);
-          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-          const u32 want_neg = plus ? 0u : 1u;
-          u32 nk = 0;
-#pragma unroll
-          for (u32 e = 0; e < 4; ++e)
-            nk += (e < size) && ((neg0 ^ par32(e & dmask)) == want_neg) && nonzero(v[e]);
-          if (nk == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-          const double rs = inv_sqrt_norm(plus ? sp : sm);
-          __syncwarp();
-          if (compact) {
-            const u32 tau = want_neg ^ neg0;
-            if (tau) c ^= vec;
-            if (lane < (size >> 1)) {
-              const u32 j0 = ins_bit(lane, isq, 0);
-              const u32 src = j0 | ((tau ^ par32(j0 & dmask)) << isq);
-              const double2 vs = src == 0 ? v[0] : src == 1 ? v[1] : src == 2 ? v[2] : v[3];
-              A[lane] = cscale(vs, rs);
-            }
-            kcur = k - 1;
-          } else if (lane < size) {
-            const double2 vl = lane == 0 ? v[0] : lane == 1 ? v[1] : lane == 2 ? v[2] : v[3];
-            A[lane] = ((neg0 ^ par32(lane & dmask)) == want_neg) ? cscale(vl, rs) : Z;
-          }
-          __syncwarp();
-          cnt = nk;
-        } else if (mcase == M_DET) {
+        u32 nz = 0;
+        if (mcase == M_DET) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
           double sp = 0.0, sm = 0.0;
-          if (lst && cnt <= scap && size >= kSparseMin) {
-            const bool valid = lane < cnt;
-            const u32 j = valid ? L[lane] : 0u;
-            const double2 v = valid ? A[j] : Z;
-            const bool ng = (neg0 ^ par32(j & dmask)) != 0;
-            const double a2 = abs2(v);
-            if (valid) {
-              if (ng) sm = a2; else sp = a2;
+          for (u32 j = 0; j < size; ++j) {
+            const double a2 = abs2(AN(j));
+            if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+          }
+          plus = pick_plus(sp);
+          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+          if (chosen < 1e-12) { sst = ST_CORRUPT; saux = (int)instr; continue; }
+          const u32 want_neg = plus ? 0u : 1u;
+          const double rs = inv_sqrt_norm(plus ? sp : sm);
+          if (fl & MF_COMPACT) {
+            const u32 tau = want_neg ^ neg0;
+            for (u32 jp = 0; jp < (size >> 1); ++jp) {
+              const u32 j0 = ins_bit(jp, isq, 0);
+              const double2 v = cscale(AN(j0 | ((tau ^ par32(j0 & dmask)) << isq)), rs);
+              AN(jp) = v;
+              nz += nonzero(v);
             }
-            sp = warp_sum_live(sp, cnt);
-            sm = warp_sum_live(sm, cnt);
-            plus = pick_plus(sp);
-            const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const bool keep = valid && (ng == !plus);
-            const double rs = inv_sqrt_norm(plus ? sp : sm);
-            u32 dst = j;
-            if (compact) {
-              const u32 tau = (plus ? 0u : 1u) ^ neg0;
-              if (tau) c ^= vec;
-              if (valid) A[j] = Z;
-              __syncwarp();
-              dst = ((j >> (isq + 1)) << isq) | (j & ((1u << isq) - 1u));
-              if (keep) A[dst] = cscale(v, rs);
-              kcur = k - 1;
-            } else if (valid) {
-              A[j] = keep ? cscale(v, rs) : Z;
+            if (tau) sc ^= vec;
+            sk = k - 1;
+          } else {
+            for (u32 j = 0; j < size; ++j) {
+              const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
+              const double2 v = keep ? cscale(AN(j), rs) : Z;
+              AN(j) = v;
+              nz += nonzero(v);
             }
-            u32 ncnt = 0;
-            list_push(L, ncnt, keep, dst, lane);
-            __syncwarp();
-            cnt = ncnt;
-        } else {
-            for (u32 j = lane; j < size; j += 32) {
-              const double a2 = abs2(A[j]);
-              if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
-              else sp = __dadd_rn(sp, a2);
-            }
-            sp = warp_sum_live(sp, size);
-            sm = warp_sum_live(sm, size);
-            plus = pick_plus(sp);
-            const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const u32 want_neg = plus ? 0u : 1u;
-            const double rs = inv_sqrt_norm(plus ? sp : sm);
-            u32 nz = 0;
-            u32 nsize = size;
-            if (compact) {
-              const u32 tau = want_neg ^ neg0;
-              const u32 half = size >> 1;
-              for (u32 base = 0; base < half; base += 32) {
-                const u32 jp = base + lane;
-                double2 v = Z;
-                if (jp < half) {
-                  const u32 j0 = ins_bit(jp, isq, 0);
-                  v = A[j0 | ((tau ^ par32(j0 & dmask)) << isq)];
-                }
-                __syncwarp();
-                if (jp < half) {
-                  v = cscale(v, rs);
-                  A[jp] = v;
-                  nz += nonzero(v);
-                }
-                __syncwarp();
-              }
-              if (tau) c ^= vec;
-              kcur = k - 1;
-              nsize = half;
-            } else {
-              for (u32 j = lane; j < size; j += 32) {
-                const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
-                const double2 v = keep ? cscale(A[j], rs) : Z;
-                A[j] = v;
-                nz += nonzero(v);
-              }
-              __syncwarp();
-            }
-            cnt = warp_sum_u32(nz);
-            lst = cnt <= scap && nsize >= kSparseMin;
-            if (lst) build_list(A, L, nsize, lane);
           }
         } else {
           // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
-          const double2 I = ipow(xi0);
-          const double2 xpp = I;            // i^xi0 * (+1), exact
-          const double2 xpm = cneg(I);
-          const u32 ct = (u32)(c >> t) & 1u;
+          const double2 xpp = ipow(xi0);
+          const double2 xpm = cneg(xpp);
+          const u32 ct = (u32)(sc >> t) & 1u;
           const bool span = mcase == M_PIVOT_SPAN;
-          if (size <= GS_SMALL_MAX) {
-            // <= 4 amplitudes: redundant per-lane evaluation, no reductions
-            double2 v[4];
-#pragma unroll
-            for (u32 e = 0; e < 4; ++e) v[e] = e < size ? A[e] : Z;
-            const u32 npairs = span ? (size >> 1) : size;
-            // w(m, sign) for pair / entry m: rep + sign * xi_part * part
-            auto pair_w = [&](u32 m, bool plus_branch) -> double2 {
-              if (span) {
-                const u32 j0 = ins_bit(m, isq, 0);
-                const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-                const u32 part = rep ^ cb;
-                const double2 vr = rep == 0 ? v[0] : rep == 1 ? v[1] : rep == 2 ? v[2] : v[3];
-                const double2 vp = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
-                const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, vp);
-                return plus_branch ? cadd(vr, prod) : csub(vr, prod);
-              }
-              const double2 vm = m == 0 ? v[0] : m == 1 ? v[1] : m == 2 ? v[2] : v[3];
-              if (ct ^ par32(m & tmask)) {
-                const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, vm);
-                return plus_branch ? cadd(Z, prod) : csub(Z, prod);
-              }
-              return vm;
-            };
-            double sp = 0.0;
-#pragma unroll
-            for (u32 m = 0; m < 4; ++m)
-              if (m < npairs) sp = __dadd_rn(sp, abs2(pair_w(m, true)));
-            const double pp = __dmul_rn(0.5, sp);
-            plus = pick_plus(pp);
-            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-            double sk = 0.0;
-            u32 nz = 0;
-            double2 wp[4];
-#pragma unroll
-            for (u32 m = 0; m < 4; ++m) {
-              wp[m] = m < npairs ? prune(pair_w(m, plus)) : Z;
-              sk = __dadd_rn(sk, abs2(wp[m]));
-              nz += nonzero(wp[m]);
-            }
-            if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const double rs = inv_sqrt_norm(sk);
-            __syncwarp();
-            if (lane < npairs) {
-              const double2 wl = lane == 0 ? wp[0] : lane == 1 ? wp[1] : lane == 2 ? wp[2] : wp[3];
-              A[lane] = cscale(wl, rs);
-            }
-            __syncwarp();
-            if (span) kcur = k - 1;
-            cnt = nz;
-          } else if (lst && cnt <= scap && size >= kSparseMin) {
-            const bool valid = lane < cnt;
-            const u32 j = valid ? L[lane] : 0u;
-            const bool is_part = (ct ^ par32(j & tmask)) != 0;
-            u32 rep = j;
-            double2 vr = Z, pr = Z;
-            bool proc = valid;
-            if (valid) {
-              if (span) {
-                const u32 other = j ^ cb;
-                rep = is_part ? other : j;
-                const u32 part = is_part ? j : other;
-                vr = A[rep];
-                proc = !(is_part && nonzero(vr));
-                pr = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
-              } else if (is_part) {
-                pr = cmul((dc ^ par32(j & dmask)) ? xpm : xpp, A[j]);  // rep absent
-              } else {
-                vr = A[j];
-              }
-            }
-            const double sp = warp_sum_live(proc ? abs2(cadd(vr, pr)) : 0.0, cnt);
-            const double pp = __dmul_rn(0.5, sp);
-            plus = pick_plus(pp);
-            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-            double2 w = Z;
-            if (proc) w = prune(plus ? cadd(vr, pr) : csub(vr, pr));
-            const bool wnz = nonzero(w);
-            const double sk = warp_sum_live(abs2(w), cnt);
-            if (!__any_sync(FULL, wnz)) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const double rs = inv_sqrt_norm(sk);
-            u32 dst = rep;
+          const u32 npairs = span ? (size >> 1) : size;
+          double sp = 0.0;
+          for (u32 m = 0; m < npairs; ++m) {
+            double2 wpv;
             if (span) {
-              __syncwarp();
-              if (proc) { A[rep] = Z; A[rep ^ cb] = Z; }
-              __syncwarp();
-              dst = ((rep >> (isq + 1)) << isq) | (rep & ((1u << isq) - 1u));
-              kcur = k - 1;
-            }
-            if (proc) A[dst] = wnz ? cscale(w, rs) : Z;
-            u32 ncnt = 0;
-            list_push(L, ncnt, wnz, dst, lane);
-            __syncwarp();
-            cnt = ncnt;
-        } else {
-            double sp = 0.0;
-            const u32 npairs = span ? (size >> 1) : size;
-            for (u32 m = lane; m < npairs; m += 32) {
-              double2 wpv;
-              if (span) {
-                const u32 j0 = ins_bit(m, isq, 0);
-                const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-                const u32 part = rep ^ cb;
-                wpv = cadd(A[rep], cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]));
-              } else {
-                const double2 v = A[m];
-                wpv = (ct ^ par32(m & tmask)) ? cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v)) : v;
-              }
-              sp = __dadd_rn(sp, abs2(wpv));
-            }
-            sp = warp_sum_live(sp, npairs);
-            const double pp = __dmul_rn(0.5, sp);
-            plus = pick_plus(pp);
-            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-            double sk = 0.0;
-            u32 nz = 0;
-            for (u32 m = lane; m < npairs; m += 32) {
-              double2 w;
-              u32 dst;
-              if (span) {
-                const u32 j0 = ins_bit(m, isq, 0);
-                const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-                const u32 part = rep ^ cb;
-                const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
-                w = plus ? cadd(A[rep], prod) : csub(A[rep], prod);
-                dst = rep;
-              } else {
-                const double2 v = A[m];
-                if (ct ^ par32(m & tmask)) {
-                  const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
-                  w = plus ? cadd(Z, prod) : csub(Z, prod);
-                } else {
-                  w = v;
-                }
-                dst = m;
-              }
-              w = prune(w);
-              A[dst] = w;
-              sk = __dadd_rn(sk, abs2(w));
-              nz += nonzero(w);
-            }
-            __syncwarp();
-            sk = warp_sum_live(sk, npairs);
-            nz = warp_sum_u32(nz);
-            if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-            const double rs = inv_sqrt_norm(sk);
-            u32 nsize = size;
-            if (span) {
-              const u32 half = size >> 1;
-              for (u32 base = 0; base < half; base += 32) {
-                const u32 jp = base + lane;
-                double2 v = Z;
-                if (jp < half) {
-                  const u32 j0 = ins_bit(jp, isq, 0);
-                  v = A[j0 | ((ct ^ par32(j0 & tmask)) << isq)];
-                }
-                __syncwarp();
-                if (jp < half) A[jp] = cscale(v, rs);
-                __syncwarp();
-              }
-              kcur = k - 1;
-              nsize = half;
+              const u32 j0 = ins_bit(m, isq, 0);
+              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+              const u32 part = rep ^ cb;
+              wpv = cadd(AN(rep), cmul((dc ^ par32(part & dmask)) ? xpm : xpp, AN(part)));
             } else {
-              for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], rs);
-              __syncwarp();
+              const double2 v = AN(m);
+              wpv = (ct ^ par32(m & tmask)) ? cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v)) : v;
             }
-            cnt = nz;
-            lst = cnt <= scap && nsize >= kSparseMin;
-            if (lst) build_list(A, L, nsize, lane);
+            sp = __dadd_rn(sp, abs2(wpv));
           }
-          if (ct) c ^= vec;
+          const double pp = __dmul_rn(0.5, sp);
+          plus = pick_plus(pp);
+          const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+          if (chosen < 1e-12) { sst = ST_CORRUPT; saux = (int)instr; continue; }
+          double sk2 = 0.0;
+          for (u32 m = 0; m < npairs; ++m) {
+            double2 w;
+            u32 dst;
+            if (span) {
+              const u32 j0 = ins_bit(m, isq, 0);
+              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+              const u32 part = rep ^ cb;
+              const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, AN(part));
+              w = plus ? cadd(AN(rep), prod) : csub(AN(rep), prod);
+              dst = rep;
+            } else {
+              const double2 v = AN(m);
+              if (ct ^ par32(m & tmask)) {
+                const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
+                w = plus ? cadd(Z, prod) : csub(Z, prod);
+              } else {
+                w = v;
+              }
+              dst = m;
+            }
+            w = prune(w);
+            AN(dst) = w;
+            sk2 = __dadd_rn(sk2, abs2(w));
+            nz += nonzero(w);
+          }
+          if (nz == 0) { sst = ST_CORRUPT; saux = (int)instr; continue; }
+          const double rs = inv_sqrt_norm(sk2);
+          if (span) {
+            for (u32 jp = 0; jp < (size >> 1); ++jp) {
+              const u32 j0 = ins_bit(jp, isq, 0);
+              AN(jp) = cscale(AN(j0 | ((ct ^ par32(j0 & tmask)) << isq)), rs);
+            }
+            sk = k - 1;
+          } else {
+            for (u32 j = 0; j < size; ++j) AN(j) = cscale(AN(j), rs);
+          }
+          if (ct) sc ^= vec;
           // tableau sign update of the pivot (ref tableau.py:176-200)
-          const u32 v = (u32)(sig_hi >> t) & 1u;
-          if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
-          sig_lo ^= __ldg(op + 11);
-          sig_hi ^= __ldg(op + 12);
-          sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
-          sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
+          const u32 v = (u32)(s_hi >> t) & 1u;
+          if (v) { s_lo ^= __ldg(op + 9); s_hi ^= __ldg(op + 10); }
+          s_lo ^= __ldg(op + 11);
+          s_hi ^= __ldg(op + 12);
+          s_lo = (s_lo & ~(1ull << t)) | ((u64)v << t);
+          s_hi = (s_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
         }
-        mbytes += (u64)kEntryBytes * (cin + cnt);
+        scnt = nz;
+        smb += (u64)kEntryBytes * (cin + nz);
         const u32 bout = plus ? 0u : 1u;
         u32 rb = bout;
-        if ((fl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
-        if (fl & MF_RECORD) {
-          if (lane == 0 && rb) rec[slot >> 5] |= 1u << (slot & 31);
-          __syncwarp();
-        }
-        if ((fl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
+        if ((fl & MF_FLIP) && draw53(seed, R.master, shot, udraw + 1, philox) < __ldg(op + 14)) rb ^= 1u;
+        if ((fl & MF_RECORD) && rb) recb[(slot >> 5) * 32u + lane] |= 1u << (slot & 31);
+        if ((fl & MF_RESET) && bout) { s_lo ^= __ldg(op + 15); s_hi ^= __ldg(op + 16); }
         continue;
       }
 
       if (kind == OP_FEEDBACK) {
         const u32 idx = (u32)__ldg(op + 1);
-        if ((rec[idx >> 5] >> (idx & 31)) & 1u) {
-          sig_lo ^= __ldg(op + 2);
-          sig_hi ^= __ldg(op + 3);
-          mbytes += __ldg(op + 4);
+        if ((recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u) {
+          s_lo ^= __ldg(op + 2);
+          s_hi ^= __ldg(op + 3);
+          smb += __ldg(op + 4);
         }
         continue;
       }
@@ -1051,75 +1501,84 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u64 w1 = __ldg(op + 1);
         const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
         const u64 off = __ldg(op + 2);
-        u32 bb = 0;
-        for (u32 i = lane; i < nidx; i += 32) {
+        u32 parity = 0;
+        for (u32 i = 0; i < nidx; ++i) {
           const u32 idx = (u32)__ldg(tables + off + i);
-          bb ^= (rec[idx >> 5] >> (idx & 31)) & 1u;
+          parity ^= (recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u;
         }
-        const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
         if (kind == OP_DETECTOR) {
-          if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
+          if ((R.flags & GS_POSTSELECT) && parity) { sst = ST_DISCARDED; saux = (int)id; }
         } else {
-          obs ^= (u64)parity << id;
+          sobs ^= (u64)parity << id;
         }
         continue;
       }
 
       if (kind == OP_END) {
-        sig_lo ^= __ldg(op + 1);
-        sig_hi ^= __ldg(op + 2);
-        mbytes += __ldg(op + 3);
-        status = ST_PRESERVED;
-        break;
+        s_lo ^= __ldg(op + 1);
+        s_hi ^= __ldg(op + 2);
+        smb += __ldg(op + 3);
+        sst = ST_PRESERVED;
+        continue;
       }
-      status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
-      aux = -2;
+      sst = ST_UNSUPPORTED;  // unknown opcode: fail loudly
+      saux = -2;
     }
+    __syncwarp();
 
     // -------------------------------------------------------- shot outputs
-    n_tot += 1;
-    mbytes_all += mbytes;
-    if (status == ST_PRESERVED) {
-      n_pres += 1;
-      if (obs) {
-        n_err += 1;
-        if (lane == 0) {
-          for (u64 o = obs; o; o &= o - 1)
+    if (valid) {
+      n_tot += 1;
+      mbytes_all += smb;
+      if (sst == ST_PRESERVED) {
+        n_pres += 1;
+        if (sobs) {
+          n_err += 1;
+          for (u64 o = sobs; o; o &= o - 1)
             atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
           if (O.witness) {
             const u32 wi = atomicAdd(O.witness_count, 1u);
             if (wi < O.witness_cap) O.witness[wi] = shot;
           }
         }
-      }
-    } else if (status == ST_DISCARDED) n_disc += 1;
-    else if (status == ST_OVERFLOW) n_ovf += 1;
-    else if (status == ST_CORRUPT) n_cor += 1;
-    else n_uns += 1;
-    if (O.mode != MODE_COUNTERS) {
-      if (lane == 0) {
-        O.status[sl] = (u8)status;
-        O.aux[sl] = aux;
-        O.obs[sl] = obs;
-      }
-      const u32 rw64 = (P.nmeas + 63) / 64;
-      for (u32 w = lane; w < rw64; w += 32) {
-        const u32 lo = rec[2 * w];
-        const u32 hi = (2 * w + 1 < P.rec_words32) ? rec[2 * w + 1] : 0u;
-        O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
-      }
-      if (O.mode == MODE_DUMP) {
-        if (lane == 0) {
-          O.sig[2 * sl] = sig_lo;
-          O.sig[2 * sl + 1] = sig_hi;
-          O.cvec[sl] = c;
-          O.dim[sl] = kcur;
+      } else if (sst == ST_DISCARDED) n_disc += 1;
+      else if (sst == ST_OVERFLOW) n_ovf += 1;
+      else if (sst == ST_CORRUPT) n_cor += 1;
+      else n_uns += 1;
+      if (O.mode != MODE_COUNTERS) {
+        O.status[sl] = (u8)sst;
+        O.aux[sl] = saux;
+        O.obs[sl] = sobs;
+        const u32 rw64 = (P.nmeas + 63) / 64;
+        for (u32 w = 0; w < rw64; ++w) {
+          const u32 lo = recb[(2 * w) * 32u + lane];
+          const u32 hi = (2 * w + 1 < P.rec_words32) ? recb[(2 * w + 1) * 32u + lane] : 0u;
+          O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
         }
-        const u64 stride = 1ull << P.max_dim;
-        for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = A[j];
+        if (O.mode == MODE_DUMP && !dumped) {
+          O.sig[2 * sl] = s_lo;
+          O.sig[2 * sl + 1] = s_hi;
+          O.cvec[sl] = sc;
+          O.dim[sl] = sk;
+          const u64 stride = 1ull << P.max_dim;
+          for (u32 j = 0; j < (1u << sk); ++j) O.amps[sl * stride + j] = AN(j);
+        }
       }
     }
     __syncwarp();
+  }
+#undef AN
+  // warp totals, one atomic per counter per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_tot += __shfl_xor_sync(FULL, n_tot, o);
+    n_pres += __shfl_xor_sync(FULL, n_pres, o);
+    n_disc += __shfl_xor_sync(FULL, n_disc, o);
+    n_ovf += __shfl_xor_sync(FULL, n_ovf, o);
+    n_cor += __shfl_xor_sync(FULL, n_cor, o);
+    n_uns += __shfl_xor_sync(FULL, n_uns, o);
+    n_err += __shfl_xor_sync(FULL, n_err, o);
+    mbytes_all += __shfl_xor_sync(FULL, mbytes_all, o);
   }
   if (lane == 0) {
     unsigned long long *C = (unsigned long long *)O.counters;
@@ -1360,9 +1819,10 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
   const size_t chi = (size_t)16 << K;
   L.rec_words32 = ((p->info.num_measurements + 63) / 64) * 2;
   if (L.rec_words32 == 0) L.rec_words32 = 2;
-  const size_t rec_b = (size_t)L.rec_words32 * 4;
-  L.rec_in_smem = rec_b <= 2048;
-  size_t base = gs::kWinBytes + 4 * gs::kLcapMax + (L.rec_in_smem ? rec_b : 0);
+  // record bits of the warp's 32 shots (one column per lane)
+  const size_t rec_b = (size_t)L.rec_words32 * 4 * 32;
+  L.rec_in_smem = rec_b <= 4096;
+  size_t base = gs::kWinBytes + 4 * gs::kLcapMax + gs::kNarrowBytes + (L.rec_in_smem ? rec_b : 0);
   base = (base + 15) & ~(size_t)15;
   // chi in shared memory only when it is small: large chi buffers cap the
   // resident warps per SM, while the global (L1/L2-cached) placement keeps

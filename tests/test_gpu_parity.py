@@ -271,3 +271,33 @@ def test_msc_d5_dumps_match_oracle_through_t_layer():
             assert st["ph"] == rs["ph"] and st["idx"] == rs["idx"]
             np.testing.assert_allclose(np.array(st["amp"]), np.array(rs["amp"]),
                                        rtol=0, atol=AMP_TOL)
+
+
+@pytest.mark.parametrize("rng", ["splitmix", "philox"])
+def test_lane_per_shot_matches_warp_per_shot(rng):
+    """The batched lane-per-shot (narrow) interpreter and the warp-per-shot
+    (wide) interpreter give identical records, statuses and counters on
+    random programs (chi dims crossing the narrow limit back and forth), the
+    d=3 and the grown d=5 MSC workloads."""
+    from paper_2512_23037_b200.msc import msc_circuit, msc_grown_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    rnd = random.Random(21)
+    progs = [apply_noise_model(msc_circuit(3), 3e-3),
+             apply_noise_model(msc_grown_circuit(5), 3e-3)]
+    for _ in range(12):
+        n = rnd.choice((5, 9, 16))
+        progs.append(_random_program(rnd, n, 90, rnd.choice((6, 12, 20)), 0.1))
+    eng = get_engine(0)
+    for i, prog in enumerate(progs):
+        p = Program(compile_program(prog))
+        flags = _lib.GS_POSTSELECT * (i % 2) | (_lib.GS_RNG_PHILOX if rng == "philox" else 0)
+        shots = 3000 if i < 2 else 200
+        a = eng.run_records(p, Engine.params(5 + i, 0, shots, 4096, flags))
+        b = eng.run_records(p, Engine.params(5 + i, 0, shots, 4096,
+                                             flags | _lib.GS_WIDE_ONLY))
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), i
+        ca = eng.run_counters(p, Engine.params(5 + i, 0, shots, 4096, flags))
+        cb = eng.run_counters(p, Engine.params(5 + i, 0, shots, 4096,
+                                               flags | _lib.GS_WIDE_ONLY))
+        assert np.array_equal(ca, cb), i
