@@ -152,9 +152,7 @@ def main():
     ap.add_argument("--chi-global", action="store_true")
     ap.add_argument("--chi-smem", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
-    ap.add_argument("--dense-only", action="store_true")
     ap.add_argument("--wide-only", action="store_true")
-    ap.add_argument("--list-cap", type=int, default=0)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -212,8 +210,6 @@ def main():
         flags |= _lib.GS_CHI_GLOBAL
     if args.chi_smem:
         flags |= _lib.GS_CHI_SMEM
-    if args.dense_only:
-        flags |= _lib.GS_DENSE_ONLY
     if args.wide_only:
         flags |= _lib.GS_WIDE_ONLY
     S = args.shots_per_step
@@ -224,8 +220,7 @@ def main():
 
     def launch(step):
         base = step * world * S + rank * S
-        par = Engine.params(12345, base, S, 32768, flags, warps_per_block=args.wpb,
-                            list_cap=args.list_cap)
+        par = Engine.params(12345, base, S, 32768, flags, warps_per_block=args.wpb)
         eng.run_counters_async(P, par, counters.data_ptr(), stream.cuda_stream)
 
     for w in range(args.warmup):

@@ -48,7 +48,6 @@ extern "C" {
 #define GS_POSTSELECT 1u   /* discard on the first firing detector      */
 #define GS_RNG_PHILOX 2u   /* Philox4x32-10 streams (else SHA-1+SplitMix) */
 #define GS_CHI_GLOBAL 4u   /* force chi buffers into global memory (test) */
-#define GS_DENSE_ONLY 8u   /* disable the sparse occupancy list (test)   */
 #define GS_CHI_SMEM 16u    /* force chi buffers into shared memory (test) */
 #define GS_WIDE_ONLY 32u   /* run every op warp-per-shot (A/B, test)     */
 
@@ -101,7 +100,7 @@ typedef struct {
   uint32_t flags;            /* GS_POSTSELECT | GS_RNG_PHILOX | ...      */
   uint32_t warps_per_block;  /* 0 = auto                                 */
   uint32_t blocks;           /* 0 = auto (persistent grid)               */
-  uint32_t list_cap;         /* occupancy-list capacity, 0 = default 128 */
+  uint32_t reserved;         /* must be 0                                */
   const uint64_t *seeds;     /* optional host per-shot seeds (SplitMix)  */
 } gs_run_params;
 

@@ -18,7 +18,6 @@ LIB_PATH = os.path.join(HERE, LIB_NAME)
 GS_POSTSELECT = 1
 GS_RNG_PHILOX = 2
 GS_CHI_GLOBAL = 4
-GS_DENSE_ONLY = 8
 GS_CHI_SMEM = 16
 GS_WIDE_ONLY = 32
 
@@ -60,7 +59,7 @@ class GsRunParams(ct.Structure):
     _fields_ = [("master_seed", ct.c_uint64), ("shot_begin", ct.c_uint64),
                 ("shot_count", ct.c_uint64), ("capacity", ct.c_uint64),
                 ("flags", ct.c_uint32), ("warps_per_block", ct.c_uint32),
-                ("blocks", ct.c_uint32), ("list_cap", ct.c_uint32),
+                ("blocks", ct.c_uint32), ("reserved", ct.c_uint32),
                 ("seeds", ct.POINTER(ct.c_uint64))]
 
 

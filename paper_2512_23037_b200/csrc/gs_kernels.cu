@@ -22,11 +22,13 @@
 #include <stdio.h>
 #include <string.h>
 #include <math.h>
+#include <algorithm>
 #include <string>
 #include <vector>
 
 #include "../../include/gstab_sm100.h"
 
+// @region helpers
 typedef unsigned long long u64;
 typedef unsigned int u32;
 typedef unsigned char u8;
@@ -81,8 +83,9 @@ struct DevOut {
   u32 mode;
   u32 warp_bytes;       // dynamic smem bytes per warp
   u32 rec_in_smem;
-  u32 chi_off;          // byte offset of chi inside the warp's smem slice
-  u32 lcap;             // occupancy-list capacity (<= kLcapMax; 0 = dense only)
+  u32 chi_off;          // byte offset of the record columns in the warp's smem slice
+  u64 *gstash;          // per-warp lane-state stash for wide sections
+  double2 *gan;         // per-warp narrow-chi parking (shared-memory chi)
   u64 *witness;         // optional: global indices of preserved shots with a
   u32 *witness_count;   //   flipped observable (paper §V-B witnesses)
   u32 witness_cap;
@@ -133,18 +136,12 @@ __device__ __forceinline__ u32 ins_bit(u32 jp, u32 pos, u32 bit) {
   u32 low = jp & ((1u << pos) - 1u);
   return ((jp >> pos) << (pos + 1)) | (bit << pos) | low;
 }
-__device__ __forceinline__ double warp_sum(double v) {
+// butterfly sum over the warp (every lane gets the same bits); out of line:
+// one copy serves every measurement path (instruction-cache footprint)
+__device__ __noinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
   return v;
-}
-// Sum over lanes where only lanes < live can be nonzero.  A shortened
-// log2(live)-level tree would be bit-identical, but measured slower than the
-// branch-free 5-level tree (A/B on one B200: 5.70M vs 6.35M shots/s, d=5), so
-// the full tree is used.
-__device__ __forceinline__ double warp_sum_live(double v, u32 live) {
-  (void)live;
-  return warp_sum(v);
 }
 __device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(FULL, v); }
 __device__ __forceinline__ u64 warp_or64(u64 v) {
@@ -265,42 +262,296 @@ struct Rng {
   }
 };
 
-// ---------------------------------------------------------------- chi views
+// ---------------------------------------------------------------- chi storage
 //
-// The dense array A[0, 2^k) is always the storage (zero = absent entry, so
-// partner lookups are O(1)).  When at most `lcap` entries are nonzero the
-// warp also keeps their coordinates in the occupancy list L and iterates
-// only over those (sparse mode); otherwise it sweeps all 2^k coordinates
-// (dense mode).  Invariant: inside [0, 2^k) an entry is nonzero iff it is in
-// the support; positions >= 2^k are don't-care until a GROW initialises them.
+// Per shot the chi map is a dense complex128 array over the 2^k coordinates
+// of the static basis (zero = absent reference entry, so partner lookups
+// are O(1)); positions >= 2^k are don't-care until a GROW initialises them.
 
-constexpr u32 kLcapMax = 64;    // list storage; sparse ops need cnt <= 32
 #ifndef GS_KN
 #define GS_KN 4u                // narrow (lane-per-shot) chi dimension limit
 #endif
 constexpr u32 kNarrowBytes = (1u << GS_KN) * 32u * 16u;   // An[2^KN][32] double2
-constexpr u32 kSparseMin = 64;    // below this a dense sweep is <= 2 rounds
+constexpr u32 kCntBytes = 64;                              // per-warp counters
 
 __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y != 0.0; }
 
-__device__ __forceinline__ u32 lanemask_lt(u32 lane) { return (1u << lane) - 1u; }
+// ---------------------------------------------------------------- wide sweeps
+//
+// Warp-cooperative passes over a dense chi array A[0, 2^k) (lanes take
+// coordinates lane, lane+32, ...; GS_SW coordinates in flight per lane).
+// Out of line on purpose: each gets its own small register allocation, so
+// the loads of one round are all issued before the first use (memory-level
+// parallelism against L1/L2 latency) without spilling the interpreter's
+// state.  Per-lane partial results; callers reduce across the warp.
 
-// append `pos` for every lane with `flag`, preserving lane order
-__device__ __forceinline__ void list_push(u32 *L, u32 &base, bool flag, u32 pos, u32 lane) {
-  const u32 bal = __ballot_sync(FULL, flag);
-  if (flag) L[base + __popc(bal & lanemask_lt(lane))] = pos;
-  base += __popc(bal);
+#ifndef GS_SW
+#define GS_SW 1   // A/B on one B200 (shared-memory chi): 20.6M / 10.8M / 8.2M shots/s at 1 / 2 / 4
+#endif
+
+// T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129)
+__device__ __noinline__ u32 sweep_butterfly(double2 *__restrict__ A, u32 half, u32 cb,
+                                            u32 dc, u32 dmask, double2 a, double2 bx0) {
+  const u32 lane = threadIdx.x & 31u;
+  const double2 bx1 = cneg(bx0);
+  const u32 hb = 31 - __clz(cb);
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < half; b0 += 32 * GS_SW) {
+    double2 v0[GS_SW], v1[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 m = b0 + 32 * u;
+      if (m < half) {
+        const u32 j0 = ins_bit(m, hb, 0);
+        v0[u] = A[j0];
+        v1[u] = A[j0 ^ cb];
+      }
+    }
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 m = b0 + 32 * u;
+      if (m < half) {
+        const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+        const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+        const double2 n0 = prune(cadd(cmul(a, v0[u]), cmul(s1 ? bx1 : bx0, v1[u])));
+        const double2 n1 = prune(cadd(cmul(a, v1[u]), cmul(s0 ? bx1 : bx0, v0[u])));
+        A[j0] = n0;
+        A[j1] = n1;
+        nz += nonzero(n0) + nonzero(n1);
+      }
+    }
+  }
+  return nz;
 }
 
-// rebuild the occupancy list from a dense scan (only when cnt <= lcap)
-__device__ void build_list(const double2 *A, u32 *L, u32 size, u32 lane) {
-  u32 base = 0;
-  for (u32 b = 0; b < size; b += 32) {
-    const u32 j = b + lane;
-    const bool nz = j < size && nonzero(A[j]);
-    list_push(L, base, nz, j, lane);
+// T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
+__device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc, u32 dmask,
+                                       double2 a, double2 bx0) {
+  const u32 lane = threadIdx.x & 31u;
+  const double2 bx1 = cneg(bx0);
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const u32 s_ = dc ^ par32(j & dmask);
+        const double2 n0 = prune(cmul(a, v[u]));
+        const double2 n1 = prune(cmul(s_ ? bx1 : bx0, v[u]));
+        A[j] = n0;
+        A[size + j] = n1;
+        nz += nonzero(n0) + nonzero(n1);
+      }
+    }
   }
-  __syncwarp();
+  return nz;
+}
+
+// diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
+// fired noise Paulis)
+__device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 dc, u32 mask,
+                                         double2 f0, double2 f1) {
+  const u32 lane = threadIdx.x & 31u;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) A[j] = cmul(v[u], (dc ^ par32(j & mask)) ? f1 : f0);
+    }
+  }
+}
+
+// beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
+__device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u32 size, u32 dmask,
+                                               u32 neg0) {
+  const u32 lane = threadIdx.x & 31u;
+  double sp = 0.0, sm = 0.0;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const double a2 = abs2(v[u]);
+        if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+      }
+    }
+  }
+  return make_double2(sp, sm);
+}
+
+// keep the chosen eigen-entries, scaled by rs; zero the others
+__device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 dmask,
+                                         u32 neg0, u32 want_neg, double rs) {
+  const u32 lane = threadIdx.x & 31u;
+  const double2 Z = make_double2(0.0, 0.0);
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
+        const double2 w = keep ? cscale(v[u], rs) : Z;
+        A[j] = w;
+        nz += nonzero(w);
+      }
+    }
+  }
+  return nz;
+}
+
+// in-place compaction dropping coordinate isq: A[jp] = rs * A[src(jp)],
+// src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
+// at isq; src(jp) >= jp, so reads of a round finish before its writes
+__device__ __noinline__ u32 sweep_compact(double2 *__restrict__ A, u32 half, u32 isq, u32 mask,
+                                          u32 tau, double rs) {
+  const u32 lane = threadIdx.x & 31u;
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 b0 = 0; b0 < half; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 jp = b0 + 32 * u + lane;
+      if (jp < half) {
+        const u32 j0 = ins_bit(jp, isq, 0);
+        v[u] = A[j0 | ((tau ^ par32(j0 & mask)) << isq)];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 jp = b0 + 32 * u + lane;
+      if (jp < half) {
+        const double2 w = cscale(v[u], rs);
+        A[jp] = w;
+        nz += nonzero(w);
+      }
+    }
+    __syncwarp();
+  }
+  return nz;
+}
+
+// pivot measurement (ref state.py:178-208): w(m) = rep + sg * xi * part.
+// span: pairs (rep, rep^cb), rep = j0 | ((ct ^ par(j0 & tmask)) << isq);
+// no span: every entry, entries with ct ^ par(m & tmask) are `part` only.
+// pass 1 returns the per-lane sum of |w+|^2; pass 2 writes prune(w_sg) to
+// the rep slot and returns (sum |w|^2, nonzeros).
+struct PivotGeo {
+  u32 npairs, isq, tmask, ct, cb, dc, dmask;
+  bool span;
+};
+__device__ __forceinline__ void pivot_terms(const double2 *__restrict__ A, const PivotGeo &g,
+                                            double2 xpp, u32 m, double2 &vr, double2 &pr,
+                                            u32 &dst) {
+  const double2 xpm = cneg(xpp);
+  if (g.span) {
+    const u32 j0 = ins_bit(m, g.isq, 0);
+    const u32 rep = j0 | ((g.ct ^ par32(j0 & g.tmask)) << g.isq);
+    const u32 part = rep ^ g.cb;
+    vr = A[rep];
+    pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, A[part]);
+    dst = rep;
+  } else {
+    const double2 v = A[m];
+    if (g.ct ^ par32(m & g.tmask)) {
+      vr = make_double2(0.0, 0.0);
+      pr = cmul((g.dc ^ par32(m & g.dmask)) ? xpm : xpp, v);
+    } else {
+      vr = v;
+      pr = make_double2(-0.0, -0.0);   // v + (-0) == v exactly
+    }
+    dst = m;
+  }
+}
+__device__ __noinline__ double sweep_pivot_p(const double2 *__restrict__ A, PivotGeo g,
+                                             double2 xpp) {
+  const u32 lane = threadIdx.x & 31u;
+  double sp = 0.0;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < g.npairs; b0 += 32 * GS_SW) {
+    double2 vr[GS_SW], pr[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      u32 d_;
+      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], d_);
+    }
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u)
+      if (b0 + 32 * u < g.npairs) sp = __dadd_rn(sp, abs2(cadd(vr[u], pr[u])));
+  }
+  return sp;
+}
+struct SumNz {
+  double sum;
+  u32 nz;
+};
+__device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g, double2 xpp,
+                                            bool plus) {
+  const u32 lane = threadIdx.x & 31u;
+  double sk = 0.0;
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < g.npairs; b0 += 32 * GS_SW) {
+    double2 vr[GS_SW], pr[GS_SW];
+    u32 dst[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u)
+      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], dst[u]);
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      if (b0 + 32 * u < g.npairs) {
+        const double2 w = prune(plus ? cadd(vr[u], pr[u]) : csub(vr[u], pr[u]));
+        A[dst[u]] = w;
+        sk = __dadd_rn(sk, abs2(w));
+        nz += nonzero(w);
+      }
+    }
+  }
+  SumNz r;
+  r.sum = sk;
+  r.nz = nz;
+  return r;
+}
+
+// renormalise every entry: A[j] *= rs
+__device__ __noinline__ u32 sweep_phase_scale(double2 *__restrict__ A, u32 size, double rs) {
+  const u32 lane = threadIdx.x & 31u;
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const double2 w = cscale(v[u], rs);
+        A[j] = w;
+        nz += nonzero(w);
+      }
+    }
+  }
+  return nz;
 }
 
 // ---------------------------------------------------------------- kernel
@@ -315,24 +566,493 @@ __device__ void build_list(const double2 *A, u32 *L, u32 size, u32 lane) {
 //    sign-mask parities, draws) is paid once for 32 shots;
 //  * wide ops (k > GS_KN, and GROW_LIMIT) run warp-per-shot: the warp takes
 //    the live lanes' shots one at a time through the whole wide section
-//    (lanes split the 2^k coordinates, chi in a per-warp buffer) and hands
-//    each surviving shot back at the first narrow op after it.
+//    (lanes split the 2^k coordinates, chi in a per-warp buffer, WU-way
+//    unrolled sweeps for memory-level parallelism) and hands each surviving
+//    shot back at the first narrow op after it.  Lane states are parked in
+//    a per-warp global stash meanwhile, so the wide loops have the
+//    registers to themselves.
 //
 // k is static per op (shot-invariant basis, compiler.py), so every shot of
 // the batch enters and leaves a wide section at the same pc.  Shots that
 // end (discarded / preserved / overflow) leave their lane idle until the
 // batch finishes.  GS_WIDE_ONLY runs every op warp-per-shot (A/B, tests).
 
-#ifndef GS_SMALL_MAX
-#define GS_SMALL_MAX 1u   // redundant per-lane path only for one amplitude (A/B: 6.62M vs 5.99M at <=2, 5.73M at <=4)
-#endif
 #ifndef GS_MIN_BLOCKS
-#define GS_MIN_BLOCKS 4   // 128 registers: 16 resident warps/SM (measured best)
+#define GS_MIN_BLOCKS 4   // 128 registers: 16 resident warps/SM
 #endif
 
 __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
   return kind == OP_GROW_LIMIT || k > GS_KN ||
          (kind == OP_T && (fl & 3u) == T_GROW && k + 1 > GS_KN);
+}
+
+// action of a fired error E = X^ex Z^ez on the static frame:
+// alpha ^= beta, v *= i^xi (-1)^{delta.alpha}; `dm` = delta in coordinates
+struct ErrAct {
+  u64 beta, delt;
+  u32 xi, dm;
+};
+__device__ __noinline__ ErrAct compose_error(const u64 *__restrict__ tables, u64 ex, u64 ez,
+                                             u64 qmask, u64 off, u64 sig_lo, u64 sig_hi) {
+  ErrAct r;
+  r.beta = 0; r.delt = 0; r.xi = 0; r.dm = 0;
+#pragma unroll 1
+  for (u64 rem = ex | ez; rem; rem &= rem - 1) {
+    const u32 q = __ffsll((long long)rem) - 1;
+    const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
+    const u64 *tb = tables + off + 10ull * slot;
+    const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
+    const u64 xw64 = __ldg(tb + 4);
+    const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
+    const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
+    const u64 zw64 = __ldg(tb + 9);
+    const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
+    const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
+    const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
+    u64 lb, ld; u32 lxi, ldm;
+    if (hx && hz) {   // Y = i X Z
+      lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
+      lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
+    } else if (hx) {
+      lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
+    } else {
+      lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
+    }
+    r.xi = (r.xi + lxi + 2u * par64(r.delt & lb)) & 3u;
+    r.beta ^= lb; r.delt ^= ld; r.dm ^= ldm;
+  }
+  return r;
+}
+
+// letter of a fired location from its pick draw u (ref noise.py:68-100)
+__device__ __forceinline__ void noise_letter(u32 nk, u32 qa, u32 qb, double u, u64 &ex, u64 &ez) {
+  if (nk == NK_DEP1) {
+    int code = 1 + (int)(u * 3.0);
+    code = code > 3 ? 3 : code;
+    ex |= (u64)(code != 3) << qa;
+    ez |= (u64)(code != 1) << qa;
+  } else if (nk == NK_DEP2) {
+    int pick = 1 + (int)(u * 15.0);
+    pick = pick > 15 ? 15 : pick;
+    const int ca = pick & 3, cbq = pick >> 2;
+    if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+    if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+  } else if (nk == NK_XERR) {
+    ex |= 1ull << qa;
+  } else {
+    ez |= 1ull << qa;
+  }
+}
+
+// owning noise instruction of location l: last m with loc0(m) <= l
+__device__ __forceinline__ const u64 *noise_owner(const DevProg &P, u32 l) {
+  u32 lo = 0, hi = P.nnoise;
+  while (hi - lo > 1) {
+    const u32 mid = (lo + hi) >> 1;
+    if ((u32)__ldg(P.tables + P.noise_off + 4ull * mid + 1) <= l) lo = mid; else hi = mid;
+  }
+  return P.tables + P.noise_off + 4ull * lo;
+}
+
+// per-lane stash fields (u64), layout stash[f * 32 + lane]
+enum { SF_LO = 0, SF_HI, SF_C, SF_OBS, SF_MB, SF_PICK, SF_SEED, SF_SHOT, SF_CNTK, SF_ST,
+       SF_GEO, SF_FIRE, SF_N };
+
+// per-warp counters in shared memory
+enum { WC_TOT = 0, WC_PRES, WC_DISC, WC_OVF, WC_COR, WC_UNS, WC_ERR, WC_MB, WC_N };
+
+// One wide section, warp per shot: runs every live lane's shot (mask
+// `live`) from the wide op at `pc` to the first narrow op after it (its pc
+// is returned; 0xFFFFFFFF when no shot survives).  Lane states are read from
+// and written back to the per-warp stash.  Kept out of line so its unrolled
+// sweeps get their own register allocation, independent of the narrow loop.
+template <bool kSmemChi>
+__device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, const DevOut &O,
+                                         u64 base, u32 pc, u32 nm, u64 h, u32 live,
+                                         u32 *win, u32 *recb, double2 *An, double2 *A,
+                                         u64 *stash) {
+  const u32 lane = threadIdx.x & 31u;
+  const u32 n = P.n;
+  const u64 *__restrict__ ops = P.ops;
+  const u64 *__restrict__ tables = P.tables;
+  const u64 *__restrict__ locs = P.locs;
+  const double2 Z = make_double2(0.0, 0.0);
+  const bool philox = (R.flags & GS_RNG_PHILOX) != 0;
+  const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
+  const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
+  const u32 k = (u32)((h >> 16) & 0xff);
+  (void)n;
+    u32 exit_pc = 0xFFFFFFFFu, exit_k = 0;
+    // shared-memory chi: the wide buffer A aliases the narrow array An, so
+    // the lanes' narrow chi rows [0, 2^k) are parked in global memory (Ast)
+    // for the section and restored at its end
+    double2 *Ast = An;
+    if (kSmemChi) {
+      Ast = O.gan + ((u64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32ull << GS_KN);
+#pragma unroll 1
+      for (u32 i = lane; i < (32u << k); i += 32) Ast[i] = An[i];
+      __syncwarp();
+    }
+    while (live) {
+      const u32 s = __ffs(live) - 1;
+      live &= live - 1;
+      u32 *recw = recb + s;
+      Rng rng;
+      rng.philox = philox;
+      rng.master = R.master;
+      rng.shot = stash[SF_SHOT * 32 + s];
+      rng.seed = stash[SF_SEED * 32 + s];
+      u64 sig_lo = stash[SF_LO * 32 + s], sig_hi = stash[SF_HI * 32 + s];
+      u64 c = stash[SF_C * 32 + s], obs = stash[SF_OBS * 32 + s];
+      u64 mbytes = stash[SF_MB * 32 + s];
+      u32 cnt = (u32)stash[SF_CNTK * 32 + s], kcur = k;
+      int status = ST_RUNNING, aux = -1;
+      const u64 gw_ = stash[SF_GEO * 32 + s];
+      u32 gj = (u32)gw_, gpos = (u32)(gw_ >> 32);
+      u64 gpick = stash[SF_PICK * 32 + s];
+      // noise scan state: everything inserted before `pc` is applied
+      u32 cursor = P.nlocs;
+      if (nm < P.nnoise) cursor = (u32)__ldg(tables + P.noise_off + 4ull * nm + 1);
+      u32 scanned = cursor >> 5, search_w = scanned;
+      u32 next_word_pc = 0xFFFFFFFFu, fire_pc = 0xFFFFFFFFu;
+      if (philox) fire_pc = (u32)stash[SF_FIRE * 32 + s];
+      else if (scanned < P.nwords) next_word_pc = (u32)__ldg(tables + P.wordpc_off + scanned);
+#pragma unroll 1
+      for (u32 j = lane; j < (1u << k); j += 32) A[j] = Ast[j * 32u + s];
+      __syncwarp();
+      u32 wpc = pc;
+      u64 hnext = h;
+      while (status == ST_RUNNING) {
+        if (!wide_only) {
+          const u32 kind_ = (u32)(hnext & 0xff), k_ = (u32)((hnext >> 16) & 0xff),
+                    fl_ = (u32)((hnext >> 24) & 0xff);
+          if (!op_is_wide(kind_, k_, fl_)) { exit_pc = wpc; exit_k = k_; break; }
+        }
+        // @region wide: noise
+        if (wpc >= next_word_pc || wpc >= fire_pc) {
+          // apply E = OR of fired letters of one noise instruction
+          // (ref noise.py:68-100, state.py:88-102)
+          auto apply_error = [&](u64 ex, u64 ez, const u64 *nrec) {
+            if (!(ex | ez)) return;
+            const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
+                                           sig_lo, sig_hi);
+            const double2 php = ipow(e.xi);
+            sweep_phase(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php));
+            __syncwarp();
+            c ^= e.beta;
+            mbytes += 2ull * kEntryBytes * cnt + sign_bytes;
+          };
+          if (philox) {
+            // walk the candidate schedule (lane-uniform, rare)
+            fire_pc = 0xFFFFFFFFu;
+            while (gpos < P.nlocs) {
+              const u64 *nrec = noise_owner(P, gpos);
+              const u64 nw0 = __ldg(nrec);
+              const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+              if (ipc > wpc) { fire_pc = ipc; break; }
+              const u32 loc0 = (u32)__ldg(nrec + 1);
+              u64 ex = 0, ez = 0;
+              while (gpos < loc0 + nloc) {
+                const u32 l = gpos;
+                bool ok = true;
+                if (!P.noise_uniform) ok = geo_accept(R.master, rng.shot, gj - 1, __ldg(tables + P.acc_off + l));
+                if (ok) {
+                  const u64 lw = __ldg(locs + 2ull * l);
+                  noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
+                               (double)gpick * 0x1.0p-53, ex, ez);
+                }
+                const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, rng.shot, gj, l + 1);
+                gpos = gc.pos;
+                gpick = gc.pick;
+                ++gj;
+              }
+              apply_error(ex, ez, nrec);
+            }
+          } else {
+            // SplitMix: one fire draw per location, 32 locations per ballot
+            while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= wpc) {
+              const u32 l = scanned * 32u + lane;
+              bool fire = false;
+              if (l < P.nlocs) {
+                const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+                fire = rng.m53((u32)lw) < thr;
+              }
+              const u32 bits = __ballot_sync(FULL, fire);
+              if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+              ++scanned;
+            }
+            __syncwarp();
+            next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
+            fire_pc = 0xFFFFFFFFu;
+#pragma unroll 1
+            for (;;) {
+              // next fired location >= cursor among the scanned words
+              u32 fl_loc = 0xFFFFFFFFu;
+              u32 w = max(search_w, cursor >> 5);
+#pragma unroll 1
+              for (; w < scanned; ++w) {
+                u32 bits = win[w & (kWinWords - 1)];
+                if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
+                if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+              }
+              search_w = w;
+              if (fl_loc == 0xFFFFFFFFu) break;
+              const u64 *nrec = noise_owner(P, fl_loc);
+              const u64 nw0 = __ldg(nrec);
+              const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+              if (ipc > wpc) { fire_pc = ipc; break; }
+              const u32 loc0 = (u32)__ldg(nrec + 1);
+              cursor = loc0 + nloc;
+              u64 ex = 0, ez = 0;
+#pragma unroll 1
+              for (u32 i = lane; i < nloc; i += 32) {
+                const u32 l = loc0 + i;
+                if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+                const u64 lw = __ldg(locs + 2ull * l);
+                const u32 nk = (u32)(lw >> 48) & 3;
+                const double u = nk <= NK_DEP2 ? rng.uniform((u32)lw + 1) : 0.0;
+                noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+              }
+              apply_error(warp_or64(ex), warp_or64(ez), nrec);
+            }
+          }
+        }
+
+        // @region wide: dispatch
+        const u64 *op = ops + wpc;
+        const u64 hw = hnext;
+        const u32 wkind = (u32)(hw & 0xff), wlen = (u32)((hw >> 8) & 0xff);
+        const u32 wk = (u32)((hw >> 16) & 0xff), wfl = (u32)((hw >> 24) & 0xff);
+        const u32 winstr = (u32)(hw >> 32);
+        wpc += wlen;
+        hnext = __ldg(ops + wpc);       // prefetch the next header
+        kcur = wk;
+        const u32 size = 1u << wk;
+
+        // @region wide: T
+        if (wkind == OP_T || wkind == OP_GROW_LIMIT) {
+          sig_lo ^= __ldg(op + 1);
+          sig_hi ^= __ldg(op + 2);
+          // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
+          // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
+          const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
+          const u64 delta = __ldg(op + 5);
+          const u64 w6 = __ldg(op + 6);
+          const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
+          const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
+          const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
+          mbytes += __ldg(op + 11);
+          const double2 bx0 = flip ? cneg(bxs) : bxs;
+          const u32 dc = par64(delta & c);
+          const u32 tcase = wfl & 3u;
+          if (tcase == T_DIAG) {
+            // beta == 0: pure phase per entry (ref state.py:120-126)
+            sweep_phase(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)));
+            __syncwarp();
+            mbytes += 32ull * cnt;
+            continue;
+          }
+          const u32 cin = cnt;
+          if (wkind == OP_GROW_LIMIT) {
+            u32 nz = 0;
+            const double2 bx1 = cneg(bx0);
+#pragma unroll 1
+            for (u32 j = lane; j < size; j += 32) {
+              const double2 v = A[j];
+              const u32 s_ = dc ^ par32(j & dmask);
+              nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
+              nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
+            }
+            nz = warp_sum_u32(nz);
+            status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
+            aux = (int)winstr;
+            break;
+          }
+          // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
+          u32 nz;
+          if (tcase == T_BUTTERFLY) {
+            nz = sweep_butterfly(A, size >> 1, cb, dc, dmask, a, bx0);
+          } else {
+            nz = sweep_grow(A, size, dc, dmask, a, bx0);
+            kcur = wk + 1;
+          }
+          __syncwarp();
+          cnt = warp_sum_u32(nz);
+          mbytes += (u64)kEntryBytes * (cin + cnt);
+          if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
+          if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          continue;
+        }
+
+        // @region wide: meas
+        if (wkind == OP_MEAS) {
+          sig_lo ^= __ldg(op + 1);
+          sig_hi ^= __ldg(op + 2);
+          const u32 mcase = wfl & 3u;
+          const u32 xi0 = (((wfl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+          const u64 delta = __ldg(op + 5);
+          const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
+          const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
+          const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
+          const u64 vec = __ldg(op + 8);
+          const u64 w13 = __ldg(op + 13);
+          const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
+          mbytes += __ldg(op + 17);
+          const u32 dc = par64(delta & c);
+          // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
+          // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
+          auto pick_plus = [&](double pplus) -> bool {
+            if (pplus >= 1.0) return true;
+            if (pplus <= 0.0) return false;
+            return rng.uniform(udraw) < pplus;
+          };
+          const u32 cin = cnt;
+          bool plus;
+          u32 nz;
+          if (mcase == M_DET) {
+            // beta == 0: filter by eigenvalue (ref state.py:162-176)
+            const u32 neg0 = (xi0 >> 1) ^ dc;
+            const double2 part = sweep_det_sums(A, size, dmask, neg0);
+            const double sp = warp_sum(part.x);
+            const double sm = warp_sum(part.y);
+            plus = pick_plus(sp);
+            const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            const u32 want_neg = plus ? 0u : 1u;
+            const double rs = inv_sqrt_norm(plus ? sp : sm);
+            if (wfl & MF_COMPACT) {
+              const u32 tau = want_neg ^ neg0;
+              nz = sweep_compact(A, size >> 1, isq, dmask, tau, rs);
+              if (tau) c ^= vec;
+              kcur = wk - 1;
+            } else {
+              nz = sweep_filter(A, size, dmask, neg0, want_neg, rs);
+            }
+            __syncwarp();
+          } else {
+            // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
+            PivotGeo g;
+            g.span = mcase == M_PIVOT_SPAN;
+            g.npairs = g.span ? (size >> 1) : size;
+            g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
+            g.dc = dc; g.dmask = dmask;
+            const double2 xpp = ipow(xi0);   // i^xi0, exact
+            const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p(A, g, xpp)));
+            plus = pick_plus(pp);
+            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            const SumNz w = sweep_pivot_w(A, g, xpp, plus);
+            __syncwarp();
+            const double sk = warp_sum(w.sum);
+            if (warp_sum_u32(w.nz) == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            const double rs = inv_sqrt_norm(sk);
+            if (g.span) {
+              nz = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs);
+              kcur = wk - 1;
+            } else {
+              nz = sweep_phase_scale(A, size, rs);
+            }
+            __syncwarp();
+            if (g.ct) c ^= vec;
+            // tableau sign update of the pivot (ref tableau.py:176-200)
+            const u32 v = (u32)(sig_hi >> t) & 1u;
+            if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
+            sig_lo ^= __ldg(op + 11);
+            sig_hi ^= __ldg(op + 12);
+            sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
+            sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
+          }
+          cnt = warp_sum_u32(nz);
+          mbytes += (u64)kEntryBytes * (cin + cnt);
+          const u32 bout = plus ? 0u : 1u;
+          u32 rb = bout;
+          if ((wfl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
+          if (wfl & MF_RECORD) {
+            if (lane == 0 && rb) recw[(slot >> 5) * 32u] |= 1u << (slot & 31);
+            __syncwarp();
+          }
+          if ((wfl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
+          continue;
+        }
+
+        // @region wide: feedback/detector/end
+        if (wkind == OP_FEEDBACK) {
+          const u32 idx = (u32)__ldg(op + 1);
+          if ((recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u) {
+            sig_lo ^= __ldg(op + 2);
+            sig_hi ^= __ldg(op + 3);
+            mbytes += __ldg(op + 4);
+          }
+          continue;
+        }
+        if (wkind == OP_DETECTOR || wkind == OP_OBSERVABLE) {
+          const u64 w1 = __ldg(op + 1);
+          const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
+          const u64 off = __ldg(op + 2);
+          u32 bb = 0;
+#pragma unroll 1
+          for (u32 i = lane; i < nidx; i += 32) {
+            const u32 idx = (u32)__ldg(tables + off + i);
+            bb ^= (recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u;
+          }
+          const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
+          if (wkind == OP_DETECTOR) {
+            if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
+          } else {
+            obs ^= (u64)parity << id;
+          }
+          continue;
+        }
+        if (wkind == OP_END) {
+          sig_lo ^= __ldg(op + 1);
+          sig_hi ^= __ldg(op + 2);
+          mbytes += __ldg(op + 3);
+          status = ST_PRESERVED;
+          break;
+        }
+        status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
+        aux = -2;
+      }
+      // @region wide: exit
+      // hand the shot back (stash) and its chi back to its lane
+      __syncwarp();
+      if (lane == 0) {
+        stash[SF_LO * 32 + s] = sig_lo;
+        stash[SF_HI * 32 + s] = sig_hi;
+        stash[SF_C * 32 + s] = c;
+        stash[SF_OBS * 32 + s] = obs;
+        stash[SF_MB * 32 + s] = mbytes;
+        stash[SF_PICK * 32 + s] = gpick;
+        stash[SF_CNTK * 32 + s] = (u64)cnt | ((u64)kcur << 32);
+        stash[SF_ST * 32 + s] = (u64)(status & 0xff) | ((u64)(u32)aux << 32) |
+                                ((u64)(status != ST_RUNNING && O.mode == MODE_DUMP) << 8);
+        stash[SF_GEO * 32 + s] = (u64)gj | ((u64)gpos << 32);
+        stash[SF_FIRE * 32 + s] = fire_pc;
+      }
+      if (status == ST_RUNNING) {
+#pragma unroll 1
+        for (u32 j = lane; j < (1u << kcur); j += 32) Ast[j * 32u + s] = A[j];
+      } else if (O.mode == MODE_DUMP) {
+        const u64 ssl = base + s;
+        if (lane == 0) {
+          O.sig[2 * ssl] = sig_lo;
+          O.sig[2 * ssl + 1] = sig_hi;
+          O.cvec[ssl] = c;
+          O.dim[ssl] = kcur;
+        }
+        const u64 stride = 1ull << P.max_dim;
+#pragma unroll 1
+        for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[ssl * stride + j] = A[j];
+      }
+      __syncwarp();
+    }
+  if (kSmemChi && exit_pc != 0xFFFFFFFFu) {
+    __syncwarp();
+#pragma unroll 1
+    for (u32 i = lane; i < (32u << exit_k); i += 32) An[i] = Ast[i];
+  }
+  __syncwarp();
+  return exit_pc;
 }
 
 template <bool kSmemChi>
@@ -345,38 +1065,40 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
   const u64 gw = (u64)blockIdx.x * wpb + wib;
   u8 *mine = smem + (size_t)wib * O.warp_bytes;
   u32 *win = reinterpret_cast<u32 *>(mine);
-  u32 *L = reinterpret_cast<u32 *>(mine + kWinBytes);
-  double2 *An = reinterpret_cast<double2 *>(mine + kWinBytes + 4 * kLcapMax);
+  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine + kWinBytes);
+  double2 *An = reinterpret_cast<double2 *>(mine + kWinBytes + kCntBytes);
   // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
-  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kWinBytes + 4 * kLcapMax + kNarrowBytes)
+  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + O.chi_off)
                             : O.grec + gw * (u64)P.rec_words32 * 32u;
-  double2 *A = kSmemChi ? reinterpret_cast<double2 *>(mine + O.chi_off)
+  double2 *A = kSmemChi ? An
                         : O.gchi + gw * ((u64)1 << P.max_dim);
+  u64 *stash = O.gstash + gw * (u64)(SF_N * 32);
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
   const u64 *__restrict__ tables = P.tables;
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
-  const u32 scap = O.lcap < 32u ? O.lcap : 32u;   // sparse ops: <= 1 entry per lane
   const bool philox = (R.flags & GS_RNG_PHILOX) != 0;
   const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
   const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
 #define AN(j) An[(j) * 32u + lane]
 
-  long long n_tot = 0, n_pres = 0, n_disc = 0, n_ovf = 0, n_cor = 0, n_uns = 0,
-            n_err = 0;
-  unsigned long long mbytes_all = 0;
+  if (lane < WC_N) wcnt[lane] = 0;
+  __syncwarp();
 
+#pragma unroll 1
   for (;;) {
+    // @region batch setup
     u64 base = 0;
     if (lane == 0) base = atomicAdd(O.next_shot, 32ull);
     base = __shfl_sync(FULL, base, 0);
     if (base >= R.shot_count) break;
     const u64 sl = base + lane;
     const bool valid = sl < R.shot_count;
-    const u64 shot = R.shot_begin + sl;
+    u64 shot = R.shot_begin + sl;
     u64 seed = 0;
     if (valid && !philox) seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
+#pragma unroll 1
     for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
     AN(0) = make_double2(1.0, 0.0);
 
@@ -398,63 +1120,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
     }
     __syncwarp();
 
-    // apply E = OR of fired letters of one noise instruction to this lane's
-    // shot (ref noise.py:68-100, state.py:88-102)
-    auto lane_error = [&](u64 ex, u64 ez, u64 qmask, u64 off, u32 size) {
-      u64 beta = 0, delt = 0;
-      u32 xi = 0, dm = 0;
-      for (u64 rem = ex | ez; rem; rem &= rem - 1) {
-        const u32 q = __ffsll((long long)rem) - 1;
-        const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
-        const u64 *tb = tables + off + 10ull * slot;
-        const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
-        const u64 xw64 = __ldg(tb + 4);
-        const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(s_lo & __ldg(tb + 2)) ^ par64(s_hi & __ldg(tb + 3)))) & 3u;
-        const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
-        const u64 zw64 = __ldg(tb + 9);
-        const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(s_lo & __ldg(tb + 7)) ^ par64(s_hi & __ldg(tb + 8)))) & 3u;
-        const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
-        const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
-        u64 lb, ld; u32 lxi, ldm;
-        if (hx && hz) {
-          lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
-          lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
-        } else if (hx) {
-          lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
-        } else {
-          lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
-        }
-        xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
-        beta ^= lb; delt ^= ld; dm ^= ldm;
-      }
-      const double2 php = ipow(xi);
-      const double2 phm = cneg(php);
-      const u32 dcn = par64(delt & sc);
-      for (u32 j = 0; j < size; ++j) AN(j) = cmul(AN(j), (dcn ^ par32(j & dm)) ? phm : php);
-      sc ^= beta;
-      smb += 2ull * kEntryBytes * scnt + sign_bytes;
-    };
-    // letter of a fired location from its pick draw u (ref noise.py:68-100)
-    auto letter = [&](u32 nk, u32 qa, u32 qb, double u, u64 &ex, u64 &ez) {
-      if (nk == NK_DEP1) {
-        int code = 1 + (int)(u * 3.0);
-        code = code > 3 ? 3 : code;
-        ex |= (u64)(code != 3) << qa;
-        ez |= (u64)(code != 1) << qa;
-      } else if (nk == NK_DEP2) {
-        int pick = 1 + (int)(u * 15.0);
-        pick = pick > 15 ? 15 : pick;
-        const int ca = pick & 3, cbq = pick >> 2;
-        if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
-        if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
-      } else if (nk == NK_XERR) {
-        ex |= 1ull << qa;
-      } else {
-        ez |= 1ull << qa;
-      }
-    };
-
     u32 pc = 0, nm = 0;
+#pragma unroll 1
     for (;;) {
       if (!__any_sync(FULL, sst == ST_RUNNING)) break;
       const u64 h = __ldg(ops + pc);
@@ -463,783 +1130,65 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
       const u32 instr = (u32)(h >> 32);
 
       if (wide_only || op_is_wide(kind, k, fl)) {
-        // ============================== wide section, warp per shot
-        __syncwarp();
+        // @region wide: handoff
+        // park every lane's state; the wide loops read shot s from the stash
+        stash[SF_LO * 32 + lane] = s_lo;
+        stash[SF_HI * 32 + lane] = s_hi;
+        stash[SF_C * 32 + lane] = sc;
+        stash[SF_OBS * 32 + lane] = sobs;
+        stash[SF_MB * 32 + lane] = smb;
+        stash[SF_PICK * 32 + lane] = sgpick;
+        stash[SF_SEED * 32 + lane] = seed;
+        stash[SF_SHOT * 32 + lane] = shot;
+        stash[SF_CNTK * 32 + lane] = (u64)scnt | ((u64)sk << 32);
+        stash[SF_ST * 32 + lane] = (u64)(sst & 0xff) | ((u64)dumped << 8) | ((u64)(u32)saux << 32);
+        stash[SF_GEO * 32 + lane] = (u64)sgj | ((u64)sgpos << 32);
+        stash[SF_FIRE * 32 + lane] = sfire;
         u32 live = __ballot_sync(FULL, sst == ST_RUNNING);
-        u32 exit_pc = 0xFFFFFFFFu;
-        while (live) {
-          const u32 s = __ffs(live) - 1;
-          live &= live - 1;
-          u32 *recw = recb + s;
-          Rng rng;
-          rng.philox = philox;
-          rng.master = R.master;
-          rng.shot = __shfl_sync(FULL, shot, s);
-          rng.seed = __shfl_sync(FULL, seed, s);
-          const u64 wshot = rng.shot;
-          u64 sig_lo = __shfl_sync(FULL, s_lo, s), sig_hi = __shfl_sync(FULL, s_hi, s);
-          u64 c = __shfl_sync(FULL, sc, s), obs = __shfl_sync(FULL, sobs, s);
-          u64 mbytes = __shfl_sync(FULL, smb, s);
-          u32 cnt = __shfl_sync(FULL, scnt, s), kcur = k;
-          int status = ST_RUNNING, aux = -1;
-          bool lst = false;
-          // noise scan state: everything inserted before `pc` is applied
-          u32 cursor = P.nlocs;
-          if (nm < P.nnoise) cursor = (u32)__ldg(tables + P.noise_off + 4ull * nm + 1);
-          u32 scanned = cursor >> 5, search_w = scanned;
-          u32 next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
-          u32 fire_pc = 0xFFFFFFFFu;
-          const bool geo = philox;
-          u32 gj = __shfl_sync(FULL, sgj, s), gpos = __shfl_sync(FULL, sgpos, s);
-          u64 gpick = __shfl_sync(FULL, sgpick, s);
-          if (geo) {
-            next_word_pc = 0xFFFFFFFFu;
-            fire_pc = __shfl_sync(FULL, sfire, s);
-          }
-          const u32 size0 = 1u << k;
-          for (u32 j = lane; j < size0; j += 32) A[j] = An[j * 32u + s];
-          __syncwarp();
-          u32 wpc = pc;
-          u64 hnext = h;
-          {
-            u32 pc = wpc;
-            while (status == ST_RUNNING) {
-              if (!wide_only) {
-                const u32 kind_ = (u32)(hnext & 0xff), k_ = (u32)((hnext >> 16) & 0xff),
-                          fl_ = (u32)((hnext >> 24) & 0xff);
-                if (!op_is_wide(kind_, k_, fl_)) { exit_pc = pc; break; }
-              }
-            // ---- noise instructions inserted before this op (only fired ones)
-            if (pc >= next_word_pc || pc >= fire_pc) {
-              // E = OR of the fired letters of one noise instruction applied to the
-              // state (ref noise.py:68-100, state.py:88-102)
-              auto apply_error = [&](u64 ex, u64 ez, u64 qmask, u64 off) {
-                const u64 eall = ex | ez;
-                if (!eall) return;
-                // compose the action of E letter by letter
-                u64 beta = 0, delt = 0;
-                u32 xi = 0, dm = 0;
-                for (u64 rem = eall; rem; rem &= rem - 1) {
-                  const u32 q = __ffsll((long long)rem) - 1;
-                  const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
-                  const u64 *tb = tables + off + 10ull * slot;
-                  const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
-                  const u64 xw64 = __ldg(tb + 4);
-                  const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
-                  const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
-                  const u64 zw64 = __ldg(tb + 9);
-                  const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
-                  const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
-                  const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
-                  u64 lb, ld; u32 lxi, ldm;
-                  if (hx && hz) {
-                    lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
-                    lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
-                  } else if (hx) {
-                    lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
-                  } else {
-                    lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
-                  }
-                  xi = (xi + lxi + 2u * par64(delt & lb)) & 3u;
-                  beta ^= lb; delt ^= ld; dm ^= ldm;
-                }
-                // apply: v <- i^xi (-1)^{delta.alpha} v ; alpha ^= beta (ref state.py:88-102)
-                const double2 I = ipow(xi);
-                const double2 php = I;            // i^xi * (+1), exact
-                const double2 phm = cneg(I);
-                const u32 dcn = par64(delt & c);
-                if (lst) {
-                  for (u32 i = lane; i < cnt; i += 32) {
-                    const u32 j = L[i];
-                    A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
-                  }
-                } else {
-                  const u32 nsz = 1u << kcur;
-                  for (u32 j = lane; j < nsz; j += 32)
-                    A[j] = cmul(A[j], (dcn ^ par32(j & dm)) ? phm : php);
-                }
-                __syncwarp();
-                c ^= beta;
-                mbytes += 2ull * kEntryBytes * cnt + 2ull * ((2 * n + 7) / 8);
-              };
-              // owning noise instruction of location l: last m with loc0(m) <= l
-              auto owner = [&](u32 l) -> const u64 * {
-                u32 lo = 0, hi = P.nnoise;
-                while (hi - lo > 1) {
-                  const u32 mid = (lo + hi) >> 1;
-                  if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= l) lo = mid; else hi = mid;
-                }
-                return tables + P.noise_off + 4ull * lo;
-              };
-              if (geo) {
-                // Philox: walk the candidate schedule (lane-uniform, rare)
-                fire_pc = 0xFFFFFFFFu;
-                while (gpos < P.nlocs) {
-                  const u64 *nrec = owner(gpos);
-                  const u64 nw0 = __ldg(nrec);
-                  const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-                  if (ipc > pc) { fire_pc = ipc; break; }
-                  const u32 loc0 = (u32)__ldg(nrec + 1);
-                  u64 ex = 0, ez = 0;
-                  while (gpos < loc0 + nloc) {
-                    const u32 l = gpos;
-                    bool ok = true;
-                    if (!P.noise_uniform) ok = geo_accept(rng.master, wshot, gj - 1, __ldg(tables + P.acc_off + l));
-                    if (ok) {
-                      const u64 lw = __ldg(locs + 2ull * l);
-                      const u32 qa = (u32)(lw >> 32) & 0xff, qb = (u32)(lw >> 40) & 0xff,
-                                nk = (u32)(lw >> 48) & 3;
-                      const double u = (double)gpick * 0x1.0p-53;
-                      if (nk == NK_DEP1) {
-                        int code = 1 + (int)(u * 3.0);
-                        code = code > 3 ? 3 : code;
-                        ex |= (u64)(code != 3) << qa;
-                        ez |= (u64)(code != 1) << qa;
-                      } else if (nk == NK_DEP2) {
-                        int pick = 1 + (int)(u * 15.0);
-                        pick = pick > 15 ? 15 : pick;
-                        const int ca = pick & 3, cbq = pick >> 2;
-                        if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
-                        if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
-                      } else if (nk == NK_XERR) {
-                        ex |= 1ull << qa;
-                      } else {
-                        ez |= 1ull << qa;
-                      }
-                    }
-                    const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, rng.master, wshot, gj, l + 1);
-                    gpos = gc.pos;
-                    gpick = gc.pick;
-                    ++gj;
-                  }
-                  apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
-                }
-              } else {
-              while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= pc) {
-                // one fire draw per location of word `scanned`, one lane each
-                const u32 l = scanned * 32u + lane;
-                bool fire = false;
-                if (l < P.nlocs) {
-                  const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
-                  fire = rng.m53((u32)lw) < thr;
-                }
-                const u32 bits = __ballot_sync(FULL, fire);
-                if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
-                ++scanned;
-              }
-              __syncwarp();
-              next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
-              fire_pc = 0xFFFFFFFFu;
-              for (;;) {
-                // next fired location >= cursor among the scanned words
-                u32 fl_loc = 0xFFFFFFFFu;
-                u32 w = max(search_w, cursor >> 5);
-                for (; w < scanned; ++w) {
-                  u32 bits = win[w & (kWinWords - 1)];
-                  if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
-                  if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
-                }
-                search_w = w;
-                if (fl_loc == 0xFFFFFFFFu) break;
-                const u64 *nrec = owner(fl_loc);
-                const u64 nw0 = __ldg(nrec);
-                const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-                if (ipc > pc) { fire_pc = ipc; break; }
-                const u32 loc0 = (u32)__ldg(nrec + 1);
-                cursor = loc0 + nloc;
-                // build E = OR of fired letters (ref noise.py:68-100)
-                u64 ex = 0, ez = 0;
-                for (u32 i = lane; i < nloc; i += 32) {
-                  const u32 l = loc0 + i;
-                  if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
-                  const u64 lw = __ldg(locs + 2ull * l);
-                  const u32 d = (u32)lw, qa = (u32)(lw >> 32) & 0xff,
-                            qb = (u32)(lw >> 40) & 0xff, nk = (u32)(lw >> 48) & 3;
-                  if (nk == NK_DEP1) {
-                    int code = 1 + (int)(rng.uniform(d + 1) * 3.0);
-                    code = code > 3 ? 3 : code;
-                    ex |= (u64)(code != 3) << qa;
-                    ez |= (u64)(code != 1) << qa;
-                  } else if (nk == NK_DEP2) {
-                    int pick = 1 + (int)(rng.uniform(d + 1) * 15.0);
-                    pick = pick > 15 ? 15 : pick;
-                    const int ca = pick & 3, cbq = pick >> 2;
-                    if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
-                    if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
-                  } else if (nk == NK_XERR) {
-                    ex |= 1ull << qa;
-                  } else {
-                    ez |= 1ull << qa;
-                  }
-                }
-                ex = warp_or64(ex);
-                ez = warp_or64(ez);
-                apply_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3));
-              }
-              }
-            }
-
-            const u64 *op = ops + pc;
-            const u64 h = hnext;
-            const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
-            const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
-            const u32 instr = (u32)(h >> 32);
-            pc += len;
-            hnext = __ldg(ops + pc);       // prefetch the next header
-            kcur = k;
-            const u32 size = 1u << k;
-
-            if (kind == OP_T || kind == OP_GROW_LIMIT) {
-              sig_lo ^= __ldg(op + 1);
-              sig_hi ^= __ldg(op + 2);
-              // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
-              // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
-              const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
-              const u64 delta = __ldg(op + 5);
-              const u64 w6 = __ldg(op + 6);
-              const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
-              const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
-              const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
-              mbytes += __ldg(op + 11);
-              const double2 bx0 = flip ? cneg(bxs) : bxs;
-              const double2 bx1 = cneg(bx0);
-              const u32 dc = par64(delta & c);
-              const u32 tcase = fl & 3u;
-              if (tcase == T_DIAG) {
-                // beta == 0: pure phase per entry (ref state.py:120-126)
-                const double2 f0 = cadd(a, bx0), f1 = cadd(a, bx1);
-                if (lst) {
-                  for (u32 i = lane; i < cnt; i += 32) {
-                    const u32 j = L[i];
-                    A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
-                  }
-                } else {
-                  for (u32 j = lane; j < size; j += 32)
-                    A[j] = cmul(A[j], (dc ^ par32(j & dmask)) ? f1 : f0);
-                }
-                __syncwarp();
-                mbytes += 32ull * cnt;
-                continue;
-              }
-              const u32 cin = cnt;
-              if (kind == OP_GROW_LIMIT) {
-                u32 nz = 0;
-                for (u32 j = lane; j < size; j += 32) {
-                  const double2 v = A[j];
-                  const u32 s = dc ^ par32(j & dmask);
-                  nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
-                  nz += abs2(cadd(Z, cmul(s ? bx1 : bx0, v))) > kPrune2;
-                }
-                nz = warp_sum_u32(nz);
-                status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
-                aux = (int)instr;
-                break;
-              }
-              const bool grow = tcase == T_GROW;
-              u32 ncnt = 0;
-              if (lst && cnt <= scap && size >= kSparseMin) {
-                // ---- sparse merge (<= 32 entries, one per lane): each listed
-                // entry owns its pair unless it is the upper member of a pair whose
-                // lower member is listed too (ref state.py:127-129, 294-306)
-                const bool valid = lane < cnt;
-                if (grow) {
-                  for (u32 m = lane; m < size; m += 32) A[size + m] = Z;
-                  __syncwarp();
-                }
-                const u32 j = valid ? L[lane] : 0u;
-                const double2 vj = valid ? A[j] : Z;
-                const u32 p = grow ? j + size : (j ^ cb);
-                const double2 vp = (valid && !grow) ? A[p] : Z;
-                const bool proc = valid && (grow || !(((j >> (31 - __clz(cb))) & 1u) && nonzero(vp)));
-                __syncwarp();
-                bool nz0 = false, nz1 = false;
-                if (proc) {
-                  const double2 aterm = cmul(a, vj);
-                  const u32 sj = dc ^ par32(j & dmask);
-                  double2 n0, n1;
-                  if (grow) {
-                    n0 = prune(aterm);
-                    n1 = prune(cmul(sj ? bx1 : bx0, vj));
-                  } else {
-                    const u32 sp = dc ^ par32(p & dmask);
-                    n0 = prune(cadd(aterm, cmul(sp ? bx1 : bx0, vp)));
-                    n1 = prune(cadd(cmul(a, vp), cmul(sj ? bx1 : bx0, vj)));
-                  }
-                  A[j] = n0;
-                  A[p] = n1;
-                  nz0 = nonzero(n0);
-                  nz1 = nonzero(n1);
-                }
-                __syncwarp();
-                list_push(L, ncnt, nz0, j, lane);
-                list_push(L, ncnt, nz1, p, lane);
-                __syncwarp();
-                lst = true;
-              } else {
-                // ---- dense merge over all coordinates
-                u32 nz = 0;
-                if (!grow) {
-                  const u32 hb = 31 - __clz(cb);
-                  const u32 half = size >> 1;
-                  for (u32 m = lane; m < half; m += 32) {
-                    const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
-                    const double2 v0 = A[j0], v1 = A[j1];
-                    const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
-                    const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
-                    const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
-                    A[j0] = n0;
-                    A[j1] = n1;
-                    nz += nonzero(n0) + nonzero(n1);
-                  }
-                } else {
-                  for (u32 j = lane; j < size; j += 32) {
-                    const double2 v = A[j];
-                    const u32 s = dc ^ par32(j & dmask);
-                    const double2 n0 = prune(cmul(a, v));
-                    const double2 n1 = prune(cmul(s ? bx1 : bx0, v));
-                    A[j] = n0;
-                    A[size + j] = n1;
-                    nz += nonzero(n0) + nonzero(n1);
-                  }
-                }
-                __syncwarp();
-                ncnt = warp_sum_u32(nz);
-                const u32 nsz = grow ? 2 * size : size;
-                lst = ncnt <= scap && nsz >= kSparseMin;
-                if (lst) build_list(A, L, nsz, lane);
-              }
-              if (grow) kcur = k + 1;
-              cnt = ncnt;
-              mbytes += (u64)kEntryBytes * (cin + cnt);
-              if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr; break; }
-              if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-              continue;
-            }
-
-            if (kind == OP_MEAS) {
-              sig_lo ^= __ldg(op + 1);
-              sig_hi ^= __ldg(op + 2);
-              const u32 mcase = fl & 3u;
-              const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
-              const u64 delta = __ldg(op + 5);
-              const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
-              const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
-              const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
-              const u64 vec = __ldg(op + 8);
-              const u64 w13 = __ldg(op + 13);
-              const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
-              mbytes += __ldg(op + 17);
-              const u32 dc = par64(delta & c);
-              // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
-              // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
-              auto pick_plus = [&](double pplus) -> bool {
-                if (pplus >= 1.0) return true;
-                if (pplus <= 0.0) return false;
-                return rng.uniform(udraw) < pplus;
-              };
-              const u32 cin = cnt;
-              const bool compact = (fl & MF_COMPACT) != 0;
-              bool plus;
-              if (mcase == M_DET && size <= GS_SMALL_MAX) {
-                // <= 4 amplitudes: every lane evaluates the whole measurement from
-                // broadcast loads -- no cross-lane reductions (ref state.py:162-176)
-                const u32 neg0 = (xi0 >> 1) ^ dc;
-                double2 v[4];
-                double sp = 0.0, sm = 0.0;
-      #pragma unroll
-                for (u32 e = 0; e < 4; ++e) {
-                  v[e] = e < size ? A[e] : Z;
-                  if (e < size) {
-                    const double a2 = abs2(v[e]);
-                    if (neg0 ^ par32(e & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
-                  }
-                }
-                plus = pick_plus(sp);
-                const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-                if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-                const u32 want_neg = plus ? 0u : 1u;
-                u32 nk = 0;
-      #pragma unroll
-                for (u32 e = 0; e < 4; ++e)
-                  nk += (e < size) && ((neg0 ^ par32(e & dmask)) == want_neg) && nonzero(v[e]);
-                if (nk == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-                const double rs = inv_sqrt_norm(plus ? sp : sm);
-                __syncwarp();
-                if (compact) {
-                  const u32 tau = want_neg ^ neg0;
-                  if (tau) c ^= vec;
-                  if (lane < (size >> 1)) {
-                    const u32 j0 = ins_bit(lane, isq, 0);
-                    const u32 src = j0 | ((tau ^ par32(j0 & dmask)) << isq);
-                    const double2 vs = src == 0 ? v[0] : src == 1 ? v[1] : src == 2 ? v[2] : v[3];
-                    A[lane] = cscale(vs, rs);
-                  }
-                  kcur = k - 1;
-                } else if (lane < size) {
-                  const double2 vl = lane == 0 ? v[0] : lane == 1 ? v[1] : lane == 2 ? v[2] : v[3];
-                  A[lane] = ((neg0 ^ par32(lane & dmask)) == want_neg) ? cscale(vl, rs) : Z;
-                }
-                __syncwarp();
-                cnt = nk;
-              } else if (mcase == M_DET) {
-                // beta == 0: filter by eigenvalue (ref state.py:162-176)
-                const u32 neg0 = (xi0 >> 1) ^ dc;
-                double sp = 0.0, sm = 0.0;
-                if (lst && cnt <= scap && size >= kSparseMin) {
-                  const bool valid = lane < cnt;
-                  const u32 j = valid ? L[lane] : 0u;
-                  const double2 v = valid ? A[j] : Z;
-                  const bool ng = (neg0 ^ par32(j & dmask)) != 0;
-                  const double a2 = abs2(v);
-                  if (valid) {
-                    if (ng) sm = a2; else sp = a2;
-                  }
-                  sp = warp_sum_live(sp, cnt);
-                  sm = warp_sum_live(sm, cnt);
-                  plus = pick_plus(sp);
-                  const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  const bool keep = valid && (ng == !plus);
-                  const double rs = inv_sqrt_norm(plus ? sp : sm);
-                  u32 dst = j;
-                  if (compact) {
-                    const u32 tau = (plus ? 0u : 1u) ^ neg0;
-                    if (tau) c ^= vec;
-                    if (valid) A[j] = Z;
-                    __syncwarp();
-                    dst = ((j >> (isq + 1)) << isq) | (j & ((1u << isq) - 1u));
-                    if (keep) A[dst] = cscale(v, rs);
-                    kcur = k - 1;
-                  } else if (valid) {
-                    A[j] = keep ? cscale(v, rs) : Z;
-                  }
-                  u32 ncnt = 0;
-                  list_push(L, ncnt, keep, dst, lane);
-                  __syncwarp();
-                  cnt = ncnt;
-              } else {
-                  for (u32 j = lane; j < size; j += 32) {
-                    const double a2 = abs2(A[j]);
-                    if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2);
-                    else sp = __dadd_rn(sp, a2);
-                  }
-                  sp = warp_sum_live(sp, size);
-                  sm = warp_sum_live(sm, size);
-                  plus = pick_plus(sp);
-                  const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  const u32 want_neg = plus ? 0u : 1u;
-                  const double rs = inv_sqrt_norm(plus ? sp : sm);
-                  u32 nz = 0;
-                  u32 nsize = size;
-                  if (compact) {
-                    const u32 tau = want_neg ^ neg0;
-                    const u32 half = size >> 1;
-                    for (u32 base = 0; base < half; base += 32) {
-                      const u32 jp = base + lane;
-                      double2 v = Z;
-                      if (jp < half) {
-                        const u32 j0 = ins_bit(jp, isq, 0);
-                        v = A[j0 | ((tau ^ par32(j0 & dmask)) << isq)];
-                      }
-                      __syncwarp();
-                      if (jp < half) {
-                        v = cscale(v, rs);
-                        A[jp] = v;
-                        nz += nonzero(v);
-                      }
-                      __syncwarp();
-                    }
-                    if (tau) c ^= vec;
-                    kcur = k - 1;
-                    nsize = half;
-                  } else {
-                    for (u32 j = lane; j < size; j += 32) {
-                      const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
-                      const double2 v = keep ? cscale(A[j], rs) : Z;
-                      A[j] = v;
-                      nz += nonzero(v);
-                    }
-                    __syncwarp();
-                  }
-                  cnt = warp_sum_u32(nz);
-                  lst = cnt <= scap && nsize >= kSparseMin;
-                  if (lst) build_list(A, L, nsize, lane);
-                }
-              } else {
-                // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
-                const double2 I = ipow(xi0);
-                const double2 xpp = I;            // i^xi0 * (+1), exact
-                const double2 xpm = cneg(I);
-                const u32 ct = (u32)(c >> t) & 1u;
-                const bool span = mcase == M_PIVOT_SPAN;
-                if (size <= GS_SMALL_MAX) {
-                  // <= 4 amplitudes: redundant per-lane evaluation, no reductions
-                  double2 v[4];
-      #pragma unroll
-                  for (u32 e = 0; e < 4; ++e) v[e] = e < size ? A[e] : Z;
-                  const u32 npairs = span ? (size >> 1) : size;
-                  // w(m, sign) for pair / entry m: rep + sign * xi_part * part
-                  auto pair_w = [&](u32 m, bool plus_branch) -> double2 {
-                    if (span) {
-                      const u32 j0 = ins_bit(m, isq, 0);
-                      const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-                      const u32 part = rep ^ cb;
-                      const double2 vr = rep == 0 ? v[0] : rep == 1 ? v[1] : rep == 2 ? v[2] : v[3];
-                      const double2 vp = part == 0 ? v[0] : part == 1 ? v[1] : part == 2 ? v[2] : v[3];
-                      const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, vp);
-                      return plus_branch ? cadd(vr, prod) : csub(vr, prod);
-                    }
-                    const double2 vm = m == 0 ? v[0] : m == 1 ? v[1] : m == 2 ? v[2] : v[3];
-                    if (ct ^ par32(m & tmask)) {
-                      const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, vm);
-                      return plus_branch ? cadd(Z, prod) : csub(Z, prod);
-                    }
-                    return vm;
-                  };
-                  double sp = 0.0;
-      #pragma unroll
-                  for (u32 m = 0; m < 4; ++m)
-                    if (m < npairs) sp = __dadd_rn(sp, abs2(pair_w(m, true)));
-                  const double pp = __dmul_rn(0.5, sp);
-                  plus = pick_plus(pp);
-                  const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  double sk = 0.0;
-                  u32 nz = 0;
-                  double2 wp[4];
-      #pragma unroll
-                  for (u32 m = 0; m < 4; ++m) {
-                    wp[m] = m < npairs ? prune(pair_w(m, plus)) : Z;
-                    sk = __dadd_rn(sk, abs2(wp[m]));
-                    nz += nonzero(wp[m]);
-                  }
-                  if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  const double rs = inv_sqrt_norm(sk);
-                  __syncwarp();
-                  if (lane < npairs) {
-                    const double2 wl = lane == 0 ? wp[0] : lane == 1 ? wp[1] : lane == 2 ? wp[2] : wp[3];
-                    A[lane] = cscale(wl, rs);
-                  }
-                  __syncwarp();
-                  if (span) kcur = k - 1;
-                  cnt = nz;
-                } else if (lst && cnt <= scap && size >= kSparseMin) {
-                  const bool valid = lane < cnt;
-                  const u32 j = valid ? L[lane] : 0u;
-                  const bool is_part = (ct ^ par32(j & tmask)) != 0;
-                  u32 rep = j;
-                  double2 vr = Z, pr = Z;
-                  bool proc = valid;
-                  if (valid) {
-                    if (span) {
-                      const u32 other = j ^ cb;
-                      rep = is_part ? other : j;
-                      const u32 part = is_part ? j : other;
-                      vr = A[rep];
-                      proc = !(is_part && nonzero(vr));
-                      pr = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
-                    } else if (is_part) {
-                      pr = cmul((dc ^ par32(j & dmask)) ? xpm : xpp, A[j]);  // rep absent
-                    } else {
-                      vr = A[j];
-                    }
-                  }
-                  const double sp = warp_sum_live(proc ? abs2(cadd(vr, pr)) : 0.0, cnt);
-                  const double pp = __dmul_rn(0.5, sp);
-                  plus = pick_plus(pp);
-                  const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  double2 w = Z;
-                  if (proc) w = prune(plus ? cadd(vr, pr) : csub(vr, pr));
-                  const bool wnz = nonzero(w);
-                  const double sk = warp_sum_live(abs2(w), cnt);
-                  if (!__any_sync(FULL, wnz)) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  const double rs = inv_sqrt_norm(sk);
-                  u32 dst = rep;
-                  if (span) {
-                    __syncwarp();
-                    if (proc) { A[rep] = Z; A[rep ^ cb] = Z; }
-                    __syncwarp();
-                    dst = ((rep >> (isq + 1)) << isq) | (rep & ((1u << isq) - 1u));
-                    kcur = k - 1;
-                  }
-                  if (proc) A[dst] = wnz ? cscale(w, rs) : Z;
-                  u32 ncnt = 0;
-                  list_push(L, ncnt, wnz, dst, lane);
-                  __syncwarp();
-                  cnt = ncnt;
-              } else {
-                  double sp = 0.0;
-                  const u32 npairs = span ? (size >> 1) : size;
-                  for (u32 m = lane; m < npairs; m += 32) {
-                    double2 wpv;
-                    if (span) {
-                      const u32 j0 = ins_bit(m, isq, 0);
-                      const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-                      const u32 part = rep ^ cb;
-                      wpv = cadd(A[rep], cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]));
-                    } else {
-                      const double2 v = A[m];
-                      wpv = (ct ^ par32(m & tmask)) ? cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v)) : v;
-                    }
-                    sp = __dadd_rn(sp, abs2(wpv));
-                  }
-                  sp = warp_sum_live(sp, npairs);
-                  const double pp = __dmul_rn(0.5, sp);
-                  plus = pick_plus(pp);
-                  const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-                  if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  double sk = 0.0;
-                  u32 nz = 0;
-                  for (u32 m = lane; m < npairs; m += 32) {
-                    double2 w;
-                    u32 dst;
-                    if (span) {
-                      const u32 j0 = ins_bit(m, isq, 0);
-                      const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
-                      const u32 part = rep ^ cb;
-                      const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, A[part]);
-                      w = plus ? cadd(A[rep], prod) : csub(A[rep], prod);
-                      dst = rep;
-                    } else {
-                      const double2 v = A[m];
-                      if (ct ^ par32(m & tmask)) {
-                        const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
-                        w = plus ? cadd(Z, prod) : csub(Z, prod);
-                      } else {
-                        w = v;
-                      }
-                      dst = m;
-                    }
-                    w = prune(w);
-                    A[dst] = w;
-                    sk = __dadd_rn(sk, abs2(w));
-                    nz += nonzero(w);
-                  }
-                  __syncwarp();
-                  sk = warp_sum_live(sk, npairs);
-                  nz = warp_sum_u32(nz);
-                  if (nz == 0) { status = ST_CORRUPT; aux = (int)instr; break; }
-                  const double rs = inv_sqrt_norm(sk);
-                  u32 nsize = size;
-                  if (span) {
-                    const u32 half = size >> 1;
-                    for (u32 base = 0; base < half; base += 32) {
-                      const u32 jp = base + lane;
-                      double2 v = Z;
-                      if (jp < half) {
-                        const u32 j0 = ins_bit(jp, isq, 0);
-                        v = A[j0 | ((ct ^ par32(j0 & tmask)) << isq)];
-                      }
-                      __syncwarp();
-                      if (jp < half) A[jp] = cscale(v, rs);
-                      __syncwarp();
-                    }
-                    kcur = k - 1;
-                    nsize = half;
-                  } else {
-                    for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], rs);
-                    __syncwarp();
-                  }
-                  cnt = nz;
-                  lst = cnt <= scap && nsize >= kSparseMin;
-                  if (lst) build_list(A, L, nsize, lane);
-                }
-                if (ct) c ^= vec;
-                // tableau sign update of the pivot (ref tableau.py:176-200)
-                const u32 v = (u32)(sig_hi >> t) & 1u;
-                if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
-                sig_lo ^= __ldg(op + 11);
-                sig_hi ^= __ldg(op + 12);
-                sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
-                sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
-              }
-              mbytes += (u64)kEntryBytes * (cin + cnt);
-              const u32 bout = plus ? 0u : 1u;
-              u32 rb = bout;
-              if ((fl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
-              if (fl & MF_RECORD) {
-                if (lane == 0 && rb) recw[(slot >> 5) * 32u] |= 1u << (slot & 31);
-                __syncwarp();
-              }
-              if ((fl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
-              continue;
-            }
-
-            if (kind == OP_FEEDBACK) {
-              const u32 idx = (u32)__ldg(op + 1);
-              if ((recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u) {
-                sig_lo ^= __ldg(op + 2);
-                sig_hi ^= __ldg(op + 3);
-                mbytes += __ldg(op + 4);
-              }
-              continue;
-            }
-
-            if (kind == OP_DETECTOR || kind == OP_OBSERVABLE) {
-              const u64 w1 = __ldg(op + 1);
-              const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
-              const u64 off = __ldg(op + 2);
-              u32 bb = 0;
-              for (u32 i = lane; i < nidx; i += 32) {
-                const u32 idx = (u32)__ldg(tables + off + i);
-                bb ^= (recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u;
-              }
-              const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
-              if (kind == OP_DETECTOR) {
-                if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
-              } else {
-                obs ^= (u64)parity << id;
-              }
-              continue;
-            }
-
-            if (kind == OP_END) {
-              sig_lo ^= __ldg(op + 1);
-              sig_hi ^= __ldg(op + 2);
-              mbytes += __ldg(op + 3);
-              status = ST_PRESERVED;
-              break;
-            }
-            status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
-            aux = -2;
-            }
-          }
-          // hand the shot back to its lane
-          __syncwarp();
-          if (lane == s) {
-            s_lo = sig_lo; s_hi = sig_hi; sc = c; sobs = obs; smb = mbytes;
-            scnt = cnt; sk = kcur; sst = status; saux = aux;
-            sgj = gj; sgpos = gpos; sgpick = gpick; sfire = fire_pc;
-          }
-          if (status == ST_RUNNING) {
-            for (u32 j = lane; j < (1u << kcur); j += 32) An[j * 32u + s] = A[j];
-          } else if (O.mode == MODE_DUMP) {
-            const u64 ssl = base + s;
-            if (lane == 0) {
-              O.sig[2 * ssl] = sig_lo;
-              O.sig[2 * ssl + 1] = sig_hi;
-              O.cvec[ssl] = c;
-              O.dim[ssl] = kcur;
-            }
-            const u64 stride = 1ull << P.max_dim;
-            for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[ssl * stride + j] = A[j];
-            if (lane == s) dumped = true;
-          }
-          __syncwarp();
+        __syncwarp();
+        const u32 exit_pc = wide_section<kSmemChi>(P, R, O, base, pc, nm, h, live, win, recb, An,
+                                                   A, stash);
+        // every lane takes its state back
+        s_lo = stash[SF_LO * 32 + lane];
+        s_hi = stash[SF_HI * 32 + lane];
+        sc = stash[SF_C * 32 + lane];
+        sobs = stash[SF_OBS * 32 + lane];
+        smb = stash[SF_MB * 32 + lane];
+        sgpick = stash[SF_PICK * 32 + lane];
+        seed = stash[SF_SEED * 32 + lane];
+        shot = stash[SF_SHOT * 32 + lane];
+        {
+          const u64 ck = stash[SF_CNTK * 32 + lane], st = stash[SF_ST * 32 + lane],
+                    g = stash[SF_GEO * 32 + lane];
+          scnt = (u32)ck; sk = (u32)(ck >> 32);
+          sst = (int)(st & 0xff); saux = (int)(u32)(st >> 32); dumped = ((st >> 8) & 1u) != 0;
+          sgj = (u32)g; sgpos = (u32)(g >> 32);
+          sfire = (u32)stash[SF_FIRE * 32 + lane];
         }
+        __syncwarp();
         if (exit_pc == 0xFFFFFFFFu) break;   // no shot survived the section
         pc = exit_pc;
         while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) < pc) ++nm;
         continue;
       }
-
       // ============================== narrow op, lane per shot
+      // @region narrow: noise
+      // apply E to this lane's shot (ref state.py:88-102)
+      auto lane_error = [&](u64 ex, u64 ez, const u64 *nrec, u32 size) {
+        const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3), s_lo, s_hi);
+        const double2 php = ipow(e.xi);
+        const double2 phm = cneg(php);
+        const u32 dcn = par64(e.delt & sc);
+#pragma unroll 1
+        for (u32 j = 0; j < size; ++j) AN(j) = cmul(AN(j), (dcn ^ par32(j & e.dm)) ? phm : php);
+        sc ^= e.beta;
+        smb += 2ull * kEntryBytes * scnt + sign_bytes;
+      };
       const u64 *op = ops + pc;
       const u32 size = 1u << k;
       // ---- noise instructions inserted before this op
       if (!philox) {
+#pragma unroll 1
         for (; nm < P.nnoise; ++nm) {
           const u64 *nrec = tables + P.noise_off + 4ull * nm;
           const u64 nw0 = __ldg(nrec);
@@ -1247,28 +1196,24 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           if (sst != ST_RUNNING) continue;
           const u32 nloc = (u32)(nw0 >> 32), loc0 = (u32)__ldg(nrec + 1);
           u64 ex = 0, ez = 0;
+#pragma unroll 1
           for (u32 l = loc0; l < loc0 + nloc; ++l) {
             const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
             const u32 d = (u32)lw;
             if ((splitmix(seed, d) >> 11) < thr) {
               const u32 nk = (u32)(lw >> 48) & 3;
               const double u = nk <= NK_DEP2 ? (double)(splitmix(seed, d + 1) >> 11) * 0x1.0p-53 : 0.0;
-              letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+              noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
             }
           }
-          if (ex | ez) lane_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3), size);
+          if (ex | ez) lane_error(ex, ez, nrec, size);
         }
       } else {
         while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) <= pc) ++nm;
         if (sst == ST_RUNNING && pc >= sfire) {
           sfire = 0xFFFFFFFFu;
           while (sgpos < P.nlocs) {
-            u32 lo = 0, hi = P.nnoise;
-            while (hi - lo > 1) {
-              const u32 mid = (lo + hi) >> 1;
-              if ((u32)__ldg(tables + P.noise_off + 4ull * mid + 1) <= sgpos) lo = mid; else hi = mid;
-            }
-            const u64 *nrec = tables + P.noise_off + 4ull * lo;
+            const u64 *nrec = noise_owner(P, sgpos);
             const u64 nw0 = __ldg(nrec);
             const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
             if (ipc > pc) { sfire = ipc; break; }
@@ -1280,15 +1225,15 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
               if (!P.noise_uniform) ok = geo_accept(R.master, shot, sgj - 1, __ldg(tables + P.acc_off + l));
               if (ok) {
                 const u64 lw = __ldg(locs + 2ull * l);
-                letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
-                       (double)sgpick * 0x1.0p-53, ex, ez);
+                noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
+                             (double)sgpick * 0x1.0p-53, ex, ez);
               }
               const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, shot, sgj, l + 1);
               sgpos = gc.pos;
               sgpick = gc.pick;
               ++sgj;
             }
-            if (ex | ez) lane_error(ex, ez, __ldg(nrec + 2), __ldg(nrec + 3), size);
+            if (ex | ez) lane_error(ex, ez, nrec, size);
           }
         }
       }
@@ -1296,6 +1241,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
       if (sst != ST_RUNNING) continue;
       sk = k;
 
+      // @region narrow: T
       if (kind == OP_T) {
         s_lo ^= __ldg(op + 1);
         s_hi ^= __ldg(op + 2);
@@ -1313,6 +1259,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         if (tcase == T_DIAG) {
           // beta == 0: pure phase per entry (ref state.py:120-126)
           const double2 f0 = cadd(a, bx0), f1 = cadd(a, bx1);
+#pragma unroll 1
           for (u32 j = 0; j < size; ++j) AN(j) = cmul(AN(j), (dc ^ par32(j & dmask)) ? f1 : f0);
           smb += 32ull * scnt;
           continue;
@@ -1322,6 +1269,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         u32 nz = 0;
         if (tcase == T_BUTTERFLY) {
           const u32 hb = 31 - __clz(cb);
+#pragma unroll 1
           for (u32 m = 0; m < (size >> 1); ++m) {
             const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
             const double2 v0 = AN(j0), v1 = AN(j1);
@@ -1333,6 +1281,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             nz += nonzero(n0) + nonzero(n1);
           }
         } else {
+#pragma unroll 1
           for (u32 j = 0; j < size; ++j) {
             const double2 v = AN(j);
             const u32 sj = dc ^ par32(j & dmask);
@@ -1351,6 +1300,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         continue;
       }
 
+      // @region narrow: meas
       if (kind == OP_MEAS) {
         s_lo ^= __ldg(op + 1);
         s_hi ^= __ldg(op + 2);
@@ -1379,6 +1329,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
           double sp = 0.0, sm = 0.0;
+#pragma unroll 1
           for (u32 j = 0; j < size; ++j) {
             const double a2 = abs2(AN(j));
             if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
@@ -1390,6 +1341,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const double rs = inv_sqrt_norm(plus ? sp : sm);
           if (fl & MF_COMPACT) {
             const u32 tau = want_neg ^ neg0;
+#pragma unroll 1
             for (u32 jp = 0; jp < (size >> 1); ++jp) {
               const u32 j0 = ins_bit(jp, isq, 0);
               const double2 v = cscale(AN(j0 | ((tau ^ par32(j0 & dmask)) << isq)), rs);
@@ -1399,6 +1351,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
             if (tau) sc ^= vec;
             sk = k - 1;
           } else {
+#pragma unroll 1
             for (u32 j = 0; j < size; ++j) {
               const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
               const double2 v = keep ? cscale(AN(j), rs) : Z;
@@ -1414,6 +1367,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const bool span = mcase == M_PIVOT_SPAN;
           const u32 npairs = span ? (size >> 1) : size;
           double sp = 0.0;
+#pragma unroll 1
           for (u32 m = 0; m < npairs; ++m) {
             double2 wpv;
             if (span) {
@@ -1432,6 +1386,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const double chosen = plus ? pp : __dsub_rn(1.0, pp);
           if (chosen < 1e-12) { sst = ST_CORRUPT; saux = (int)instr; continue; }
           double sk2 = 0.0;
+#pragma unroll 1
           for (u32 m = 0; m < npairs; ++m) {
             double2 w;
             u32 dst;
@@ -1460,12 +1415,14 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           if (nz == 0) { sst = ST_CORRUPT; saux = (int)instr; continue; }
           const double rs = inv_sqrt_norm(sk2);
           if (span) {
+#pragma unroll 1
             for (u32 jp = 0; jp < (size >> 1); ++jp) {
               const u32 j0 = ins_bit(jp, isq, 0);
               AN(jp) = cscale(AN(j0 | ((ct ^ par32(j0 & tmask)) << isq)), rs);
             }
             sk = k - 1;
           } else {
+#pragma unroll 1
             for (u32 j = 0; j < size; ++j) AN(j) = cscale(AN(j), rs);
           }
           if (ct) sc ^= vec;
@@ -1487,6 +1444,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         continue;
       }
 
+      // @region narrow: feedback/detector/end
       if (kind == OP_FEEDBACK) {
         const u32 idx = (u32)__ldg(op + 1);
         if ((recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u) {
@@ -1502,6 +1460,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
         const u64 off = __ldg(op + 2);
         u32 parity = 0;
+#pragma unroll 1
         for (u32 i = 0; i < nidx; ++i) {
           const u32 idx = (u32)__ldg(tables + off + i);
           parity ^= (recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u;
@@ -1526,30 +1485,45 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
     }
     __syncwarp();
 
-    // -------------------------------------------------------- shot outputs
+    // @region outputs
+    {
+      const u32 pres = __ballot_sync(FULL, valid && sst == ST_PRESERVED);
+      const u32 errb = __ballot_sync(FULL, valid && sst == ST_PRESERVED && sobs != 0);
+      const u32 disc = __ballot_sync(FULL, valid && sst == ST_DISCARDED);
+      const u32 ovf = __ballot_sync(FULL, valid && sst == ST_OVERFLOW);
+      const u32 cor = __ballot_sync(FULL, valid && sst == ST_CORRUPT);
+      const u32 uns = __ballot_sync(FULL, valid && sst == ST_UNSUPPORTED);
+      const u32 val = __ballot_sync(FULL, valid);
+      u64 mb = valid ? smb : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mb += __shfl_xor_sync(FULL, mb, o);
+      if (lane == 0) {
+        wcnt[WC_TOT] += __popc(val);
+        wcnt[WC_PRES] += __popc(pres);
+        wcnt[WC_DISC] += __popc(disc);
+        wcnt[WC_OVF] += __popc(ovf);
+        wcnt[WC_COR] += __popc(cor);
+        wcnt[WC_UNS] += __popc(uns);
+        wcnt[WC_ERR] += __popc(errb);
+        wcnt[WC_MB] += mb;
+      }
+    }
     if (valid) {
-      n_tot += 1;
-      mbytes_all += smb;
-      if (sst == ST_PRESERVED) {
-        n_pres += 1;
-        if (sobs) {
-          n_err += 1;
-          for (u64 o = sobs; o; o &= o - 1)
-            atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
-          if (O.witness) {
-            const u32 wi = atomicAdd(O.witness_count, 1u);
-            if (wi < O.witness_cap) O.witness[wi] = shot;
-          }
+      if (sst == ST_PRESERVED && sobs) {
+#pragma unroll 1
+        for (u64 o = sobs; o; o &= o - 1)
+          atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
+        if (O.witness) {
+          const u32 wi = atomicAdd(O.witness_count, 1u);
+          if (wi < O.witness_cap) O.witness[wi] = shot;
         }
-      } else if (sst == ST_DISCARDED) n_disc += 1;
-      else if (sst == ST_OVERFLOW) n_ovf += 1;
-      else if (sst == ST_CORRUPT) n_cor += 1;
-      else n_uns += 1;
+      }
       if (O.mode != MODE_COUNTERS) {
         O.status[sl] = (u8)sst;
         O.aux[sl] = saux;
         O.obs[sl] = sobs;
         const u32 rw64 = (P.nmeas + 63) / 64;
+#pragma unroll 1
         for (u32 w = 0; w < rw64; ++w) {
           const u32 lo = recb[(2 * w) * 32u + lane];
           const u32 hi = (2 * w + 1 < P.rec_words32) ? recb[(2 * w + 1) * 32u + lane] : 0u;
@@ -1561,6 +1535,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           O.cvec[sl] = sc;
           O.dim[sl] = sk;
           const u64 stride = 1ull << P.max_dim;
+#pragma unroll 1
           for (u32 j = 0; j < (1u << sk); ++j) O.amps[sl * stride + j] = AN(j);
         }
       }
@@ -1568,31 +1543,16 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
     __syncwarp();
   }
 #undef AN
-  // warp totals, one atomic per counter per warp
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    n_tot += __shfl_xor_sync(FULL, n_tot, o);
-    n_pres += __shfl_xor_sync(FULL, n_pres, o);
-    n_disc += __shfl_xor_sync(FULL, n_disc, o);
-    n_ovf += __shfl_xor_sync(FULL, n_ovf, o);
-    n_cor += __shfl_xor_sync(FULL, n_cor, o);
-    n_uns += __shfl_xor_sync(FULL, n_uns, o);
-    n_err += __shfl_xor_sync(FULL, n_err, o);
-    mbytes_all += __shfl_xor_sync(FULL, mbytes_all, o);
-  }
-  if (lane == 0) {
-    unsigned long long *C = (unsigned long long *)O.counters;
-    if (n_tot) atomicAdd(C + GS_C_TOTAL, (unsigned long long)n_tot);
-    if (n_pres) atomicAdd(C + GS_C_PRESERVED, (unsigned long long)n_pres);
-    if (n_disc) atomicAdd(C + GS_C_DISCARDED, (unsigned long long)n_disc);
-    if (n_ovf) atomicAdd(C + GS_C_OVERFLOW, (unsigned long long)n_ovf);
-    if (n_cor) atomicAdd(C + GS_C_CORRUPT, (unsigned long long)n_cor);
-    if (n_uns) atomicAdd(C + GS_C_UNSUPPORTED, (unsigned long long)n_uns);
-    if (n_err) atomicAdd(C + GS_C_ERROR_SHOTS, (unsigned long long)n_err);
-    if (mbytes_all) atomicAdd(C + GS_C_MODEL_BYTES, mbytes_all);
+  __syncwarp();
+  if (lane < WC_N && wcnt[lane]) {
+    static_assert(WC_N == 8, "counter order");
+    const int dst[WC_N] = {GS_C_TOTAL, GS_C_PRESERVED, GS_C_DISCARDED, GS_C_OVERFLOW,
+                           GS_C_CORRUPT, GS_C_UNSUPPORTED, GS_C_ERROR_SHOTS, GS_C_MODEL_BYTES};
+    atomicAdd((unsigned long long *)O.counters + dst[lane], wcnt[lane]);
   }
 }
 
+// @region plugin kernels + host
 // ------------------------------------------------ kernel plugin API kernels
 // batched equivalents of ref _kernels.pyx / _kernels_py.py
 
@@ -1685,6 +1645,10 @@ struct gs_engine {
   size_t chi_bytes = 0;
   u32 *d_rec = nullptr;
   size_t rec_bytes = 0;
+  u64 *d_stash = nullptr;
+  size_t stash_bytes = 0;
+  double2 *d_gan = nullptr;
+  size_t gan_bytes = 0;
   u64 launches = 0;
   double last_ms = 0.0;
 };
@@ -1785,6 +1749,8 @@ int gs_engine_destroy(gs_engine *e) {
   cudaFree(e->d_next);
   cudaFree(e->d_chi);
   cudaFree(e->d_rec);
+  cudaFree(e->d_stash);
+  cudaFree(e->d_gan);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->stream) cudaStreamDestroy(e->stream);
@@ -1822,19 +1788,39 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
   // record bits of the warp's 32 shots (one column per lane)
   const size_t rec_b = (size_t)L.rec_words32 * 4 * 32;
   L.rec_in_smem = rec_b <= 4096;
-  size_t base = gs::kWinBytes + 4 * gs::kLcapMax + gs::kNarrowBytes + (L.rec_in_smem ? rec_b : 0);
-  base = (base + 15) & ~(size_t)15;
-  // chi in shared memory only when it is small: large chi buffers cap the
-  // resident warps per SM, while the global (L1/L2-cached) placement keeps
-  // occupancy register-bound and leaves L1 to the program stream (measured:
-  // d=5 proxy 5.9M vs 5.1M shots/s, profiles/README.md)
-  if (r->flags & GS_CHI_SMEM) L.smem_chi = chi <= 48 * 1024;
-  else if (r->flags & GS_CHI_GLOBAL) L.smem_chi = false;
-  else L.smem_chi = chi <= 4 * 1024;
-  L.chi_off = (u32)base;
-  L.warp_bytes = (u32)(base + (L.smem_chi ? chi : 0));
-  u32 wpb = r->warps_per_block ? r->warps_per_block : 4;
-  if (wpb > 4) wpb = 4;   // __launch_bounds__(128)
+  // chi of wide sections in shared memory when it fits (it then shares the
+  // warp's buffer with the narrow lane-per-shot chi An); else a per-warp
+  // global buffer (L1/L2-cached) for large max_dim
+  if (r->flags & GS_CHI_GLOBAL) L.smem_chi = false;
+  else if (r->flags & GS_CHI_SMEM) L.smem_chi = chi <= 64 * 1024;
+  else L.smem_chi = chi <= 32 * 1024;
+  const size_t buf = L.smem_chi ? std::max((size_t)gs::kNarrowBytes, chi) : (size_t)gs::kNarrowBytes;
+  const size_t base = gs::kWinBytes + gs::kCntBytes + buf;
+  L.chi_off = (u32)base;   // record columns follow the chi buffer
+  L.warp_bytes = (u32)(((L.rec_in_smem ? base + rec_b : base) + 15) & ~(size_t)15);
+  // warps per block: the most resident warps per SM (shared memory bound)
+  u32 wpb = 1;
+  if (r->warps_per_block) {
+    wpb = r->warps_per_block > 4 ? 4 : r->warps_per_block;   // __launch_bounds__(128)
+  } else {
+    int best = -1;
+    for (u32 w = 4; w >= 1; --w) {
+      if ((size_t)w * L.warp_bytes > e->smem_optin) continue;
+      int per = 0;
+      if (L.smem_chi) {
+        CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(w * L.warp_bytes)));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs::sample_kernel<true>, w * 32,
+                                                               w * L.warp_bytes));
+      } else {
+        CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(w * L.warp_bytes)));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs::sample_kernel<false>, w * 32,
+                                                               w * L.warp_bytes));
+      }
+      if (per * (int)w > best) { best = per * (int)w; wpb = w; }
+    }
+  }
   while (wpb > 1 && (size_t)wpb * L.warp_bytes > e->smem_optin) --wpb;
   if ((size_t)wpb * L.warp_bytes > e->smem_optin)
     return fail(GS_ERR_UNSUPPORTED, "per-warp state exceeds shared memory");
@@ -1857,7 +1843,8 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
   }
   if (per_sm < 1) return fail(GS_ERR_UNSUPPORTED, "kernel does not fit on an SM");
   u64 blocks = r->blocks ? r->blocks : (u64)e->num_sms * per_sm;
-  const u64 need = (r->shot_count + wpb - 1) / wpb;
+  // each warp takes batches of 32 shots
+  const u64 need = (r->shot_count + 32ull * wpb - 1) / (32ull * wpb);
   if (blocks > need) blocks = need ? need : 1;
   // bound the global chi scratch (large-k programs run fewer resident shots)
   if (!L.smem_chi) {
@@ -1874,6 +1861,26 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
       e->chi_bytes = 0;
       CUDA_TRY(cudaMalloc(&e->d_chi, want));
       e->chi_bytes = want;
+    }
+  }
+  if (L.smem_chi) {
+    const size_t want = (size_t)warps * (32u << GS_KN) * 16;
+    if (want > e->gan_bytes) {
+      cudaFree(e->d_gan);
+      e->d_gan = nullptr;
+      e->gan_bytes = 0;
+      CUDA_TRY(cudaMalloc(&e->d_gan, want));
+      e->gan_bytes = want;
+    }
+  }
+  {
+    const size_t want = (size_t)warps * gs::SF_N * 32 * 8;
+    if (want > e->stash_bytes) {
+      cudaFree(e->d_stash);
+      e->d_stash = nullptr;
+      e->stash_bytes = 0;
+      CUDA_TRY(cudaMalloc(&e->d_stash, want));
+      e->stash_bytes = want;
     }
   }
   if (!L.rec_in_smem) {
@@ -1938,8 +1945,8 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   O.warp_bytes = L.warp_bytes;
   O.rec_in_smem = L.rec_in_smem;
   O.chi_off = L.chi_off;
-  O.lcap = (r->flags & GS_DENSE_ONLY) ? 0u
-           : (r->list_cap == 0 || r->list_cap > gs::kLcapMax ? gs::kLcapMax : r->list_cap);
+  O.gstash = e->d_stash;
+  O.gan = e->d_gan;
   CUDA_TRY(cudaMemsetAsync(e->d_next, 0, sizeof(u64), st));
   if (r->shot_count) {
     if (timed) CUDA_TRY(cudaEventRecord(e->ev0, st));

@@ -81,7 +81,7 @@ class Engine:
 
     @staticmethod
     def params(master_seed=0, shot_begin=0, shot_count=0, capacity=4096,
-               flags=0, warps_per_block=0, blocks=0, seeds=None, list_cap=0):
+               flags=0, warps_per_block=0, blocks=0, seeds=None):
         p = _lib.GsRunParams()
         p.master_seed = master_seed & 0xFFFFFFFFFFFFFFFF
         p.shot_begin = shot_begin
@@ -90,7 +90,6 @@ class Engine:
         p.flags = flags
         p.warps_per_block = warps_per_block
         p.blocks = blocks
-        p.list_cap = list_cap
         p._seeds_keep = None
         if seeds is not None:
             s = np.ascontiguousarray(seeds, dtype=np.uint64)

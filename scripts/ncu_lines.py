@@ -73,15 +73,14 @@ def main():
     ts, te = sum(by_line_s.values()), sum(by_line_e.values())
     print("instructions %d, opcode mismatches %d, samples %.0f, warp-instr %.3g" %
           (len(data), mism, ts, te))
-    regions = [(1, 299, "prologue/helpers"), (300, 328, "shot setup"),
-               (329, 330, "op loop"), (331, 447, "noise scan+apply"),
-               (448, 458, "op dispatch"), (459, 490, "T diag/preamble"),
-               (491, 545, "T grow-limit/sparse"), (546, 584, "T dense merge"),
-               (586, 609, "meas preamble"), (610, 650, "meas det small"),
-               (651, 687, "meas det sparse"), (688, 735, "meas det dense"),
-               (736, 793, "meas pivot small"), (794, 838, "meas pivot sparse"),
-               (839, 915, "meas pivot dense"), (916, 934, "meas epilogue"),
-               (935, 975, "feedback/detector/obs/end"), (976, 1032, "shot outputs")]
+    src_lines = open(os.path.join(ROOT, "paper_2512_23037_b200", "csrc",
+                                  "gs_kernels.cu")).read().splitlines()
+    marks = [(i + 1, m.group(1).strip()) for i, l in enumerate(src_lines)
+             for m in [re.search(r"//\s*@region\s+(.*)$", l)] if m]
+    regions = [(a, (marks[i + 1][0] - 1) if i + 1 < len(marks) else 10 ** 9, nm)
+               for i, (a, nm) in enumerate(marks)]
+    if not regions:
+        regions = [(1, 10 ** 9, "all")]
     agg_s, agg_e = defaultdict(float), defaultdict(float)
     for line in by_line_s:
         name = "?"

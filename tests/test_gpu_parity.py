@@ -72,7 +72,8 @@ def test_golden_shot_results_bit_exact(golden_shots):
 
 
 @pytest.mark.parametrize("flag", [_lib.GS_CHI_GLOBAL, _lib.GS_CHI_SMEM,
-                                  _lib.GS_DENSE_ONLY])
+                                  _lib.GS_WIDE_ONLY,
+                                  _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM])
 def test_golden_shot_results_storage_variants(golden_shots, flag):
     for fx in golden_shots[::3]:
         prog = parse_circuit(fx["text"])
@@ -212,21 +213,15 @@ def test_msc_noiseless_is_deterministic(d):
     assert st.preserved_shots == 4096
 
 
-@pytest.mark.parametrize("variant", ["dense_only", "lcap4", "lcap32", "chi_global",
-                                     "chi_smem"])
+@pytest.mark.parametrize("variant", ["default", "wide_only", "chi_global",
+                                     "chi_smem", "wide_only_chi_smem"])
 def test_chi_storage_modes_match_oracle(variant):
-    """Sparse occupancy list / dense sweeps / global-memory chi must all give
-    the oracle's results (mode switches are exercised with tiny list caps)."""
+    """Lane-per-shot / warp-per-shot execution and shared- / global-memory
+    chi buffers must all give the oracle's results."""
     rng = random.Random(7)
-    flags_extra, lcap = 0, 0
-    if variant == "dense_only":
-        flags_extra = _lib.GS_DENSE_ONLY
-    elif variant == "chi_global":
-        flags_extra = _lib.GS_CHI_GLOBAL
-    elif variant == "chi_smem":
-        flags_extra = _lib.GS_CHI_SMEM
-    else:
-        lcap = int(variant[4:])
+    flags_extra = {"default": 0, "wide_only": _lib.GS_WIDE_ONLY,
+                   "chi_global": _lib.GS_CHI_GLOBAL, "chi_smem": _lib.GS_CHI_SMEM,
+                   "wide_only_chi_smem": _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM}[variant]
     eng = get_engine(0)
     for it in range(25):
         n = rng.choice((4, 9, 20))
@@ -234,7 +229,7 @@ def test_chi_storage_modes_match_oracle(variant):
         dp = compile_program(prog)
         p = Program(dp)
         flags = _lib.GS_POSTSELECT * (it % 2) | flags_extra
-        par = Engine.params(3 + it, 0, 16, 4096, flags, list_cap=lcap)
+        par = Engine.params(3 + it, 0, 16, 4096, flags)
         status, aux, rec, obs = eng.run_records(p, par)
         from paper_2512_23037_b200.sampler import ShotBatch
         b = ShotBatch(status, aux, rec, obs, list(dp.obs_keys), dp.num_measurements)
