@@ -59,7 +59,8 @@ def main():
     iA, iS, iE = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), \
         h.index("Instructions Executed")
     base = int(data[0][iA], 16)
-    m = disasm(lib, r"sample_kernelILb0E")
+    kname = rows[0][1] if rows and len(rows[0]) > 1 else ""
+    m = disasm(lib, r"sample_kernelILb1E" if "(bool)1" in kname else r"sample_kernelILb0E")
     by_line_s, by_line_e = defaultdict(float), defaultdict(float)
     mism = 0
     for r in data:
