@@ -300,18 +300,16 @@ __device__ __noinline__ u32 sweep_butterfly(double2 *__restrict__ A, u32 half, u
   const u32 pl = dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 r = 0; r < half; r += 32) {
-    const u32 jr = ins_bit(r, hb, 0);
+  for (u32 m = lane; m < half; m += 32) {
+    const u32 jr = ins_bit(m & ~31u, hb, 0);
     const u32 j0 = jr | jl, j1 = j0 ^ cb;
     const u32 s0 = pl ^ par32(jr & dmask), s1 = s0 ^ pcb;
-    if (r + lane < half) {
-      const double2 v0 = A[j0], v1 = A[j1];
-      const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
-      const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
-      A[j0] = n0;
-      A[j1] = n1;
-      nz += nonzero(n0) + nonzero(n1);
-    }
+    const double2 v0 = A[j0], v1 = A[j1];
+    const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
+    const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
+    A[j0] = n0;
+    A[j1] = n1;
+    nz += nonzero(n0) + nonzero(n1);
   }
   return nz;
 }
@@ -324,17 +322,14 @@ __device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc
   const u32 pl = dc ^ par32(lane & dmask);
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 r = 0; r < size; r += 32) {
-    const u32 j = r + lane;
-    const u32 s_ = pl ^ par32(r & dmask);
-    if (j < size) {
-      const double2 v = A[j];
-      const double2 n0 = prune(cmul(a, v));
-      const double2 n1 = prune(cmul(s_ ? bx1 : bx0, v));
-      A[j] = n0;
-      A[size + j] = n1;
-      nz += nonzero(n0) + nonzero(n1);
-    }
+  for (u32 j = lane; j < size; j += 32) {
+    const u32 s_ = pl ^ par32((j & ~31u) & dmask);
+    const double2 v = A[j];
+    const double2 n0 = prune(cmul(a, v));
+    const double2 n1 = prune(cmul(s_ ? bx1 : bx0, v));
+    A[j] = n0;
+    A[size + j] = n1;
+    nz += nonzero(n0) + nonzero(n1);
   }
   return nz;
 }
@@ -346,11 +341,8 @@ __device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 
   const u32 lane = threadIdx.x & 31u;
   const u32 pl = dc ^ par32(lane & mask);
 #pragma unroll 1
-  for (u32 r = 0; r < size; r += 32) {
-    const u32 j = r + lane;
-    const u32 s_ = pl ^ par32(r & mask);
-    if (j < size) A[j] = cmul(A[j], s_ ? f1 : f0);
-  }
+  for (u32 j = lane; j < size; j += 32)
+    A[j] = cmul(A[j], (pl ^ par32((j & ~31u) & mask)) ? f1 : f0);
 }
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
@@ -360,12 +352,9 @@ __device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u3
   const u32 pl = neg0 ^ par32(lane & dmask);
   double sp = 0.0, sm = 0.0;
 #pragma unroll 1
-  for (u32 r = 0; r < size; r += 32) {
-    const u32 j = r + lane;
-    if (j < size) {
-      const double a2 = abs2(A[j]);
-      if (pl ^ par32(r & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
-    }
+  for (u32 j = lane; j < size; j += 32) {
+    const double a2 = abs2(A[j]);
+    if (pl ^ par32((j & ~31u) & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
   }
   return make_double2(sp, sm);
 }
@@ -378,14 +367,11 @@ __device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 
   const u32 pl = neg0 ^ want_neg ^ par32(lane & dmask);
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 r = 0; r < size; r += 32) {
-    const u32 j = r + lane;
-    const bool keep = (pl ^ par32(r & dmask)) == 0;
-    if (j < size) {
-      const double2 w = keep ? cscale(A[j], rs) : Z;
-      A[j] = w;
-      nz += nonzero(w);
-    }
+  for (u32 j = lane; j < size; j += 32) {
+    const bool keep = (pl ^ par32((j & ~31u) & dmask)) == 0;
+    const double2 w = keep ? cscale(A[j], rs) : Z;
+    A[j] = w;
+    nz += nonzero(w);
   }
   return nz;
 }
