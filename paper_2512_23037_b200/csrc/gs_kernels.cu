@@ -279,37 +279,51 @@ __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y !=
 // @region sweeps
 // ---------------------------------------------------------------- wide sweeps
 //
-// Warp-cooperative passes over a dense chi array A[0, 2^k): in round r lane
-// l takes coordinate 32r + l (pair index for pair sweeps).  Every sign
-// parity par(j & mask) splits into a per-lane constant and a warp-uniform
-// per-round term, because j = J(32r) | J(l) with disjoint bits (J inserts
-// the pair bit; see ins_bit).  One coordinate in flight per lane: unrolling
-// (2, 4 in flight) measured slower on the B200 (20.6M vs 10.8M / 8.2M
-// shots/s), the chi buffer is in shared memory and 12 warps/SM cover its
-// latency.  Out of line: one copy serves every caller (instruction cache).
-// Per-lane partial results; callers reduce across the warp.
+// Warp-cooperative passes over a dense chi array A[0, 2^k) (lanes take
+// coordinates lane, lane+32, ...; GS_SW coordinates in flight per lane).
+// Out of line on purpose: each gets its own small register allocation, so
+// the loads of one round are all issued before the first use (memory-level
+// parallelism against L1/L2 latency) without spilling the interpreter's
+// state.  Per-lane partial results; callers reduce across the warp.
 
-// T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
-// 294-306: a-term then b-term, pruned at |.| <= 1e-12)
+#ifndef GS_SW
+#define GS_SW 1   // A/B on one B200 (shared-memory chi): 20.6M / 10.8M / 8.2M shots/s at 1 / 2 / 4
+#endif
+// (A per-lane / per-round split of the sign parities measured slower too:
+// 20.8M vs 21.6M shots/s -- the guarded round loops add convergence barriers.)
+
+// T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129)
 __device__ __noinline__ u32 sweep_butterfly(double2 *__restrict__ A, u32 half, u32 cb,
                                             u32 dc, u32 dmask, double2 a, double2 bx0) {
   const u32 lane = threadIdx.x & 31u;
   const double2 bx1 = cneg(bx0);
   const u32 hb = 31 - __clz(cb);
-  const u32 jl = ins_bit(lane, hb, 0);
-  const u32 pl = dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 m = lane; m < half; m += 32) {
-    const u32 jr = ins_bit(m & ~31u, hb, 0);
-    const u32 j0 = jr | jl, j1 = j0 ^ cb;
-    const u32 s0 = pl ^ par32(jr & dmask), s1 = s0 ^ pcb;
-    const double2 v0 = A[j0], v1 = A[j1];
-    const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
-    const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
-    A[j0] = n0;
-    A[j1] = n1;
-    nz += nonzero(n0) + nonzero(n1);
+  for (u32 b0 = lane; b0 < half; b0 += 32 * GS_SW) {
+    double2 v0[GS_SW], v1[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 m = b0 + 32 * u;
+      if (m < half) {
+        const u32 j0 = ins_bit(m, hb, 0);
+        v0[u] = A[j0];
+        v1[u] = A[j0 ^ cb];
+      }
+    }
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 m = b0 + 32 * u;
+      if (m < half) {
+        const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+        const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+        const double2 n0 = prune(cadd(cmul(a, v0[u]), cmul(s1 ? bx1 : bx0, v1[u])));
+        const double2 n1 = prune(cadd(cmul(a, v1[u]), cmul(s0 ? bx1 : bx0, v0[u])));
+        A[j0] = n0;
+        A[j1] = n1;
+        nz += nonzero(n0) + nonzero(n1);
+      }
+    }
   }
   return nz;
 }
@@ -319,17 +333,24 @@ __device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc
                                        double2 a, double2 bx0) {
   const u32 lane = threadIdx.x & 31u;
   const double2 bx1 = cneg(bx0);
-  const u32 pl = dc ^ par32(lane & dmask);
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) {
-    const u32 s_ = pl ^ par32((j & ~31u) & dmask);
-    const double2 v = A[j];
-    const double2 n0 = prune(cmul(a, v));
-    const double2 n1 = prune(cmul(s_ ? bx1 : bx0, v));
-    A[j] = n0;
-    A[size + j] = n1;
-    nz += nonzero(n0) + nonzero(n1);
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const u32 s_ = dc ^ par32(j & dmask);
+        const double2 n0 = prune(cmul(a, v[u]));
+        const double2 n1 = prune(cmul(s_ ? bx1 : bx0, v[u]));
+        A[j] = n0;
+        A[size + j] = n1;
+        nz += nonzero(n0) + nonzero(n1);
+      }
+    }
   }
   return nz;
 }
@@ -339,22 +360,37 @@ __device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc
 __device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 dc, u32 mask,
                                          double2 f0, double2 f1) {
   const u32 lane = threadIdx.x & 31u;
-  const u32 pl = dc ^ par32(lane & mask);
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32)
-    A[j] = cmul(A[j], (pl ^ par32((j & ~31u) & mask)) ? f1 : f0);
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) A[j] = cmul(v[u], (dc ^ par32(j & mask)) ? f1 : f0);
+    }
+  }
 }
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
 __device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u32 size, u32 dmask,
                                                u32 neg0) {
   const u32 lane = threadIdx.x & 31u;
-  const u32 pl = neg0 ^ par32(lane & dmask);
   double sp = 0.0, sm = 0.0;
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) {
-    const double a2 = abs2(A[j]);
-    if (pl ^ par32((j & ~31u) & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const double a2 = abs2(v[u]);
+        if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+      }
+    }
   }
   return make_double2(sp, sm);
 }
@@ -364,14 +400,22 @@ __device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 
                                          u32 neg0, u32 want_neg, double rs) {
   const u32 lane = threadIdx.x & 31u;
   const double2 Z = make_double2(0.0, 0.0);
-  const u32 pl = neg0 ^ want_neg ^ par32(lane & dmask);
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) {
-    const bool keep = (pl ^ par32((j & ~31u) & dmask)) == 0;
-    const double2 w = keep ? cscale(A[j], rs) : Z;
-    A[j] = w;
-    nz += nonzero(w);
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
+        const double2 w = keep ? cscale(v[u], rs) : Z;
+        A[j] = w;
+        nz += nonzero(w);
+      }
+    }
   }
   return nz;
 }
@@ -382,21 +426,27 @@ __device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 
 __device__ __noinline__ u32 sweep_compact(double2 *__restrict__ A, u32 half, u32 isq, u32 mask,
                                           u32 tau, double rs) {
   const u32 lane = threadIdx.x & 31u;
-  const u32 jl = ins_bit(lane, isq, 0);
-  const u32 pl = tau ^ par32(jl & mask);
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 r = 0; r < half; r += 32) {
-    const u32 jr = ins_bit(r, isq, 0);
-    const u32 j0 = jr | jl;
-    const u32 jp = r + lane;
-    double2 v = make_double2(0.0, 0.0);
-    if (jp < half) v = A[j0 | ((pl ^ par32(jr & mask)) << isq)];
+  for (u32 b0 = 0; b0 < half; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 jp = b0 + 32 * u + lane;
+      if (jp < half) {
+        const u32 j0 = ins_bit(jp, isq, 0);
+        v[u] = A[j0 | ((tau ^ par32(j0 & mask)) << isq)];
+      }
+    }
     __syncwarp();
-    if (jp < half) {
-      const double2 w = cscale(v, rs);
-      A[jp] = w;
-      nz += nonzero(w);
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 jp = b0 + 32 * u + lane;
+      if (jp < half) {
+        const double2 w = cscale(v[u], rs);
+        A[jp] = w;
+        nz += nonzero(w);
+      }
     }
     __syncwarp();
   }
@@ -440,11 +490,16 @@ __device__ __noinline__ double sweep_pivot_p(const double2 *__restrict__ A, Pivo
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0;
 #pragma unroll 1
-  for (u32 m = lane; m < g.npairs; m += 32) {
-    double2 vr, pr;
-    u32 d_;
-    pivot_terms(A, g, xpp, m, vr, pr, d_);
-    sp = __dadd_rn(sp, abs2(cadd(vr, pr)));
+  for (u32 b0 = lane; b0 < g.npairs; b0 += 32 * GS_SW) {
+    double2 vr[GS_SW], pr[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      u32 d_;
+      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], d_);
+    }
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u)
+      if (b0 + 32 * u < g.npairs) sp = __dadd_rn(sp, abs2(cadd(vr[u], pr[u])));
   }
   return sp;
 }
@@ -458,14 +513,21 @@ __device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g,
   double sk = 0.0;
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 m = lane; m < g.npairs; m += 32) {
-    double2 vr, pr;
-    u32 dst;
-    pivot_terms(A, g, xpp, m, vr, pr, dst);
-    const double2 w = prune(plus ? cadd(vr, pr) : csub(vr, pr));
-    A[dst] = w;
-    sk = __dadd_rn(sk, abs2(w));
-    nz += nonzero(w);
+  for (u32 b0 = lane; b0 < g.npairs; b0 += 32 * GS_SW) {
+    double2 vr[GS_SW], pr[GS_SW];
+    u32 dst[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u)
+      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], dst[u]);
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      if (b0 + 32 * u < g.npairs) {
+        const double2 w = prune(plus ? cadd(vr[u], pr[u]) : csub(vr[u], pr[u]));
+        A[dst[u]] = w;
+        sk = __dadd_rn(sk, abs2(w));
+        nz += nonzero(w);
+      }
+    }
   }
   SumNz r;
   r.sum = sk;
@@ -478,10 +540,19 @@ __device__ __noinline__ u32 sweep_phase_scale(double2 *__restrict__ A, u32 size,
   const u32 lane = threadIdx.x & 31u;
   u32 nz = 0;
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) {
-    const double2 w = cscale(A[j], rs);
-    A[j] = w;
-    nz += nonzero(w);
+  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
+    double2 v[GS_SW];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+#pragma unroll
+    for (u32 u = 0; u < GS_SW; ++u) {
+      const u32 j = b0 + 32 * u;
+      if (j < size) {
+        const double2 w = cscale(v[u], rs);
+        A[j] = w;
+        nz += nonzero(w);
+      }
+    }
   }
   return nz;
 }
