@@ -292,9 +292,17 @@ __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y !=
 // (A per-lane / per-round split of the sign parities measured slower too:
 // 20.8M vs 21.6M shots/s -- the guarded round loops add convergence barriers.)
 
+// A[i] with a renormalisation still pending (ps != 1): the reference would
+// have stored v * ps (ref state.py:311), so every reader applies it first --
+// the same rounding, one pass later
+__device__ __forceinline__ double2 ldps(const double2 *__restrict__ A, u32 i, double ps) {
+  const double2 v = A[i];
+  return ps != 1.0 ? cscale(v, ps) : v;
+}
+
 // T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129)
 __device__ __noinline__ u32 sweep_butterfly(double2 *__restrict__ A, u32 half, u32 cb,
-                                            u32 dc, u32 dmask, double2 a, double2 bx0) {
+                                            u32 dc, u32 dmask, double2 a, double2 bx0, double ps) {
   const u32 lane = threadIdx.x & 31u;
   const double2 bx1 = cneg(bx0);
   const u32 hb = 31 - __clz(cb);
@@ -307,8 +315,8 @@ __device__ __noinline__ u32 sweep_butterfly(double2 *__restrict__ A, u32 half, u
       const u32 m = b0 + 32 * u;
       if (m < half) {
         const u32 j0 = ins_bit(m, hb, 0);
-        v0[u] = A[j0];
-        v1[u] = A[j0 ^ cb];
+        v0[u] = ldps(A, j0, ps);
+        v1[u] = ldps(A, j0 ^ cb, ps);
       }
     }
 #pragma unroll
@@ -330,7 +338,7 @@ __device__ __noinline__ u32 sweep_butterfly(double2 *__restrict__ A, u32 half, u
 
 // T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
 __device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc, u32 dmask,
-                                       double2 a, double2 bx0) {
+                                       double2 a, double2 bx0, double ps) {
   const u32 lane = threadIdx.x & 31u;
   const double2 bx1 = cneg(bx0);
   u32 nz = 0;
@@ -338,7 +346,7 @@ __device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc
   for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
     double2 v[GS_SW];
 #pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u) {
       const u32 j = b0 + 32 * u;
@@ -358,13 +366,13 @@ __device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc
 // diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
 // fired noise Paulis)
 __device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 dc, u32 mask,
-                                         double2 f0, double2 f1) {
+                                         double2 f0, double2 f1, double ps) {
   const u32 lane = threadIdx.x & 31u;
 #pragma unroll 1
   for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
     double2 v[GS_SW];
 #pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u) {
       const u32 j = b0 + 32 * u;
@@ -375,14 +383,14 @@ __device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
 __device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u32 size, u32 dmask,
-                                               u32 neg0) {
+                                               u32 neg0, double ps) {
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0, sm = 0.0;
 #pragma unroll 1
   for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
     double2 v[GS_SW];
 #pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u) {
       const u32 j = b0 + 32 * u;
@@ -397,7 +405,7 @@ __device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u3
 
 // keep the chosen eigen-entries, scaled by rs; zero the others
 __device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 dmask,
-                                         u32 neg0, u32 want_neg, double rs) {
+                                         u32 neg0, u32 want_neg, double rs, double ps) {
   const u32 lane = threadIdx.x & 31u;
   const double2 Z = make_double2(0.0, 0.0);
   u32 nz = 0;
@@ -405,7 +413,7 @@ __device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 
   for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
     double2 v[GS_SW];
 #pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u) {
       const u32 j = b0 + 32 * u;
@@ -424,7 +432,7 @@ __device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 
 // src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
 // at isq; src(jp) >= jp, so reads of a round finish before its writes
 __device__ __noinline__ u32 sweep_compact(double2 *__restrict__ A, u32 half, u32 isq, u32 mask,
-                                          u32 tau, double rs) {
+                                          u32 tau, double rs, double ps) {
   const u32 lane = threadIdx.x & 31u;
   u32 nz = 0;
 #pragma unroll 1
@@ -435,7 +443,7 @@ __device__ __noinline__ u32 sweep_compact(double2 *__restrict__ A, u32 half, u32
       const u32 jp = b0 + 32 * u + lane;
       if (jp < half) {
         const u32 j0 = ins_bit(jp, isq, 0);
-        v[u] = A[j0 | ((tau ^ par32(j0 & mask)) << isq)];
+        v[u] = ldps(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
       }
     }
     __syncwarp();
@@ -464,17 +472,17 @@ struct PivotGeo {
 };
 __device__ __forceinline__ void pivot_terms(const double2 *__restrict__ A, const PivotGeo &g,
                                             double2 xpp, u32 m, double2 &vr, double2 &pr,
-                                            u32 &dst) {
+                                            u32 &dst, double ps) {
   const double2 xpm = cneg(xpp);
   if (g.span) {
     const u32 j0 = ins_bit(m, g.isq, 0);
     const u32 rep = j0 | ((g.ct ^ par32(j0 & g.tmask)) << g.isq);
     const u32 part = rep ^ g.cb;
-    vr = A[rep];
-    pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, A[part]);
+    vr = ldps(A, rep, ps);
+    pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, ldps(A, part, ps));
     dst = rep;
   } else {
-    const double2 v = A[m];
+    const double2 v = ldps(A, m, ps);
     if (g.ct ^ par32(m & g.tmask)) {
       vr = make_double2(0.0, 0.0);
       pr = cmul((g.dc ^ par32(m & g.dmask)) ? xpm : xpp, v);
@@ -486,7 +494,7 @@ __device__ __forceinline__ void pivot_terms(const double2 *__restrict__ A, const
   }
 }
 __device__ __noinline__ double sweep_pivot_p(const double2 *__restrict__ A, PivotGeo g,
-                                             double2 xpp) {
+                                             double2 xpp, double ps) {
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0;
 #pragma unroll 1
@@ -495,7 +503,7 @@ __device__ __noinline__ double sweep_pivot_p(const double2 *__restrict__ A, Pivo
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u) {
       u32 d_;
-      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], d_);
+      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], d_, ps);
     }
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u)
@@ -508,7 +516,7 @@ struct SumNz {
   u32 nz;
 };
 __device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g, double2 xpp,
-                                            bool plus) {
+                                            bool plus, double ps) {
   const u32 lane = threadIdx.x & 31u;
   double sk = 0.0;
   u32 nz = 0;
@@ -518,7 +526,7 @@ __device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g,
     u32 dst[GS_SW];
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u)
-      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], dst[u]);
+      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], dst[u], ps);
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u) {
       if (b0 + 32 * u < g.npairs) {
@@ -536,14 +544,15 @@ __device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g,
 }
 
 // renormalise every entry: A[j] *= rs
-__device__ __noinline__ u32 sweep_phase_scale(double2 *__restrict__ A, u32 size, double rs) {
+__device__ __noinline__ u32 sweep_phase_scale(double2 *__restrict__ A, u32 size, double rs,
+                                              double ps) {
   const u32 lane = threadIdx.x & 31u;
   u32 nz = 0;
 #pragma unroll 1
   for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
     double2 v[GS_SW];
 #pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = A[b0 + 32 * u];
+    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
 #pragma unroll
     for (u32 u = 0; u < GS_SW; ++u) {
       const u32 j = b0 + 32 * u;
@@ -710,6 +719,7 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
       u64 mbytes = stash[SF_MB * 32 + s];
       u32 cnt = (u32)stash[SF_CNTK * 32 + s], kcur = k;
       int status = ST_RUNNING, aux = -1;
+      double ps = 1.0;        // renormalisation pending on A (see ldps)
       const u64 gw_ = stash[SF_GEO * 32 + s];
       u32 gj = (u32)gw_, gpos = (u32)(gw_ >> 32);
       u64 gpick = stash[SF_PICK * 32 + s];
@@ -740,7 +750,8 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
                                            sig_lo, sig_hi);
             const double2 php = ipow(e.xi);
-            sweep_phase(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php));
+            sweep_phase(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
+            ps = 1.0;
             __syncwarp();
             c ^= e.beta;
             mbytes += 2ull * kEntryBytes * cnt + sign_bytes;
@@ -850,7 +861,8 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
           const u32 tcase = wfl & 3u;
           if (tcase == T_DIAG) {
             // beta == 0: pure phase per entry (ref state.py:120-126)
-            sweep_phase(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)));
+            sweep_phase(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
+            ps = 1.0;
             __syncwarp();
             mbytes += 32ull * cnt;
             continue;
@@ -861,7 +873,7 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             const double2 bx1 = cneg(bx0);
 #pragma unroll 1
             for (u32 j = lane; j < size; j += 32) {
-              const double2 v = A[j];
+              const double2 v = ldps(A, j, ps);
               const u32 s_ = dc ^ par32(j & dmask);
               nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
               nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
@@ -874,11 +886,12 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
           // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
           u32 nz;
           if (tcase == T_BUTTERFLY) {
-            nz = sweep_butterfly(A, size >> 1, cb, dc, dmask, a, bx0);
+            nz = sweep_butterfly(A, size >> 1, cb, dc, dmask, a, bx0, ps);
           } else {
-            nz = sweep_grow(A, size, dc, dmask, a, bx0);
+            nz = sweep_grow(A, size, dc, dmask, a, bx0, ps);
             kcur = wk + 1;
           }
+          ps = 1.0;
           __syncwarp();
           cnt = warp_sum_u32(nz);
           mbytes += (u64)kEntryBytes * (cin + cnt);
@@ -915,7 +928,7 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
           if (mcase == M_DET) {
             // beta == 0: filter by eigenvalue (ref state.py:162-176)
             const u32 neg0 = (xi0 >> 1) ^ dc;
-            const double2 part = sweep_det_sums(A, size, dmask, neg0);
+            const double2 part = sweep_det_sums(A, size, dmask, neg0, ps);
             const double sp = warp_sum(part.x);
             const double sm = warp_sum(part.y);
             plus = pick_plus(sp);
@@ -925,11 +938,22 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             const double rs = inv_sqrt_norm(plus ? sp : sm);
             if (wfl & MF_COMPACT) {
               const u32 tau = want_neg ^ neg0;
-              nz = sweep_compact(A, size >> 1, isq, dmask, tau, rs);
+              nz = sweep_compact(A, size >> 1, isq, dmask, tau, rs, ps);
+              ps = 1.0;
               if (tau) c ^= vec;
               kcur = wk - 1;
             } else {
-              nz = sweep_filter(A, size, dmask, neg0, want_neg, rs);
+              if ((plus ? sm : sp) == 0.0) {
+                // every entry of the other eigenspace is already zero: the
+                // filter is a pure renormalisation -- defer it to the next
+                // pass over A (ldps); the nonzero count is unchanged
+                if (ps != 1.0) sweep_phase_scale(A, size, 1.0, ps);
+                ps = rs;
+                nz = lane == 0 ? cnt : 0u;
+              } else {
+                nz = sweep_filter(A, size, dmask, neg0, want_neg, rs, ps);
+                ps = 1.0;
+              }
             }
             __syncwarp();
           } else {
@@ -940,20 +964,23 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
             g.dc = dc; g.dmask = dmask;
             const double2 xpp = ipow(xi0);   // i^xi0, exact
-            const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p(A, g, xpp)));
+            const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p(A, g, xpp, ps)));
             plus = pick_plus(pp);
             const double chosen = plus ? pp : __dsub_rn(1.0, pp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
-            const SumNz w = sweep_pivot_w(A, g, xpp, plus);
+            const SumNz w = sweep_pivot_w(A, g, xpp, plus, ps);
+            ps = 1.0;
             __syncwarp();
             const double sk = warp_sum(w.sum);
             if (warp_sum_u32(w.nz) == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
             const double rs = inv_sqrt_norm(sk);
             if (g.span) {
-              nz = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs);
+              nz = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
               kcur = wk - 1;
             } else {
-              nz = sweep_phase_scale(A, size, rs);
+              // pure renormalisation: deferred (see above)
+              ps = rs;
+              nz = w.nz;
             }
             __syncwarp();
             if (g.ct) c ^= vec;
@@ -1034,7 +1061,7 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
       }
       if (status == ST_RUNNING) {
 #pragma unroll 1
-        for (u32 j = lane; j < (1u << kcur); j += 32) Ast[j * 32u + s] = A[j];
+        for (u32 j = lane; j < (1u << kcur); j += 32) Ast[j * 32u + s] = ldps(A, j, ps);
       } else if (O.mode == MODE_DUMP) {
         const u64 ssl = base + s;
         if (lane == 0) {
@@ -1045,7 +1072,7 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
         }
         const u64 stride = 1ull << P.max_dim;
 #pragma unroll 1
-        for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[ssl * stride + j] = A[j];
+        for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[ssl * stride + j] = ldps(A, j, ps);
       }
       __syncwarp();
     }
