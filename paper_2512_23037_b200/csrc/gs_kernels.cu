@@ -279,18 +279,19 @@ __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y !=
 // @region sweeps
 // ---------------------------------------------------------------- wide sweeps
 //
-// Warp-cooperative passes over a dense chi array A[0, 2^k) (lanes take
-// coordinates lane, lane+32, ...; GS_SW coordinates in flight per lane).
-// Out of line on purpose: each gets its own small register allocation, so
-// the loads of one round are all issued before the first use (memory-level
-// parallelism against L1/L2 latency) without spilling the interpreter's
-// state.  Per-lane partial results; callers reduce across the warp.
+// Warp-cooperative passes over a dense chi array A[0, 2^k): lane l takes
+// coordinates l, l+32, ... (pair indices for pair sweeps), one in flight.
+// Measured on the B200 (shared-memory chi, 12 warps/SM): 2 or 4 coordinates
+// in flight per lane 10.8M / 8.2M vs 20.6M shots/s; a per-round split of the
+// sign parities 20.8M vs 21.6M.  Out of line: one copy serves every caller
+// (instruction cache).  Per-lane partial results (nonzero count, sum of
+// |v|^2 of the written entries = the chi norm the next deterministic
+// measurement needs); callers reduce across the warp.
 
-#ifndef GS_SW
-#define GS_SW 1   // A/B on one B200 (shared-memory chi): 20.6M / 10.8M / 8.2M shots/s at 1 / 2 / 4
-#endif
-// (A per-lane / per-round split of the sign parities measured slower too:
-// 20.8M vs 21.6M shots/s -- the guarded round loops add convergence barriers.)
+struct SumNz {
+  double sum;
+  u32 nz;
+};
 
 // A[i] with a renormalisation still pending (ps != 1): the reference would
 // have stored v * ps (ref state.py:311), so every reader applies it first --
@@ -299,68 +300,54 @@ __device__ __forceinline__ double2 ldps(const double2 *__restrict__ A, u32 i, do
   const double2 v = A[i];
   return ps != 1.0 ? cscale(v, ps) : v;
 }
+// prune at |v| <= 1e-12 (ref state.py:298), accumulating |v|^2 of the kept
+__device__ __forceinline__ double2 prune_acc(double2 v, double &sum, u32 &nz) {
+  const double q = abs2(v);
+  if (q > kPrune2) {
+    sum = __dadd_rn(sum, q);
+    nz += 1;
+    return v;
+  }
+  return make_double2(0.0, 0.0);
+}
 
-// T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129)
-__device__ __noinline__ u32 sweep_butterfly(double2 *__restrict__ A, u32 half, u32 cb,
-                                            u32 dc, u32 dmask, double2 a, double2 bx0, double ps) {
+// T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
+// 294-306: a-term then b-term)
+__device__ __noinline__ SumNz sweep_butterfly(double2 *__restrict__ A, u32 half, u32 cb, u32 dc,
+                                              u32 dmask, double2 a, double2 bx0, double ps) {
   const u32 lane = threadIdx.x & 31u;
   const double2 bx1 = cneg(bx0);
   const u32 hb = 31 - __clz(cb);
-  u32 nz = 0;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
 #pragma unroll 1
-  for (u32 b0 = lane; b0 < half; b0 += 32 * GS_SW) {
-    double2 v0[GS_SW], v1[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 m = b0 + 32 * u;
-      if (m < half) {
-        const u32 j0 = ins_bit(m, hb, 0);
-        v0[u] = ldps(A, j0, ps);
-        v1[u] = ldps(A, j0 ^ cb, ps);
-      }
-    }
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 m = b0 + 32 * u;
-      if (m < half) {
-        const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
-        const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
-        const double2 n0 = prune(cadd(cmul(a, v0[u]), cmul(s1 ? bx1 : bx0, v1[u])));
-        const double2 n1 = prune(cadd(cmul(a, v1[u]), cmul(s0 ? bx1 : bx0, v0[u])));
-        A[j0] = n0;
-        A[j1] = n1;
-        nz += nonzero(n0) + nonzero(n1);
-      }
-    }
+  for (u32 m = lane; m < half; m += 32) {
+    const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+    const double2 v0 = ldps(A, j0, ps), v1 = ldps(A, j1, ps);
+    const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+    A[j0] = prune_acc(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)), r.sum, r.nz);
+    A[j1] = prune_acc(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)), r.sum, r.nz);
   }
-  return nz;
+  return r;
 }
 
 // T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
-__device__ __noinline__ u32 sweep_grow(double2 *__restrict__ A, u32 size, u32 dc, u32 dmask,
-                                       double2 a, double2 bx0, double ps) {
+__device__ __noinline__ SumNz sweep_grow(double2 *__restrict__ A, u32 size, u32 dc, u32 dmask,
+                                         double2 a, double2 bx0, double ps) {
   const u32 lane = threadIdx.x & 31u;
   const double2 bx1 = cneg(bx0);
-  u32 nz = 0;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
 #pragma unroll 1
-  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
-    double2 v[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 j = b0 + 32 * u;
-      if (j < size) {
-        const u32 s_ = dc ^ par32(j & dmask);
-        const double2 n0 = prune(cmul(a, v[u]));
-        const double2 n1 = prune(cmul(s_ ? bx1 : bx0, v[u]));
-        A[j] = n0;
-        A[size + j] = n1;
-        nz += nonzero(n0) + nonzero(n1);
-      }
-    }
+  for (u32 j = lane; j < size; j += 32) {
+    const double2 v = ldps(A, j, ps);
+    const u32 s_ = dc ^ par32(j & dmask);
+    A[j] = prune_acc(cmul(a, v), r.sum, r.nz);
+    A[size + j] = prune_acc(cmul(s_ ? bx1 : bx0, v), r.sum, r.nz);
   }
-  return nz;
+  return r;
 }
 
 // diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
@@ -369,16 +356,8 @@ __device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 
                                          double2 f0, double2 f1, double ps) {
   const u32 lane = threadIdx.x & 31u;
 #pragma unroll 1
-  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
-    double2 v[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 j = b0 + 32 * u;
-      if (j < size) A[j] = cmul(v[u], (dc ^ par32(j & mask)) ? f1 : f0);
-    }
-  }
+  for (u32 j = lane; j < size; j += 32)
+    A[j] = cmul(ldps(A, j, ps), (dc ^ par32(j & mask)) ? f1 : f0);
 }
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
@@ -387,78 +366,62 @@ __device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u3
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0, sm = 0.0;
 #pragma unroll 1
-  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
-    double2 v[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 j = b0 + 32 * u;
-      if (j < size) {
-        const double a2 = abs2(v[u]);
-        if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
-      }
-    }
+  for (u32 j = lane; j < size; j += 32) {
+    const double a2 = abs2(ldps(A, j, ps));
+    if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
   }
   return make_double2(sp, sm);
 }
 
 // keep the chosen eigen-entries, scaled by rs; zero the others
-__device__ __noinline__ u32 sweep_filter(double2 *__restrict__ A, u32 size, u32 dmask,
-                                         u32 neg0, u32 want_neg, double rs, double ps) {
+__device__ __noinline__ SumNz sweep_filter(double2 *__restrict__ A, u32 size, u32 dmask,
+                                           u32 neg0, u32 want_neg, double rs, double ps) {
   const u32 lane = threadIdx.x & 31u;
-  const double2 Z = make_double2(0.0, 0.0);
-  u32 nz = 0;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
 #pragma unroll 1
-  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
-    double2 v[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 j = b0 + 32 * u;
-      if (j < size) {
-        const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
-        const double2 w = keep ? cscale(v[u], rs) : Z;
-        A[j] = w;
-        nz += nonzero(w);
-      }
+  for (u32 j = lane; j < size; j += 32) {
+    const double2 v = ldps(A, j, ps);
+    if ((neg0 ^ par32(j & dmask)) == want_neg) {
+      const double2 w = cscale(v, rs);
+      A[j] = w;
+      r.sum = __dadd_rn(r.sum, abs2(w));
+      r.nz += nonzero(w);
+    } else {
+      A[j] = make_double2(0.0, 0.0);
     }
   }
-  return nz;
+  return r;
 }
 
 // in-place compaction dropping coordinate isq: A[jp] = rs * A[src(jp)],
 // src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
 // at isq; src(jp) >= jp, so reads of a round finish before its writes
-__device__ __noinline__ u32 sweep_compact(double2 *__restrict__ A, u32 half, u32 isq, u32 mask,
-                                          u32 tau, double rs, double ps) {
+__device__ __noinline__ SumNz sweep_compact(double2 *__restrict__ A, u32 half, u32 isq, u32 mask,
+                                            u32 tau, double rs, double ps) {
   const u32 lane = threadIdx.x & 31u;
-  u32 nz = 0;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
 #pragma unroll 1
-  for (u32 b0 = 0; b0 < half; b0 += 32 * GS_SW) {
-    double2 v[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 jp = b0 + 32 * u + lane;
-      if (jp < half) {
-        const u32 j0 = ins_bit(jp, isq, 0);
-        v[u] = ldps(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
-      }
+  for (u32 b0 = 0; b0 < half; b0 += 32) {
+    const u32 jp = b0 + lane;
+    double2 v = make_double2(0.0, 0.0);
+    if (jp < half) {
+      const u32 j0 = ins_bit(jp, isq, 0);
+      v = ldps(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
     }
     __syncwarp();
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 jp = b0 + 32 * u + lane;
-      if (jp < half) {
-        const double2 w = cscale(v[u], rs);
-        A[jp] = w;
-        nz += nonzero(w);
-      }
+    if (jp < half) {
+      const double2 w = cscale(v, rs);
+      A[jp] = w;
+      r.sum = __dadd_rn(r.sum, abs2(w));
+      r.nz += nonzero(w);
     }
     __syncwarp();
   }
-  return nz;
+  return r;
 }
 
 // pivot measurement (ref state.py:178-208): w(m) = rep + sg * xi * part.
@@ -498,72 +461,35 @@ __device__ __noinline__ double sweep_pivot_p(const double2 *__restrict__ A, Pivo
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0;
 #pragma unroll 1
-  for (u32 b0 = lane; b0 < g.npairs; b0 += 32 * GS_SW) {
-    double2 vr[GS_SW], pr[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      u32 d_;
-      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], d_, ps);
-    }
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u)
-      if (b0 + 32 * u < g.npairs) sp = __dadd_rn(sp, abs2(cadd(vr[u], pr[u])));
+  for (u32 m = lane; m < g.npairs; m += 32) {
+    double2 vr, pr;
+    u32 d_;
+    pivot_terms(A, g, xpp, m, vr, pr, d_, ps);
+    sp = __dadd_rn(sp, abs2(cadd(vr, pr)));
   }
   return sp;
 }
-struct SumNz {
-  double sum;
-  u32 nz;
-};
 __device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g, double2 xpp,
                                             bool plus, double ps) {
   const u32 lane = threadIdx.x & 31u;
-  double sk = 0.0;
-  u32 nz = 0;
-#pragma unroll 1
-  for (u32 b0 = lane; b0 < g.npairs; b0 += 32 * GS_SW) {
-    double2 vr[GS_SW], pr[GS_SW];
-    u32 dst[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u)
-      if (b0 + 32 * u < g.npairs) pivot_terms(A, g, xpp, b0 + 32 * u, vr[u], pr[u], dst[u], ps);
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      if (b0 + 32 * u < g.npairs) {
-        const double2 w = prune(plus ? cadd(vr[u], pr[u]) : csub(vr[u], pr[u]));
-        A[dst[u]] = w;
-        sk = __dadd_rn(sk, abs2(w));
-        nz += nonzero(w);
-      }
-    }
-  }
   SumNz r;
-  r.sum = sk;
-  r.nz = nz;
+  r.sum = 0.0;
+  r.nz = 0;
+#pragma unroll 1
+  for (u32 m = lane; m < g.npairs; m += 32) {
+    double2 vr, pr;
+    u32 dst;
+    pivot_terms(A, g, xpp, m, vr, pr, dst, ps);
+    A[dst] = prune_acc(plus ? cadd(vr, pr) : csub(vr, pr), r.sum, r.nz);
+  }
   return r;
 }
 
-// renormalise every entry: A[j] *= rs
-__device__ __noinline__ u32 sweep_phase_scale(double2 *__restrict__ A, u32 size, double rs,
-                                              double ps) {
+// apply a pending renormalisation in place: A[j] = ps * A[j]
+__device__ __noinline__ void sweep_scale(double2 *__restrict__ A, u32 size, double ps) {
   const u32 lane = threadIdx.x & 31u;
-  u32 nz = 0;
 #pragma unroll 1
-  for (u32 b0 = lane; b0 < size; b0 += 32 * GS_SW) {
-    double2 v[GS_SW];
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) if (b0 + 32 * u < size) v[u] = ldps(A, b0 + 32 * u, ps);
-#pragma unroll
-    for (u32 u = 0; u < GS_SW; ++u) {
-      const u32 j = b0 + 32 * u;
-      if (j < size) {
-        const double2 w = cscale(v[u], rs);
-        A[j] = w;
-        nz += nonzero(w);
-      }
-    }
-  }
-  return nz;
+  for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], ps);
 }
 
 // ---------------------------------------------------------------- kernel
@@ -730,8 +656,15 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
       u32 next_word_pc = 0xFFFFFFFFu, fire_pc = 0xFFFFFFFFu;
       if (philox) fire_pc = (u32)stash[SF_FIRE * 32 + s];
       else if (scanned < P.nwords) next_word_pc = (u32)__ldg(tables + P.wordpc_off + scanned);
+      // chi in, and its norm (same per-lane order + tree as a sum pass)
+      double nrm = 0.0;
 #pragma unroll 1
-      for (u32 j = lane; j < (1u << k); j += 32) A[j] = Ast[j * 32u + s];
+      for (u32 j = lane; j < (1u << k); j += 32) {
+        const double2 v = Ast[j * 32u + s];
+        A[j] = v;
+        nrm = __dadd_rn(nrm, abs2(v));
+      }
+      nrm = warp_sum(nrm);
       __syncwarp();
       u32 wpc = pc;
       u64 hnext = h;
@@ -860,7 +793,8 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
           const u32 dc = par64(delta & c);
           const u32 tcase = wfl & 3u;
           if (tcase == T_DIAG) {
-            // beta == 0: pure phase per entry (ref state.py:120-126)
+            // beta == 0: pure phase per entry (ref state.py:120-126); the
+            // factors have modulus 1, the norm is kept
             sweep_phase(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
             ps = 1.0;
             __syncwarp();
@@ -884,16 +818,17 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             break;
           }
           // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
-          u32 nz;
+          SumNz r;
           if (tcase == T_BUTTERFLY) {
-            nz = sweep_butterfly(A, size >> 1, cb, dc, dmask, a, bx0, ps);
+            r = sweep_butterfly(A, size >> 1, cb, dc, dmask, a, bx0, ps);
           } else {
-            nz = sweep_grow(A, size, dc, dmask, a, bx0, ps);
+            r = sweep_grow(A, size, dc, dmask, a, bx0, ps);
             kcur = wk + 1;
           }
           ps = 1.0;
           __syncwarp();
-          cnt = warp_sum_u32(nz);
+          cnt = warp_sum_u32(r.nz);
+          nrm = warp_sum(r.sum);
           mbytes += (u64)kEntryBytes * (cin + cnt);
           if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
           if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
@@ -922,15 +857,28 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             if (pplus <= 0.0) return false;
             return rng.uniform(udraw) < pplus;
           };
+          // a renormalisation by rs that needs no data movement: deferred to
+          // the next pass over chi (ldps); nonzero count unchanged
+          auto defer_scale = [&](double rs) {
+            if (ps != 1.0) sweep_scale(A, size, ps);
+            ps = rs;
+            nrm = __dmul_rn(__dmul_rn(nrm, rs), rs);
+          };
           const u32 cin = cnt;
           bool plus;
-          u32 nz;
           if (mcase == M_DET) {
             // beta == 0: filter by eigenvalue (ref state.py:162-176)
             const u32 neg0 = (xi0 >> 1) ^ dc;
-            const double2 part = sweep_det_sums(A, size, dmask, neg0, ps);
-            const double sp = warp_sum(part.x);
-            const double sm = warp_sum(part.y);
+            double sp, sm;
+            if (dmask == 0) {
+              // every coordinate has eigenvalue (-1)^neg0: P+ is the norm
+              sp = neg0 ? 0.0 : nrm;
+              sm = neg0 ? nrm : 0.0;
+            } else {
+              const double2 part = sweep_det_sums(A, size, dmask, neg0, ps);
+              sp = warp_sum(part.x);
+              sm = warp_sum(part.y);
+            }
             plus = pick_plus(sp);
             const double chosen = plus ? sp : __dsub_rn(1.0, sp);
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
@@ -938,24 +886,24 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             const double rs = inv_sqrt_norm(plus ? sp : sm);
             if (wfl & MF_COMPACT) {
               const u32 tau = want_neg ^ neg0;
-              nz = sweep_compact(A, size >> 1, isq, dmask, tau, rs, ps);
+              const SumNz r = sweep_compact(A, size >> 1, isq, dmask, tau, rs, ps);
               ps = 1.0;
+              __syncwarp();
+              cnt = warp_sum_u32(r.nz);
+              nrm = warp_sum(r.sum);
               if (tau) c ^= vec;
               kcur = wk - 1;
+            } else if ((plus ? sm : sp) == 0.0) {
+              // the other eigenspace is empty: the filter is a pure
+              // renormalisation
+              defer_scale(rs);
             } else {
-              if ((plus ? sm : sp) == 0.0) {
-                // every entry of the other eigenspace is already zero: the
-                // filter is a pure renormalisation -- defer it to the next
-                // pass over A (ldps); the nonzero count is unchanged
-                if (ps != 1.0) sweep_phase_scale(A, size, 1.0, ps);
-                ps = rs;
-                nz = lane == 0 ? cnt : 0u;
-              } else {
-                nz = sweep_filter(A, size, dmask, neg0, want_neg, rs, ps);
-                ps = 1.0;
-              }
+              const SumNz r = sweep_filter(A, size, dmask, neg0, want_neg, rs, ps);
+              ps = 1.0;
+              __syncwarp();
+              cnt = warp_sum_u32(r.nz);
+              nrm = warp_sum(r.sum);
             }
-            __syncwarp();
           } else {
             // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
             PivotGeo g;
@@ -972,17 +920,19 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             ps = 1.0;
             __syncwarp();
             const double sk = warp_sum(w.sum);
-            if (warp_sum_u32(w.nz) == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            cnt = warp_sum_u32(w.nz);
+            if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
             const double rs = inv_sqrt_norm(sk);
             if (g.span) {
-              nz = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+              const SumNz r = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+              __syncwarp();
+              cnt = warp_sum_u32(r.nz);
+              nrm = warp_sum(r.sum);
               kcur = wk - 1;
             } else {
-              // pure renormalisation: deferred (see above)
-              ps = rs;
-              nz = w.nz;
+              nrm = sk;
+              defer_scale(rs);
             }
-            __syncwarp();
             if (g.ct) c ^= vec;
             // tableau sign update of the pivot (ref tableau.py:176-200)
             const u32 v = (u32)(sig_hi >> t) & 1u;
@@ -992,7 +942,6 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
             sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
           }
-          cnt = warp_sum_u32(nz);
           mbytes += (u64)kEntryBytes * (cin + cnt);
           const u32 bout = plus ? 0u : 1u;
           u32 rb = bout;
