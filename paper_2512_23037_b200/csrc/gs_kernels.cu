@@ -604,7 +604,7 @@ enum { WC_TOT = 0, WC_PRES, WC_DISC, WC_OVF, WC_COR, WC_UNS, WC_ERR, WC_MB, WC_N
 // is returned; 0xFFFFFFFF when no shot survives).  Lane states are read from
 // and written back to the per-warp stash.  Kept out of line so its unrolled
 // sweeps get their own register allocation, independent of the narrow loop.
-template <bool kSmemChi>
+template <bool kSmemChi, bool kPhilox>
 __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, const DevOut &O,
                                          u64 base, u32 pc, u32 nm, u64 h, u32 live,
                                          u32 *win, u32 *recb, double2 *An, double2 *A,
@@ -615,7 +615,7 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
   const u64 *__restrict__ tables = P.tables;
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
-  const bool philox = (R.flags & GS_RNG_PHILOX) != 0;
+  constexpr bool philox = kPhilox;   // RNG mode is a template parameter
   const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
   const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
   const u32 k = (u32)((h >> 16) & 0xff);
@@ -1034,7 +1034,7 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
   return exit_pc;
 }
 
-template <bool kSmemChi>
+template <bool kSmemChi, bool kPhilox>
 __global__ void __launch_bounds__(128, GS_MIN_BLOCKS)
 sample_kernel(DevProg P, DevRun R, DevOut O) {
   extern __shared__ __align__(16) u8 smem[];
@@ -1057,7 +1057,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
   const u64 *__restrict__ tables = P.tables;
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
-  const bool philox = (R.flags & GS_RNG_PHILOX) != 0;
+  constexpr bool philox = kPhilox;   // RNG mode is a template parameter
   const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
   const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
 #define AN(j) An[(j) * 32u + lane]
@@ -1125,7 +1125,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         stash[SF_FIRE * 32 + lane] = sfire;
         u32 live = __ballot_sync(FULL, sst == ST_RUNNING);
         __syncwarp();
-        const u32 exit_pc = wide_section<kSmemChi>(P, R, O, base, pc, nm, h, live, win, recb, An,
+        const u32 exit_pc = wide_section<kSmemChi, kPhilox>(P, R, O, base, pc, nm, h, live, win, recb, An,
                                                    A, stash);
         // every lane takes its state back
         s_lo = stash[SF_LO * 32 + lane];
@@ -1646,6 +1646,13 @@ static int fail(int code, const std::string &msg) {
       return fail(GS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// the four sampling kernels: chi placement x RNG mode
+template <typename F>
+static cudaError_t with_sample_kernel(bool smem_chi, bool philox, F f) {
+  if (smem_chi) return philox ? f(gs::sample_kernel<true, true>) : f(gs::sample_kernel<true, false>);
+  return philox ? f(gs::sample_kernel<false, true>) : f(gs::sample_kernel<false, false>);
+}
+
 extern "C" {
 
 const char *gs_last_error(void) { return g_err.c_str(); }
@@ -1760,6 +1767,7 @@ struct LaunchCfg {
 };
 
 static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &L) {
+  const bool philox = (r->flags & GS_RNG_PHILOX) != 0;
   const u32 K = p->info.max_dim;
   const size_t chi = (size_t)16 << K;
   L.rec_words32 = ((p->info.num_measurements + 63) / 64) * 2;
@@ -1786,17 +1794,11 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
     for (u32 w = 4; w >= 1; --w) {
       if ((size_t)w * L.warp_bytes > e->smem_optin) continue;
       int per = 0;
-      if (L.smem_chi) {
-        CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(w * L.warp_bytes)));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs::sample_kernel<true>, w * 32,
-                                                               w * L.warp_bytes));
-      } else {
-        CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(w * L.warp_bytes)));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs::sample_kernel<false>, w * 32,
-                                                               w * L.warp_bytes));
-      }
+      const size_t sm = w * L.warp_bytes;
+      CUDA_TRY(with_sample_kernel(L.smem_chi, philox, [&](auto kern) {
+        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        return err != cudaSuccess ? err : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, w * 32, sm);
+      }));
       if (per * (int)w > best) { best = per * (int)w; wpb = w; }
     }
   }
@@ -1805,21 +1807,12 @@ static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &
     return fail(GS_ERR_UNSUPPORTED, "per-warp state exceeds shared memory");
   L.wpb = wpb;
   L.smem = (size_t)wpb * L.warp_bytes;
-  if (L.smem_chi) {
-    CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
-  } else {
-    CUDA_TRY(cudaFuncSetAttribute(gs::sample_kernel<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
-  }
   int per_sm = 0;
-  if (L.smem_chi) {
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::sample_kernel<true>,
-                                                           wpb * 32, L.smem));
-  } else {
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs::sample_kernel<false>,
-                                                           wpb * 32, L.smem));
-  }
+  CUDA_TRY(with_sample_kernel(L.smem_chi, philox, [&](auto kern) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    return err != cudaSuccess ? err
+                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, L.smem);
+  }));
   if (per_sm < 1) return fail(GS_ERR_UNSUPPORTED, "kernel does not fit on an SM");
   u64 blocks = r->blocks ? r->blocks : (u64)e->num_sms * per_sm;
   // each warp takes batches of 32 shots
@@ -1929,10 +1922,10 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   CUDA_TRY(cudaMemsetAsync(e->d_next, 0, sizeof(u64), st));
   if (r->shot_count) {
     if (timed) CUDA_TRY(cudaEventRecord(e->ev0, st));
-    if (L.smem_chi)
-      gs::sample_kernel<true><<<L.blocks, L.wpb * 32, L.smem, st>>>(P, R, O);
-    else
-      gs::sample_kernel<false><<<L.blocks, L.wpb * 32, L.smem, st>>>(P, R, O);
+    CUDA_TRY(with_sample_kernel(L.smem_chi, (r->flags & GS_RNG_PHILOX) != 0, [&](auto kern) {
+      kern<<<L.blocks, L.wpb * 32, L.smem, st>>>(P, R, O);
+      return cudaGetLastError();
+    }));
     CUDA_TRY(cudaGetLastError());
     if (timed) CUDA_TRY(cudaEventRecord(e->ev1, st));
     e->launches += 1;

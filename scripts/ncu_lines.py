@@ -47,6 +47,32 @@ def disasm(lib, kernel_regex):
     return m
 
 
+def functions(lib, kernel_regex):
+    """offset -> device function name (noinline callees live inside the
+    kernel's .text section as $kernel$callee labels)."""
+    tmp = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, check=True,
+                   capture_output=True)
+    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
+    out = subprocess.run(["nvdisasm", "-c", os.path.join(tmp, cub)],
+                         capture_output=True, text=True).stdout
+    fn, inside, m = "kernel", False, {}
+    for ln in out.splitlines():
+        if ln.startswith("//---") and ".text." in ln:
+            inside = re.search(kernel_regex, ln) is not None
+            fn = "kernel"
+            continue
+        if not inside:
+            continue
+        g = re.match(r"^\$\S+\$_ZN2gs\d+(\w+?)E", ln)
+        if g:
+            fn = g.group(1)
+        g = re.match(r"\s+/\*([0-9a-f]{4,})\*/", ln)
+        if g:
+            m[int(g.group(1), 16)] = fn
+    return m
+
+
 def main():
     path = sys.argv[1]
     lib = os.path.abspath(sys.argv[2]) if len(sys.argv) > 2 else os.path.join(
@@ -60,7 +86,11 @@ def main():
         h.index("Instructions Executed")
     base = int(data[0][iA], 16)
     kname = rows[0][1] if rows and len(rows[0]) > 1 else ""
-    m = disasm(lib, r"sample_kernelILb1E" if "(bool)1" in kname else r"sample_kernelILb0E")
+    import re as _re
+    bools = _re.findall(r"\(bool\)(\d)", kname)
+    kre = "sample_kernel" + "".join("ILb%sE" % b if i == 0 else "Lb%sE" % b
+                                    for i, b in enumerate(bools)) if bools else "sample_kernel"
+    m = disasm(lib, kre)
     by_line_s, by_line_e = defaultdict(float), defaultdict(float)
     mism = 0
     for r in data:
@@ -92,6 +122,16 @@ def main():
         agg_e[name] += by_line_e[line]
     for nm in sorted(agg_s, key=lambda k: -agg_s[k]):
         print("%-28s %6.2f%% samp %6.2f%% inst" % (nm, 100 * agg_s[nm] / ts, 100 * agg_e[nm] / te))
+    fm = functions(lib, kre)
+    fs, fe = defaultdict(float), defaultdict(float)
+    for r in data:
+        f = fm.get(int(r[iA], 16) - base, "?")
+        fs[f] += float(r[iS] or 0)
+        fe[f] += float(r[iE] or 0)
+    print("-- per device function")
+    for f in sorted(fs, key=lambda k: -fs[k]):
+        print("%-28s %6.2f%% samp %6.2f%% inst" % (f, 100 * fs[f] / ts, 100 * fe[f] / te))
+    print("-- per source line")
     src = open(os.path.join(ROOT, "paper_2512_23037_b200", "csrc", "gs_kernels.cu")).read().splitlines()
     for line in sorted(by_line_s, key=lambda k: -by_line_s[k])[:top]:
         txt = src[line - 1].strip()[:80] if line else "?"

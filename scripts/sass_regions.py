@@ -29,7 +29,7 @@ cur = None
 inside = False
 for ln in out.splitlines():
     if ln.startswith("//---") and ".text." in ln:
-        inside = ("sample_kernelILb%s" % os.environ.get("GS_KERNEL_SMEM", "1")) in ln
+        inside = os.environ.get("GS_KERNEL", "sample_kernelILb1ELb1E") in ln
         continue
     if not inside:
         continue
