@@ -1147,7 +1147,8 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         __syncwarp();
         if (exit_pc == 0xFFFFFFFFu) break;   // no shot survived the section
         pc = exit_pc;
-        while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) < pc) ++nm;
+        if (!philox)   // the SplitMix wide scan starts at noise instruction nm
+          while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) < pc) ++nm;
         continue;
       }
       // ============================== narrow op, lane per shot
@@ -1188,7 +1189,6 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           if (ex | ez) lane_error(ex, ez, nrec, size);
         }
       } else {
-        while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) <= pc) ++nm;
         if (sst == ST_RUNNING && pc >= sfire) {
           sfire = 0xFFFFFFFFu;
           while (sgpos < P.nlocs) {
