@@ -311,12 +311,30 @@ __device__ __forceinline__ double2 prune_acc(double2 v, double &sum, u32 &nz) {
   return make_double2(0.0, 0.0);
 }
 
+// The T sweeps are the hottest code (about half of all instructions): chi
+// is addressed as shared memory when it lives there (LDS/STS instead of
+// generic loads), and the per-coordinate sign (-1)^s of the b-term is applied
+// to the product b*v by flipping sign bits -- cmul(-b, v) == -cmul(b, v)
+// bit for bit, since fma(-x, y, -z) == -fma(x, y, z).
+template <bool kS>
+__device__ __forceinline__ double2 *chi_ptr(double2 *A) {
+  if (!kS) return A;
+  extern __shared__ __align__(16) u8 smem_dyn[];
+  return reinterpret_cast<double2 *>(smem_dyn + (reinterpret_cast<u8 *>(A) - smem_dyn));
+}
+__device__ __forceinline__ double2 neg_if(double2 v, u32 s) {
+  const long long m = (long long)s << 63;
+  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ m),
+                      __longlong_as_double(__double_as_longlong(v.y) ^ m));
+}
+
 // T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
-// 294-306: a-term then b-term)
-__device__ __noinline__ SumNz sweep_butterfly(double2 *__restrict__ A, u32 half, u32 cb, u32 dc,
-                                              u32 dmask, double2 a, double2 bx0, double ps) {
+// 294-306: a-term then b-term); no renormalisation pending (caller)
+template <bool kS>
+__device__ __noinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32 dc, u32 dmask,
+                                              double2 a, double2 bx0) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
-  const double2 bx1 = cneg(bx0);
   const u32 hb = 31 - __clz(cb);
   SumNz r;
   r.sum = 0.0;
@@ -324,28 +342,28 @@ __device__ __noinline__ SumNz sweep_butterfly(double2 *__restrict__ A, u32 half,
 #pragma unroll 1
   for (u32 m = lane; m < half; m += 32) {
     const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
-    const double2 v0 = ldps(A, j0, ps), v1 = ldps(A, j1, ps);
+    const double2 v0 = A[j0], v1 = A[j1];
     const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
-    A[j0] = prune_acc(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)), r.sum, r.nz);
-    A[j1] = prune_acc(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)), r.sum, r.nz);
+    A[j0] = prune_acc(cadd(cmul(a, v0), neg_if(cmul(bx0, v1), s1)), r.sum, r.nz);
+    A[j1] = prune_acc(cadd(cmul(a, v1), neg_if(cmul(bx0, v0), s0)), r.sum, r.nz);
   }
   return r;
 }
 
 // T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
-__device__ __noinline__ SumNz sweep_grow(double2 *__restrict__ A, u32 size, u32 dc, u32 dmask,
-                                         double2 a, double2 bx0, double ps) {
+template <bool kS>
+__device__ __noinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmask, double2 a,
+                                         double2 bx0) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
-  const double2 bx1 = cneg(bx0);
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
 #pragma unroll 1
   for (u32 j = lane; j < size; j += 32) {
-    const double2 v = ldps(A, j, ps);
-    const u32 s_ = dc ^ par32(j & dmask);
+    const double2 v = A[j];
     A[j] = prune_acc(cmul(a, v), r.sum, r.nz);
-    A[size + j] = prune_acc(cmul(s_ ? bx1 : bx0, v), r.sum, r.nz);
+    A[size + j] = prune_acc(neg_if(cmul(bx0, v), dc ^ par32(j & dmask)), r.sum, r.nz);
   }
   return r;
 }
@@ -818,14 +836,15 @@ __device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, cons
             break;
           }
           // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
+          if (ps != 1.0) sweep_scale(A, size, ps);   // rare: right after a deferral
+          ps = 1.0;
           SumNz r;
           if (tcase == T_BUTTERFLY) {
-            r = sweep_butterfly(A, size >> 1, cb, dc, dmask, a, bx0, ps);
+            r = sweep_butterfly<kSmemChi>(A, size >> 1, cb, dc, dmask, a, bx0);
           } else {
-            r = sweep_grow(A, size, dc, dmask, a, bx0, ps);
+            r = sweep_grow<kSmemChi>(A, size, dc, dmask, a, bx0);
             kcur = wk + 1;
           }
-          ps = 1.0;
           __syncwarp();
           cnt = warp_sum_u32(r.nz);
           nrm = warp_sum(r.sum);
