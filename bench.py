@@ -96,7 +96,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -157,7 +157,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--shots-per-step", type=int, default=1 << 22)
+    ap.add_argument("--shots-per-step", type=int, default=1 << 24)
     ap.add_argument("--workload", default="msc_d5", choices=sorted(WORKLOADS))
     ap.add_argument("--p", type=float, default=1e-3)
     ap.add_argument("--rng", default="philox", choices=["philox", "splitmix"])
