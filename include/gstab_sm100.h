@@ -100,7 +100,7 @@ typedef struct {
   uint32_t flags;            /* GS_POSTSELECT | GS_RNG_PHILOX | ...      */
   uint32_t warps_per_block;  /* 0 = auto                                 */
   uint32_t blocks;           /* 0 = auto (persistent grid)               */
-  uint32_t reserved;         /* must be 0                                */
+  uint32_t chunk_shots;      /* shots per section pass, 0 = auto (test)  */
   const uint64_t *seeds;     /* optional host per-shot seeds (SplitMix)  */
 } gs_run_params;
 

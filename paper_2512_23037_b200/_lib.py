@@ -59,7 +59,7 @@ class GsRunParams(ct.Structure):
     _fields_ = [("master_seed", ct.c_uint64), ("shot_begin", ct.c_uint64),
                 ("shot_count", ct.c_uint64), ("capacity", ct.c_uint64),
                 ("flags", ct.c_uint32), ("warps_per_block", ct.c_uint32),
-                ("blocks", ct.c_uint32), ("reserved", ct.c_uint32),
+                ("blocks", ct.c_uint32), ("chunk_shots", ct.c_uint32),
                 ("seeds", ct.POINTER(ct.c_uint64))]
 
 

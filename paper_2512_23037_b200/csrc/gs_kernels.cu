@@ -69,7 +69,6 @@ struct DevRun {
 
 struct DevOut {
   long long *counters;
-  u64 *next_shot;
   u8 *status;
   int *aux;
   u64 *rec;
@@ -83,9 +82,7 @@ struct DevOut {
   u32 mode;
   u32 warp_bytes;       // dynamic smem bytes per warp
   u32 rec_in_smem;
-  u32 chi_off;          // byte offset of the record columns in the warp's smem slice
-  u64 *gstash;          // per-warp lane-state stash for wide sections
-  double2 *gan;         // per-warp narrow-chi parking (shared-memory chi)
+  u32 chi_off;          // wide kernel: byte offset of chi in the warp's smem slice
   u64 *witness;         // optional: global indices of preserved shots with a
   u32 *witness_count;   //   flipped observable (paper §V-B witnesses)
   u32 witness_cap;
@@ -275,6 +272,8 @@ constexpr u32 kNarrowBytes = (1u << GS_KN) * 32u * 16u;   // An[2^KN][32] double
 constexpr u32 kCntBytes = 64;                              // per-warp counters
 
 __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y != 0.0; }
+
+__device__ __forceinline__ u32 lanemask_lt(u32 lane) { return (1u << lane) - 1u; }
 
 // @region sweeps
 // ---------------------------------------------------------------- wide sweeps
@@ -510,34 +509,36 @@ __device__ __noinline__ void sweep_scale(double2 *__restrict__ A, u32 size, doub
   for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], ps);
 }
 
-// ---------------------------------------------------------------- kernel
+// ---------------------------------------------------------------- kernels
 //
-// Execution model.  A warp takes a BATCH of 32 consecutive shots (one per
-// lane) and walks the static op stream with all lanes at the same pc:
+// Execution model: breadth-first SECTIONS.  k is static per op
+// (shot-invariant basis, compiler.py), so the op stream splits on the host
+// into alternating sections of narrow ops (chi dimension k <= GS_KN before
+// and after the op) and wide ops (k > GS_KN, GROW_LIMIT).  One launch per
+// section runs every live shot of the chunk through it:
 //
-//  * narrow ops (chi dimension k <= GS_KN before and after the op) run
-//    lane-per-shot: every lane applies the op to its own shot, chi lives in
-//    shared memory as An[j * 32 + lane] (row j uniform across lanes, so
-//    accesses are bank-conflict free) -- the fixed per-op cost (decode,
-//    sign-mask parities, draws) is paid once for 32 shots;
-//  * wide ops (k > GS_KN, and GROW_LIMIT) run warp-per-shot: the warp takes
-//    the live lanes' shots one at a time through the whole wide section
-//    (lanes split the 2^k coordinates, chi in a per-warp buffer, WU-way
-//    unrolled sweeps for memory-level parallelism) and hands each surviving
-//    shot back at the first narrow op after it.  Lane states are parked in
-//    a per-warp global stash meanwhile, so the wide loops have the
-//    registers to themselves.
+//  * narrow_kernel: a warp takes 32 shots (one per lane) and walks the
+//    section with all lanes at the same pc; chi lives in shared memory as
+//    An[j * 32 + lane] (row j uniform across lanes, conflict free); the
+//    fixed per-op cost (decode, sign-mask popcounts, static tables) is paid
+//    once per 32 shots;
+//  * wide_kernel: a warp takes one shot and splits its 2^k coordinates over
+//    the lanes (chi in the warp's shared-memory buffer; `sweep_*`).
 //
-// k is static per op (shot-invariant basis, compiler.py), so every shot of
-// the batch enters and leaves a wide section at the same pc.  Shots that
-// end (discarded / preserved / overflow) leave their lane idle until the
-// batch finishes.  GS_WIDE_ONLY runs every op warp-per-shot (A/B, tests).
+// Shots that survive a section are appended to a global queue (fixed-size
+// slots: state words, record bits, chi of dimension <= GS_KN) read by the
+// next section's launch.  Each launch keeps only its own code hot, which is
+// what the instruction cache needs (B200: 32 KB L1.5).
+// GS_WIDE_ONLY runs the whole program as one wide section (A/B, tests).
 
-#ifndef GS_MIN_BLOCKS
-#define GS_MIN_BLOCKS 3   // <= 168 registers (no spills); shared memory holds 12-13 warps/SM anyway (A/B: 21.6M vs 20.7M at 4)
+#ifndef GS_NARROW_BLOCKS
+#define GS_NARROW_BLOCKS 4
+#endif
+#ifndef GS_WIDE_BLOCKS
+#define GS_WIDE_BLOCKS 3   // <= 168 registers (no spills); shared memory holds 12-13 warps/SM anyway
 #endif
 
-__device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
+__host__ __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
   return kind == OP_GROW_LIMIT || k > GS_KN ||
          (kind == OP_T && (fl & 3u) == T_GROW && k + 1 > GS_KN);
 }
@@ -610,515 +611,122 @@ __device__ __forceinline__ const u64 *noise_owner(const DevProg &P, u32 l) {
   return P.tables + P.noise_off + 4ull * lo;
 }
 
-// per-lane stash fields (u64), layout stash[f * 32 + lane]
-enum { SF_LO = 0, SF_HI, SF_C, SF_OBS, SF_MB, SF_PICK, SF_SEED, SF_SHOT, SF_CNTK, SF_ST,
-       SF_GEO, SF_FIRE, SF_N };
+// queue slot layout (u64 words): state, then record bits (u32 words), then
+// the chi rows [0, 2^GS_KN)
+enum { Q_SL = 0, Q_LO, Q_HI, Q_C, Q_OBS, Q_MB, Q_PICK, Q_SEED, Q_CNTK, Q_GEO, Q_FIRE, Q_HDR = 12 };
+
+struct DevSec {
+  u32 pc0, k0, nm0;        // first op, its chi dimension, first noise instr. with ipc >= pc0
+  u64 first, count;        // fresh shots (q_in == nullptr): run-local indices [first, first+count)
+  const u64 *q_in;         // else: queue slots and their number
+  const u32 *n_in;
+  u64 *q_out;              // survivors at the section end (nullptr: last section)
+  u32 *n_out;
+  unsigned long long *work; // atomic work counter
+};
+
+// record words of a slot, rounded to 16 B so the chi rows are double2-aligned
+__host__ __device__ __forceinline__ u32 rec_u64(u32 rec_words32) { return ((rec_words32 + 3) / 4) * 2; }
+
+__device__ __forceinline__ u32 slot_u64(const DevProg &P) {
+  return Q_HDR + rec_u64(P.rec_words32) + 2 * (1u << GS_KN);
+}
 
 // per-warp counters in shared memory
 enum { WC_TOT = 0, WC_PRES, WC_DISC, WC_OVF, WC_COR, WC_UNS, WC_ERR, WC_MB, WC_N };
 
-// One wide section, warp per shot: runs every live lane's shot (mask
-// `live`) from the wide op at `pc` to the first narrow op after it (its pc
-// is returned; 0xFFFFFFFF when no shot survives).  Lane states are read from
-// and written back to the per-warp stash.  Kept out of line so its unrolled
-// sweeps get their own register allocation, independent of the narrow loop.
-template <bool kSmemChi, bool kPhilox>
-__device__ __noinline__ u32 wide_section(const DevProg &P, const DevRun &R, const DevOut &O,
-                                         u64 base, u32 pc, u32 nm, u64 h, u32 live,
-                                         u32 *win, u32 *recb, double2 *An, double2 *A,
-                                         u64 *stash) {
-  const u32 lane = threadIdx.x & 31u;
-  const u32 n = P.n;
-  const u64 *__restrict__ ops = P.ops;
-  const u64 *__restrict__ tables = P.tables;
-  const u64 *__restrict__ locs = P.locs;
-  const double2 Z = make_double2(0.0, 0.0);
-  constexpr bool philox = kPhilox;   // RNG mode is a template parameter
-  const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
-  const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
-  const u32 k = (u32)((h >> 16) & 0xff);
-  (void)n;
-    u32 exit_pc = 0xFFFFFFFFu, exit_k = 0;
-    // shared-memory chi: the wide buffer A aliases the narrow array An, so
-    // the lanes' narrow chi rows [0, 2^k) are parked in global memory (Ast)
-    // for the section and restored at its end
-    double2 *Ast = An;
-    if (kSmemChi) {
-      Ast = O.gan + ((u64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32ull << GS_KN);
-#pragma unroll 1
-      for (u32 i = lane; i < (32u << k); i += 32) Ast[i] = An[i];
-      __syncwarp();
-    }
-    while (live) {
-      const u32 s = __ffs(live) - 1;
-      live &= live - 1;
-      u32 *recw = recb + s;
-      Rng rng;
-      rng.philox = philox;
-      rng.master = R.master;
-      rng.shot = stash[SF_SHOT * 32 + s];
-      rng.seed = stash[SF_SEED * 32 + s];
-      u64 sig_lo = stash[SF_LO * 32 + s], sig_hi = stash[SF_HI * 32 + s];
-      u64 c = stash[SF_C * 32 + s], obs = stash[SF_OBS * 32 + s];
-      u64 mbytes = stash[SF_MB * 32 + s];
-      u32 cnt = (u32)stash[SF_CNTK * 32 + s], kcur = k;
-      int status = ST_RUNNING, aux = -1;
-      double ps = 1.0;        // renormalisation pending on A (see ldps)
-      const u64 gw_ = stash[SF_GEO * 32 + s];
-      u32 gj = (u32)gw_, gpos = (u32)(gw_ >> 32);
-      u64 gpick = stash[SF_PICK * 32 + s];
-      // noise scan state: everything inserted before `pc` is applied
-      u32 cursor = P.nlocs;
-      if (nm < P.nnoise) cursor = (u32)__ldg(tables + P.noise_off + 4ull * nm + 1);
-      u32 scanned = cursor >> 5, search_w = scanned;
-      u32 next_word_pc = 0xFFFFFFFFu, fire_pc = 0xFFFFFFFFu;
-      if (philox) fire_pc = (u32)stash[SF_FIRE * 32 + s];
-      else if (scanned < P.nwords) next_word_pc = (u32)__ldg(tables + P.wordpc_off + scanned);
-      // chi in, and its norm (same per-lane order + tree as a sum pass)
-      double nrm = 0.0;
-#pragma unroll 1
-      for (u32 j = lane; j < (1u << k); j += 32) {
-        const double2 v = Ast[j * 32u + s];
-        A[j] = v;
-        nrm = __dadd_rn(nrm, abs2(v));
-      }
-      nrm = warp_sum(nrm);
-      __syncwarp();
-      u32 wpc = pc;
-      u64 hnext = h;
-      while (status == ST_RUNNING) {
-        if (!wide_only) {
-          const u32 kind_ = (u32)(hnext & 0xff), k_ = (u32)((hnext >> 16) & 0xff),
-                    fl_ = (u32)((hnext >> 24) & 0xff);
-          if (!op_is_wide(kind_, k_, fl_)) { exit_pc = wpc; exit_k = k_; break; }
-        }
-        // @region wide: noise
-        if (wpc >= next_word_pc || wpc >= fire_pc) {
-          // apply E = OR of fired letters of one noise instruction
-          // (ref noise.py:68-100, state.py:88-102)
-          auto apply_error = [&](u64 ex, u64 ez, const u64 *nrec) {
-            if (!(ex | ez)) return;
-            const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
-                                           sig_lo, sig_hi);
-            const double2 php = ipow(e.xi);
-            sweep_phase(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
-            ps = 1.0;
-            __syncwarp();
-            c ^= e.beta;
-            mbytes += 2ull * kEntryBytes * cnt + sign_bytes;
-          };
-          if (philox) {
-            // walk the candidate schedule (lane-uniform, rare)
-            fire_pc = 0xFFFFFFFFu;
-            while (gpos < P.nlocs) {
-              const u64 *nrec = noise_owner(P, gpos);
-              const u64 nw0 = __ldg(nrec);
-              const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-              if (ipc > wpc) { fire_pc = ipc; break; }
-              const u32 loc0 = (u32)__ldg(nrec + 1);
-              u64 ex = 0, ez = 0;
-              while (gpos < loc0 + nloc) {
-                const u32 l = gpos;
-                bool ok = true;
-                if (!P.noise_uniform) ok = geo_accept(R.master, rng.shot, gj - 1, __ldg(tables + P.acc_off + l));
-                if (ok) {
-                  const u64 lw = __ldg(locs + 2ull * l);
-                  noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
-                               (double)gpick * 0x1.0p-53, ex, ez);
-                }
-                const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, rng.shot, gj, l + 1);
-                gpos = gc.pos;
-                gpick = gc.pick;
-                ++gj;
-              }
-              apply_error(ex, ez, nrec);
-            }
-          } else {
-            // SplitMix: one fire draw per location, 32 locations per ballot
-            while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= wpc) {
-              const u32 l = scanned * 32u + lane;
-              bool fire = false;
-              if (l < P.nlocs) {
-                const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
-                fire = rng.m53((u32)lw) < thr;
-              }
-              const u32 bits = __ballot_sync(FULL, fire);
-              if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
-              ++scanned;
-            }
-            __syncwarp();
-            next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
-            fire_pc = 0xFFFFFFFFu;
-#pragma unroll 1
-            for (;;) {
-              // next fired location >= cursor among the scanned words
-              u32 fl_loc = 0xFFFFFFFFu;
-              u32 w = max(search_w, cursor >> 5);
-#pragma unroll 1
-              for (; w < scanned; ++w) {
-                u32 bits = win[w & (kWinWords - 1)];
-                if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
-                if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
-              }
-              search_w = w;
-              if (fl_loc == 0xFFFFFFFFu) break;
-              const u64 *nrec = noise_owner(P, fl_loc);
-              const u64 nw0 = __ldg(nrec);
-              const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-              if (ipc > wpc) { fire_pc = ipc; break; }
-              const u32 loc0 = (u32)__ldg(nrec + 1);
-              cursor = loc0 + nloc;
-              u64 ex = 0, ez = 0;
-#pragma unroll 1
-              for (u32 i = lane; i < nloc; i += 32) {
-                const u32 l = loc0 + i;
-                if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
-                const u64 lw = __ldg(locs + 2ull * l);
-                const u32 nk = (u32)(lw >> 48) & 3;
-                const double u = nk <= NK_DEP2 ? rng.uniform((u32)lw + 1) : 0.0;
-                noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
-              }
-              apply_error(warp_or64(ex), warp_or64(ez), nrec);
-            }
-          }
-        }
-
-        // @region wide: dispatch
-        const u64 *op = ops + wpc;
-        const u64 hw = hnext;
-        const u32 wkind = (u32)(hw & 0xff), wlen = (u32)((hw >> 8) & 0xff);
-        const u32 wk = (u32)((hw >> 16) & 0xff), wfl = (u32)((hw >> 24) & 0xff);
-        const u32 winstr = (u32)(hw >> 32);
-        wpc += wlen;
-        hnext = __ldg(ops + wpc);       // prefetch the next header
-        kcur = wk;
-        const u32 size = 1u << wk;
-
-        // @region wide: T
-        if (wkind == OP_T || wkind == OP_GROW_LIMIT) {
-          sig_lo ^= __ldg(op + 1);
-          sig_hi ^= __ldg(op + 2);
-          // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
-          // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
-          const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
-          const u64 delta = __ldg(op + 5);
-          const u64 w6 = __ldg(op + 6);
-          const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
-          const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
-          const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
-          mbytes += __ldg(op + 11);
-          const double2 bx0 = flip ? cneg(bxs) : bxs;
-          const u32 dc = par64(delta & c);
-          const u32 tcase = wfl & 3u;
-          if (tcase == T_DIAG) {
-            // beta == 0: pure phase per entry (ref state.py:120-126); the
-            // factors have modulus 1, the norm is kept
-            sweep_phase(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
-            ps = 1.0;
-            __syncwarp();
-            mbytes += 32ull * cnt;
-            continue;
-          }
-          const u32 cin = cnt;
-          if (wkind == OP_GROW_LIMIT) {
-            u32 nz = 0;
-            const double2 bx1 = cneg(bx0);
-#pragma unroll 1
-            for (u32 j = lane; j < size; j += 32) {
-              const double2 v = ldps(A, j, ps);
-              const u32 s_ = dc ^ par32(j & dmask);
-              nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
-              nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
-            }
-            nz = warp_sum_u32(nz);
-            status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
-            aux = (int)winstr;
-            break;
-          }
-          // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
-          if (ps != 1.0) sweep_scale(A, size, ps);   // rare: right after a deferral
-          ps = 1.0;
-          SumNz r;
-          if (tcase == T_BUTTERFLY) {
-            r = sweep_butterfly<kSmemChi>(A, size >> 1, cb, dc, dmask, a, bx0);
-          } else {
-            r = sweep_grow<kSmemChi>(A, size, dc, dmask, a, bx0);
-            kcur = wk + 1;
-          }
-          __syncwarp();
-          cnt = warp_sum_u32(r.nz);
-          nrm = warp_sum(r.sum);
-          mbytes += (u64)kEntryBytes * (cin + cnt);
-          if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
-          if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
-          continue;
-        }
-
-        // @region wide: meas
-        if (wkind == OP_MEAS) {
-          sig_lo ^= __ldg(op + 1);
-          sig_hi ^= __ldg(op + 2);
-          const u32 mcase = wfl & 3u;
-          const u32 xi0 = (((wfl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
-          const u64 delta = __ldg(op + 5);
-          const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
-          const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
-          const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
-          const u64 vec = __ldg(op + 8);
-          const u64 w13 = __ldg(op + 13);
-          const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
-          mbytes += __ldg(op + 17);
-          const u32 dc = par64(delta & c);
-          // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
-          // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
-          auto pick_plus = [&](double pplus) -> bool {
-            if (pplus >= 1.0) return true;
-            if (pplus <= 0.0) return false;
-            return rng.uniform(udraw) < pplus;
-          };
-          // a renormalisation by rs that needs no data movement: deferred to
-          // the next pass over chi (ldps); nonzero count unchanged
-          auto defer_scale = [&](double rs) {
-            if (ps != 1.0) sweep_scale(A, size, ps);
-            ps = rs;
-            nrm = __dmul_rn(__dmul_rn(nrm, rs), rs);
-          };
-          const u32 cin = cnt;
-          bool plus;
-          if (mcase == M_DET) {
-            // beta == 0: filter by eigenvalue (ref state.py:162-176)
-            const u32 neg0 = (xi0 >> 1) ^ dc;
-            double sp, sm;
-            if (dmask == 0) {
-              // every coordinate has eigenvalue (-1)^neg0: P+ is the norm
-              sp = neg0 ? 0.0 : nrm;
-              sm = neg0 ? nrm : 0.0;
-            } else {
-              const double2 part = sweep_det_sums(A, size, dmask, neg0, ps);
-              sp = warp_sum(part.x);
-              sm = warp_sum(part.y);
-            }
-            plus = pick_plus(sp);
-            const double chosen = plus ? sp : __dsub_rn(1.0, sp);
-            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
-            const u32 want_neg = plus ? 0u : 1u;
-            const double rs = inv_sqrt_norm(plus ? sp : sm);
-            if (wfl & MF_COMPACT) {
-              const u32 tau = want_neg ^ neg0;
-              const SumNz r = sweep_compact(A, size >> 1, isq, dmask, tau, rs, ps);
-              ps = 1.0;
-              __syncwarp();
-              cnt = warp_sum_u32(r.nz);
-              nrm = warp_sum(r.sum);
-              if (tau) c ^= vec;
-              kcur = wk - 1;
-            } else if ((plus ? sm : sp) == 0.0) {
-              // the other eigenspace is empty: the filter is a pure
-              // renormalisation
-              defer_scale(rs);
-            } else {
-              const SumNz r = sweep_filter(A, size, dmask, neg0, want_neg, rs, ps);
-              ps = 1.0;
-              __syncwarp();
-              cnt = warp_sum_u32(r.nz);
-              nrm = warp_sum(r.sum);
-            }
-          } else {
-            // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
-            PivotGeo g;
-            g.span = mcase == M_PIVOT_SPAN;
-            g.npairs = g.span ? (size >> 1) : size;
-            g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
-            g.dc = dc; g.dmask = dmask;
-            const double2 xpp = ipow(xi0);   // i^xi0, exact
-            const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p(A, g, xpp, ps)));
-            plus = pick_plus(pp);
-            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
-            const SumNz w = sweep_pivot_w(A, g, xpp, plus, ps);
-            ps = 1.0;
-            __syncwarp();
-            const double sk = warp_sum(w.sum);
-            cnt = warp_sum_u32(w.nz);
-            if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
-            const double rs = inv_sqrt_norm(sk);
-            if (g.span) {
-              const SumNz r = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
-              __syncwarp();
-              cnt = warp_sum_u32(r.nz);
-              nrm = warp_sum(r.sum);
-              kcur = wk - 1;
-            } else {
-              nrm = sk;
-              defer_scale(rs);
-            }
-            if (g.ct) c ^= vec;
-            // tableau sign update of the pivot (ref tableau.py:176-200)
-            const u32 v = (u32)(sig_hi >> t) & 1u;
-            if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
-            sig_lo ^= __ldg(op + 11);
-            sig_hi ^= __ldg(op + 12);
-            sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
-            sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
-          }
-          mbytes += (u64)kEntryBytes * (cin + cnt);
-          const u32 bout = plus ? 0u : 1u;
-          u32 rb = bout;
-          if ((wfl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
-          if (wfl & MF_RECORD) {
-            if (lane == 0 && rb) recw[(slot >> 5) * 32u] |= 1u << (slot & 31);
-            __syncwarp();
-          }
-          if ((wfl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
-          continue;
-        }
-
-        // @region wide: feedback/detector/end
-        if (wkind == OP_FEEDBACK) {
-          const u32 idx = (u32)__ldg(op + 1);
-          if ((recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u) {
-            sig_lo ^= __ldg(op + 2);
-            sig_hi ^= __ldg(op + 3);
-            mbytes += __ldg(op + 4);
-          }
-          continue;
-        }
-        if (wkind == OP_DETECTOR || wkind == OP_OBSERVABLE) {
-          const u64 w1 = __ldg(op + 1);
-          const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
-          const u64 off = __ldg(op + 2);
-          u32 bb = 0;
-#pragma unroll 1
-          for (u32 i = lane; i < nidx; i += 32) {
-            const u32 idx = (u32)__ldg(tables + off + i);
-            bb ^= (recw[(idx >> 5) * 32u] >> (idx & 31)) & 1u;
-          }
-          const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
-          if (wkind == OP_DETECTOR) {
-            if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
-          } else {
-            obs ^= (u64)parity << id;
-          }
-          continue;
-        }
-        if (wkind == OP_END) {
-          sig_lo ^= __ldg(op + 1);
-          sig_hi ^= __ldg(op + 2);
-          mbytes += __ldg(op + 3);
-          status = ST_PRESERVED;
-          break;
-        }
-        status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
-        aux = -2;
-      }
-      // @region wide: exit
-      // hand the shot back (stash) and its chi back to its lane
-      __syncwarp();
-      if (lane == 0) {
-        stash[SF_LO * 32 + s] = sig_lo;
-        stash[SF_HI * 32 + s] = sig_hi;
-        stash[SF_C * 32 + s] = c;
-        stash[SF_OBS * 32 + s] = obs;
-        stash[SF_MB * 32 + s] = mbytes;
-        stash[SF_PICK * 32 + s] = gpick;
-        stash[SF_CNTK * 32 + s] = (u64)cnt | ((u64)kcur << 32);
-        stash[SF_ST * 32 + s] = (u64)(status & 0xff) | ((u64)(u32)aux << 32) |
-                                ((u64)(status != ST_RUNNING && O.mode == MODE_DUMP) << 8);
-        stash[SF_GEO * 32 + s] = (u64)gj | ((u64)gpos << 32);
-        stash[SF_FIRE * 32 + s] = fire_pc;
-      }
-      if (status == ST_RUNNING) {
-#pragma unroll 1
-        for (u32 j = lane; j < (1u << kcur); j += 32) Ast[j * 32u + s] = ldps(A, j, ps);
-      } else if (O.mode == MODE_DUMP) {
-        const u64 ssl = base + s;
-        if (lane == 0) {
-          O.sig[2 * ssl] = sig_lo;
-          O.sig[2 * ssl + 1] = sig_hi;
-          O.cvec[ssl] = c;
-          O.dim[ssl] = kcur;
-        }
-        const u64 stride = 1ull << P.max_dim;
-#pragma unroll 1
-        for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[ssl * stride + j] = ldps(A, j, ps);
-      }
-      __syncwarp();
-    }
-  if (kSmemChi && exit_pc != 0xFFFFFFFFu) {
-    __syncwarp();
-#pragma unroll 1
-    for (u32 i = lane; i < (32u << exit_k); i += 32) An[i] = Ast[i];
-  }
+__device__ __forceinline__ void flush_counters(const DevOut &O, unsigned long long *wcnt, u32 lane) {
   __syncwarp();
-  return exit_pc;
+  if (lane < WC_N && wcnt[lane]) {
+    static_assert(WC_N == 8, "counter order");
+    const int dst[WC_N] = {GS_C_TOTAL, GS_C_PRESERVED, GS_C_DISCARDED, GS_C_OVERFLOW,
+                           GS_C_CORRUPT, GS_C_UNSUPPORTED, GS_C_ERROR_SHOTS, GS_C_MODEL_BYTES};
+    atomicAdd((unsigned long long *)O.counters + dst[lane], wcnt[lane]);
+  }
 }
 
-template <bool kSmemChi, bool kPhilox>
-__global__ void __launch_bounds__(128, GS_MIN_BLOCKS)
-sample_kernel(DevProg P, DevRun R, DevOut O) {
+// ---------------------------------------------------------------- narrow
+
+template <bool kPhilox>
+__global__ void __launch_bounds__(128, GS_NARROW_BLOCKS)
+narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   extern __shared__ __align__(16) u8 smem[];
   const u32 lane = threadIdx.x & 31u;
   const u32 wib = threadIdx.x >> 5;
   const u32 wpb = blockDim.x >> 5;
   const u64 gw = (u64)blockIdx.x * wpb + wib;
   u8 *mine = smem + (size_t)wib * O.warp_bytes;
-  u32 *win = reinterpret_cast<u32 *>(mine);
-  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine + kWinBytes);
-  double2 *An = reinterpret_cast<double2 *>(mine + kWinBytes + kCntBytes);
+  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
+  double2 *An = reinterpret_cast<double2 *>(mine + kCntBytes);
   // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
-  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + O.chi_off)
+  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kNarrowBytes)
                             : O.grec + gw * (u64)P.rec_words32 * 32u;
-  double2 *A = kSmemChi ? An
-                        : O.gchi + gw * ((u64)1 << P.max_dim);
-  u64 *stash = O.gstash + gw * (u64)(SF_N * 32);
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
   const u64 *__restrict__ tables = P.tables;
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
   constexpr bool philox = kPhilox;   // RNG mode is a template parameter
-  const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
   const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
+  const u32 SU = slot_u64(P);
 #define AN(j) An[(j) * 32u + lane]
 
   if (lane < WC_N) wcnt[lane] = 0;
   __syncwarp();
+  const u64 total = S.q_in ? (u64)*S.n_in : S.count;
 
 #pragma unroll 1
   for (;;) {
-    // @region batch setup
+    // @region narrow: batch setup
     u64 base = 0;
-    if (lane == 0) base = atomicAdd(O.next_shot, 32ull);
+    if (lane == 0) base = atomicAdd(S.work, 32ull);
     base = __shfl_sync(FULL, base, 0);
-    if (base >= R.shot_count) break;
-    const u64 sl = base + lane;
-    const bool valid = sl < R.shot_count;
-    u64 shot = R.shot_begin + sl;
-    u64 seed = 0;
-    if (valid && !philox) seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
-#pragma unroll 1
-    for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
-    AN(0) = make_double2(1.0, 0.0);
-
+    if (base >= total) break;
+    const u64 idx = base + lane;
+    const bool valid = idx < total;
     // this lane's shot (ref sampler.py:169-255 state: tableau signs, coset
     // offset, record, observables)
+    u64 sl = 0, shot = 0, seed = 0;
     u64 s_lo = 0, s_hi = 0, sc = 0, sobs = 0, smb = 0;
-    u32 scnt = 1, sk = 0;
+    u32 scnt = 1, sk = S.k0;
     int sst = valid ? ST_RUNNING : ST_PRESERVED, saux = -1;
-    bool dumped = false;
     // Philox fire schedule of this shot
     u32 sgj = 0, sgpos = 0xFFFFFFFFu, sfire = 0xFFFFFFFFu;
     u64 sgpick = 0;
-    if (philox && valid && P.geo_len > 1 && P.nlocs) {
-      const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, shot, 0u, 0u);
-      sgpos = gc.pos;
-      sgpick = gc.pick;
-      sgj = 1;
-      sfire = sgpos < P.nlocs ? 0u : 0xFFFFFFFFu;
+    if (!S.q_in) {
+      sl = S.first + idx;
+      shot = R.shot_begin + sl;
+      if (valid && !philox) seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
+#pragma unroll 1
+      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
+      AN(0) = make_double2(1.0, 0.0);
+      if (philox && valid && P.geo_len > 1 && P.nlocs) {
+        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, shot, 0u, 0u);
+        sgpos = gc.pos;
+        sgpick = gc.pick;
+        sgj = 1;
+        sfire = sgpos < P.nlocs ? 0u : 0xFFFFFFFFu;
+      }
+    } else if (valid) {
+      const u64 *q = S.q_in + idx * SU;
+      sl = q[Q_SL];
+      shot = R.shot_begin + sl;
+      s_lo = q[Q_LO]; s_hi = q[Q_HI]; sc = q[Q_C]; sobs = q[Q_OBS]; smb = q[Q_MB];
+      sgpick = q[Q_PICK]; seed = q[Q_SEED];
+      scnt = (u32)q[Q_CNTK];
+      sgj = (u32)q[Q_GEO]; sgpos = (u32)(q[Q_GEO] >> 32);
+      sfire = (u32)q[Q_FIRE];
+      const u32 *qr = reinterpret_cast<const u32 *>(q + Q_HDR);
+#pragma unroll 1
+      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = qr[w];
+      const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+      for (u32 j = 0; j < (1u << S.k0); ++j) AN(j) = qc[j];
     }
     __syncwarp();
 
-    u32 pc = 0, nm = 0;
+    u32 pc = S.pc0, nm = S.nm0;
+    u32 exit_k = 0;
 #pragma unroll 1
     for (;;) {
       if (!__any_sync(FULL, sst == ST_RUNNING)) break;
@@ -1126,50 +734,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
       const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
       const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
       const u32 instr = (u32)(h >> 32);
-
-      if (wide_only || op_is_wide(kind, k, fl)) {
-        // @region wide: handoff
-        // park every lane's state; the wide loops read shot s from the stash
-        stash[SF_LO * 32 + lane] = s_lo;
-        stash[SF_HI * 32 + lane] = s_hi;
-        stash[SF_C * 32 + lane] = sc;
-        stash[SF_OBS * 32 + lane] = sobs;
-        stash[SF_MB * 32 + lane] = smb;
-        stash[SF_PICK * 32 + lane] = sgpick;
-        stash[SF_SEED * 32 + lane] = seed;
-        stash[SF_SHOT * 32 + lane] = shot;
-        stash[SF_CNTK * 32 + lane] = (u64)scnt | ((u64)sk << 32);
-        stash[SF_ST * 32 + lane] = (u64)(sst & 0xff) | ((u64)dumped << 8) | ((u64)(u32)saux << 32);
-        stash[SF_GEO * 32 + lane] = (u64)sgj | ((u64)sgpos << 32);
-        stash[SF_FIRE * 32 + lane] = sfire;
-        u32 live = __ballot_sync(FULL, sst == ST_RUNNING);
-        __syncwarp();
-        const u32 exit_pc = wide_section<kSmemChi, kPhilox>(P, R, O, base, pc, nm, h, live, win, recb, An,
-                                                   A, stash);
-        // every lane takes its state back
-        s_lo = stash[SF_LO * 32 + lane];
-        s_hi = stash[SF_HI * 32 + lane];
-        sc = stash[SF_C * 32 + lane];
-        sobs = stash[SF_OBS * 32 + lane];
-        smb = stash[SF_MB * 32 + lane];
-        sgpick = stash[SF_PICK * 32 + lane];
-        seed = stash[SF_SEED * 32 + lane];
-        shot = stash[SF_SHOT * 32 + lane];
-        {
-          const u64 ck = stash[SF_CNTK * 32 + lane], st = stash[SF_ST * 32 + lane],
-                    g = stash[SF_GEO * 32 + lane];
-          scnt = (u32)ck; sk = (u32)(ck >> 32);
-          sst = (int)(st & 0xff); saux = (int)(u32)(st >> 32); dumped = ((st >> 8) & 1u) != 0;
-          sgj = (u32)g; sgpos = (u32)(g >> 32);
-          sfire = (u32)stash[SF_FIRE * 32 + lane];
-        }
-        __syncwarp();
-        if (exit_pc == 0xFFFFFFFFu) break;   // no shot survived the section
-        pc = exit_pc;
-        if (!philox)   // the SplitMix wide scan starts at noise instruction nm
-          while (nm < P.nnoise && (u32)__ldg(tables + P.noise_off + 4ull * nm) < pc) ++nm;
-        continue;
-      }
+      if (op_is_wide(kind, k, fl)) { exit_k = k; break; }   // section end
       // ============================== narrow op, lane per shot
       // @region narrow: noise
       // apply E to this lane's shot (ref state.py:88-102)
@@ -1483,16 +1048,38 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
     }
     __syncwarp();
 
-    // @region outputs
+    // @region narrow: outputs
+    // survivors go to the next (wide) section's queue, in lane order
+    const u32 run = __ballot_sync(FULL, valid && sst == ST_RUNNING);
+    if (run) {
+      u32 o = 0;
+      if (lane == 0) o = atomicAdd(S.n_out, (u32)__popc(run));
+      o = __shfl_sync(FULL, o, 0);
+      if ((run >> lane) & 1u) {
+        u64 *q = S.q_out + (u64)(o + __popc(run & lanemask_lt(lane))) * SU;
+        q[Q_SL] = sl; q[Q_LO] = s_lo; q[Q_HI] = s_hi; q[Q_C] = sc; q[Q_OBS] = sobs;
+        q[Q_MB] = smb; q[Q_PICK] = sgpick; q[Q_SEED] = seed;
+        q[Q_CNTK] = (u64)scnt;
+        q[Q_GEO] = (u64)sgj | ((u64)sgpos << 32);
+        q[Q_FIRE] = sfire;
+        u32 *qr = reinterpret_cast<u32 *>(q + Q_HDR);
+#pragma unroll 1
+        for (u32 w = 0; w < P.rec_words32; ++w) qr[w] = recb[w * 32u + lane];
+        double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+        for (u32 j = 0; j < (1u << exit_k); ++j) qc[j] = AN(j);
+      }
+    }
+    const bool fin = valid && sst != ST_RUNNING;
     {
-      const u32 pres = __ballot_sync(FULL, valid && sst == ST_PRESERVED);
-      const u32 errb = __ballot_sync(FULL, valid && sst == ST_PRESERVED && sobs != 0);
-      const u32 disc = __ballot_sync(FULL, valid && sst == ST_DISCARDED);
-      const u32 ovf = __ballot_sync(FULL, valid && sst == ST_OVERFLOW);
-      const u32 cor = __ballot_sync(FULL, valid && sst == ST_CORRUPT);
-      const u32 uns = __ballot_sync(FULL, valid && sst == ST_UNSUPPORTED);
-      const u32 val = __ballot_sync(FULL, valid);
-      u64 mb = valid ? smb : 0ull;
+      const u32 pres = __ballot_sync(FULL, fin && sst == ST_PRESERVED);
+      const u32 errb = __ballot_sync(FULL, fin && sst == ST_PRESERVED && sobs != 0);
+      const u32 disc = __ballot_sync(FULL, fin && sst == ST_DISCARDED);
+      const u32 ovf = __ballot_sync(FULL, fin && sst == ST_OVERFLOW);
+      const u32 cor = __ballot_sync(FULL, fin && sst == ST_CORRUPT);
+      const u32 uns = __ballot_sync(FULL, fin && sst == ST_UNSUPPORTED);
+      const u32 val = __ballot_sync(FULL, fin);
+      u64 mb = fin ? smb : 0ull;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mb += __shfl_xor_sync(FULL, mb, o);
       if (lane == 0) {
@@ -1506,7 +1093,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
         wcnt[WC_MB] += mb;
       }
     }
-    if (valid) {
+    if (fin) {
       if (sst == ST_PRESERVED && sobs) {
 #pragma unroll 1
         for (u64 o = sobs; o; o &= o - 1)
@@ -1527,7 +1114,7 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
           const u32 hi = (2 * w + 1 < P.rec_words32) ? recb[(2 * w + 1) * 32u + lane] : 0u;
           O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
         }
-        if (O.mode == MODE_DUMP && !dumped) {
+        if (O.mode == MODE_DUMP) {
           O.sig[2 * sl] = s_lo;
           O.sig[2 * sl + 1] = s_hi;
           O.cvec[sl] = sc;
@@ -1541,13 +1128,506 @@ sample_kernel(DevProg P, DevRun R, DevOut O) {
     __syncwarp();
   }
 #undef AN
+  flush_counters(O, wcnt, lane);
+}
+
+// ---------------------------------------------------------------- wide
+
+template <bool kSmemChi, bool kPhilox>
+__global__ void __launch_bounds__(128, GS_WIDE_BLOCKS)
+wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
+  extern __shared__ __align__(16) u8 smem[];
+  const u32 lane = threadIdx.x & 31u;
+  const u32 wib = threadIdx.x >> 5;
+  const u32 wpb = blockDim.x >> 5;
+  const u64 gw = (u64)blockIdx.x * wpb + wib;
+  u8 *mine = smem + (size_t)wib * O.warp_bytes;
+  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
+  u32 *win = reinterpret_cast<u32 *>(mine + kCntBytes);
+  u32 *recw = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kWinBytes)
+                            : O.grec + gw * (u64)P.rec_words32;
+  double2 *A = kSmemChi ? chi_ptr<true>(reinterpret_cast<double2 *>(mine + O.chi_off))
+                        : O.gchi + gw * ((u64)1 << P.max_dim);
+  const u32 n = P.n;
+  const u64 *__restrict__ ops = P.ops;
+  const u64 *__restrict__ tables = P.tables;
+  const u64 *__restrict__ locs = P.locs;
+  const double2 Z = make_double2(0.0, 0.0);
+  constexpr bool philox = kPhilox;
+  const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
+  const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
+  const u32 SU = slot_u64(P);
+  (void)n;
+
+  if (lane < WC_N) wcnt[lane] = 0;
   __syncwarp();
-  if (lane < WC_N && wcnt[lane]) {
-    static_assert(WC_N == 8, "counter order");
-    const int dst[WC_N] = {GS_C_TOTAL, GS_C_PRESERVED, GS_C_DISCARDED, GS_C_OVERFLOW,
-                           GS_C_CORRUPT, GS_C_UNSUPPORTED, GS_C_ERROR_SHOTS, GS_C_MODEL_BYTES};
-    atomicAdd((unsigned long long *)O.counters + dst[lane], wcnt[lane]);
+  const u64 total = S.q_in ? (u64)*S.n_in : S.count;
+
+#pragma unroll 1
+  for (;;) {
+    // @region wide: shot setup
+    u64 idx = 0;
+    if (lane == 0) idx = atomicAdd(S.work, 1ull);
+    idx = __shfl_sync(FULL, idx, 0);
+    if (idx >= total) break;
+    Rng rng;
+    rng.philox = philox;
+    rng.master = R.master;
+    u64 sl, sig_lo = 0, sig_hi = 0, c = 0, obs = 0, mbytes = 0, gpick = 0;
+    u32 cnt = 1, gj = 0, gpos = 0xFFFFFFFFu, fire_pc = 0xFFFFFFFFu;
+    const u32 k = S.k0;
+    double nrm = 0.0;
+    if (!S.q_in) {
+      sl = S.first + idx;
+      rng.shot = R.shot_begin + sl;
+      rng.seed = 0;
+      if (!philox) rng.seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, rng.shot);
+#pragma unroll 1
+      for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
+      if (lane == 0) A[0] = make_double2(1.0, 0.0);
+      nrm = 1.0;
+      if (philox && P.geo_len > 1 && P.nlocs) {
+        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, rng.shot, 0u, 0u);
+        gpos = gc.pos;
+        gpick = gc.pick;
+        gj = 1;
+        fire_pc = gpos < P.nlocs ? 0u : 0xFFFFFFFFu;
+      }
+    } else {
+      const u64 *q = S.q_in + idx * SU;
+      sl = q[Q_SL];
+      rng.shot = R.shot_begin + sl;
+      rng.seed = q[Q_SEED];
+      sig_lo = q[Q_LO]; sig_hi = q[Q_HI]; c = q[Q_C]; obs = q[Q_OBS]; mbytes = q[Q_MB];
+      gpick = q[Q_PICK];
+      cnt = (u32)q[Q_CNTK];
+      gj = (u32)q[Q_GEO]; gpos = (u32)(q[Q_GEO] >> 32);
+      fire_pc = (u32)q[Q_FIRE];
+      const u32 *qr = reinterpret_cast<const u32 *>(q + Q_HDR);
+#pragma unroll 1
+      for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = qr[w];
+      // chi in, and its norm (same per-lane order + tree as a sum pass)
+      const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+      for (u32 j = lane; j < (1u << k); j += 32) {
+        const double2 v = qc[j];
+        A[j] = v;
+        nrm = __dadd_rn(nrm, abs2(v));
+      }
+      nrm = warp_sum(nrm);
+    }
+    if (!philox) fire_pc = 0xFFFFFFFFu;
+    u32 kcur = k;
+    int status = ST_RUNNING, aux = -1;
+    double ps = 1.0;        // renormalisation pending on A (see ldps)
+    // SplitMix noise scan state: everything inserted before pc0 is applied
+    u32 cursor = P.nlocs;
+    if (S.nm0 < P.nnoise) cursor = (u32)__ldg(tables + P.noise_off + 4ull * S.nm0 + 1);
+    u32 scanned = cursor >> 5, search_w = scanned;
+    u32 next_word_pc = 0xFFFFFFFFu;
+    if (!philox && scanned < P.nwords) next_word_pc = (u32)__ldg(tables + P.wordpc_off + scanned);
+    __syncwarp();
+    u32 wpc = S.pc0;
+    u64 hnext = __ldg(ops + wpc);
+    u32 exit_pc = 0xFFFFFFFFu;
+#pragma unroll 1
+    while (status == ST_RUNNING) {
+      if (!wide_only) {
+        const u32 kind_ = (u32)(hnext & 0xff), k_ = (u32)((hnext >> 16) & 0xff),
+                  fl_ = (u32)((hnext >> 24) & 0xff);
+        if (!op_is_wide(kind_, k_, fl_)) { exit_pc = wpc; break; }
+      }
+      // @region wide: noise
+      if (wpc >= next_word_pc || wpc >= fire_pc) {
+        // apply E = OR of fired letters of one noise instruction
+        // (ref noise.py:68-100, state.py:88-102)
+        auto apply_error = [&](u64 ex, u64 ez, const u64 *nrec) {
+          if (!(ex | ez)) return;
+          const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
+                                         sig_lo, sig_hi);
+          const double2 php = ipow(e.xi);
+          sweep_phase(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
+          ps = 1.0;
+          __syncwarp();
+          c ^= e.beta;
+          mbytes += 2ull * kEntryBytes * cnt + sign_bytes;
+        };
+        if (philox) {
+          // walk the candidate schedule (lane-uniform, rare)
+          fire_pc = 0xFFFFFFFFu;
+          while (gpos < P.nlocs) {
+            const u64 *nrec = noise_owner(P, gpos);
+            const u64 nw0 = __ldg(nrec);
+            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+            if (ipc > wpc) { fire_pc = ipc; break; }
+            const u32 loc0 = (u32)__ldg(nrec + 1);
+            u64 ex = 0, ez = 0;
+            while (gpos < loc0 + nloc) {
+              const u32 l = gpos;
+              bool ok = true;
+              if (!P.noise_uniform) ok = geo_accept(R.master, rng.shot, gj - 1, __ldg(tables + P.acc_off + l));
+              if (ok) {
+                const u64 lw = __ldg(locs + 2ull * l);
+                noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
+                             (double)gpick * 0x1.0p-53, ex, ez);
+              }
+              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, rng.shot, gj, l + 1);
+              gpos = gc.pos;
+              gpick = gc.pick;
+              ++gj;
+            }
+            apply_error(ex, ez, nrec);
+          }
+        } else {
+          // SplitMix: one fire draw per location, 32 locations per ballot
+          while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= wpc) {
+            const u32 l = scanned * 32u + lane;
+            bool fire = false;
+            if (l < P.nlocs) {
+              const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+              fire = rng.m53((u32)lw) < thr;
+            }
+            const u32 bits = __ballot_sync(FULL, fire);
+            if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+            ++scanned;
+          }
+          __syncwarp();
+          next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
+          fire_pc = 0xFFFFFFFFu;
+#pragma unroll 1
+          for (;;) {
+            // next fired location >= cursor among the scanned words
+            u32 fl_loc = 0xFFFFFFFFu;
+            u32 w = max(search_w, cursor >> 5);
+#pragma unroll 1
+            for (; w < scanned; ++w) {
+              u32 bits = win[w & (kWinWords - 1)];
+              if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
+              if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+            }
+            search_w = w;
+            if (fl_loc == 0xFFFFFFFFu) break;
+            const u64 *nrec = noise_owner(P, fl_loc);
+            const u64 nw0 = __ldg(nrec);
+            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+            if (ipc > wpc) { fire_pc = ipc; break; }
+            const u32 loc0 = (u32)__ldg(nrec + 1);
+            cursor = loc0 + nloc;
+            u64 ex = 0, ez = 0;
+#pragma unroll 1
+            for (u32 i = lane; i < nloc; i += 32) {
+              const u32 l = loc0 + i;
+              if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+              const u64 lw = __ldg(locs + 2ull * l);
+              const u32 nk = (u32)(lw >> 48) & 3;
+              const double u = nk <= NK_DEP2 ? rng.uniform((u32)lw + 1) : 0.0;
+              noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+            }
+            apply_error(warp_or64(ex), warp_or64(ez), nrec);
+          }
+        }
+      }
+
+      // @region wide: dispatch
+      const u64 *op = ops + wpc;
+      const u64 hw = hnext;
+      const u32 wkind = (u32)(hw & 0xff), wlen = (u32)((hw >> 8) & 0xff);
+      const u32 wk = (u32)((hw >> 16) & 0xff), wfl = (u32)((hw >> 24) & 0xff);
+      const u32 winstr = (u32)(hw >> 32);
+      wpc += wlen;
+      hnext = __ldg(ops + wpc);       // prefetch the next header
+      kcur = wk;
+      const u32 size = 1u << wk;
+
+      // @region wide: T
+      if (wkind == OP_T || wkind == OP_GROW_LIMIT) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
+        // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
+        const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6);
+        const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
+        const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
+        const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
+        mbytes += __ldg(op + 11);
+        const double2 bx0 = flip ? cneg(bxs) : bxs;
+        const u32 dc = par64(delta & c);
+        const u32 tcase = wfl & 3u;
+        if (tcase == T_DIAG) {
+          // beta == 0: pure phase per entry (ref state.py:120-126); the
+          // factors have modulus 1, the norm is kept
+          sweep_phase(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
+          ps = 1.0;
+          __syncwarp();
+          mbytes += 32ull * cnt;
+          continue;
+        }
+        const u32 cin = cnt;
+        if (wkind == OP_GROW_LIMIT) {
+          u32 nz = 0;
+          const double2 bx1 = cneg(bx0);
+#pragma unroll 1
+          for (u32 j = lane; j < size; j += 32) {
+            const double2 v = ldps(A, j, ps);
+            const u32 s_ = dc ^ par32(j & dmask);
+            nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
+            nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
+          }
+          nz = warp_sum_u32(nz);
+          status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
+          aux = (int)winstr;
+          break;
+        }
+        // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
+        if (ps != 1.0) sweep_scale(A, size, ps);   // rare: right after a deferral
+        ps = 1.0;
+        SumNz r;
+        if (tcase == T_BUTTERFLY) {
+          r = sweep_butterfly<kSmemChi>(A, size >> 1, cb, dc, dmask, a, bx0);
+        } else {
+          r = sweep_grow<kSmemChi>(A, size, dc, dmask, a, bx0);
+          kcur = wk + 1;
+        }
+        __syncwarp();
+        cnt = warp_sum_u32(r.nz);
+        nrm = warp_sum(r.sum);
+        mbytes += (u64)kEntryBytes * (cin + cnt);
+        if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
+        if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+        continue;
+      }
+
+      // @region wide: meas
+      if (wkind == OP_MEAS) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        const u32 mcase = wfl & 3u;
+        const u32 xi0 = (((wfl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
+        const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
+        const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
+        const u64 vec = __ldg(op + 8);
+        const u64 w13 = __ldg(op + 13);
+        const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
+        mbytes += __ldg(op + 17);
+        const u32 dc = par64(delta & c);
+        // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
+        // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
+        auto pick_plus = [&](double pplus) -> bool {
+          if (pplus >= 1.0) return true;
+          if (pplus <= 0.0) return false;
+          return rng.uniform(udraw) < pplus;
+        };
+        // a renormalisation by rs that needs no data movement: deferred to
+        // the next pass over chi (ldps); nonzero count unchanged
+        auto defer_scale = [&](double rs) {
+          if (ps != 1.0) sweep_scale(A, size, ps);
+          ps = rs;
+          nrm = __dmul_rn(__dmul_rn(nrm, rs), rs);
+        };
+        const u32 cin = cnt;
+        bool plus;
+        if (mcase == M_DET) {
+          // beta == 0: filter by eigenvalue (ref state.py:162-176)
+          const u32 neg0 = (xi0 >> 1) ^ dc;
+          double sp, sm;
+          if (dmask == 0) {
+            // every coordinate has eigenvalue (-1)^neg0: P+ is the norm
+            sp = neg0 ? 0.0 : nrm;
+            sm = neg0 ? nrm : 0.0;
+          } else {
+            const double2 part = sweep_det_sums(A, size, dmask, neg0, ps);
+            sp = warp_sum(part.x);
+            sm = warp_sum(part.y);
+          }
+          plus = pick_plus(sp);
+          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          const u32 want_neg = plus ? 0u : 1u;
+          const double rs = inv_sqrt_norm(plus ? sp : sm);
+          if (wfl & MF_COMPACT) {
+            const u32 tau = want_neg ^ neg0;
+            const SumNz r = sweep_compact(A, size >> 1, isq, dmask, tau, rs, ps);
+            ps = 1.0;
+            __syncwarp();
+            cnt = warp_sum_u32(r.nz);
+            nrm = warp_sum(r.sum);
+            if (tau) c ^= vec;
+            kcur = wk - 1;
+          } else if ((plus ? sm : sp) == 0.0) {
+            // the other eigenspace is empty: the filter is a pure
+            // renormalisation
+            defer_scale(rs);
+          } else {
+            const SumNz r = sweep_filter(A, size, dmask, neg0, want_neg, rs, ps);
+            ps = 1.0;
+            __syncwarp();
+            cnt = warp_sum_u32(r.nz);
+            nrm = warp_sum(r.sum);
+          }
+        } else {
+          // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
+          PivotGeo g;
+          g.span = mcase == M_PIVOT_SPAN;
+          g.npairs = g.span ? (size >> 1) : size;
+          g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
+          g.dc = dc; g.dmask = dmask;
+          const double2 xpp = ipow(xi0);   // i^xi0, exact
+          const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p(A, g, xpp, ps)));
+          plus = pick_plus(pp);
+          const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          const SumNz w = sweep_pivot_w(A, g, xpp, plus, ps);
+          ps = 1.0;
+          __syncwarp();
+          const double sk = warp_sum(w.sum);
+          cnt = warp_sum_u32(w.nz);
+          if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          const double rs = inv_sqrt_norm(sk);
+          if (g.span) {
+            const SumNz r = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+            __syncwarp();
+            cnt = warp_sum_u32(r.nz);
+            nrm = warp_sum(r.sum);
+            kcur = wk - 1;
+          } else {
+            nrm = sk;
+            defer_scale(rs);
+          }
+          if (g.ct) c ^= vec;
+          // tableau sign update of the pivot (ref tableau.py:176-200)
+          const u32 v = (u32)(sig_hi >> t) & 1u;
+          if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
+          sig_lo ^= __ldg(op + 11);
+          sig_hi ^= __ldg(op + 12);
+          sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
+          sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
+        }
+        mbytes += (u64)kEntryBytes * (cin + cnt);
+        const u32 bout = plus ? 0u : 1u;
+        u32 rb = bout;
+        if ((wfl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
+        if (wfl & MF_RECORD) {
+          if (lane == 0 && rb) recw[slot >> 5] |= 1u << (slot & 31);
+          __syncwarp();
+        }
+        if ((wfl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
+        continue;
+      }
+
+      // @region wide: feedback/detector/end
+      if (wkind == OP_FEEDBACK) {
+        const u32 idx = (u32)__ldg(op + 1);
+        if ((recw[idx >> 5] >> (idx & 31)) & 1u) {
+          sig_lo ^= __ldg(op + 2);
+          sig_hi ^= __ldg(op + 3);
+          mbytes += __ldg(op + 4);
+        }
+        continue;
+      }
+      if (wkind == OP_DETECTOR || wkind == OP_OBSERVABLE) {
+        const u64 w1 = __ldg(op + 1);
+        const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
+        const u64 off = __ldg(op + 2);
+        u32 bb = 0;
+#pragma unroll 1
+        for (u32 i = lane; i < nidx; i += 32) {
+          const u32 idx = (u32)__ldg(tables + off + i);
+          bb ^= (recw[idx >> 5] >> (idx & 31)) & 1u;
+        }
+        const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
+        if (wkind == OP_DETECTOR) {
+          if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
+        } else {
+          obs ^= (u64)parity << id;
+        }
+        continue;
+      }
+      if (wkind == OP_END) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        mbytes += __ldg(op + 3);
+        status = ST_PRESERVED;
+        break;
+      }
+      status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
+      aux = -2;
+    }
+    // @region wide: outputs
+    __syncwarp();
+    if (status == ST_RUNNING) {
+      // survivor: hand it to the next (narrow) section's queue
+      u32 o = 0;
+      if (lane == 0) o = atomicAdd(S.n_out, 1u);
+      o = __shfl_sync(FULL, o, 0);
+      u64 *q = S.q_out + (u64)o * SU;
+      if (lane == 0) {
+        q[Q_SL] = sl; q[Q_LO] = sig_lo; q[Q_HI] = sig_hi; q[Q_C] = c; q[Q_OBS] = obs;
+        q[Q_MB] = mbytes; q[Q_PICK] = gpick; q[Q_SEED] = rng.seed;
+        q[Q_CNTK] = (u64)cnt;
+        q[Q_GEO] = (u64)gj | ((u64)gpos << 32);
+        q[Q_FIRE] = fire_pc;
+      }
+      u32 *qr = reinterpret_cast<u32 *>(q + Q_HDR);
+#pragma unroll 1
+      for (u32 w = lane; w < P.rec_words32; w += 32) qr[w] = recw[w];
+      double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+      for (u32 j = lane; j < (1u << kcur); j += 32) qc[j] = ldps(A, j, ps);
+      (void)exit_pc;
+    } else {
+      if (lane == 0) {
+        wcnt[WC_TOT] += 1;
+        wcnt[WC_MB] += mbytes;
+        if (status == ST_PRESERVED) {
+          wcnt[WC_PRES] += 1;
+          if (obs) {
+            wcnt[WC_ERR] += 1;
+#pragma unroll 1
+            for (u64 o = obs; o; o &= o - 1)
+              atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
+            if (O.witness) {
+              const u32 wi = atomicAdd(O.witness_count, 1u);
+              if (wi < O.witness_cap) O.witness[wi] = rng.shot;
+            }
+          }
+        } else if (status == ST_DISCARDED) wcnt[WC_DISC] += 1;
+        else if (status == ST_OVERFLOW) wcnt[WC_OVF] += 1;
+        else if (status == ST_CORRUPT) wcnt[WC_COR] += 1;
+        else wcnt[WC_UNS] += 1;
+      }
+      if (O.mode != MODE_COUNTERS) {
+        if (lane == 0) {
+          O.status[sl] = (u8)status;
+          O.aux[sl] = aux;
+          O.obs[sl] = obs;
+        }
+        const u32 rw64 = (P.nmeas + 63) / 64;
+#pragma unroll 1
+        for (u32 w = lane; w < rw64; w += 32) {
+          const u32 lo = recw[2 * w];
+          const u32 hi = (2 * w + 1 < P.rec_words32) ? recw[2 * w + 1] : 0u;
+          O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
+        }
+        if (O.mode == MODE_DUMP) {
+          if (lane == 0) {
+            O.sig[2 * sl] = sig_lo;
+            O.sig[2 * sl + 1] = sig_hi;
+            O.cvec[sl] = c;
+            O.dim[sl] = kcur;
+          }
+          const u64 stride = 1ull << P.max_dim;
+#pragma unroll 1
+          for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = ldps(A, j, ps);
+        }
+      }
+    }
+    __syncwarp();
   }
+  flush_counters(O, wcnt, lane);
 }
 
 // @region plugin kernels + host
@@ -1638,15 +1718,14 @@ struct gs_engine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   long long *d_counters = nullptr;
   size_t counters_cap = 0;
-  u64 *d_next = nullptr;
   double2 *d_chi = nullptr;
   size_t chi_bytes = 0;
   u32 *d_rec = nullptr;
   size_t rec_bytes = 0;
-  u64 *d_stash = nullptr;
-  size_t stash_bytes = 0;
-  double2 *d_gan = nullptr;
-  size_t gan_bytes = 0;
+  u64 *d_queue[2] = {nullptr, nullptr};
+  size_t queue_bytes[2] = {0, 0};
+  unsigned long long *d_work = nullptr;
+  size_t work_bytes = 0;
   u64 launches = 0;
   double last_ms = 0.0;
 };
@@ -1664,13 +1743,6 @@ static int fail(int code, const std::string &msg) {
     if (e_ != cudaSuccess)                                                     \
       return fail(GS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
-
-// the four sampling kernels: chi placement x RNG mode
-template <typename F>
-static cudaError_t with_sample_kernel(bool smem_chi, bool philox, F f) {
-  if (smem_chi) return philox ? f(gs::sample_kernel<true, true>) : f(gs::sample_kernel<true, false>);
-  return philox ? f(gs::sample_kernel<false, true>) : f(gs::sample_kernel<false, false>);
-}
 
 extern "C" {
 
@@ -1742,7 +1814,6 @@ int gs_engine_create(int device, gs_engine **out) {
   CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreate(&e->ev0));
   CUDA_TRY(cudaEventCreate(&e->ev1));
-  CUDA_TRY(cudaMalloc(&e->d_next, sizeof(u64)));
   *out = e;
   return GS_OK;
 }
@@ -1751,11 +1822,11 @@ int gs_engine_destroy(gs_engine *e) {
   if (!e) return GS_OK;
   cudaSetDevice(e->device);
   cudaFree(e->d_counters);
-  cudaFree(e->d_next);
   cudaFree(e->d_chi);
   cudaFree(e->d_rec);
-  cudaFree(e->d_stash);
-  cudaFree(e->d_gan);
+  cudaFree(e->d_queue[0]);
+  cudaFree(e->d_queue[1]);
+  cudaFree(e->d_work);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->stream) cudaStreamDestroy(e->stream);
@@ -1779,113 +1850,87 @@ static int upload(gs_engine *e, gs_program *p) {
   return GS_OK;
 }
 
-struct LaunchCfg {
-  bool smem_chi;
-  u32 wpb, blocks, warp_bytes, chi_off, rec_in_smem, rec_words32;
-  size_t smem;
+// static section split of the op stream (see the kernels' header comment)
+struct Section {
+  u32 pc0, k0, nm0;
+  bool wide;
 };
 
-static int plan(gs_engine *e, gs_program *p, const gs_run_params *r, LaunchCfg &L) {
-  const bool philox = (r->flags & GS_RNG_PHILOX) != 0;
-  const u32 K = p->info.max_dim;
-  const size_t chi = (size_t)16 << K;
-  L.rec_words32 = ((p->info.num_measurements + 63) / 64) * 2;
-  if (L.rec_words32 == 0) L.rec_words32 = 2;
-  // record bits of the warp's 32 shots (one column per lane)
-  const size_t rec_b = (size_t)L.rec_words32 * 4 * 32;
-  L.rec_in_smem = rec_b <= 4096;
-  // chi of wide sections in shared memory when it fits (it then shares the
-  // warp's buffer with the narrow lane-per-shot chi An); else a per-warp
-  // global buffer (L1/L2-cached) for large max_dim
-  if (r->flags & GS_CHI_GLOBAL) L.smem_chi = false;
-  else if (r->flags & GS_CHI_SMEM) L.smem_chi = chi <= 64 * 1024;
-  else L.smem_chi = chi <= 32 * 1024;
-  const size_t buf = L.smem_chi ? std::max((size_t)gs::kNarrowBytes, chi) : (size_t)gs::kNarrowBytes;
-  const size_t base = gs::kWinBytes + gs::kCntBytes + buf;
-  L.chi_off = (u32)base;   // record columns follow the chi buffer
-  L.warp_bytes = (u32)(((L.rec_in_smem ? base + rec_b : base) + 15) & ~(size_t)15);
-  // warps per block: the most resident warps per SM (shared memory bound)
+static void sections_of(const gs_program *p, bool wide_only, std::vector<Section> &out) {
+  out.clear();
+  const std::vector<u64> &ops = p->ops;
+  size_t pc = 0, nm = 0;
+  const u32 nn = p->info.num_noise;
+  while (pc < ops.size()) {
+    const u64 h = ops[pc];
+    const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
+    const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
+    const bool wide = wide_only || gs::op_is_wide(kind, k, fl);
+    if (out.empty() || out.back().wide != wide) {
+      while (nm < nn && (u32)p->tables[p->info.noise_off + 4 * nm] < (u32)pc) ++nm;
+      out.push_back(Section{(u32)pc, k, (u32)nm, wide});
+    }
+    if (kind == gs::OP_END || len == 0) break;
+    pc += len;
+  }
+}
+
+extern "C++" {
+// the sampling kernels: RNG mode (x chi placement for the wide kernel)
+template <typename F>
+static cudaError_t with_narrow_kernel(bool philox, F f) {
+  return philox ? f(gs::narrow_kernel<true>) : f(gs::narrow_kernel<false>);
+}
+template <typename F>
+static cudaError_t with_wide_kernel(bool smem_chi, bool philox, F f) {
+  if (smem_chi) return philox ? f(gs::wide_kernel<true, true>) : f(gs::wide_kernel<true, false>);
+  return philox ? f(gs::wide_kernel<false, true>) : f(gs::wide_kernel<false, false>);
+}
+
+struct KernelCfg {
+  u32 wpb = 1, blocks = 1, warp_bytes = 0, chi_off = 0, rec_in_smem = 0;
+  size_t smem = 0;
+};
+
+// warps per block = the most resident warps per SM; grid = SMs x blocks/SM
+template <typename W>
+static int occupancy(gs_engine *e, u32 warp_bytes, u32 want_wpb, W with, KernelCfg &K) {
   u32 wpb = 1;
-  if (r->warps_per_block) {
-    wpb = r->warps_per_block > 4 ? 4 : r->warps_per_block;   // __launch_bounds__(128)
-  } else {
-    int best = -1;
-    for (u32 w = 4; w >= 1; --w) {
-      if ((size_t)w * L.warp_bytes > e->smem_optin) continue;
-      int per = 0;
-      const size_t sm = w * L.warp_bytes;
-      CUDA_TRY(with_sample_kernel(L.smem_chi, philox, [&](auto kern) {
-        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        return err != cudaSuccess ? err : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, w * 32, sm);
-      }));
-      if (per * (int)w > best) { best = per * (int)w; wpb = w; }
-    }
+  int best = -1;
+  for (u32 w = 4; w >= 1; --w) {
+    if (want_wpb && w != want_wpb) continue;
+    if ((size_t)w * warp_bytes > e->smem_optin) continue;
+    int per = 0;
+    const size_t sm = (size_t)w * warp_bytes;
+    CUDA_TRY(with([&](auto kern) {
+      cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      return err != cudaSuccess ? err : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, w * 32, sm);
+    }));
+    if (per * (int)w > best) { best = per * (int)w; wpb = w; }
   }
-  while (wpb > 1 && (size_t)wpb * L.warp_bytes > e->smem_optin) --wpb;
-  if ((size_t)wpb * L.warp_bytes > e->smem_optin)
-    return fail(GS_ERR_UNSUPPORTED, "per-warp state exceeds shared memory");
-  L.wpb = wpb;
-  L.smem = (size_t)wpb * L.warp_bytes;
-  int per_sm = 0;
-  CUDA_TRY(with_sample_kernel(L.smem_chi, philox, [&](auto kern) {
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-    return err != cudaSuccess ? err
-                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, L.smem);
+  if (best < 1) return fail(GS_ERR_UNSUPPORTED, "per-warp state exceeds shared memory");
+  K.wpb = wpb;
+  K.warp_bytes = warp_bytes;
+  K.smem = (size_t)wpb * warp_bytes;
+  CUDA_TRY(with([&](auto kern) {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K.smem);
   }));
-  if (per_sm < 1) return fail(GS_ERR_UNSUPPORTED, "kernel does not fit on an SM");
-  u64 blocks = r->blocks ? r->blocks : (u64)e->num_sms * per_sm;
-  // each warp takes batches of 32 shots
-  const u64 need = (r->shot_count + 32ull * wpb - 1) / (32ull * wpb);
-  if (blocks > need) blocks = need ? need : 1;
-  // bound the global chi scratch (large-k programs run fewer resident shots)
-  if (!L.smem_chi) {
-    const u64 max_warps = ((u64)8 << 30) / chi;
-    if (blocks * wpb > max_warps) blocks = max_warps / wpb ? max_warps / wpb : 1;
-  }
-  L.blocks = (u32)blocks;
-  const u64 warps = (u64)L.blocks * wpb;
-  if (!L.smem_chi) {
-    const size_t want = (size_t)warps * chi;
-    if (want > e->chi_bytes) {
-      cudaFree(e->d_chi);
-      e->d_chi = nullptr;
-      e->chi_bytes = 0;
-      CUDA_TRY(cudaMalloc(&e->d_chi, want));
-      e->chi_bytes = want;
-    }
-  }
-  if (L.smem_chi) {
-    const size_t want = (size_t)warps * (32u << GS_KN) * 16;
-    if (want > e->gan_bytes) {
-      cudaFree(e->d_gan);
-      e->d_gan = nullptr;
-      e->gan_bytes = 0;
-      CUDA_TRY(cudaMalloc(&e->d_gan, want));
-      e->gan_bytes = want;
-    }
-  }
-  {
-    const size_t want = (size_t)warps * gs::SF_N * 32 * 8;
-    if (want > e->stash_bytes) {
-      cudaFree(e->d_stash);
-      e->d_stash = nullptr;
-      e->stash_bytes = 0;
-      CUDA_TRY(cudaMalloc(&e->d_stash, want));
-      e->stash_bytes = want;
-    }
-  }
-  if (!L.rec_in_smem) {
-    const size_t want = (size_t)warps * rec_b;
-    if (want > e->rec_bytes) {
-      cudaFree(e->d_rec);
-      e->d_rec = nullptr;
-      e->rec_bytes = 0;
-      CUDA_TRY(cudaMalloc(&e->d_rec, want));
-      e->rec_bytes = want;
-    }
-  }
+  K.blocks = (u32)(e->num_sms * (best / (int)wpb));
   return GS_OK;
 }
+
+template <typename T>
+static int ensure_buf(T **d, size_t *cap, size_t want) {
+  if (want <= *cap) return GS_OK;
+  cudaFree(*d);
+  *d = nullptr;
+  *cap = 0;
+  CUDA_TRY(cudaMalloc(d, want));
+  *cap = want;
+  return GS_OK;
+}
+
+}  // extern "C++"
 
 static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOut O,
                   cudaStream_t st, bool timed) {
@@ -1896,9 +1941,8 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   CUDA_TRY(cudaSetDevice(e->device));
   int rc = upload(e, p);
   if (rc) return rc;
-  LaunchCfg L;
-  rc = plan(e, p, r, L);
-  if (rc) return rc;
+  const bool philox = (r->flags & GS_RNG_PHILOX) != 0;
+  const bool wide_only = (r->flags & GS_WIDE_ONLY) != 0;
   gs::DevProg P;
   P.ops = p->d_ops;
   P.tables = p->d_tables;
@@ -1907,7 +1951,8 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   P.nmeas = p->info.num_measurements;
   P.max_dim = p->info.max_dim;
   P.nobs = p->info.num_obs;
-  P.rec_words32 = L.rec_words32;
+  P.rec_words32 = ((p->info.num_measurements + 63) / 64) * 2;
+  if (P.rec_words32 == 0) P.rec_words32 = 2;
   P.nlocs = p->info.num_locations;
   P.nnoise = p->info.num_noise;
   P.nwords = p->info.num_words;
@@ -1924,30 +1969,117 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   R.cap = r->capacity;
   R.flags = r->flags;
   R.seeds = nullptr;
+
+  std::vector<Section> secs;
+  sections_of(p, wide_only, secs);
+  bool any_narrow = false, any_wide = false;
+  for (const Section &s : secs) (s.wide ? any_wide : any_narrow) = true;
+
+  // launch shapes: narrow warps hold 32 shots' chi rows and record columns,
+  // wide warps one shot's chi (shared memory when 2^max_dim entries fit)
+  const size_t chi = (size_t)16 << P.max_dim;
+  bool smem_chi;
+  if (r->flags & GS_CHI_GLOBAL) smem_chi = false;
+  else if (r->flags & GS_CHI_SMEM) smem_chi = chi <= 64 * 1024;
+  else smem_chi = chi <= 32 * 1024;
+  const size_t nrec_b = (size_t)P.rec_words32 * 4 * 32, wrec_b = (size_t)P.rec_words32 * 4;
+  KernelCfg KN, KW;
+  KN.rec_in_smem = nrec_b <= 4096;
+  KW.rec_in_smem = wrec_b <= 4096;
+  if (any_narrow) {
+    const u32 wb = (u32)((gs::kCntBytes + gs::kNarrowBytes + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
+    rc = occupancy(e, wb, r->warps_per_block,
+                   [&](auto f) { return with_narrow_kernel(philox, f); }, KN);
+    if (rc) return rc;
+  }
+  if (any_wide) {
+    size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_in_smem ? ((wrec_b + 15) & ~(size_t)15) : 0);
+    KW.chi_off = (u32)base;
+    const u32 wb = (u32)(base + (smem_chi ? chi : 0));
+    rc = occupancy(e, wb, r->warps_per_block,
+                   [&](auto f) { return with_wide_kernel(smem_chi, philox, f); }, KW);
+    if (rc) return rc;
+    if (!smem_chi) {   // bound the global chi scratch
+      const u64 max_warps = ((u64)8 << 30) / chi;
+      if ((u64)KW.blocks * KW.wpb > max_warps) KW.blocks = (u32)std::max<u64>(1, max_warps / KW.wpb);
+    }
+  }
+  if (r->blocks) { KN.blocks = r->blocks; KW.blocks = r->blocks; }
+  const u64 nwarps = std::max((u64)KN.blocks * KN.wpb, (u64)KW.blocks * KW.wpb);
+  if (!smem_chi && any_wide) {
+    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * KW.wpb * chi);
+    if (rc) return rc;
+  }
+  if (!KN.rec_in_smem || !KW.rec_in_smem) {
+    rc = ensure_buf(&e->d_rec, &e->rec_bytes, (size_t)nwarps * nrec_b);
+    if (rc) return rc;
+  }
+  // queues between sections: fixed slots, chunks of at most `chunk` shots
+  const u64 slot_b = 8ull * (gs::Q_HDR + gs::rec_u64(P.rec_words32) + 2 * (1u << GS_KN));
+  u64 chunk = r->shot_count ? r->shot_count : 1;
+  const u64 qbudget = (u64)2 << 30;   // bytes per queue
+  if (secs.size() > 1 && chunk * slot_b > qbudget) chunk = std::max<u64>(32, qbudget / slot_b);
+  if (r->chunk_shots && r->chunk_shots < chunk) chunk = r->chunk_shots;   // tests
+  if (secs.size() > 1) {
+    rc = ensure_buf(&e->d_queue[0], &e->queue_bytes[0], (size_t)(chunk * slot_b));
+    if (rc) return rc;
+    rc = ensure_buf(&e->d_queue[1], &e->queue_bytes[1], (size_t)(chunk * slot_b));
+    if (rc) return rc;
+  }
+  rc = ensure_buf(&e->d_work, &e->work_bytes, sizeof(unsigned long long) * (secs.size() + 2));
+  if (rc) return rc;
+  u32 *d_qn = reinterpret_cast<u32 *>(e->d_work + secs.size());   // two u32 queue lengths
+
   u64 *d_seeds = nullptr;
   if (r->seeds && r->shot_count) {
     CUDA_TRY(cudaMallocAsync(&d_seeds, r->shot_count * 8, st));
     CUDA_TRY(cudaMemcpyAsync(d_seeds, r->seeds, r->shot_count * 8, cudaMemcpyHostToDevice, st));
     R.seeds = d_seeds;
   }
-  O.next_shot = e->d_next;
   O.gchi = e->d_chi;
   O.grec = e->d_rec;
-  O.warp_bytes = L.warp_bytes;
-  O.rec_in_smem = L.rec_in_smem;
-  O.chi_off = L.chi_off;
-  O.gstash = e->d_stash;
-  O.gan = e->d_gan;
-  CUDA_TRY(cudaMemsetAsync(e->d_next, 0, sizeof(u64), st));
   if (r->shot_count) {
     if (timed) CUDA_TRY(cudaEventRecord(e->ev0, st));
-    CUDA_TRY(with_sample_kernel(L.smem_chi, (r->flags & GS_RNG_PHILOX) != 0, [&](auto kern) {
-      kern<<<L.blocks, L.wpb * 32, L.smem, st>>>(P, R, O);
-      return cudaGetLastError();
-    }));
-    CUDA_TRY(cudaGetLastError());
+    for (u64 first = 0; first < r->shot_count; first += chunk) {
+      const u64 count = std::min(chunk, r->shot_count - first);
+      CUDA_TRY(cudaMemsetAsync(e->d_work, 0, sizeof(unsigned long long) * (secs.size() + 2), st));
+      for (size_t i = 0; i < secs.size(); ++i) {
+        gs::DevSec S;
+        S.pc0 = secs[i].pc0;
+        S.k0 = secs[i].k0;
+        S.nm0 = secs[i].nm0;
+        S.first = first;
+        S.count = count;
+        S.q_in = i ? e->d_queue[(i - 1) & 1] : nullptr;
+        S.n_in = i ? d_qn + ((i - 1) & 1) : nullptr;
+        S.q_out = i + 1 < secs.size() ? e->d_queue[i & 1] : nullptr;
+        S.n_out = d_qn + (i & 1);
+        S.work = e->d_work + i;
+        if (i >= 1 && i + 1 < secs.size())   // the queue written here was read by section i-1
+          CUDA_TRY(cudaMemsetAsync(d_qn + (i & 1), 0, sizeof(u32), st));
+        if (secs[i].wide) {
+          gs::DevOut Ow = O;
+          Ow.warp_bytes = KW.warp_bytes;
+          Ow.rec_in_smem = KW.rec_in_smem;
+          Ow.chi_off = KW.chi_off;
+          CUDA_TRY(with_wide_kernel(smem_chi, philox, [&](auto kern) {
+            kern<<<KW.blocks, KW.wpb * 32, KW.smem, st>>>(P, R, Ow, S);
+            return cudaGetLastError();
+          }));
+        } else {
+          gs::DevOut On = O;
+          On.warp_bytes = KN.warp_bytes;
+          On.rec_in_smem = KN.rec_in_smem;
+          On.chi_off = 0;
+          CUDA_TRY(with_narrow_kernel(philox, [&](auto kern) {
+            kern<<<KN.blocks, KN.wpb * 32, KN.smem, st>>>(P, R, On, S);
+            return cudaGetLastError();
+          }));
+        }
+        e->launches += 1;
+      }
+    }
     if (timed) CUDA_TRY(cudaEventRecord(e->ev1, st));
-    e->launches += 1;
   }
   if (d_seeds) CUDA_TRY(cudaFreeAsync(d_seeds, st));
   return GS_OK;

@@ -81,7 +81,7 @@ class Engine:
 
     @staticmethod
     def params(master_seed=0, shot_begin=0, shot_count=0, capacity=4096,
-               flags=0, warps_per_block=0, blocks=0, seeds=None):
+               flags=0, warps_per_block=0, blocks=0, seeds=None, chunk_shots=0):
         p = _lib.GsRunParams()
         p.master_seed = master_seed & 0xFFFFFFFFFFFFFFFF
         p.shot_begin = shot_begin
@@ -90,6 +90,7 @@ class Engine:
         p.flags = flags
         p.warps_per_block = warps_per_block
         p.blocks = blocks
+        p.chunk_shots = chunk_shots
         p._seeds_keep = None
         if seeds is not None:
             s = np.ascontiguousarray(seeds, dtype=np.uint64)

@@ -296,3 +296,25 @@ def test_lane_per_shot_matches_warp_per_shot(rng):
         cb = eng.run_counters(p, Engine.params(5 + i, 0, shots, 4096,
                                                flags | _lib.GS_WIDE_ONLY))
         assert np.array_equal(ca, cb), i
+
+
+@pytest.mark.parametrize("rng", ["splitmix", "philox"])
+def test_section_chunking_invariance(rng):
+    """Shots pass through the narrow/wide section queues in chunks; records
+    and counters do not depend on the chunk size (incl. ragged last
+    chunks) or on the launch shape."""
+    from paper_2512_23037_b200.msc import msc_grown_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(msc_grown_circuit(5), 3e-3)
+    p = Program(compile_program(prog))
+    eng = get_engine(0)
+    flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if rng == "philox" else 0)
+    ref = eng.run_records(p, Engine.params(9, 100, 5000, 4096, flags))
+    for kw in ({"chunk_shots": 1000}, {"chunk_shots": 333}, {"chunk_shots": 64, "blocks": 7},
+               {"warps_per_block": 1}):
+        got = eng.run_records(p, Engine.params(9, 100, 5000, 4096, flags, **kw))
+        for x, y in zip(ref, got):
+            assert np.array_equal(x, y), kw
+    c0 = eng.run_counters(p, Engine.params(9, 100, 5000, 4096, flags))
+    c1 = eng.run_counters(p, Engine.params(9, 100, 5000, 4096, flags, chunk_shots=777))
+    assert np.array_equal(c0, c1)
