@@ -21,7 +21,7 @@ done
 if [[ " $* " != *" --no-ncu "* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_bench_${TAG}.json 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sample_kernel -s 3 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"(narrow|wide)_kernel" -s 12 -c 4 \
     -o gpurun_out/prof_${TAG} python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_${TAG}.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_full_${TAG}.log
 fi
