@@ -56,6 +56,7 @@ OP_GROW_LIMIT = 7
 
 # T cases
 T_DIAG, T_BUTTERFLY, T_GROW = 0, 1, 2
+TF_FUSE = 1 << 4     # T flag: apply together with the next (BUTTERFLY) op
 # measurement cases
 M_DET, M_PIVOT_SPAN, M_PIVOT_NOSPAN = 0, 1, 2
 # measurement flags (bits of the header flag byte, above the 2-bit case and
@@ -634,6 +635,7 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
     pre_lo, pre_hi, cnt = flush_words()
     em.op(OP_END, len(span.vecs), 0, 0xFFFFFFFF,
           [pre_lo, pre_hi, cnt * sign_bytes])
+    _mark_fused_t_pairs(em.ops, {r[0] for r in noise_ops})
     # noise instruction table (4 words each) and, per 32-location word of the
     # fire bitset, the insertion pc of the instruction owning its first
     # location (the device scans a word only once execution reaches it)
@@ -672,6 +674,32 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         noise_off=noise_off, num_noise=len(noise_ops), wordpc_off=wordpc_off,
         num_words=(nloc_total + 31) // 32, geo_off=geo_off, geo_len=len(geo),
         noise_uniform=noise_uniform, acc_off=acc_off, p_max=p_max)
+
+
+def _mark_fused_t_pairs(ops, noise_pcs):
+    """Set TF_FUSE on a T BUTTERFLY op whose successor is a T BUTTERFLY of
+    the same dimension with a different partner vector and no noise inserted
+    between them: the device applies both gates in one pass over 4-element
+    groups (same arithmetic and pruning order as two passes).  Pairs are
+    taken greedily left to right."""
+    pc = 0
+    prev = None
+    while True:
+        kind, ln, k, fl, _ = decode_header(ops[pc])
+        if kind == OP_END:
+            break
+        if (prev is not None and kind == OP_T and (fl & 3) == T_BUTTERFLY
+                and pc not in noise_pcs):
+            ppc, pk, pcb = prev
+            cb = ops[pc + 6] & 0xFFFFFFFF
+            if pk == k and pcb != cb and k >= 2:
+                ops[ppc] |= TF_FUSE << 24
+                prev = None
+                pc += ln
+                continue
+        prev = (pc, k, ops[pc + 6] & 0xFFFFFFFF) if (
+            kind == OP_T and (fl & 3) == T_BUTTERFLY) else None
+        pc += ln
 
 
 def decode_header(w: int):

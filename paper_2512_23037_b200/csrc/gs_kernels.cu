@@ -40,6 +40,7 @@ namespace gs {
 enum { OP_END = 0, OP_T = 1, OP_MEAS = 2, OP_NOISE = 3, OP_FEEDBACK = 4,
        OP_DETECTOR = 5, OP_OBSERVABLE = 6, OP_GROW_LIMIT = 7 };
 enum { T_DIAG = 0, T_BUTTERFLY = 1, T_GROW = 2 };
+enum { TF_FUSE = 16 };   // T flag: apply together with the next BUTTERFLY op
 enum { M_DET = 0, M_PIVOT_SPAN = 1, M_PIVOT_NOSPAN = 2 };
 enum { MF_RECORD = 16, MF_FLIP = 32, MF_RESET = 64, MF_COMPACT = 128 };
 enum { NK_DEP1 = 0, NK_DEP2 = 1, NK_XERR = 2, NK_ZERR = 3 };
@@ -346,6 +347,57 @@ __device__ __noinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32
     A[j0] = prune_acc(cadd(cmul(a, v0), neg_if(cmul(bx0, v1), s1)), r.sum, r.nz);
     A[j1] = prune_acc(cadd(cmul(a, v1), neg_if(cmul(bx0, v0), s0)), r.sum, r.nz);
   }
+  return r;
+}
+
+// Two consecutive T gates with partner vectors cb1 != cb2 (compiler flag
+// TF_FUSE): one pass over the 4-element groups {x, x^cb1, x^cb2,
+// x^cb1^cb2}; gate 1 on the cb1 pairs, prune, gate 2 on the cb2 pairs,
+// prune -- exactly the two single-gate passes' arithmetic, half the memory
+// traffic and index work.  Groups are enumerated by inserting zeros at the
+// pivot bits h1 = top(cb1) and h2 = top(cb2 reduced by cb1).
+struct Gate {
+  double2 a, bx0;
+  u32 cb, dc, dmask;
+};
+struct SumNz2 {
+  double sum;
+  u32 nz, nz1;
+};
+template <bool kS>
+__device__ __noinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g1, Gate g2) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  const u32 h1 = 31 - __clz(g1.cb);
+  const u32 cr = ((g2.cb >> h1) & 1u) ? (g2.cb ^ g1.cb) : g2.cb;
+  const u32 h2 = 31 - __clz(cr);
+  const u32 plo = min(h1, h2), phi = max(h1, h2);
+  SumNz2 r;
+  r.sum = 0.0;
+  r.nz = 0;
+  r.nz1 = 0;
+  double dummy = 0.0;
+#pragma unroll 1
+  for (u32 m = lane; m < quarter; m += 32) {
+    const u32 x0 = ins_bit(ins_bit(m, plo, 0), phi, 0);
+    const u32 x1 = x0 ^ g1.cb, x2 = x0 ^ g2.cb, x3 = x1 ^ g2.cb;
+    const double2 v0 = A[x0], v1 = A[x1], v2 = A[x2], v3 = A[x3];
+    // gate 1: pairs (x0, x1), (x2, x3)
+    const u32 s0 = g1.dc ^ par32(x0 & g1.dmask), s1 = g1.dc ^ par32(x1 & g1.dmask);
+    const u32 s2 = g1.dc ^ par32(x2 & g1.dmask), s3 = g1.dc ^ par32(x3 & g1.dmask);
+    const double2 u0 = prune_acc(cadd(cmul(g1.a, v0), neg_if(cmul(g1.bx0, v1), s1)), dummy, r.nz1);
+    const double2 u1 = prune_acc(cadd(cmul(g1.a, v1), neg_if(cmul(g1.bx0, v0), s0)), dummy, r.nz1);
+    const double2 u2 = prune_acc(cadd(cmul(g1.a, v2), neg_if(cmul(g1.bx0, v3), s3)), dummy, r.nz1);
+    const double2 u3 = prune_acc(cadd(cmul(g1.a, v3), neg_if(cmul(g1.bx0, v2), s2)), dummy, r.nz1);
+    // gate 2: pairs (x0, x2), (x1, x3)
+    const u32 t0 = g2.dc ^ par32(x0 & g2.dmask), t1 = g2.dc ^ par32(x1 & g2.dmask);
+    const u32 t2 = g2.dc ^ par32(x2 & g2.dmask), t3 = g2.dc ^ par32(x3 & g2.dmask);
+    A[x0] = prune_acc(cadd(cmul(g2.a, u0), neg_if(cmul(g2.bx0, u2), t2)), r.sum, r.nz);
+    A[x2] = prune_acc(cadd(cmul(g2.a, u2), neg_if(cmul(g2.bx0, u0), t0)), r.sum, r.nz);
+    A[x1] = prune_acc(cadd(cmul(g2.a, u1), neg_if(cmul(g2.bx0, u3), t3)), r.sum, r.nz);
+    A[x3] = prune_acc(cadd(cmul(g2.a, u3), neg_if(cmul(g2.bx0, u1), t1)), r.sum, r.nz);
+  }
+  (void)dummy;
   return r;
 }
 
@@ -1383,6 +1435,40 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
         if (ps != 1.0) sweep_scale(A, size, ps);   // rare: right after a deferral
         ps = 1.0;
+        if (tcase == T_BUTTERFLY && (wfl & TF_FUSE)) {
+          // this gate and the next one (also a BUTTERFLY at the same k, no
+          // noise between) in one pass
+          const u64 *op2 = ops + wpc;
+          const u64 h2 = hnext;
+          const u32 instr2 = (u32)(h2 >> 32);
+          sig_lo ^= __ldg(op2 + 1);
+          sig_hi ^= __ldg(op2 + 2);
+          const u32 flip2 = par64(sig_lo & __ldg(op2 + 3)) ^ par64(sig_hi & __ldg(op2 + 4));
+          const u64 w62 = __ldg(op2 + 6);
+          Gate g1, g2;
+          g1.a = a; g1.bx0 = bx0; g1.cb = cb; g1.dc = dc; g1.dmask = dmask;
+          g2.a = make_double2(dbits(__ldg(op2 + 7)), dbits(__ldg(op2 + 8)));
+          const double2 bxs2 = make_double2(dbits(__ldg(op2 + 9)), dbits(__ldg(op2 + 10)));
+          g2.bx0 = flip2 ? cneg(bxs2) : bxs2;
+          g2.cb = (u32)w62;
+          g2.dmask = (u32)(w62 >> 32);
+          g2.dc = par64(__ldg(op2 + 5) & c);
+          mbytes += __ldg(op2 + 11);
+          wpc += (u32)((h2 >> 8) & 0xff);
+          hnext = __ldg(ops + wpc);
+          const SumNz2 r2 = sweep_butterfly2<kSmemChi>(A, size >> 2, g1, g2);
+          __syncwarp();
+          const u32 cnt1 = warp_sum_u32(r2.nz1);
+          mbytes += (u64)kEntryBytes * (cin + cnt1);
+          if ((u64)cnt1 > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
+          if (cnt1 == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          cnt = warp_sum_u32(r2.nz);
+          nrm = warp_sum(r2.sum);
+          mbytes += (u64)kEntryBytes * (cnt1 + cnt);
+          if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr2; break; }
+          if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr2; break; }
+          continue;
+        }
         SumNz r;
         if (tcase == T_BUTTERFLY) {
           r = sweep_butterfly<kSmemChi>(A, size >> 1, cb, dc, dmask, a, bx0);

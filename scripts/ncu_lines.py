@@ -81,15 +81,22 @@ def main():
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     h = rows[hi]
-    data = [r for r in rows[hi + 1:] if len(r) == len(h)]
+    data = []
+    for r in rows[hi + 1:]:   # first kernel of the listing only
+        if r and r[0] in ("Address", "Kernel Name"):
+            break
+        if len(r) == len(h):
+            data.append(r)
     iA, iS, iE = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), \
         h.index("Instructions Executed")
     base = int(data[0][iA], 16)
     kname = rows[0][1] if rows and len(rows[0]) > 1 else ""
     import re as _re
     bools = _re.findall(r"\(bool\)(\d)", kname)
-    kre = "sample_kernel" + "".join("ILb%sE" % b if i == 0 else "Lb%sE" % b
-                                    for i, b in enumerate(bools)) if bools else "sample_kernel"
+    kn = _re.search(r"(\w+_kernel)<", kname)
+    kn = kn.group(1) if kn else "sample_kernel"
+    kre = ("%d%s" % (len(kn), kn)) + "".join("ILb%sE" % b if i == 0 else "Lb%sE" % b
+                                          for i, b in enumerate(bools))
     m = disasm(lib, kre)
     by_line_s, by_line_e = defaultdict(float), defaultdict(float)
     mism = 0
