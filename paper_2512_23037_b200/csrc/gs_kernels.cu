@@ -1228,7 +1228,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     u64 sl, sig_lo = 0, sig_hi = 0, c = 0, obs = 0, mbytes = 0, gpick = 0;
     u32 cnt = 1, gj = 0, gpos = 0xFFFFFFFFu, fire_pc = 0xFFFFFFFFu;
     const u32 k = S.k0;
-    double nrm = 0.0;
+    // chi norm, kept as per-lane partial sums and reduced only when a
+    // deterministic measurement needs it
+    double nrm_l = 0.0;
     if (!S.q_in) {
       sl = S.first + idx;
       rng.shot = R.shot_begin + sl;
@@ -1237,7 +1239,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 #pragma unroll 1
       for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
       if (lane == 0) A[0] = make_double2(1.0, 0.0);
-      nrm = 1.0;
+      nrm_l = lane == 0 ? 1.0 : 0.0;
       if (philox && P.geo_len > 1 && P.nlocs) {
         const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, rng.shot, 0u, 0u);
         gpos = gc.pos;
@@ -1264,9 +1266,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       for (u32 j = lane; j < (1u << k); j += 32) {
         const double2 v = qc[j];
         A[j] = v;
-        nrm = __dadd_rn(nrm, abs2(v));
+        nrm_l = __dadd_rn(nrm_l, abs2(v));
       }
-      nrm = warp_sum(nrm);
     }
     if (!philox) fire_pc = 0xFFFFFFFFu;
     u32 kcur = k;
@@ -1463,7 +1464,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           if ((u64)cnt1 > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
           if (cnt1 == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
           cnt = warp_sum_u32(r2.nz);
-          nrm = warp_sum(r2.sum);
+          nrm_l = r2.sum;
           mbytes += (u64)kEntryBytes * (cnt1 + cnt);
           if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr2; break; }
           if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr2; break; }
@@ -1478,7 +1479,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         }
         __syncwarp();
         cnt = warp_sum_u32(r.nz);
-        nrm = warp_sum(r.sum);
+        nrm_l = r.sum;
         mbytes += (u64)kEntryBytes * (cin + cnt);
         if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
         if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
@@ -1509,10 +1510,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         };
         // a renormalisation by rs that needs no data movement: deferred to
         // the next pass over chi (ldps); nonzero count unchanged
-        auto defer_scale = [&](double rs) {
+        auto defer_scale = [&](double rs, double kept) {
           if (ps != 1.0) sweep_scale(A, size, ps);
           ps = rs;
-          nrm = __dmul_rn(__dmul_rn(nrm, rs), rs);
+          nrm_l = lane == 0 ? __dmul_rn(__dmul_rn(kept, rs), rs) : 0.0;
         };
         const u32 cin = cnt;
         bool plus;
@@ -1522,6 +1523,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           double sp, sm;
           if (dmask == 0) {
             // every coordinate has eigenvalue (-1)^neg0: P+ is the norm
+            const double nrm = warp_sum(nrm_l);
             sp = neg0 ? 0.0 : nrm;
             sm = neg0 ? nrm : 0.0;
           } else {
@@ -1540,19 +1542,19 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             ps = 1.0;
             __syncwarp();
             cnt = warp_sum_u32(r.nz);
-            nrm = warp_sum(r.sum);
+            nrm_l = r.sum;
             if (tau) c ^= vec;
             kcur = wk - 1;
           } else if ((plus ? sm : sp) == 0.0) {
             // the other eigenspace is empty: the filter is a pure
             // renormalisation
-            defer_scale(rs);
+            defer_scale(rs, plus ? sp : sm);
           } else {
             const SumNz r = sweep_filter(A, size, dmask, neg0, want_neg, rs, ps);
             ps = 1.0;
             __syncwarp();
             cnt = warp_sum_u32(r.nz);
-            nrm = warp_sum(r.sum);
+            nrm_l = r.sum;
           }
         } else {
           // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
@@ -1577,11 +1579,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             const SumNz r = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
             __syncwarp();
             cnt = warp_sum_u32(r.nz);
-            nrm = warp_sum(r.sum);
+            nrm_l = r.sum;
             kcur = wk - 1;
           } else {
-            nrm = sk;
-            defer_scale(rs);
+            defer_scale(rs, sk);
           }
           if (g.ct) c ^= vec;
           // tableau sign update of the pivot (ref tableau.py:176-200)
