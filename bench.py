@@ -36,15 +36,15 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
 def _ncu_latest(workload: str, shots: int):
-    """DRAM traffic + issue utilisation of the sampling kernel from the
-    committed ncu --set full capture (profiles/ncu_latest.json), if it was
-    taken on this workload with this launch size."""
+    """DRAM traffic + issue utilisation of the section kernels from the
+    committed ncu --set full capture (profiles/ncu_latest.json) of this
+    workload (per-shot DRAM bytes; `shots` kept for the call signature)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_latest.json")) as fh:
             d = json.load(fh)
     except Exception:
         return None
-    if d.get("workload") != workload or int(d.get("shots_per_launch", 0)) != shots:
+    if d.get("workload") != workload:
         return None
     return d
 
@@ -310,8 +310,8 @@ def main():
         roofline = {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak,
-            # DRAM bytes per launch of gs::sample_kernel, ncu --set full
-            "traffic": ncu["dram_bytes_per_launch"] if ncu else None,
+            # DRAM bytes per step (all section launches), ncu --set full
+            "traffic": ncu["dram_bytes_per_shot"] * S if ncu else None,
             "peak_source": peak_src,
             "model_bytes_per_shot": model_bytes / max(total_shots, 1),
             "note": ("achieved = SURVEY 8(d) state-touch bytes of the reference "
@@ -324,6 +324,8 @@ def main():
             roofline["issue_active_pct"] = ncu["issue_active_pct"]
             roofline["fp64_pipe_pct"] = ncu["fp64_pipe_pct"]
             roofline["ncu_capture"] = ncu["capture"]
+            roofline["dominant_kernel"] = ncu["dominant_kernel"]
+            roofline["dominant_share"] = ncu["dominant_share"]
         if not args.no_cpu_baseline:
             cb = cpu_baseline(prog, args.cpu_seconds, args.rng, args.p)
         line = {
