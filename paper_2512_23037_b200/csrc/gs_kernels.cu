@@ -584,7 +584,7 @@ __device__ __noinline__ void sweep_scale(double2 *__restrict__ A, u32 size, doub
 // GS_WIDE_ONLY runs the whole program as one wide section (A/B, tests).
 
 #ifndef GS_NARROW_BLOCKS
-#define GS_NARROW_BLOCKS 4
+#define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
 #endif
 #ifndef GS_WIDE_BLOCKS
 #define GS_WIDE_BLOCKS 3   // <= 168 registers (no spills); shared memory holds 12-13 warps/SM anyway
