@@ -377,21 +377,28 @@ __device__ __noinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g
   r.nz = 0;
   r.nz1 = 0;
   double dummy = 0.0;
+  // sign parities: the zero-insertion J is bitwise linear, so for
+  // m = 32r + lane, par(J(m) & mask) = par(J(32r) & mask) ^ par(J(lane) & mask)
+  // (a per-round and a per-lane term); the group members differ by cb1, cb2
+  const u32 jl = ins_bit(ins_bit(lane, plo, 0), phi, 0);
+  const u32 l1 = g1.dc ^ par32(jl & g1.dmask), l2 = g2.dc ^ par32(jl & g2.dmask);
+  const u32 a1 = par32(g1.cb & g1.dmask), b1 = par32(g2.cb & g1.dmask);
+  const u32 a2 = par32(g1.cb & g2.dmask), b2 = par32(g2.cb & g2.dmask);
 #pragma unroll 1
   for (u32 m = lane; m < quarter; m += 32) {
-    const u32 x0 = ins_bit(ins_bit(m, plo, 0), phi, 0);
+    const u32 jr = ins_bit(ins_bit(m & ~31u, plo, 0), phi, 0);
+    const u32 x0 = jr | jl;
     const u32 x1 = x0 ^ g1.cb, x2 = x0 ^ g2.cb, x3 = x1 ^ g2.cb;
     const double2 v0 = A[x0], v1 = A[x1], v2 = A[x2], v3 = A[x3];
+    const u32 p1 = l1 ^ par32(jr & g1.dmask), p2 = l2 ^ par32(jr & g2.dmask);
     // gate 1: pairs (x0, x1), (x2, x3)
-    const u32 s0 = g1.dc ^ par32(x0 & g1.dmask), s1 = g1.dc ^ par32(x1 & g1.dmask);
-    const u32 s2 = g1.dc ^ par32(x2 & g1.dmask), s3 = g1.dc ^ par32(x3 & g1.dmask);
+    const u32 s0 = p1, s1 = p1 ^ a1, s2 = p1 ^ b1, s3 = p1 ^ a1 ^ b1;
     const double2 u0 = prune_acc(cadd(cmul(g1.a, v0), neg_if(cmul(g1.bx0, v1), s1)), dummy, r.nz1);
     const double2 u1 = prune_acc(cadd(cmul(g1.a, v1), neg_if(cmul(g1.bx0, v0), s0)), dummy, r.nz1);
     const double2 u2 = prune_acc(cadd(cmul(g1.a, v2), neg_if(cmul(g1.bx0, v3), s3)), dummy, r.nz1);
     const double2 u3 = prune_acc(cadd(cmul(g1.a, v3), neg_if(cmul(g1.bx0, v2), s2)), dummy, r.nz1);
     // gate 2: pairs (x0, x2), (x1, x3)
-    const u32 t0 = g2.dc ^ par32(x0 & g2.dmask), t1 = g2.dc ^ par32(x1 & g2.dmask);
-    const u32 t2 = g2.dc ^ par32(x2 & g2.dmask), t3 = g2.dc ^ par32(x3 & g2.dmask);
+    const u32 t0 = p2, t1 = p2 ^ a2, t2 = p2 ^ b2, t3 = p2 ^ a2 ^ b2;
     A[x0] = prune_acc(cadd(cmul(g2.a, u0), neg_if(cmul(g2.bx0, u2), t2)), r.sum, r.nz);
     A[x2] = prune_acc(cadd(cmul(g2.a, u2), neg_if(cmul(g2.bx0, u0), t0)), r.sum, r.nz);
     A[x1] = prune_acc(cadd(cmul(g2.a, u1), neg_if(cmul(g2.bx0, u3), t3)), r.sum, r.nz);
