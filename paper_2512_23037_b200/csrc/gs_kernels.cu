@@ -60,6 +60,7 @@ struct DevProg {
   u64 noise_off, wordpc_off;
   u64 geo_off, acc_off;   // Philox fire schedule: gap table, thinning table
   u32 geo_len, noise_uniform;
+  float geo_ilq;          // 1 / log(1 - p_max), the gap search's first guess
 };
 
 struct DevRun {
@@ -225,13 +226,27 @@ struct GeoCand {
   u64 pick;
   u32 pos;
 };
-__device__ __noinline__ GeoCand geo_candidate(const u64 *__restrict__ T, u32 tlen,
+// The search starts from the float guess log(u)/log(1-p_max) (`ilq` =
+// 1/log(T[1] 2^-53)) and narrows to a 3-entry window before bisecting, so a
+// gap costs ~4 table loads instead of log2(tlen); the table decides (exact).
+__device__ __noinline__ GeoCand geo_candidate(const u64 *__restrict__ T, u32 tlen, float ilq,
                                               u64 master, u64 shot, u32 j, u32 start) {
   const uint4 x = philox4(j, 1u, shot, master);
   const u64 m = ((((u64)x.y) << 32) | x.x) >> 11;
   GeoCand c;
   c.pick = ((((u64)x.w) << 32) | x.z) >> 11;
-  u32 lo = 0, hi = tlen - 1;
+  const u32 G = tlen - 1;
+  // answer = max{g <= G : m < T[g]}; invariant: m < T[lo], answer <= hi
+  const float gf = __logf(((float)m + 0.5f) * 0x1.0p-53f) * ilq;
+  u32 g = gf >= (float)G ? G : (gf > 0.f ? (u32)gf : 0u);
+  u32 lo = 0, hi = G;
+  if (m < __ldg(T + g)) {
+    lo = g;
+    if (g + 3 <= G && !(m < __ldg(T + g + 3))) hi = g + 2;
+  } else {
+    hi = g - 1;                      // g >= 1: T[0] = 2^53 > m
+    if (g >= 3 && m < __ldg(T + g - 3)) lo = g - 3;
+  }
   while (lo < hi) {
     const u32 mid = (lo + hi + 1) >> 1;
     if (m < __ldg(T + mid)) lo = mid; else hi = mid - 1;
@@ -760,7 +775,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
       AN(0) = make_double2(1.0, 0.0);
       if (philox && valid && P.geo_len > 1 && P.nlocs) {
-        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, shot, 0u, 0u);
+        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, shot, 0u, 0u);
         sgpos = gc.pos;
         sgpick = gc.pick;
         sgj = 1;
@@ -850,7 +865,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
                 noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
                              (double)sgpick * 0x1.0p-53, ex, ez);
               }
-              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, shot, sgj, l + 1);
+              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, shot, sgj, l + 1);
               sgpos = gc.pos;
               sgpick = gc.pick;
               ++sgj;
@@ -1248,7 +1263,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       if (lane == 0) A[0] = make_double2(1.0, 0.0);
       nrm_l = lane == 0 ? 1.0 : 0.0;
       if (philox && P.geo_len > 1 && P.nlocs) {
-        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, rng.shot, 0u, 0u);
+        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, rng.shot, 0u, 0u);
         gpos = gc.pos;
         gpick = gc.pick;
         gj = 1;
@@ -1331,7 +1346,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
                 noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
                              (double)gpick * 0x1.0p-53, ex, ez);
               }
-              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, R.master, rng.shot, gj, l + 1);
+              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, rng.shot, gj, l + 1);
               gpos = gc.pos;
               gpick = gc.pick;
               ++gj;
@@ -2056,6 +2071,11 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   P.geo_len = p->info.geo_len;
   P.acc_off = p->info.acc_off;
   P.noise_uniform = p->info.noise_uniform;
+  P.geo_ilq = 0.f;
+  if (p->info.geo_len >= 2) {
+    const double q = (double)p->tables[p->info.geo_off + 1] * 0x1.0p-53;
+    if (q < 1.0) P.geo_ilq = (float)(1.0 / log(q));
+  }
   gs::DevRun R;
   R.master = r->master_seed;
   R.shot_begin = r->shot_begin;
