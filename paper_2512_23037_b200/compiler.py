@@ -67,6 +67,7 @@ MF_RESET = 1 << 6
 MF_COMPACT = 1 << 7
 # noise kinds in location words
 NK_DEP1, NK_DEP2, NK_XERR, NK_ZERR = 0, 1, 2, 3
+OWNER_LIMIT = 1 << 14     # noise instructions addressable from a location word
 _NOISE_KIND = {"DEPOLARIZE1": NK_DEP1, "DEPOLARIZE2": NK_DEP2,
                "X_ERROR": NK_XERR, "Z_ERROR": NK_ZERR}
 
@@ -514,19 +515,23 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         kind = _NOISE_KIND[name]
         thr = _threshold(p)
         loc0 = len(em.locs) // 2
+        # owning noise instruction index in bits 50..63 of every location
+        # word (device O(1) owner lookup; the device bisects the noise table
+        # when the program has more than OWNER_LIMIT noise instructions)
+        kword = kind | ((len(noise_ops) << 2) if len(noise_ops) < OWNER_LIMIT else 0)
         if kind == NK_DEP2:
             pairs = list(zip(targets[0::2], targets[1::2]))
             for j, (a, b) in enumerate(pairs):
                 em.locs += [(draws + 2 * j) | (a << 32) | (b << 40)
-                            | (kind << 48), thr]
+                            | (kword << 48), thr]
             draws += 2 * len(pairs)
         elif kind == NK_DEP1:
             for j, q in enumerate(targets):
-                em.locs += [(draws + 2 * j) | (q << 32) | (kind << 48), thr]
+                em.locs += [(draws + 2 * j) | (q << 32) | (kword << 48), thr]
             draws += 2 * len(targets)
         else:
             for j, q in enumerate(targets):
-                em.locs += [(draws + j) | (q << 32) | (kind << 48), thr]
+                em.locs += [(draws + j) | (q << 32) | (kword << 48), thr]
             draws += len(targets)
         nloc = len(em.locs) // 2 - loc0
         if nloc > 1024:

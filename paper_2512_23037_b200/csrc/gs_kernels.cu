@@ -675,8 +675,12 @@ __device__ __forceinline__ void noise_letter(u32 nk, u32 qa, u32 qb, double u, u
   }
 }
 
-// owning noise instruction of location l: last m with loc0(m) <= l
+// owning noise instruction of location l: its index sits in bits 50..63 of
+// the location word when the program has < 2^14 noise instructions
+// (compiler.OWNER_LIMIT), else bisect: last m with loc0(m) <= l
 __device__ __forceinline__ const u64 *noise_owner(const DevProg &P, u32 l) {
+  if (P.nnoise <= (1u << 14))
+    return P.tables + P.noise_off + 4ull * (u32)(__ldg(P.locs + 2ull * l) >> 50);
   u32 lo = 0, hi = P.nnoise;
   while (hi - lo > 1) {
     const u32 mid = (lo + hi) >> 1;
