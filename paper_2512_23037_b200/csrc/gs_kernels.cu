@@ -354,11 +354,14 @@ __device__ __noinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
+  const u32 jl = ins_bit(lane, hb, 0);
+  const u32 pl = dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
 #pragma unroll 1
   for (u32 m = lane; m < half; m += 32) {
-    const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+    const u32 jr = ins_bit(m & ~31u, hb, 0);
+    const u32 j0 = jr | jl, j1 = j0 ^ cb;
     const double2 v0 = A[j0], v1 = A[j1];
-    const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+    const u32 s0 = pl ^ par32(jr & dmask), s1 = s0 ^ pcb;
     A[j0] = prune_acc(cadd(cmul(a, v0), neg_if(cmul(bx0, v1), s1)), r.sum, r.nz);
     A[j1] = prune_acc(cadd(cmul(a, v1), neg_if(cmul(bx0, v0), s0)), r.sum, r.nz);
   }
