@@ -295,10 +295,10 @@ __device__ __forceinline__ u32 lanemask_lt(u32 lane) { return (1u << lane) - 1u;
 // ---------------------------------------------------------------- wide sweeps
 //
 // Warp-cooperative passes over a dense chi array A[0, 2^k): lane l takes
-// coordinates l, l+32, ... (pair indices for pair sweeps), one in flight.
-// Measured on the B200 (shared-memory chi, 12 warps/SM): 2 or 4 coordinates
-// in flight per lane 10.8M / 8.2M vs 20.6M shots/s; a per-round split of the
-// sign parities 20.8M vs 21.6M.  Out of line: one copy serves every caller
+// coordinates l, l+32, ... (pair / group indices for the T sweeps), one
+// group in flight per lane -- measured on the B200, more per lane (unrolled
+// rounds, 8-element groups of three fused gates) was slower every time
+// (profiles/README.md).  Out of line: one copy serves every caller
 // (instruction cache).  Per-lane partial results (nonzero count, sum of
 // |v|^2 of the written entries = the chi norm the next deterministic
 // measurement needs); callers reduce across the warp.
