@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--chi-smem", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
     ap.add_argument("--wide-only", action="store_true")
+    ap.add_argument("--print-sections", action="store_true",
+                    help="print the number of section launches per chunk and exit")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -218,6 +220,9 @@ def main():
             dist.init_process_group(backend)
     dp = compile_program(prog)
     P = Program(dp)
+    if args.print_sections:
+        print(P.sections(_lib.GS_WIDE_ONLY if args.wide_only else 0))
+        return 0
     eng = Engine(dev)
     flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if args.rng == "philox" else 0)
     if args.chi_global:

@@ -109,6 +109,9 @@ int gs_program_create(const gs_program_info *info, const uint64_t *ops,
                       size_t n_ops, const uint64_t *tables, size_t n_tables,
                       const uint64_t *locs, size_t n_locs, gs_program **out);
 int gs_program_destroy(gs_program *prog);
+/* number of narrow/wide sections (= sampling launches per chunk of shots)
+   the program runs as under `flags` (GS_WIDE_ONLY); <0 on error */
+int gs_program_sections(const gs_program *prog, uint32_t flags);
 
 int gs_engine_create(int device, gs_engine **out);
 int gs_engine_destroy(gs_engine *eng);

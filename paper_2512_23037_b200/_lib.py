@@ -32,7 +32,7 @@ GS_C_MODEL_BYTES = 7
 GS_C_PER_OBS = 8
 
 EXPORTED = (
-    "gs_program_create", "gs_program_destroy", "gs_engine_create",
+    "gs_program_create", "gs_program_destroy", "gs_program_sections", "gs_engine_create",
     "gs_engine_destroy", "gs_run_counters", "gs_run_counters_witness",
     "gs_run_counters_async",
     "gs_run_records", "gs_dump_shots", "gs_anticommute_mask",
@@ -84,6 +84,8 @@ def load(path: str | None = None):
                                       u64p, ct.c_size_t, u64p, ct.c_size_t,
                                       ct.POINTER(vp)]
     lib.gs_program_destroy.argtypes = [vp]
+    lib.gs_program_sections.argtypes = [vp, ct.c_uint32]
+    lib.gs_program_sections.restype = ct.c_int
     lib.gs_engine_create.argtypes = [ct.c_int, ct.POINTER(vp)]
     lib.gs_engine_destroy.argtypes = [vp]
     lib.gs_run_counters.argtypes = [vp, vp, ct.POINTER(GsRunParams),

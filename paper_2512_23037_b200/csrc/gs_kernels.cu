@@ -698,6 +698,7 @@ enum { Q_SL = 0, Q_LO, Q_HI, Q_C, Q_OBS, Q_MB, Q_PICK, Q_SEED, Q_CNTK, Q_GEO, Q_
 
 struct DevSec {
   u32 pc0, k0, nm0;        // first op, its chi dimension, first noise instr. with ipc >= pc0
+  u32 pc_end;              // narrow: stop before this op (0xFFFFFFFF: at the first wide op)
   u64 first, count;        // fresh shots (q_in == nullptr): run-local indices [first, first+count)
   const u64 *q_in;         // else: queue slots and their number
   const u32 *n_in;
@@ -815,7 +816,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
       const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
       const u32 instr = (u32)(h >> 32);
-      if (op_is_wide(kind, k, fl)) { exit_k = k; break; }   // section end
+      if (pc == S.pc_end || op_is_wide(kind, k, fl)) { exit_k = k; break; }   // section end
       // ============================== narrow op, lane per shot
       // @region narrow: noise
       // apply E to this lane's shot (ref state.py:88-102)
@@ -1972,24 +1973,42 @@ struct Section {
   bool wide;
 };
 
+#ifndef GS_NARROW_SPLIT
+#define GS_NARROW_SPLIT 75  // split narrow sections every N ops (0: never) so the survivors of
+                            // early discards re-pack into full warps (A/B: 51.2M at 75, 49.4M unsplit,
+                            // 50.6M at 150, 50.3M at 40)
+#endif
+
 static void sections_of(const gs_program *p, bool wide_only, std::vector<Section> &out) {
   out.clear();
   const std::vector<u64> &ops = p->ops;
   size_t pc = 0, nm = 0;
+  u32 nops = 0;
   const u32 nn = p->info.num_noise;
   while (pc < ops.size()) {
     const u64 h = ops[pc];
     const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
     const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
     const bool wide = wide_only || gs::op_is_wide(kind, k, fl);
-    if (out.empty() || out.back().wide != wide) {
+    const bool split = !wide && (GS_NARROW_SPLIT > 0) && nops >= (u32)GS_NARROW_SPLIT;
+    if (out.empty() || out.back().wide != wide || split) {
       while (nm < nn && (u32)p->tables[p->info.noise_off + 4 * nm] < (u32)pc) ++nm;
       out.push_back(Section{(u32)pc, k, (u32)nm, wide});
+      nops = 0;
     }
+    ++nops;
     if (kind == gs::OP_END || len == 0) break;
     pc += len;
   }
 }
+
+int gs_program_sections(const gs_program *p, uint32_t flags) {
+  if (!p) return fail(GS_ERR_ARG, "null argument");
+  std::vector<Section> secs;
+  sections_of(p, (flags & GS_WIDE_ONLY) != 0, secs);
+  return (int)secs.size();
+}
+
 
 extern "C++" {
 // the sampling kernels: RNG mode (x chi placement for the wide kernel)
@@ -2169,6 +2188,7 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
         S.pc0 = secs[i].pc0;
         S.k0 = secs[i].k0;
         S.nm0 = secs[i].nm0;
+        S.pc_end = (i + 1 < secs.size() && !secs[i + 1].wide) ? secs[i + 1].pc0 : 0xFFFFFFFFu;
         S.first = first;
         S.count = count;
         S.q_in = i ? e->d_queue[(i - 1) & 1] : nullptr;

@@ -42,6 +42,13 @@ class Program:
                                          self._locs.size, ct.byref(h)))
         self.handle = h
 
+    def sections(self, flags: int = 0) -> int:
+        """Narrow/wide sections (= sampling launches per chunk of shots)."""
+        n = _lib.load().gs_program_sections(self.handle, flags)
+        if n < 0:
+            _lib.check(n)
+        return n
+
     @classmethod
     def compile(cls, prog, **kw) -> "Program":
         return cls(compile_program(prog, **kw))
