@@ -446,8 +446,10 @@ __device__ __noinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmas
 
 // diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
 // fired noise Paulis)
-__device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 dc, u32 mask,
+template <bool kS>
+__device__ __noinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask,
                                          double2 f0, double2 f1, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
 #pragma unroll 1
   for (u32 j = lane; j < size; j += 32)
@@ -455,8 +457,10 @@ __device__ __noinline__ void sweep_phase(double2 *__restrict__ A, u32 size, u32 
 }
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
-__device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u32 size, u32 dmask,
-                                               u32 neg0, double ps) {
+template <bool kS>
+__device__ __noinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask, u32 neg0,
+                                               double ps) {
+  const double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0, sm = 0.0;
 #pragma unroll 1
@@ -468,8 +472,10 @@ __device__ __noinline__ double2 sweep_det_sums(const double2 *__restrict__ A, u3
 }
 
 // keep the chosen eigen-entries, scaled by rs; zero the others
-__device__ __noinline__ SumNz sweep_filter(double2 *__restrict__ A, u32 size, u32 dmask,
-                                           u32 neg0, u32 want_neg, double rs, double ps) {
+template <bool kS>
+__device__ __noinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32 neg0,
+                                           u32 want_neg, double rs, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
   SumNz r;
   r.sum = 0.0;
@@ -492,8 +498,10 @@ __device__ __noinline__ SumNz sweep_filter(double2 *__restrict__ A, u32 size, u3
 // in-place compaction dropping coordinate isq: A[jp] = rs * A[src(jp)],
 // src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
 // at isq; src(jp) >= jp, so reads of a round finish before its writes
-__device__ __noinline__ SumNz sweep_compact(double2 *__restrict__ A, u32 half, u32 isq, u32 mask,
-                                            u32 tau, double rs, double ps) {
+template <bool kS>
+__device__ __noinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
+                                            double rs, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
   SumNz r;
   r.sum = 0.0;
@@ -550,8 +558,9 @@ __device__ __forceinline__ void pivot_terms(const double2 *__restrict__ A, const
     dst = m;
   }
 }
-__device__ __noinline__ double sweep_pivot_p(const double2 *__restrict__ A, PivotGeo g,
-                                             double2 xpp, double ps) {
+template <bool kS>
+__device__ __noinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2 xpp, double ps) {
+  const double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0;
 #pragma unroll 1
@@ -563,8 +572,10 @@ __device__ __noinline__ double sweep_pivot_p(const double2 *__restrict__ A, Pivo
   }
   return sp;
 }
-__device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g, double2 xpp,
-                                            bool plus, double ps) {
+template <bool kS>
+__device__ __noinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 xpp, bool plus,
+                                            double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
   SumNz r;
   r.sum = 0.0;
@@ -580,7 +591,9 @@ __device__ __noinline__ SumNz sweep_pivot_w(double2 *__restrict__ A, PivotGeo g,
 }
 
 // apply a pending renormalisation in place: A[j] = ps * A[j]
-__device__ __noinline__ void sweep_scale(double2 *__restrict__ A, u32 size, double ps) {
+template <bool kS>
+__device__ __noinline__ void sweep_scale(double2 *A_, u32 size, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
 #pragma unroll 1
   for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], ps);
@@ -1329,7 +1342,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
                                          sig_lo, sig_hi);
           const double2 php = ipow(e.xi);
-          sweep_phase(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
+          sweep_phase<kSmemChi>(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
           ps = 1.0;
           __syncwarp();
           c ^= e.beta;
@@ -1441,7 +1454,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         if (tcase == T_DIAG) {
           // beta == 0: pure phase per entry (ref state.py:120-126); the
           // factors have modulus 1, the norm is kept
-          sweep_phase(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
+          sweep_phase<kSmemChi>(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
           ps = 1.0;
           __syncwarp();
           mbytes += 32ull * cnt;
@@ -1464,7 +1477,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           break;
         }
         // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
-        if (ps != 1.0) sweep_scale(A, size, ps);   // rare: right after a deferral
+        if (ps != 1.0) sweep_scale<kSmemChi>(A, size, ps);   // rare: right after a deferral
         ps = 1.0;
         if (tcase == T_BUTTERFLY && (wfl & TF_FUSE)) {
           // this gate and the next one (also a BUTTERFLY at the same k, no
@@ -1541,7 +1554,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         // a renormalisation by rs that needs no data movement: deferred to
         // the next pass over chi (ldps); nonzero count unchanged
         auto defer_scale = [&](double rs, double kept) {
-          if (ps != 1.0) sweep_scale(A, size, ps);
+          if (ps != 1.0) sweep_scale<kSmemChi>(A, size, ps);
           ps = rs;
           nrm_l = lane == 0 ? __dmul_rn(__dmul_rn(kept, rs), rs) : 0.0;
         };
@@ -1557,7 +1570,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             sp = neg0 ? 0.0 : nrm;
             sm = neg0 ? nrm : 0.0;
           } else {
-            const double2 part = sweep_det_sums(A, size, dmask, neg0, ps);
+            const double2 part = sweep_det_sums<kSmemChi>(A, size, dmask, neg0, ps);
             sp = warp_sum(part.x);
             sm = warp_sum(part.y);
           }
@@ -1568,7 +1581,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const double rs = inv_sqrt_norm(plus ? sp : sm);
           if (wfl & MF_COMPACT) {
             const u32 tau = want_neg ^ neg0;
-            const SumNz r = sweep_compact(A, size >> 1, isq, dmask, tau, rs, ps);
+            const SumNz r = sweep_compact<kSmemChi>(A, size >> 1, isq, dmask, tau, rs, ps);
             ps = 1.0;
             __syncwarp();
             cnt = warp_sum_u32(r.nz);
@@ -1580,7 +1593,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             // renormalisation
             defer_scale(rs, plus ? sp : sm);
           } else {
-            const SumNz r = sweep_filter(A, size, dmask, neg0, want_neg, rs, ps);
+            const SumNz r = sweep_filter<kSmemChi>(A, size, dmask, neg0, want_neg, rs, ps);
             ps = 1.0;
             __syncwarp();
             cnt = warp_sum_u32(r.nz);
@@ -1594,11 +1607,11 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
           g.dc = dc; g.dmask = dmask;
           const double2 xpp = ipow(xi0);   // i^xi0, exact
-          const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p(A, g, xpp, ps)));
+          const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p<kSmemChi>(A, g, xpp, ps)));
           plus = pick_plus(pp);
           const double chosen = plus ? pp : __dsub_rn(1.0, pp);
           if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
-          const SumNz w = sweep_pivot_w(A, g, xpp, plus, ps);
+          const SumNz w = sweep_pivot_w<kSmemChi>(A, g, xpp, plus, ps);
           ps = 1.0;
           __syncwarp();
           const double sk = warp_sum(w.sum);
@@ -1606,7 +1619,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
           const double rs = inv_sqrt_norm(sk);
           if (g.span) {
-            const SumNz r = sweep_compact(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+            const SumNz r = sweep_compact<kSmemChi>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
             __syncwarp();
             cnt = warp_sum_u32(r.nz);
             nrm_l = r.sum;
