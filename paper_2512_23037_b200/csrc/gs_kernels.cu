@@ -299,10 +299,11 @@ __device__ __forceinline__ u32 lanemask_lt(u32 lane) { return (1u << lane) - 1u;
 // coordinates l, l+32, ... (pair / group indices for the T sweeps), one
 // group in flight per lane -- measured on the B200, more per lane (unrolled
 // rounds, 8-element groups of three fused gates) was slower every time
-// (profiles/README.md).  Out of line: one copy serves every caller
-// (instruction cache).  Per-lane partial results (nonzero count, sum of
-// |v|^2 of the written entries = the chi norm the next deterministic
-// measurement needs); callers reduce across the warp.
+// (profiles/README.md).  Inlined into wide_kernel (+1.4 % over out-of-line
+// copies once each section kernel has its own code).  Per-lane partial
+// results (nonzero count, sum of |v|^2 of the written entries = the chi
+// norm the next deterministic measurement needs); callers reduce across
+// the warp.
 
 struct SumNz {
   double sum;
@@ -347,7 +348,7 @@ __device__ __forceinline__ double2 neg_if(double2 v, u32 s) {
 // T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
 // 294-306: a-term then b-term); no renormalisation pending (caller)
 template <bool kS>
-__device__ __noinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32 dc, u32 dmask,
+__device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32 dc, u32 dmask,
                                               double2 a, double2 bx0) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
@@ -384,7 +385,7 @@ struct SumNz2 {
   u32 nz, nz1;
 };
 template <bool kS>
-__device__ __noinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g1, Gate g2) {
+__device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g1, Gate g2) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
   const u32 h1 = 31 - __clz(g1.cb);
@@ -429,7 +430,7 @@ __device__ __noinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g
 
 // T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
 template <bool kS>
-__device__ __noinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmask, double2 a,
+__device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmask, double2 a,
                                          double2 bx0) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
@@ -448,7 +449,7 @@ __device__ __noinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmas
 // diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
 // fired noise Paulis)
 template <bool kS>
-__device__ __noinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask,
+__device__ __forceinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask,
                                          double2 f0, double2 f1, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
@@ -459,7 +460,7 @@ __device__ __noinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
 template <bool kS>
-__device__ __noinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask, u32 neg0,
+__device__ __forceinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask, u32 neg0,
                                                double ps) {
   const double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
@@ -474,7 +475,7 @@ __device__ __noinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask,
 
 // keep the chosen eigen-entries, scaled by rs; zero the others
 template <bool kS>
-__device__ __noinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32 neg0,
+__device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32 neg0,
                                            u32 want_neg, double rs, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
@@ -500,7 +501,7 @@ __device__ __noinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32
 // src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
 // at isq; src(jp) >= jp, so reads of a round finish before its writes
 template <bool kS>
-__device__ __noinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
+__device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
                                             double rs, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
@@ -560,7 +561,7 @@ __device__ __forceinline__ void pivot_terms(const double2 *__restrict__ A, const
   }
 }
 template <bool kS>
-__device__ __noinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2 xpp, double ps) {
+__device__ __forceinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2 xpp, double ps) {
   const double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
   double sp = 0.0;
@@ -574,7 +575,7 @@ __device__ __noinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2 xp
   return sp;
 }
 template <bool kS>
-__device__ __noinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 xpp, bool plus,
+__device__ __forceinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 xpp, bool plus,
                                             double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
@@ -593,7 +594,7 @@ __device__ __noinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 xpp
 
 // apply a pending renormalisation in place: A[j] = ps * A[j]
 template <bool kS>
-__device__ __noinline__ void sweep_scale(double2 *A_, u32 size, double ps) {
+__device__ __forceinline__ void sweep_scale(double2 *A_, u32 size, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = threadIdx.x & 31u;
 #pragma unroll 1
