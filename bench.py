@@ -326,7 +326,10 @@ def main():
                      "issue-bound (`issue_active_pct`)"),
         }
         if ncu:
+            # measured HBM traffic of the section queues at this run's rate
+            roofline["dram_achieved_gbs"] = ncu["dram_bytes_per_shot"] * value / 1e9
             roofline["issue_active_pct"] = ncu["issue_active_pct"]
+            roofline["smem_wavefront_pct"] = ncu.get("smem_wavefront_pct")
             roofline["fp64_pipe_pct"] = ncu["fp64_pipe_pct"]
             roofline["ncu_capture"] = ncu["capture"]
             roofline["dominant_kernel"] = ncu["dominant_kernel"]

@@ -38,13 +38,16 @@ for r in rows[2:]:
         "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "fp64_pipe_pct": val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "warp_instructions": val(r, "smsp__inst_executed.sum"),
-        "warps_active_per_sm": val(r, "sm__warps_active.avg.per_cycle_active")})
+        "warps_active_per_sm": val(r, "sm__warps_active.avg.per_cycle_active"),
+        "smem_wavefront_pct": val(r, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")})
 tot_t = sum(k["duration_s"] for k in kernels) or 1.0
 dom = max(kernels, key=lambda k: k["duration_s"])
 d = {"capture": tag, "workload": workload, "shots_in_capture": shots,
      "dram_bytes_per_shot": sum(k["dram_bytes"] for k in kernels) / shots,
      "issue_active_pct": sum(k["issue_active_pct"] * k["duration_s"] for k in kernels) / tot_t,
      "fp64_pipe_pct": sum(k["fp64_pipe_pct"] * k["duration_s"] for k in kernels) / tot_t,
+     "smem_wavefront_pct": sum(k["smem_wavefront_pct"] * k["duration_s"] for k in kernels) / tot_t,
+     "dram_gbs_serialised": sum(k["dram_bytes"] for k in kernels) / tot_t / 1e9,
      "dominant_kernel": dom["kernel"], "dominant_share": dom["duration_s"] / tot_t,
      "kernels": kernels}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
