@@ -65,6 +65,12 @@ WORKLOADS = {
     "msc_d5_2check": ("msc_d5_2check_proxy", lambda m: m.msc_circuit(5)),
     # BASELINE config 2
     "msc_d3": ("msc_d3_proxy", lambda m: m.msc_circuit(3)),
+    # BASELINE config 3
+    "injection_d3": ("d3_injection_3_rounds", lambda m: m.injection_circuit(3, 3)),
+    # BASELINE config 1 and two points of the config-4 sweep
+    "config1": ("config1_random_n8_t4", lambda m: m.config1_circuit(1)),
+    "config4_n32_t24": ("config4_random_n32_t24", lambda m: m.config4_circuit(32, 24, seed=56)),
+    "config4_n64_t32": ("config4_random_n64_t32", lambda m: m.config4_circuit(64, 32, seed=96)),
 }
 
 
