@@ -1972,7 +1972,9 @@ double gs_engine_last_kernel_ms(gs_engine *e) { return e ? e->last_ms : 0.0; }
 static int upload(gs_engine *e, gs_program *p) {
   if (p->dev == e->device) return GS_OK;
   if (p->dev >= 0) return fail(GS_ERR_ARG, "program already bound to another device");
-  CUDA_TRY(cudaMalloc(&p->d_ops, p->ops.size() * 8));
+  // one zero word past END: the interpreters prefetch the next header
+  CUDA_TRY(cudaMalloc(&p->d_ops, (p->ops.size() + 1) * 8));
+  CUDA_TRY(cudaMemset(p->d_ops + p->ops.size(), 0, 8));
   CUDA_TRY(cudaMalloc(&p->d_tables, p->tables.size() * 8));
   CUDA_TRY(cudaMalloc(&p->d_locs, p->locs.size() * 8));
   CUDA_TRY(cudaMemcpy(p->d_ops, p->ops.data(), p->ops.size() * 8, cudaMemcpyHostToDevice));
