@@ -1,0 +1,1166 @@
+// gs_sections.cuh -- section pipeline: shared helpers, narrow_kernel (lane per shot), wide_kernel (warp per shot).
+// Part of gs_kernels.cu (one translation unit; included inside namespace gs).
+#pragma once
+
+// ---------------------------------------------------------------- kernels
+//
+// Execution model: breadth-first SECTIONS.  k is static per op
+// (shot-invariant basis, compiler.py), so the op stream splits on the host
+// into alternating sections of narrow ops (chi dimension k <= GS_KN before
+// and after the op) and wide ops (k > GS_KN, GROW_LIMIT).  One launch per
+// section runs every live shot of the chunk through it:
+//
+//  * narrow_kernel: a warp takes 32 shots (one per lane) and walks the
+//    section with all lanes at the same pc; chi lives in shared memory as
+//    An[j * 32 + lane] (row j uniform across lanes, conflict free); the
+//    fixed per-op cost (decode, sign-mask popcounts, static tables) is paid
+//    once per 32 shots;
+//  * wide_kernel: a warp takes one shot and splits its 2^k coordinates over
+//    the lanes (chi in the warp's shared-memory buffer; `sweep_*`).
+//
+// Shots that survive a section are appended to a global queue (fixed-size
+// slots: state words, record bits, chi of dimension <= GS_KN) read by the
+// next section's launch.  Each launch keeps only its own code hot, which is
+// what the instruction cache needs (B200: 32 KB L1.5).
+// GS_WIDE_ONLY runs the whole program as one wide section (A/B, tests).
+
+#ifndef GS_NARROW_BLOCKS
+#define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
+#endif
+#ifndef GS_WIDE_BLOCKS
+#define GS_WIDE_BLOCKS 3   // <= 168 registers (no spills); shared memory holds 12-13 warps/SM anyway
+#endif
+
+__host__ __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
+  return kind == OP_GROW_LIMIT || k > GS_KN ||
+         (kind == OP_T && (fl & 3u) == T_GROW && k + 1 > GS_KN);
+}
+
+// action of a fired error E = X^ex Z^ez on the static frame:
+// alpha ^= beta, v *= i^xi (-1)^{delta.alpha}; `dm` = delta in coordinates
+struct ErrAct {
+  u64 beta, delt;
+  u32 xi, dm;
+};
+__device__ __noinline__ ErrAct compose_error(const u64 *__restrict__ tables, u64 ex, u64 ez,
+                                             u64 qmask, u64 off, u64 sig_lo, u64 sig_hi) {
+  ErrAct r;
+  r.beta = 0; r.delt = 0; r.xi = 0; r.dm = 0;
+#pragma unroll 1
+  for (u64 rem = ex | ez; rem; rem &= rem - 1) {
+    const u32 q = __ffsll((long long)rem) - 1;
+    const u32 slot = __popcll(qmask & ((1ull << q) - 1ull));
+    const u64 *tb = tables + off + 10ull * slot;
+    const u64 xb_ = __ldg(tb + 0), xd_ = __ldg(tb + 1);
+    const u64 xw64 = __ldg(tb + 4);
+    const u32 xx = (((u32)xw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 2)) ^ par64(sig_hi & __ldg(tb + 3)))) & 3u;
+    const u64 zb_ = __ldg(tb + 5), zd_ = __ldg(tb + 6);
+    const u64 zw64 = __ldg(tb + 9);
+    const u32 zx = (((u32)zw64 & 3u) + 2u * (par64(sig_lo & __ldg(tb + 7)) ^ par64(sig_hi & __ldg(tb + 8)))) & 3u;
+    const u32 xdm = (u32)(xw64 >> 8), zdm = (u32)(zw64 >> 8);
+    const bool hx = (ex >> q) & 1, hz = (ez >> q) & 1;
+    u64 lb, ld; u32 lxi, ldm;
+    if (hx && hz) {   // Y = i X Z
+      lb = xb_ ^ zb_; ld = xd_ ^ zd_; ldm = xdm ^ zdm;
+      lxi = (1u + xx + zx + 2u * par64(xd_ & zb_)) & 3u;
+    } else if (hx) {
+      lb = xb_; ld = xd_; lxi = xx; ldm = xdm;
+    } else {
+      lb = zb_; ld = zd_; lxi = zx; ldm = zdm;
+    }
+    r.xi = (r.xi + lxi + 2u * par64(r.delt & lb)) & 3u;
+    r.beta ^= lb; r.delt ^= ld; r.dm ^= ldm;
+  }
+  return r;
+}
+
+// letter of a fired location from its pick draw u (ref noise.py:68-100)
+__device__ __forceinline__ void noise_letter(u32 nk, u32 qa, u32 qb, double u, u64 &ex, u64 &ez) {
+  if (nk == NK_DEP1) {
+    int code = 1 + (int)(u * 3.0);
+    code = code > 3 ? 3 : code;
+    ex |= (u64)(code != 3) << qa;
+    ez |= (u64)(code != 1) << qa;
+  } else if (nk == NK_DEP2) {
+    int pick = 1 + (int)(u * 15.0);
+    pick = pick > 15 ? 15 : pick;
+    const int ca = pick & 3, cbq = pick >> 2;
+    if (ca) { ex |= (u64)(ca != 3) << qa; ez |= (u64)(ca != 1) << qa; }
+    if (cbq) { ex |= (u64)(cbq != 3) << qb; ez |= (u64)(cbq != 1) << qb; }
+  } else if (nk == NK_XERR) {
+    ex |= 1ull << qa;
+  } else {
+    ez |= 1ull << qa;
+  }
+}
+
+// owning noise instruction of location l: its index sits in bits 50..63 of
+// the location word when the program has < 2^14 noise instructions
+// (compiler.OWNER_LIMIT), else bisect: last m with loc0(m) <= l
+__device__ __forceinline__ const u64 *noise_owner(const DevProg &P, u32 l) {
+  if (P.nnoise <= (1u << 14))
+    return P.tables + P.noise_off + 4ull * (u32)(__ldg(P.locs + 2ull * l) >> 50);
+  u32 lo = 0, hi = P.nnoise;
+  while (hi - lo > 1) {
+    const u32 mid = (lo + hi) >> 1;
+    if ((u32)__ldg(P.tables + P.noise_off + 4ull * mid + 1) <= l) lo = mid; else hi = mid;
+  }
+  return P.tables + P.noise_off + 4ull * lo;
+}
+
+// queue slot layout (u64 words): state, then record bits (u32 words), then
+// the chi rows [0, 2^GS_KN)
+enum { Q_SL = 0, Q_LO, Q_HI, Q_C, Q_OBS, Q_MB, Q_PICK, Q_SEED, Q_CNTK, Q_GEO, Q_FIRE, Q_HDR = 12 };
+
+struct DevSec {
+  u32 pc0, k0, nm0;        // first op, its chi dimension, first noise instr. with ipc >= pc0
+  u32 pc_end;              // narrow: stop before this op (0xFFFFFFFF: at the first wide op)
+  u64 first, count;        // fresh shots (q_in == nullptr): run-local indices [first, first+count)
+  const u64 *q_in;         // else: queue slots and their number
+  const u32 *n_in;
+  u64 *q_out;              // survivors at the section end (nullptr: last section)
+  u32 *n_out;
+  unsigned long long *work; // atomic work counter
+};
+
+// record words of a slot, rounded to 16 B so the chi rows are double2-aligned
+__host__ __device__ __forceinline__ u32 rec_u64(u32 rec_words32) { return ((rec_words32 + 3) / 4) * 2; }
+
+__device__ __forceinline__ u32 slot_u64(const DevProg &P) {
+  return Q_HDR + rec_u64(P.rec_words32) + 2 * (1u << GS_KN);
+}
+
+// per-warp counters in shared memory
+enum { WC_TOT = 0, WC_PRES, WC_DISC, WC_OVF, WC_COR, WC_UNS, WC_ERR, WC_MB, WC_N };
+
+__device__ __forceinline__ void flush_counters(const DevOut &O, unsigned long long *wcnt, u32 lane) {
+  __syncwarp();
+  if (lane < WC_N && wcnt[lane]) {
+    static_assert(WC_N == 8, "counter order");
+    const int dst[WC_N] = {GS_C_TOTAL, GS_C_PRESERVED, GS_C_DISCARDED, GS_C_OVERFLOW,
+                           GS_C_CORRUPT, GS_C_UNSUPPORTED, GS_C_ERROR_SHOTS, GS_C_MODEL_BYTES};
+    atomicAdd((unsigned long long *)O.counters + dst[lane], wcnt[lane]);
+  }
+}
+
+// ---------------------------------------------------------------- narrow
+
+// @region narrow: prologue
+template <bool kPhilox>
+__global__ void __launch_bounds__(128, GS_NARROW_BLOCKS)
+narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
+  extern __shared__ __align__(16) u8 smem[];
+  const u32 lane = threadIdx.x & 31u;
+  const u32 wib = threadIdx.x >> 5;
+  const u32 wpb = blockDim.x >> 5;
+  const u64 gw = (u64)blockIdx.x * wpb + wib;
+  u8 *mine = smem + (size_t)wib * O.warp_bytes;
+  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
+  double2 *An = reinterpret_cast<double2 *>(mine + kCntBytes);
+  // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
+  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kNarrowBytes)
+                            : O.grec + gw * (u64)P.rec_words32 * 32u;
+  const u32 n = P.n;
+  const u64 *__restrict__ ops = P.ops;
+  const u64 *__restrict__ tables = P.tables;
+  const u64 *__restrict__ locs = P.locs;
+  const double2 Z = make_double2(0.0, 0.0);
+  constexpr bool philox = kPhilox;   // RNG mode is a template parameter
+  const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
+  const u32 SU = slot_u64(P);
+#define AN(j) An[(j) * 32u + lane]
+
+  if (lane < WC_N) wcnt[lane] = 0;
+  __syncwarp();
+  const u64 total = S.q_in ? (u64)*S.n_in : S.count;
+
+#pragma unroll 1
+  for (;;) {
+    // @region narrow: batch setup
+    u64 base = 0;
+    if (lane == 0) base = atomicAdd(S.work, 32ull);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= total) break;
+    const u64 idx = base + lane;
+    const bool valid = idx < total;
+    // this lane's shot (ref sampler.py:169-255 state: tableau signs, coset
+    // offset, record, observables)
+    u64 sl = 0, shot = 0, seed = 0;
+    u64 s_lo = 0, s_hi = 0, sc = 0, sobs = 0, smb = 0;
+    u32 scnt = 1, sk = S.k0;
+    int sst = valid ? ST_RUNNING : ST_PRESERVED, saux = -1;
+    // Philox fire schedule of this shot
+    u32 sgj = 0, sgpos = 0xFFFFFFFFu, sfire = 0xFFFFFFFFu;
+    u64 sgpick = 0;
+    if (!S.q_in) {
+      sl = S.first + idx;
+      shot = R.shot_begin + sl;
+      if (valid && !philox) seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
+#pragma unroll 1
+      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
+      AN(0) = make_double2(1.0, 0.0);
+      if (philox && valid && P.geo_len > 1 && P.nlocs) {
+        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, shot, 0u, 0u);
+        sgpos = gc.pos;
+        sgpick = gc.pick;
+        sgj = 1;
+        sfire = sgpos < P.nlocs ? 0u : 0xFFFFFFFFu;
+      }
+    } else if (valid) {
+      const u64 *q = S.q_in + idx * SU;
+      sl = q[Q_SL];
+      shot = R.shot_begin + sl;
+      s_lo = q[Q_LO]; s_hi = q[Q_HI]; sc = q[Q_C]; sobs = q[Q_OBS]; smb = q[Q_MB];
+      sgpick = q[Q_PICK]; seed = q[Q_SEED];
+      scnt = (u32)q[Q_CNTK];
+      sgj = (u32)q[Q_GEO]; sgpos = (u32)(q[Q_GEO] >> 32);
+      sfire = (u32)q[Q_FIRE];
+      const u32 *qr = reinterpret_cast<const u32 *>(q + Q_HDR);
+#pragma unroll 1
+      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = qr[w];
+      const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+      for (u32 j = 0; j < (1u << S.k0); ++j) AN(j) = qc[j];
+    }
+    __syncwarp();
+
+    u32 pc = S.pc0, nm = S.nm0;
+    u32 exit_k = 0;
+#pragma unroll 1
+    for (;;) {
+      if (!__any_sync(FULL, sst == ST_RUNNING)) break;
+      const u64 h = __ldg(ops + pc);
+      const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
+      const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
+      const u32 instr = (u32)(h >> 32);
+      if (pc == S.pc_end || op_is_wide(kind, k, fl)) { exit_k = k; break; }   // section end
+      // ============================== narrow op, lane per shot
+      // @region narrow: noise
+      // apply E to this lane's shot (ref state.py:88-102)
+      auto lane_error = [&](u64 ex, u64 ez, const u64 *nrec, u32 size) {
+        const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3), s_lo, s_hi);
+        const double2 php = ipow(e.xi);
+        const double2 phm = cneg(php);
+        const u32 dcn = par64(e.delt & sc);
+#pragma unroll 1
+        for (u32 j = 0; j < size; ++j) AN(j) = cmul(AN(j), (dcn ^ par32(j & e.dm)) ? phm : php);
+        sc ^= e.beta;
+        smb += 2ull * kEntryBytes * scnt + sign_bytes;
+      };
+      const u64 *op = ops + pc;
+      const u32 size = 1u << k;
+      // ---- noise instructions inserted before this op
+      if (!philox) {
+#pragma unroll 1
+        for (; nm < P.nnoise; ++nm) {
+          const u64 *nrec = tables + P.noise_off + 4ull * nm;
+          const u64 nw0 = __ldg(nrec);
+          if ((u32)nw0 > pc) break;
+          if (sst != ST_RUNNING) continue;
+          const u32 nloc = (u32)(nw0 >> 32), loc0 = (u32)__ldg(nrec + 1);
+          u64 ex = 0, ez = 0;
+#pragma unroll 1
+          for (u32 l = loc0; l < loc0 + nloc; ++l) {
+            const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+            const u32 d = (u32)lw;
+            if ((splitmix(seed, d) >> 11) < thr) {
+              const u32 nk = (u32)(lw >> 48) & 3;
+              const double u = nk <= NK_DEP2 ? (double)(splitmix(seed, d + 1) >> 11) * 0x1.0p-53 : 0.0;
+              noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+            }
+          }
+          if (ex | ez) lane_error(ex, ez, nrec, size);
+        }
+      } else {
+        if (sst == ST_RUNNING && pc >= sfire) {
+          sfire = 0xFFFFFFFFu;
+          while (sgpos < P.nlocs) {
+            const u64 *nrec = noise_owner(P, sgpos);
+            const u64 nw0 = __ldg(nrec);
+            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+            if (ipc > pc) { sfire = ipc; break; }
+            const u32 loc0 = (u32)__ldg(nrec + 1);
+            u64 ex = 0, ez = 0;
+            while (sgpos < loc0 + nloc) {
+              const u32 l = sgpos;
+              bool ok = true;
+              if (!P.noise_uniform) ok = geo_accept(R.master, shot, sgj - 1, __ldg(tables + P.acc_off + l));
+              if (ok) {
+                const u64 lw = __ldg(locs + 2ull * l);
+                noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
+                             (double)sgpick * 0x1.0p-53, ex, ez);
+              }
+              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, shot, sgj, l + 1);
+              sgpos = gc.pos;
+              sgpick = gc.pick;
+              ++sgj;
+            }
+            if (ex | ez) lane_error(ex, ez, nrec, size);
+          }
+        }
+      }
+      pc += len;
+      if (sst != ST_RUNNING) continue;
+      sk = k;
+
+      // @region narrow: T
+      if (kind == OP_T) {
+        s_lo ^= __ldg(op + 1);
+        s_hi ^= __ldg(op + 2);
+        const u32 flip = par64(s_lo & __ldg(op + 3)) ^ par64(s_hi & __ldg(op + 4));
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6);
+        const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
+        const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
+        const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
+        smb += __ldg(op + 11);
+        const double2 bx0 = flip ? cneg(bxs) : bxs;
+        const double2 bx1 = cneg(bx0);
+        const u32 dc = par64(delta & sc);
+        const u32 tcase = fl & 3u;
+        if (tcase == T_DIAG) {
+          // beta == 0: pure phase per entry (ref state.py:120-126)
+          const double2 f0 = cadd(a, bx0), f1 = cadd(a, bx1);
+#pragma unroll 1
+          for (u32 j = 0; j < size; ++j) AN(j) = cmul(AN(j), (dc ^ par32(j & dmask)) ? f1 : f0);
+          smb += 32ull * scnt;
+          continue;
+        }
+        // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
+        const u32 cin = scnt;
+        u32 nz = 0;
+        if (tcase == T_BUTTERFLY) {
+          const u32 hb = 31 - __clz(cb);
+#pragma unroll 1
+          for (u32 m = 0; m < (size >> 1); ++m) {
+            const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+            const double2 v0 = AN(j0), v1 = AN(j1);
+            const u32 s0 = dc ^ par32(j0 & dmask), s1 = dc ^ par32(j1 & dmask);
+            const double2 n0 = prune(cadd(cmul(a, v0), cmul(s1 ? bx1 : bx0, v1)));
+            const double2 n1 = prune(cadd(cmul(a, v1), cmul(s0 ? bx1 : bx0, v0)));
+            AN(j0) = n0;
+            AN(j1) = n1;
+            nz += nonzero(n0) + nonzero(n1);
+          }
+        } else {
+#pragma unroll 1
+          for (u32 j = 0; j < size; ++j) {
+            const double2 v = AN(j);
+            const u32 sj = dc ^ par32(j & dmask);
+            const double2 n0 = prune(cmul(a, v));
+            const double2 n1 = prune(cmul(sj ? bx1 : bx0, v));
+            AN(j) = n0;
+            AN(size + j) = n1;
+            nz += nonzero(n0) + nonzero(n1);
+          }
+          sk = k + 1;
+        }
+        scnt = nz;
+        smb += (u64)kEntryBytes * (cin + nz);
+        if ((u64)nz > R.cap) { sst = ST_OVERFLOW; saux = (int)instr; }
+        else if (nz == 0) { sst = ST_CORRUPT; saux = (int)instr; }
+        continue;
+      }
+
+      // @region narrow: meas
+      if (kind == OP_MEAS) {
+        s_lo ^= __ldg(op + 1);
+        s_hi ^= __ldg(op + 2);
+        const u32 mcase = fl & 3u;
+        const u32 xi0 = (((fl >> 2) & 3u) + 2u * (par64(s_lo & __ldg(op + 3)) ^ par64(s_hi & __ldg(op + 4)))) & 3u;
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
+        const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
+        const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
+        const u64 vec = __ldg(op + 8);
+        const u64 w13 = __ldg(op + 13);
+        const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
+        smb += __ldg(op + 17);
+        const u32 dc = par64(delta & sc);
+        // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
+        // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
+        auto pick_plus = [&](double pplus) -> bool {
+          if (pplus >= 1.0) return true;
+          if (pplus <= 0.0) return false;
+          return (double)draw53(seed, R.master, shot, udraw, philox) * 0x1.0p-53 < pplus;
+        };
+        const u32 cin = scnt;
+        bool plus;
+        u32 nz = 0;
+        if (mcase == M_DET) {
+          // beta == 0: filter by eigenvalue (ref state.py:162-176)
+          const u32 neg0 = (xi0 >> 1) ^ dc;
+          double sp = 0.0, sm = 0.0;
+#pragma unroll 1
+          for (u32 j = 0; j < size; ++j) {
+            const double a2 = abs2(AN(j));
+            if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+          }
+          plus = pick_plus(sp);
+          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+          if (chosen < 1e-12) { sst = ST_CORRUPT; saux = (int)instr; continue; }
+          const u32 want_neg = plus ? 0u : 1u;
+          const double rs = inv_sqrt_norm(plus ? sp : sm);
+          if (fl & MF_COMPACT) {
+            const u32 tau = want_neg ^ neg0;
+#pragma unroll 1
+            for (u32 jp = 0; jp < (size >> 1); ++jp) {
+              const u32 j0 = ins_bit(jp, isq, 0);
+              const double2 v = cscale(AN(j0 | ((tau ^ par32(j0 & dmask)) << isq)), rs);
+              AN(jp) = v;
+              nz += nonzero(v);
+            }
+            if (tau) sc ^= vec;
+            sk = k - 1;
+          } else {
+#pragma unroll 1
+            for (u32 j = 0; j < size; ++j) {
+              const bool keep = (neg0 ^ par32(j & dmask)) == want_neg;
+              const double2 v = keep ? cscale(AN(j), rs) : Z;
+              AN(j) = v;
+              nz += nonzero(v);
+            }
+          }
+        } else {
+          // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
+          const double2 xpp = ipow(xi0);
+          const double2 xpm = cneg(xpp);
+          const u32 ct = (u32)(sc >> t) & 1u;
+          const bool span = mcase == M_PIVOT_SPAN;
+          const u32 npairs = span ? (size >> 1) : size;
+          double sp = 0.0;
+#pragma unroll 1
+          for (u32 m = 0; m < npairs; ++m) {
+            double2 wpv;
+            if (span) {
+              const u32 j0 = ins_bit(m, isq, 0);
+              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+              const u32 part = rep ^ cb;
+              wpv = cadd(AN(rep), cmul((dc ^ par32(part & dmask)) ? xpm : xpp, AN(part)));
+            } else {
+              const double2 v = AN(m);
+              wpv = (ct ^ par32(m & tmask)) ? cadd(Z, cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v)) : v;
+            }
+            sp = __dadd_rn(sp, abs2(wpv));
+          }
+          const double pp = __dmul_rn(0.5, sp);
+          plus = pick_plus(pp);
+          const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+          if (chosen < 1e-12) { sst = ST_CORRUPT; saux = (int)instr; continue; }
+          double sk2 = 0.0;
+#pragma unroll 1
+          for (u32 m = 0; m < npairs; ++m) {
+            double2 w;
+            u32 dst;
+            if (span) {
+              const u32 j0 = ins_bit(m, isq, 0);
+              const u32 rep = j0 | ((ct ^ par32(j0 & tmask)) << isq);
+              const u32 part = rep ^ cb;
+              const double2 prod = cmul((dc ^ par32(part & dmask)) ? xpm : xpp, AN(part));
+              w = plus ? cadd(AN(rep), prod) : csub(AN(rep), prod);
+              dst = rep;
+            } else {
+              const double2 v = AN(m);
+              if (ct ^ par32(m & tmask)) {
+                const double2 prod = cmul((dc ^ par32(m & dmask)) ? xpm : xpp, v);
+                w = plus ? cadd(Z, prod) : csub(Z, prod);
+              } else {
+                w = v;
+              }
+              dst = m;
+            }
+            w = prune(w);
+            AN(dst) = w;
+            sk2 = __dadd_rn(sk2, abs2(w));
+            nz += nonzero(w);
+          }
+          if (nz == 0) { sst = ST_CORRUPT; saux = (int)instr; continue; }
+          const double rs = inv_sqrt_norm(sk2);
+          if (span) {
+#pragma unroll 1
+            for (u32 jp = 0; jp < (size >> 1); ++jp) {
+              const u32 j0 = ins_bit(jp, isq, 0);
+              AN(jp) = cscale(AN(j0 | ((ct ^ par32(j0 & tmask)) << isq)), rs);
+            }
+            sk = k - 1;
+          } else {
+#pragma unroll 1
+            for (u32 j = 0; j < size; ++j) AN(j) = cscale(AN(j), rs);
+          }
+          if (ct) sc ^= vec;
+          // tableau sign update of the pivot (ref tableau.py:176-200)
+          const u32 v = (u32)(s_hi >> t) & 1u;
+          if (v) { s_lo ^= __ldg(op + 9); s_hi ^= __ldg(op + 10); }
+          s_lo ^= __ldg(op + 11);
+          s_hi ^= __ldg(op + 12);
+          s_lo = (s_lo & ~(1ull << t)) | ((u64)v << t);
+          s_hi = (s_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
+        }
+        scnt = nz;
+        smb += (u64)kEntryBytes * (cin + nz);
+        const u32 bout = plus ? 0u : 1u;
+        u32 rb = bout;
+        if ((fl & MF_FLIP) && draw53(seed, R.master, shot, udraw + 1, philox) < __ldg(op + 14)) rb ^= 1u;
+        if ((fl & MF_RECORD) && rb) recb[(slot >> 5) * 32u + lane] |= 1u << (slot & 31);
+        if ((fl & MF_RESET) && bout) { s_lo ^= __ldg(op + 15); s_hi ^= __ldg(op + 16); }
+        continue;
+      }
+
+      // @region narrow: feedback/detector/end
+      if (kind == OP_FEEDBACK) {
+        const u32 idx = (u32)__ldg(op + 1);
+        if ((recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u) {
+          s_lo ^= __ldg(op + 2);
+          s_hi ^= __ldg(op + 3);
+          smb += __ldg(op + 4);
+        }
+        continue;
+      }
+
+      if (kind == OP_DETECTOR || kind == OP_OBSERVABLE) {
+        const u64 w1 = __ldg(op + 1);
+        const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
+        const u64 off = __ldg(op + 2);
+        u32 parity = 0;
+#pragma unroll 1
+        for (u32 i = 0; i < nidx; ++i) {
+          const u32 idx = (u32)__ldg(tables + off + i);
+          parity ^= (recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u;
+        }
+        if (kind == OP_DETECTOR) {
+          if ((R.flags & GS_POSTSELECT) && parity) { sst = ST_DISCARDED; saux = (int)id; }
+        } else {
+          sobs ^= (u64)parity << id;
+        }
+        continue;
+      }
+
+      if (kind == OP_END) {
+        s_lo ^= __ldg(op + 1);
+        s_hi ^= __ldg(op + 2);
+        smb += __ldg(op + 3);
+        sst = ST_PRESERVED;
+        continue;
+      }
+      sst = ST_UNSUPPORTED;  // unknown opcode: fail loudly
+      saux = -2;
+    }
+    __syncwarp();
+
+    // @region narrow: outputs
+    // survivors go to the next (wide) section's queue, in lane order
+    const u32 run = __ballot_sync(FULL, valid && sst == ST_RUNNING);
+    if (run) {
+      u32 o = 0;
+      if (lane == 0) o = atomicAdd(S.n_out, (u32)__popc(run));
+      o = __shfl_sync(FULL, o, 0);
+      if ((run >> lane) & 1u) {
+        u64 *q = S.q_out + (u64)(o + __popc(run & lanemask_lt(lane))) * SU;
+        q[Q_SL] = sl; q[Q_LO] = s_lo; q[Q_HI] = s_hi; q[Q_C] = sc; q[Q_OBS] = sobs;
+        q[Q_MB] = smb; q[Q_PICK] = sgpick; q[Q_SEED] = seed;
+        q[Q_CNTK] = (u64)scnt;
+        q[Q_GEO] = (u64)sgj | ((u64)sgpos << 32);
+        q[Q_FIRE] = sfire;
+        u32 *qr = reinterpret_cast<u32 *>(q + Q_HDR);
+#pragma unroll 1
+        for (u32 w = 0; w < P.rec_words32; ++w) qr[w] = recb[w * 32u + lane];
+        double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+        for (u32 j = 0; j < (1u << exit_k); ++j) qc[j] = AN(j);
+      }
+    }
+    const bool fin = valid && sst != ST_RUNNING;
+    {
+      const u32 pres = __ballot_sync(FULL, fin && sst == ST_PRESERVED);
+      const u32 errb = __ballot_sync(FULL, fin && sst == ST_PRESERVED && sobs != 0);
+      const u32 disc = __ballot_sync(FULL, fin && sst == ST_DISCARDED);
+      const u32 ovf = __ballot_sync(FULL, fin && sst == ST_OVERFLOW);
+      const u32 cor = __ballot_sync(FULL, fin && sst == ST_CORRUPT);
+      const u32 uns = __ballot_sync(FULL, fin && sst == ST_UNSUPPORTED);
+      const u32 val = __ballot_sync(FULL, fin);
+      u64 mb = fin ? smb : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mb += __shfl_xor_sync(FULL, mb, o);
+      if (lane == 0) {
+        wcnt[WC_TOT] += __popc(val);
+        wcnt[WC_PRES] += __popc(pres);
+        wcnt[WC_DISC] += __popc(disc);
+        wcnt[WC_OVF] += __popc(ovf);
+        wcnt[WC_COR] += __popc(cor);
+        wcnt[WC_UNS] += __popc(uns);
+        wcnt[WC_ERR] += __popc(errb);
+        wcnt[WC_MB] += mb;
+      }
+    }
+    if (fin) {
+      if (sst == ST_PRESERVED && sobs) {
+#pragma unroll 1
+        for (u64 o = sobs; o; o &= o - 1)
+          atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
+        if (O.witness) {
+          const u32 wi = atomicAdd(O.witness_count, 1u);
+          if (wi < O.witness_cap) O.witness[wi] = shot;
+        }
+      }
+      if (O.mode != MODE_COUNTERS) {
+        O.status[sl] = (u8)sst;
+        O.aux[sl] = saux;
+        O.obs[sl] = sobs;
+        const u32 rw64 = (P.nmeas + 63) / 64;
+#pragma unroll 1
+        for (u32 w = 0; w < rw64; ++w) {
+          const u32 lo = recb[(2 * w) * 32u + lane];
+          const u32 hi = (2 * w + 1 < P.rec_words32) ? recb[(2 * w + 1) * 32u + lane] : 0u;
+          O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
+        }
+        if (O.mode == MODE_DUMP) {
+          O.sig[2 * sl] = s_lo;
+          O.sig[2 * sl + 1] = s_hi;
+          O.cvec[sl] = sc;
+          O.dim[sl] = sk;
+          const u64 stride = 1ull << P.max_dim;
+#pragma unroll 1
+          for (u32 j = 0; j < (1u << sk); ++j) O.amps[sl * stride + j] = AN(j);
+        }
+      }
+    }
+    __syncwarp();
+  }
+#undef AN
+  flush_counters(O, wcnt, lane);
+}
+
+// ---------------------------------------------------------------- wide
+
+// @region wide: prologue
+template <bool kSmemChi, bool kPhilox>
+__global__ void __launch_bounds__(128, GS_WIDE_BLOCKS)
+wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
+  extern __shared__ __align__(16) u8 smem[];
+  const u32 lane = threadIdx.x & 31u;
+  const u32 wib = threadIdx.x >> 5;
+  const u32 wpb = blockDim.x >> 5;
+  const u64 gw = (u64)blockIdx.x * wpb + wib;
+  u8 *mine = smem + (size_t)wib * O.warp_bytes;
+  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
+  u32 *win = reinterpret_cast<u32 *>(mine + kCntBytes);
+  u32 *recw = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kWinBytes)
+                            : O.grec + gw * (u64)P.rec_words32;
+  double2 *A = kSmemChi ? chi_ptr<true>(reinterpret_cast<double2 *>(mine + O.chi_off))
+                        : O.gchi + gw * ((u64)1 << P.max_dim);
+  const u32 n = P.n;
+  const u64 *__restrict__ ops = P.ops;
+  const u64 *__restrict__ tables = P.tables;
+  const u64 *__restrict__ locs = P.locs;
+  const double2 Z = make_double2(0.0, 0.0);
+  constexpr bool philox = kPhilox;
+  const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
+  const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
+  const u32 SU = slot_u64(P);
+  (void)n;
+
+  if (lane < WC_N) wcnt[lane] = 0;
+  __syncwarp();
+  const u64 total = S.q_in ? (u64)*S.n_in : S.count;
+
+#pragma unroll 1
+  for (;;) {
+    // @region wide: shot setup
+    u64 idx = 0;
+    if (lane == 0) idx = atomicAdd(S.work, 1ull);
+    idx = __shfl_sync(FULL, idx, 0);
+    if (idx >= total) break;
+    Rng rng;
+    rng.philox = philox;
+    rng.master = R.master;
+    u64 sl, sig_lo = 0, sig_hi = 0, c = 0, obs = 0, mbytes = 0, gpick = 0;
+    u32 cnt = 1, gj = 0, gpos = 0xFFFFFFFFu, fire_pc = 0xFFFFFFFFu;
+    const u32 k = S.k0;
+    // chi norm, kept as per-lane partial sums and reduced only when a
+    // deterministic measurement needs it
+    double nrm_l = 0.0;
+    if (!S.q_in) {
+      sl = S.first + idx;
+      rng.shot = R.shot_begin + sl;
+      rng.seed = 0;
+      if (!philox) rng.seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, rng.shot);
+#pragma unroll 1
+      for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
+      if (lane == 0) A[0] = make_double2(1.0, 0.0);
+      nrm_l = lane == 0 ? 1.0 : 0.0;
+      if (philox && P.geo_len > 1 && P.nlocs) {
+        const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, rng.shot, 0u, 0u);
+        gpos = gc.pos;
+        gpick = gc.pick;
+        gj = 1;
+        fire_pc = gpos < P.nlocs ? 0u : 0xFFFFFFFFu;
+      }
+    } else {
+      const u64 *q = S.q_in + idx * SU;
+      sl = q[Q_SL];
+      rng.shot = R.shot_begin + sl;
+      rng.seed = q[Q_SEED];
+      sig_lo = q[Q_LO]; sig_hi = q[Q_HI]; c = q[Q_C]; obs = q[Q_OBS]; mbytes = q[Q_MB];
+      gpick = q[Q_PICK];
+      cnt = (u32)q[Q_CNTK];
+      gj = (u32)q[Q_GEO]; gpos = (u32)(q[Q_GEO] >> 32);
+      fire_pc = (u32)q[Q_FIRE];
+      const u32 *qr = reinterpret_cast<const u32 *>(q + Q_HDR);
+#pragma unroll 1
+      for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = qr[w];
+      // chi in, and its norm (same per-lane order + tree as a sum pass)
+      const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+      for (u32 j = lane; j < (1u << k); j += 32) {
+        const double2 v = qc[j];
+        A[j] = v;
+        nrm_l = __dadd_rn(nrm_l, abs2(v));
+      }
+    }
+    if (!philox) fire_pc = 0xFFFFFFFFu;
+    u32 kcur = k;
+    int status = ST_RUNNING, aux = -1;
+    double ps = 1.0;        // renormalisation pending on A (see ldps)
+    // SplitMix noise scan state: everything inserted before pc0 is applied
+    u32 cursor = P.nlocs;
+    if (S.nm0 < P.nnoise) cursor = (u32)__ldg(tables + P.noise_off + 4ull * S.nm0 + 1);
+    u32 scanned = cursor >> 5, search_w = scanned;
+    u32 next_word_pc = 0xFFFFFFFFu;
+    if (!philox && scanned < P.nwords) next_word_pc = (u32)__ldg(tables + P.wordpc_off + scanned);
+    __syncwarp();
+    u32 wpc = S.pc0;
+    u64 hnext = __ldg(ops + wpc);
+    u32 exit_pc = 0xFFFFFFFFu;
+#pragma unroll 1
+    while (status == ST_RUNNING) {
+      if (!wide_only) {
+        const u32 kind_ = (u32)(hnext & 0xff), k_ = (u32)((hnext >> 16) & 0xff),
+                  fl_ = (u32)((hnext >> 24) & 0xff);
+        if (!op_is_wide(kind_, k_, fl_)) { exit_pc = wpc; break; }
+      }
+      // @region wide: noise
+      if (wpc >= next_word_pc || wpc >= fire_pc) {
+        // apply E = OR of fired letters of one noise instruction
+        // (ref noise.py:68-100, state.py:88-102)
+        auto apply_error = [&](u64 ex, u64 ez, const u64 *nrec) {
+          if (!(ex | ez)) return;
+          const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
+                                         sig_lo, sig_hi);
+          const double2 php = ipow(e.xi);
+          sweep_phase<kSmemChi>(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
+          ps = 1.0;
+          __syncwarp();
+          c ^= e.beta;
+          mbytes += 2ull * kEntryBytes * cnt + sign_bytes;
+        };
+        if (philox) {
+          // walk the candidate schedule (lane-uniform, rare)
+          fire_pc = 0xFFFFFFFFu;
+          while (gpos < P.nlocs) {
+            const u64 *nrec = noise_owner(P, gpos);
+            const u64 nw0 = __ldg(nrec);
+            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+            if (ipc > wpc) { fire_pc = ipc; break; }
+            const u32 loc0 = (u32)__ldg(nrec + 1);
+            u64 ex = 0, ez = 0;
+            while (gpos < loc0 + nloc) {
+              const u32 l = gpos;
+              bool ok = true;
+              if (!P.noise_uniform) ok = geo_accept(R.master, rng.shot, gj - 1, __ldg(tables + P.acc_off + l));
+              if (ok) {
+                const u64 lw = __ldg(locs + 2ull * l);
+                noise_letter((u32)(lw >> 48) & 3, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff,
+                             (double)gpick * 0x1.0p-53, ex, ez);
+              }
+              const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, rng.shot, gj, l + 1);
+              gpos = gc.pos;
+              gpick = gc.pick;
+              ++gj;
+            }
+            apply_error(ex, ez, nrec);
+          }
+        } else {
+          // SplitMix: one fire draw per location, 32 locations per ballot
+          while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= wpc) {
+            const u32 l = scanned * 32u + lane;
+            bool fire = false;
+            if (l < P.nlocs) {
+              const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+              fire = rng.m53((u32)lw) < thr;
+            }
+            const u32 bits = __ballot_sync(FULL, fire);
+            if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+            ++scanned;
+          }
+          __syncwarp();
+          next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
+          fire_pc = 0xFFFFFFFFu;
+#pragma unroll 1
+          for (;;) {
+            // next fired location >= cursor among the scanned words
+            u32 fl_loc = 0xFFFFFFFFu;
+            u32 w = max(search_w, cursor >> 5);
+#pragma unroll 1
+            for (; w < scanned; ++w) {
+              u32 bits = win[w & (kWinWords - 1)];
+              if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
+              if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+            }
+            search_w = w;
+            if (fl_loc == 0xFFFFFFFFu) break;
+            const u64 *nrec = noise_owner(P, fl_loc);
+            const u64 nw0 = __ldg(nrec);
+            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+            if (ipc > wpc) { fire_pc = ipc; break; }
+            const u32 loc0 = (u32)__ldg(nrec + 1);
+            cursor = loc0 + nloc;
+            u64 ex = 0, ez = 0;
+#pragma unroll 1
+            for (u32 i = lane; i < nloc; i += 32) {
+              const u32 l = loc0 + i;
+              if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+              const u64 lw = __ldg(locs + 2ull * l);
+              const u32 nk = (u32)(lw >> 48) & 3;
+              const double u = nk <= NK_DEP2 ? rng.uniform((u32)lw + 1) : 0.0;
+              noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+            }
+            apply_error(warp_or64(ex), warp_or64(ez), nrec);
+          }
+        }
+      }
+
+      // @region wide: dispatch
+      const u64 *op = ops + wpc;
+      const u64 hw = hnext;
+      const u32 wkind = (u32)(hw & 0xff), wlen = (u32)((hw >> 8) & 0xff);
+      const u32 wk = (u32)((hw >> 16) & 0xff), wfl = (u32)((hw >> 24) & 0xff);
+      const u32 winstr = (u32)(hw >> 32);
+      wpc += wlen;
+      hnext = __ldg(ops + wpc);       // prefetch the next header
+      kcur = wk;
+      const u32 size = 1u << wk;
+
+      // @region wide: T
+      if (wkind == OP_T || wkind == OP_GROW_LIMIT) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        // xi0 = xi_s + 2 par(sigma & M); b * i^{xi0} is the host constant
+        // b * i^{xi_s} (an exact swap/negation of b), negated when par = 1
+        const u32 flip = par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4));
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6);
+        const u32 cb = (u32)w6, dmask = (u32)(w6 >> 32);
+        const double2 a = make_double2(dbits(__ldg(op + 7)), dbits(__ldg(op + 8)));
+        const double2 bxs = make_double2(dbits(__ldg(op + 9)), dbits(__ldg(op + 10)));
+        mbytes += __ldg(op + 11);
+        const double2 bx0 = flip ? cneg(bxs) : bxs;
+        const u32 dc = par64(delta & c);
+        const u32 tcase = wfl & 3u;
+        if (tcase == T_DIAG) {
+          // beta == 0: pure phase per entry (ref state.py:120-126); the
+          // factors have modulus 1, the norm is kept
+          sweep_phase<kSmemChi>(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
+          ps = 1.0;
+          __syncwarp();
+          mbytes += 32ull * cnt;
+          continue;
+        }
+        const u32 cin = cnt;
+        if (wkind == OP_GROW_LIMIT) {
+          u32 nz = 0;
+          const double2 bx1 = cneg(bx0);
+#pragma unroll 1
+          for (u32 j = lane; j < size; j += 32) {
+            const double2 v = ldps(A, j, ps);
+            const u32 s_ = dc ^ par32(j & dmask);
+            nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
+            nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
+          }
+          nz = warp_sum_u32(nz);
+          status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
+          aux = (int)winstr;
+          break;
+        }
+        // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
+        if (ps != 1.0) sweep_scale<kSmemChi>(A, size, ps);   // rare: right after a deferral
+        ps = 1.0;
+        if (tcase == T_BUTTERFLY && (wfl & TF_FUSE)) {
+          // this gate and the next one (also a BUTTERFLY at the same k, no
+          // noise between) in one pass
+          const u64 *op2 = ops + wpc;
+          const u64 h2 = hnext;
+          const u32 instr2 = (u32)(h2 >> 32);
+          sig_lo ^= __ldg(op2 + 1);
+          sig_hi ^= __ldg(op2 + 2);
+          const u32 flip2 = par64(sig_lo & __ldg(op2 + 3)) ^ par64(sig_hi & __ldg(op2 + 4));
+          const u64 w62 = __ldg(op2 + 6);
+          Gate g1, g2;
+          g1.a = a; g1.bx0 = bx0; g1.cb = cb; g1.dc = dc; g1.dmask = dmask;
+          g2.a = make_double2(dbits(__ldg(op2 + 7)), dbits(__ldg(op2 + 8)));
+          const double2 bxs2 = make_double2(dbits(__ldg(op2 + 9)), dbits(__ldg(op2 + 10)));
+          g2.bx0 = flip2 ? cneg(bxs2) : bxs2;
+          g2.cb = (u32)w62;
+          g2.dmask = (u32)(w62 >> 32);
+          g2.dc = par64(__ldg(op2 + 5) & c);
+          mbytes += __ldg(op2 + 11);
+          wpc += (u32)((h2 >> 8) & 0xff);
+          hnext = __ldg(ops + wpc);
+          const SumNz2 r2 = sweep_butterfly2<kSmemChi>(A, size >> 2, g1, g2);
+          __syncwarp();
+          const u32 cnt1 = warp_sum_u32(r2.nz1);
+          mbytes += (u64)kEntryBytes * (cin + cnt1);
+          if ((u64)cnt1 > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
+          if (cnt1 == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          cnt = warp_sum_u32(r2.nz);
+          nrm_l = r2.sum;
+          mbytes += (u64)kEntryBytes * (cnt1 + cnt);
+          if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr2; break; }
+          if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr2; break; }
+          continue;
+        }
+        SumNz r;
+        if (tcase == T_BUTTERFLY) {
+          r = sweep_butterfly<kSmemChi>(A, size >> 1, cb, dc, dmask, a, bx0);
+        } else {
+          r = sweep_grow<kSmemChi>(A, size, dc, dmask, a, bx0);
+          kcur = wk + 1;
+        }
+        __syncwarp();
+        cnt = warp_sum_u32(r.nz);
+        nrm_l = r.sum;
+        mbytes += (u64)kEntryBytes * (cin + cnt);
+        if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
+        if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+        continue;
+      }
+
+      // @region wide: meas
+      if (wkind == OP_MEAS) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        const u32 mcase = wfl & 3u;
+        const u32 xi0 = (((wfl >> 2) & 3u) + 2u * (par64(sig_lo & __ldg(op + 3)) ^ par64(sig_hi & __ldg(op + 4)))) & 3u;
+        const u64 delta = __ldg(op + 5);
+        const u64 w6 = __ldg(op + 6), w7 = __ldg(op + 7);
+        const u32 dmask = (u32)w6, tmask = (u32)(w6 >> 32);
+        const u32 cb = (u32)w7, t = (u32)(w7 >> 32) & 0xff, isq = (u32)(w7 >> 40) & 0xff;
+        const u64 vec = __ldg(op + 8);
+        const u64 w13 = __ldg(op + 13);
+        const u32 slot = (u32)w13, udraw = (u32)(w13 >> 32);
+        mbytes += __ldg(op + 17);
+        const u32 dc = par64(delta & c);
+        // u < P+ with u in [0, 1-2^-53]: P+ >= 1 or P+ <= 0 decide without
+        // drawing (exact); otherwise draw u (ref sampler.py:262, state.py:168)
+        auto pick_plus = [&](double pplus) -> bool {
+          if (pplus >= 1.0) return true;
+          if (pplus <= 0.0) return false;
+          return rng.uniform(udraw) < pplus;
+        };
+        // a renormalisation by rs that needs no data movement: deferred to
+        // the next pass over chi (ldps); nonzero count unchanged
+        auto defer_scale = [&](double rs, double kept) {
+          if (ps != 1.0) sweep_scale<kSmemChi>(A, size, ps);
+          ps = rs;
+          nrm_l = lane == 0 ? __dmul_rn(__dmul_rn(kept, rs), rs) : 0.0;
+        };
+        const u32 cin = cnt;
+        bool plus;
+        if (mcase == M_DET) {
+          // beta == 0: filter by eigenvalue (ref state.py:162-176)
+          const u32 neg0 = (xi0 >> 1) ^ dc;
+          double sp, sm;
+          if (dmask == 0) {
+            // every coordinate has eigenvalue (-1)^neg0: P+ is the norm
+            const double nrm = warp_sum(nrm_l);
+            sp = neg0 ? 0.0 : nrm;
+            sm = neg0 ? nrm : 0.0;
+          } else {
+            const double2 part = sweep_det_sums<kSmemChi>(A, size, dmask, neg0, ps);
+            sp = warp_sum(part.x);
+            sm = warp_sum(part.y);
+          }
+          plus = pick_plus(sp);
+          const double chosen = plus ? sp : __dsub_rn(1.0, sp);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          const u32 want_neg = plus ? 0u : 1u;
+          const double rs = inv_sqrt_norm(plus ? sp : sm);
+          if (wfl & MF_COMPACT) {
+            const u32 tau = want_neg ^ neg0;
+            const SumNz r = sweep_compact<kSmemChi>(A, size >> 1, isq, dmask, tau, rs, ps);
+            ps = 1.0;
+            __syncwarp();
+            cnt = warp_sum_u32(r.nz);
+            nrm_l = r.sum;
+            if (tau) c ^= vec;
+            kcur = wk - 1;
+          } else if ((plus ? sm : sp) == 0.0) {
+            // the other eigenspace is empty: the filter is a pure
+            // renormalisation
+            defer_scale(rs, plus ? sp : sm);
+          } else {
+            const SumNz r = sweep_filter<kSmemChi>(A, size, dmask, neg0, want_neg, rs, ps);
+            ps = 1.0;
+            __syncwarp();
+            cnt = warp_sum_u32(r.nz);
+            nrm_l = r.sum;
+          }
+        } else {
+          // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
+          PivotGeo g;
+          g.span = mcase == M_PIVOT_SPAN;
+          g.npairs = g.span ? (size >> 1) : size;
+          g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
+          g.dc = dc; g.dmask = dmask;
+          const double2 xpp = ipow(xi0);   // i^xi0, exact
+          const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p<kSmemChi>(A, g, xpp, ps)));
+          plus = pick_plus(pp);
+          const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          const SumNz w = sweep_pivot_w<kSmemChi>(A, g, xpp, plus, ps);
+          ps = 1.0;
+          __syncwarp();
+          const double sk = warp_sum(w.sum);
+          cnt = warp_sum_u32(w.nz);
+          if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+          const double rs = inv_sqrt_norm(sk);
+          if (g.span) {
+            const SumNz r = sweep_compact<kSmemChi>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+            __syncwarp();
+            cnt = warp_sum_u32(r.nz);
+            nrm_l = r.sum;
+            kcur = wk - 1;
+          } else {
+            defer_scale(rs, sk);
+          }
+          if (g.ct) c ^= vec;
+          // tableau sign update of the pivot (ref tableau.py:176-200)
+          const u32 v = (u32)(sig_hi >> t) & 1u;
+          if (v) { sig_lo ^= __ldg(op + 9); sig_hi ^= __ldg(op + 10); }
+          sig_lo ^= __ldg(op + 11);
+          sig_hi ^= __ldg(op + 12);
+          sig_lo = (sig_lo & ~(1ull << t)) | ((u64)v << t);
+          sig_hi = (sig_hi & ~(1ull << t)) | ((u64)(plus ? 0u : 1u) << t);
+        }
+        mbytes += (u64)kEntryBytes * (cin + cnt);
+        const u32 bout = plus ? 0u : 1u;
+        u32 rb = bout;
+        if ((wfl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
+        if (wfl & MF_RECORD) {
+          if (lane == 0 && rb) recw[slot >> 5] |= 1u << (slot & 31);
+          __syncwarp();
+        }
+        if ((wfl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
+        continue;
+      }
+
+      // @region wide: feedback/detector/end
+      if (wkind == OP_FEEDBACK) {
+        const u32 idx = (u32)__ldg(op + 1);
+        if ((recw[idx >> 5] >> (idx & 31)) & 1u) {
+          sig_lo ^= __ldg(op + 2);
+          sig_hi ^= __ldg(op + 3);
+          mbytes += __ldg(op + 4);
+        }
+        continue;
+      }
+      if (wkind == OP_DETECTOR || wkind == OP_OBSERVABLE) {
+        const u64 w1 = __ldg(op + 1);
+        const u32 id = (u32)w1, nidx = (u32)(w1 >> 32);
+        const u64 off = __ldg(op + 2);
+        u32 bb = 0;
+#pragma unroll 1
+        for (u32 i = lane; i < nidx; i += 32) {
+          const u32 idx = (u32)__ldg(tables + off + i);
+          bb ^= (recw[idx >> 5] >> (idx & 31)) & 1u;
+        }
+        const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
+        if (wkind == OP_DETECTOR) {
+          if ((R.flags & GS_POSTSELECT) && parity) { status = ST_DISCARDED; aux = (int)id; }
+        } else {
+          obs ^= (u64)parity << id;
+        }
+        continue;
+      }
+      if (wkind == OP_END) {
+        sig_lo ^= __ldg(op + 1);
+        sig_hi ^= __ldg(op + 2);
+        mbytes += __ldg(op + 3);
+        status = ST_PRESERVED;
+        break;
+      }
+      status = ST_UNSUPPORTED;  // unknown opcode: fail loudly
+      aux = -2;
+    }
+    // @region wide: outputs
+    __syncwarp();
+    if (status == ST_RUNNING) {
+      // survivor: hand it to the next (narrow) section's queue
+      u32 o = 0;
+      if (lane == 0) o = atomicAdd(S.n_out, 1u);
+      o = __shfl_sync(FULL, o, 0);
+      u64 *q = S.q_out + (u64)o * SU;
+      if (lane == 0) {
+        q[Q_SL] = sl; q[Q_LO] = sig_lo; q[Q_HI] = sig_hi; q[Q_C] = c; q[Q_OBS] = obs;
+        q[Q_MB] = mbytes; q[Q_PICK] = gpick; q[Q_SEED] = rng.seed;
+        q[Q_CNTK] = (u64)cnt;
+        q[Q_GEO] = (u64)gj | ((u64)gpos << 32);
+        q[Q_FIRE] = fire_pc;
+      }
+      u32 *qr = reinterpret_cast<u32 *>(q + Q_HDR);
+#pragma unroll 1
+      for (u32 w = lane; w < P.rec_words32; w += 32) qr[w] = recw[w];
+      double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+#pragma unroll 1
+      for (u32 j = lane; j < (1u << kcur); j += 32) qc[j] = ldps(A, j, ps);
+      (void)exit_pc;
+    } else {
+      if (lane == 0) {
+        wcnt[WC_TOT] += 1;
+        wcnt[WC_MB] += mbytes;
+        if (status == ST_PRESERVED) {
+          wcnt[WC_PRES] += 1;
+          if (obs) {
+            wcnt[WC_ERR] += 1;
+#pragma unroll 1
+            for (u64 o = obs; o; o &= o - 1)
+              atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
+            if (O.witness) {
+              const u32 wi = atomicAdd(O.witness_count, 1u);
+              if (wi < O.witness_cap) O.witness[wi] = rng.shot;
+            }
+          }
+        } else if (status == ST_DISCARDED) wcnt[WC_DISC] += 1;
+        else if (status == ST_OVERFLOW) wcnt[WC_OVF] += 1;
+        else if (status == ST_CORRUPT) wcnt[WC_COR] += 1;
+        else wcnt[WC_UNS] += 1;
+      }
+      if (O.mode != MODE_COUNTERS) {
+        if (lane == 0) {
+          O.status[sl] = (u8)status;
+          O.aux[sl] = aux;
+          O.obs[sl] = obs;
+        }
+        const u32 rw64 = (P.nmeas + 63) / 64;
+#pragma unroll 1
+        for (u32 w = lane; w < rw64; w += 32) {
+          const u32 lo = recw[2 * w];
+          const u32 hi = (2 * w + 1 < P.rec_words32) ? recw[2 * w + 1] : 0u;
+          O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
+        }
+        if (O.mode == MODE_DUMP) {
+          if (lane == 0) {
+            O.sig[2 * sl] = sig_lo;
+            O.sig[2 * sl + 1] = sig_hi;
+            O.cvec[sl] = c;
+            O.dim[sl] = kcur;
+          }
+          const u64 stride = 1ull << P.max_dim;
+#pragma unroll 1
+          for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = ldps(A, j, ps);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  flush_counters(O, wcnt, lane);
+}

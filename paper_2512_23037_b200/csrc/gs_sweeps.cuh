@@ -1,0 +1,312 @@
+// gs_sweeps.cuh -- warp-cooperative passes over a dense chi array (wide sections).
+// Part of gs_kernels.cu (one translation unit; included inside namespace gs).
+#pragma once
+
+// @region sweeps
+// ---------------------------------------------------------------- wide sweeps
+//
+// Warp-cooperative passes over a dense chi array A[0, 2^k): lane l takes
+// coordinates l, l+32, ... (pair / group indices for the T sweeps), one
+// group in flight per lane -- measured on the B200, more per lane (unrolled
+// rounds, 8-element groups of three fused gates) was slower every time
+// (profiles/README.md).  Inlined into wide_kernel (+1.4 % over out-of-line
+// copies once each section kernel has its own code).  Per-lane partial
+// results (nonzero count, sum of |v|^2 of the written entries = the chi
+// norm the next deterministic measurement needs); callers reduce across
+// the warp.
+
+struct SumNz {
+  double sum;
+  u32 nz;
+};
+
+// A[i] with a renormalisation still pending (ps != 1): the reference would
+// have stored v * ps (ref state.py:311), so every reader applies it first --
+// the same rounding, one pass later
+__device__ __forceinline__ double2 ldps(const double2 *__restrict__ A, u32 i, double ps) {
+  const double2 v = A[i];
+  return ps != 1.0 ? cscale(v, ps) : v;
+}
+// prune at |v| <= 1e-12 (ref state.py:298), accumulating |v|^2 of the kept
+__device__ __forceinline__ double2 prune_acc(double2 v, double &sum, u32 &nz) {
+  const double q = abs2(v);
+  if (q > kPrune2) {
+    sum = __dadd_rn(sum, q);
+    nz += 1;
+    return v;
+  }
+  return make_double2(0.0, 0.0);
+}
+
+// The T sweeps are the hottest code (about half of all instructions): chi
+// is addressed as shared memory when it lives there (LDS/STS instead of
+// generic loads), and the per-coordinate sign (-1)^s of the b-term is applied
+// to the product b*v by flipping sign bits -- cmul(-b, v) == -cmul(b, v)
+// bit for bit, since fma(-x, y, -z) == -fma(x, y, z).
+template <bool kS>
+__device__ __forceinline__ double2 *chi_ptr(double2 *A) {
+  if (!kS) return A;
+  extern __shared__ __align__(16) u8 smem_dyn[];
+  return reinterpret_cast<double2 *>(smem_dyn + (reinterpret_cast<u8 *>(A) - smem_dyn));
+}
+__device__ __forceinline__ double2 neg_if(double2 v, u32 s) {
+  const long long m = (long long)s << 63;
+  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ m),
+                      __longlong_as_double(__double_as_longlong(v.y) ^ m));
+}
+
+// T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
+// 294-306: a-term then b-term); no renormalisation pending (caller)
+template <bool kS>
+__device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32 dc, u32 dmask,
+                                              double2 a, double2 bx0) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  const u32 hb = 31 - __clz(cb);
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+  const u32 jl = ins_bit(lane, hb, 0);
+  const u32 pl = dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
+#pragma unroll 1
+  for (u32 m = lane; m < half; m += 32) {
+    const u32 jr = ins_bit(m & ~31u, hb, 0);
+    const u32 j0 = jr | jl, j1 = j0 ^ cb;
+    const double2 v0 = A[j0], v1 = A[j1];
+    const u32 s0 = pl ^ par32(jr & dmask), s1 = s0 ^ pcb;
+    A[j0] = prune_acc(cadd(cmul(a, v0), neg_if(cmul(bx0, v1), s1)), r.sum, r.nz);
+    A[j1] = prune_acc(cadd(cmul(a, v1), neg_if(cmul(bx0, v0), s0)), r.sum, r.nz);
+  }
+  return r;
+}
+
+// Two consecutive T gates with partner vectors cb1 != cb2 (compiler flag
+// TF_FUSE): one pass over the 4-element groups {x, x^cb1, x^cb2,
+// x^cb1^cb2}; gate 1 on the cb1 pairs, prune, gate 2 on the cb2 pairs,
+// prune -- exactly the two single-gate passes' arithmetic, half the memory
+// traffic and index work.  Groups are enumerated by inserting zeros at the
+// pivot bits h1 = top(cb1) and h2 = top(cb2 reduced by cb1).
+struct Gate {
+  double2 a, bx0;
+  u32 cb, dc, dmask;
+};
+struct SumNz2 {
+  double sum;
+  u32 nz, nz1;
+};
+template <bool kS>
+__device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g1, Gate g2) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  const u32 h1 = 31 - __clz(g1.cb);
+  const u32 cr = ((g2.cb >> h1) & 1u) ? (g2.cb ^ g1.cb) : g2.cb;
+  const u32 h2 = 31 - __clz(cr);
+  const u32 plo = min(h1, h2), phi = max(h1, h2);
+  SumNz2 r;
+  r.sum = 0.0;
+  r.nz = 0;
+  r.nz1 = 0;
+  double dummy = 0.0;
+  // sign parities: the zero-insertion J is bitwise linear, so for
+  // m = 32r + lane, par(J(m) & mask) = par(J(32r) & mask) ^ par(J(lane) & mask)
+  // (a per-round and a per-lane term); the group members differ by cb1, cb2
+  const u32 jl = ins_bit(ins_bit(lane, plo, 0), phi, 0);
+  const u32 l1 = g1.dc ^ par32(jl & g1.dmask), l2 = g2.dc ^ par32(jl & g2.dmask);
+  const u32 a1 = par32(g1.cb & g1.dmask), b1 = par32(g2.cb & g1.dmask);
+  const u32 a2 = par32(g1.cb & g2.dmask), b2 = par32(g2.cb & g2.dmask);
+#pragma unroll 1
+  for (u32 m = lane; m < quarter; m += 32) {
+    const u32 jr = ins_bit(ins_bit(m & ~31u, plo, 0), phi, 0);
+    const u32 x0 = jr | jl;
+    const u32 x1 = x0 ^ g1.cb, x2 = x0 ^ g2.cb, x3 = x1 ^ g2.cb;
+    const double2 v0 = A[x0], v1 = A[x1], v2 = A[x2], v3 = A[x3];
+    const u32 p1 = l1 ^ par32(jr & g1.dmask), p2 = l2 ^ par32(jr & g2.dmask);
+    // gate 1: pairs (x0, x1), (x2, x3)
+    const u32 s0 = p1, s1 = p1 ^ a1, s2 = p1 ^ b1, s3 = p1 ^ a1 ^ b1;
+    const double2 u0 = prune_acc(cadd(cmul(g1.a, v0), neg_if(cmul(g1.bx0, v1), s1)), dummy, r.nz1);
+    const double2 u1 = prune_acc(cadd(cmul(g1.a, v1), neg_if(cmul(g1.bx0, v0), s0)), dummy, r.nz1);
+    const double2 u2 = prune_acc(cadd(cmul(g1.a, v2), neg_if(cmul(g1.bx0, v3), s3)), dummy, r.nz1);
+    const double2 u3 = prune_acc(cadd(cmul(g1.a, v3), neg_if(cmul(g1.bx0, v2), s2)), dummy, r.nz1);
+    // gate 2: pairs (x0, x2), (x1, x3)
+    const u32 t0 = p2, t1 = p2 ^ a2, t2 = p2 ^ b2, t3 = p2 ^ a2 ^ b2;
+    A[x0] = prune_acc(cadd(cmul(g2.a, u0), neg_if(cmul(g2.bx0, u2), t2)), r.sum, r.nz);
+    A[x2] = prune_acc(cadd(cmul(g2.a, u2), neg_if(cmul(g2.bx0, u0), t0)), r.sum, r.nz);
+    A[x1] = prune_acc(cadd(cmul(g2.a, u1), neg_if(cmul(g2.bx0, u3), t3)), r.sum, r.nz);
+    A[x3] = prune_acc(cadd(cmul(g2.a, u3), neg_if(cmul(g2.bx0, u1), t1)), r.sum, r.nz);
+  }
+  (void)dummy;
+  return r;
+}
+
+// T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
+template <bool kS>
+__device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmask, double2 a,
+                                         double2 bx0) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+#pragma unroll 1
+  for (u32 j = lane; j < size; j += 32) {
+    const double2 v = A[j];
+    A[j] = prune_acc(cmul(a, v), r.sum, r.nz);
+    A[size + j] = prune_acc(neg_if(cmul(bx0, v), dc ^ par32(j & dmask)), r.sum, r.nz);
+  }
+  return r;
+}
+
+// diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
+// fired noise Paulis)
+template <bool kS>
+__device__ __forceinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask,
+                                         double2 f0, double2 f1, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+#pragma unroll 1
+  for (u32 j = lane; j < size; j += 32)
+    A[j] = cmul(ldps(A, j, ps), (dc ^ par32(j & mask)) ? f1 : f0);
+}
+
+// beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
+template <bool kS>
+__device__ __forceinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask, u32 neg0,
+                                               double ps) {
+  const double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  double sp = 0.0, sm = 0.0;
+#pragma unroll 1
+  for (u32 j = lane; j < size; j += 32) {
+    const double a2 = abs2(ldps(A, j, ps));
+    if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+  }
+  return make_double2(sp, sm);
+}
+
+// keep the chosen eigen-entries, scaled by rs; zero the others
+template <bool kS>
+__device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32 neg0,
+                                           u32 want_neg, double rs, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+#pragma unroll 1
+  for (u32 j = lane; j < size; j += 32) {
+    const double2 v = ldps(A, j, ps);
+    if ((neg0 ^ par32(j & dmask)) == want_neg) {
+      const double2 w = cscale(v, rs);
+      A[j] = w;
+      r.sum = __dadd_rn(r.sum, abs2(w));
+      r.nz += nonzero(w);
+    } else {
+      A[j] = make_double2(0.0, 0.0);
+    }
+  }
+  return r;
+}
+
+// in-place compaction dropping coordinate isq: A[jp] = rs * A[src(jp)],
+// src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
+// at isq; src(jp) >= jp, so reads of a round finish before its writes
+template <bool kS>
+__device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
+                                            double rs, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+#pragma unroll 1
+  for (u32 b0 = 0; b0 < half; b0 += 32) {
+    const u32 jp = b0 + lane;
+    double2 v = make_double2(0.0, 0.0);
+    if (jp < half) {
+      const u32 j0 = ins_bit(jp, isq, 0);
+      v = ldps(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
+    }
+    __syncwarp();
+    if (jp < half) {
+      const double2 w = cscale(v, rs);
+      A[jp] = w;
+      r.sum = __dadd_rn(r.sum, abs2(w));
+      r.nz += nonzero(w);
+    }
+    __syncwarp();
+  }
+  return r;
+}
+
+// pivot measurement (ref state.py:178-208): w(m) = rep + sg * xi * part.
+// span: pairs (rep, rep^cb), rep = j0 | ((ct ^ par(j0 & tmask)) << isq);
+// no span: every entry, entries with ct ^ par(m & tmask) are `part` only.
+// pass 1 returns the per-lane sum of |w+|^2; pass 2 writes prune(w_sg) to
+// the rep slot and returns (sum |w|^2, nonzeros).
+struct PivotGeo {
+  u32 npairs, isq, tmask, ct, cb, dc, dmask;
+  bool span;
+};
+__device__ __forceinline__ void pivot_terms(const double2 *__restrict__ A, const PivotGeo &g,
+                                            double2 xpp, u32 m, double2 &vr, double2 &pr,
+                                            u32 &dst, double ps) {
+  const double2 xpm = cneg(xpp);
+  if (g.span) {
+    const u32 j0 = ins_bit(m, g.isq, 0);
+    const u32 rep = j0 | ((g.ct ^ par32(j0 & g.tmask)) << g.isq);
+    const u32 part = rep ^ g.cb;
+    vr = ldps(A, rep, ps);
+    pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, ldps(A, part, ps));
+    dst = rep;
+  } else {
+    const double2 v = ldps(A, m, ps);
+    if (g.ct ^ par32(m & g.tmask)) {
+      vr = make_double2(0.0, 0.0);
+      pr = cmul((g.dc ^ par32(m & g.dmask)) ? xpm : xpp, v);
+    } else {
+      vr = v;
+      pr = make_double2(-0.0, -0.0);   // v + (-0) == v exactly
+    }
+    dst = m;
+  }
+}
+template <bool kS>
+__device__ __forceinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2 xpp, double ps) {
+  const double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  double sp = 0.0;
+#pragma unroll 1
+  for (u32 m = lane; m < g.npairs; m += 32) {
+    double2 vr, pr;
+    u32 d_;
+    pivot_terms(A, g, xpp, m, vr, pr, d_, ps);
+    sp = __dadd_rn(sp, abs2(cadd(vr, pr)));
+  }
+  return sp;
+}
+template <bool kS>
+__device__ __forceinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 xpp, bool plus,
+                                            double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+#pragma unroll 1
+  for (u32 m = lane; m < g.npairs; m += 32) {
+    double2 vr, pr;
+    u32 dst;
+    pivot_terms(A, g, xpp, m, vr, pr, dst, ps);
+    A[dst] = prune_acc(plus ? cadd(vr, pr) : csub(vr, pr), r.sum, r.nz);
+  }
+  return r;
+}
+
+// apply a pending renormalisation in place: A[j] = ps * A[j]
+template <bool kS>
+__device__ __forceinline__ void sweep_scale(double2 *A_, u32 size, double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = threadIdx.x & 31u;
+#pragma unroll 1
+  for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], ps);
+}

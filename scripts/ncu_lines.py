@@ -5,6 +5,9 @@ by instruction offset against ``nvdisasm -g`` of the locally built cubin
 
     ncu -i prof.ncu-rep --page source --csv --print-source sass > sass.csv
     python scripts/ncu_lines.py sass.csv [lib.so] [top]
+
+Lines are (file, line) of the outermost inlined call site; regions are the
+``// @region`` markers of each csrc file (scripts/_srcmap.py).
 """
 import csv
 import os
@@ -14,7 +17,8 @@ import sys
 import tempfile
 from collections import defaultdict
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _srcmap import ROOT, parse_loc, region, source_line  # noqa: E402
 
 
 def disasm(lib, kernel_regex):
@@ -37,9 +41,9 @@ def disasm(lib, kernel_regex):
         if ln.strip().startswith("//##"):
             # innermost-first chain "line A inlined at ... line B": keep the
             # outermost call site (the kernel body line)
-            nums = re.findall(r'line (\d+)', ln)
-            if nums:
-                cur_line = int(nums[-1])
+            loc = parse_loc(ln)
+            if loc:
+                cur_line = loc
             continue
         g = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
         if g:
@@ -111,22 +115,11 @@ def main():
     ts, te = sum(by_line_s.values()), sum(by_line_e.values())
     print("instructions %d, opcode mismatches %d, samples %.0f, warp-instr %.3g" %
           (len(data), mism, ts, te))
-    src_lines = open(os.path.join(ROOT, "paper_2512_23037_b200", "csrc",
-                                  "gs_kernels.cu")).read().splitlines()
-    marks = [(i + 1, m.group(1).strip()) for i, l in enumerate(src_lines)
-             for m in [re.search(r"//\s*@region\s+(.*)$", l)] if m]
-    regions = [(a, (marks[i + 1][0] - 1) if i + 1 < len(marks) else 10 ** 9, nm)
-               for i, (a, nm) in enumerate(marks)]
-    if not regions:
-        regions = [(1, 10 ** 9, "all")]
     agg_s, agg_e = defaultdict(float), defaultdict(float)
-    for line in by_line_s:
-        name = "?"
-        for a, b, nm in regions:
-            if line and a <= line <= b:
-                name = nm
-        agg_s[name] += by_line_s[line]
-        agg_e[name] += by_line_e[line]
+    for loc in by_line_s:
+        name = region(loc)
+        agg_s[name] += by_line_s[loc]
+        agg_e[name] += by_line_e[loc]
     for nm in sorted(agg_s, key=lambda k: -agg_s[k]):
         print("%-28s %6.2f%% samp %6.2f%% inst" % (nm, 100 * agg_s[nm] / ts, 100 * agg_e[nm] / te))
     fm = functions(lib, kre)
@@ -139,11 +132,11 @@ def main():
     for f in sorted(fs, key=lambda k: -fs[k]):
         print("%-28s %6.2f%% samp %6.2f%% inst" % (f, 100 * fs[f] / ts, 100 * fe[f] / te))
     print("-- per source line")
-    src = open(os.path.join(ROOT, "paper_2512_23037_b200", "csrc", "gs_kernels.cu")).read().splitlines()
-    for line in sorted(by_line_s, key=lambda k: -by_line_s[k])[:top]:
-        txt = src[line - 1].strip()[:80] if line else "?"
-        print("%5s %6.2f%% samp %6.2f%% inst  %s" % (line, 100 * by_line_s[line] / ts,
-                                                     100 * by_line_e[line] / te, txt))
+    for loc in sorted(by_line_s, key=lambda k: -by_line_s[k])[:top]:
+        where = "%s:%d" % loc if loc else "?"
+        print("%-22s %6.2f%% samp %6.2f%% inst  %s" % (where, 100 * by_line_s[loc] / ts,
+                                                       100 * by_line_e[loc] / te,
+                                                       source_line(loc)[:80]))
 
 
 if __name__ == "__main__":

@@ -1,5 +1,6 @@
-"""Static SASS size per @region of gs_kernels.cu (nvdisasm -gi line info,
-outermost inlined call site):  python scripts/sass_regions.py [lib.so]"""
+"""Static SASS size per @region of the csrc files (nvdisasm -gi line info,
+outermost inlined call site):  GS_KERNEL=<mangled substring>
+python scripts/sass_regions.py [lib.so]"""
 import os
 import re
 import subprocess
@@ -7,7 +8,8 @@ import sys
 import tempfile
 from collections import Counter
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _srcmap import ROOT, parse_loc, region  # noqa: E402
 lib = os.path.abspath(sys.argv[1] if len(sys.argv) > 1 else os.path.join(
     ROOT, "paper_2512_23037_b200", "libgstab_sm100a.so"))
 tmp = tempfile.mkdtemp()
@@ -15,28 +17,19 @@ subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, check=True, capture_
 cub = sorted(os.listdir(tmp))[0]
 out = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True,
                      text=True).stdout
-src = open(os.path.join(ROOT, "paper_2512_23037_b200", "csrc", "gs_kernels.cu")).read().splitlines()
-marks = [(i + 1, m.group(1).strip()) for i, l in enumerate(src)
-         for m in [re.search(r"//\s*@region\s+(.*)$", l)] if m]
-def region(line):
-    name = "?"
-    for a, nm in marks:
-        if line and line >= a:
-            name = nm
-    return name
 cnt = Counter()
 cur = None
 inside = False
 for ln in out.splitlines():
     if ln.startswith("//---") and ".text." in ln:
-        inside = os.environ.get("GS_KERNEL", "sample_kernelILb1ELb1E") in ln
+        inside = os.environ.get("GS_KERNEL", "wide_kernelILb1ELb1E") in ln
         continue
     if not inside:
         continue
     if ln.strip().startswith("//##"):
-        nums = re.findall(r"line (\d+)", ln)
-        if nums:
-            cur = int(nums[-1])
+        loc = parse_loc(ln)
+        if loc:
+            cur = loc
         continue
     if re.match(r"\s+/\*[0-9a-f]{4,}\*/", ln):
         cnt[region(cur)] += 1
