@@ -65,13 +65,15 @@ WORKLOADS = {
     "msc_d5_2check": ("msc_d5_2check_proxy", lambda m: m.msc_circuit(5)),
     # BASELINE config 2
     "msc_d3": ("msc_d3_proxy", lambda m: m.msc_circuit(3)),
-    # BASELINE config 3
+    # BASELINE config 3 (quoted at p=5e-4: see DEFAULT_P)
     "injection_d3": ("d3_injection_3_rounds", lambda m: m.injection_circuit(3, 3)),
     # BASELINE config 1 and two points of the config-4 sweep
     "config1": ("config1_random_n8_t4", lambda m: m.config1_circuit(1)),
     "config4_n32_t24": ("config4_random_n32_t24", lambda m: m.config4_circuit(32, 24, seed=56)),
     "config4_n64_t32": ("config4_random_n64_t32", lambda m: m.config4_circuit(64, 32, seed=96)),
 }
+# noise strength each BASELINE config is quoted at (others: 1e-3)
+DEFAULT_P = {"injection_d3": 5e-4}
 
 
 def _workload(key: str, p: float):
@@ -165,7 +167,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--shots-per-step", type=int, default=1 << 24)
     ap.add_argument("--workload", default="msc_d5", choices=sorted(WORKLOADS))
-    ap.add_argument("--p", type=float, default=1e-3)
+    ap.add_argument("--p", type=float, default=None,
+                    help="depolarizing strength (default: the workload's BASELINE p)")
     ap.add_argument("--rng", default="philox", choices=["philox", "splitmix"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -180,6 +183,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.p is None:
+        args.p = DEFAULT_P.get(args.workload, 1e-3)
     workload, prog, stats = _workload(args.workload, args.p)
     config = {"workload": workload, "noise_p": args.p, "postselect": True,
               "rng": args.rng, "shots_per_step_per_gpu": args.shots_per_step,
