@@ -268,10 +268,11 @@ struct KernelCfg {
 
 // warps per block = the most resident warps per SM; grid = SMs x blocks/SM
 template <typename W>
-static int occupancy(gs_engine *e, u32 warp_bytes, u32 want_wpb, W with, KernelCfg &K) {
+static int occupancy(gs_engine *e, u32 warp_bytes, u32 want_wpb, u32 max_wpb, W with,
+                     KernelCfg &K) {
   u32 wpb = 1;
   int best = -1;
-  for (u32 w = 4; w >= 1; --w) {
+  for (u32 w = max_wpb; w >= 1; --w) {
     if (want_wpb && w != want_wpb) continue;
     if ((size_t)w * warp_bytes > e->smem_optin) continue;
     int per = 0;
@@ -367,7 +368,7 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   KW.rec_in_smem = wrec_b <= 4096;
   if (any_narrow) {
     const u32 wb = (u32)((gs::kCntBytes + gs::kNarrowBytes + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
-    rc = occupancy(e, wb, r->warps_per_block,
+    rc = occupancy(e, wb, r->warps_per_block, 4,
                    [&](auto f) { return with_narrow_kernel(philox, f); }, KN);
     if (rc) return rc;
   }
@@ -375,7 +376,7 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
     size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_in_smem ? ((wrec_b + 15) & ~(size_t)15) : 0);
     KW.chi_off = (u32)base;
     const u32 wb = (u32)(base + (smem_chi ? chi : 0));
-    rc = occupancy(e, wb, r->warps_per_block,
+    rc = occupancy(e, wb, r->warps_per_block, GS_WIDE_WARPS,
                    [&](auto f) { return with_wide_kernel(smem_chi, philox, f); }, KW);
     if (rc) return rc;
     if (!smem_chi) {   // bound the global chi scratch

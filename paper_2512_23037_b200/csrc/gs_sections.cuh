@@ -28,7 +28,13 @@
 #define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
 #endif
 #ifndef GS_WIDE_BLOCKS
-#define GS_WIDE_BLOCKS 3   // <= 168 registers (no spills); shared memory holds 12-13 warps/SM anyway
+// launch bound only: <= 128 registers, no spills; shared memory still holds
+// 3 four-warp blocks (12 warps/SM) at d=5.  A/B (r01bl): 55.2M vs 54.0M at
+// the 146-register build (bound 3), 53.3M / 52.2M with __maxnreg__ 120 / 112
+#define GS_WIDE_BLOCKS 4
+#endif
+#ifndef GS_WIDE_WARPS
+#define GS_WIDE_WARPS 4    // most warps per wide block (13 in one block: 53.5M)
 #endif
 
 __host__ __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
@@ -634,7 +640,11 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 
 // @region wide: prologue
 template <bool kSmemChi, bool kPhilox>
-__global__ void __launch_bounds__(128, GS_WIDE_BLOCKS)
+#ifdef GS_WIDE_MAXREG
+__global__ void __maxnreg__(GS_WIDE_MAXREG)
+#else
+__global__ void __launch_bounds__(32 * GS_WIDE_WARPS, GS_WIDE_BLOCKS)
+#endif
 wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   extern __shared__ __align__(16) u8 smem[];
   const u32 lane = threadIdx.x & 31u;

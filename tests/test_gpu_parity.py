@@ -174,6 +174,20 @@ def test_random_programs_match_oracle(mode):
         assert got == ref, (it, prog.serialize())
 
 
+@pytest.mark.parametrize("mode", ["splitmix", "philox"])
+def test_shot_indices_beyond_32_bits(mode):
+    # BASELINE config 5 runs >= 1e10 shots: global indices past 2^32 (and a
+    # master seed with its high word set) must key the same streams as the
+    # oracle (SHA-1 of <QQ, Philox counter words 2-3 / key words 0-1)
+    rng = random.Random(77)
+    prog = _random_program(rng, 9, 60, 10, 0.05)
+    for begin in ((1 << 32) - 8, 12_345_678_901, (1 << 62) + 5):
+        master = (0xDEADBEEF << 32) | 17
+        got = _gpu_results(prog, master, 16, 4096, True, rng=mode, shot_begin=begin)
+        ref = _oracle_results(prog, master, 16, 4096, True, mode=mode, shot_begin=begin)
+        assert got == ref, (mode, begin)
+
+
 def test_run_shot_api_matches_reference_examples():
     prog = parse_circuit("H 0\nH 1\nT 0\nT 1\n")
     ctx = ShotContext(prog.num_qubits, 2)
