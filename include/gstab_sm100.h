@@ -50,6 +50,8 @@ extern "C" {
 #define GS_CHI_GLOBAL 4u   /* force chi buffers into global memory (test) */
 #define GS_CHI_SMEM 16u    /* force chi buffers into shared memory (test) */
 #define GS_WIDE_ONLY 32u   /* run every op warp-per-shot (A/B, test)     */
+#define GS_CHI_BLOCK 64u   /* wide sections: one block of warps per shot
+                              (the default when chi exceeds 32 KB)       */
 
 /* per-shot status codes (gs_run_records) */
 #define GS_ST_PRESERVED 1

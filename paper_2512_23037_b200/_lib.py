@@ -19,6 +19,7 @@ GS_POSTSELECT = 1
 GS_RNG_PHILOX = 2
 GS_CHI_GLOBAL = 4
 GS_CHI_SMEM = 16
+GS_CHI_BLOCK = 64
 GS_WIDE_ONLY = 32
 
 GS_C_TOTAL = 0

@@ -115,6 +115,71 @@ __device__ __forceinline__ u64 warp_or64(u64 v) {
   return ((u64)hi << 32) | lo;
 }
 
+// Threads that share one shot's chi in the wide kernel: one warp (kG = 1,
+// every lane its own coordinates) or, for large chi, the whole block of kG
+// warps (blockDim = 32 kG).  In the block form every warp runs the shot's
+// scalar logic redundantly (same inputs, same results) and only the chi
+// passes are split; group reductions sum the warps' totals in warp order
+// through a two-slot shared scratch, so every warp sees the same bits.
+template <int kG>
+__device__ __forceinline__ u32 glane() { return kG == 1 ? (threadIdx.x & 31u) : threadIdx.x; }
+template <int kG>
+__device__ __forceinline__ void gsync() {
+  if (kG == 1) __syncwarp(); else __syncthreads();
+}
+// barrier on entry to a chi pass (block form): orders it after the previous
+// pass's writes by other warps
+template <int kG>
+__device__ __forceinline__ void gbar_in() {
+  if (kG > 1) __syncthreads();
+}
+struct GroupScratch {
+  u64 *slots;   // 2 x 32 words of shared memory (block form only)
+  u32 tog;      // alternating half: a slot half is rewritten only after the
+                // barrier of the next reduction, which every reader passed
+};
+template <int kG>
+__device__ __forceinline__ double group_sum(double v, GroupScratch &g) {
+  v = warp_sum(v);
+  if (kG == 1) return v;
+  u64 *s = g.slots + 32u * g.tog;
+  g.tog ^= 1u;
+  if ((threadIdx.x & 31u) == 0) s[threadIdx.x >> 5] = (u64)__double_as_longlong(v);
+  __syncthreads();
+  double t = __longlong_as_double((long long)s[0]);
+#pragma unroll 1
+  for (int w = 1; w < kG; ++w) t = __dadd_rn(t, __longlong_as_double((long long)s[w]));
+  return t;
+}
+template <int kG>
+__device__ __forceinline__ u32 group_sum_u32(u32 v, GroupScratch &g) {
+  v = warp_sum_u32(v);
+  if (kG == 1) return v;
+  u64 *s = g.slots + 32u * g.tog;
+  g.tog ^= 1u;
+  if ((threadIdx.x & 31u) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  u32 t = 0;
+#pragma unroll 1
+  for (int w = 0; w < kG; ++w) t += (u32)s[w];
+  return t;
+}
+// thread 0's value to the whole group (kG == 1: lane 0's)
+template <int kG>
+__device__ __forceinline__ u64 group_bcast(u64 v, GroupScratch &g) {
+  if (kG == 1) return __shfl_sync(FULL, v, 0);
+  u64 *s = g.slots + 32u * g.tog;
+  g.tog ^= 1u;
+  if (threadIdx.x == 0) s[0] = v;
+  __syncthreads();
+  return s[0];
+}
+template <int kG>
+__device__ __forceinline__ u32 group_bcast32(u32 v, GroupScratch &g) {
+  if (kG == 1) return __shfl_sync(FULL, v, 0);
+  return (u32)group_bcast<kG>(v, g);
+}
+
 // ---------------------------------------------------------------- RNG
 
 __device__ __forceinline__ u32 bswap32(u32 x) { return __byte_perm(x, 0, 0x0123); }

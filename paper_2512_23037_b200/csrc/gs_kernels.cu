@@ -256,9 +256,14 @@ static cudaError_t with_narrow_kernel(bool philox, F f) {
   return philox ? f(gs::narrow_kernel<true>) : f(gs::narrow_kernel<false>);
 }
 template <typename F>
-static cudaError_t with_wide_kernel(bool smem_chi, bool philox, F f) {
-  if (smem_chi) return philox ? f(gs::wide_kernel<true, true>) : f(gs::wide_kernel<true, false>);
-  return philox ? f(gs::wide_kernel<false, true>) : f(gs::wide_kernel<false, false>);
+static cudaError_t with_wide_kernel(bool smem_chi, bool philox, bool block, F f) {
+  constexpr int G = GS_BLOCK_WARPS;
+  if (block) {
+    if (smem_chi) return philox ? f(gs::wide_kernel<true, true, G>) : f(gs::wide_kernel<true, false, G>);
+    return philox ? f(gs::wide_kernel<false, true, G>) : f(gs::wide_kernel<false, false, G>);
+  }
+  if (smem_chi) return philox ? f(gs::wide_kernel<true, true, 1>) : f(gs::wide_kernel<true, false, 1>);
+  return philox ? f(gs::wide_kernel<false, true, 1>) : f(gs::wide_kernel<false, false, 1>);
 }
 
 struct KernelCfg {
@@ -357,9 +362,18 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
 
   // launch shapes: narrow warps hold 32 shots' chi rows and record columns,
   // wide warps one shot's chi (shared memory when 2^max_dim entries fit)
+  // chi of 2^14 entries or more: one block of GS_BLOCK_WARPS warps per shot
+  // on a per-block global buffer (the ~150-300 shots in flight keep it
+  // L2-resident to k ~ 15; r01bm config-4 sweep: 1.4-5.5x over a warp per
+  // shot).  k = 12-13 stays warp per shot on a global buffer (more shots in
+  // flight beat the block's per-pass barriers there); GS_CHI_BLOCK forces the
+  // block form, with chi in shared memory when it fits
   const size_t chi = (size_t)16 << P.max_dim;
+  const bool block = (r->flags & GS_CHI_BLOCK) ||
+                     (!(r->flags & (GS_CHI_GLOBAL | GS_CHI_SMEM)) && P.max_dim >= GS_BLOCK_MIN_DIM);
   bool smem_chi;
   if (r->flags & GS_CHI_GLOBAL) smem_chi = false;
+  else if (block) smem_chi = true;   // decided below against the opt-in limit
   else if (r->flags & GS_CHI_SMEM) smem_chi = chi <= 64 * 1024;
   else smem_chi = chi <= 32 * 1024;
   const size_t nrec_b = (size_t)P.rec_words32 * 4 * 32, wrec_b = (size_t)P.rec_words32 * 4;
@@ -372,22 +386,44 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
                    [&](auto f) { return with_narrow_kernel(philox, f); }, KN);
     if (rc) return rc;
   }
-  if (any_wide) {
+  if (any_wide && !block) {
     size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_in_smem ? ((wrec_b + 15) & ~(size_t)15) : 0);
     KW.chi_off = (u32)base;
     const u32 wb = (u32)(base + (smem_chi ? chi : 0));
     rc = occupancy(e, wb, r->warps_per_block, GS_WIDE_WARPS,
-                   [&](auto f) { return with_wide_kernel(smem_chi, philox, f); }, KW);
+                   [&](auto f) { return with_wide_kernel(smem_chi, philox, false, f); }, KW);
     if (rc) return rc;
     if (!smem_chi) {   // bound the global chi scratch
       const u64 max_warps = ((u64)8 << 30) / chi;
       if ((u64)KW.blocks * KW.wpb > max_warps) KW.blocks = (u32)std::max<u64>(1, max_warps / KW.wpb);
     }
   }
+  if (any_wide && block) {
+    // [per-warp slices][group scratch: 2 x 32 u64][chi]
+    const size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_in_smem ? ((wrec_b + 15) & ~(size_t)15) : 0);
+    const size_t head = (size_t)GS_BLOCK_WARPS * base + 64 * sizeof(u64);
+    if (smem_chi && head + chi > e->smem_optin) smem_chi = false;
+    KW.wpb = GS_BLOCK_WARPS;
+    KW.warp_bytes = (u32)base;
+    KW.chi_off = (u32)head;
+    KW.smem = head + (smem_chi ? chi : 0);
+    int per = 0;
+    CUDA_TRY(with_wide_kernel(smem_chi, philox, true, [&](auto kern) {
+      cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KW.smem);
+      return err != cudaSuccess ? err
+                                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, GS_BLOCK_WARPS * 32, KW.smem);
+    }));
+    if (per < 1) return fail(GS_ERR_UNSUPPORTED, "block-per-shot state exceeds the SM");
+    KW.blocks = (u32)(e->num_sms * per);
+    if (!smem_chi) {
+      const u64 max_blocks = ((u64)8 << 30) / chi;
+      if ((u64)KW.blocks > max_blocks) KW.blocks = (u32)std::max<u64>(1, max_blocks);
+    }
+  }
   if (r->blocks) { KN.blocks = r->blocks; KW.blocks = r->blocks; }
   const u64 nwarps = std::max((u64)KN.blocks * KN.wpb, (u64)KW.blocks * KW.wpb);
   if (!smem_chi && any_wide) {
-    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * KW.wpb * chi);
+    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 1 : KW.wpb) * chi);
     if (rc) return rc;
   }
   if (!KN.rec_in_smem || !KW.rec_in_smem) {
@@ -443,7 +479,7 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
           Ow.warp_bytes = KW.warp_bytes;
           Ow.rec_in_smem = KW.rec_in_smem;
           Ow.chi_off = KW.chi_off;
-          CUDA_TRY(with_wide_kernel(smem_chi, philox, [&](auto kern) {
+          CUDA_TRY(with_wide_kernel(smem_chi, philox, block, [&](auto kern) {
             kern<<<KW.blocks, KW.wpb * 32, KW.smem, st>>>(P, R, Ow, S);
             return cudaGetLastError();
           }));

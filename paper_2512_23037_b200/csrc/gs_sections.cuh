@@ -36,6 +36,12 @@
 #ifndef GS_WIDE_WARPS
 #define GS_WIDE_WARPS 4    // most warps per wide block (13 in one block: 53.5M)
 #endif
+#ifndef GS_BLOCK_WARPS
+#define GS_BLOCK_WARPS 16  // warps sharing one shot's chi (block form)
+#endif
+#ifndef GS_BLOCK_MIN_DIM
+#define GS_BLOCK_MIN_DIM 14   // chi dimension from which the block form is the default
+#endif
 
 __host__ __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
   return kind == OP_GROW_LIMIT || k > GS_KN ||
@@ -639,11 +645,13 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 // ---------------------------------------------------------------- wide
 
 // @region wide: prologue
-template <bool kSmemChi, bool kPhilox>
+// kG = 1: warp per shot, kG > 1: block of kG warps per shot (large chi,
+// see GroupScratch)
+template <bool kSmemChi, bool kPhilox, int kG>
 #ifdef GS_WIDE_MAXREG
 __global__ void __maxnreg__(GS_WIDE_MAXREG)
 #else
-__global__ void __launch_bounds__(32 * GS_WIDE_WARPS, GS_WIDE_BLOCKS)
+__global__ void __launch_bounds__(kG == 1 ? 32 * GS_WIDE_WARPS : 32 * kG, kG == 1 ? GS_WIDE_BLOCKS : 1)
 #endif
 wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   extern __shared__ __align__(16) u8 smem[];
@@ -656,8 +664,16 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   u32 *win = reinterpret_cast<u32 *>(mine + kCntBytes);
   u32 *recw = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kWinBytes)
                             : O.grec + gw * (u64)P.rec_words32;
-  double2 *A = kSmemChi ? chi_ptr<true>(reinterpret_cast<double2 *>(mine + O.chi_off))
-                        : O.gchi + gw * ((u64)1 << P.max_dim);
+  // block form: per-warp slices, then the group scratch, then chi
+  const u32 gl = glane<kG>();
+  constexpr u32 NT = 32u * kG;
+  const bool leader = kG == 1 || wib == 0;   // the warp that writes outputs
+  GroupScratch grp;
+  grp.slots = reinterpret_cast<u64 *>(smem + (size_t)wpb * O.warp_bytes);
+  grp.tog = 0;
+  double2 *A = kSmemChi ? chi_ptr<true>(reinterpret_cast<double2 *>(
+                              kG == 1 ? mine + O.chi_off : smem + O.chi_off))
+                        : O.gchi + (kG == 1 ? gw : (u64)blockIdx.x) * ((u64)1 << P.max_dim);
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
   const u64 *__restrict__ tables = P.tables;
@@ -677,8 +693,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   for (;;) {
     // @region wide: shot setup
     u64 idx = 0;
-    if (lane == 0) idx = atomicAdd(S.work, 1ull);
-    idx = __shfl_sync(FULL, idx, 0);
+    if (gl == 0) idx = atomicAdd(S.work, 1ull);
+    idx = group_bcast<kG>(idx, grp);
     if (idx >= total) break;
     Rng rng;
     rng.philox = philox;
@@ -696,8 +712,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       if (!philox) rng.seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, rng.shot);
 #pragma unroll 1
       for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
-      if (lane == 0) A[0] = make_double2(1.0, 0.0);
-      nrm_l = lane == 0 ? 1.0 : 0.0;
+      if (gl == 0) A[0] = make_double2(1.0, 0.0);
+      nrm_l = gl == 0 ? 1.0 : 0.0;
       if (philox && P.geo_len > 1 && P.nlocs) {
         const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, rng.shot, 0u, 0u);
         gpos = gc.pos;
@@ -721,13 +737,14 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       // chi in, and its norm (same per-lane order + tree as a sum pass)
       const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
 #pragma unroll 1
-      for (u32 j = lane; j < (1u << k); j += 32) {
+      for (u32 j = gl; j < (1u << k); j += NT) {
         const double2 v = qc[j];
         A[j] = v;
         nrm_l = __dadd_rn(nrm_l, abs2(v));
       }
     }
     if (!philox) fire_pc = 0xFFFFFFFFu;
+    if (kG > 1) __syncthreads();   // chi init before the first pass
     u32 kcur = k;
     int status = ST_RUNNING, aux = -1;
     double ps = 1.0;        // renormalisation pending on A (see ldps)
@@ -757,9 +774,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
                                          sig_lo, sig_hi);
           const double2 php = ipow(e.xi);
-          sweep_phase<kSmemChi>(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
+          sweep_phase<kSmemChi, kG>(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
           ps = 1.0;
-          __syncwarp();
+          gsync<kG>();
           c ^= e.beta;
           mbytes += 2ull * kEntryBytes * cnt + sign_bytes;
         };
@@ -869,9 +886,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         if (tcase == T_DIAG) {
           // beta == 0: pure phase per entry (ref state.py:120-126); the
           // factors have modulus 1, the norm is kept
-          sweep_phase<kSmemChi>(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
+          sweep_phase<kSmemChi, kG>(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
           ps = 1.0;
-          __syncwarp();
+          gsync<kG>();
           mbytes += 32ull * cnt;
           continue;
         }
@@ -879,20 +896,21 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         if (wkind == OP_GROW_LIMIT) {
           u32 nz = 0;
           const double2 bx1 = cneg(bx0);
+          gbar_in<kG>();
 #pragma unroll 1
-          for (u32 j = lane; j < size; j += 32) {
+          for (u32 j = gl; j < size; j += NT) {
             const double2 v = ldps(A, j, ps);
             const u32 s_ = dc ^ par32(j & dmask);
             nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
             nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
           }
-          nz = warp_sum_u32(nz);
+          nz = group_sum_u32<kG>(nz, grp);
           status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
           aux = (int)winstr;
           break;
         }
         // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
-        if (ps != 1.0) sweep_scale<kSmemChi>(A, size, ps);   // rare: right after a deferral
+        if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);   // rare: right after a deferral
         ps = 1.0;
         if (tcase == T_BUTTERFLY && (wfl & TF_FUSE)) {
           // this gate and the next one (also a BUTTERFLY at the same k, no
@@ -915,13 +933,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           mbytes += __ldg(op2 + 11);
           wpc += (u32)((h2 >> 8) & 0xff);
           hnext = __ldg(ops + wpc);
-          const SumNz2 r2 = sweep_butterfly2<kSmemChi>(A, size >> 2, g1, g2);
-          __syncwarp();
-          const u32 cnt1 = warp_sum_u32(r2.nz1);
+          const SumNz2 r2 = sweep_butterfly2<kSmemChi, kG>(A, size >> 2, g1, g2);
+          gsync<kG>();
+          const u32 cnt1 = group_sum_u32<kG>(r2.nz1, grp);
           mbytes += (u64)kEntryBytes * (cin + cnt1);
           if ((u64)cnt1 > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
           if (cnt1 == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
-          cnt = warp_sum_u32(r2.nz);
+          cnt = group_sum_u32<kG>(r2.nz, grp);
           nrm_l = r2.sum;
           mbytes += (u64)kEntryBytes * (cnt1 + cnt);
           if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr2; break; }
@@ -930,13 +948,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         }
         SumNz r;
         if (tcase == T_BUTTERFLY) {
-          r = sweep_butterfly<kSmemChi>(A, size >> 1, cb, dc, dmask, a, bx0);
+          r = sweep_butterfly<kSmemChi, kG>(A, size >> 1, cb, dc, dmask, a, bx0);
         } else {
-          r = sweep_grow<kSmemChi>(A, size, dc, dmask, a, bx0);
+          r = sweep_grow<kSmemChi, kG>(A, size, dc, dmask, a, bx0);
           kcur = wk + 1;
         }
-        __syncwarp();
-        cnt = warp_sum_u32(r.nz);
+        gsync<kG>();
+        cnt = group_sum_u32<kG>(r.nz, grp);
         nrm_l = r.sum;
         mbytes += (u64)kEntryBytes * (cin + cnt);
         if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
@@ -969,9 +987,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         // a renormalisation by rs that needs no data movement: deferred to
         // the next pass over chi (ldps); nonzero count unchanged
         auto defer_scale = [&](double rs, double kept) {
-          if (ps != 1.0) sweep_scale<kSmemChi>(A, size, ps);
+          if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);
           ps = rs;
-          nrm_l = lane == 0 ? __dmul_rn(__dmul_rn(kept, rs), rs) : 0.0;
+          nrm_l = gl == 0 ? __dmul_rn(__dmul_rn(kept, rs), rs) : 0.0;
         };
         const u32 cin = cnt;
         bool plus;
@@ -981,13 +999,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           double sp, sm;
           if (dmask == 0) {
             // every coordinate has eigenvalue (-1)^neg0: P+ is the norm
-            const double nrm = warp_sum(nrm_l);
+            const double nrm = group_sum<kG>(nrm_l, grp);
             sp = neg0 ? 0.0 : nrm;
             sm = neg0 ? nrm : 0.0;
           } else {
-            const double2 part = sweep_det_sums<kSmemChi>(A, size, dmask, neg0, ps);
-            sp = warp_sum(part.x);
-            sm = warp_sum(part.y);
+            const double2 part = sweep_det_sums<kSmemChi, kG>(A, size, dmask, neg0, ps);
+            sp = group_sum<kG>(part.x, grp);
+            sm = group_sum<kG>(part.y, grp);
           }
           plus = pick_plus(sp);
           const double chosen = plus ? sp : __dsub_rn(1.0, sp);
@@ -996,10 +1014,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const double rs = inv_sqrt_norm(plus ? sp : sm);
           if (wfl & MF_COMPACT) {
             const u32 tau = want_neg ^ neg0;
-            const SumNz r = sweep_compact<kSmemChi>(A, size >> 1, isq, dmask, tau, rs, ps);
+            const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, rs, ps);
             ps = 1.0;
-            __syncwarp();
-            cnt = warp_sum_u32(r.nz);
+            gsync<kG>();
+            cnt = group_sum_u32<kG>(r.nz, grp);
             nrm_l = r.sum;
             if (tau) c ^= vec;
             kcur = wk - 1;
@@ -1008,10 +1026,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             // renormalisation
             defer_scale(rs, plus ? sp : sm);
           } else {
-            const SumNz r = sweep_filter<kSmemChi>(A, size, dmask, neg0, want_neg, rs, ps);
+            const SumNz r = sweep_filter<kSmemChi, kG>(A, size, dmask, neg0, want_neg, rs, ps);
             ps = 1.0;
-            __syncwarp();
-            cnt = warp_sum_u32(r.nz);
+            gsync<kG>();
+            cnt = group_sum_u32<kG>(r.nz, grp);
             nrm_l = r.sum;
           }
         } else {
@@ -1022,21 +1040,21 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
           g.dc = dc; g.dmask = dmask;
           const double2 xpp = ipow(xi0);   // i^xi0, exact
-          const double pp = __dmul_rn(0.5, warp_sum(sweep_pivot_p<kSmemChi>(A, g, xpp, ps)));
+          const double pp = __dmul_rn(0.5, group_sum<kG>(sweep_pivot_p<kSmemChi, kG>(A, g, xpp, ps), grp));
           plus = pick_plus(pp);
           const double chosen = plus ? pp : __dsub_rn(1.0, pp);
           if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
-          const SumNz w = sweep_pivot_w<kSmemChi>(A, g, xpp, plus, ps);
+          const SumNz w = sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
           ps = 1.0;
-          __syncwarp();
-          const double sk = warp_sum(w.sum);
-          cnt = warp_sum_u32(w.nz);
+          gsync<kG>();
+          const double sk = group_sum<kG>(w.sum, grp);
+          cnt = group_sum_u32<kG>(w.nz, grp);
           if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
           const double rs = inv_sqrt_norm(sk);
           if (g.span) {
-            const SumNz r = sweep_compact<kSmemChi>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
-            __syncwarp();
-            cnt = warp_sum_u32(r.nz);
+            const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+            gsync<kG>();
+            cnt = group_sum_u32<kG>(r.nz, grp);
             nrm_l = r.sum;
             kcur = wk - 1;
           } else {
@@ -1102,14 +1120,14 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       aux = -2;
     }
     // @region wide: outputs
-    __syncwarp();
+    gsync<kG>();
     if (status == ST_RUNNING) {
       // survivor: hand it to the next (narrow) section's queue
       u32 o = 0;
-      if (lane == 0) o = atomicAdd(S.n_out, 1u);
-      o = __shfl_sync(FULL, o, 0);
+      if (gl == 0) o = atomicAdd(S.n_out, 1u);
+      o = group_bcast32<kG>(o, grp);
       u64 *q = S.q_out + (u64)o * SU;
-      if (lane == 0) {
+      if (gl == 0) {
         q[Q_SL] = sl; q[Q_LO] = sig_lo; q[Q_HI] = sig_hi; q[Q_C] = c; q[Q_OBS] = obs;
         q[Q_MB] = mbytes; q[Q_PICK] = gpick; q[Q_SEED] = rng.seed;
         q[Q_CNTK] = (u64)cnt;
@@ -1118,13 +1136,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       }
       u32 *qr = reinterpret_cast<u32 *>(q + Q_HDR);
 #pragma unroll 1
-      for (u32 w = lane; w < P.rec_words32; w += 32) qr[w] = recw[w];
+      for (u32 w = lane; leader && w < P.rec_words32; w += 32) qr[w] = recw[w];
       double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
 #pragma unroll 1
-      for (u32 j = lane; j < (1u << kcur); j += 32) qc[j] = ldps(A, j, ps);
+      for (u32 j = gl; j < (1u << kcur); j += NT) qc[j] = ldps(A, j, ps);
       (void)exit_pc;
     } else {
-      if (lane == 0) {
+      if (gl == 0) {
         wcnt[WC_TOT] += 1;
         wcnt[WC_MB] += mbytes;
         if (status == ST_PRESERVED) {
@@ -1144,7 +1162,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         else if (status == ST_CORRUPT) wcnt[WC_COR] += 1;
         else wcnt[WC_UNS] += 1;
       }
-      if (O.mode != MODE_COUNTERS) {
+      if (O.mode != MODE_COUNTERS && leader) {
         if (lane == 0) {
           O.status[sl] = (u8)status;
           O.aux[sl] = aux;
@@ -1166,11 +1184,11 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           }
           const u64 stride = 1ull << P.max_dim;
 #pragma unroll 1
-          for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = ldps(A, j, ps);
+          for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = ldps(A, j, ps);   // leader warp
         }
       }
     }
-    __syncwarp();
+    gsync<kG>();
   }
   flush_counters(O, wcnt, lane);
 }

@@ -57,11 +57,12 @@ __device__ __forceinline__ double2 neg_if(double2 v, u32 s) {
 
 // T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
 // 294-306: a-term then b-term); no renormalisation pending (caller)
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32 dc, u32 dmask,
                                               double2 a, double2 bx0) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   const u32 hb = 31 - __clz(cb);
   SumNz r;
   r.sum = 0.0;
@@ -69,8 +70,8 @@ __device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, 
   const u32 jl = ins_bit(lane, hb, 0);
   const u32 pl = dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
 #pragma unroll 1
-  for (u32 m = lane; m < half; m += 32) {
-    const u32 jr = ins_bit(m & ~31u, hb, 0);
+  for (u32 m = lane; m < half; m += 32u * kG) {
+    const u32 jr = ins_bit(m & ~(32u * kG - 1u), hb, 0);
     const u32 j0 = jr | jl, j1 = j0 ^ cb;
     const double2 v0 = A[j0], v1 = A[j1];
     const u32 s0 = pl ^ par32(jr & dmask), s1 = s0 ^ pcb;
@@ -94,10 +95,11 @@ struct SumNz2 {
   double sum;
   u32 nz, nz1;
 };
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g1, Gate g2) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   const u32 h1 = 31 - __clz(g1.cb);
   const u32 cr = ((g2.cb >> h1) & 1u) ? (g2.cb ^ g1.cb) : g2.cb;
   const u32 h2 = 31 - __clz(cr);
@@ -115,8 +117,8 @@ __device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gat
   const u32 a1 = par32(g1.cb & g1.dmask), b1 = par32(g2.cb & g1.dmask);
   const u32 a2 = par32(g1.cb & g2.dmask), b2 = par32(g2.cb & g2.dmask);
 #pragma unroll 1
-  for (u32 m = lane; m < quarter; m += 32) {
-    const u32 jr = ins_bit(ins_bit(m & ~31u, plo, 0), phi, 0);
+  for (u32 m = lane; m < quarter; m += 32u * kG) {
+    const u32 jr = ins_bit(ins_bit(m & ~(32u * kG - 1u), plo, 0), phi, 0);
     const u32 x0 = jr | jl;
     const u32 x1 = x0 ^ g1.cb, x2 = x0 ^ g2.cb, x3 = x1 ^ g2.cb;
     const double2 v0 = A[x0], v1 = A[x1], v2 = A[x2], v3 = A[x3];
@@ -139,16 +141,17 @@ __device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gat
 }
 
 // T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmask, double2 a,
                                          double2 bx0) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) {
+  for (u32 j = lane; j < size; j += 32u * kG) {
     const double2 v = A[j];
     A[j] = prune_acc(cmul(a, v), r.sum, r.nz);
     A[size + j] = prune_acc(neg_if(cmul(bx0, v), dc ^ par32(j & dmask)), r.sum, r.nz);
@@ -158,25 +161,27 @@ __device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 d
 
 // diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
 // fired noise Paulis)
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask,
                                          double2 f0, double2 f1, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32)
+  for (u32 j = lane; j < size; j += 32u * kG)
     A[j] = cmul(ldps(A, j, ps), (dc ^ par32(j & mask)) ? f1 : f0);
 }
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask, u32 neg0,
                                                double ps) {
   const double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   double sp = 0.0, sm = 0.0;
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) {
+  for (u32 j = lane; j < size; j += 32u * kG) {
     const double a2 = abs2(ldps(A, j, ps));
     if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
   }
@@ -184,16 +189,17 @@ __device__ __forceinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dma
 }
 
 // keep the chosen eigen-entries, scaled by rs; zero the others
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32 neg0,
                                            u32 want_neg, double rs, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) {
+  for (u32 j = lane; j < size; j += 32u * kG) {
     const double2 v = ldps(A, j, ps);
     if ((neg0 ^ par32(j & dmask)) == want_neg) {
       const double2 w = cscale(v, rs);
@@ -210,30 +216,31 @@ __device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, 
 // in-place compaction dropping coordinate isq: A[jp] = rs * A[src(jp)],
 // src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
 // at isq; src(jp) >= jp, so reads of a round finish before its writes
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
                                             double rs, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
 #pragma unroll 1
-  for (u32 b0 = 0; b0 < half; b0 += 32) {
+  for (u32 b0 = 0; b0 < half; b0 += 32u * kG) {
     const u32 jp = b0 + lane;
     double2 v = make_double2(0.0, 0.0);
     if (jp < half) {
       const u32 j0 = ins_bit(jp, isq, 0);
       v = ldps(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
     }
-    __syncwarp();
+    gsync<kG>();
     if (jp < half) {
       const double2 w = cscale(v, rs);
       A[jp] = w;
       r.sum = __dadd_rn(r.sum, abs2(w));
       r.nz += nonzero(w);
     }
-    __syncwarp();
+    gsync<kG>();
   }
   return r;
 }
@@ -270,13 +277,14 @@ __device__ __forceinline__ void pivot_terms(const double2 *__restrict__ A, const
     dst = m;
   }
 }
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2 xpp, double ps) {
   const double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   double sp = 0.0;
 #pragma unroll 1
-  for (u32 m = lane; m < g.npairs; m += 32) {
+  for (u32 m = lane; m < g.npairs; m += 32u * kG) {
     double2 vr, pr;
     u32 d_;
     pivot_terms(A, g, xpp, m, vr, pr, d_, ps);
@@ -284,16 +292,17 @@ __device__ __forceinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2
   }
   return sp;
 }
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 xpp, bool plus,
                                             double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
 #pragma unroll 1
-  for (u32 m = lane; m < g.npairs; m += 32) {
+  for (u32 m = lane; m < g.npairs; m += 32u * kG) {
     double2 vr, pr;
     u32 dst;
     pivot_terms(A, g, xpp, m, vr, pr, dst, ps);
@@ -303,10 +312,11 @@ __device__ __forceinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 
 }
 
 // apply a pending renormalisation in place: A[j] = ps * A[j]
-template <bool kS>
+template <bool kS, int kG = 1>
 __device__ __forceinline__ void sweep_scale(double2 *A_, u32 size, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
-  const u32 lane = threadIdx.x & 31u;
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
 #pragma unroll 1
-  for (u32 j = lane; j < size; j += 32) A[j] = cscale(A[j], ps);
+  for (u32 j = lane; j < size; j += 32u * kG) A[j] = cscale(A[j], ps);
 }

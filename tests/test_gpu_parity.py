@@ -73,7 +73,8 @@ def test_golden_shot_results_bit_exact(golden_shots):
 
 @pytest.mark.parametrize("flag", [_lib.GS_CHI_GLOBAL, _lib.GS_CHI_SMEM,
                                   _lib.GS_WIDE_ONLY,
-                                  _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM])
+                                  _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM,
+                                  _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK])
 def test_golden_shot_results_storage_variants(golden_shots, flag):
     for fx in golden_shots[::3]:
         prog = parse_circuit(fx["text"])
@@ -188,6 +189,33 @@ def test_shot_indices_beyond_32_bits(mode):
         assert got == ref, (mode, begin)
 
 
+@pytest.mark.parametrize("n,t", [(56, 16), (48, 24)])
+def test_large_chi_block_per_shot_matches_oracle(n, t):
+    """Config-4 programs with chi beyond 32 KB (k <= 13: the block's shared
+    memory; k = 15: a per-block global buffer) run one block of warps per
+    shot by default; records, statuses and overflow points must equal the
+    oracle's and the warp-per-shot global-buffer path's."""
+    from paper_2512_23037_b200.msc import config4_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(config4_circuit(n, t, seed=n + t), 1e-3)
+    dp = compile_program(prog, max_dim=16)
+    assert dp.max_dim > 11
+    shots = 6
+    for mode in ("splitmix", "philox"):
+        flags = _lib.GS_RNG_PHILOX if mode == "philox" else 0
+        p = Program(dp)
+        eng = get_engine(0)
+        outs = []
+        for extra in (0, _lib.GS_CHI_GLOBAL):
+            par = Engine.params(9, 0, shots, 32768, flags | extra)
+            outs.append(eng.run_records(p, par))
+        for x, y in zip(*outs):
+            assert np.array_equal(x, y), mode
+        ref = _oracle_results(prog, 9, shots, 32768, False, mode=mode)
+        got = _gpu_results(prog, 9, shots, 32768, False, rng=mode)
+        assert got == ref, mode
+
+
 def test_run_shot_api_matches_reference_examples():
     prog = parse_circuit("H 0\nH 1\nT 0\nT 1\n")
     ctx = ShotContext(prog.num_qubits, 2)
@@ -228,14 +256,18 @@ def test_msc_noiseless_is_deterministic(d):
 
 
 @pytest.mark.parametrize("variant", ["default", "wide_only", "chi_global",
-                                     "chi_smem", "wide_only_chi_smem"])
+                                     "chi_smem", "wide_only_chi_smem", "chi_block",
+                                     "chi_block_global", "wide_only_chi_block"])
 def test_chi_storage_modes_match_oracle(variant):
-    """Lane-per-shot / warp-per-shot execution and shared- / global-memory
-    chi buffers must all give the oracle's results."""
+    """Lane-per-shot / warp-per-shot / block-per-shot execution and shared- /
+    global-memory chi buffers must all give the oracle's results."""
     rng = random.Random(7)
     flags_extra = {"default": 0, "wide_only": _lib.GS_WIDE_ONLY,
                    "chi_global": _lib.GS_CHI_GLOBAL, "chi_smem": _lib.GS_CHI_SMEM,
-                   "wide_only_chi_smem": _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM}[variant]
+                   "wide_only_chi_smem": _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM,
+                   "chi_block": _lib.GS_CHI_BLOCK,
+                   "chi_block_global": _lib.GS_CHI_BLOCK | _lib.GS_CHI_GLOBAL,
+                   "wide_only_chi_block": _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK}[variant]
     eng = get_engine(0)
     for it in range(25):
         n = rng.choice((4, 9, 20))
@@ -254,9 +286,11 @@ def test_chi_storage_modes_match_oracle(variant):
             assert r.record == ref[i]["record"], (variant, it, i)
 
 
-def test_msc_d5_dumps_match_oracle_through_t_layer():
+@pytest.mark.parametrize("flag", [0, _lib.GS_CHI_BLOCK])
+def test_msc_d5_dumps_match_oracle_through_t_layer(flag):
     """Full-size state check: the d=5 proxy with chi peaking at 1024
-    entries, dumped after the first T layer and after the undo layer."""
+    entries, dumped after the first T layer and after the undo layer
+    (warp per shot, and one block of warps per shot)."""
     from paper_2512_23037_b200.msc import msc_circuit
     from paper_2512_23037_b200.noise import apply_noise_model
     prog = apply_noise_model(msc_circuit(5), 2e-3)
@@ -268,7 +302,7 @@ def test_msc_d5_dumps_match_oracle_through_t_layer():
         p = Program(dp)
         for shot in range(3):
             seeds = np.array([derive_seed(4, shot)], dtype=np.uint64)
-            d = eng.dump(p, Engine.params(4, 0, 1, 1 << 20, 0, seeds=seeds))
+            d = eng.dump(p, Engine.params(4, 0, 1, 1 << 20, flag, seeds=seeds))
             ref = orc.run_one_shot(flat, prog.num_qubits,
                                    orc.DrawStream("splitmix", 4, shot), 1 << 20,
                                    False, stop_after=stop, snapshot=True)
