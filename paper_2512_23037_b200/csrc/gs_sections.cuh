@@ -705,6 +705,12 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     // chi norm, kept as per-lane partial sums and reduced only when a
     // deterministic measurement needs it
     double nrm_l = 0.0;
+    // after a deferred renormalisation the norm sits in thread 0's nrm_l
+    // alone and every thread knows it (nrm_u): the reduction would return
+    // exactly nrm_u (x + 0.0 == x), so consecutive dmask = 0 measurements
+    // skip it
+    bool nrm_lane0 = false;
+    double nrm_u = 0.0;
     if (!S.q_in) {
       sl = S.first + idx;
       rng.shot = R.shot_begin + sl;
@@ -714,6 +720,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
       if (gl == 0) A[0] = make_double2(1.0, 0.0);
       nrm_l = gl == 0 ? 1.0 : 0.0;
+      nrm_lane0 = true;
+      nrm_u = 1.0;
       if (philox && P.geo_len > 1 && P.nlocs) {
         const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, rng.shot, 0u, 0u);
         gpos = gc.pos;
@@ -941,6 +949,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           if (cnt1 == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
           cnt = group_sum_u32<kG>(r2.nz, grp);
           nrm_l = r2.sum;
+          nrm_lane0 = false;
           mbytes += (u64)kEntryBytes * (cnt1 + cnt);
           if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)instr2; break; }
           if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr2; break; }
@@ -956,6 +965,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         gsync<kG>();
         cnt = group_sum_u32<kG>(r.nz, grp);
         nrm_l = r.sum;
+        nrm_lane0 = false;
         mbytes += (u64)kEntryBytes * (cin + cnt);
         if ((u64)cnt > R.cap) { status = ST_OVERFLOW; aux = (int)winstr; break; }
         if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
@@ -989,7 +999,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         auto defer_scale = [&](double rs, double kept) {
           if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);
           ps = rs;
-          nrm_l = gl == 0 ? __dmul_rn(__dmul_rn(kept, rs), rs) : 0.0;
+          nrm_u = __dmul_rn(__dmul_rn(kept, rs), rs);
+          nrm_l = gl == 0 ? nrm_u : 0.0;
+          nrm_lane0 = true;
         };
         const u32 cin = cnt;
         bool plus;
@@ -999,7 +1011,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           double sp, sm;
           if (dmask == 0) {
             // every coordinate has eigenvalue (-1)^neg0: P+ is the norm
-            const double nrm = group_sum<kG>(nrm_l, grp);
+            const double nrm = nrm_lane0 ? nrm_u : group_sum<kG>(nrm_l, grp);
             sp = neg0 ? 0.0 : nrm;
             sm = neg0 ? nrm : 0.0;
           } else {
@@ -1019,6 +1031,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             gsync<kG>();
             cnt = group_sum_u32<kG>(r.nz, grp);
             nrm_l = r.sum;
+            nrm_lane0 = false;
             if (tau) c ^= vec;
             kcur = wk - 1;
           } else if ((plus ? sm : sp) == 0.0) {
@@ -1031,6 +1044,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             gsync<kG>();
             cnt = group_sum_u32<kG>(r.nz, grp);
             nrm_l = r.sum;
+            nrm_lane0 = false;
           }
         } else {
           // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
@@ -1056,6 +1070,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             gsync<kG>();
             cnt = group_sum_u32<kG>(r.nz, grp);
             nrm_l = r.sum;
+            nrm_lane0 = false;
             kcur = wk - 1;
           } else {
             defer_scale(rs, sk);
