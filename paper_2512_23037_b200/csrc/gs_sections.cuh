@@ -28,9 +28,9 @@
 #define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
 #endif
 #ifndef GS_WIDE_BLOCKS
-// launch bound only: <= 128 registers, no spills; shared memory still holds
-// 3 four-warp blocks (12 warps/SM) at d=5.  A/B (r01bl): 55.2M vs 54.0M at
-// the 146-register build (bound 3), 53.3M / 52.2M with __maxnreg__ 120 / 112
+// launch bound only: <= 128 registers, no spills, so 13 one-warp blocks fit
+// per SM at d=5 (shared memory bound; 12 at 146 registers).  A/B (r01bl):
+// 55.2M vs 54.0M, 53.3M / 52.2M with __maxnreg__ 120 / 112
 #define GS_WIDE_BLOCKS 4
 #endif
 #ifndef GS_WIDE_WARPS

@@ -96,11 +96,17 @@ def main():
     base = int(data[0][iA], 16)
     kname = rows[0][1] if rows and len(rows[0]) > 1 else ""
     import re as _re
-    bools = _re.findall(r"\(bool\)(\d)", kname)
-    kn = _re.search(r"(\w+_kernel)<", kname)
+    kn = _re.search(r"(\w+_kernel)<([^>]*)>", kname)
+    targs = [a.strip() for a in kn.group(2).split(",")] if kn else []
     kn = kn.group(1) if kn else "sample_kernel"
-    kre = ("%d%s" % (len(kn), kn)) + "".join("ILb%sE" % b if i == 0 else "Lb%sE" % b
-                                          for i, b in enumerate(bools))
+    # Itanium mangling of the template arguments: (bool)1 -> Lb1E, 16 -> Li16E
+    code = {"bool": "b", "int": "i", "unsigned int": "j"}
+
+    def mangle(a):
+        t = _re.match(r"\(([\w ]+)\)(-?\d+)$", a)
+        return "L%s%sE" % (code[t.group(1)], t.group(2)) if t else "Li%sE" % a
+    mang = "".join(mangle(a) for a in targs)
+    kre = ("%d%s" % (len(kn), kn)) + ("I%sE" % mang if targs else "")
     m = disasm(lib, kre)
     by_line_s, by_line_e = defaultdict(float), defaultdict(float)
     mism = 0
