@@ -57,6 +57,11 @@ OP_GROW_LIMIT = 7
 # T cases
 T_DIAG, T_BUTTERFLY, T_GROW = 0, 1, 2
 TF_FUSE = 1 << 4     # T flag: apply together with the next (BUTTERFLY) op
+# T flag: BUTTERFLY / GROW with b' = b / phase purely imaginary (xi_s even):
+# the wide kernel runs it as c v + i ss w with the global phase
+# e^{+-i pi/8} counted instead of multiplied in (gs_sweeps.cuh t_mix);
+# payload word 12: bit 0 = ss < 0, bit 1 = T_DAG
+TF_RED = 1 << 5
 # measurement cases
 M_DET, M_PIVOT_SPAN, M_PIVOT_NOSPAN = 0, 1, 2
 # measurement flags (bits of the header flag byte, above the 2-bit case and
@@ -430,10 +435,17 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         # components, so this host constant is exact; the device negates it
         # when the per-shot sign parity adds 2 to xi0
         bxs = b * (1.0 + 0.0j, 1.0j, -1.0 + 0.0j, -1.0j)[xis]
-        em.op(kind, k, case | (xis << 2), instr,
+        flags = case | (xis << 2)
+        # b / phase = -+i s * i^{xi_s} = i ss with ss = -+s (T / T_DAG),
+        # negated for xi_s = 2
+        ss_neg = int((not dagger) ^ (xis == 2))
+        if kind == OP_T and case != T_DIAG and xis % 2 == 0:
+            flags |= TF_RED
+        em.op(kind, k, flags, instr,
               [pre_lo, pre_hi, m_lo, m_hi, delta, cb | (dmask << 32),
                _dbl_bits(a.real), _dbl_bits(a.imag), _dbl_bits(bxs.real),
-               _dbl_bits(bxs.imag), (cnt + 1) * sign_bytes])
+               _dbl_bits(bxs.imag), (cnt + 1) * sign_bytes,
+               ss_neg | (int(dagger) << 1)])
         if kind == OP_GROW_LIMIT:
             truncated = instr
             return False
@@ -684,9 +696,9 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
 def _mark_fused_t_pairs(ops, noise_pcs):
     """Set TF_FUSE on a T BUTTERFLY op whose successor is a T BUTTERFLY of
     the same dimension with a different partner vector and no noise inserted
-    between them: the device applies both gates in one pass over 4-element
-    groups (same arithmetic and pruning order as two passes).  Pairs are
-    taken greedily left to right."""
+    between them and the same TF_RED form: the device applies both gates in
+    one pass over 4-element groups (same arithmetic and pruning order as two
+    passes).  Pairs are taken greedily left to right."""
     pc = 0
     prev = None
     while True:
@@ -695,14 +707,14 @@ def _mark_fused_t_pairs(ops, noise_pcs):
             break
         if (prev is not None and kind == OP_T and (fl & 3) == T_BUTTERFLY
                 and pc not in noise_pcs):
-            ppc, pk, pcb = prev
+            ppc, pk, pcb, pred = prev
             cb = ops[pc + 6] & 0xFFFFFFFF
-            if pk == k and pcb != cb and k >= 2:
+            if pk == k and pcb != cb and k >= 2 and pred == (fl & TF_RED):
                 ops[ppc] |= TF_FUSE << 24
                 prev = None
                 pc += ln
                 continue
-        prev = (pc, k, ops[pc + 6] & 0xFFFFFFFF) if (
+        prev = (pc, k, ops[pc + 6] & 0xFFFFFFFF, fl & TF_RED) if (
             kind == OP_T and (fl & 3) == T_BUTTERFLY) else None
         pc += ln
 

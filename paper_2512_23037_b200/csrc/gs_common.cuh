@@ -6,6 +6,7 @@ enum { OP_END = 0, OP_T = 1, OP_MEAS = 2, OP_NOISE = 3, OP_FEEDBACK = 4,
        OP_DETECTOR = 5, OP_OBSERVABLE = 6, OP_GROW_LIMIT = 7 };
 enum { T_DIAG = 0, T_BUTTERFLY = 1, T_GROW = 2 };
 enum { TF_FUSE = 16 };   // T flag: apply together with the next BUTTERFLY op
+enum { TF_RED = 32 };    // T flag: BUTTERFLY / GROW in the reduced form (t_mix)
 enum { M_DET = 0, M_PIVOT_SPAN = 1, M_PIVOT_NOSPAN = 2 };
 enum { MF_RECORD = 16, MF_FLIP = 32, MF_RESET = 64, MF_COMPACT = 128 };
 enum { NK_DEP1 = 0, NK_DEP2 = 1, NK_XERR = 2, NK_ZERR = 3 };
@@ -80,7 +81,19 @@ __device__ __forceinline__ double2 prune(double2 v) {
   return abs2(v) > kPrune2 ? v : make_double2(0.0, 0.0);
 }
 __device__ __forceinline__ u32 par64(u64 x) { return __popcll(x) & 1u; }
-// 1/sqrt(sum |v|^2) of ref state.py:311; exactly 1 when the sum is 1
+// e^{i pi n / 8} * v: the global phase the reduced T ops leave out of chi,
+// restored where amplitudes leave the device (dumps)
+#define GS_C8 0x1.d906bcf328d46p-1   /* cos(pi/8) */
+#define GS_S8 0x1.87de2a6aea963p-2   /* sin(pi/8) */
+#define GS_R2 0x1.6a09e667f3bcdp-1   /* sqrt(1/2) */
+__constant__ double2 kPhase16[16] = {
+    {1.0, 0.0},     {GS_C8, GS_S8},   {GS_R2, GS_R2},   {GS_S8, GS_C8},
+    {0.0, 1.0},     {-GS_S8, GS_C8},  {-GS_R2, GS_R2},  {-GS_C8, GS_S8},
+    {-1.0, 0.0},    {-GS_C8, -GS_S8}, {-GS_R2, -GS_R2}, {-GS_S8, -GS_C8},
+    {0.0, -1.0},    {GS_S8, -GS_C8},  {GS_R2, -GS_R2},  {GS_C8, -GS_S8}};
+__device__ __forceinline__ double2 with_phase(u32 n, double2 v) {
+  return (n & 15u) ? cmul(kPhase16[n & 15u], v) : v;
+}
 __device__ __forceinline__ double inv_sqrt_norm(double s) {
   return s == 1.0 ? 1.0 : 1.0 / sqrt(s);
 }

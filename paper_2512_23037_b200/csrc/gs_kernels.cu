@@ -20,13 +20,15 @@
 // Everything shot-invariant (x/z tableau trajectory, pivot rows, coordinate
 // basis, draw offsets) was folded into the op stream on the host.
 //
-// Per-element arithmetic mirrors the reference's numpy forms:
+// Per-element arithmetic follows the reference's numpy forms:
 //   complex product  (fma(ar,br,-(ai*bi)), fma(ar,bi,ai*br))
 //   |v|^2            abs2: see gs_common.cuh                     np.abs()**2
 //   prune            |v|^2 > kPrune2 (numpy abs()>1e-12)     ref state.py:298
 //   renormalise      v * (1/sqrt(sum |v|^2))                ref state.py:311
-// so amplitudes agree with the reference to rounding of the (differently
-// ordered) sums only.
+// except the wide kernel's T updates (TF_RED, gs_sweeps.cuh t_mix), which
+// factor T = e^{+-i pi/8} (c I + b' Z) and count the global phase instead of
+// multiplying it in; amplitudes agree with the reference to a few ulps
+// (tests: 1e-12 absolute), records and counters exactly.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -210,6 +212,7 @@ static int upload(gs_engine *e, gs_program *p) {
 struct Section {
   u32 pc0, k0, nm0;
   bool wide;
+  u32 pn0;   // reduced-T phase count on entry: TF_RED ops of earlier wide sections
 };
 
 #ifndef GS_NARROW_SPLIT
@@ -222,7 +225,7 @@ static void sections_of(const gs_program *p, bool wide_only, std::vector<Section
   out.clear();
   const std::vector<u64> &ops = p->ops;
   size_t pc = 0, nm = 0;
-  u32 nops = 0;
+  u32 nops = 0, pn = 0;
   const u32 nn = p->info.num_noise;
   while (pc < ops.size()) {
     const u64 h = ops[pc];
@@ -232,10 +235,14 @@ static void sections_of(const gs_program *p, bool wide_only, std::vector<Section
     const bool split = !wide && (GS_NARROW_SPLIT > 0) && nops >= (u32)GS_NARROW_SPLIT;
     if (out.empty() || out.back().wide != wide || split) {
       while (nm < nn && (u32)p->tables[p->info.noise_off + 4 * nm] < (u32)pc) ++nm;
-      out.push_back(Section{(u32)pc, k, (u32)nm, wide});
+      out.push_back(Section{(u32)pc, k, (u32)nm, wide, pn});
       nops = 0;
     }
     ++nops;
+    // the wide kernel runs TF_RED ops in the reduced form (gs_sweeps.cuh
+    // t_mix); every shot entering a later section executed all of them
+    if (wide && kind == gs::OP_T && (fl & gs::TF_RED) && len > 12)
+      pn = (pn + ((ops[pc + 12] & 2u) ? 15u : 1u)) & 15u;
     if (kind == gs::OP_END || len == 0) break;
     pc += len;
   }
@@ -472,6 +479,7 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
         S.q_out = i + 1 < secs.size() ? e->d_queue[i & 1] : nullptr;
         S.n_out = d_qn + (i & 1);
         S.work = e->d_work + i;
+        S.pn0 = secs[i].pn0;
         if (i >= 1 && i + 1 < secs.size())   // the queue written here was read by section i-1
           CUDA_TRY(cudaMemsetAsync(d_qn + (i & 1), 0, sizeof(u32), st));
         if (secs[i].wide) {

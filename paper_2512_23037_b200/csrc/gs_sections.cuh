@@ -133,6 +133,7 @@ struct DevSec {
   u64 *q_out;              // survivors at the section end (nullptr: last section)
   u32 *n_out;
   unsigned long long *work; // atomic work counter
+  u32 pn0;                 // reduced-T phase count at pc0 (static; see t_mix)
 };
 
 // record words of a slot, rounded to 16 B so the chi rows are double2-aligned
@@ -156,6 +157,13 @@ __device__ __forceinline__ void flush_counters(const DevOut &O, unsigned long lo
 }
 
 // ---------------------------------------------------------------- narrow
+
+// dumps: restore the global phase of earlier reduced T ops (cold path, out
+// of line so the narrow kernel's registers are unaffected)
+__device__ __noinline__ void narrow_dump_phase(double2 *amps, u32 n, u32 pn) {
+#pragma unroll 1
+  for (u32 j = 0; j < n; ++j) amps[j] = with_phase(pn, amps[j]);
+}
 
 // @region narrow: prologue
 template <bool kPhilox>
@@ -633,6 +641,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const u64 stride = 1ull << P.max_dim;
 #pragma unroll 1
           for (u32 j = 0; j < (1u << sk); ++j) O.amps[sl * stride + j] = AN(j);
+          if (S.pn0) narrow_dump_phase(O.amps + sl * stride, 1u << sk, S.pn0);
         }
       }
     }
@@ -754,6 +763,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     if (!philox) fire_pc = 0xFFFFFFFFu;
     if (kG > 1) __syncthreads();   // chi init before the first pass
     u32 kcur = k;
+    u32 pn = S.pn0;   // chi = e^{i pi pn / 8} * A (reduced T ops, TF_RED)
     int status = ST_RUNNING, aux = -1;
     double ps = 1.0;        // renormalisation pending on A (see ldps)
     // SplitMix noise scan state: everything inserted before pc0 is applied
@@ -891,6 +901,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         const double2 bx0 = flip ? cneg(bxs) : bxs;
         const u32 dc = par64(delta & c);
         const u32 tcase = wfl & 3u;
+        // TF_RED: BUTTERFLY / GROW in the reduced form (global phase counted
+        // in pn, see t_mix); word 12: bit 0 = sign of ss, bit 1 = T_DAG
+        const bool red = (wfl & TF_RED) != 0;
         if (tcase == T_DIAG) {
           // beta == 0: pure phase per entry (ref state.py:120-126); the
           // factors have modulus 1, the norm is kept
@@ -932,6 +945,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const u64 w62 = __ldg(op2 + 6);
           Gate g1, g2;
           g1.a = a; g1.bx0 = bx0; g1.cb = cb; g1.dc = dc; g1.dmask = dmask;
+          g1.ss = 0.0; g2.ss = 0.0;
+          if (red) {   // the compiler fuses only pairs of the same form
+            const u64 w12 = __ldg(op + 12), w122 = __ldg(op2 + 12);
+            g1.ss = neg_if1(kTs, ((u32)w12 & 1u) ^ flip);
+            g2.ss = neg_if1(kTs, ((u32)w122 & 1u) ^ flip2);
+            pn = (pn + ((w12 & 2u) ? 15u : 1u) + ((w122 & 2u) ? 15u : 1u)) & 15u;
+          }
           g2.a = make_double2(dbits(__ldg(op2 + 7)), dbits(__ldg(op2 + 8)));
           const double2 bxs2 = make_double2(dbits(__ldg(op2 + 9)), dbits(__ldg(op2 + 10)));
           g2.bx0 = flip2 ? cneg(bxs2) : bxs2;
@@ -941,7 +961,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           mbytes += __ldg(op2 + 11);
           wpc += (u32)((h2 >> 8) & 0xff);
           hnext = __ldg(ops + wpc);
-          const SumNz2 r2 = sweep_butterfly2<kSmemChi, kG>(A, size >> 2, g1, g2);
+          const SumNz2 r2 = red ? sweep_butterfly2<kSmemChi, kG, true>(A, size >> 2, g1, g2)
+                                : sweep_butterfly2<kSmemChi, kG, false>(A, size >> 2, g1, g2);
           gsync<kG>();
           const u32 cnt1 = group_sum_u32<kG>(r2.nz1, grp);
           mbytes += (u64)kEntryBytes * (cin + cnt1);
@@ -955,11 +976,20 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           if (cnt == 0) { status = ST_CORRUPT; aux = (int)instr2; break; }
           continue;
         }
+        Gate g;
+        g.a = a; g.bx0 = bx0; g.cb = cb; g.dc = dc; g.dmask = dmask;
+        g.ss = 0.0;
+        if (red) {
+          const u64 w12 = __ldg(op + 12);
+          g.ss = neg_if1(kTs, ((u32)w12 & 1u) ^ flip);
+          pn = (pn + ((w12 & 2u) ? 15u : 1u)) & 15u;
+        }
         SumNz r;
         if (tcase == T_BUTTERFLY) {
-          r = sweep_butterfly<kSmemChi, kG>(A, size >> 1, cb, dc, dmask, a, bx0);
+          r = red ? sweep_butterfly<kSmemChi, kG, true>(A, size >> 1, g)
+                  : sweep_butterfly<kSmemChi, kG, false>(A, size >> 1, g);
         } else {
-          r = sweep_grow<kSmemChi, kG>(A, size, dc, dmask, a, bx0);
+          r = red ? sweep_grow<kSmemChi, kG, true>(A, size, g) : sweep_grow<kSmemChi, kG, false>(A, size, g);
           kcur = wk + 1;
         }
         gsync<kG>();
@@ -1199,7 +1229,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           }
           const u64 stride = 1ull << P.max_dim;
 #pragma unroll 1
-          for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = ldps(A, j, ps);   // leader warp
+          for (u32 j = lane; j < (1u << kcur); j += 32)   // leader warp
+            O.amps[sl * stride + j] = with_phase(pn, ldps(A, j, ps));
         }
       }
     }

@@ -55,28 +55,52 @@ __device__ __forceinline__ double2 neg_if(double2 v, u32 s) {
                       __longlong_as_double(__double_as_longlong(v.y) ^ m));
 }
 
+// One T gate's pair update new = a v + (-1)^s b w.  kR: the reduced form of
+// a TF_RED op -- T = phi (c I + b' Z) with b' = i ss purely imaginary, the
+// global phase phi = e^{+-i pi/8} left out of chi (the kernel counts it in
+// `pn` and applies it only where amplitudes leave the device, dumps): 4
+// FP64 operations instead of 10 (c v + (-1)^s i ss w).
+constexpr double kTc = GS_C8;   // cos(pi/8), ref state.py:107
+constexpr double kTs = GS_S8;   // sin(pi/8)
+struct Gate {
+  double2 a, bx0;   // full form
+  double ss;        // reduced form: b' = i ss (per-shot sign included)
+  u32 cb, dc, dmask;
+};
+__device__ __forceinline__ double neg_if1(double x, u32 s) {
+  return __longlong_as_double(__double_as_longlong(x) ^ ((long long)s << 63));
+}
+template <bool kR>
+__device__ __forceinline__ double2 t_mix(const Gate &g, double2 v, double2 w, u32 s) {
+  if (kR) {
+    const double sx = neg_if1(g.ss, s);
+    return make_double2(__fma_rn(kTc, v.x, -__dmul_rn(sx, w.y)), __fma_rn(kTc, v.y, __dmul_rn(sx, w.x)));
+  }
+  return cadd(cmul(g.a, v), neg_if(cmul(g.bx0, w), s));
+}
+
 // T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
 // 294-306: a-term then b-term); no renormalisation pending (caller)
-template <bool kS, int kG = 1>
-__device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, u32 dc, u32 dmask,
-                                              double2 a, double2 bx0) {
+template <bool kS, int kG = 1, bool kR = false>
+__device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, const Gate &g) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = glane<kG>();
   gbar_in<kG>();
+  const u32 cb = g.cb, dmask = g.dmask;
   const u32 hb = 31 - __clz(cb);
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
   const u32 jl = ins_bit(lane, hb, 0);
-  const u32 pl = dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
+  const u32 pl = g.dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
 #pragma unroll 1
   for (u32 m = lane; m < half; m += 32u * kG) {
     const u32 jr = ins_bit(m & ~(32u * kG - 1u), hb, 0);
     const u32 j0 = jr | jl, j1 = j0 ^ cb;
     const double2 v0 = A[j0], v1 = A[j1];
     const u32 s0 = pl ^ par32(jr & dmask), s1 = s0 ^ pcb;
-    A[j0] = prune_acc(cadd(cmul(a, v0), neg_if(cmul(bx0, v1), s1)), r.sum, r.nz);
-    A[j1] = prune_acc(cadd(cmul(a, v1), neg_if(cmul(bx0, v0), s0)), r.sum, r.nz);
+    A[j0] = prune_acc(t_mix<kR>(g, v0, v1, s1), r.sum, r.nz);
+    A[j1] = prune_acc(t_mix<kR>(g, v1, v0, s0), r.sum, r.nz);
   }
   return r;
 }
@@ -87,16 +111,13 @@ __device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, u32 cb, 
 // prune -- exactly the two single-gate passes' arithmetic, half the memory
 // traffic and index work.  Groups are enumerated by inserting zeros at the
 // pivot bits h1 = top(cb1) and h2 = top(cb2 reduced by cb1).
-struct Gate {
-  double2 a, bx0;
-  u32 cb, dc, dmask;
-};
 struct SumNz2 {
   double sum;
   u32 nz, nz1;
 };
-template <bool kS, int kG = 1>
-__device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gate g1, Gate g2) {
+template <bool kS, int kG = 1, bool kR = false>
+__device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, const Gate &g1,
+                                                const Gate &g2) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = glane<kG>();
   gbar_in<kG>();
@@ -125,25 +146,25 @@ __device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, Gat
     const u32 p1 = l1 ^ par32(jr & g1.dmask), p2 = l2 ^ par32(jr & g2.dmask);
     // gate 1: pairs (x0, x1), (x2, x3)
     const u32 s0 = p1, s1 = p1 ^ a1, s2 = p1 ^ b1, s3 = p1 ^ a1 ^ b1;
-    const double2 u0 = prune_acc(cadd(cmul(g1.a, v0), neg_if(cmul(g1.bx0, v1), s1)), dummy, r.nz1);
-    const double2 u1 = prune_acc(cadd(cmul(g1.a, v1), neg_if(cmul(g1.bx0, v0), s0)), dummy, r.nz1);
-    const double2 u2 = prune_acc(cadd(cmul(g1.a, v2), neg_if(cmul(g1.bx0, v3), s3)), dummy, r.nz1);
-    const double2 u3 = prune_acc(cadd(cmul(g1.a, v3), neg_if(cmul(g1.bx0, v2), s2)), dummy, r.nz1);
+    const double2 u0 = prune_acc(t_mix<kR>(g1, v0, v1, s1), dummy, r.nz1);
+    const double2 u1 = prune_acc(t_mix<kR>(g1, v1, v0, s0), dummy, r.nz1);
+    const double2 u2 = prune_acc(t_mix<kR>(g1, v2, v3, s3), dummy, r.nz1);
+    const double2 u3 = prune_acc(t_mix<kR>(g1, v3, v2, s2), dummy, r.nz1);
     // gate 2: pairs (x0, x2), (x1, x3)
     const u32 t0 = p2, t1 = p2 ^ a2, t2 = p2 ^ b2, t3 = p2 ^ a2 ^ b2;
-    A[x0] = prune_acc(cadd(cmul(g2.a, u0), neg_if(cmul(g2.bx0, u2), t2)), r.sum, r.nz);
-    A[x2] = prune_acc(cadd(cmul(g2.a, u2), neg_if(cmul(g2.bx0, u0), t0)), r.sum, r.nz);
-    A[x1] = prune_acc(cadd(cmul(g2.a, u1), neg_if(cmul(g2.bx0, u3), t3)), r.sum, r.nz);
-    A[x3] = prune_acc(cadd(cmul(g2.a, u3), neg_if(cmul(g2.bx0, u1), t1)), r.sum, r.nz);
+    A[x0] = prune_acc(t_mix<kR>(g2, u0, u2, t2), r.sum, r.nz);
+    A[x2] = prune_acc(t_mix<kR>(g2, u2, u0, t0), r.sum, r.nz);
+    A[x1] = prune_acc(t_mix<kR>(g2, u1, u3, t3), r.sum, r.nz);
+    A[x3] = prune_acc(t_mix<kR>(g2, u3, u1, t1), r.sum, r.nz);
   }
   (void)dummy;
   return r;
 }
 
-// T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j
-template <bool kS, int kG = 1>
-__device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 dmask, double2 a,
-                                         double2 bx0) {
+// T with a new basis vector: A[j] = a v_j, A[size+j] = b_j v_j (reduced
+// form: c v_j and (-1)^s i ss v_j)
+template <bool kS, int kG = 1, bool kR = false>
+__device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, const Gate &g) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = glane<kG>();
   gbar_in<kG>();
@@ -153,8 +174,15 @@ __device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, u32 dc, u32 d
 #pragma unroll 1
   for (u32 j = lane; j < size; j += 32u * kG) {
     const double2 v = A[j];
-    A[j] = prune_acc(cmul(a, v), r.sum, r.nz);
-    A[size + j] = prune_acc(neg_if(cmul(bx0, v), dc ^ par32(j & dmask)), r.sum, r.nz);
+    const u32 s = g.dc ^ par32(j & g.dmask);
+    if (kR) {
+      const double sx = neg_if1(g.ss, s);
+      A[j] = prune_acc(make_double2(__dmul_rn(kTc, v.x), __dmul_rn(kTc, v.y)), r.sum, r.nz);
+      A[size + j] = prune_acc(make_double2(-__dmul_rn(sx, v.y), __dmul_rn(sx, v.x)), r.sum, r.nz);
+    } else {
+      A[j] = prune_acc(cmul(g.a, v), r.sum, r.nz);
+      A[size + j] = prune_acc(neg_if(cmul(g.bx0, v), s), r.sum, r.nz);
+    }
   }
   return r;
 }
