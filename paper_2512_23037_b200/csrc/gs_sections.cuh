@@ -1027,8 +1027,12 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         // a renormalisation by rs that needs no data movement: deferred to
         // the next pass over chi (ldps); nonzero count unchanged
         auto defer_scale = [&](double rs, double kept) {
-          if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);
-          ps = rs;
+          // a factor of exactly 1 changes no entry: any pending scale stays
+          // pending instead of being applied by a pass now
+          if (rs != 1.0) {
+            if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);
+            ps = rs;
+          }
           nrm_u = __dmul_rn(__dmul_rn(kept, rs), rs);
           nrm_l = gl == 0 ? nrm_u : 0.0;
           nrm_lane0 = true;
