@@ -333,8 +333,8 @@ def main():
             "note": ("achieved = SURVEY 8(d) state-touch bytes of the reference "
                      "layout (24 B per chi entry touched, sign vectors) / kernel "
                      "time; the chi state lives in shared memory, so real DRAM "
-                     "traffic (`traffic`) is ~1 B/shot and the kernel is "
-                     "issue-bound (`issue_active_pct`)"),
+                     "traffic (`traffic`) is the section queues, ~1 KB/shot, "
+                     "and the kernel is issue-bound (`issue_active_pct`)"),
         }
         if ncu:
             # measured HBM traffic of the section queues at this run's rate
