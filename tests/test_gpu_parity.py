@@ -366,3 +366,34 @@ def test_section_chunking_invariance(rng):
     c0 = eng.run_counters(p, Engine.params(9, 100, 5000, 4096, flags))
     c1 = eng.run_counters(p, Engine.params(9, 100, 5000, 4096, flags, chunk_shots=777))
     assert np.array_equal(c0, c1)
+
+
+@pytest.mark.parametrize("flag", [0, _lib.GS_CHI_BLOCK])
+def test_dumps_restore_the_reduced_t_phase(flag):
+    """Reduced-form T ops leave their global phase e^{+-i pi/8} out of chi
+    and count it; dumps must restore it both inside the wide section that
+    ran them (the kernel's count) and in a later narrow section (the static
+    entry count of that section)."""
+    text = ("H 0 1 2 3 4 5 6\nT 0 1 2 3 4 5\nT_DAG 6\n"   # k grows 0..7, wide from k=4
+            "CX 0 1\nM 0 1 2 3\n"                         # back to k=3: narrow
+            "H 0\nS 1\nCX 1 2\n")
+    prog = parse_circuit(text)
+    flat = list(prog.flat())
+    eng = get_engine(0)
+    t_last = max(i for i, ins in enumerate(flat) if ins.name in ("T", "T_DAG"))
+    for stop in (t_last, len(flat) - 1):
+        dp = compile_program(prog, stop_after=stop, keep_frames=True)
+        p = Program(dp)
+        for shot in range(4):
+            seeds = np.array([derive_seed(6, shot)], dtype=np.uint64)
+            d = eng.dump(p, Engine.params(6, 0, 1, 4096, flag, seeds=seeds))
+            ref = orc.run_one_shot(flat, prog.num_qubits, orc.DrawStream("splitmix", 6, shot),
+                                   4096, False, stop_after=stop, snapshot=True)
+            assert int(d["status"][0]) == 1
+            st = reconstruct_state(dp, stop, int(d["sig"][0][0]) |
+                                   (int(d["sig"][0][1]) << prog.num_qubits),
+                                   int(d["c"][0]), d["amps"][0])
+            rs = ref["state"]
+            assert st["ph"] == rs["ph"] and st["idx"] == rs["idx"], (stop, shot)
+            np.testing.assert_allclose(np.array(st["amp"]), np.array(rs["amp"]),
+                                       rtol=0, atol=AMP_TOL)
