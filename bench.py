@@ -140,22 +140,32 @@ class ClockSampler:
 
 
 def cpu_baseline(prog, seconds: float, mode: str, p_noise: float):
-    """Time the CPU oracle port on all host cores for a bounded sample."""
+    """Time the CPU oracle port on all host cores for a bounded sample.
+
+    Always in the reference's own random stream (SHA-1 seeds + SplitMix,
+    ref sampler.py:37-61): the reference has no Philox mode, and the port's
+    pure-Python Philox is ~3x slower than its SplitMix path, which would
+    understate the CPU.  `mode` is recorded only."""
+    mode_run = "splitmix"
     from oracle import gstab_oracle as orc
     cores = os.cpu_count() or 1
-    # calibrate on one core, then size the parallel sample to ~`seconds`
+    # calibrate on one core after a warm-up call (first-call costs: table
+    # builds, numpy dispatch), then size the parallel sample to ~`seconds`
+    # so the process-pool start-up is a small part of it
+    orc.run_counters(prog, 8, 1, mode=mode_run, postselect=True)
     t0 = time.perf_counter()
-    orc.run_counters(prog, 16, 1, mode=mode, postselect=True)
-    per_shot = max((time.perf_counter() - t0) / 16, 1e-5)
-    shots = max(cores * 8, int(seconds * cores / per_shot))
+    orc.run_counters(prog, 64, 1, mode=mode_run, postselect=True)
+    per_shot = max((time.perf_counter() - t0) / 64, 1e-5)
+    shots = max(cores * 32, int(seconds * cores / per_shot))
     t0 = time.perf_counter()
-    c = orc.run_counters_parallel(prog, shots, cores, master_seed=1, mode=mode,
+    c = orc.run_counters_parallel(prog, shots, cores, master_seed=1, mode=mode_run,
                                   postselect=True)
     dt = time.perf_counter() - t0
     return {"value": c["total"] / dt, "unit": "shots/s", "cores": cores,
             "kind": "port",
             "sample": "%d shots of the same workload (oracle/gstab_oracle.py, "
-                      "%d processes, %.1f s)" % (c["total"], cores, dt),
+                      "%d processes, %.1f s, reference SplitMix stream; the GPU "
+                      "arm's stream: %s)" % (c["total"], cores, dt, mode),
             "discard_rate": c["discarded"] / max(c["total"], 1)}
 
 

@@ -1,0 +1,65 @@
+"""Large-sample statistical parity (opt-in: GS_LONG_STATS=1, ~6 min on one
+B200 + 16 host cores): the headline workload (grown d=5 MSC proxy, p=1e-3,
+post-selection) sampled with GS_LONG_GPU_SHOTS Philox shots on the GPU
+against GS_LONG_CPU_SHOTS reference-stream (SplitMix) shots of the CPU
+oracle.  Discard rate and logical-error rate must agree within a binomial
+z < 4.5; the summary line is printed for profiles/.
+
+    GS_LONG_STATS=1 python -m pytest tests/test_gpu_statistics_long.py -m gpu -s
+"""
+
+import json
+import math
+import os
+import time
+
+import pytest
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(os.environ.get("GS_LONG_STATS") != "1",
+                                 reason="opt-in long run (GS_LONG_STATS=1)")]
+
+from oracle import gstab_oracle as orc
+from paper_2512_23037_b200 import SamplerConfig, run_batch
+from paper_2512_23037_b200.msc import msc_grown_circuit
+from paper_2512_23037_b200.noise import apply_noise_model
+
+
+def _z(k1, n1, k2, n2):
+    p = (k1 + k2) / (n1 + n2)
+    se = math.sqrt(max(p * (1 - p), 1e-15) * (1 / n1 + 1 / n2))
+    return abs(k1 / n1 - k2 / n2) / se
+
+
+def test_d5_discard_and_logical_error_rates_large_sample():
+    gpu_shots = int(os.environ.get("GS_LONG_GPU_SHOTS", str(4 * 10 ** 9)))
+    cpu_shots = int(os.environ.get("GS_LONG_CPU_SHOTS", "60000"))
+    prog = apply_noise_model(msc_grown_circuit(5), 1e-3)
+    t0 = time.perf_counter()
+    gpu = run_batch(prog, SamplerConfig(shots=gpu_shots, master_seed=2026,
+                                        postselect=True, rng="philox"))
+    t_gpu = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    cpu = orc.run_counters_parallel(prog, cpu_shots, os.cpu_count() or 1,
+                                    master_seed=7, mode="splitmix", postselect=True)
+    t_cpu = time.perf_counter() - t0
+    z_disc = _z(gpu.discarded_shots, gpu.total_shots, cpu["discarded"], cpu["total"])
+    z_ler = _z(gpu.logical_error_shots, gpu.preserved_shots,
+               cpu["error_shots"], max(cpu["preserved"], 1))
+    lo, hi = gpu.bayes_interval
+    summary = {
+        "workload": "msc_d5_grown_proxy", "p": 1e-3,
+        "gpu": {"shots": gpu.total_shots, "rng": "philox", "wall_s": t_gpu,
+                "shots_per_s": gpu.total_shots / t_gpu,
+                "discard_rate": gpu.discard_rate,
+                "logical_error_rate": gpu.logical_error_rate,
+                "bayes_interval": [lo, hi], "overflow": gpu.overflow_count},
+        "cpu_oracle": {"shots": cpu["total"], "rng": "splitmix", "wall_s": t_cpu,
+                       "discard_rate": cpu["discarded"] / cpu["total"],
+                       "logical_error_rate": cpu["error_shots"] / max(cpu["preserved"], 1),
+                       "processes": os.cpu_count()},
+        "z_discard": z_disc, "z_logical_error": z_ler,
+    }
+    print("LONG_STATS " + json.dumps(summary))
+    assert gpu.total_shots == gpu_shots and gpu.overflow_count == 0
+    assert z_disc < 4.5 and z_ler < 4.5
