@@ -1,9 +1,10 @@
 """Large-sample statistical parity (opt-in: GS_LONG_STATS=1, ~6 min on one
-B200 + 16 host cores): the headline workload (grown d=5 MSC proxy, p=1e-3,
-post-selection) sampled with GS_LONG_GPU_SHOTS Philox shots on the GPU
-against GS_LONG_CPU_SHOTS reference-stream (SplitMix) shots of the CPU
-oracle.  Discard rate and logical-error rate must agree within a binomial
-z < 4.5; the summary line is printed for profiles/.
+B200 + 16 host cores): the headline workload (grown d=5 MSC proxy, p=1e-3)
+and BASELINE configs 2 and 3, post-selected, sampled with billions of
+Philox shots on the GPU against reference-stream (SplitMix) shots of the
+CPU oracle (GS_LONG_SCALE scales both sample sizes).  Discard rate and
+logical-error rate must agree within a binomial z < 4.5; the summary line
+is printed for profiles/.
 
     GS_LONG_STATS=1 python -m pytest tests/test_gpu_statistics_long.py -m gpu -s
 """
@@ -21,7 +22,7 @@ pytestmark = [pytest.mark.gpu,
 
 from oracle import gstab_oracle as orc
 from paper_2512_23037_b200 import SamplerConfig, run_batch
-from paper_2512_23037_b200.msc import msc_grown_circuit
+from paper_2512_23037_b200.msc import injection_circuit, msc_circuit, msc_grown_circuit
 from paper_2512_23037_b200.noise import apply_noise_model
 
 
@@ -31,10 +32,23 @@ def _z(k1, n1, k2, n2):
     return abs(k1 / n1 - k2 / n2) / se
 
 
-def test_d5_discard_and_logical_error_rates_large_sample():
-    gpu_shots = int(os.environ.get("GS_LONG_GPU_SHOTS", str(4 * 10 ** 9)))
-    cpu_shots = int(os.environ.get("GS_LONG_CPU_SHOTS", "60000"))
-    prog = apply_noise_model(msc_grown_circuit(5), 1e-3)
+WORKLOADS = {
+    # name: (builder, p, default GPU shots, default CPU shots)
+    "msc_d5_grown_proxy": (lambda: msc_grown_circuit(5), 1e-3, 4 * 10 ** 9, 60000),
+    # BASELINE config 2: MSC d=3, 1e8 shots on one B200
+    "msc_d3_proxy": (lambda: msc_circuit(3), 1e-3, 10 ** 8, 200000),
+    # BASELINE config 3: d=3 injection + 3 rounds, p=5e-4
+    "d3_injection_3_rounds": (lambda: injection_circuit(3, 3), 5e-4, 10 ** 9, 100000),
+}
+
+
+@pytest.mark.parametrize("name", sorted(WORKLOADS))
+def test_discard_and_logical_error_rates_large_sample(name):
+    build, p_noise, gpu_default, cpu_default = WORKLOADS[name]
+    scale = float(os.environ.get("GS_LONG_SCALE", "1"))
+    gpu_shots = int(gpu_default * scale)
+    cpu_shots = int(cpu_default * scale)
+    prog = apply_noise_model(build(), p_noise)
     t0 = time.perf_counter()
     gpu = run_batch(prog, SamplerConfig(shots=gpu_shots, master_seed=2026,
                                         postselect=True, rng="philox"))
@@ -48,13 +62,14 @@ def test_d5_discard_and_logical_error_rates_large_sample():
                cpu["error_shots"], max(cpu["preserved"], 1))
     lo, hi = gpu.bayes_interval
     summary = {
-        "workload": "msc_d5_grown_proxy", "p": 1e-3,
+        "workload": name, "p": p_noise,
         "gpu": {"shots": gpu.total_shots, "rng": "philox", "wall_s": t_gpu,
                 "shots_per_s": gpu.total_shots / t_gpu,
                 "discard_rate": gpu.discard_rate,
                 "logical_error_rate": gpu.logical_error_rate,
                 "bayes_interval": [lo, hi], "overflow": gpu.overflow_count},
         "cpu_oracle": {"shots": cpu["total"], "rng": "splitmix", "wall_s": t_cpu,
+                       "shots_per_s": cpu["total"] / t_cpu,
                        "discard_rate": cpu["discarded"] / cpu["total"],
                        "logical_error_rate": cpu["error_shots"] / max(cpu["preserved"], 1),
                        "processes": os.cpu_count()},
