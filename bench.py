@@ -186,6 +186,8 @@ def main():
     ap.add_argument("--chi-smem", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
     ap.add_argument("--wide-only", action="store_true")
+    ap.add_argument("--fixed-batch", action="store_true",
+                    help="keep --shots-per-step even when a step is shorter than 0.2 s")
     ap.add_argument("--print-sections", action="store_true",
                     help="print the number of section launches per chunk and exit")
     args = ap.parse_args()
@@ -266,6 +268,24 @@ def main():
     for w in range(args.warmup):
         launch(w)
     torch.cuda.synchronize()
+    # fast workloads: grow the batch so a step lasts >= ~0.2 s (the clock
+    # sampler needs the timed region to span several 100 ms samples); the
+    # headline workload (2^24 shots, ~0.27 s per step) is unaffected
+    if not args.fixed_batch:
+        t0 = time.perf_counter()
+        launch(args.warmup)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        while dt * (S / args.shots_per_step) < 0.2 and S < (1 << 31):
+            S *= 2
+        if world > 1:   # every rank must use the same batch
+            t = torch.tensor([S], dtype=torch.int64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            S = int(t.item())
+        if S != args.shots_per_step:
+            config["shots_per_step_per_gpu"] = S
+            launch(args.warmup)
+            torch.cuda.synchronize()
     counters.zero_()
     if world > 1:
         dist.barrier()
