@@ -1,0 +1,203 @@
+"""The reference's sampler / state / noise semantics tests, restated through
+the CUDA path (ref tests/test_sampler.py:100-199, tests/test_state.py:72-106,
+tests/test_noise.py:62-80).  Single shots go through ``run_shot`` with an
+explicit SplitMix seed exactly like the reference's ``run_text`` helper;
+batch properties through ``run_batch`` / ``sample``; rates against the
+closed forms the reference checks (binomial z < 5)."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import gstab_oracle as orc
+from paper_2512_23037_b200 import (SamplerConfig, ShotContext, derive_seed,
+                                   parse_circuit, run_batch, run_shot, sample)
+from paper_2512_23037_b200.sampler import ShotStatus, _records_before
+
+
+def run_text(text, seed=0, shot=0, **kw):
+    prog = parse_circuit(text)
+    ctx = ShotContext(prog.num_qubits, 4096)
+    ctx.reset(derive_seed(seed, shot))
+    return run_shot(prog, ctx, keep_record=True, **kw)
+
+
+def _rate_ok(k, n, p, z=5.0):
+    return abs(k / n - p) <= z * math.sqrt(p * (1 - p) / n) + 1e-12
+
+
+# -- ref tests/test_sampler.py ----------------------------------------------
+
+def test_mr_resets():
+    assert run_text("X 0\nMR 0\nM 0\n").record == [1, 0]
+
+
+def test_reset_collapses_superposition():
+    for shot in range(20):
+        assert run_text("H 0\nR 0\nM 0\n", shot=shot).record == [0]
+
+
+def test_mpp_products():
+    for shot in range(20):
+        assert run_text("H 0\nCX 0 1\nMPP Z0*Z1 X0*X1\n", shot=shot).record == [0, 0]
+
+
+def test_mpp_flip_argument():
+    assert run_text("MPP(1.0) Z0\n").record == [1]
+
+
+def test_overflow_reports_instruction():
+    prog = parse_circuit("H 0\nH 1\nT 0\nT 1\n")
+    ctx = ShotContext(prog.num_qubits, 2)
+    ctx.reset(derive_seed(0, 0))
+    res = run_shot(prog, ctx)
+    assert res.status is ShotStatus.OVERFLOW
+    assert res.overflow_instruction == 3
+
+
+def test_overflow_rerun_doubles_capacity():
+    prog = parse_circuit("H 0\nH 1\nT 0\nT 1\nM 0\n")
+    st = run_batch(prog, SamplerConfig(shots=5, master_seed=1, entry_capacity=2,
+                                       rerun_on_overflow=True))
+    assert st.overflow_count == 0 and st.preserved_shots == 5
+    st = run_batch(prog, SamplerConfig(shots=5, master_seed=1, entry_capacity=2,
+                                       rerun_on_overflow=False))
+    assert st.overflow_count == 5
+
+
+def test_run_batch_conservation():
+    prog = parse_circuit("H 0\nDEPOLARIZE1(0.3) 0\nM 0\n"
+                         "DETECTOR rec[-1]\nOBSERVABLE_INCLUDE(0) rec[-1]\n")
+    for rng in ("splitmix", "philox"):
+        st = run_batch(prog, SamplerConfig(shots=400, master_seed=3, postselect=True,
+                                           rng=rng))
+        assert (st.preserved_shots + st.discarded_shots + st.overflow_count
+                == st.total_shots == 400)
+        assert 0 < st.discarded_shots < 400
+
+
+def test_run_batch_deterministic_across_batchings():
+    # the reference varies threads / batch_size; here batch_size, the
+    # engine's chunking and the shard split must not change any counter
+    prog = parse_circuit("H 0\nCX 0 1\nDEPOLARIZE1(0.1) 0 1\nT 0\nM 0\nM 1\n"
+                         "DETECTOR rec[-1] rec[-2]\nOBSERVABLE_INCLUDE(0) rec[-1]\n")
+    base = None
+    for batch in (64, 17, 1024):
+        st = run_batch(prog, SamplerConfig(shots=300, master_seed=5, batch_size=batch,
+                                           postselect=True))
+        a = run_batch(prog, SamplerConfig(shots=120, master_seed=5, batch_size=batch,
+                                          postselect=True))
+        b = run_batch(prog, SamplerConfig(shots=180, master_seed=5, batch_size=batch,
+                                          postselect=True), shot_begin=120)
+        key = (st.total_shots, st.preserved_shots, st.discarded_shots,
+               st.overflow_count, st.logical_error_shots,
+               tuple(sorted(st.logical_errors.items())))
+        split = (a.total_shots + b.total_shots, a.preserved_shots + b.preserved_shots,
+                 a.discarded_shots + b.discarded_shots, a.overflow_count + b.overflow_count,
+                 a.logical_error_shots + b.logical_error_shots)
+        assert split == key[:5]
+        base = base or key
+        assert key == base
+
+
+def test_early_discard_matches_full_run():
+    prog = parse_circuit("H 0\nDEPOLARIZE1(0.4) 0\nM 0\nDETECTOR rec[-1]\n"
+                         "X_ERROR(0.3) 0\nM 0\nDETECTOR rec[-1] rec[-2]\n")
+    det_indices = prog.detectors
+    for shot in range(40):
+        full = run_text(prog.serialize(), seed=9, shot=shot, postselect=False)
+        early = run_text(prog.serialize(), seed=9, shot=shot, postselect=True)
+        parities = []
+        for lookups in det_indices:
+            par = 0
+            for m in lookups:
+                par ^= full.record[m]
+            parities.append(par)
+        first_fire = next((i for i, p in enumerate(parities) if p), None)
+        if first_fire is None:
+            assert early.status is ShotStatus.PRESERVED
+        else:
+            assert early.status is ShotStatus.DISCARDED
+            assert early.discarded_detector == first_fire
+
+
+def test_detector_ignored_without_postselect():
+    prog = parse_circuit("X_ERROR(1) 0\nM 0\nDETECTOR rec[-1]\n")
+    assert run_batch(prog, SamplerConfig(shots=64)).discarded_shots == 0
+    assert run_batch(prog, SamplerConfig(shots=64, postselect=True)).discarded_shots == 64
+
+
+def test_feedback_corrects_random_bit():
+    for shot in range(20):
+        rec = run_text("H 0\nM 0\nCX rec[-1] 1\nM 1\n", shot=shot).record
+        assert rec[0] == rec[1]
+
+
+def test_feedback_cz_and_conditional_z():
+    # |+> on 1, CZ controlled by a random record then H: the Z-flip shows up
+    for shot in range(20):
+        rec = run_text("H 0\nM 0\nH 1\nCZ rec[-1] 1\nH 1\nM 1\n", shot=shot).record
+        assert rec[1] == rec[0]
+        rec = run_text("H 0\nM 0\nH 1\nZ rec[-1] 1\nH 1\nM 1\n", shot=shot).record
+        assert rec[1] == rec[0]
+
+
+# -- ref tests/test_state.py (T algebra, branch probabilities) ----------------
+
+def test_t_on_plus_branch_probability():
+    # H T H |0>: P(0) = cos^2(pi/8) (ref test_state.py:72-78)
+    prog = parse_circuit("H 0\nT 0\nH 0\nM 0\n")
+    b = sample(prog, SamplerConfig(shots=1 << 18, master_seed=4))
+    ones = int(b.record_bits()[:, 0].sum())
+    assert _rate_ok(ones, 1 << 18, math.sin(math.pi / 8) ** 2)
+
+
+def test_four_t_gates_merge_to_clifford():
+    # T^4 = Z: H T^4 H |0> = |1> deterministically (ref test_state.py:81-93)
+    for shot in range(8):
+        assert run_text("H 0\nT 0\nT 0\nT 0\nT 0\nH 0\nM 0\n", shot=shot).record == [1]
+
+
+def test_t_dagger_inverts_t():
+    # ref test_state.py:96-106
+    for shot in range(8):
+        assert run_text("H 0\nT 0\nT_DAG 0\nH 0\nM 0\n", shot=shot).record == [0]
+        assert run_text("H 0 1\nT 0 1\nCX 0 1\nCX 0 1\nT_DAG 1 0\nH 0 1\n"
+                        "M 0 1\n", shot=shot).record == [0, 0]
+
+
+# -- ref tests/test_noise.py (channels at the extremes, letter frequencies) ----
+
+@pytest.mark.parametrize("rng", ["splitmix", "philox"])
+def test_error_channels_at_extremes(rng):
+    n = 1 << 14
+    cases = [("X_ERROR(0) 0\nM 0\n", 0.0), ("X_ERROR(1) 0\nM 0\n", 1.0),
+             ("Z_ERROR(1) 0\nM 0\n", 0.0), ("H 0\nZ_ERROR(1) 0\nH 0\nM 0\n", 1.0),
+             # DEPOLARIZE1(1): X, Y, Z uniformly -> M flips with 2/3
+             ("DEPOLARIZE1(1) 0\nM 0\n", 2 / 3),
+             # DEPOLARIZE2(1): 15 non-identity letters, qubit 0 flips on 8
+             ("DEPOLARIZE2(1) 0 1\nM 0\n", 8 / 15),
+             ("X_ERROR(0.5) 0\nM 0\n", 0.5)]
+    for text, p1 in cases:
+        b = sample(parse_circuit(text), SamplerConfig(shots=n, master_seed=8, rng=rng))
+        ones = int(b.record_bits()[:, 0].sum())
+        if p1 in (0.0, 1.0):
+            assert ones == int(p1 * n), (text, rng)
+        else:
+            assert _rate_ok(ones, n, p1), (text, rng, ones / n)
+
+
+def test_extreme_channels_bit_exact_vs_oracle():
+    text = ("H 0\nDEPOLARIZE1(1) 0 1\nX_ERROR(1) 2\nDEPOLARIZE2(1) 1 2\n"
+            "T 0\nM 0 1 2\nDETECTOR rec[-1] rec[-2]\n")
+    prog = parse_circuit(text)
+    for rng in ("splitmix", "philox"):
+        b = sample(prog, SamplerConfig(shots=64, master_seed=3, rng=rng, postselect=True))
+        flat = list(prog.flat())
+        for s in range(64):
+            ref = orc.run_one_shot(flat, prog.num_qubits, orc.DrawStream(rng, 3, s), 4096, True)
+            got = b.result(s, measured=_records_before(prog, b, s))
+            assert got.status.value == ref["status"] and got.record == ref["record"], (rng, s)
