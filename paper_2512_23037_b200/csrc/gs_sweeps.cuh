@@ -27,6 +27,13 @@ __device__ __forceinline__ double2 ldps(const double2 *__restrict__ A, u32 i, do
   const double2 v = A[i];
   return ps != 1.0 ? cscale(v, ps) : v;
 }
+// ldps with the "pending scale?" test hoisted out of a pass: passes are
+// instantiated for both and dispatch once (ps is uniform over the pass)
+template <bool kPS>
+__device__ __forceinline__ double2 ldp(const double2 *__restrict__ A, u32 i, double ps) {
+  const double2 v = A[i];
+  return kPS ? cscale(v, ps) : v;
+}
 // prune at |v| <= 1e-12 (ref state.py:298), accumulating |v|^2 of the kept
 __device__ __forceinline__ double2 prune_acc(double2 v, double &sum, u32 &nz) {
   const double q = abs2(v);
@@ -189,20 +196,26 @@ __device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, const Gate &g
 
 // diagonal phase: A[j] *= (dc ^ par(j & mask)) ? f1 : f0  (T with beta = 0,
 // fired noise Paulis)
-template <bool kS, int kG = 1>
-__device__ __forceinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask,
+template <bool kS, int kG, bool kPS>
+__device__ __forceinline__ void sweep_phase_impl(double2 *A_, u32 size, u32 dc, u32 mask,
                                          double2 f0, double2 f1, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = glane<kG>();
   gbar_in<kG>();
 #pragma unroll 1
   for (u32 j = lane; j < size; j += 32u * kG)
-    A[j] = cmul(ldps(A, j, ps), (dc ^ par32(j & mask)) ? f1 : f0);
+    A[j] = cmul(ldp<kPS>(A, j, ps), (dc ^ par32(j & mask)) ? f1 : f0);
+}
+template <bool kS, int kG = 1>
+__device__ __forceinline__ void sweep_phase(double2 *A_, u32 size, u32 dc, u32 mask,
+                                         double2 f0, double2 f1, double ps) {
+  if (ps == 1.0) sweep_phase_impl<kS, kG, false>(A_, size, dc, mask, f0, f1, ps);
+  else sweep_phase_impl<kS, kG, true>(A_, size, dc, mask, f0, f1, ps);
 }
 
 // beta = 0 measurement weights: (sum over +1 eigen-entries, sum over -1)
-template <bool kS, int kG = 1>
-__device__ __forceinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask, u32 neg0,
+template <bool kS, int kG, bool kPS>
+__device__ __forceinline__ double2 sweep_det_sums_impl(double2 *A_, u32 size, u32 dmask, u32 neg0,
                                                double ps) {
   const double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = glane<kG>();
@@ -210,15 +223,21 @@ __device__ __forceinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dma
   double sp = 0.0, sm = 0.0;
 #pragma unroll 1
   for (u32 j = lane; j < size; j += 32u * kG) {
-    const double a2 = abs2(ldps(A, j, ps));
+    const double a2 = abs2(ldp<kPS>(A, j, ps));
     if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
   }
   return make_double2(sp, sm);
 }
+template <bool kS, int kG = 1>
+__device__ __forceinline__ double2 sweep_det_sums(double2 *A_, u32 size, u32 dmask, u32 neg0,
+                                               double ps) {
+  if (ps == 1.0) return sweep_det_sums_impl<kS, kG, false>(A_, size, dmask, neg0, ps);
+  return sweep_det_sums_impl<kS, kG, true>(A_, size, dmask, neg0, ps);
+}
 
 // keep the chosen eigen-entries, scaled by rs; zero the others
-template <bool kS, int kG = 1>
-__device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32 neg0,
+template <bool kS, int kG, bool kPS>
+__device__ __forceinline__ SumNz sweep_filter_impl(double2 *A_, u32 size, u32 dmask, u32 neg0,
                                            u32 want_neg, double rs, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = glane<kG>();
@@ -228,7 +247,7 @@ __device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, 
   r.nz = 0;
 #pragma unroll 1
   for (u32 j = lane; j < size; j += 32u * kG) {
-    const double2 v = ldps(A, j, ps);
+    const double2 v = ldp<kPS>(A, j, ps);
     if ((neg0 ^ par32(j & dmask)) == want_neg) {
       const double2 w = cscale(v, rs);
       A[j] = w;
@@ -240,12 +259,18 @@ __device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, 
   }
   return r;
 }
+template <bool kS, int kG = 1>
+__device__ __forceinline__ SumNz sweep_filter(double2 *A_, u32 size, u32 dmask, u32 neg0,
+                                           u32 want_neg, double rs, double ps) {
+  if (ps == 1.0) return sweep_filter_impl<kS, kG, false>(A_, size, dmask, neg0, want_neg, rs, ps);
+  return sweep_filter_impl<kS, kG, true>(A_, size, dmask, neg0, want_neg, rs, ps);
+}
 
 // in-place compaction dropping coordinate isq: A[jp] = rs * A[src(jp)],
 // src(jp) = j0 | ((tau ^ par(j0 & mask)) << isq), j0 = jp with a 0 inserted
 // at isq; src(jp) >= jp, so reads of a round finish before its writes
-template <bool kS, int kG = 1>
-__device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
+template <bool kS, int kG, bool kPS>
+__device__ __forceinline__ SumNz sweep_compact_impl(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
                                             double rs, double ps) {
   double2 *__restrict__ A = chi_ptr<kS>(A_);
   const u32 lane = glane<kG>();
@@ -259,7 +284,7 @@ __device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u
     double2 v = make_double2(0.0, 0.0);
     if (jp < half) {
       const u32 j0 = ins_bit(jp, isq, 0);
-      v = ldps(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
+      v = ldp<kPS>(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
     }
     gsync<kG>();
     if (jp < half) {
@@ -271,6 +296,12 @@ __device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u
     gsync<kG>();
   }
   return r;
+}
+template <bool kS, int kG = 1>
+__device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
+                                            double rs, double ps) {
+  if (ps == 1.0) return sweep_compact_impl<kS, kG, false>(A_, half, isq, mask, tau, rs, ps);
+  return sweep_compact_impl<kS, kG, true>(A_, half, isq, mask, tau, rs, ps);
 }
 
 // pivot measurement (ref state.py:178-208): w(m) = rep + sg * xi * part.
