@@ -432,6 +432,8 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             }
             if (tau) sc ^= vec;
             sk = k - 1;
+          } else if (rs == 1.0 && dmask == 0 && neg0 == want_neg) {
+            nz = scnt;   // every entry kept and scaled by exactly 1: nothing changes
           } else {
 #pragma unroll 1
             for (u32 j = 0; j < size; ++j) {
