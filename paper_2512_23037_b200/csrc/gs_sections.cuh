@@ -208,6 +208,9 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     u64 sl = 0, shot = 0, seed = 0;
     u64 s_lo = 0, s_hi = 0, sc = 0, sobs = 0, smb = 0;
     u32 scnt = 1, sk = S.k0;
+    // chi unchanged since a sum of all |v|^2 came out exactly 1 (so the next
+    // dmask = 0 measurement's sums are known without the loop)
+    bool sone = false;
     int sst = valid ? ST_RUNNING : ST_PRESERVED, saux = -1;
     // Philox fire schedule of this shot
     u32 sgj = 0, sgpos = 0xFFFFFFFFu, sfire = 0xFFFFFFFFu;
@@ -219,6 +222,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 #pragma unroll 1
       for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
       AN(0) = make_double2(1.0, 0.0);
+      sone = true;
       if (philox && valid && P.geo_len > 1 && P.nlocs) {
         const GeoCand gc = geo_candidate(tables + P.geo_off, P.geo_len, P.geo_ilq, R.master, shot, 0u, 0u);
         sgpos = gc.pos;
@@ -258,6 +262,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       // @region narrow: noise
       // apply E to this lane's shot (ref state.py:88-102)
       auto lane_error = [&](u64 ex, u64 ez, const u64 *nrec, u32 size) {
+        sone = false;
         const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3), s_lo, s_hi);
         const double2 php = ipow(e.xi);
         const double2 phm = cneg(php);
@@ -325,6 +330,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 
       // @region narrow: T
       if (kind == OP_T) {
+        sone = false;
         s_lo ^= __ldg(op + 1);
         s_hi ^= __ldg(op + 2);
         const u32 flip = par64(s_lo & __ldg(op + 3)) ^ par64(s_hi & __ldg(op + 4));
@@ -411,11 +417,18 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           // beta == 0: filter by eigenvalue (ref state.py:162-176)
           const u32 neg0 = (xi0 >> 1) ^ dc;
           double sp = 0.0, sm = 0.0;
+          if (sone && dmask == 0) {
+            // same entries, same order: the loop would return exactly these
+            sp = neg0 ? 0.0 : 1.0;
+            sm = neg0 ? 1.0 : 0.0;
+          } else {
 #pragma unroll 1
-          for (u32 j = 0; j < size; ++j) {
-            const double a2 = abs2(AN(j));
-            if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+            for (u32 j = 0; j < size; ++j) {
+              const double a2 = abs2(AN(j));
+              if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+            }
           }
+          sone = false;
           plus = pick_plus(sp);
           const double chosen = plus ? sp : __dsub_rn(1.0, sp);
           if (chosen < 1e-12) { sst = ST_CORRUPT; saux = (int)instr; continue; }
@@ -434,6 +447,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             sk = k - 1;
           } else if (rs == 1.0 && dmask == 0 && neg0 == want_neg) {
             nz = scnt;   // every entry kept and scaled by exactly 1: nothing changes
+            sone = true;
           } else {
 #pragma unroll 1
             for (u32 j = 0; j < size; ++j) {
@@ -445,6 +459,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           }
         } else {
           // beta != 0: pair-merge + tableau pivot (ref state.py:178-208)
+          sone = false;
           const double2 xpp = ipow(xi0);
           const double2 xpm = cneg(xpp);
           const u32 ct = (u32)(sc >> t) & 1u;
