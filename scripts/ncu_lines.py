@@ -98,7 +98,7 @@ def main():
     import re as _re
     kn = _re.search(r"(\w+_kernel)<([^>]*)>", kname)
     targs = [a.strip() for a in kn.group(2).split(",")] if kn else []
-    kn = kn.group(1) if kn else "sample_kernel"
+    kn = kn.group(1) if kn else "wide_kernel"
     # Itanium mangling of the template arguments: (bool)1 -> Lb1E, 16 -> Li16E
     code = {"bool": "b", "int": "i", "unsigned int": "j"}
 
