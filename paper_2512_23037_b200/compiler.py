@@ -62,6 +62,9 @@ TF_FUSE = 1 << 4     # T flag: apply together with the next (BUTTERFLY) op
 # e^{+-i pi/8} counted instead of multiplied in (gs_sweeps.cuh t_mix);
 # payload word 12: bit 0 = ss < 0, bit 1 = T_DAG
 TF_RED = 1 << 5
+# T flag: like TF_FUSE, but noise is inserted before the partner; the
+# Philox-mode device fuses only when none of it fires for the shot
+TF_FUSEQ = 1 << 6
 # measurement cases
 M_DET, M_PIVOT_SPAN, M_PIVOT_NOSPAN = 0, 1, 2
 # measurement flags (bits of the header flag byte, above the 2-bit case and
@@ -695,22 +698,24 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
 
 def _mark_fused_t_pairs(ops, noise_pcs):
     """Set TF_FUSE on a T BUTTERFLY op whose successor is a T BUTTERFLY of
-    the same dimension with a different partner vector and no noise inserted
+    the same dimension with a different partner vector, no noise inserted
     between them and the same TF_RED form: the device applies both gates in
     one pass over 4-element groups (same arithmetic and pruning order as two
-    passes).  Pairs are taken greedily left to right."""
+    passes).  With noise inserted before the successor the flag is TF_FUSEQ:
+    the Philox-mode device fuses only when none of that noise fires for the
+    shot (its schedule knows), else runs the two gates separately.  Pairs
+    are taken greedily left to right."""
     pc = 0
     prev = None
     while True:
         kind, ln, k, fl, _ = decode_header(ops[pc])
         if kind == OP_END:
             break
-        if (prev is not None and kind == OP_T and (fl & 3) == T_BUTTERFLY
-                and pc not in noise_pcs):
+        if prev is not None and kind == OP_T and (fl & 3) == T_BUTTERFLY:
             ppc, pk, pcb, pred = prev
             cb = ops[pc + 6] & 0xFFFFFFFF
             if pk == k and pcb != cb and k >= 2 and pred == (fl & TF_RED):
-                ops[ppc] |= TF_FUSE << 24
+                ops[ppc] |= (TF_FUSEQ if pc in noise_pcs else TF_FUSE) << 24
                 prev = None
                 pc += ln
                 continue

@@ -7,6 +7,7 @@ enum { OP_END = 0, OP_T = 1, OP_MEAS = 2, OP_NOISE = 3, OP_FEEDBACK = 4,
 enum { T_DIAG = 0, T_BUTTERFLY = 1, T_GROW = 2 };
 enum { TF_FUSE = 16 };   // T flag: apply together with the next BUTTERFLY op
 enum { TF_RED = 32 };    // T flag: BUTTERFLY / GROW in the reduced form (t_mix)
+enum { TF_FUSEQ = 64 };  // T flag: TF_FUSE if no noise fires before the partner (Philox)
 enum { M_DET = 0, M_PIVOT_SPAN = 1, M_PIVOT_NOSPAN = 2 };
 enum { MF_RECORD = 16, MF_FLIP = 32, MF_RESET = 64, MF_COMPACT = 128 };
 enum { NK_DEP1 = 0, NK_DEP2 = 1, NK_XERR = 2, NK_ZERR = 3 };

@@ -950,7 +950,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
         if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);   // rare: right after a deferral
         ps = 1.0;
-        if (tcase == T_BUTTERFLY && (wfl & TF_FUSE)) {
+        // TF_FUSEQ: the partner follows a noise insertion; fusable when the
+        // shot's Philox schedule puts no candidate there (fire_pc > its pc)
+        if (tcase == T_BUTTERFLY && ((wfl & TF_FUSE) || (kPhilox && (wfl & TF_FUSEQ) && fire_pc > wpc))) {
           // this gate and the next one (also a BUTTERFLY at the same k, no
           // noise between) in one pass
           const u64 *op2 = ops + wpc;
