@@ -15,7 +15,7 @@ import random
 
 from paper_2512_23037_b200 import msc
 from paper_2512_23037_b200.compiler import (OP_END, OP_T, T_BUTTERFLY, T_DIAG,
-                                            TF_FUSE, TF_RED, compile_program,
+                                            TF_FUSE, TF_FUSEQ, TF_RED, compile_program,
                                             decode_header)
 from paper_2512_23037_b200.noise import apply_noise_model
 
@@ -69,15 +69,22 @@ def test_reduced_form_reproduces_the_full_constants():
     assert n_red > 50 and n_full > 0
 
 
+def _noise_pcs(dp):
+    return {int(dp.tables[dp.noise_off + 4 * m]) & 0xFFFFFFFF for m in range(dp.num_noise)}
+
+
 def test_fused_pairs_share_dimension_and_form():
+    n_q = 0
     for prog in _programs():
         dp = compile_program(prog)
+        noise = _noise_pcs(dp)
         tops = list(_t_ops(dp))
         by_pc = {pc: (k, fl, w) for pc, k, fl, w in tops}
         pcs = [pc for pc, *_ in tops]
         for i, (pc, k, fl, w) in enumerate(tops):
-            if not fl & TF_FUSE:
+            if not fl & (TF_FUSE | TF_FUSEQ):
                 continue
+            assert not (fl & TF_FUSE and fl & TF_FUSEQ)
             assert (fl & 3) == T_BUTTERFLY and k >= 2
             nxt = pcs[i + 1]
             k2, fl2, w2 = by_pc[nxt]
@@ -87,7 +94,12 @@ def test_fused_pairs_share_dimension_and_form():
             assert (fl2 & 3) == T_BUTTERFLY and k2 == k
             assert (fl2 & TF_RED) == (fl & TF_RED)
             assert (w2[5] & 0xFFFFFFFF) != (w[5] & 0xFFFFFFFF)
-            assert not fl2 & TF_FUSE
+            assert not fl2 & (TF_FUSE | TF_FUSEQ)
+            # TF_FUSE: no noise before the partner; TF_FUSEQ: noise there
+            # (the device fuses only when none of it fires)
+            assert (nxt in noise) == bool(fl & TF_FUSEQ)
+            n_q += bool(fl & TF_FUSEQ)
+    assert n_q > 0
 
 
 def test_random_programs_compile_both_forms():
