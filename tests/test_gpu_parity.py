@@ -255,12 +255,15 @@ def test_msc_noiseless_is_deterministic(d):
     assert st.preserved_shots == 4096
 
 
+@pytest.mark.parametrize("mode", ["splitmix", "philox"])
 @pytest.mark.parametrize("variant", ["default", "wide_only", "chi_global",
                                      "chi_smem", "wide_only_chi_smem", "chi_block",
                                      "chi_block_global", "wide_only_chi_block"])
-def test_chi_storage_modes_match_oracle(variant):
+def test_chi_storage_modes_match_oracle(variant, mode):
     """Lane-per-shot / warp-per-shot / block-per-shot execution and shared- /
-    global-memory chi buffers must all give the oracle's results."""
+    global-memory chi buffers must all give the oracle's results, in both
+    random streams (Philox also exercises the conditional T-pair fusion,
+    TF_FUSEQ, which depends on the shot's noise schedule)."""
     rng = random.Random(7)
     flags_extra = {"default": 0, "wide_only": _lib.GS_WIDE_ONLY,
                    "chi_global": _lib.GS_CHI_GLOBAL, "chi_smem": _lib.GS_CHI_SMEM,
@@ -275,11 +278,13 @@ def test_chi_storage_modes_match_oracle(variant):
         dp = compile_program(prog)
         p = Program(dp)
         flags = _lib.GS_POSTSELECT * (it % 2) | flags_extra
+        if mode == "philox":
+            flags |= _lib.GS_RNG_PHILOX
         par = Engine.params(3 + it, 0, 16, 4096, flags)
         status, aux, rec, obs = eng.run_records(p, par)
         from paper_2512_23037_b200.sampler import ShotBatch
         b = ShotBatch(status, aux, rec, obs, list(dp.obs_keys), dp.num_measurements)
-        ref = _oracle_results(prog, 3 + it, 16, 4096, bool(it % 2))
+        ref = _oracle_results(prog, 3 + it, 16, 4096, bool(it % 2), mode=mode)
         for i in range(16):
             r = b.result(i, measured=_records_before(prog, b, i))
             assert r.status.value == ref[i]["status"], (variant, it, i)
@@ -397,3 +402,27 @@ def test_dumps_restore_the_reduced_t_phase(flag):
             assert st["ph"] == rs["ph"] and st["idx"] == rs["idx"], (stop, shot)
             np.testing.assert_allclose(np.array(st["amp"]), np.array(rs["amp"]),
                                        rtol=0, atol=AMP_TOL)
+
+
+@pytest.mark.parametrize("flag", [0, _lib.GS_WIDE_ONLY, _lib.GS_CHI_BLOCK])
+def test_conditional_pair_fusion_matches_oracle(flag):
+    """TF_FUSEQ pairs (T gates with a noise insertion between them) are fused
+    only for shots whose Philox schedule has no candidate there: with noise
+    strong enough that many shots do fire there, every shot's record and
+    status must still equal the oracle's (which never fuses)."""
+    from paper_2512_23037_b200.msc import msc_grown_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    from paper_2512_23037_b200.compiler import TF_FUSEQ, decode_header
+    prog = apply_noise_model(msc_grown_circuit(5), 4e-3)
+    dp = compile_program(prog)
+    pc, n_q = 0, 0
+    while pc < len(dp.ops):
+        kind, ln, _, fl, _ = decode_header(int(dp.ops[pc]))
+        n_q += kind == 1 and bool(fl & TF_FUSEQ)
+        if kind == 0:
+            break
+        pc += ln
+    assert n_q > 0
+    got = _gpu_results(prog, 21, 48, 4096, False, rng="philox", flags_extra=flag)
+    ref = _oracle_results(prog, 21, 48, 4096, False, mode="philox")
+    assert got == ref
