@@ -250,10 +250,11 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 
     u32 pc = S.pc0, nm = S.nm0;
     u32 exit_k = 0;
+    u64 hnext = __ldg(ops + pc);
 #pragma unroll 1
     for (;;) {
       if (!__any_sync(FULL, sst == ST_RUNNING)) break;
-      const u64 h = __ldg(ops + pc);
+      const u64 h = hnext;
       const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
       const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
       const u32 instr = (u32)(h >> 32);
@@ -325,6 +326,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         }
       }
       pc += len;
+      hnext = __ldg(ops + pc);   // the next header, loaded while this op runs
       if (sst != ST_RUNNING) continue;
       sk = k;
 
