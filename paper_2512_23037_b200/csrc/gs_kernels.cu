@@ -440,7 +440,10 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   // queues between sections: fixed slots, chunks of at most `chunk` shots
   const u64 slot_b = 8ull * (gs::Q_HDR + gs::rec_u64(P.rec_words32) + 2 * (1u << GS_KN));
   u64 chunk = r->shot_count ? r->shot_count : 1;
-  const u64 qbudget = (u64)2 << 30;   // bytes per queue
+#ifndef GS_QUEUE_GB
+#define GS_QUEUE_GB 8   // per section queue: one chunk for a 2^24-shot step (A/B +0.4 % over 2 GB)
+#endif
+  const u64 qbudget = (u64)GS_QUEUE_GB << 30;   // bytes per queue
   if (secs.size() > 1 && chunk * slot_b > qbudget) chunk = std::max<u64>(32, qbudget / slot_b);
   if (r->chunk_shots && r->chunk_shots < chunk) chunk = r->chunk_shots;   // tests
   if (secs.size() > 1) {
