@@ -63,7 +63,7 @@ TF_FUSE = 1 << 4     # T flag: apply together with the next (BUTTERFLY) op
 # payload word 12: bit 0 = ss < 0, bit 1 = T_DAG
 TF_RED = 1 << 5
 # T flag: like TF_FUSE, but noise is inserted before the partner; the
-# Philox-mode device fuses only when none of it fires for the shot
+# device fuses only when none of it fires for the shot
 TF_FUSEQ = 1 << 6
 # measurement cases
 M_DET, M_PIVOT_SPAN, M_PIVOT_NOSPAN = 0, 1, 2
@@ -702,8 +702,9 @@ def _mark_fused_t_pairs(ops, noise_pcs):
     between them and the same TF_RED form: the device applies both gates in
     one pass over 4-element groups (same arithmetic and pruning order as two
     passes).  With noise inserted before the successor the flag is TF_FUSEQ:
-    the Philox-mode device fuses only when none of that noise fires for the
-    shot (its schedule knows), else runs the two gates separately.  Pairs
+    the device fuses only when none of that noise fires for the shot (the
+    Philox schedule or the scanned SplitMix fire bits say so), else runs the
+    two gates separately.  Pairs
     are taken greedily left to right."""
     pc = 0
     prev = None

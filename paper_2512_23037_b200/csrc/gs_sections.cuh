@@ -952,9 +952,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
         if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);   // rare: right after a deferral
         ps = 1.0;
-        // TF_FUSEQ: the partner follows a noise insertion; fusable when the
-        // shot's Philox schedule puts no candidate there (fire_pc > its pc)
-        if (tcase == T_BUTTERFLY && ((wfl & TF_FUSE) || (kPhilox && (wfl & TF_FUSEQ) && fire_pc > wpc))) {
+        // TF_FUSEQ: the partner follows a noise insertion; fusable when no
+        // location there fires for this shot: Philox -- its schedule has no
+        // candidate up to the partner (fire_pc > its pc); SplitMix -- every
+        // fire-bit word that can hold those locations is scanned
+        // (next_word_pc > its pc; always true in Philox mode) and none fired
+        if (tcase == T_BUTTERFLY &&
+            ((wfl & TF_FUSE) || ((wfl & TF_FUSEQ) && fire_pc > wpc && next_word_pc > wpc))) {
           // this gate and the next one (also a BUTTERFLY at the same k, no
           // noise between) in one pass
           const u64 *op2 = ops + wpc;
