@@ -474,7 +474,7 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
         S.pc0 = secs[i].pc0;
         S.k0 = secs[i].k0;
         S.nm0 = secs[i].nm0;
-        S.pc_end = (i + 1 < secs.size() && !secs[i + 1].wide) ? secs[i + 1].pc0 : 0xFFFFFFFFu;
+        S.pc_end = i + 1 < secs.size() ? secs[i + 1].pc0 : 0xFFFFFFFFu;   // the next section's first op
         S.first = first;
         S.count = count;
         S.q_in = i ? e->d_queue[(i - 1) & 1] : nullptr;

@@ -126,7 +126,7 @@ enum { Q_SL = 0, Q_LO, Q_HI, Q_C, Q_OBS, Q_MB, Q_PICK, Q_SEED, Q_CNTK, Q_GEO, Q_
 
 struct DevSec {
   u32 pc0, k0, nm0;        // first op, its chi dimension, first noise instr. with ipc >= pc0
-  u32 pc_end;              // narrow: stop before this op (0xFFFFFFFF: at the first wide op)
+  u32 pc_end;              // stop before this op: the next section's first (0xFFFFFFFF: last section)
   u64 first, count;        // fresh shots (q_in == nullptr): run-local indices [first, first+count)
   const u64 *q_in;         // else: queue slots and their number
   const u32 *n_in;
@@ -258,7 +258,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
       const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
       const u32 instr = (u32)(h >> 32);
-      if (pc == S.pc_end || op_is_wide(kind, k, fl)) { exit_k = k; break; }   // section end
+      if (pc == S.pc_end) { exit_k = k; break; }   // the next section starts (host plan)
       // ============================== narrow op, lane per shot
       // @region narrow: noise
       // apply E to this lane's shot (ref state.py:88-102)
@@ -708,7 +708,6 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   const u64 *__restrict__ locs = P.locs;
   const double2 Z = make_double2(0.0, 0.0);
   constexpr bool philox = kPhilox;
-  const bool wide_only = (R.flags & GS_WIDE_ONLY) != 0;
   const u32 sign_bytes = 2u * ((2u * n + 7u) / 8u);
   const u32 SU = slot_u64(P);
   (void)n;
@@ -797,11 +796,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     u32 exit_pc = 0xFFFFFFFFu;
 #pragma unroll 1
     while (status == ST_RUNNING) {
-      if (!wide_only) {
-        const u32 kind_ = (u32)(hnext & 0xff), k_ = (u32)((hnext >> 16) & 0xff),
-                  fl_ = (u32)((hnext >> 24) & 0xff);
-        if (!op_is_wide(kind_, k_, fl_)) { exit_pc = wpc; break; }
-      }
+      if (wpc == S.pc_end) { exit_pc = wpc; break; }   // the next (narrow) section starts
       // @region wide: noise
       if (wpc >= next_word_pc || wpc >= fire_pc) {
         // apply E = OR of fired letters of one noise instruction
