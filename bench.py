@@ -10,11 +10,17 @@ is bracketed by CUDA events on the launching stream; L2 is flushed (256 MiB
 write) between steps outside the events; the max over ranks is reported.
 
 Extra keys: ``roofline`` (state-touch model bytes counted on device / kernel
-time vs measured HBM copy bandwidth), ``cpu_baseline`` (the CPU oracle port
-timed on this host's cores, rank 0, bounded sample), ``e2e`` (the public
+time vs measured HBM copy bandwidth), ``cpu_baseline`` (the reference
+itself -- oracle/_ref, built by oracle/build_ref.py with its Cython backend --
+through its own run_batch on all host cores, rank 0, bounded sample; the
+oracle port when oracle/_ref is absent or with --ref-port), ``e2e`` (the public
 C-ABI path with host buffers: program upload + launch + counter readback),
 ``clocks`` (nvidia-smi sampled during the timed region) and
 ``gpu_launches``.
+
+``--impl reference``: each step is one reference ``run_batch`` call
+(threads = all host cores, batch_size=1024, post-selection) over a bounded
+sample of the same workload, parsed and noised by the reference itself.
 """
 
 from __future__ import annotations
@@ -82,7 +88,7 @@ def _workload(key: str, p: float):
     from paper_2512_23037_b200.circuit import compute_stats
     name, make = WORKLOADS[key]
     base = make(msc)
-    return name, apply_noise_model(base, p), compute_stats(base).as_dict()
+    return name, apply_noise_model(base, p), compute_stats(base).as_dict(), base.serialize()
 
 
 class ClockSampler:
@@ -169,6 +175,61 @@ def cpu_baseline(prog, seconds: float, mode: str, p_noise: float):
             "discard_rate": c["discarded"] / max(c["total"], 1)}
 
 
+def _ref_program(text: str, p: float):
+    """The workload parsed and noised by the reference itself (oracle/_ref:
+    gstab.circuit.parse_circuit, gstab.noise.apply_noise_model)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from build_ref import import_reference
+    gstab = import_reference()
+    prog = gstab.circuit.parse_circuit(text)
+    return gstab, (gstab.noise.apply_noise_model(prog, p) if p > 0 else prog)
+
+
+def reference_run(gstab, prog, shots: int, shot_begin: int, cores: int):
+    """One bounded sample through the reference's own public API:
+    gstab.sampler.run_batch(prog, SamplerConfig(threads=cores,
+    batch_size=1024, postselect=True)) (ref sampler.py:348-382), timed by
+    the wall clock around the call (its process pool included).  The shot
+    range is moved by re-keying the master seed (seeds are per (master,
+    shot), ref sampler.py:37-42)."""
+    cfg = gstab.sampler.SamplerConfig(shots=shots, master_seed=1 + shot_begin,
+                                      threads=cores, batch_size=1024,
+                                      postselect=True)
+    t0 = time.perf_counter()
+    st = gstab.sampler.run_batch(prog, cfg)
+    dt = time.perf_counter() - t0
+    return st, dt
+
+
+def reference_baseline(text: str, p: float, seconds: float):
+    """The real reference (oracle/_ref, Cython backend) on all host cores
+    for a bounded ~`seconds` sample of the workload, in its own SplitMix
+    stream."""
+    gstab, prog = _ref_program(text, p)
+    cores = os.cpu_count() or 1
+    # calibrate on one core (first call pays imports / dispatch), then size
+    # the parallel sample
+    cal = gstab.sampler.SamplerConfig(shots=8, master_seed=99, postselect=True)
+    gstab.sampler.run_batch(prog, cal)
+    cal = gstab.sampler.SamplerConfig(shots=48, master_seed=98, postselect=True)
+    t0 = time.perf_counter()
+    gstab.sampler.run_batch(prog, cal)
+    per_shot = max((time.perf_counter() - t0) / 48, 1e-5)
+    shots = max(cores * 64, int(seconds * cores / per_shot) // 1024 * 1024)
+    st, dt = reference_run(gstab, prog, shots, 0, cores)
+    return {"value": st.total_shots / dt, "unit": "shots/s", "cores": cores,
+            "kind": "reference", "backend": gstab.backend.name(),
+            "sample": "%d shots of the same workload through the reference's "
+                      "run_batch (oracle/_ref gstab, %s backend, threads=%d, "
+                      "batch_size=1024, %.1f s, its SplitMix stream)"
+                      % (st.total_shots, gstab.backend.name(), cores, dt),
+            "discard_rate": st.discarded_shots / max(st.total_shots, 1)}
+
+
+def _have_reference() -> bool:
+    return os.path.isfile(os.path.join(ROOT, "oracle", "_ref", "gstab", "sampler.py"))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
@@ -182,6 +243,8 @@ def main():
     ap.add_argument("--rng", default="philox", choices=["philox", "splitmix"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-port", action="store_true",
+                    help="time the oracle port instead of the reference (oracle/_ref)")
     ap.add_argument("--chi-global", action="store_true")
     ap.add_argument("--chi-smem", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
@@ -197,7 +260,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.p is None:
         args.p = DEFAULT_P.get(args.workload, 1e-3)
-    workload, prog, stats = _workload(args.workload, args.p)
+    workload, prog, stats, text = _workload(args.workload, args.p)
     config = {"workload": workload, "noise_p": args.p, "postselect": True,
               "rng": args.rng, "shots_per_step_per_gpu": args.shots_per_step,
               "circuit": stats, "parallelism": "shot-dp%d" % world,
@@ -206,20 +269,52 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        vals = []
-        samples = []
-        for _ in range(args.warmup + args.steps):
-            cb = cpu_baseline(prog, max(2.0, args.cpu_seconds / 3), args.rng, args.p)
-            vals.append(cb["value"])
-            samples.append(cb)
-        v = sorted(vals[args.warmup:])[len(vals[args.warmup:]) // 2]
-        cb = samples[-1]
-        cb["value"] = v
+        cores = os.cpu_count() or 1
+        if _have_reference() and not args.ref_port:
+            # the reference itself: each step is one run_batch call over a
+            # bounded sample of the workload on all host cores
+            gstab, rprog = _ref_program(text, args.p)
+            cal = gstab.sampler.SamplerConfig(shots=48, master_seed=98, postselect=True)
+            gstab.sampler.run_batch(rprog, cal)
+            t0 = time.perf_counter()
+            gstab.sampler.run_batch(rprog, cal)
+            per_shot = max((time.perf_counter() - t0) / 48, 1e-5)
+            step_s = max(1.0, args.cpu_seconds / 4)
+            shots = max(cores * 64, int(step_s * cores / per_shot) // 1024 * 1024)
+            tot_shots = tot_s = 0.0
+            disc = 0
+            for s_ in range(args.warmup + args.steps):
+                st, dt = reference_run(gstab, rprog, shots, s_ * shots, cores)
+                if s_ >= args.warmup:
+                    tot_shots += st.total_shots
+                    tot_s += dt
+                    disc += st.discarded_shots
+            v = tot_shots / tot_s
+            cb = {"value": v, "unit": "shots/s", "cores": cores, "kind": "reference",
+                  "backend": gstab.backend.name(),
+                  "sample": "%d shots per step through the reference's run_batch "
+                            "(oracle/_ref gstab, %s backend, threads=%d, "
+                            "batch_size=1024, ~%.1f s per step, its SplitMix stream)"
+                            % (shots, gstab.backend.name(), cores, tot_s / args.steps),
+                  "discard_rate": disc / max(tot_shots, 1)}
+            ms = 1000.0 * tot_s / args.steps
+        else:
+            vals = []
+            samples = []
+            for _ in range(args.warmup + args.steps):
+                cb = cpu_baseline(prog, max(2.0, args.cpu_seconds / 3), args.rng, args.p)
+                vals.append(cb["value"])
+                samples.append(cb)
+            v = sorted(vals[args.warmup:])[len(vals[args.warmup:]) // 2]
+            cb = samples[-1]
+            cb["value"] = v
+            ms = 1000.0 / v if v else None
         line = {"metric": METRIC, "value": v, "unit": "shots/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1000.0 / v if v else None, "higher_is_better": True,
+                "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded Philox noise on the generated MSC proxy)",
+                "data": "synthetic (seeded SplitMix noise, the reference's own "
+                        "stream, on the generated MSC workload)",
                 "config": config, "cpu_baseline": cb,
                 "e2e": {"value": v, "unit": "shots/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -376,7 +471,10 @@ def main():
             roofline["dominant_kernel"] = ncu["dominant_kernel"]
             roofline["dominant_share"] = ncu["dominant_share"]
         if not args.no_cpu_baseline:
-            cb = cpu_baseline(prog, args.cpu_seconds, args.rng, args.p)
+            if _have_reference() and not args.ref_port:
+                cb = reference_baseline(text, args.p, args.cpu_seconds)
+            else:
+                cb = cpu_baseline(prog, args.cpu_seconds, args.rng, args.p)
         line = {
             "metric": METRIC, "value": value, "unit": "shots/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
