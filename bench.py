@@ -55,6 +55,87 @@ def _ncu_latest(workload: str, shots: int):
     return d
 
 
+def _micro_peaks():
+    """Measured SMEM / FP64 / issue ceilings of this B200 (scripts/peaks.cu,
+    run on the box; profiles/peaks.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+def _roofline(secs, ncu, total_shots, value, model_bytes, hbm_peak, hbm_src):
+    """Roofline of the dominant section kernel against the resource that
+    binds it: chi lives in shared memory, so HBM carries only
+    the section queues; the kernels are issue-bound.
+
+    * issue: warp instructions of the dominant launch per shot (ncu capture
+      of the same workload, profiles/ncu_latest.json) x the shots it ran /
+      its live device time (CUDA events around that launch in this run), vs
+      the measured LOP3 issue ceiling (profiles/peaks.json);
+    * smem: SURVEY §8(d) state-touch bytes the dominant section executed
+      (counted on the device, GS_SECTION_STATS) / its live time, vs the
+      measured LDS.128+STS.128 ceiling -- the 24 B/entry model includes the
+      8-byte index the dense chi layout keeps implicit, so this overstates
+      the shared-memory bytes actually moved (ncu wavefronts: smem_pct);
+    * hbm: ncu DRAM bytes per shot x this run's rate, vs the measured copy
+      bandwidth (MEASURED_PEAKS.json)."""
+    mp = _micro_peaks()
+    out = {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
+           "traffic": None}
+    if not secs:
+        return out
+    tot_ms = sum(s["device_ms"] for s in secs) or 1.0
+    i = max(range(len(secs)), key=lambda j: secs[j]["device_ms"])
+    d = secs[i]
+    dev_s = d["device_ms"] * 1e-3
+    launches = max(d["launches"], 1)
+    sec_rows = [{"section": j, "kernel": s["kernel"], "pc0": s["pc0"],
+                 "shots_in": s["shots_in"], "device_ms": s["device_ms"],
+                 "share": s["device_ms"] / tot_ms,
+                 "model_gbs": s["model_bytes"] / max(s["device_ms"] * 1e-3, 1e-12) / 1e9}
+                for j, s in enumerate(secs)]
+    kern = None
+    if ncu and len(ncu.get("kernels", [])) == len(secs):
+        kern = ncu["kernels"][i]
+    smem_ach = d["model_bytes"] / dev_s / 1e9 if dev_s > 0 else None
+    out.update({"kernel": "%s_kernel (section %d of %d)" % (d["kernel"], i, len(secs)),
+                "kernel_share": d["device_ms"] / tot_ms,
+                "launches": d["launches"],
+                "shots_per_launch": d["shots_in"] / launches,
+                "model_bytes_per_launch": d["model_bytes"] / launches,
+                "device_ms_per_launch": d["device_ms"] / launches,
+                "sections": sec_rows})
+    if mp and smem_ach is not None:
+        out["smem"] = {"achieved": smem_ach, "peak": mp["smem_ldst_gbs"], "unit": "GB/s",
+                       "frac": smem_ach / mp["smem_ldst_gbs"],
+                       "bytes": "SURVEY 8(d) state-touch model, device-counted"}
+    if kern:
+        scale = total_shots / ncu["shots_in_capture"]    # capture = one chunk
+        inst = kern["warp_instructions"] * scale
+        out["issue_active_pct_ncu"] = kern["issue_active_pct"]
+        out["fp64_pipe_pct_ncu"] = kern["fp64_pipe_pct"]
+        out["smem_wavefront_pct_ncu"] = kern.get("smem_wavefront_pct")
+        out["ncu_capture"] = ncu["capture"]
+        out["traffic"] = kern["dram_bytes"] * scale / launches
+        if mp:
+            ach = inst / dev_s / 1e9
+            out.update({"bound": "issue", "achieved": ach, "peak": mp["issue_ginst"],
+                        "unit": "Gwarp-inst/s", "frac": ach / mp["issue_ginst"],
+                        "peak_source": "measured (profiles/peaks.json, scripts/peaks.cu LOP3)"})
+    if out["bound"] is None and "smem" in out:
+        out.update({"bound": "smem", "achieved": out["smem"]["achieved"],
+                    "peak": out["smem"]["peak"], "unit": "GB/s", "frac": out["smem"]["frac"],
+                    "peak_source": "measured (profiles/peaks.json, LDS.128+STS.128)"})
+    if ncu:
+        dram = ncu["dram_bytes_per_shot"] * value / 1e9
+        out["hbm"] = {"dram_achieved_gbs": dram, "peak": hbm_peak, "frac": dram / hbm_peak,
+                      "peak_source": hbm_src}
+    out["model_bytes_per_shot"] = model_bytes / max(total_shots, 1)
+    return out
+
+
 def _peaks():
     try:
         with open(PEAKS) as fh:
@@ -91,8 +172,22 @@ def _workload(key: str, p: float):
     return name, apply_noise_model(base, p), compute_stats(base).as_dict(), base.serialize()
 
 
+def physical_gpu_id(dev: int) -> str:
+    """nvidia-smi -i selector of CUDA ordinal `dev`: its UUID (immune to a
+    CUDA_VISIBLE_DEVICES remap), else the ordinal."""
+    try:
+        import torch
+        u = str(torch.cuda.get_device_properties(dev).uuid)
+        if u and u != "None":
+            return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        pass
+    return str(dev)
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region
+    (`index`: an nvidia-smi -i selector, see physical_gpu_id)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,"
@@ -243,6 +338,10 @@ def main():
     ap.add_argument("--rng", default="philox", choices=["philox", "splitmix"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-waves", type=int, default=16,
+                    help="e2e sample: this many steps' worth of shots per GPU")
+    ap.add_argument("--no-section-stats", action="store_true",
+                    help="time the steps without per-section events / byte attribution")
     ap.add_argument("--ref-port", action="store_true",
                     help="time the oracle port instead of the reference (oracle/_ref)")
     ap.add_argument("--chi-global", action="store_true")
@@ -355,9 +454,10 @@ def main():
     counters = torch.zeros(nc, dtype=torch.int64, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 
-    def launch(step):
+    def launch(step, fl=None):
         base = step * world * S + rank * S
-        par = Engine.params(12345, base, S, 32768, flags, warps_per_block=args.wpb)
+        par = Engine.params(12345, base, S, 32768, flags if fl is None else fl,
+                            warps_per_block=args.wpb)
         eng.run_counters_async(P, par, counters.data_ptr(), stream.cuda_stream)
 
     for w in range(args.warmup):
@@ -382,9 +482,14 @@ def main():
             launch(args.warmup)
             torch.cuda.synchronize()
     counters.zero_()
+    # per-section device time (CUDA events around each section launch, on
+    # the launching stream) and device-counted model bytes, over exactly the
+    # timed steps
+    eng.section_stats(reset=True)
+    tflags = flags | (0 if args.no_section_stats else _lib.GS_SECTION_STATS)
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(dev)
+    clocks = ClockSampler(physical_gpu_id(dev))
     clocks.start()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -394,7 +499,7 @@ def main():
     for s in range(args.steps):
         flush.zero_()
         ev[s][0].record(stream)
-        launch(args.warmup + s)
+        launch(args.warmup + s, tflags)
         ev[s][1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -402,6 +507,7 @@ def main():
     t_wall = time.perf_counter() - t_wall
     ck = clocks.stop()
     kernel_ms = [a.elapsed_time(b) for a, b in ev]
+    secs = eng.section_stats(reset=True)
     my_ms = sum(kernel_ms)
     launches = eng.launches - launches0
     if world > 1:
@@ -416,60 +522,49 @@ def main():
     value = total_shots / (tot_ms * 1e-3)
     model_bytes = int(c[_lib.GS_C_MODEL_BYTES])
     peak, peak_src = _peaks()
-    # roofline of the (only) kernel: algorithmic state-touch bytes / time,
-    # per GPU (each rank's kernel sees its own shots)
-    achieved = (model_bytes / world) / (my_ms * 1e-3) / 1e9
 
-    # e2e through the public C ABI with host buffers, on every rank: each
-    # step creates the program (host->device upload of the op stream),
-    # samples this rank's shots and reads the counters back (device->host);
-    # wall time between barriers, max over ranks
+    # e2e through the public Python API, as a user calls it: a fresh
+    # CircuitProgram (so the host compile to device bytecode is inside the
+    # timed region, once), then run_batch over this rank's shots in waves of
+    # 2^24 (each wave: gs_run_counters with host buffers -- the op stream
+    # uploaded host->device, counters read back device->host); N > 1:
+    # run_batch_distributed (the same per rank + one all-reduce of the
+    # counters).  Wall time between barriers, max over ranks.
+    from paper_2512_23037_b200 import SamplerConfig, parse_circuit, run_batch
+    from paper_2512_23037_b200.distributed import run_batch_distributed
+    noisy_text = prog.serialize()
     h2d = int(dp.ops.nbytes + dp.tables.nbytes + dp.locs.nbytes)
     d2h = nc * 8
-    e2e_steps = max(2, min(args.steps, 3))
+    e2e_shots = S * max(1, args.e2e_waves)
+    cfg_e = SamplerConfig(shots=e2e_shots * world, master_seed=777, postselect=True,
+                          rng=args.rng, entry_capacity=4096)
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for s in range(e2e_steps):
-        Pe = Program(dp)
-        base = (1 << 40) + s * world * S + rank * S
-        par = Engine.params(777, base, S, 32768, flags, warps_per_block=args.wpb)
-        eng.run_counters(Pe, par)
-        del Pe
+    user_prog = parse_circuit(noisy_text)
+    if world > 1:
+        st_e = run_batch_distributed(user_prog, cfg_e)
+    else:
+        st_e = run_batch(user_prog, cfg_e, shot_begin=1 << 40)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": e2e_steps * world * S / e2e_s, "unit": "shots/s",
-           "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-           "steps": e2e_steps,
-           "path": "gs_program_create + gs_run_counters (host buffers), all ranks"}
+    waves = -(-e2e_shots // S)
+    e2e = {"value": st_e.total_shots / e2e_s, "unit": "shots/s",
+           "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * waves * world,
+           "shots": st_e.total_shots, "wall_s": e2e_s,
+           "path": ("parse_circuit + run_batch%s (host compile, op-stream upload, "
+                    "%d waves of gs_run_counters with host counter readback)"
+                    % ("_distributed" if world > 1 else "", waves))}
     cb = None
     if rank == 0:
         ncu = _ncu_latest(workload, S)
-        roofline = {
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak,
-            # DRAM bytes per step (all section launches), ncu --set full
-            "traffic": ncu["dram_bytes_per_shot"] * S if ncu else None,
-            "peak_source": peak_src,
-            "model_bytes_per_shot": model_bytes / max(total_shots, 1),
-            "note": ("achieved = SURVEY 8(d) state-touch bytes of the reference "
-                     "layout (24 B per chi entry touched, sign vectors) / kernel "
-                     "time; the chi state lives in shared memory, so real DRAM "
-                     "traffic (`traffic`) is the section queues, ~1 KB/shot, "
-                     "and the kernel is issue-bound (`issue_active_pct`)"),
-        }
-        if ncu:
-            # measured HBM traffic of the section queues at this run's rate
-            roofline["dram_achieved_gbs"] = ncu["dram_bytes_per_shot"] * value / 1e9
-            roofline["issue_active_pct"] = ncu["issue_active_pct"]
-            roofline["smem_wavefront_pct"] = ncu.get("smem_wavefront_pct")
-            roofline["fp64_pipe_pct"] = ncu["fp64_pipe_pct"]
-            roofline["ncu_capture"] = ncu["capture"]
-            roofline["dominant_kernel"] = ncu["dominant_kernel"]
-            roofline["dominant_share"] = ncu["dominant_share"]
+        # per GPU: this rank's section launches, shots and rate
+        roofline = _roofline(secs, ncu, S * args.steps, value / world,
+                             model_bytes // world, peak, peak_src)
         if not args.no_cpu_baseline:
             if _have_reference() and not args.ref_port:
                 cb = reference_baseline(text, args.p, args.cpu_seconds)

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 2
+#define GS_ABI_VERSION 3
 
 /* error codes */
 #define GS_OK 0
@@ -52,6 +52,10 @@ extern "C" {
 #define GS_WIDE_ONLY 32u   /* run every op warp-per-shot (A/B, test)     */
 #define GS_CHI_BLOCK 64u   /* wide sections: one block of warps per shot
                               (the default when chi exceeds 32 KB)       */
+#define GS_SECTION_STATS 128u /* per-section device time (CUDA events on
+                              the launch stream) and model bytes / shots
+                              (a small reduction launch after each
+                              section); read with gs_engine_section_stats */
 
 /* per-shot status codes (gs_run_records) */
 #define GS_ST_PRESERVED 1
@@ -164,6 +168,35 @@ int gs_mul_rows(gs_engine *eng, uint64_t *xs, uint64_t *zs, uint8_t *ph,
                 const uint64_t *px, const uint64_t *pz, const uint32_t *pe);
 int gs_parity_pm(gs_engine *eng, const uint64_t *idx, size_t count,
                  uint64_t mask, double *out);
+
+/* per-section statistics accumulated by GS_SECTION_STATS runs since the
+   last read (reset = 1 clears them): out[i * GS_SEC_FIELDS + f] for section
+   i < *n (at most `cap` sections written), fields below.  Synchronizes with
+   the streams the timed launches ran on. */
+#define GS_SEC_SHOTS_IN 0     /* shots that entered the section            */
+#define GS_SEC_SHOTS_OUT 1    /* shots it handed to the next section       */
+#define GS_SEC_MODEL_BYTES 2  /* SURVEY §8(d) state-touch bytes it executed */
+#define GS_SEC_DEVICE_NS 3    /* summed launch durations (CUDA events), ns */
+#define GS_SEC_LAUNCHES 4     /* launches of the section                   */
+#define GS_SEC_WIDE 5         /* 1: wide_kernel (warp/block per shot)      */
+#define GS_SEC_PC0 6          /* first op word of the section              */
+#define GS_SEC_FIELDS 7
+int gs_engine_section_stats(gs_engine *eng, uint64_t *out, uint32_t cap,
+                            uint32_t *n, int reset);
+
+/* inter-section queue budget in bytes per queue (two queues); 0 = auto:
+   min(8 GiB, 1/16 of the device memory free when first sized).  A run
+   larger than the budget is split into chunks (results are identical). */
+int gs_engine_set_queue_budget(gs_engine *eng, uint64_t bytes_per_queue);
+/* free the engine's scratch (queues, global chi/record buffers) after the
+   pending work; the next run re-allocates what it needs */
+int gs_engine_trim(gs_engine *eng);
+
+/* Streams: synchronous calls run on the engine's own stream; *_async calls
+   on the caller's.  Launches are ordered across streams by the engine (an
+   event recorded after each run is waited on by the next run's stream), so
+   mixing the two is safe; concurrent calls from several host threads on
+   one engine are not supported. */
 
 /* diagnostics */
 const char *gs_last_error(void);

@@ -72,6 +72,8 @@ def import_reference(out: str = OUT):
     if out not in sys.path:
         sys.path.insert(0, out)
     import gstab  # noqa: F401
+    if not os.path.abspath(gstab.__file__).startswith(os.path.abspath(out)):
+        raise ImportError("a different gstab is already imported: %s" % gstab.__file__)
     import gstab.backend
     import gstab.circuit
     import gstab.noise

@@ -21,6 +21,17 @@ GS_CHI_GLOBAL = 4
 GS_CHI_SMEM = 16
 GS_CHI_BLOCK = 64
 GS_WIDE_ONLY = 32
+GS_SECTION_STATS = 128
+
+# gs_engine_section_stats fields
+GS_SEC_SHOTS_IN = 0
+GS_SEC_SHOTS_OUT = 1
+GS_SEC_MODEL_BYTES = 2
+GS_SEC_DEVICE_NS = 3
+GS_SEC_LAUNCHES = 4
+GS_SEC_WIDE = 5
+GS_SEC_PC0 = 6
+GS_SEC_FIELDS = 7
 
 GS_C_TOTAL = 0
 GS_C_PRESERVED = 1
@@ -39,7 +50,9 @@ EXPORTED = (
     "gs_run_records", "gs_dump_shots", "gs_anticommute_mask",
     "gs_conj_gate_rows", "gs_mul_rows", "gs_parity_pm", "gs_last_error",
     "gs_abi_version", "gs_engine_launches", "gs_engine_last_kernel_ms",
+    "gs_engine_section_stats", "gs_engine_set_queue_budget", "gs_engine_trim",
 )
+ABI_VERSION = 3
 
 
 class EngineUnavailable(RuntimeError):
@@ -111,6 +124,13 @@ def load(path: str | None = None):
     lib.gs_engine_launches.restype = ct.c_uint64
     lib.gs_engine_last_kernel_ms.argtypes = [vp]
     lib.gs_engine_last_kernel_ms.restype = ct.c_double
+    lib.gs_engine_section_stats.argtypes = [vp, vp, ct.c_uint32, ct.POINTER(ct.c_uint32),
+                                            ct.c_int]
+    lib.gs_engine_set_queue_budget.argtypes = [vp, ct.c_uint64]
+    lib.gs_engine_trim.argtypes = [vp]
+    if lib.gs_abi_version() != ABI_VERSION:
+        raise EngineUnavailable("%s has ABI %d, expected %d (rebuild)"
+                                % (p, lib.gs_abi_version(), ABI_VERSION))
     if path is None:
         _lib = lib
     return lib

@@ -98,7 +98,8 @@ def cmd_bench(a):
     if a.shots > 0:
         cfg = SamplerConfig(shots=a.shots, master_seed=a.seed,
                             entry_capacity=a.entry_capacity,
-                            postselect=a.postselect, rng=a.rng)
+                            postselect=a.postselect, rng=a.rng,
+                            batch_size=a.batch_size)
         try:
             rows = throughput_bench(prog, cfg, a.sweep, vals)
         except NoiseModelError as exc:
@@ -127,7 +128,8 @@ def build_parser():
     s.add_argument("--shots", type=int, required=True)
     s.add_argument("--seed", type=int, default=0)
     s.add_argument("--threads", type=int, default=None, help="accepted, ignored")
-    s.add_argument("--batch-size", type=int, default=1024)
+    s.add_argument("--batch-size", type=int, default=None,
+                   help="shots resident per launch (default 2^24)")
     s.add_argument("--noise", type=float, default=None)
     s.add_argument("--postselect", action=argparse.BooleanOptionalAction, default=False)
     s.add_argument("--entry-capacity", type=int, default=4096)
@@ -145,6 +147,8 @@ def build_parser():
     b.add_argument("--sweep", choices=("batch-size", "noise"), required=True)
     b.add_argument("--values", required=True)
     b.add_argument("--shots", type=int, default=10000)
+    b.add_argument("--batch-size", type=int, default=None,
+                   help="wave size for --sweep noise (default 2^24)")
     b.add_argument("--seed", type=int, default=0)
     b.add_argument("--postselect", action=argparse.BooleanOptionalAction, default=False)
     b.add_argument("--entry-capacity", type=int, default=4096)

@@ -84,6 +84,21 @@ struct gs_engine {
   size_t work_bytes = 0;
   u64 launches = 0;
   double last_ms = 0.0;
+  // cross-stream ordering: recorded after every run, waited on by the next
+  // run when it is issued on a different stream (engine scratch is shared)
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
+  // inter-section queue budget per queue (0: auto, sized on first use)
+  u64 queue_budget = 0;
+  // GS_SECTION_STATS: device accumulators [sec][GS_SEC_FIELDS] (+1 word: model
+  // bytes already attributed), and the pending per-launch event pairs
+  u64 *d_secstats = nullptr;
+  size_t secstats_cap = 0;   // sections
+  struct TimedLaunch { u32 sec; cudaEvent_t a, b; };
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> spare_ev;
+  std::vector<u64> sec_meta;  // per section: wide, pc0 of the last stats run
 };
 
 static thread_local std::string g_err;
@@ -170,6 +185,7 @@ int gs_engine_create(int device, gs_engine **out) {
   CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreate(&e->ev0));
   CUDA_TRY(cudaEventCreate(&e->ev1));
+  CUDA_TRY(cudaEventCreateWithFlags(&e->order_ev, cudaEventDisableTiming));
   *out = e;
   return GS_OK;
 }
@@ -183,6 +199,10 @@ int gs_engine_destroy(gs_engine *e) {
   cudaFree(e->d_queue[0]);
   cudaFree(e->d_queue[1]);
   cudaFree(e->d_work);
+  cudaFree(e->d_secstats);
+  for (auto &t : e->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  for (cudaEvent_t ev : e->spare_ev) cudaEventDestroy(ev);
+  if (e->order_ev) cudaEventDestroy(e->order_ev);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->stream) cudaStreamDestroy(e->stream);
@@ -193,17 +213,22 @@ int gs_engine_destroy(gs_engine *e) {
 uint64_t gs_engine_launches(gs_engine *e) { return e ? e->launches : 0; }
 double gs_engine_last_kernel_ms(gs_engine *e) { return e ? e->last_ms : 0.0; }
 
-static int upload(gs_engine *e, gs_program *p) {
+// copies are issued on the launch stream `st`, so they are ordered before
+// the kernels that read them (the engine's stream is non-blocking: legacy
+// stream copies would not be); the host vectors outlive the copies
+static int upload(gs_engine *e, gs_program *p, cudaStream_t st) {
   if (p->dev == e->device) return GS_OK;
   if (p->dev >= 0) return fail(GS_ERR_ARG, "program already bound to another device");
   // one zero word past END: the interpreters prefetch the next header
   CUDA_TRY(cudaMalloc(&p->d_ops, (p->ops.size() + 1) * 8));
-  CUDA_TRY(cudaMemset(p->d_ops + p->ops.size(), 0, 8));
-  CUDA_TRY(cudaMalloc(&p->d_tables, p->tables.size() * 8));
-  CUDA_TRY(cudaMalloc(&p->d_locs, p->locs.size() * 8));
-  CUDA_TRY(cudaMemcpy(p->d_ops, p->ops.data(), p->ops.size() * 8, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(p->d_tables, p->tables.data(), p->tables.size() * 8, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(p->d_locs, p->locs.data(), p->locs.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&p->d_tables, std::max<size_t>(p->tables.size(), 1) * 8));
+  CUDA_TRY(cudaMalloc(&p->d_locs, std::max<size_t>(p->locs.size(), 1) * 8));
+  CUDA_TRY(cudaMemsetAsync(p->d_ops + p->ops.size(), 0, 8, st));
+  CUDA_TRY(cudaMemcpyAsync(p->d_ops, p->ops.data(), p->ops.size() * 8, cudaMemcpyHostToDevice, st));
+  if (!p->tables.empty())
+    CUDA_TRY(cudaMemcpyAsync(p->d_tables, p->tables.data(), p->tables.size() * 8, cudaMemcpyHostToDevice, st));
+  if (!p->locs.empty())
+    CUDA_TRY(cudaMemcpyAsync(p->d_locs, p->locs.data(), p->locs.size() * 8, cudaMemcpyHostToDevice, st));
   p->dev = e->device;
   return GS_OK;
 }
@@ -319,6 +344,10 @@ static int ensure_buf(T **d, size_t *cap, size_t want) {
 
 }  // extern "C++"
 
+static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOut O,
+                       cudaStream_t st, bool timed);
+typedef gs_engine::TimedLaunch Engine_TimedLaunch;
+
 static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOut O,
                   cudaStream_t st, bool timed) {
   if (!e || !p || !r) return fail(GS_ERR_ARG, "null argument");
@@ -326,8 +355,25 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   if ((r->flags & GS_RNG_PHILOX) && r->seeds)
     return fail(GS_ERR_ARG, "explicit seeds require the SplitMix RNG");
   CUDA_TRY(cudaSetDevice(e->device));
-  int rc = upload(e, p);
+  // engine scratch is shared by every stream this engine runs on: order this
+  // run after the previous one when the stream changes
+  if (e->has_last && e->last_stream != st) CUDA_TRY(cudaStreamWaitEvent(st, e->order_ev, 0));
+  int rc = upload(e, p, st);
   if (rc) return rc;
+  rc = launch_body(e, p, r, O, st, timed);
+  // recorded even after a failed launch, so a later run never overtakes work
+  // already queued on this stream
+  cudaError_t er = cudaEventRecord(e->order_ev, st);
+  e->last_stream = st;
+  e->has_last = true;
+  if (rc) return rc;
+  if (er != cudaSuccess) return fail(GS_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(er));
+  return GS_OK;
+}
+
+static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOut O,
+                       cudaStream_t st, bool timed) {
+  int rc = GS_OK;
   const bool philox = (r->flags & GS_RNG_PHILOX) != 0;
   const bool wide_only = (r->flags & GS_WIDE_ONLY) != 0;
   gs::DevProg P;
@@ -443,7 +489,12 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
 #ifndef GS_QUEUE_GB
 #define GS_QUEUE_GB 8   // per section queue: one chunk for a 2^24-shot step (A/B +0.4 % over 2 GB)
 #endif
-  const u64 qbudget = (u64)GS_QUEUE_GB << 30;   // bytes per queue
+  if (!e->queue_budget) {   // auto: min(8 GiB, 1/16 of the free device memory)
+    size_t fr = 0, tot = 0;
+    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    e->queue_budget = std::max<u64>(64ull << 20, std::min<u64>((u64)GS_QUEUE_GB << 30, fr / 16));
+  }
+  const u64 qbudget = e->queue_budget;   // bytes per queue
   if (secs.size() > 1 && chunk * slot_b > qbudget) chunk = std::max<u64>(32, qbudget / slot_b);
   if (r->chunk_shots && r->chunk_shots < chunk) chunk = r->chunk_shots;   // tests
   if (secs.size() > 1) {
@@ -464,11 +515,39 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
   }
   O.gchi = e->d_chi;
   O.grec = e->d_rec;
+  const bool stats = (r->flags & GS_SECTION_STATS) != 0;
+  if (stats) {
+    if (secs.size() > e->secstats_cap) {   // (re)size: accumulations restart
+      cudaFree(e->d_secstats);
+      e->d_secstats = nullptr;
+      e->secstats_cap = 0;
+      const size_t cap = std::max<size_t>(64, secs.size());
+      CUDA_TRY(cudaMalloc(&e->d_secstats, (cap * 4 + 1) * 8));
+      CUDA_TRY(cudaMemsetAsync(e->d_secstats, 0, (cap * 4 + 1) * 8, st));
+      e->secstats_cap = cap;
+    }
+    e->sec_meta.assign(2 * secs.size(), 0);
+    for (size_t i = 0; i < secs.size(); ++i) {
+      e->sec_meta[2 * i] = secs[i].wide;
+      e->sec_meta[2 * i + 1] = secs[i].pc0;
+    }
+  }
+  u64 *d_mbprev = stats ? e->d_secstats + 4 * e->secstats_cap : nullptr;
+  auto grab_event = [&](cudaEvent_t *ev) -> int {
+    if (!e->spare_ev.empty()) { *ev = e->spare_ev.back(); e->spare_ev.pop_back(); return GS_OK; }
+    CUDA_TRY(cudaEventCreate(ev));
+    return GS_OK;
+  };
   if (r->shot_count) {
     if (timed) CUDA_TRY(cudaEventRecord(e->ev0, st));
     for (u64 first = 0; first < r->shot_count; first += chunk) {
       const u64 count = std::min(chunk, r->shot_count - first);
       CUDA_TRY(cudaMemsetAsync(e->d_work, 0, sizeof(unsigned long long) * (secs.size() + 2), st));
+      if (stats) {
+        gs::mb_snapshot_kernel<<<1, 1, 0, st>>>(O.counters + GS_C_MODEL_BYTES, d_mbprev);
+        CUDA_TRY(cudaGetLastError());
+        e->launches += 1;
+      }
       for (size_t i = 0; i < secs.size(); ++i) {
         gs::DevSec S;
         S.pc0 = secs[i].pc0;
@@ -485,6 +564,11 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
         S.pn0 = secs[i].pn0;
         if (i >= 1 && i + 1 < secs.size())   // the queue written here was read by section i-1
           CUDA_TRY(cudaMemsetAsync(d_qn + (i & 1), 0, sizeof(u32), st));
+        Engine_TimedLaunch tl{(u32)i, nullptr, nullptr};
+        if (stats) {
+          if (grab_event(&tl.a) || grab_event(&tl.b)) return GS_ERR_CUDA;
+          CUDA_TRY(cudaEventRecord(tl.a, st));
+        }
         if (secs[i].wide) {
           gs::DevOut Ow = O;
           Ow.warp_bytes = KW.warp_bytes;
@@ -505,6 +589,17 @@ static int launch(gs_engine *e, gs_program *p, const gs_run_params *r, gs::DevOu
           }));
         }
         e->launches += 1;
+        if (stats) {
+          CUDA_TRY(cudaEventRecord(tl.b, st));
+          e->timed.push_back({tl.sec, tl.a, tl.b});
+          const u64 nq = secs.size() > 1 ? chunk : 0;
+          const u32 grid = (u32)std::max<u64>(1, std::min<u64>((u64)e->num_sms * 4, (nq + 255) / 256));
+          gs::section_stats_kernel<<<grid, 256, 0, st>>>(
+              S.q_in, S.n_in, count, S.q_out, S.n_out, (u32)(slot_b / 8),
+              O.counters + GS_C_MODEL_BYTES, d_mbprev, e->d_secstats + 4 * i);
+          CUDA_TRY(cudaGetLastError());
+          e->launches += 1;
+        }
       }
     }
     if (timed) CUDA_TRY(cudaEventRecord(e->ev1, st));
@@ -647,6 +742,57 @@ static int run_out(gs_engine *e, gs_program *p, const gs_run_params *r, uint8_t 
   float ms = 0.f;
   if (S) CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
   e->last_ms = ms;
+  return GS_OK;
+}
+
+int gs_engine_section_stats(gs_engine *e, uint64_t *out, uint32_t cap, uint32_t *n, int reset) {
+  if (!e || !n || (cap && !out)) return fail(GS_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaDeviceSynchronize());   // the timed runs may sit on any stream
+  const size_t nsec = e->sec_meta.size() / 2;
+  std::vector<u64> dev(4 * std::max<size_t>(nsec, 1), 0);
+  if (nsec && e->d_secstats)
+    CUDA_TRY(cudaMemcpy(dev.data(), e->d_secstats, nsec * 4 * 8, cudaMemcpyDeviceToHost));
+  std::vector<double> ns(nsec, 0.0);
+  std::vector<u64> nl(nsec, 0);
+  for (auto &t : e->timed) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, t.a, t.b));
+    if (t.sec < nsec) { ns[t.sec] += 1e6 * (double)ms; nl[t.sec] += 1; }
+  }
+  *n = (uint32_t)nsec;
+  for (size_t i = 0; i < nsec && i < cap; ++i) {
+    uint64_t *o = out + i * GS_SEC_FIELDS;
+    o[GS_SEC_SHOTS_IN] = dev[4 * i];
+    o[GS_SEC_SHOTS_OUT] = dev[4 * i + 1];
+    o[GS_SEC_MODEL_BYTES] = dev[4 * i + 2];
+    o[GS_SEC_DEVICE_NS] = (uint64_t)llround(ns[i]);
+    o[GS_SEC_LAUNCHES] = nl[i];
+    o[GS_SEC_WIDE] = e->sec_meta[2 * i];
+    o[GS_SEC_PC0] = e->sec_meta[2 * i + 1];
+  }
+  if (reset) {
+    if (e->d_secstats) CUDA_TRY(cudaMemset(e->d_secstats, 0, (e->secstats_cap * 4 + 1) * 8));
+    for (auto &t : e->timed) { e->spare_ev.push_back(t.a); e->spare_ev.push_back(t.b); }
+    e->timed.clear();
+  }
+  return GS_OK;
+}
+
+int gs_engine_set_queue_budget(gs_engine *e, uint64_t bytes_per_queue) {
+  if (!e) return fail(GS_ERR_ARG, "null argument");
+  e->queue_budget = bytes_per_queue;
+  return GS_OK;
+}
+
+int gs_engine_trim(gs_engine *e) {
+  if (!e) return fail(GS_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(e->d_queue[0]); e->d_queue[0] = nullptr; e->queue_bytes[0] = 0;
+  cudaFree(e->d_queue[1]); e->d_queue[1] = nullptr; e->queue_bytes[1] = 0;
+  cudaFree(e->d_chi); e->d_chi = nullptr; e->chi_bytes = 0;
+  cudaFree(e->d_rec); e->d_rec = nullptr; e->rec_bytes = 0;
   return GS_OK;
 }
 

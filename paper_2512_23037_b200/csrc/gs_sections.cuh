@@ -1262,3 +1262,36 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   }
   flush_counters(O, wcnt, lane);
 }
+
+// ---------------------------------------------------------------- section stats
+// GS_SECTION_STATS (measurement only): after a section launch, on its stream,
+// attribute the SURVEY §8(d) model bytes it executed: shots that finished in
+// it added their totals to the MODEL_BYTES counter (delta since the last
+// snapshot), shots it handed on carry their running totals in Q_MB, shots it
+// received brought theirs in.  st = [shots_in, shots_out, model_bytes, -].
+__global__ void mb_snapshot_kernel(const long long *mb_counter, u64 *mb_prev) {
+  *mb_prev = (u64)*mb_counter;
+}
+
+__global__ void section_stats_kernel(const u64 *q_in, const u32 *n_in, u64 fresh,
+                                     const u64 *q_out, const u32 *n_out, u32 su,
+                                     const long long *mb_counter, u64 *mb_prev, u64 *st) {
+  const u64 nin = q_in ? (u64)*n_in : fresh;
+  const u64 nout = q_out ? (u64)*n_out : 0ull;
+  const u64 nq = q_in ? (nin > nout ? nin : nout) : nout;
+  u64 acc = 0;   // out - in, two's complement
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += (u64)gridDim.x * blockDim.x) {
+    if (q_in && i < nin) acc -= q_in[i * su + Q_MB];
+    if (i < nout) acc += q_out[i * su + Q_MB];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if ((threadIdx.x & 31u) == 0 && acc) atomicAdd((unsigned long long *)st + 2, acc);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const u64 now = (u64)*mb_counter;
+    atomicAdd((unsigned long long *)st + 2, now - *mb_prev);
+    *mb_prev = now;
+    atomicAdd((unsigned long long *)st + 0, nin);
+    atomicAdd((unsigned long long *)st + 1, nout);
+  }
+}

@@ -12,6 +12,7 @@ the device buffer the kernel accumulated into (NCCL over NVLink on B200).
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -29,23 +30,34 @@ def shard_range(total: int, rank: int, world: int):
     return begin, base + (1 if rank < extra else 0)
 
 
+def rank_device(cfg: SamplerConfig) -> int:
+    """CUDA ordinal of this rank: LOCAL_RANK (one process per GPU, torchrun)
+    modulo the visible devices, else ``cfg.device``."""
+    import torch
+    n = max(torch.cuda.device_count(), 1)
+    lr = os.environ.get("LOCAL_RANK")
+    return int(lr) % n if lr is not None else cfg.device
+
+
 def _gpu_shard_counters(prog, cfg: SamplerConfig, begin: int, count: int):
-    """Run one rank's shard on its GPU; counters stay on the device."""
+    """Run one rank's shard on its GPU (set explicitly, not inherited from
+    the caller's current device); counters stay on that device."""
     import torch
     from .engine import Engine, get_engine
     p = _program_for(prog, cfg.dim_limit)
-    dev = torch.cuda.current_device()
-    eng = get_engine(dev)
-    counters = torch.zeros(p.num_counters, dtype=torch.int64, device="cuda")
-    stream = torch.cuda.current_stream()
-    chunk = 1 << 26
-    done = 0
-    while done < count:
-        n = min(chunk, count - done)
-        par = Engine.params(cfg.master_seed, begin + done, n,
-                            cfg.effective_capacity, cfg.run_flags())
-        eng.run_counters_async(p, par, counters.data_ptr(), stream.cuda_stream)
-        done += n
+    dev = rank_device(cfg)
+    with torch.cuda.device(dev):
+        eng = get_engine(dev)
+        counters = torch.zeros(p.num_counters, dtype=torch.int64, device=dev)
+        stream = torch.cuda.current_stream(dev)
+        chunk = cfg.wave_shots
+        done = 0
+        while done < count:
+            n = min(chunk, count - done)
+            par = Engine.params(cfg.master_seed, begin + done, n,
+                                cfg.effective_capacity, cfg.run_flags())
+            eng.run_counters_async(p, par, counters.data_ptr(), stream.cuda_stream)
+            done += n
     return counters, p.dp.obs_keys
 
 

@@ -164,7 +164,36 @@ class Engine:
                 "obs": obs[:S], "sig": sig[:S], "c": cv[:S],
                 "amps": amps[:S, :, 0] + 1j * amps[:S, :, 1], "dim": dim[:S]}
 
+    # -- scratch ------------------------------------------------------
+
+    def set_queue_budget(self, bytes_per_queue: int) -> None:
+        """Inter-section queue budget per queue (0 = auto: min(8 GiB, 1/16
+        of free device memory)); larger runs are chunked, same results."""
+        _lib.check(_lib.load().gs_engine_set_queue_budget(self.handle, int(bytes_per_queue)))
+
+    def trim(self) -> None:
+        """Free the engine's scratch buffers (re-allocated on demand)."""
+        _lib.check(_lib.load().gs_engine_trim(self.handle))
+
     # -- diagnostics --------------------------------------------------
+
+    def section_stats(self, reset: bool = True) -> list:
+        """Per-section statistics of the GS_SECTION_STATS runs since the last
+        reset: shots in/out, SURVEY §8(d) model bytes, summed device time
+        (CUDA events), launches, kind and first op."""
+        cap = 256
+        out = np.zeros(cap * _lib.GS_SEC_FIELDS, dtype=np.uint64)
+        n = ct.c_uint32(0)
+        _lib.check(_lib.load().gs_engine_section_stats(
+            self.handle, out.ctypes.data, cap, ct.byref(n), int(reset)))
+        rows = out[:min(n.value, cap) * _lib.GS_SEC_FIELDS].reshape(-1, _lib.GS_SEC_FIELDS)
+        return [{"shots_in": int(r[_lib.GS_SEC_SHOTS_IN]),
+                 "shots_out": int(r[_lib.GS_SEC_SHOTS_OUT]),
+                 "model_bytes": int(r[_lib.GS_SEC_MODEL_BYTES]),
+                 "device_ms": int(r[_lib.GS_SEC_DEVICE_NS]) * 1e-6,
+                 "launches": int(r[_lib.GS_SEC_LAUNCHES]),
+                 "kernel": "wide" if r[_lib.GS_SEC_WIDE] else "narrow",
+                 "pc0": int(r[_lib.GS_SEC_PC0])} for r in rows]
 
     @property
     def launches(self) -> int:

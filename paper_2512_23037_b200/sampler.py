@@ -36,7 +36,7 @@ from . import _lib
 from .engine import Engine, Program, get_engine
 
 _M64 = (1 << 64) - 1
-_CHUNK = 1 << 26        # shots per kernel launch in run_batch
+_WAVE = 1 << 24         # default shots resident per launch (batch_size=None)
 
 
 class CorruptStateError(RuntimeError):
@@ -80,7 +80,10 @@ class ShotResult:
 class SamplerConfig:
     shots: int
     master_seed: int = 0
-    batch_size: int = 1024
+    # shots resident per launch (one wave = one gs_run_counters call, the
+    # GPU analogue of the reference's waves, ref sampler.py:348-382);
+    # None = 2^24, which saturates a B200 (Fig. 4 analogue: bench --sweep)
+    batch_size: int | None = None
     entry_capacity: int = 4096
     threads: int = 1
     postselect: bool = False
@@ -93,7 +96,7 @@ class SamplerConfig:
     def __post_init__(self):
         if self.shots < 0:
             raise ValueError("shots must be >= 0")
-        if self.batch_size < 1:
+        if self.batch_size is not None and self.batch_size < 1:
             raise ValueError("batch_size must be >= 1")
         if self.entry_capacity < 2:
             raise ValueError("entry_capacity must be >= 2")
@@ -110,6 +113,10 @@ class SamplerConfig:
         if self.max_dim is not None:
             return self.max_dim
         return min(24, max(1, (self.effective_capacity - 1).bit_length() + 5))
+
+    @property
+    def wave_shots(self) -> int:
+        return _WAVE if self.batch_size is None else int(self.batch_size)
 
     @property
     def effective_capacity(self) -> int:
@@ -234,7 +241,10 @@ def counters_to_stats(c: np.ndarray, obs_keys, wall: float,
 def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
               engine: Engine | None = None, witnesses: int = 0) -> RunStats:
     """Counters of shots [shot_begin, shot_begin + cfg.shots) (global shot
-    indices, so shards of one run combine exactly).
+    indices, so shards of one run combine exactly), issued in waves of
+    ``cfg.batch_size`` shots -- one synchronous gs_run_counters call per wave,
+    as the reference issues waves of batch_size (ref sampler.py:348-382).
+    Counters do not depend on the wave size.
 
     ``witnesses > 0`` also collects the global indices of up to that many
     preserved shots whose observables flipped ("rare-failure witnesses",
@@ -249,7 +259,7 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     dev_s = 0.0
     done = 0
     while done < cfg.shots:
-        cnt = min(_CHUNK, cfg.shots - done)
+        cnt = min(cfg.wave_shots, cfg.shots - done)
         par = Engine.params(cfg.master_seed, shot_begin + done, cnt,
                             cfg.effective_capacity, cfg.run_flags())
         if witnesses > len(wit):
@@ -290,7 +300,11 @@ class ShotBatch:
         st = _STATUS.get(int(self.status[i]))
         if st is None:
             raise CorruptStateError("shot %d ended in status %d" % (i, self.status[i]))
-        bits = self.record_bits()[i]
+        if self.num_measurements:
+            bits = np.unpackbits(np.ascontiguousarray(self.records[i]).view(np.uint8),
+                                 bitorder="little")[: self.num_measurements]
+        else:
+            bits = np.zeros(0, dtype=np.uint8)
         nrec = len(bits) if measured is None else measured
         obs = {}
         if st is ShotStatus.PRESERVED:
@@ -353,6 +367,30 @@ def run_shot(prog, ctx: ShotContext, *, postselect: bool = False,
     return res
 
 
+_PREFIX: dict = {}
+
+
+def _measure_prefix(prog):
+    """(measurements before flat instruction j, measurements before the
+    d-th executed DETECTOR), computed once per program."""
+    hit = _PREFIX.get(id(prog))
+    if hit is not None and hit[0] is prog:
+        return hit[1], hit[2]
+    by_instr, by_det = [], []
+    m = 0
+    for ins in prog.flat():
+        by_instr.append(m)
+        if ins.name in ("M", "MR", "MPP"):
+            m += len(ins.targets)
+        elif ins.name == "DETECTOR":
+            by_det.append(m)
+    by_instr.append(m)
+    if len(_PREFIX) > 64:
+        _PREFIX.clear()
+    _PREFIX[id(prog)] = (prog, by_instr, by_det)
+    return by_instr, by_det
+
+
 def _records_before(prog, batch: ShotBatch, i: int) -> int:
     """Number of measurements made before a shot stopped (the reference
     returns the partial record of discarded / overflowed shots)."""
@@ -360,18 +398,12 @@ def _records_before(prog, batch: ShotBatch, i: int) -> int:
     if st == 1:
         return batch.num_measurements
     stop = int(batch.aux[i])
-    m = 0
-    det = -1
-    for j, ins in enumerate(prog.flat()):
-        if st == 3 and j == stop:
-            return m
-        if ins.name in ("M", "MR", "MPP"):
-            m += len(ins.targets)
-        elif ins.name == "DETECTOR":
-            det += 1
-            if st == 2 and det == stop:
-                return m
-    return m
+    by_instr, by_det = _measure_prefix(prog)
+    if st == 3:
+        return by_instr[min(max(stop, 0), len(by_instr) - 1)]
+    if st == 2 and 0 <= stop < len(by_det):
+        return by_det[stop]
+    return by_instr[-1]
 
 
 # ----------------------------------------------------------------------

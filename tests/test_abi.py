@@ -38,7 +38,7 @@ def test_header_declares_core_entry_points():
 def test_library_exports_every_declared_symbol(lib):
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.gs_abi_version() == 2
+    assert lib.gs_abi_version() == 3
 
 
 def test_python_binding_lists_match_header():

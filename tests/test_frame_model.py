@@ -1,6 +1,8 @@
 """Compiler correctness on CPU: the frame model (a CPU transliteration of the
 device interpreter) must reproduce the reference's golden per-shot results
-bit-for-bit and its state snapshots to 1e-12."""
+bit-for-bit and its state snapshots to 1e-10 relative per entry."""
+
+from chi_check import assert_chi_close
 
 import numpy as np
 import pytest
@@ -37,8 +39,7 @@ def test_frame_model_states(golden_states):
             assert st["xs"] == snap["xs"] and st["zs"] == snap["zs"]
             assert st["ph"] == snap["ph"], (fx["text"], snap["i"])
             assert st["idx"] == snap["idx"], (fx["text"], snap["i"])
-            np.testing.assert_allclose(np.array(st["amp"]), np.array(snap["amp"]),
-                                       rtol=0, atol=1e-12)
+            assert_chi_close(st["amp"], snap["amp"])
 
 
 def test_frame_model_random_programs_vs_oracle():

@@ -2,7 +2,8 @@
 reference-generated records), config 4 chi-growth stress with capacity tiers
 (overflow statuses bit-exact vs the oracle), and statistical parity of
 discard / logical-error rates on the d=3 and d=5 MSC proxies
-(Philox GPU stream vs SplitMix oracle stream, binomial CIs), and the
+(Philox GPU stream vs SplitMix oracle stream: Bayes-factor-1000 intervals
+overlap and z < 4.5, tests/stats_check.py), and the
 headline MSC workloads' 20,000 reference-generated shots bit-exact."""
 
 import math
@@ -18,6 +19,7 @@ from paper_2512_23037_b200 import SamplerConfig, parse_circuit, run_batch, sampl
 from paper_2512_23037_b200.msc import config4_circuit, msc_circuit, injection_circuit
 from paper_2512_23037_b200.noise import apply_noise_model
 from paper_2512_23037_b200.sampler import _records_before
+from stats_check import assert_rates_agree
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "config1_records.npz")
 
@@ -52,12 +54,6 @@ def test_config4_overflow_parity(n, t, cap, rerun):
         assert got.record == ref["record"]
 
 
-def _z(k1, n1, k2, n2):
-    p = (k1 + k2) / (n1 + n2)
-    se = math.sqrt(max(p * (1 - p), 1e-12) * (1 / n1 + 1 / n2))
-    return abs(k1 / n1 - k2 / n2) / se
-
-
 @pytest.mark.parametrize("d,cpu_shots", [(3, 4000), (5, 800)])
 def test_msc_statistics_match_oracle(d, cpu_shots):
     prog = apply_noise_model(msc_circuit(d), 1e-3)
@@ -66,10 +62,10 @@ def test_msc_statistics_match_oracle(d, cpu_shots):
     cpu = orc.run_counters_parallel(prog, cpu_shots, os.cpu_count() or 1,
                                     master_seed=11, mode="splitmix",
                                     postselect=True)
-    assert _z(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
-              cpu["total"]) < 4.5
-    assert _z(gpu.logical_error_shots, gpu.preserved_shots,
-              cpu["error_shots"], max(cpu["preserved"], 1)) < 4.5
+    assert_rates_agree(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
+              cpu["total"])
+    assert_rates_agree(gpu.logical_error_shots, gpu.preserved_shots,
+              cpu["error_shots"], max(cpu["preserved"], 1))
 
 
 def test_config3_injection_rounds_statistics():
@@ -78,8 +74,8 @@ def test_config3_injection_rounds_statistics():
                                         postselect=True, rng="philox"))
     cpu = orc.run_counters_parallel(prog, 3000, os.cpu_count() or 1,
                                     master_seed=2, mode="splitmix", postselect=True)
-    assert _z(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
-              cpu["total"]) < 4.5
+    assert_rates_agree(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
+              cpu["total"])
 
 
 def test_d5_full_size_properties():
@@ -131,7 +127,7 @@ def test_grown_d5_statistics_match_oracle():
     cpu = orc.run_counters_parallel(prog, 1600, os.cpu_count() or 1,
                                     master_seed=11, mode="splitmix",
                                     postselect=True)
-    assert _z(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
-              cpu["total"]) < 4.5
-    assert _z(gpu.logical_error_shots, gpu.preserved_shots,
-              cpu["error_shots"], max(cpu["preserved"], 1)) < 4.5
+    assert_rates_agree(gpu.discarded_shots, gpu.total_shots, cpu["discarded"],
+              cpu["total"])
+    assert_rates_agree(gpu.logical_error_shots, gpu.preserved_shots,
+              cpu["error_shots"], max(cpu["preserved"], 1))

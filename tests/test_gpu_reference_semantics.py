@@ -201,3 +201,28 @@ def test_extreme_channels_bit_exact_vs_oracle():
             ref = orc.run_one_shot(flat, prog.num_qubits, orc.DrawStream(rng, 3, s), 4096, True)
             got = b.result(s, measured=_records_before(prog, b, s))
             assert got.status.value == ref["status"] and got.record == ref["record"], (rng, s)
+
+
+def _at_most_one_inversion(vals, increasing=True):
+    bad = sum(1 for a, b in zip(vals, vals[1:]) if (b < a if increasing else b > a))
+    return bad <= 1
+
+
+def test_criterion_9_batch_size_saturation():
+    """Ref tests/test_acceptance.py:238-248 on the GPU: batch_size is the
+    number of shots resident per launch; tiny waves leave the B200 idle
+    between launches, large ones saturate it (paper Fig. 4), and the
+    counters never depend on it."""
+    from paper_2512_23037_b200 import throughput_bench
+    from paper_2512_23037_b200.noise import apply_noise_model
+    layer = "R 0 1\nH 0\nCX 0 1\nT 0\nT_DAG 0\nM 0 1\nDETECTOR rec[-1] rec[-2]"
+    prog = apply_noise_model(parse_circuit("\n".join([layer] * 4) + "\n"), 0.002)
+    cfg = SamplerConfig(shots=1 << 22, master_seed=2, rng="philox", postselect=True)
+    run_batch(prog, cfg)   # warm-up: program upload, scratch allocation
+    values = [1 << 10, 1 << 13, 1 << 16, 1 << 19, 1 << 22]
+    rows = throughput_bench(prog, cfg, "batch-size", values)
+    tputs = [r[1] for r in rows]
+    assert _at_most_one_inversion(tputs, increasing=True), rows
+    assert tputs[-1] <= 1.5 * max(tputs[:-1]), rows
+    assert tputs[-1] >= 4 * tputs[0], rows
+    assert len({r[2] for r in rows}) == 1, rows   # identical discard counts

@@ -3,7 +3,8 @@ B200 + 16 host cores): the headline workload (grown d=5 MSC proxy, p=1e-3)
 and BASELINE configs 2 and 3, post-selected, sampled with billions of
 Philox shots on the GPU against reference-stream (SplitMix) shots of the
 CPU oracle (GS_LONG_SCALE scales both sample sizes).  Discard rate and
-logical-error rate must agree within a binomial z < 4.5; the summary line
+logical-error rate must agree (Bayes-factor-1000 intervals overlap and
+z < 4.5, tests/stats_check.py); the summary line
 is printed for profiles/.
 
     GS_LONG_STATS=1 python -m pytest tests/test_gpu_statistics_long.py -m gpu -s
@@ -24,12 +25,7 @@ from oracle import gstab_oracle as orc
 from paper_2512_23037_b200 import SamplerConfig, run_batch
 from paper_2512_23037_b200.msc import injection_circuit, msc_circuit, msc_grown_circuit
 from paper_2512_23037_b200.noise import apply_noise_model
-
-
-def _z(k1, n1, k2, n2):
-    p = (k1 + k2) / (n1 + n2)
-    se = math.sqrt(max(p * (1 - p), 1e-15) * (1 / n1 + 1 / n2))
-    return abs(k1 / n1 - k2 / n2) / se
+from stats_check import assert_rates_agree, z_score as _z
 
 
 WORKLOADS = {
@@ -77,4 +73,6 @@ def test_discard_and_logical_error_rates_large_sample(name):
     }
     print("LONG_STATS " + json.dumps(summary))
     assert gpu.total_shots == gpu_shots and gpu.overflow_count == 0
-    assert z_disc < 4.5 and z_ler < 4.5
+    assert_rates_agree(gpu.discarded_shots, gpu.total_shots, cpu["discarded"], cpu["total"])
+    assert_rates_agree(gpu.logical_error_shots, gpu.preserved_shots,
+                       cpu["error_shots"], cpu["preserved"])
