@@ -4,9 +4,10 @@
 //   smem_ld_gbs      LDS.128, conflict-free, all SMs (bytes read / s)
 //   smem_ldst_gbs    LDS.128 + STS.128 pairs (bytes read + written / s)
 //   fp64_gflops      DFMA, 8 independent chains per thread (2 flop / DFMA)
-//   issue_ginst      LOP3 warp instructions / s, 8 independent chains per
-//                    thread (one warp instruction each): the issue ceiling
-//   imad_ginst       IMAD warp instructions / s (index arithmetic mix)
+//   issue_ginst      warp instructions / s at the issue limit: the best of
+//                    FP32 FMA chains and an FMA+LOP3 mix (8 independent
+//                    chains per thread; one instruction per SMSP per clock)
+//   lop3_ginst, imad_ginst  the integer pipe (half rate on B200)
 //
 // Each is the best of 5 timed launches (CUDA events) after a warm-up, at full
 // occupancy (grid = SMs x resident blocks).  Prints one JSON object.
@@ -14,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdint.h>
+#include <algorithm>
 
 #define CK(x)                                                                        \
   do {                                                                               \
@@ -123,6 +125,46 @@ __global__ void __launch_bounds__(1024) imad_issue(int iters, uint32_t *sink) {
   if (s == 0x12345678u) sink[0] = s;
 }
 
+// FP32 FMA chains: full-rate on Blackwell (128 lanes/clk/SM = 4 warp
+// instructions / clk / SM), so this one is bound by instruction issue
+__global__ void __launch_bounds__(1024) ffma_issue(int iters, float *sink) {
+  float x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = 1.0f + 1e-6f * (threadIdx.x + c);
+  const float m = 0.9999999f, k = 1e-7f;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(m), "f"(k));
+  }
+  float s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += x[c];
+  if (s == 12345.0f) sink[0] = s;
+}
+
+// alternating FP32 FMA and LOP3 chains (two pipes): issue-bound mix
+__global__ void __launch_bounds__(1024) mix_issue(int iters, float *sink) {
+  float x[4];
+  uint32_t y[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) { x[c] = 1.0f + 1e-6f * (threadIdx.x + c); y[c] = threadIdx.x * (c + 1); }
+  const float m = 0.9999999f, k = 1e-7f;
+  const uint32_t a = blockIdx.x | 0x55u, b = 0x0f0f0f0fu;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(m), "f"(k));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y[c]) : "r"(a), "r"(b));
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) s += x[c] + (float)(y[c] & 1u);
+  if (s == 12345.0f) sink[0] = s;
+}
+
 template <typename F>
 static float best_ms(F launch) {
   cudaEvent_t a, b;
@@ -186,15 +228,31 @@ int main() {
   const float t_m = best_ms([&] { imad_issue<<<sms * per5, 1024>>>(it_i, sink); });
   CK(cudaGetLastError());
   const double wm = (double)sms * per5 * 32 * it_i * 8;
+  float *fsink;
+  CK(cudaMalloc(&fsink, 64));
+  int per6 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per6, ffma_issue, 1024, 0));
+  const float t_ff = best_ms([&] { ffma_issue<<<sms * per6, 1024>>>(it_i, fsink); });
+  CK(cudaGetLastError());
+  const double wf = (double)sms * per6 * 32 * it_i * 8;
+  int per7 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per7, mix_issue, 1024, 0));
+  const float t_mx = best_ms([&] { mix_issue<<<sms * per7, 1024>>>(it_i, fsink); });
+  CK(cudaGetLastError());
+  const double wx = (double)sms * per7 * 32 * it_i * 8;
+  const double issue = std::max(wf / t_ff, wx / t_mx) / 1e6;
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"sm_clock_max_mhz\": %.0f, "
          "\"smem_ld_gbs\": %.1f, \"smem_ldst_gbs\": %.1f, \"fp64_gflops\": %.1f, "
-         "\"issue_ginst\": %.1f, \"imad_ginst\": %.1f, "
+         "\"issue_ginst\": %.1f, \"lop3_ginst\": %.1f, \"imad_ginst\": %.1f, "
+         "\"ffma_ginst\": %.1f, \"mix_ginst\": %.1f, "
          "\"per_sm_per_clk\": {\"smem_ld_bytes\": %.1f, \"smem_ldst_bytes\": %.1f, "
-         "\"dfma_warp_inst\": %.3f, \"lop3_warp_inst\": %.3f, \"imad_warp_inst\": %.3f}}\n",
+         "\"dfma_warp_inst\": %.3f, \"lop3_warp_inst\": %.3f, \"imad_warp_inst\": %.3f, "
+         "\"issue_warp_inst\": %.3f}}\n",
          prop.name, sms, clk_khz / 1e3, b_ld / t_ld / 1e6, b_ls / t_ls / 1e6, fl / t_f / 1e6,
-         wi / t_i / 1e6, wm / t_m / 1e6,
+         issue, wi / t_i / 1e6, wm / t_m / 1e6, wf / t_ff / 1e6, wx / t_mx / 1e6,
          b_ld / (t_ld * 1e-3) / sms / (clk_khz * 1e3), b_ls / (t_ls * 1e-3) / sms / (clk_khz * 1e3),
          fl / 2 / (t_f * 1e-3) / sms / (clk_khz * 1e3) / 32.0,
-         wi / (t_i * 1e-3) / sms / (clk_khz * 1e3), wm / (t_m * 1e-3) / sms / (clk_khz * 1e3));
+         wi / (t_i * 1e-3) / sms / (clk_khz * 1e3), wm / (t_m * 1e-3) / sms / (clk_khz * 1e3),
+         issue * 1e9 / sms / (clk_khz * 1e3));
   return 0;
 }
