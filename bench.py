@@ -1,5 +1,5 @@
-"""Benchmark: MSC d=5 (grown proxy, 42 q, 72 T) shots/s on 1..8 B200, p=1e-3,
-post-selection.
+"""Benchmark: MSC d=5 (Table 2 shape: 42 q, 741 gates, 72 T) shots/s on 1..8
+B200, p=1e-3, post-selection.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
@@ -146,12 +146,16 @@ def _peaks():
 
 
 WORKLOADS = {
-    # BASELINE config 5: d=3 -> d=5 grown cultivation proxy, 42 q, 72 T
-    "msc_d5": ("msc_d5_grown_proxy", lambda m: m.msc_grown_circuit(5)),
-    # round-1 headline: all checks at d=5 (42 q, 96 T; more chi work)
+    # BASELINE config 5: d=5 cultivation with Table 2's shape (42 q, 741
+    # gates, 477 2Q, 93 M, 72 T, support 19, T-depth 6; msc.msc_d5_circuit)
+    "msc_d5": ("msc_d5_table2", lambda m: m.msc_d5_circuit()),
+    # round-1 headline: d=3 -> d=5 grown proxy (42 q, 72 T, 542 gates)
+    "msc_d5_grown": ("msc_d5_grown_proxy", lambda m: m.msc_grown_circuit(5)),
+    # all checks at d=5 (42 q, 96 T; more chi work)
     "msc_d5_2check": ("msc_d5_2check_proxy", lambda m: m.msc_circuit(5)),
-    # BASELINE config 2
-    "msc_d3": ("msc_d3_proxy", lambda m: m.msc_circuit(3)),
+    # BASELINE config 2: d=3 cultivation with Table 2's shape
+    "msc_d3": ("msc_d3_table2", lambda m: m.msc_d3_circuit()),
+    "msc_d3_proxy": ("msc_d3_proxy", lambda m: m.msc_circuit(3)),
     # BASELINE config 3 (quoted at p=5e-4: see DEFAULT_P)
     "injection_d3": ("d3_injection_3_rounds", lambda m: m.injection_circuit(3, 3)),
     # BASELINE config 1 and two points of the config-4 sweep
