@@ -1,14 +1,16 @@
-"""Golden records for the headline MSC workloads, produced by the REAL
-reference (/root/reference/pkg/src/gstab, numpy backend) in the build
-container:
+"""Golden records for the MSC workloads, produced by the REAL reference in
+the build container: the noiseless circuit text is parsed and noised by the
+reference itself (gstab.circuit.parse_circuit + gstab.noise.apply_noise_model,
+ref noise.py:104-194) and sampled by its run_shot (oracle/_ref build, Cython
+backend, bit-identical to the numpy one by ref tests/test_kernels.py):
 
-* ``msc_d5_records.npz``: the d=3 -> d=5 grown cultivation proxy
-  (``msc_grown_circuit(5)``: 42 qubits, 72 T/T_DAG) under uniform
-  depolarizing noise p=1e-3, post-selection on, 20,000 shots;
-* ``msc_d3_records.npz``: the d=3 proxy (``msc_circuit(3)``), p=1e-3,
-  20,000 shots.
+* ``msc_d5_table2_records.npz``: msc_d5_circuit() (Table 2 d=5 shape),
+  p=1e-3, post-selection, 20,000 shots;
+* ``msc_d3_table2_records.npz``: msc_d3_circuit() (Table 2 d=3), p=1e-3;
+* ``msc_d5_records.npz``: the d=3 -> d=5 grown proxy (msc_grown_circuit(5));
+* ``msc_d3_records.npz``: the d=3 proxy (msc_circuit(3)).
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_msc.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_msc.py [names]
 
 Each file holds the circuit text, master seed, statuses (1 preserved /
 2 discarded / 3 overflow), the discarding detector index and the packed
@@ -23,9 +25,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
-sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))   # oracle/build_ref.py
 sys.path.insert(0, ROOT)
-os.environ.setdefault("GSTAB_BACKEND", "python")
 
 SHOTS = 20_000
 MASTER = 20261017
@@ -76,16 +77,22 @@ def make(name, text):
     print(name, "statuses:", np.bincount(st), "errors:", int(obs[st == 1].sum()))
 
 
+def ref_noisy(prog, p):
+    """The reference's own parse + uniform noise transform of the text."""
+    from gstab.circuit import parse_circuit
+    from gstab.noise import apply_noise_model
+    return apply_noise_model(parse_circuit(prog.serialize()), p).serialize()
+
+
 def main():
-    from paper_2512_23037_b200.msc import msc_circuit, msc_grown_circuit
-    from paper_2512_23037_b200.noise import apply_noise_model
-    which = sys.argv[1:] or ["d5", "d3"]
-    if "d5" in which:
-        make("msc_d5_records.npz",
-             apply_noise_model(msc_grown_circuit(5), 1e-3).serialize())
-    if "d3" in which:
-        make("msc_d3_records.npz",
-             apply_noise_model(msc_circuit(3), 1e-3).serialize())
+    from paper_2512_23037_b200 import msc
+    jobs = {"d5t": ("msc_d5_table2_records.npz", msc.msc_d5_circuit),
+            "d3t": ("msc_d3_table2_records.npz", msc.msc_d3_circuit),
+            "d5": ("msc_d5_records.npz", lambda: msc.msc_grown_circuit(5)),
+            "d3": ("msc_d3_records.npz", lambda: msc.msc_circuit(3))}
+    for key in sys.argv[1:] or list(jobs):
+        name, build = jobs[key]
+        make(name, ref_noisy(build(), 1e-3))
 
 
 if __name__ == "__main__":

@@ -98,7 +98,8 @@ def test_d5_full_size_properties():
     assert int(c[_lib.GS_C_ERROR_SHOTS]) == a.logical_error_shots
 
 
-@pytest.mark.parametrize("name", ["msc_d5_records.npz", "msc_d3_records.npz"])
+@pytest.mark.parametrize("name", ["msc_d5_table2_records.npz", "msc_d3_table2_records.npz",
+                                  "msc_d5_records.npz", "msc_d3_records.npz"])
 def test_msc_golden_records_bit_exact(name):
     """Headline workloads: every one of the 20,000 reference-generated shots
     (statuses, discarding detector, observable, record bits) bit-exact."""
@@ -131,3 +132,39 @@ def test_grown_d5_statistics_match_oracle():
               cpu["total"])
     assert_rates_agree(gpu.logical_error_shots, gpu.preserved_shots,
               cpu["error_shots"], max(cpu["preserved"], 1))
+
+
+@pytest.mark.parametrize("d,p,rate,tol,shots", [
+    (5, 5e-4, 0.6210, 0.005, 10 ** 8),
+    (5, 1e-3, 0.8560, 0.003, 10 ** 8),
+    (5, 2e-3, 0.9792, 0.003, 10 ** 8),
+    (3, 1e-3, 0.313, 0.005, 10 ** 8)])
+def test_table2_discard_rates_match_the_paper(d, p, rate, tol, shots):
+    """Criteria 5 and 6 of the reference (ref tests/test_acceptance.py:174-199,
+    PAPER.md Table 3 / the Zenodo d=3 rate) on the Table-2 circuits with
+    10^8 GPU shots: d=5 within the reference's 0.3 points at p=1e-3, 2e-3
+    and 0.5 points at 5e-4; d=3 within 0.5 points.  Preserved shots keep a
+    logical error rate far below p (fault-tolerant observable)."""
+    from paper_2512_23037_b200.msc import msc_d3_circuit, msc_d5_circuit
+    prog = apply_noise_model(msc_d5_circuit() if d == 5 else msc_d3_circuit(), p)
+    st = run_batch(prog, SamplerConfig(shots=shots, master_seed=99, postselect=True,
+                                       rng="philox"))
+    assert abs(st.discard_rate - rate) <= tol, st.discard_rate
+    assert st.overflow_count == 0
+    assert st.logical_error_rate < (1e-4 if d == 5 else 1e-3) * (p / 1e-3) ** 2
+
+
+def test_table2_d5_statistics_match_the_reference_golden_run():
+    """The GPU's Philox stream against the reference's own 20,000-shot run
+    of the same program (tests/golden/msc_d5_table2_records.npz)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden",
+                             "msc_d5_table2_records.npz"))
+    prog = parse_circuit(str(g["text"]))
+    gpu = run_batch(prog, SamplerConfig(shots=1 << 24, master_seed=5,
+                                        postselect=True, rng="philox"))
+    n = len(g["status"])
+    assert_rates_agree(gpu.discarded_shots, gpu.total_shots,
+                       int((g["status"] == 2).sum()), n)
+    assert_rates_agree(gpu.logical_error_shots, gpu.preserved_shots,
+                       int(g["observable"][g["status"] == 1].sum()),
+                       int((g["status"] == 1).sum()))
