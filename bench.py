@@ -65,7 +65,16 @@ def _micro_peaks():
         return None
 
 
-def _roofline(secs, ncu, total_shots, value, model_bytes, hbm_peak, hbm_src):
+def _ceiling(mp, key, sm_mhz):
+    """A measured per-SM-per-clock ceiling at this run's SM clock (GB/s,
+    Gflop/s or G warp-inst/s)."""
+    per = mp[key]["per_sm_per_clk"] if isinstance(mp.get(key), dict) else None
+    if per is None:
+        return None
+    return per * mp["sms"] * (sm_mhz or mp["sm_clock_max_mhz"]) * 1e-3
+
+
+def _roofline(secs, ncu, total_shots, value, model_bytes, hbm_peak, hbm_src, sm_mhz=None):
     """Roofline of the dominant section kernel against the resource that
     binds it: chi lives in shared memory, so HBM carries only
     the section queues; the kernels are issue-bound.
@@ -73,10 +82,12 @@ def _roofline(secs, ncu, total_shots, value, model_bytes, hbm_peak, hbm_src):
     * issue: warp instructions of the dominant launch per shot (ncu capture
       of the same workload, profiles/ncu_latest.json) x the shots it ran /
       its live device time (CUDA events around that launch in this run), vs
-      the measured LOP3 issue ceiling (profiles/peaks.json);
+      the measured issue ceiling (profiles/peaks.json: warp instructions per
+      SM per clock of FP32-FMA / FMA+LOP3 chains x SMs x this run's SM clock);
     * smem: SURVEY §8(d) state-touch bytes the dominant section executed
       (counted on the device, GS_SECTION_STATS) / its live time, vs the
-      measured LDS.128+STS.128 ceiling -- the 24 B/entry model includes the
+      measured LDS.128+STS.128 ceiling (per SM per clock x SMs x clock) --
+      the 24 B/entry model includes the
       8-byte index the dense chi layout keeps implicit, so this overstates
       the shared-memory bytes actually moved (ncu wavefronts: smem_pct);
     * hbm: ncu DRAM bytes per shot x this run's rate, vs the measured copy
@@ -107,9 +118,12 @@ def _roofline(secs, ncu, total_shots, value, model_bytes, hbm_peak, hbm_src):
                 "model_bytes_per_launch": d["model_bytes"] / launches,
                 "device_ms_per_launch": d["device_ms"] / launches,
                 "sections": sec_rows})
-    if mp and smem_ach is not None:
-        out["smem"] = {"achieved": smem_ach, "peak": mp["smem_ldst_gbs"], "unit": "GB/s",
-                       "frac": smem_ach / mp["smem_ldst_gbs"],
+    smem_peak = _ceiling(mp, "smem_ldst_gbs", sm_mhz) if mp else None
+    issue_peak = (mp["issue_ipc_per_sm"] * mp["sms"] * (sm_mhz or mp["sm_clock_max_mhz"]) * 1e-3
+                  if mp and "issue_ipc_per_sm" in mp else None)
+    if smem_peak and smem_ach is not None:
+        out["smem"] = {"achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
+                       "frac": smem_ach / smem_peak,
                        "bytes": "SURVEY 8(d) state-touch model, device-counted"}
     if kern:
         scale = total_shots / ncu["shots_in_capture"]    # capture = one chunk
@@ -119,11 +133,12 @@ def _roofline(secs, ncu, total_shots, value, model_bytes, hbm_peak, hbm_src):
         out["smem_wavefront_pct_ncu"] = kern.get("smem_wavefront_pct")
         out["ncu_capture"] = ncu["capture"]
         out["traffic"] = kern["dram_bytes"] * scale / launches
-        if mp:
+        if issue_peak:
             ach = inst / dev_s / 1e9
-            out.update({"bound": "issue", "achieved": ach, "peak": mp["issue_ginst"],
-                        "unit": "Gwarp-inst/s", "frac": ach / mp["issue_ginst"],
-                        "peak_source": "measured (profiles/peaks.json, scripts/peaks.cu LOP3)"})
+            out.update({"bound": "issue", "achieved": ach, "peak": issue_peak,
+                        "unit": "Gwarp-inst/s", "frac": ach / issue_peak,
+                        "peak_source": "measured (profiles/peaks.json: scripts/peaks.cu "
+                                       "issue IPC per SM x SMs x this run's SM clock)"})
     if out["bound"] is None and "smem" in out:
         out.update({"bound": "smem", "achieved": out["smem"]["achieved"],
                     "peak": out["smem"]["peak"], "unit": "GB/s", "frac": out["smem"]["frac"],
@@ -568,7 +583,7 @@ def main():
         ncu = _ncu_latest(workload, S)
         # per GPU: this rank's section launches, shots and rate
         roofline = _roofline(secs, ncu, S * args.steps, value / world,
-                             model_bytes // world, peak, peak_src)
+                             model_bytes // world, peak, peak_src, ck.get("sm_mhz"))
         if not args.no_cpu_baseline:
             if _have_reference() and not args.ref_port:
                 cb = reference_baseline(text, args.p, args.cpu_seconds)

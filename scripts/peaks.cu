@@ -4,18 +4,23 @@
 //   smem_ld_gbs      LDS.128, conflict-free, all SMs (bytes read / s)
 //   smem_ldst_gbs    LDS.128 + STS.128 pairs (bytes read + written / s)
 //   fp64_gflops      DFMA, 8 independent chains per thread (2 flop / DFMA)
-//   issue_ginst      warp instructions / s at the issue limit: the best of
-//                    FP32 FMA chains and an FMA+LOP3 mix (8 independent
-//                    chains per thread; one instruction per SMSP per clock)
+//   ffma_ginst, mix_ginst  warp instructions / s of FP32 FMA chains and an
+//                    FMA+LOP3 mix (8 independent chains per thread): the
+//                    issue limit, one instruction per SMSP per clock
 //   lop3_ginst, imad_ginst  the integer pipe (half rate on B200)
 //
 // Each is the best of 5 timed launches (CUDA events) after a warm-up, at full
-// occupancy (grid = SMs x resident blocks).  Prints one JSON object.
+// occupancy (grid = SMs x resident blocks).  Heavy FP loads can pull the SM
+// clock below its maximum, so every kernel also reports the clock it ran at
+// (clock64 / globaltimer per block) and its rate per SM per clock; the
+// ceilings a kernel running at clock f is held to are per_sm_per_clk x SMs x
+// f (issue_ipc_per_sm, ..._at_max_clock).  Prints one JSON object.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/peaks scripts/peaks.cu
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdint.h>
 #include <algorithm>
+#include <vector>
 
 #define CK(x)                                                                        \
   do {                                                                               \
@@ -26,15 +31,36 @@
     }                                                                                \
   } while (0)
 
+// per-block elapsed SM cycles and ns (thread 0, between two barriers): the
+// clock the SMs actually ran at during the measurement (heavy FP loads can
+// drop below the maximum), so rates are also reported per SM per clock
+struct Tm { unsigned long long c0, t0; };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ Tm tstart() {
+  __syncthreads();
+  return Tm{(unsigned long long)clock64(), gtimer()};
+}
+__device__ __forceinline__ void tstop(Tm t, unsigned long long *cyc, unsigned long long *ns) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cyc[blockIdx.x] = (unsigned long long)clock64() - t.c0;
+    ns[blockIdx.x] = gtimer() - t.t0;
+  }
+}
+
 constexpr int kSmemWords = 8192;   // 16-B words; each block uses half (64 KB)
 
-__global__ void __launch_bounds__(1024) smem_ld(int iters, uint32_t *sink) {
+__global__ void __launch_bounds__(1024) smem_ld(int iters, uint32_t *sink, unsigned long long *cyc, unsigned long long *ns) {
   extern __shared__ uint4 buf[];
   const int n = kSmemWords / 2;    // 64 KB per block: two blocks per SM
   for (int i = threadIdx.x; i < n; i += blockDim.x) buf[i] = make_uint4(i, i * 3, i * 5, i * 7);
-  __syncthreads();
   uint32_t a = 0, b = 0, c = 0, d = 0;
   int idx = threadIdx.x;
+  const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -47,15 +73,16 @@ __global__ void __launch_bounds__(1024) smem_ld(int iters, uint32_t *sink) {
     }
     idx += 32;
   }
+  tstop(tm, cyc, ns);
   if ((a ^ b ^ c ^ d) == 0x12345678u) sink[0] = a;
 }
 
-__global__ void __launch_bounds__(1024) smem_ldst(int iters, uint32_t *sink) {
+__global__ void __launch_bounds__(1024) smem_ldst(int iters, uint32_t *sink, unsigned long long *cyc, unsigned long long *ns) {
   extern __shared__ uint4 buf[];
   const int n = kSmemWords / 2;
   for (int i = threadIdx.x; i < n; i += blockDim.x) buf[i] = make_uint4(i, i * 3, i * 5, i * 7);
-  __syncthreads();
   int idx = threadIdx.x;
+  const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -71,54 +98,60 @@ __global__ void __launch_bounds__(1024) smem_ldst(int iters, uint32_t *sink) {
     }
     idx += 32;    // conflict-free rows; slot values are irrelevant (bandwidth only)
   }
-  __syncthreads();
+  tstop(tm, cyc, ns);
   if (buf[threadIdx.x].x == 0x12345678u) sink[0] = 1;
 }
 
-__global__ void __launch_bounds__(512) fp64_fma(int iters, double *sink) {
+__global__ void __launch_bounds__(512) fp64_fma(int iters, double *sink, unsigned long long *cyc, unsigned long long *ns) {
   double x[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) x[c] = 1.0 + 1e-9 * (threadIdx.x + c);
   const double m = 0.999999999, k = 1e-9;
+const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) x[c] = fma(x[c], m, k);
   }
+  tstop(tm, cyc, ns);
   double s = 0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) s += x[c];
   if (s == 12345.0) sink[0] = s;
 }
 
-__global__ void __launch_bounds__(1024) lop3_issue(int iters, uint32_t *sink) {
+__global__ void __launch_bounds__(1024) lop3_issue(int iters, uint32_t *sink, unsigned long long *cyc, unsigned long long *ns) {
   uint32_t x[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) x[c] = threadIdx.x * (c + 1);
   const uint32_t y = blockIdx.x | 0x55u, z = 0x0f0f0f0fu;
+const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(y), "r"(z));
   }
+  tstop(tm, cyc, ns);
   uint32_t s = 0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) s ^= x[c];
   if (s == 0x12345678u) sink[0] = s;
 }
 
-__global__ void __launch_bounds__(1024) imad_issue(int iters, uint32_t *sink) {
+__global__ void __launch_bounds__(1024) imad_issue(int iters, uint32_t *sink, unsigned long long *cyc, unsigned long long *ns) {
   uint32_t x[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) x[c] = threadIdx.x * (c + 1);
   const uint32_t y = blockIdx.x | 3u, z = 0x9e3779b9u;
+const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(y), "r"(z));
   }
+  tstop(tm, cyc, ns);
   uint32_t s = 0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) s ^= x[c];
@@ -127,16 +160,18 @@ __global__ void __launch_bounds__(1024) imad_issue(int iters, uint32_t *sink) {
 
 // FP32 FMA chains: full-rate on Blackwell (128 lanes/clk/SM = 4 warp
 // instructions / clk / SM), so this one is bound by instruction issue
-__global__ void __launch_bounds__(1024) ffma_issue(int iters, float *sink) {
+__global__ void __launch_bounds__(1024) ffma_issue(int iters, float *sink, unsigned long long *cyc, unsigned long long *ns) {
   float x[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) x[c] = 1.0f + 1e-6f * (threadIdx.x + c);
   const float m = 0.9999999f, k = 1e-7f;
+const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(m), "f"(k));
   }
+  tstop(tm, cyc, ns);
   float s = 0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) s += x[c];
@@ -144,13 +179,14 @@ __global__ void __launch_bounds__(1024) ffma_issue(int iters, float *sink) {
 }
 
 // alternating FP32 FMA and LOP3 chains (two pipes): issue-bound mix
-__global__ void __launch_bounds__(1024) mix_issue(int iters, float *sink) {
+__global__ void __launch_bounds__(1024) mix_issue(int iters, float *sink, unsigned long long *cyc, unsigned long long *ns) {
   float x[4];
   uint32_t y[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) { x[c] = 1.0f + 1e-6f * (threadIdx.x + c); y[c] = threadIdx.x * (c + 1); }
   const float m = 0.9999999f, k = 1e-7f;
   const uint32_t a = blockIdx.x | 0x55u, b = 0x0f0f0f0fu;
+const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -159,6 +195,7 @@ __global__ void __launch_bounds__(1024) mix_issue(int iters, float *sink) {
       asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y[c]) : "r"(a), "r"(b));
     }
   }
+  tstop(tm, cyc, ns);
   float s = 0;
 #pragma unroll
   for (int c = 0; c < 4; ++c) s += x[c] + (float)(y[c] & 1u);
@@ -187,72 +224,107 @@ static float best_ms(F launch) {
   return best;
 }
 
+struct Res {
+  double rate;       // units / s (wall, CUDA events)
+  double mhz;        // SM clock during the last launch (clock64 / globaltimer)
+  double per_sm_clk; // units per SM per clock at that clock
+};
+
+static unsigned long long *g_cyc, *g_ns;
+static int g_sms;
+
+// units = total work units of one launch of `blocks` blocks
+template <typename F>
+static Res measure(F launch, double units, int blocks) {
+  const float ms = best_ms(launch);
+  std::vector<unsigned long long> c(blocks), n(blocks);
+  cudaMemcpy(c.data(), g_cyc, blocks * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(n.data(), g_ns, blocks * 8, cudaMemcpyDeviceToHost);
+  double sc = 0, sn = 0;
+  for (int i = 0; i < blocks; ++i) { sc += (double)c[i]; sn += (double)n[i]; }
+  Res r;
+  r.rate = units / (ms * 1e-3);
+  r.mhz = sn > 0 ? 1e3 * sc / sn : 0.0;
+  r.per_sm_clk = r.mhz > 0 ? r.rate / g_sms / (r.mhz * 1e6) : 0.0;
+  return r;
+}
+
+static void emit(const char *name, Res r, double scale, bool last = false) {
+  printf("\"%s\": {\"rate\": %.1f, \"sm_mhz\": %.0f, \"per_sm_per_clk\": %.3f}%s", name,
+         r.rate * scale, r.mhz, r.per_sm_clk, last ? "" : ", ");
+}
+
 int main() {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, 0));
   const int sms = prop.multiProcessorCount;
+  g_sms = sms;
   int clk_khz = 0;
   CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
   uint32_t *sink;
   double *dsink;
+  float *fsink;
   CK(cudaMalloc(&sink, 64));
   CK(cudaMalloc(&dsink, 64));
+  CK(cudaMalloc(&fsink, 64));
+  CK(cudaMalloc(&g_cyc, 1 << 20));
+  CK(cudaMalloc(&g_ns, 1 << 20));
+  unsigned long long *cy = g_cyc, *ns = g_ns;
   const size_t smem = (size_t)kSmemWords / 2 * 16;   // 64 KB
   CK(cudaFuncSetAttribute(smem_ld, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(smem_ldst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per = 0;
+  const int it_s = 4096, it_f = 8192, it_i = 8192;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, smem_ld, 1024, smem));
-  const int it_s = 4096;
-  const float t_ld = best_ms([&] { smem_ld<<<sms * per, 1024, smem>>>(it_s, sink); });
+  const int b1 = sms * per;
+  const Res ld = measure([&] { smem_ld<<<b1, 1024, smem>>>(it_s, sink, cy, ns); },
+                         (double)b1 * 1024 * it_s * 8 * 16, b1);
   CK(cudaGetLastError());
-  const double b_ld = (double)sms * per * 1024 * it_s * 8 * 16;
-  int per2 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, smem_ldst, 1024, smem));
-  const float t_ls = best_ms([&] { smem_ldst<<<sms * per2, 1024, smem>>>(it_s, sink); });
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, smem_ldst, 1024, smem));
+  const int b2 = sms * per;
+  const Res ls = measure([&] { smem_ldst<<<b2, 1024, smem>>>(it_s, sink, cy, ns); },
+                         (double)b2 * 1024 * it_s * 4 * 32, b2);
   CK(cudaGetLastError());
-  const double b_ls = (double)sms * per2 * 1024 * it_s * 4 * 32;
-  int per3 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per3, fp64_fma, 512, 0));
-  const int it_f = 8192;
-  const float t_f = best_ms([&] { fp64_fma<<<sms * per3, 512>>>(it_f, dsink); });
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fp64_fma, 512, 0));
+  const int b3 = sms * per;
+  const Res fp = measure([&] { fp64_fma<<<b3, 512>>>(it_f, dsink, cy, ns); },
+                         (double)b3 * 512 * it_f * 8 * 2, b3);
   CK(cudaGetLastError());
-  const double fl = (double)sms * per3 * 512 * it_f * 8 * 2;
-  int per4 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per4, lop3_issue, 1024, 0));
-  const int it_i = 8192;
-  const float t_i = best_ms([&] { lop3_issue<<<sms * per4, 1024>>>(it_i, sink); });
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lop3_issue, 1024, 0));
+  const int b4 = sms * per;
+  const Res lo = measure([&] { lop3_issue<<<b4, 1024>>>(it_i, sink, cy, ns); },
+                         (double)b4 * 32 * it_i * 8, b4);
   CK(cudaGetLastError());
-  const double wi = (double)sms * per4 * 32 * it_i * 8;
-  int per5 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per5, imad_issue, 1024, 0));
-  const float t_m = best_ms([&] { imad_issue<<<sms * per5, 1024>>>(it_i, sink); });
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, imad_issue, 1024, 0));
+  const int b5 = sms * per;
+  const Res im = measure([&] { imad_issue<<<b5, 1024>>>(it_i, sink, cy, ns); },
+                         (double)b5 * 32 * it_i * 8, b5);
   CK(cudaGetLastError());
-  const double wm = (double)sms * per5 * 32 * it_i * 8;
-  float *fsink;
-  CK(cudaMalloc(&fsink, 64));
-  int per6 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per6, ffma_issue, 1024, 0));
-  const float t_ff = best_ms([&] { ffma_issue<<<sms * per6, 1024>>>(it_i, fsink); });
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ffma_issue, 1024, 0));
+  const int b6 = sms * per;
+  const Res ff = measure([&] { ffma_issue<<<b6, 1024>>>(it_i, fsink, cy, ns); },
+                         (double)b6 * 32 * it_i * 8, b6);
   CK(cudaGetLastError());
-  const double wf = (double)sms * per6 * 32 * it_i * 8;
-  int per7 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per7, mix_issue, 1024, 0));
-  const float t_mx = best_ms([&] { mix_issue<<<sms * per7, 1024>>>(it_i, fsink); });
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mix_issue, 1024, 0));
+  const int b7 = sms * per;
+  const Res mx = measure([&] { mix_issue<<<b7, 1024>>>(it_i, fsink, cy, ns); },
+                         (double)b7 * 32 * it_i * 8, b7);
   CK(cudaGetLastError());
-  const double wx = (double)sms * per7 * 32 * it_i * 8;
-  const double issue = std::max(wf / t_ff, wx / t_mx) / 1e6;
-  printf("{\"gpu\": \"%s\", \"sms\": %d, \"sm_clock_max_mhz\": %.0f, "
-         "\"smem_ld_gbs\": %.1f, \"smem_ldst_gbs\": %.1f, \"fp64_gflops\": %.1f, "
-         "\"issue_ginst\": %.1f, \"lop3_ginst\": %.1f, \"imad_ginst\": %.1f, "
-         "\"ffma_ginst\": %.1f, \"mix_ginst\": %.1f, "
-         "\"per_sm_per_clk\": {\"smem_ld_bytes\": %.1f, \"smem_ldst_bytes\": %.1f, "
-         "\"dfma_warp_inst\": %.3f, \"lop3_warp_inst\": %.3f, \"imad_warp_inst\": %.3f, "
-         "\"issue_warp_inst\": %.3f}}\n",
-         prop.name, sms, clk_khz / 1e3, b_ld / t_ld / 1e6, b_ls / t_ls / 1e6, fl / t_f / 1e6,
-         issue, wi / t_i / 1e6, wm / t_m / 1e6, wf / t_ff / 1e6, wx / t_mx / 1e6,
-         b_ld / (t_ld * 1e-3) / sms / (clk_khz * 1e3), b_ls / (t_ls * 1e-3) / sms / (clk_khz * 1e3),
-         fl / 2 / (t_f * 1e-3) / sms / (clk_khz * 1e3) / 32.0,
-         wi / (t_i * 1e-3) / sms / (clk_khz * 1e3), wm / (t_m * 1e-3) / sms / (clk_khz * 1e3),
-         issue * 1e9 / sms / (clk_khz * 1e3));
+  // the issue ceiling per SM per clock (best instruction mix), and the
+  // rates it implies at the maximum SM clock
+  const double ipc = std::max(ff.per_sm_clk, mx.per_sm_clk);
+  const double fmax = clk_khz / 1e3;
+  printf("{\"gpu\": \"%s\", \"sms\": %d, \"sm_clock_max_mhz\": %.0f, ", prop.name, sms, fmax);
+  emit("smem_ld_gbs", ld, 1e-9);
+  emit("smem_ldst_gbs", ls, 1e-9);
+  emit("fp64_gflops", fp, 1e-9);
+  emit("lop3_ginst", lo, 1e-9);
+  emit("imad_ginst", im, 1e-9);
+  emit("ffma_ginst", ff, 1e-9);
+  emit("mix_ginst", mx, 1e-9);
+  printf("\"issue_ipc_per_sm\": %.3f, \"issue_ginst_at_max_clock\": %.1f, "
+         "\"smem_ldst_gbs_at_max_clock\": %.1f, \"fp64_gflops_at_max_clock\": %.1f}\n",
+         ipc, ipc * sms * fmax * 1e-3, ls.per_sm_clk * sms * fmax * 1e-3,
+         fp.per_sm_clk * sms * fmax * 1e-3);
   return 0;
 }
