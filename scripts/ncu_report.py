@@ -49,10 +49,19 @@ def main():
             if m in h:
                 i = h.index(m)
                 print("  %-80s %s %s" % (m, r[i], units[i]))
-    for kern, label in (("narrow", "narrow_kernel (first section)"),
-                        ("wide", "wide_kernel (first wide section)")):
+    # source attribution of the longest launch of each kernel
+    it = h.index("gpu__time_duration.sum")
+    for kern in ("narrow", "wide"):
+        mine = [r for r in rows[2:] if r[h.index("Kernel Name")].startswith("void %s_kernel" % kern)]
+        if not mine:
+            continue
+        dur = [float(r[it]) if r[it] not in ("", "-nan", "nan") else 0.0 for r in mine]
+        skip = max(range(len(mine)), key=lambda i: dur[i])
+        label = "%s_kernel (its longest launch: #%d of %d, %s %s)" % (
+            kern, skip, len(mine), mine[skip][it], units[it])
         src = ncu(rep, "--page", "source", "--csv", "--print-source", "sass",
-                  "-k", "regex:%s_kernel" % kern, "--launch-count", "1")
+                  "-k", "regex:%s_kernel" % kern, "--launch-skip", str(skip),
+                  "--launch-count", "1")
         if not src.strip():
             continue
         with tempfile.NamedTemporaryFile("w", suffix=".csv", delete=False) as f:
