@@ -39,6 +39,9 @@
 #ifndef GS_BLOCK_WARPS
 #define GS_BLOCK_WARPS 16  // warps sharing one shot's chi (block form)
 #endif
+#ifndef GS_BLOCK_MINB
+#define GS_BLOCK_MINB 1   // resident blocks the block form is compiled for (register bound)
+#endif
 #ifndef GS_BLOCK_MIN_DIM
 #define GS_BLOCK_MIN_DIM 14   // chi dimension from which the block form is the default
 #endif
@@ -679,7 +682,7 @@ template <bool kSmemChi, bool kPhilox, int kG>
 #ifdef GS_WIDE_MAXREG
 __global__ void __maxnreg__(GS_WIDE_MAXREG)
 #else
-__global__ void __launch_bounds__(kG == 1 ? 32 * GS_WIDE_WARPS : 32 * kG, kG == 1 ? GS_WIDE_BLOCKS : 1)
+__global__ void __launch_bounds__(kG == 1 ? 32 * GS_WIDE_WARPS : 32 * kG, kG == 1 ? GS_WIDE_BLOCKS : GS_BLOCK_MINB)
 #endif
 wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   extern __shared__ __align__(16) u8 smem[];

@@ -77,13 +77,20 @@ struct Gate {
 __device__ __forceinline__ double neg_if1(double x, u32 s) {
   return __longlong_as_double(__double_as_longlong(x) ^ ((long long)s << 63));
 }
+// The sign arrives as a mask m (0 or 1u << 31, the high word's sign bit) and
+// is XORed into the high words of the products ss*w: (-ss)*w == -(ss*w) bit
+// for bit, and callers fold the static part of m into the same LOP3 (the
+// fused-pair loop: 171 instead of 177 instructions per group).
+__device__ __forceinline__ double flip_hi(double x, u32 m) {
+  return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
 template <bool kR>
-__device__ __forceinline__ double2 t_mix(const Gate &g, double2 v, double2 w, u32 s) {
+__device__ __forceinline__ double2 t_mix(const Gate &g, double2 v, double2 w, u32 m) {
   if (kR) {
-    const double sx = neg_if1(g.ss, s);
-    return make_double2(__fma_rn(kTc, v.x, -__dmul_rn(sx, w.y)), __fma_rn(kTc, v.y, __dmul_rn(sx, w.x)));
+    const double px = flip_hi(__dmul_rn(g.ss, w.y), m), py = flip_hi(__dmul_rn(g.ss, w.x), m);
+    return make_double2(__fma_rn(kTc, v.x, -px), __fma_rn(kTc, v.y, py));
   }
-  return cadd(cmul(g.a, v), neg_if(cmul(g.bx0, w), s));
+  return cadd(cmul(g.a, v), neg_if(cmul(g.bx0, w), m >> 31));
 }
 
 // T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
@@ -99,15 +106,15 @@ __device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, const Ga
   r.sum = 0.0;
   r.nz = 0;
   const u32 jl = ins_bit(lane, hb, 0);
-  const u32 pl = g.dc ^ par32(jl & dmask), pcb = par32(cb & dmask);
+  const u32 pl = g.dc ^ par32(jl & dmask), pcb = par32(cb & dmask) << 31;
 #pragma unroll 1
   for (u32 m = lane; m < half; m += 32u * kG) {
     const u32 jr = ins_bit(m & ~(32u * kG - 1u), hb, 0);
     const u32 j0 = jr | jl, j1 = j0 ^ cb;
     const double2 v0 = A[j0], v1 = A[j1];
-    const u32 s0 = pl ^ par32(jr & dmask), s1 = s0 ^ pcb;
-    A[j0] = prune_acc(t_mix<kR>(g, v0, v1, s1), r.sum, r.nz);
-    A[j1] = prune_acc(t_mix<kR>(g, v1, v0, s0), r.sum, r.nz);
+    const u32 m0 = (pl ^ par32(jr & dmask)) << 31, m1 = m0 ^ pcb;
+    A[j0] = prune_acc(t_mix<kR>(g, v0, v1, m1), r.sum, r.nz);
+    A[j1] = prune_acc(t_mix<kR>(g, v1, v0, m0), r.sum, r.nz);
   }
   return r;
 }
@@ -142,15 +149,16 @@ __device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, con
   // (a per-round and a per-lane term); the group members differ by cb1, cb2
   const u32 jl = ins_bit(ins_bit(lane, plo, 0), phi, 0);
   const u32 l1 = g1.dc ^ par32(jl & g1.dmask), l2 = g2.dc ^ par32(jl & g2.dmask);
-  const u32 a1 = par32(g1.cb & g1.dmask), b1 = par32(g2.cb & g1.dmask);
-  const u32 a2 = par32(g1.cb & g2.dmask), b2 = par32(g2.cb & g2.dmask);
+  // static sign masks (bit 31) of the group members relative to x0
+  const u32 a1 = par32(g1.cb & g1.dmask) << 31, b1 = par32(g2.cb & g1.dmask) << 31;
+  const u32 a2 = par32(g1.cb & g2.dmask) << 31, b2 = par32(g2.cb & g2.dmask) << 31;
 #pragma unroll 1
   for (u32 m = lane; m < quarter; m += 32u * kG) {
     const u32 jr = ins_bit(ins_bit(m & ~(32u * kG - 1u), plo, 0), phi, 0);
     const u32 x0 = jr | jl;
     const u32 x1 = x0 ^ g1.cb, x2 = x0 ^ g2.cb, x3 = x1 ^ g2.cb;
     const double2 v0 = A[x0], v1 = A[x1], v2 = A[x2], v3 = A[x3];
-    const u32 p1 = l1 ^ par32(jr & g1.dmask), p2 = l2 ^ par32(jr & g2.dmask);
+    const u32 p1 = (l1 ^ par32(jr & g1.dmask)) << 31, p2 = (l2 ^ par32(jr & g2.dmask)) << 31;
     // gate 1: pairs (x0, x1), (x2, x3)
     const u32 s0 = p1, s1 = p1 ^ a1, s2 = p1 ^ b1, s3 = p1 ^ a1 ^ b1;
     const double2 u0 = prune_acc(t_mix<kR>(g1, v0, v1, s1), dummy, r.nz1);

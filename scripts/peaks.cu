@@ -8,6 +8,7 @@
 //                    FMA+LOP3 mix (8 independent chains per thread): the
 //                    issue limit, one instruction per SMSP per clock
 //   lop3_ginst, imad_ginst  the integer pipe (half rate on B200)
+//   l2_rw_gbs        L2-resident float4 read + write streams, one block per SM
 //
 // Each is the best of 5 timed launches (CUDA events) after a warm-up, at full
 // occupancy (grid = SMs x resident blocks).  Heavy FP loads can pull the SM
@@ -102,6 +103,31 @@ __global__ void __launch_bounds__(1024) smem_ldst(int iters, uint32_t *sink, uns
   if (buf[threadIdx.x].x == 0x12345678u) sink[0] = 1;
 }
 
+// L2-resident read + write: every block streams its own slice of a buffer
+// that fits in L2 (the block-per-shot chi lives in such a buffer; DESIGN
+// §3), float4 loads 4 deep per thread, then stores; bytes read + written
+__global__ void __launch_bounds__(512) l2_rw(int iters, uint4 *buf, size_t slice_u4, uint32_t *sink,
+                                             unsigned long long *cyc, unsigned long long *ns) {
+  uint4 *mine = buf + (size_t)blockIdx.x * slice_u4;
+  const Tm tm = tstart();
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 1
+    for (size_t i = threadIdx.x; i + 3 * blockDim.x < slice_u4; i += 4 * blockDim.x) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(mine + i + u * blockDim.x);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u].x ^= 1u;
+        __stcg(mine + i + u * blockDim.x, v[u]);
+      }
+    }
+  }
+  tstop(tm, cyc, ns);
+  if (mine[threadIdx.x].y == 0x12345678u) sink[0] = 1;
+}
+
 __global__ void __launch_bounds__(512) fp64_fma(int iters, double *sink, unsigned long long *cyc, unsigned long long *ns) {
   double x[8];
 #pragma unroll
@@ -158,6 +184,8 @@ const Tm tm = tstart();
   if (s == 0x12345678u) sink[0] = s;
 }
 
+constexpr int kIssueUnroll = 16;
+
 // FP32 FMA chains: full-rate on Blackwell (128 lanes/clk/SM = 4 warp
 // instructions / clk / SM), so this one is bound by instruction issue
 __global__ void __launch_bounds__(1024) ffma_issue(int iters, float *sink, unsigned long long *cyc, unsigned long long *ns) {
@@ -168,8 +196,12 @@ __global__ void __launch_bounds__(1024) ffma_issue(int iters, float *sink, unsig
 const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
+    // kIssueUnroll x 8 FMAs per trip: the loop's own counter/compare/branch
+    // (3 instructions) stay below 3 % of what is issued
 #pragma unroll
-    for (int c = 0; c < 8; ++c) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(m), "f"(k));
+    for (int u = 0; u < kIssueUnroll; ++u)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(m), "f"(k));
   }
   tstop(tm, cyc, ns);
   float s = 0;
@@ -190,10 +222,12 @@ const Tm tm = tstart();
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(m), "f"(k));
-      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y[c]) : "r"(a), "r"(b));
-    }
+    for (int u = 0; u < kIssueUnroll; ++u)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(x[c]) : "f"(m), "f"(k));
+        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y[c]) : "r"(a), "r"(b));
+      }
   }
   tstop(tm, cyc, ns);
   float s = 0;
@@ -302,13 +336,25 @@ int main() {
   CK(cudaGetLastError());
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ffma_issue, 1024, 0));
   const int b6 = sms * per;
-  const Res ff = measure([&] { ffma_issue<<<b6, 1024>>>(it_i, fsink, cy, ns); },
-                         (double)b6 * 32 * it_i * 8, b6);
+  const int it_u = it_i / kIssueUnroll;
+  const Res ff = measure([&] { ffma_issue<<<b6, 1024>>>(it_u, fsink, cy, ns); },
+                         (double)b6 * 32 * it_u * kIssueUnroll * 8, b6);
   CK(cudaGetLastError());
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mix_issue, 1024, 0));
   const int b7 = sms * per;
-  const Res mx = measure([&] { mix_issue<<<b7, 1024>>>(it_i, fsink, cy, ns); },
-                         (double)b7 * 32 * it_i * 8, b7);
+  const Res mx = measure([&] { mix_issue<<<b7, 1024>>>(it_u, fsink, cy, ns); },
+                         (double)b7 * 32 * it_u * kIssueUnroll * 8, b7);
+  CK(cudaGetLastError());
+  // L2: 48 MiB in total (below one die's half of the 126 MB L2), one
+  // 512-thread block per SM streaming its slice
+  uint4 *l2buf;
+  const size_t l2_bytes = (size_t)48 << 20;
+  CK(cudaMalloc(&l2buf, l2_bytes));
+  CK(cudaMemset(l2buf, 0, l2_bytes));
+  const size_t slice = l2_bytes / 16 / sms / 2048 * 2048;
+  const int it_l2 = 64;
+  const Res l2 = measure([&] { l2_rw<<<sms, 512>>>(it_l2, l2buf, slice, sink, cy, ns); },
+                         (double)sms * slice * 16 * 2 * it_l2, sms);
   CK(cudaGetLastError());
   // the issue ceiling per SM per clock (best instruction mix), and the
   // rates it implies at the maximum SM clock
@@ -322,6 +368,7 @@ int main() {
   emit("imad_ginst", im, 1e-9);
   emit("ffma_ginst", ff, 1e-9);
   emit("mix_ginst", mx, 1e-9);
+  emit("l2_rw_gbs", l2, 1e-9);
   printf("\"issue_ipc_per_sm\": %.3f, \"issue_ginst_at_max_clock\": %.1f, "
          "\"smem_ldst_gbs_at_max_clock\": %.1f, \"fp64_gflops_at_max_clock\": %.1f}\n",
          ipc, ipc * sms * fmax * 1e-3, ls.per_sm_clk * sms * fmax * 1e-3,
