@@ -18,7 +18,7 @@ from .circuit import (Block, CircuitProgram, Instruction, ParseError,
                       PauliProduct, Rec, compute_stats, parse_circuit)
 from .noise import NoiseModelError, NoiseOp, apply_noise_model
 from .compiler import CompileError, DeviceProgram, compile_program
-from .sampler import (CorruptStateError, RunStats, SamplerConfig, ShotBatch,
+from .sampler import (CorruptStateError, UnsupportedCircuitError, RunStats, SamplerConfig, ShotBatch,
                       ShotContext, ShotResult, ShotStatus, bayes_interval,
                       derive_seed, run_batch, run_shot, sample,
                       throughput_bench)
@@ -29,7 +29,7 @@ __all__ = [
     "Block", "CircuitProgram", "Instruction", "ParseError", "PauliProduct",
     "Rec", "compute_stats", "parse_circuit", "NoiseModelError", "NoiseOp",
     "apply_noise_model", "CompileError", "DeviceProgram", "compile_program",
-    "CorruptStateError", "RunStats", "SamplerConfig", "ShotBatch",
+    "CorruptStateError", "UnsupportedCircuitError", "RunStats", "SamplerConfig", "ShotBatch",
     "ShotContext", "ShotResult", "ShotStatus", "bayes_interval", "derive_seed",
     "run_batch", "run_shot", "sample", "throughput_bench", "__version__",
 ]

@@ -469,14 +469,14 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     if (per < 1) return fail(GS_ERR_UNSUPPORTED, "block-per-shot state exceeds the SM");
     KW.blocks = (u32)(e->num_sms * per);
     if (!smem_chi) {
-      const u64 max_blocks = ((u64)8 << 30) / chi;
+      const u64 max_blocks = ((u64)8 << 30) / (2 * chi);   // two buffers per block
       if ((u64)KW.blocks > max_blocks) KW.blocks = (u32)std::max<u64>(1, max_blocks);
     }
   }
   if (r->blocks) { KN.blocks = r->blocks; KW.blocks = r->blocks; }
   const u64 nwarps = std::max((u64)KN.blocks * KN.wpb, (u64)KW.blocks * KW.wpb);
   if (!smem_chi && any_wide) {
-    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 1 : KW.wpb) * chi);
+    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 2 : KW.wpb) * chi);
     if (rc) return rc;
   }
   if (!KN.rec_in_smem || !KW.rec_in_smem) {

@@ -702,9 +702,14 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   GroupScratch grp;
   grp.slots = reinterpret_cast<u64 *>(smem + (size_t)wpb * O.warp_bytes);
   grp.tog = 0;
+  // block form on global memory: two chi buffers per block (ping-pong), so
+  // the compacting passes write the other buffer in one pass without
+  // per-round barriers (kPP)
+  constexpr bool kPP = kG > 1 && !kSmemChi;
   double2 *A = kSmemChi ? chi_ptr<true>(reinterpret_cast<double2 *>(
                               kG == 1 ? mine + O.chi_off : smem + O.chi_off))
-                        : O.gchi + (kG == 1 ? gw : (u64)blockIdx.x) * ((u64)1 << P.max_dim);
+                        : O.gchi + (kG == 1 ? gw : 2ull * blockIdx.x) * ((u64)1 << P.max_dim);
+  double2 *Bf = kPP ? A + ((u64)1 << P.max_dim) : nullptr;
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
   const u64 *__restrict__ tables = P.tables;
@@ -1083,7 +1088,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const double rs = inv_sqrt_norm(plus ? sp : sm);
           if (wfl & MF_COMPACT) {
             const u32 tau = want_neg ^ neg0;
-            const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, rs, ps);
+            SumNz r;
+            if (kPP) {
+              r = sweep_compact_to<kG>(A, Bf, size >> 1, isq, dmask, tau, rs, ps);
+              double2 *t_ = A; A = Bf; Bf = t_;
+            } else {
+              r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, rs, ps);
+            }
             ps = 1.0;
             gsync<kG>();
             cnt = group_sum_u32<kG>(r.nz, grp);
@@ -1111,18 +1122,32 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
           g.dc = dc; g.dmask = dmask;
           const double2 xpp = ipow(xi0);   // i^xi0, exact
-          const double pp = __dmul_rn(0.5, group_sum<kG>(sweep_pivot_p<kSmemChi, kG>(A, g, xpp, ps), grp));
+          // no span: every entry is either its pair's rep (w = v) or its
+          // part (w = +-i^xi0 v, an exact rotation), so sum |w+|^2 is the
+          // chi norm the writer passes track -- no read pass
+          const double pp = __dmul_rn(0.5, g.span ? group_sum<kG>(sweep_pivot_p<kSmemChi, kG>(A, g, xpp, ps), grp)
+                                                  : (nrm_lane0 ? nrm_u : group_sum<kG>(nrm_l, grp)));
           plus = pick_plus(pp);
           const double chosen = plus ? pp : __dsub_rn(1.0, pp);
           if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
-          const SumNz w = sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
+          // ping-pong (block form on global memory): a span pivot writes
+          // the merged pairs straight to their compacted slots in the other
+          // buffer (the compaction's source slot is the pair's rep slot) and
+          // the renormalisation is deferred (ldps) -- two passes, not three
+          const bool fused = kPP && g.span;
+          const SumNz w = fused ? sweep_pivot_wc<kG>(A, Bf, g, xpp, plus, ps)
+                                : sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
           ps = 1.0;
           gsync<kG>();
           const double sk = group_sum<kG>(w.sum, grp);
           cnt = group_sum_u32<kG>(w.nz, grp);
           if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
           const double rs = inv_sqrt_norm(sk);
-          if (g.span) {
+          if (fused) {
+            double2 *t_ = A; A = Bf; Bf = t_;
+            kcur = wk - 1;
+            defer_scale(rs, sk);
+          } else if (g.span) {
             const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
             gsync<kG>();
             cnt = group_sum_u32<kG>(r.nz, grp);

@@ -3,6 +3,11 @@
 #pragma once
 
 // @region sweeps
+#ifndef GS_GUNROLL
+#define GS_GUNROLL 2   // block form (kG > 1, chi in L2): read-only / out-of-place passes
+                       // keep this many iterations' loads in flight per thread (A/B r02g: 2 ~ 4 > 1)
+#endif
+constexpr int kGUnroll = GS_GUNROLL;   // (pragmas do not expand macros)
 // ---------------------------------------------------------------- wide sweeps
 //
 // Warp-cooperative passes over a dense chi array A[0, 2^k): lane l takes
@@ -186,9 +191,7 @@ __device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, const Gate &g
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
-#pragma unroll 1
-  for (u32 j = lane; j < size; j += 32u * kG) {
-    const double2 v = A[j];
+  auto one = [&](u32 j, double2 v) {
     const u32 s = g.dc ^ par32(j & g.dmask);
     if (kR) {
       const double sx = neg_if1(g.ss, s);
@@ -198,7 +201,26 @@ __device__ __forceinline__ SumNz sweep_grow(double2 *A_, u32 size, const Gate &g
       A[j] = prune_acc(cmul(g.a, v), r.sum, r.nz);
       A[size + j] = prune_acc(neg_if(cmul(g.bx0, v), s), r.sum, r.nz);
     }
+  };
+  if (kG > 1) {
+    // block form (chi in L2): the loads of kGUnroll iterations first -- they
+    // never alias the stores (A[size + j]) or another iteration's A[j] --
+    // then the same per-thread order of updates (and of the norm sum)
+    constexpr u32 NT = 32u * kG;
+#pragma unroll 1
+    for (u32 j0 = lane; j0 < size; j0 += NT * kGUnroll) {
+      double2 v[kGUnroll];
+#pragma unroll
+      for (int u = 0; u < kGUnroll; ++u)
+        if (j0 + u * NT < size) v[u] = A[j0 + u * NT];
+#pragma unroll
+      for (int u = 0; u < kGUnroll; ++u)
+        if (j0 + u * NT < size) one(j0 + u * NT, v[u]);
+    }
+    return r;
   }
+#pragma unroll 1
+  for (u32 j = lane; j < size; j += 32u * kG) one(j, A[j]);
   return r;
 }
 
@@ -229,7 +251,7 @@ __device__ __forceinline__ double2 sweep_det_sums_impl(double2 *A_, u32 size, u3
   const u32 lane = glane<kG>();
   gbar_in<kG>();
   double sp = 0.0, sm = 0.0;
-#pragma unroll 1
+#pragma unroll (kG > 1 ? kGUnroll : 1)
   for (u32 j = lane; j < size; j += 32u * kG) {
     const double a2 = abs2(ldp<kPS>(A, j, ps));
     if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
@@ -305,6 +327,27 @@ __device__ __forceinline__ SumNz sweep_compact_impl(double2 *A_, u32 half, u32 i
   }
   return r;
 }
+// out of place (ping-pong buffers, global chi): D[jp] = rs * A[src(jp)] in
+// one pass, no per-round barriers
+template <int kG>
+__device__ __forceinline__ SumNz sweep_compact_to(const double2 *__restrict__ A, double2 *__restrict__ D,
+                                               u32 half, u32 isq, u32 mask, u32 tau, double rs,
+                                               double ps) {
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+#pragma unroll (kG > 1 ? kGUnroll : 1)
+  for (u32 jp = lane; jp < half; jp += 32u * kG) {
+    const u32 j0 = ins_bit(jp, isq, 0);
+    const double2 w = cscale(ldps(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps), rs);
+    D[jp] = w;
+    r.sum = __dadd_rn(r.sum, abs2(w));
+    r.nz += nonzero(w);
+  }
+  return r;
+}
 template <bool kS, int kG = 1>
 __device__ __forceinline__ SumNz sweep_compact(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
                                             double rs, double ps) {
@@ -350,7 +393,7 @@ __device__ __forceinline__ double sweep_pivot_p(double2 *A_, PivotGeo g, double2
   const u32 lane = glane<kG>();
   gbar_in<kG>();
   double sp = 0.0;
-#pragma unroll 1
+#pragma unroll (kG > 1 ? kGUnroll : 1)
   for (u32 m = lane; m < g.npairs; m += 32u * kG) {
     double2 vr, pr;
     u32 d_;
@@ -374,6 +417,27 @@ __device__ __forceinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 
     u32 dst;
     pivot_terms(A, g, xpp, m, vr, pr, dst, ps);
     A[dst] = prune_acc(plus ? cadd(vr, pr) : csub(vr, pr), r.sum, r.nz);
+  }
+  return r;
+}
+
+// span pivot with the compaction fused in (ping-pong buffers): pair m's
+// merged value goes to slot m of D -- the compaction of the rep slots
+// (sweep_compact with mask = tmask, tau = ct reads rep(m) for slot m)
+template <int kG>
+__device__ __forceinline__ SumNz sweep_pivot_wc(const double2 *__restrict__ A, double2 *__restrict__ D,
+                                             PivotGeo g, double2 xpp, bool plus, double ps) {
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+#pragma unroll (kG > 1 ? kGUnroll : 1)
+  for (u32 m = lane; m < g.npairs; m += 32u * kG) {
+    double2 vr, pr;
+    u32 dst;
+    pivot_terms(A, g, xpp, m, vr, pr, dst, ps);
+    D[m] = prune_acc(plus ? cadd(vr, pr) : csub(vr, pr), r.sum, r.nz);
   }
   return r;
 }

@@ -43,6 +43,30 @@ class CorruptStateError(RuntimeError):
     """A shot hit a ~zero-weight measurement branch (ref state.py:40-41)."""
 
 
+class UnsupportedCircuitError(RuntimeError):
+    """A shot reached an op whose static chi dimension exceeds the program's
+    dimension limit (``SamplerConfig.dim_limit``) while its support still
+    fit the entry capacity.  The static frame keeps every T
+    coordinate of the shot-invariant span until a measurement removes it, so
+    a circuit whose T gates cancel back to a small support (e.g. many
+    ``H q; T q; T_DAG q; H q`` blocks on distinct qubits) needs a dense chi
+    over the whole span where the reference's sparse map holds one entry
+    (ref state.py:294-306).  Raising ``SamplerConfig(max_dim=...)`` runs it
+    (block form, chi in global memory, up to 2^24 entries per shot); the
+    error is never silent."""
+
+    def __init__(self, shots: int, instruction: int | None, limit: int | None):
+        self.shots = shots
+        self.instruction = instruction
+        self.limit = limit
+        at = "" if instruction is None else " at flat instruction %d" % instruction
+        lim = "" if limit is None else " %d" % limit
+        super().__init__(
+            "%d shot(s) reached a chi dimension above the limit%s%s while within the entry "
+            "capacity (the static frame keeps cancelled T coordinates until a measurement "
+            "drops them; raise SamplerConfig(max_dim=...))" % (shots, lim, at))
+
+
 class CapacityError(RuntimeError):
     """Raised by ``run_shot`` callers expecting the reference exception type;
     batch APIs report overflow as a per-shot status instead."""
@@ -212,16 +236,16 @@ def _program_for(prog, max_dim: int) -> Program:
 
 
 def counters_to_stats(c: np.ndarray, obs_keys, wall: float,
-                      device_s: float = 0.0) -> RunStats:
+                      device_s: float = 0.0, dp=None) -> RunStats:
     """Host counter vector -> RunStats; corrupt shots raise like the
     reference (ref state.py:170-171 propagates out of run_batch)."""
     if c[_lib.GS_C_CORRUPT]:
         raise CorruptStateError("%d shot(s) selected a ~zero-weight measurement "
                                 "branch" % int(c[_lib.GS_C_CORRUPT]))
     if c[_lib.GS_C_UNSUPPORTED]:
-        raise RuntimeError("%d shot(s) exceeded the engine's chi dimension "
-                           "limit (raise SamplerConfig.max_dim)"
-                           % int(c[_lib.GS_C_UNSUPPORTED]))
+        raise UnsupportedCircuitError(int(c[_lib.GS_C_UNSUPPORTED]),
+                                      getattr(dp, "truncated_at", None),
+                                      getattr(dp, "max_dim", None))
     per = {}
     for i, k in enumerate(obs_keys):
         v = int(c[_lib.GS_C_PER_OBS + i])
@@ -271,7 +295,7 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
         dev_s += eng.last_kernel_ms * 1e-3
         done += cnt
     st = counters_to_stats(total, p.dp.obs_keys, time.perf_counter() - t0,
-                           dev_s)
+                           dev_s, dp=p.dp)
     st.witnesses = sorted(wit)
     return st
 
@@ -328,7 +352,8 @@ def sample(prog, cfg: SamplerConfig, *, shot_begin: int = 0, seeds=None,
     if np.any(status == 4):
         raise CorruptStateError("a shot selected a ~zero-weight branch")
     if np.any(status == 5):
-        raise RuntimeError("a shot exceeded the engine's chi dimension limit")
+        raise UnsupportedCircuitError(int(np.sum(status == 5)), int(aux[status == 5][0]),
+                                      p.dp.max_dim)
     return ShotBatch(status, aux, rec, obs, list(p.dp.obs_keys),
                      p.dp.num_measurements)
 

@@ -20,9 +20,23 @@ ap.add_argument("n", type=int)
 ap.add_argument("t", type=int)
 ap.add_argument("--shots", type=int, default=20000)
 ap.add_argument("--warm", type=int, default=2048)
+ap.add_argument("--flags", default="", help="extra run flags, e.g. CHI_BLOCK,CHI_GLOBAL")
 args = ap.parse_args()
+from paper_2512_23037_b200 import _lib  # noqa: E402
+EXTRA = 0
+for f in filter(None, args.flags.split(",")):
+    EXTRA |= getattr(_lib, "GS_" + f)
+
+
+class Cfg(SamplerConfig):
+    def run_flags(self) -> int:
+        return super().run_flags() | EXTRA
+
+
+SamplerConfig = Cfg  # noqa: F811
 prog = apply_noise_model(config4_circuit(args.n, args.t, seed=args.n + args.t), 1e-3)
-run_batch(prog, SamplerConfig(shots=args.warm, master_seed=1, rng="philox"))
+if args.warm:
+    run_batch(prog, SamplerConfig(shots=args.warm, master_seed=1, rng="philox"))
 cfg = SamplerConfig(shots=args.shots, master_seed=args.n * 1000 + args.t, rng="philox",
                     postselect=True)
 st = run_batch(prog, cfg)
@@ -30,4 +44,4 @@ p = _program_for(prog, cfg.dim_limit)
 print(json.dumps({"n": args.n, "t": args.t, "shots": st.total_shots,
                   "device_shots_per_s": st.device_dict()["device_shots_per_s"],
                   "overflow": st.overflow_count, "max_dim": p.dp.max_dim,
-                  "sections": p.sections()}))
+                  "sections": p.sections(), "flags": args.flags}))

@@ -111,3 +111,22 @@ def test_random_programs_compile_both_forms():
             seen.add((fl & 3, bool(fl & TF_RED)))
     # both forms occur (the non-reduced one when xi_s is odd)
     assert (T_BUTTERFLY, True) in seen and (T_BUTTERFLY, False) in seen
+
+
+def test_static_span_keeps_cancelled_t_coordinates():
+    """ADVICE r01 (medium), pinned: H q; T q; T_DAG q; H q on 24 distinct
+    qubits has a one-entry support per noiseless shot in the reference, but
+    the shot-invariant span grows by one coordinate per qubit until the
+    final measurements.  Past the dimension limit the compile truncates at
+    the first T that would exceed it (shots reaching it end UNSUPPORTED or
+    OVERFLOW, never silently wrong); at the span's size it compiles whole."""
+    from paper_2512_23037_b200 import compile_program, parse_circuit
+    text = "".join("H %d\nT %d\nT_DAG %d\nH %d\n" % (q, q, q, q) for q in range(24))
+    text += "M " + " ".join(map(str, range(24))) + "\n"
+    prog = parse_circuit(text)
+    cut = compile_program(prog, max_dim=20)
+    assert cut.max_dim == 20
+    flat = list(prog.flat())
+    assert flat[cut.truncated_at].name == "T" and flat[cut.truncated_at].targets[0] == 20
+    whole = compile_program(prog, max_dim=24)
+    assert whole.truncated_at is None and whole.max_dim == 24

@@ -102,3 +102,28 @@ def test_cli_sample_json_schema(tmp_path):
     d = json.loads(out.read_text())
     assert d["total_shots"] == 1000
     assert set(d) >= {"preserved_shots", "discard_rate", "bayes_lo", "throughput"}
+
+
+def _cancelled_t(nq: int, noise: bool) -> str:
+    """T gates that cancel back to a one-entry support.
+    The static span keeps every T coordinate until the final measurements
+    (DESIGN.md §8), so the dense chi needs nq dimensions."""
+    body = "".join("H %d\nT %d\n%sT_DAG %d\nH %d\n"
+                   % (q, q, "DEPOLARIZE1(0.02) %d\n" % q if noise else "", q, q)
+                   for q in range(nq))
+    return body + "M " + " ".join(map(str, range(nq))) + "\nDETECTOR rec[-1]\n"
+
+
+def test_cancelled_t_span_beyond_dim_limit_is_loud_then_runs():
+    from paper_2512_23037_b200 import UnsupportedCircuitError
+    prog = parse_circuit(_cancelled_t(22, True))
+    cfg = SamplerConfig(shots=8, master_seed=5)
+    assert cfg.dim_limit == 20
+    with pytest.raises(UnsupportedCircuitError) as ei:
+        run_batch(prog, cfg)
+    assert ei.value.limit == 20 and ei.value.instruction is not None
+    # with the limit raised to the span the records equal the reference
+    # restatement's (sparse map, one or two entries per shot)
+    _check(prog, 5, 8, dict(max_dim=22, postselect=True), 32768)
+    st = run_batch(prog, SamplerConfig(shots=8, master_seed=5, max_dim=22))
+    assert st.total_shots == 8 and st.overflow_count == 0
