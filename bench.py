@@ -367,6 +367,8 @@ def main():
     ap.add_argument("--chi-smem", action="store_true")
     ap.add_argument("--wpb", type=int, default=0)
     ap.add_argument("--wide-only", action="store_true")
+    ap.add_argument("--narrow-k", default="auto", choices=["auto", "4", "5"],
+                    help="narrow (lane-per-shot) chi limit; auto = timed per program")
     ap.add_argument("--fixed-batch", action="store_true",
                     help="keep --shots-per-step even when a step is shorter than 0.2 s")
     ap.add_argument("--print-sections", action="store_true",
@@ -457,7 +459,8 @@ def main():
     dp = compile_program(prog)
     P = Program(dp)
     if args.print_sections:
-        print(P.sections(_lib.GS_WIDE_ONLY if args.wide_only else 0))
+        print(P.sections((_lib.GS_WIDE_ONLY if args.wide_only else 0) |
+                         (_lib.GS_NARROW_K5 if args.narrow_k == "5" else 0)))
         return 0
     eng = Engine(dev)
     flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if args.rng == "philox" else 0)
@@ -467,6 +470,20 @@ def main():
         flags |= _lib.GS_CHI_SMEM
     if args.wide_only:
         flags |= _lib.GS_WIDE_ONLY
+    # narrow chi limit 4 or 5: timed on a probe per program (Program.narrow_flag;
+    # results identical either way), rank 0's choice on every rank
+    if args.narrow_k == "auto":
+        nf = P.narrow_flag(eng, flags, 32768)
+        if world > 1:
+            t = torch.tensor([nf], dtype=torch.int64, device="cuda")
+            dist.broadcast(t, 0)
+            nf = int(t.item())
+    else:
+        nf = _lib.GS_NARROW_K5 if args.narrow_k == "5" else 0
+    flags |= nf
+    config["narrow_kn"] = 5 if nf else 4
+    if getattr(P, "narrow_tuning", None):
+        config["narrow_tuning"] = P.narrow_tuning
     S = args.shots_per_step
     nc = P.num_counters
     stream = torch.cuda.current_stream()

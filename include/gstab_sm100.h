@@ -56,6 +56,9 @@ extern "C" {
                               the launch stream) and model bytes / shots
                               (a small reduction launch after each
                               section); read with gs_engine_section_stats */
+#define GS_NARROW_K5 256u  /* lane-per-shot sections up to chi dimension 5
+                              (default 4): a pure performance choice, the
+                              results are identical either way */
 
 /* per-shot status codes (gs_run_records) */
 #define GS_ST_PRESERVED 1

@@ -10,8 +10,9 @@ and sample shots on the GPU with post-selection and logical-error counters.
     stats = run_batch(prog, SamplerConfig(shots=10**7, postselect=True))
 
 The sampling path is ``compiler.compile_program`` (host, once per circuit)
--> ``libgstab_sm100a.so`` (CUDA, one warp per shot).  There is no CPU
-fallback.
+-> ``libgstab_sm100a.so`` (CUDA sections: lane-per-shot for chi dimension
+<= 4 or 5, warp-per-shot above, a block of warps per shot for chi >= 2^14).
+There is no CPU fallback.
 """
 
 from .circuit import (Block, CircuitProgram, Instruction, ParseError,

@@ -28,6 +28,7 @@ struct DevProg {
   u64 geo_off, acc_off;   // Philox fire schedule: gap table, thinning table
   u32 geo_len, noise_uniform;
   float geo_ilq;          // 1 / log(1 - p_max), the gap search's first guess
+  u32 kn;                 // narrow chi dimension limit (narrow_kn)
 };
 
 struct DevRun {
@@ -326,10 +327,12 @@ struct Rng {
 // of the static basis (zero = absent reference entry, so partner lookups
 // are O(1)); positions >= 2^k are don't-care until a GROW initialises them.
 
-#ifndef GS_KN
-#define GS_KN 4u                // narrow (lane-per-shot) chi dimension limit
-#endif
-constexpr u32 kNarrowBytes = (1u << GS_KN) * 32u * 16u;   // An[2^KN][32] double2
+// narrow (lane-per-shot) chi dimension limit kn, a run-time choice: 4, or
+// 5 with GS_NARROW_K5 (A/B r02j: the Table-2 d=5 headline +10.3 % at 5, the
+// d=3 workload -23 % and the grown proxy -8.5 %; sampler.Program tunes it
+// per program by timing both on a probe run -- results are identical)
+__host__ __device__ __forceinline__ u32 narrow_kn(u32 flags) { return (flags & GS_NARROW_K5) ? 5u : 4u; }
+__host__ __device__ __forceinline__ u32 narrow_bytes(u32 kn) { return (1u << kn) * 32u * 16u; }   // An[2^kn][32] double2
 constexpr u32 kCntBytes = 64;                              // per-warp counters
 
 __device__ __forceinline__ bool nonzero(double2 v) { return v.x != 0.0 || v.y != 0.0; }

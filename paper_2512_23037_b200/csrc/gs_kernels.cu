@@ -9,7 +9,7 @@
 //   this file       host side: program upload, section plan, launch loop, C ABI
 //
 // The op stream is cut on the host into sections (see sections_of): narrow
-// sections (every op has k <= GS_KN) run one lane per shot in narrow_kernel,
+// sections (every op has k <= kn) run one lane per shot in narrow_kernel,
 // wide sections one warp per shot in wide_kernel; surviving shots pass from
 // section to section through global slot queues.  The per-shot state is the
 // static-frame state of compiler.py:
@@ -246,7 +246,7 @@ struct Section {
                             // 50.6M at 150, 50.3M at 40)
 #endif
 
-static void sections_of(const gs_program *p, bool wide_only, std::vector<Section> &out) {
+static void sections_of(const gs_program *p, bool wide_only, u32 kn, std::vector<Section> &out) {
   out.clear();
   const std::vector<u64> &ops = p->ops;
   size_t pc = 0, nm = 0;
@@ -256,7 +256,7 @@ static void sections_of(const gs_program *p, bool wide_only, std::vector<Section
     const u64 h = ops[pc];
     const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
     const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
-    const bool wide = wide_only || gs::op_is_wide(kind, k, fl);
+    const bool wide = wide_only || gs::op_is_wide(kind, k, fl, kn);
     const bool split = !wide && (GS_NARROW_SPLIT > 0) && nops >= (u32)GS_NARROW_SPLIT;
     if (out.empty() || out.back().wide != wide || split) {
       while (nm < nn && (u32)p->tables[p->info.noise_off + 4 * nm] < (u32)pc) ++nm;
@@ -276,7 +276,7 @@ static void sections_of(const gs_program *p, bool wide_only, std::vector<Section
 int gs_program_sections(const gs_program *p, uint32_t flags) {
   if (!p) return fail(GS_ERR_ARG, "null argument");
   std::vector<Section> secs;
-  sections_of(p, (flags & GS_WIDE_ONLY) != 0, secs);
+  sections_of(p, (flags & GS_WIDE_ONLY) != 0, gs::narrow_kn(flags), secs);
   return (int)secs.size();
 }
 
@@ -395,6 +395,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   P.geo_len = p->info.geo_len;
   P.acc_off = p->info.acc_off;
   P.noise_uniform = p->info.noise_uniform;
+  P.kn = gs::narrow_kn(r->flags);
   P.geo_ilq = 0.f;
   if (p->info.geo_len >= 2) {
     const double q = (double)p->tables[p->info.geo_off + 1] * 0x1.0p-53;
@@ -409,7 +410,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   R.seeds = nullptr;
 
   std::vector<Section> secs;
-  sections_of(p, wide_only, secs);
+  sections_of(p, wide_only, P.kn, secs);
   bool any_narrow = false, any_wide = false;
   for (const Section &s : secs) (s.wide ? any_wide : any_narrow) = true;
 
@@ -434,7 +435,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   KN.rec_in_smem = nrec_b <= 4096;
   KW.rec_in_smem = wrec_b <= 4096;
   if (any_narrow) {
-    const u32 wb = (u32)((gs::kCntBytes + gs::kNarrowBytes + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
+    const u32 wb = (u32)((gs::kCntBytes + gs::narrow_bytes(P.kn) + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
     rc = occupancy(e, wb, r->warps_per_block, 4,
                    [&](auto f) { return with_narrow_kernel(philox, f); }, KN);
     if (rc) return rc;
@@ -469,14 +470,14 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     if (per < 1) return fail(GS_ERR_UNSUPPORTED, "block-per-shot state exceeds the SM");
     KW.blocks = (u32)(e->num_sms * per);
     if (!smem_chi) {
-      const u64 max_blocks = ((u64)8 << 30) / (2 * chi);   // two buffers per block
+      const u64 max_blocks = ((u64)8 << 30) / (3 * chi);   // two 1.5-chi buffers per block
       if ((u64)KW.blocks > max_blocks) KW.blocks = (u32)std::max<u64>(1, max_blocks);
     }
   }
   if (r->blocks) { KN.blocks = r->blocks; KW.blocks = r->blocks; }
   const u64 nwarps = std::max((u64)KN.blocks * KN.wpb, (u64)KW.blocks * KW.wpb);
   if (!smem_chi && any_wide) {
-    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 2 : KW.wpb) * chi);
+    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 3 : KW.wpb) * chi);
     if (rc) return rc;
   }
   if (!KN.rec_in_smem || !KW.rec_in_smem) {
@@ -484,7 +485,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     if (rc) return rc;
   }
   // queues between sections: fixed slots, chunks of at most `chunk` shots
-  const u64 slot_b = 8ull * (gs::Q_HDR + gs::rec_u64(P.rec_words32) + 2 * (1u << GS_KN));
+  const u64 slot_b = 8ull * (gs::Q_HDR + gs::rec_u64(P.rec_words32) + 2 * (1u << P.kn));
   u64 chunk = r->shot_count ? r->shot_count : 1;
 #ifndef GS_QUEUE_GB
 #define GS_QUEUE_GB 8   // per section queue: one chunk for a 2^24-shot step (A/B +0.4 % over 2 GB)

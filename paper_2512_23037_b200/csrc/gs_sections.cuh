@@ -6,8 +6,8 @@
 //
 // Execution model: breadth-first SECTIONS.  k is static per op
 // (shot-invariant basis, compiler.py), so the op stream splits on the host
-// into alternating sections of narrow ops (chi dimension k <= GS_KN before
-// and after the op) and wide ops (k > GS_KN, GROW_LIMIT).  One launch per
+// into alternating sections of narrow ops (chi dimension k <= kn before
+// and after the op) and wide ops (k > kn, GROW_LIMIT).  One launch per
 // section runs every live shot of the chunk through it:
 //
 //  * narrow_kernel: a warp takes 32 shots (one per lane) and walks the
@@ -19,7 +19,7 @@
 //    the lanes (chi in the warp's shared-memory buffer; `sweep_*`).
 //
 // Shots that survive a section are appended to a global queue (fixed-size
-// slots: state words, record bits, chi of dimension <= GS_KN) read by the
+// slots: state words, record bits, chi of dimension <= kn) read by the
 // next section's launch.  Each launch keeps only its own code hot, which is
 // what the instruction cache needs (B200: 32 KB L1.5).
 // GS_WIDE_ONLY runs the whole program as one wide section (A/B, tests).
@@ -46,9 +46,9 @@
 #define GS_BLOCK_MIN_DIM 14   // chi dimension from which the block form is the default
 #endif
 
-__host__ __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl) {
-  return kind == OP_GROW_LIMIT || k > GS_KN ||
-         (kind == OP_T && (fl & 3u) == T_GROW && k + 1 > GS_KN);
+__host__ __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl, u32 kn) {
+  return kind == OP_GROW_LIMIT || k > kn ||
+         (kind == OP_T && (fl & 3u) == T_GROW && k + 1 > kn);
 }
 
 // action of a fired error E = X^ex Z^ez on the static frame:
@@ -124,7 +124,7 @@ __device__ __forceinline__ const u64 *noise_owner(const DevProg &P, u32 l) {
 }
 
 // queue slot layout (u64 words): state, then record bits (u32 words), then
-// the chi rows [0, 2^GS_KN)
+// the chi rows [0, 2^kn)
 enum { Q_SL = 0, Q_LO, Q_HI, Q_C, Q_OBS, Q_MB, Q_PICK, Q_SEED, Q_CNTK, Q_GEO, Q_FIRE, Q_HDR = 12 };
 
 struct DevSec {
@@ -143,7 +143,7 @@ struct DevSec {
 __host__ __device__ __forceinline__ u32 rec_u64(u32 rec_words32) { return ((rec_words32 + 3) / 4) * 2; }
 
 __device__ __forceinline__ u32 slot_u64(const DevProg &P) {
-  return Q_HDR + rec_u64(P.rec_words32) + 2 * (1u << GS_KN);
+  return Q_HDR + rec_u64(P.rec_words32) + 2 * (1u << P.kn);
 }
 
 // per-warp counters in shared memory
@@ -181,7 +181,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
   double2 *An = reinterpret_cast<double2 *>(mine + kCntBytes);
   // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
-  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kNarrowBytes)
+  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + narrow_bytes(P.kn))
                             : O.grec + gw * (u64)P.rec_words32 * 32u;
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
@@ -702,14 +702,20 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   GroupScratch grp;
   grp.slots = reinterpret_cast<u64 *>(smem + (size_t)wpb * O.warp_bytes);
   grp.tog = 0;
-  // block form on global memory: two chi buffers per block (ping-pong), so
-  // the compacting passes write the other buffer in one pass without
-  // per-round barriers (kPP)
+  // block form on global memory (kPP): two chi buffers per block of 1.5 x
+  // 2^max_dim entries each (ping-pong).  The compacting passes write the
+  // other buffer in one pass without per-round barriers; a span pivot writes
+  // both outcomes' compacted halves there (w+ at [0, half), w- at [half,
+  // 2 half)) while it sums P+, and chi continues at the chosen half -- so a
+  // later growth to 2^max_dim from an offset of half still fits
   constexpr bool kPP = kG > 1 && !kSmemChi;
+  const u64 pp_stride = ((u64)3 << P.max_dim) >> 1;
   double2 *A = kSmemChi ? chi_ptr<true>(reinterpret_cast<double2 *>(
                               kG == 1 ? mine + O.chi_off : smem + O.chi_off))
-                        : O.gchi + (kG == 1 ? gw : 2ull * blockIdx.x) * ((u64)1 << P.max_dim);
-  double2 *Bf = kPP ? A + ((u64)1 << P.max_dim) : nullptr;
+                        : O.gchi + (kG == 1 ? gw * ((u64)1 << P.max_dim) : 2ull * blockIdx.x * pp_stride);
+  double2 *const b0 = A;
+  double2 *const b1 = kPP ? A + pp_stride : nullptr;
+  u32 cur = 0;   // kPP: the buffer A lies in
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
   const u64 *__restrict__ tables = P.tables;
@@ -1090,8 +1096,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             const u32 tau = want_neg ^ neg0;
             SumNz r;
             if (kPP) {
-              r = sweep_compact_to<kG>(A, Bf, size >> 1, isq, dmask, tau, rs, ps);
-              double2 *t_ = A; A = Bf; Bf = t_;
+              double2 *D = cur ? b0 : b1;
+              r = sweep_compact_to<kG>(A, D, size >> 1, isq, dmask, tau, rs, ps);
+              A = D;
+              cur ^= 1u;
             } else {
               r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, rs, ps);
             }
@@ -1122,41 +1130,62 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
           g.dc = dc; g.dmask = dmask;
           const double2 xpp = ipow(xi0);   // i^xi0, exact
-          // no span: every entry is either its pair's rep (w = v) or its
-          // part (w = +-i^xi0 v, an exact rotation), so sum |w+|^2 is the
-          // chi norm the writer passes track -- no read pass
-          const double pp = __dmul_rn(0.5, g.span ? group_sum<kG>(sweep_pivot_p<kSmemChi, kG>(A, g, xpp, ps), grp)
-                                                  : (nrm_lane0 ? nrm_u : group_sum<kG>(nrm_l, grp)));
-          plus = pick_plus(pp);
-          const double chosen = plus ? pp : __dsub_rn(1.0, pp);
-          if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
-          // ping-pong (block form on global memory): a span pivot writes
-          // the merged pairs straight to their compacted slots in the other
-          // buffer (the compaction's source slot is the pair's rep slot) and
-          // the renormalisation is deferred (ldps) -- two passes, not three
-          const bool fused = kPP && g.span;
-          const SumNz w = fused ? sweep_pivot_wc<kG>(A, Bf, g, xpp, plus, ps)
-                                : sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
-          ps = 1.0;
-          gsync<kG>();
-          const double sk = group_sum<kG>(w.sum, grp);
-          cnt = group_sum_u32<kG>(w.nz, grp);
-          if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
-          const double rs = inv_sqrt_norm(sk);
-          if (fused) {
-            double2 *t_ = A; A = Bf; Bf = t_;
-            kcur = wk - 1;
-            defer_scale(rs, sk);
-          } else if (g.span) {
-            const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+          if (kPP && g.span) {
+            // one pass: P+ and both outcomes' merged, pruned, compacted
+            // pairs (sweep_pivot_both), then chi continues at the chosen
+            // half with the renormalisation deferred
+            double2 *D = cur ? b0 : b1;
+            const u32 half = size >> 1;
+            const PivotBoth pb = sweep_pivot_both<kG>(A, D, g, xpp, ps);
             gsync<kG>();
-            cnt = group_sum_u32<kG>(r.nz, grp);
-            nrm_l = r.sum;
-            nrm_lane0 = false;
+            const double pp = __dmul_rn(0.5, group_sum<kG>(pb.pp, grp));
+            plus = pick_plus(pp);
+            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            const double sk = group_sum<kG>(plus ? pb.sump : pb.summ, grp);
+            cnt = group_sum_u32<kG>(plus ? pb.nzp : pb.nzm, grp);
+            if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            ps = 1.0;
+            A = D + (plus ? 0u : half);
+            cur ^= 1u;
             kcur = wk - 1;
+            defer_scale(inv_sqrt_norm(sk), sk);
           } else {
-            defer_scale(rs, sk);
+            // no span: every entry is either its pair's rep (w = v) or its
+            // part (w = +-i^xi0 v, an exact rotation), so sum |w+|^2 is the
+            // chi norm the writer passes track -- no read pass
+            const double nrm0 = g.span ? 0.0 : (nrm_lane0 ? nrm_u : group_sum<kG>(nrm_l, grp));
+            const double pp = __dmul_rn(0.5, g.span ? group_sum<kG>(sweep_pivot_p<kSmemChi, kG>(A, g, xpp, ps), grp)
+                                                    : nrm0);
+            plus = pick_plus(pp);
+            const double chosen = plus ? pp : __dsub_rn(1.0, pp);
+            if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            if (!g.span && ps == 1.0) {
+              // rotate the part entries only; norm and count carry over
+              sweep_pivot_part<kSmemChi, kG>(A, g, xpp, plus, size);
+              gsync<kG>();
+              defer_scale(inv_sqrt_norm(nrm0), nrm0);
+              goto pivot_signs;
+            }
+            const SumNz w = sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
+            ps = 1.0;
+            gsync<kG>();
+            const double sk = group_sum<kG>(w.sum, grp);
+            cnt = group_sum_u32<kG>(w.nz, grp);
+            if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+            const double rs = inv_sqrt_norm(sk);
+            if (g.span) {
+              const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+              gsync<kG>();
+              cnt = group_sum_u32<kG>(r.nz, grp);
+              nrm_l = r.sum;
+              nrm_lane0 = false;
+              kcur = wk - 1;
+            } else {
+              defer_scale(rs, sk);
+            }
           }
+        pivot_signs:
           if (g.ct) c ^= vec;
           // tableau sign update of the pivot (ref tableau.py:176-200)
           const u32 v = (u32)(sig_hi >> t) & 1u;

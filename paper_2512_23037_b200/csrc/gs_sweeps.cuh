@@ -421,25 +421,63 @@ __device__ __forceinline__ SumNz sweep_pivot_w(double2 *A_, PivotGeo g, double2 
   return r;
 }
 
-// span pivot with the compaction fused in (ping-pong buffers): pair m's
-// merged value goes to slot m of D -- the compaction of the rep slots
-// (sweep_compact with mask = tmask, tau = ct reads rep(m) for slot m)
+// span pivot in one pass (ping-pong buffers): sums P+ = sum |w+|^2 in the
+// order sweep_pivot_p does, and writes both outcomes' merged, pruned pairs
+// to their compacted slots of D -- w+ at m, w- at half + m (the compaction
+// of the rep slots, sweep_compact with mask = tmask, tau = ct, reads rep(m)
+// for slot m) -- with each outcome's kept sum and count
+struct PivotBoth {
+  double pp, sump, summ;
+  u32 nzp, nzm;
+};
 template <int kG>
-__device__ __forceinline__ SumNz sweep_pivot_wc(const double2 *__restrict__ A, double2 *__restrict__ D,
-                                             PivotGeo g, double2 xpp, bool plus, double ps) {
+__device__ __forceinline__ PivotBoth sweep_pivot_both(const double2 *__restrict__ A, double2 *__restrict__ D,
+                                                   PivotGeo g, double2 xpp, double ps) {
   const u32 lane = glane<kG>();
   gbar_in<kG>();
-  SumNz r;
-  r.sum = 0.0;
-  r.nz = 0;
+  PivotBoth r;
+  r.pp = 0.0; r.sump = 0.0; r.summ = 0.0;
+  r.nzp = 0; r.nzm = 0;
+  double2 *__restrict__ Dm = D + g.npairs;
 #pragma unroll (kG > 1 ? kGUnroll : 1)
   for (u32 m = lane; m < g.npairs; m += 32u * kG) {
     double2 vr, pr;
     u32 dst;
     pivot_terms(A, g, xpp, m, vr, pr, dst, ps);
-    D[m] = prune_acc(plus ? cadd(vr, pr) : csub(vr, pr), r.sum, r.nz);
+    const double2 wp = cadd(vr, pr);
+    r.pp = __dadd_rn(r.pp, abs2(wp));
+    D[m] = prune_acc(wp, r.sump, r.nzp);
+    Dm[m] = prune_acc(csub(vr, pr), r.summ, r.nzm);
   }
   return r;
+}
+
+// no-span pivot without a pending scale: rep entries keep v (w = v +- (-0)
+// == v), so only the part entries -- those with ct ^ par(m & tmask) = 1, an
+// affine half enumerated by inserting the parity bit at the top bit h of
+// tmask -- are rewritten, as +-(+-i^xi0) v (exact rotations: no entry's
+// modulus changes, the norm and nonzero count carry over)
+template <bool kS, int kG = 1>
+__device__ __forceinline__ void sweep_pivot_part(double2 *A_, const PivotGeo &g, double2 xpp, bool plus,
+                                                 u32 size) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
+  const double2 xp = plus ? xpp : cneg(xpp), xm = cneg(xp);
+  if (g.tmask == 0) {
+    if (!g.ct) return;
+#pragma unroll 1
+    for (u32 m = lane; m < size; m += 32u * kG)
+      A[m] = cmul((g.dc ^ par32(m & g.dmask)) ? xm : xp, A[m]);
+    return;
+  }
+  const u32 h = 31 - __clz(g.tmask);
+#pragma unroll 1
+  for (u32 i = lane; i < (size >> 1); i += 32u * kG) {
+    const u32 j0 = ins_bit(i, h, 0);
+    const u32 m = j0 | ((g.ct ^ 1u ^ par32(j0 & g.tmask)) << h);
+    A[m] = cmul((g.dc ^ par32(m & g.dmask)) ? xm : xp, A[m]);
+  }
 }
 
 // apply a pending renormalisation in place: A[j] = ps * A[j]

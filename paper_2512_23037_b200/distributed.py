@@ -18,7 +18,7 @@ import time
 import numpy as np
 
 from . import _lib
-from .sampler import SamplerConfig, counters_to_stats, _program_for
+from .sampler import SamplerConfig, counters_to_stats, _program_for, tuned_flags
 
 
 def shard_range(total: int, rank: int, world: int):
@@ -51,11 +51,12 @@ def _gpu_shard_counters(prog, cfg: SamplerConfig, begin: int, count: int):
         counters = torch.zeros(p.num_counters, dtype=torch.int64, device=dev)
         stream = torch.cuda.current_stream(dev)
         chunk = cfg.wave_shots
+        flags = cfg.run_flags() | tuned_flags(p, eng, cfg)
         done = 0
         while done < count:
             n = min(chunk, count - done)
             par = Engine.params(cfg.master_seed, begin + done, n,
-                                cfg.effective_capacity, cfg.run_flags())
+                                cfg.effective_capacity, flags)
             eng.run_counters_async(p, par, counters.data_ptr(), stream.cuda_stream)
             done += n
     return counters, p.dp.obs_keys

@@ -42,6 +42,40 @@ class Program:
                                          self._locs.size, ct.byref(h)))
         self.handle = h
 
+    # probe size of the narrow-limit tuning (narrow_flag)
+    TUNE_SHOTS = 1 << 20
+
+    def narrow_flag(self, engine: "Engine", flags: int, capacity: int) -> int:
+        """``GS_NARROW_K5`` or 0: the narrow (lane-per-shot) chi dimension
+        limit that ran this program faster on a probe of ``TUNE_SHOTS``
+        shots (each setting warmed up, then timed on the device), cached per
+        device and run flags.  Only the section split changes -- records
+        and counters are identical either way (tests/test_gpu_parity.py) --
+        so the choice is a pure performance decision: 5 moves the k = 5 ops
+        of the MSC d=5 window into lane-per-shot sections (+10 % there) but
+        costs narrow occupancy elsewhere (d=3: 4 is 30 % faster)."""
+        if flags & _lib.GS_WIDE_ONLY:
+            return 0
+        cache = self.__dict__.setdefault("_narrow", {})
+        key = (engine.device, flags & (_lib.GS_RNG_PHILOX | _lib.GS_POSTSELECT |
+                                       _lib.GS_CHI_GLOBAL | _lib.GS_CHI_SMEM | _lib.GS_CHI_BLOCK))
+        if key in cache:
+            return cache[key]
+        if self.dp.max_dim < 5:
+            cache[key] = 0          # every op is narrow at either limit
+            return 0
+        times = {}
+        for extra in (0, _lib.GS_NARROW_K5):
+            par = Engine.params(0x7E57, 1 << 40, self.TUNE_SHOTS, capacity, flags | extra)
+            engine.run_counters(self, par)            # warm-up (queues, occupancy)
+            engine.run_counters(self, par)
+            times[extra] = engine.last_kernel_ms
+        best = min(times, key=times.get)
+        cache[key] = best
+        self.narrow_tuning = {"k4_ms": times[0], "k5_ms": times[_lib.GS_NARROW_K5],
+                              "probe_shots": self.TUNE_SHOTS}
+        return best
+
     def sections(self, flags: int = 0) -> int:
         """Narrow/wide sections (= sampling launches per chunk of shots)."""
         n = _lib.load().gs_program_sections(self.handle, flags)

@@ -235,6 +235,20 @@ def _program_for(prog, max_dim: int) -> Program:
     return p
 
 
+# runs at least this long (shots) tune the narrow limit first (the probe
+# costs 4 x Program.TUNE_SHOTS shots, once per program)
+TUNE_MIN_SHOTS = 1 << 23
+
+
+def tuned_flags(p: Program, eng: Engine, cfg: SamplerConfig) -> int:
+    """Performance-only run flags measured for this program (the narrow chi
+    limit, ``Program.narrow_flag``); 0 for short runs."""
+    if cfg.shots < TUNE_MIN_SHOTS:
+        return p.__dict__.get("_narrow", {}).get(
+            (eng.device, cfg.run_flags() & (_lib.GS_RNG_PHILOX | _lib.GS_POSTSELECT)), 0)
+    return p.narrow_flag(eng, cfg.run_flags(), cfg.effective_capacity)
+
+
 def counters_to_stats(c: np.ndarray, obs_keys, wall: float,
                       device_s: float = 0.0, dp=None) -> RunStats:
     """Host counter vector -> RunStats; corrupt shots raise like the
@@ -278,6 +292,7 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     t0 = time.perf_counter()
     p = _program_for(prog, cfg.dim_limit)
     eng = engine or get_engine(cfg.device)
+    flags = cfg.run_flags() | tuned_flags(p, eng, cfg)
     total = np.zeros(p.num_counters, dtype=np.int64)
     wit: list = []
     dev_s = 0.0
@@ -285,7 +300,7 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     while done < cfg.shots:
         cnt = min(cfg.wave_shots, cfg.shots - done)
         par = Engine.params(cfg.master_seed, shot_begin + done, cnt,
-                            cfg.effective_capacity, cfg.run_flags())
+                            cfg.effective_capacity, flags)
         if witnesses > len(wit):
             c, w, _ = eng.run_counters_witness(p, par, witnesses - len(wit))
             total += c
@@ -342,12 +357,13 @@ class ShotBatch:
 
 
 def sample(prog, cfg: SamplerConfig, *, shot_begin: int = 0, seeds=None,
-           engine: Engine | None = None) -> ShotBatch:
-    """Per-shot statuses, measurement records and observables."""
+           engine: Engine | None = None, extra_flags: int = 0) -> ShotBatch:
+    """Per-shot statuses, measurement records and observables.
+    ``extra_flags``: performance-only run flags (e.g. ``GS_NARROW_K5``)."""
     p = _program_for(prog, cfg.dim_limit)
     eng = engine or get_engine(cfg.device)
     par = Engine.params(cfg.master_seed, shot_begin, cfg.shots,
-                        cfg.effective_capacity, cfg.run_flags(), seeds=seeds)
+                        cfg.effective_capacity, cfg.run_flags() | extra_flags, seeds=seeds)
     status, aux, rec, obs = eng.run_records(p, par)
     if np.any(status == 4):
         raise CorruptStateError("a shot selected a ~zero-weight branch")

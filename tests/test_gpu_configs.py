@@ -15,7 +15,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 from oracle import gstab_oracle as orc
-from paper_2512_23037_b200 import SamplerConfig, parse_circuit, run_batch, sample
+from paper_2512_23037_b200 import SamplerConfig, _lib, parse_circuit, run_batch, sample
 from paper_2512_23037_b200.msc import config4_circuit, msc_circuit, injection_circuit
 from paper_2512_23037_b200.noise import apply_noise_model
 from paper_2512_23037_b200.sampler import _records_before
@@ -98,16 +98,18 @@ def test_d5_full_size_properties():
     assert int(c[_lib.GS_C_ERROR_SHOTS]) == a.logical_error_shots
 
 
+@pytest.mark.parametrize("narrow", [0, _lib.GS_NARROW_K5])
 @pytest.mark.parametrize("name", ["msc_d5_table2_records.npz", "msc_d3_table2_records.npz",
                                   "msc_d5_records.npz", "msc_d3_records.npz"])
-def test_msc_golden_records_bit_exact(name):
+def test_msc_golden_records_bit_exact(name, narrow):
     """Headline workloads: every one of the 20,000 reference-generated shots
-    (statuses, discarding detector, observable, record bits) bit-exact."""
+    (statuses, discarding detector, observable, record bits) bit-exact, at
+    either narrow chi limit (4, or 5 with GS_NARROW_K5)."""
     g = np.load(os.path.join(os.path.dirname(__file__), "golden", name))
     prog = parse_circuit(str(g["text"]))
     shots = len(g["status"])
     b = sample(prog, SamplerConfig(shots=shots, master_seed=int(g["master"]),
-                                   postselect=True))
+                                   postselect=True), extra_flags=narrow)
     assert np.array_equal(b.status, g["status"])
     m = int(g["num_measurements"])
     want = np.unpackbits(g["records"], axis=1, bitorder="little")[:, :m]

@@ -257,7 +257,7 @@ def test_msc_noiseless_is_deterministic(d):
 @pytest.mark.parametrize("mode", ["splitmix", "philox"])
 @pytest.mark.parametrize("variant", ["default", "wide_only", "chi_global",
                                      "chi_smem", "wide_only_chi_smem", "chi_block",
-                                     "chi_block_global", "wide_only_chi_block"])
+                                     "chi_block_global", "wide_only_chi_block", "narrow_k5"])
 def test_chi_storage_modes_match_oracle(variant, mode):
     """Lane-per-shot / warp-per-shot / block-per-shot execution and shared- /
     global-memory chi buffers must all give the oracle's results, in both
@@ -269,7 +269,8 @@ def test_chi_storage_modes_match_oracle(variant, mode):
                    "wide_only_chi_smem": _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM,
                    "chi_block": _lib.GS_CHI_BLOCK,
                    "chi_block_global": _lib.GS_CHI_BLOCK | _lib.GS_CHI_GLOBAL,
-                   "wide_only_chi_block": _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK}[variant]
+                   "wide_only_chi_block": _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK,
+                   "narrow_k5": _lib.GS_NARROW_K5}[variant]
     eng = get_engine(0)
     for it in range(25):
         n = rng.choice((4, 9, 20))

@@ -151,3 +151,28 @@ def test_run_batch_distributed_over_nccl_world_size_1(d5):
     assert (got.total_shots, got.preserved_shots, got.discarded_shots,
             got.logical_error_shots) == (want.total_shots, want.preserved_shots,
                                          want.discarded_shots, want.logical_error_shots)
+
+
+def test_narrow_limit_tuning_is_cached_and_result_neutral():
+    """Program.narrow_flag times both narrow chi limits on a probe and keeps
+    the faster; the counters of a run are identical under either limit."""
+    from paper_2512_23037_b200 import SamplerConfig, _lib, run_batch
+    from paper_2512_23037_b200.engine import Engine, get_engine
+    from paper_2512_23037_b200.msc import msc_d5_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    from paper_2512_23037_b200.sampler import _program_for
+    prog = apply_noise_model(msc_d5_circuit(), 1e-3)
+    cfg = SamplerConfig(shots=1 << 21, master_seed=4, postselect=True, rng="philox")
+    p = _program_for(prog, cfg.dim_limit)
+    eng = get_engine(0)
+    f = p.narrow_flag(eng, cfg.run_flags(), cfg.effective_capacity)
+    assert f in (0, _lib.GS_NARROW_K5)
+    assert set(p.narrow_tuning) == {"k4_ms", "k5_ms", "probe_shots"}
+    assert p.narrow_flag(eng, cfg.run_flags(), cfg.effective_capacity) == f   # cached
+    assert p.sections(cfg.run_flags()) != p.sections(cfg.run_flags() | _lib.GS_NARROW_K5)
+    got = [eng.run_counters(p, Engine.params(4, 0, cfg.shots, cfg.effective_capacity,
+                                             cfg.run_flags() | x))
+           for x in (0, _lib.GS_NARROW_K5)]
+    assert (got[0] == got[1]).all()
+    st = run_batch(prog, cfg)
+    assert st.total_shots == cfg.shots and st.preserved_shots == int(got[0][_lib.GS_C_PRESERVED])
