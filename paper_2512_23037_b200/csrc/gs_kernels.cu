@@ -284,8 +284,9 @@ int gs_program_sections(const gs_program *p, uint32_t flags) {
 extern "C++" {
 // the sampling kernels: RNG mode (x chi placement for the wide kernel)
 template <typename F>
-static cudaError_t with_narrow_kernel(bool philox, F f) {
-  return philox ? f(gs::narrow_kernel<true>) : f(gs::narrow_kernel<false>);
+static cudaError_t with_narrow_kernel(bool philox, bool k5, F f) {
+  if (k5) return philox ? f(gs::narrow_kernel<true, true>) : f(gs::narrow_kernel<false, true>);
+  return philox ? f(gs::narrow_kernel<true, false>) : f(gs::narrow_kernel<false, false>);
 }
 template <typename F>
 static cudaError_t with_wide_kernel(bool smem_chi, bool philox, bool block, F f) {
@@ -437,7 +438,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   if (any_narrow) {
     const u32 wb = (u32)((gs::kCntBytes + gs::narrow_bytes(P.kn) + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
     rc = occupancy(e, wb, r->warps_per_block, 4,
-                   [&](auto f) { return with_narrow_kernel(philox, f); }, KN);
+                   [&](auto f) { return with_narrow_kernel(philox, P.kn == 5, f); }, KN);
     if (rc) return rc;
   }
   if (any_wide && !block) {
@@ -584,7 +585,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
           On.warp_bytes = KN.warp_bytes;
           On.rec_in_smem = KN.rec_in_smem;
           On.chi_off = 0;
-          CUDA_TRY(with_narrow_kernel(philox, [&](auto kern) {
+          CUDA_TRY(with_narrow_kernel(philox, P.kn == 5, [&](auto kern) {
             kern<<<KN.blocks, KN.wpb * 32, KN.smem, st>>>(P, R, On, S);
             return cudaGetLastError();
           }));

@@ -24,6 +24,9 @@
 // what the instruction cache needs (B200: 32 KB L1.5).
 // GS_WIDE_ONLY runs the whole program as one wide section (A/B, tests).
 
+#ifndef GS_NARROW_BLOCKS_K5
+#define GS_NARROW_BLOCKS_K5 3
+#endif
 #ifndef GS_NARROW_BLOCKS
 #define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
 #endif
@@ -169,8 +172,12 @@ __device__ __noinline__ void narrow_dump_phase(double2 *amps, u32 n, u32 pn) {
 }
 
 // @region narrow: prologue
-template <bool kPhilox>
-__global__ void __launch_bounds__(128, GS_NARROW_BLOCKS)
+// kK5: the narrow limit kn = 5 build -- 16 KB of chi rows per warp make
+// shared memory the occupancy limit (3 blocks = 12 warps/SM), so it is
+// compiled for 3 resident blocks (more registers: no spills in the queue
+// reads); kn = 4 keeps 5 blocks = 20 warps/SM
+template <bool kPhilox, bool kK5>
+__global__ void __launch_bounds__(128, kK5 ? GS_NARROW_BLOCKS_K5 : GS_NARROW_BLOCKS)
 narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   extern __shared__ __align__(16) u8 smem[];
   const u32 lane = threadIdx.x & 31u;
@@ -244,10 +251,22 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       sfire = (u32)q[Q_FIRE];
       const u32 *qr = reinterpret_cast<const u32 *>(q + Q_HDR);
 #pragma unroll 1
-      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = qr[w];
+      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = __ldg(qr + w);
+      // chi rows: every lane reads its own slot (a strided gather across
+      // the warp), so keep several loads in flight per lane instead of one
       const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+      const u32 n0 = 1u << S.k0;
 #pragma unroll 1
-      for (u32 j = 0; j < (1u << S.k0); ++j) AN(j) = qc[j];
+      constexpr u32 kQ = kK5 ? 8u : 1u;
+      for (u32 j0 = 0; j0 < n0; j0 += kQ) {
+        double2 t[kQ];
+#pragma unroll
+        for (u32 u = 0; u < kQ; ++u)
+          if (j0 + u < n0) t[u] = __ldg(qc + j0 + u);
+#pragma unroll
+        for (u32 u = 0; u < kQ; ++u)
+          if (j0 + u < n0) AN(j0 + u) = t[u];
+      }
     }
     __syncwarp();
 

@@ -8,6 +8,10 @@
                        // keep this many iterations' loads in flight per thread (A/B r02g: 2 ~ 4 > 1)
 #endif
 constexpr int kGUnroll = GS_GUNROLL;   // (pragmas do not expand macros)
+#ifndef GS_WUNROLL
+#define GS_WUNROLL 1   // warp form (chi in shared memory): det-sum / compaction rounds in flight
+#endif
+constexpr u32 kWUnroll = GS_WUNROLL;
 // ---------------------------------------------------------------- wide sweeps
 //
 // Warp-cooperative passes over a dense chi array A[0, 2^k): lane l takes
@@ -251,7 +255,7 @@ __device__ __forceinline__ double2 sweep_det_sums_impl(double2 *A_, u32 size, u3
   const u32 lane = glane<kG>();
   gbar_in<kG>();
   double sp = 0.0, sm = 0.0;
-#pragma unroll (kG > 1 ? kGUnroll : 1)
+#pragma unroll (kG > 1 ? kGUnroll : kWUnroll)
   for (u32 j = lane; j < size; j += 32u * kG) {
     const double a2 = abs2(ldp<kPS>(A, j, ps));
     if (neg0 ^ par32(j & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
@@ -308,20 +312,34 @@ __device__ __forceinline__ SumNz sweep_compact_impl(double2 *A_, u32 half, u32 i
   SumNz r;
   r.sum = 0.0;
   r.nz = 0;
+  // kB rounds per barrier pair: a batch reads src(jp) >= jp for its own jp
+  // range before any of its writes, and later batches read above it, so
+  // batching keeps the in-place order safe with kB loads in flight per lane
+  // (and the per-lane order of the norm sum)
+  constexpr u32 kB = kG == 1 ? kWUnroll : 1;
+  constexpr u32 NT = 32u * kG;
 #pragma unroll 1
-  for (u32 b0 = 0; b0 < half; b0 += 32u * kG) {
-    const u32 jp = b0 + lane;
-    double2 v = make_double2(0.0, 0.0);
-    if (jp < half) {
-      const u32 j0 = ins_bit(jp, isq, 0);
-      v = ldp<kPS>(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
+  for (u32 b0 = 0; b0 < half; b0 += NT * kB) {
+    double2 v[kB];
+#pragma unroll
+    for (u32 u = 0; u < kB; ++u) {
+      const u32 jp = b0 + u * NT + lane;
+      v[u] = make_double2(0.0, 0.0);
+      if (jp < half) {
+        const u32 j0 = ins_bit(jp, isq, 0);
+        v[u] = ldp<kPS>(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
+      }
     }
     gsync<kG>();
-    if (jp < half) {
-      const double2 w = cscale(v, rs);
-      A[jp] = w;
-      r.sum = __dadd_rn(r.sum, abs2(w));
-      r.nz += nonzero(w);
+#pragma unroll
+    for (u32 u = 0; u < kB; ++u) {
+      const u32 jp = b0 + u * NT + lane;
+      if (jp < half) {
+        const double2 w = cscale(v[u], rs);
+        A[jp] = w;
+        r.sum = __dadd_rn(r.sum, abs2(w));
+        r.nz += nonzero(w);
+      }
     }
     gsync<kG>();
   }
