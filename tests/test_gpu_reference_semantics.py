@@ -226,3 +226,28 @@ def test_criterion_9_batch_size_saturation():
     assert tputs[-1] <= 1.5 * max(tputs[:-1]), rows
     assert tputs[-1] >= 4 * tputs[0], rows
     assert len({r[2] for r in rows}) == 1, rows   # identical discard counts
+
+
+def test_criterion_9_noise_speeds_up_postselection():
+    """Ref tests/test_acceptance.py:251-260 on the GPU: stronger noise
+    discards more shots early, so post-selected throughput rises with it
+    (device shots/s; each noise level is a fresh program, so the first
+    wave's upload is excluded by a warm-up run of each)."""
+    from paper_2512_23037_b200 import throughput_bench
+    from paper_2512_23037_b200.noise import apply_noise_model
+    layer = "R 0 1\nH 0\nCX 0 1\nT 0\nT_DAG 0\nM 0 1\nDETECTOR rec[-1] rec[-2]"
+    prog = parse_circuit("\n".join([layer] * 4) + "\n")
+    cfg = SamplerConfig(shots=1 << 22, master_seed=2, rng="philox", postselect=True)
+    values = [0.0005, 0.005, 0.05]
+    rows = []
+    for v in values:
+        noisy = apply_noise_model(prog, v)
+        run_batch(noisy, cfg)                         # warm-up
+        st = run_batch(noisy, cfg)
+        rows.append((v, st.total_shots / st.device_time_s, st.discard_rate))
+    discards = [r[2] for r in rows]
+    assert discards == sorted(discards) and discards[-1] > discards[0], rows
+    assert _at_most_one_inversion([r[1] for r in rows], increasing=True), rows
+    # the reference's own sweep helper gives the same discard rates
+    ref_rows = throughput_bench(prog, cfg, "noise", values)
+    assert [r[2] for r in ref_rows] == discards
