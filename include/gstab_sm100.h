@@ -59,6 +59,7 @@ extern "C" {
 #define GS_NARROW_K5 256u  /* lane-per-shot sections up to chi dimension 5
                               (default 4): a pure performance choice, the
                               results are identical either way */
+#define GS_BLOCK8 512u     /* with GS_CHI_BLOCK: 8 warps per shot (test)   */
 
 /* per-shot status codes (gs_run_records) */
 #define GS_ST_PRESERVED 1

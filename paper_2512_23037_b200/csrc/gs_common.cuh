@@ -330,7 +330,9 @@ struct Rng {
 // narrow (lane-per-shot) chi dimension limit kn, a run-time choice: 4, or
 // 5 with GS_NARROW_K5 (A/B r02j: the Table-2 d=5 headline +10.3 % at 5, the
 // d=3 workload -23 % and the grown proxy -8.5 %; sampler.Program tunes it
-// per program by timing both on a probe run -- results are identical)
+// per program by timing both on a probe run -- results are identical).  At
+// 5 only the narrow sections that hold a k = 5 op use 2^5 chi rows per lane
+// (12 warps/SM); the others keep the 2^4-row, 20-warp layout (Section::kn)
 __host__ __device__ __forceinline__ u32 narrow_kn(u32 flags) { return (flags & GS_NARROW_K5) ? 5u : 4u; }
 __host__ __device__ __forceinline__ u32 narrow_bytes(u32 kn) { return (1u << kn) * 32u * 16u; }   // An[2^kn][32] double2
 constexpr u32 kCntBytes = 64;                              // per-warp counters

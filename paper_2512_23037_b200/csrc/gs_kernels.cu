@@ -238,6 +238,7 @@ struct Section {
   u32 pc0, k0, nm0;
   bool wide;
   u32 pn0;   // reduced-T phase count on entry: TF_RED ops of earlier wide sections
+  u32 kn;    // narrow sections: the chi rows they need, 4 or 5 (kn_max 5 only)
 };
 
 #ifndef GS_NARROW_SPLIT
@@ -260,9 +261,12 @@ static void sections_of(const gs_program *p, bool wide_only, u32 kn, std::vector
     const bool split = !wide && (GS_NARROW_SPLIT > 0) && nops >= (u32)GS_NARROW_SPLIT;
     if (out.empty() || out.back().wide != wide || split) {
       while (nm < nn && (u32)p->tables[p->info.noise_off + 4 * nm] < (u32)pc) ++nm;
-      out.push_back(Section{(u32)pc, k, (u32)nm, wide, pn});
+      out.push_back(Section{(u32)pc, k, (u32)nm, wide, pn, 4u});
       nops = 0;
     }
+    // a narrow section needs 2^5 chi rows per lane only if one of its ops
+    // would be wide at limit 4; the others keep the 20-warp/SM layout
+    if (!wide && gs::op_is_wide(kind, k, fl, 4u)) out.back().kn = kn;
     ++nops;
     // the wide kernel runs TF_RED ops in the reduced form (gs_sweeps.cuh
     // t_mix); every shot entering a later section executed all of them
@@ -288,10 +292,15 @@ static cudaError_t with_narrow_kernel(bool philox, bool k5, F f) {
   if (k5) return philox ? f(gs::narrow_kernel<true, true>) : f(gs::narrow_kernel<false, true>);
   return philox ? f(gs::narrow_kernel<true, false>) : f(gs::narrow_kernel<false, false>);
 }
+// gw = warps sharing one shot: 1 (warp per shot), 8 or GS_BLOCK_WARPS (16)
 template <typename F>
-static cudaError_t with_wide_kernel(bool smem_chi, bool philox, bool block, F f) {
+static cudaError_t with_wide_kernel(bool smem_chi, bool philox, u32 gw, F f) {
   constexpr int G = GS_BLOCK_WARPS;
-  if (block) {
+  if (gw == 8) {
+    if (smem_chi) return philox ? f(gs::wide_kernel<true, true, 8>) : f(gs::wide_kernel<true, false, 8>);
+    return philox ? f(gs::wide_kernel<false, true, 8>) : f(gs::wide_kernel<false, false, 8>);
+  }
+  if (gw > 1) {
     if (smem_chi) return philox ? f(gs::wide_kernel<true, true, G>) : f(gs::wide_kernel<true, false, G>);
     return philox ? f(gs::wide_kernel<false, true, G>) : f(gs::wide_kernel<false, false, G>);
   }
@@ -417,28 +426,37 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
 
   // launch shapes: narrow warps hold 32 shots' chi rows and record columns,
   // wide warps one shot's chi (shared memory when 2^max_dim entries fit)
-  // chi of 2^14 entries or more: one block of GS_BLOCK_WARPS warps per shot
-  // on a per-block global buffer (the ~150-300 shots in flight keep it
-  // L2-resident to k ~ 15; r01bm config-4 sweep: 1.4-5.5x over a warp per
-  // shot).  k = 12-13 stays warp per shot on a global buffer (more shots in
-  // flight beat the block's per-pass barriers there); GS_CHI_BLOCK forces the
-  // block form, with chi in shared memory when it fits
+  // chi of 2^13 entries or more: one block of warps per shot on two global
+  // ping-pong buffers per block -- 8 warps and 2 blocks per SM at k = 13-14
+  // (2 x 148 shots in flight stay L2-resident; A/B r02o: 1.2-1.7x over a
+  // warp per shot at k = 13), 16 warps and 1 block per SM from k = 15 (r01bm
+  // config-4 sweep: 1.4-5.5x over a warp per shot; 8 warps lose there).
+  // GS_CHI_BLOCK forces the block form (16 warps, GS_BLOCK8: 8) with chi in
+  // shared memory when it fits, GS_CHI_BLOCK | GS_CHI_GLOBAL on global memory
   const size_t chi = (size_t)16 << P.max_dim;
-  const bool block = (r->flags & GS_CHI_BLOCK) ||
+  const bool forced_block = (r->flags & GS_CHI_BLOCK) != 0;
+  const bool block = forced_block ||
                      (!(r->flags & (GS_CHI_GLOBAL | GS_CHI_SMEM)) && P.max_dim >= GS_BLOCK_MIN_DIM);
+  const u32 gwarps = !block ? 1u
+                     : forced_block ? ((r->flags & GS_BLOCK8) ? 8u : (u32)GS_BLOCK_WARPS)
+                     : (P.max_dim < 15 ? 8u : (u32)GS_BLOCK_WARPS);
   bool smem_chi;
   if (r->flags & GS_CHI_GLOBAL) smem_chi = false;
-  else if (block) smem_chi = true;   // decided below against the opt-in limit
+  else if (block) smem_chi = forced_block;   // decided below against the opt-in limit
   else if (r->flags & GS_CHI_SMEM) smem_chi = chi <= 64 * 1024;
   else smem_chi = chi <= 32 * 1024;
   const size_t nrec_b = (size_t)P.rec_words32 * 4 * 32, wrec_b = (size_t)P.rec_words32 * 4;
-  KernelCfg KN, KW;
-  KN.rec_in_smem = nrec_b <= 4096;
+  KernelCfg KN4, KN5, KW;   // narrow launch shapes for sections needing 4 / 5 chi dims
+  KN4.rec_in_smem = KN5.rec_in_smem = nrec_b <= 4096;
   KW.rec_in_smem = wrec_b <= 4096;
-  if (any_narrow) {
-    const u32 wb = (u32)((gs::kCntBytes + gs::narrow_bytes(P.kn) + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
+  for (u32 kn : {4u, 5u}) {
+    bool used = false;
+    for (const Section &sc : secs) used |= !sc.wide && sc.kn == kn;
+    if (!used) continue;
+    KernelCfg &KN = kn == 5 ? KN5 : KN4;
+    const u32 wb = (u32)((gs::kCntBytes + gs::narrow_bytes(kn) + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
     rc = occupancy(e, wb, r->warps_per_block, 4,
-                   [&](auto f) { return with_narrow_kernel(philox, P.kn == 5, f); }, KN);
+                   [&](auto f) { return with_narrow_kernel(philox, kn == 5, f); }, KN);
     if (rc) return rc;
   }
   if (any_wide && !block) {
@@ -446,7 +464,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     KW.chi_off = (u32)base;
     const u32 wb = (u32)(base + (smem_chi ? chi : 0));
     rc = occupancy(e, wb, r->warps_per_block, GS_WIDE_WARPS,
-                   [&](auto f) { return with_wide_kernel(smem_chi, philox, false, f); }, KW);
+                   [&](auto f) { return with_wide_kernel(smem_chi, philox, 1u, f); }, KW);
     if (rc) return rc;
     if (!smem_chi) {   // bound the global chi scratch
       const u64 max_warps = ((u64)8 << 30) / chi;
@@ -456,17 +474,17 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   if (any_wide && block) {
     // [per-warp slices][group scratch: 2 x 32 u64][chi]
     const size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_in_smem ? ((wrec_b + 15) & ~(size_t)15) : 0);
-    const size_t head = (size_t)GS_BLOCK_WARPS * base + 64 * sizeof(u64);
+    const size_t head = (size_t)gwarps * base + 64 * sizeof(u64);
     if (smem_chi && head + chi > e->smem_optin) smem_chi = false;
-    KW.wpb = GS_BLOCK_WARPS;
+    KW.wpb = gwarps;
     KW.warp_bytes = (u32)base;
     KW.chi_off = (u32)head;
     KW.smem = head + (smem_chi ? chi : 0);
     int per = 0;
-    CUDA_TRY(with_wide_kernel(smem_chi, philox, true, [&](auto kern) {
+    CUDA_TRY(with_wide_kernel(smem_chi, philox, gwarps, [&](auto kern) {
       cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KW.smem);
       return err != cudaSuccess ? err
-                                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, GS_BLOCK_WARPS * 32, KW.smem);
+                                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, gwarps * 32, KW.smem);
     }));
     if (per < 1) return fail(GS_ERR_UNSUPPORTED, "block-per-shot state exceeds the SM");
     KW.blocks = (u32)(e->num_sms * per);
@@ -475,13 +493,14 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
       if ((u64)KW.blocks > max_blocks) KW.blocks = (u32)std::max<u64>(1, max_blocks);
     }
   }
-  if (r->blocks) { KN.blocks = r->blocks; KW.blocks = r->blocks; }
-  const u64 nwarps = std::max((u64)KN.blocks * KN.wpb, (u64)KW.blocks * KW.wpb);
+  if (r->blocks) { KN4.blocks = KN5.blocks = r->blocks; KW.blocks = r->blocks; }
+  const u64 nwarps = std::max({(u64)KN4.blocks * KN4.wpb, (u64)KN5.blocks * KN5.wpb,
+                               (u64)KW.blocks * KW.wpb});
   if (!smem_chi && any_wide) {
     rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 3 : KW.wpb) * chi);
     if (rc) return rc;
   }
-  if (!KN.rec_in_smem || !KW.rec_in_smem) {
+  if (!KN4.rec_in_smem || !KW.rec_in_smem) {
     rc = ensure_buf(&e->d_rec, &e->rec_bytes, (size_t)nwarps * nrec_b);
     if (rc) return rc;
   }
@@ -564,6 +583,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
         S.n_out = d_qn + (i & 1);
         S.work = e->d_work + i;
         S.pn0 = secs[i].pn0;
+        S.kn = secs[i].kn;
         if (i >= 1 && i + 1 < secs.size())   // the queue written here was read by section i-1
           CUDA_TRY(cudaMemsetAsync(d_qn + (i & 1), 0, sizeof(u32), st));
         Engine_TimedLaunch tl{(u32)i, nullptr, nullptr};
@@ -576,16 +596,17 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
           Ow.warp_bytes = KW.warp_bytes;
           Ow.rec_in_smem = KW.rec_in_smem;
           Ow.chi_off = KW.chi_off;
-          CUDA_TRY(with_wide_kernel(smem_chi, philox, block, [&](auto kern) {
+          CUDA_TRY(with_wide_kernel(smem_chi, philox, gwarps, [&](auto kern) {
             kern<<<KW.blocks, KW.wpb * 32, KW.smem, st>>>(P, R, Ow, S);
             return cudaGetLastError();
           }));
         } else {
+          const KernelCfg &KN = secs[i].kn == 5 ? KN5 : KN4;
           gs::DevOut On = O;
           On.warp_bytes = KN.warp_bytes;
           On.rec_in_smem = KN.rec_in_smem;
           On.chi_off = 0;
-          CUDA_TRY(with_narrow_kernel(philox, P.kn == 5, [&](auto kern) {
+          CUDA_TRY(with_narrow_kernel(philox, secs[i].kn == 5, [&](auto kern) {
             kern<<<KN.blocks, KN.wpb * 32, KN.smem, st>>>(P, R, On, S);
             return cudaGetLastError();
           }));

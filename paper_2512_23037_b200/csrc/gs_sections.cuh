@@ -46,7 +46,7 @@
 #define GS_BLOCK_MINB 1   // resident blocks the block form is compiled for (register bound)
 #endif
 #ifndef GS_BLOCK_MIN_DIM
-#define GS_BLOCK_MIN_DIM 14   // chi dimension from which the block form is the default
+#define GS_BLOCK_MIN_DIM 13   // chi dimension from which the block form is the default
 #endif
 
 __host__ __device__ __forceinline__ bool op_is_wide(u32 kind, u32 k, u32 fl, u32 kn) {
@@ -140,6 +140,7 @@ struct DevSec {
   u32 *n_out;
   unsigned long long *work; // atomic work counter
   u32 pn0;                 // reduced-T phase count at pc0 (static; see t_mix)
+  u32 kn;                  // narrow sections: chi rows per lane 2^kn (4 or 5)
 };
 
 // record words of a slot, rounded to 16 B so the chi rows are double2-aligned
@@ -188,7 +189,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
   double2 *An = reinterpret_cast<double2 *>(mine + kCntBytes);
   // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
-  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + narrow_bytes(P.kn))
+  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + narrow_bytes(S.kn))
                             : O.grec + gw * (u64)P.rec_words32 * 32u;
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
@@ -701,7 +702,8 @@ template <bool kSmemChi, bool kPhilox, int kG>
 #ifdef GS_WIDE_MAXREG
 __global__ void __maxnreg__(GS_WIDE_MAXREG)
 #else
-__global__ void __launch_bounds__(kG == 1 ? 32 * GS_WIDE_WARPS : 32 * kG, kG == 1 ? GS_WIDE_BLOCKS : GS_BLOCK_MINB)
+__global__ void __launch_bounds__(kG == 1 ? 32 * GS_WIDE_WARPS : 32 * kG,
+                                  kG == 1 ? GS_WIDE_BLOCKS : (kG == 8 ? 2 : GS_BLOCK_MINB))
 #endif
 wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   extern __shared__ __align__(16) u8 smem[];

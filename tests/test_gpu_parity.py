@@ -190,10 +190,11 @@ def test_shot_indices_beyond_32_bits(mode):
 
 @pytest.mark.parametrize("n,t", [(56, 16), (48, 24)])
 def test_large_chi_block_per_shot_matches_oracle(n, t):
-    """Config-4 programs with chi beyond 32 KB (k <= 13: the block's shared
-    memory; k = 15: a per-block global buffer) run one block of warps per
-    shot by default; records, statuses and overflow points must equal the
-    oracle's and the warp-per-shot global-buffer path's."""
+    """Config-4 programs with chi beyond 32 KB run one block of warps per
+    shot by default (k = 13: 8 warps, 2 blocks per SM; k = 15: 16 warps; both
+    on global ping-pong buffers); records, statuses and overflow points must
+    equal the oracle's and those of every other large-chi form (warp per
+    shot on a global buffer, 16- and 8-warp blocks on shared or global chi)."""
     from paper_2512_23037_b200.msc import config4_circuit
     from paper_2512_23037_b200.noise import apply_noise_model
     prog = apply_noise_model(config4_circuit(n, t, seed=n + t), 1e-3)
@@ -205,11 +206,14 @@ def test_large_chi_block_per_shot_matches_oracle(n, t):
         p = Program(dp)
         eng = get_engine(0)
         outs = []
-        for extra in (0, _lib.GS_CHI_GLOBAL):
+        for extra in (0, _lib.GS_CHI_GLOBAL, _lib.GS_CHI_BLOCK,
+                      _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8,
+                      _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8 | _lib.GS_CHI_GLOBAL):
             par = Engine.params(9, 0, shots, 32768, flags | extra)
             outs.append(eng.run_records(p, par))
-        for x, y in zip(*outs):
-            assert np.array_equal(x, y), mode
+        for other in outs[1:]:
+            for x, y in zip(outs[0], other):
+                assert np.array_equal(x, y), mode
         ref = _oracle_results(prog, 9, shots, 32768, False, mode=mode)
         got = _gpu_results(prog, 9, shots, 32768, False, rng=mode)
         assert got == ref, mode
@@ -257,7 +261,8 @@ def test_msc_noiseless_is_deterministic(d):
 @pytest.mark.parametrize("mode", ["splitmix", "philox"])
 @pytest.mark.parametrize("variant", ["default", "wide_only", "chi_global",
                                      "chi_smem", "wide_only_chi_smem", "chi_block",
-                                     "chi_block_global", "wide_only_chi_block", "narrow_k5"])
+                                     "chi_block_global", "wide_only_chi_block", "narrow_k5",
+                                     "chi_block8", "chi_block8_global"])
 def test_chi_storage_modes_match_oracle(variant, mode):
     """Lane-per-shot / warp-per-shot / block-per-shot execution and shared- /
     global-memory chi buffers must all give the oracle's results, in both
@@ -270,7 +275,9 @@ def test_chi_storage_modes_match_oracle(variant, mode):
                    "chi_block": _lib.GS_CHI_BLOCK,
                    "chi_block_global": _lib.GS_CHI_BLOCK | _lib.GS_CHI_GLOBAL,
                    "wide_only_chi_block": _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK,
-                   "narrow_k5": _lib.GS_NARROW_K5}[variant]
+                   "narrow_k5": _lib.GS_NARROW_K5,
+                   "chi_block8": _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8,
+                   "chi_block8_global": _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8 | _lib.GS_CHI_GLOBAL}[variant]
     eng = get_engine(0)
     for it in range(25):
         n = rng.choice((4, 9, 20))
