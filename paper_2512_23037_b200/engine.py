@@ -35,6 +35,8 @@ class Program:
         self._ops = np.ascontiguousarray(dp.ops, dtype=np.uint64)
         self._tables = np.ascontiguousarray(dp.tables, dtype=np.uint64)
         self._locs = np.ascontiguousarray(dp.locs, dtype=np.uint64)
+        self._narrow = {}            # (device, flags) -> tuned narrow flag
+        self.narrow_tuning = None    # probe times of the last tuning
         h = ct.c_void_p()
         _lib.check(lib.gs_program_create(ct.byref(info), _u64p(self._ops),
                                          self._ops.size, _u64p(self._tables),
@@ -56,9 +58,8 @@ class Program:
         costs narrow occupancy elsewhere (d=3: 4 is 30 % faster)."""
         if flags & _lib.GS_WIDE_ONLY:
             return 0
-        cache = self.__dict__.setdefault("_narrow", {})
-        key = (engine.device, flags & (_lib.GS_RNG_PHILOX | _lib.GS_POSTSELECT |
-                                       _lib.GS_CHI_GLOBAL | _lib.GS_CHI_SMEM | _lib.GS_CHI_BLOCK))
+        cache = self._narrow
+        key = self.tuning_key(engine, flags)
         if key in cache:
             return cache[key]
         if self.dp.max_dim < 5:
@@ -75,6 +76,12 @@ class Program:
         self.narrow_tuning = {"k4_ms": times[0], "k5_ms": times[_lib.GS_NARROW_K5],
                               "probe_shots": self.TUNE_SHOTS}
         return best
+
+    @staticmethod
+    def tuning_key(engine: "Engine", flags: int):
+        return (engine.device, flags & (_lib.GS_RNG_PHILOX | _lib.GS_POSTSELECT |
+                                        _lib.GS_CHI_GLOBAL | _lib.GS_CHI_SMEM |
+                                        _lib.GS_CHI_BLOCK))
 
     def sections(self, flags: int = 0) -> int:
         """Narrow/wide sections (= sampling launches per chunk of shots)."""

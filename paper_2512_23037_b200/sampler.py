@@ -243,9 +243,8 @@ TUNE_MIN_SHOTS = 1 << 23
 def tuned_flags(p: Program, eng: Engine, cfg: SamplerConfig) -> int:
     """Performance-only run flags measured for this program (the narrow chi
     limit, ``Program.narrow_flag``); 0 for short runs."""
-    if cfg.shots < TUNE_MIN_SHOTS:
-        return p.__dict__.get("_narrow", {}).get(
-            (eng.device, cfg.run_flags() & (_lib.GS_RNG_PHILOX | _lib.GS_POSTSELECT)), 0)
+    if cfg.shots < TUNE_MIN_SHOTS:   # reuse an earlier tuning, never probe
+        return p._narrow.get(Program.tuning_key(eng, cfg.run_flags()), 0)
     return p.narrow_flag(eng, cfg.run_flags(), cfg.effective_capacity)
 
 
