@@ -241,6 +241,9 @@ struct Section {
   u32 kn;    // narrow sections: the chi rows they need, 4 or 5 (kn_max 5 only)
 };
 
+#ifndef GS_NARROW_KSPLIT
+#define GS_NARROW_KSPLIT 30  // narrow sections of >= N ops also split where the 2^5-row need changes
+#endif
 #ifndef GS_NARROW_SPLIT
 #define GS_NARROW_SPLIT 75  // split narrow sections every N ops (0: never) so the survivors of
                             // early discards re-pack into full warps (A/B: 51.2M at 75, 49.4M unsplit,
@@ -250,30 +253,59 @@ struct Section {
 static void sections_of(const gs_program *p, bool wide_only, u32 kn, std::vector<Section> &out) {
   out.clear();
   const std::vector<u64> &ops = p->ops;
-  size_t pc = 0, nm = 0;
+  // op starts, then for every op the length of the narrow run from it to the
+  // next wide op (a k-split never leaves a short tail section)
+  std::vector<u32> at;
+  for (size_t pc = 0; pc < ops.size();) {
+    at.push_back((u32)pc);
+    const u32 kind = (u32)(ops[pc] & 0xff), len = (u32)((ops[pc] >> 8) & 0xff);
+    if (kind == gs::OP_END || len == 0) break;
+    pc += len;
+  }
+  auto hdr = [&](size_t i, u32 &kind, u32 &len, u32 &k, u32 &fl) {
+    const u64 h = ops[at[i]];
+    kind = (u32)(h & 0xff); len = (u32)((h >> 8) & 0xff);
+    k = (u32)((h >> 16) & 0xff); fl = (u32)((h >> 24) & 0xff);
+  };
+  std::vector<u32> run(at.size() + 1, 0);
+  for (size_t i = at.size(); i-- > 0;) {
+    u32 kind, len, k, fl;
+    hdr(i, kind, len, k, fl);
+    run[i] = (wide_only || gs::op_is_wide(kind, k, fl, kn)) ? 0u : run[i + 1] + 1u;
+  }
+  size_t nm = 0;
   u32 nops = 0, pn = 0;
+  bool prev5 = false;
   const u32 nn = p->info.num_noise;
-  while (pc < ops.size()) {
-    const u64 h = ops[pc];
-    const u32 kind = (u32)(h & 0xff), len = (u32)((h >> 8) & 0xff);
-    const u32 k = (u32)((h >> 16) & 0xff), fl = (u32)((h >> 24) & 0xff);
+  for (size_t i = 0; i < at.size(); ++i) {
+    const u32 pc = at[i];
+    u32 kind, len, k, fl;
+    hdr(i, kind, len, k, fl);
     const bool wide = wide_only || gs::op_is_wide(kind, k, fl, kn);
-    const bool split = !wide && (GS_NARROW_SPLIT > 0) && nops >= (u32)GS_NARROW_SPLIT;
+    // needs5: a narrow op that needs 2^5 chi rows (wide at limit 4)
+    const bool needs5 = !wide && kn > 4u && gs::op_is_wide(kind, k, fl, 4u);
+    bool split = !wide && (GS_NARROW_SPLIT > 0) && nops >= (u32)GS_NARROW_SPLIT;
+    // a 2^4-row narrow section of >= GS_NARROW_KSPLIT ops ends where the
+    // ops start needing 2^5 rows (if >= 16 narrow ops follow), so the
+    // k <= 4 stretch keeps the 20-warp layout instead of inheriting the
+    // 12-warp one (the Table-2 d=5 injection + d=3 round)
+    if (!wide && GS_NARROW_KSPLIT > 0 && !out.empty() && !out.back().wide && out.back().kn == 4u &&
+        nops >= (u32)GS_NARROW_KSPLIT && needs5 && !prev5 && run[i] >= 16u)
+      split = true;
     if (out.empty() || out.back().wide != wide || split) {
-      while (nm < nn && (u32)p->tables[p->info.noise_off + 4 * nm] < (u32)pc) ++nm;
-      out.push_back(Section{(u32)pc, k, (u32)nm, wide, pn, 4u});
+      while (nm < nn && (u32)p->tables[p->info.noise_off + 4 * nm] < pc) ++nm;
+      out.push_back(Section{pc, k, (u32)nm, wide, pn, 4u});
       nops = 0;
     }
     // a narrow section needs 2^5 chi rows per lane only if one of its ops
     // would be wide at limit 4; the others keep the 20-warp/SM layout
-    if (!wide && gs::op_is_wide(kind, k, fl, 4u)) out.back().kn = kn;
+    if (needs5) out.back().kn = kn;
+    prev5 = needs5;
     ++nops;
     // the wide kernel runs TF_RED ops in the reduced form (gs_sweeps.cuh
     // t_mix); every shot entering a later section executed all of them
     if (wide && kind == gs::OP_T && (fl & gs::TF_RED) && len > 12)
       pn = (pn + ((ops[pc + 12] & 2u) ? 15u : 1u)) & 15u;
-    if (kind == gs::OP_END || len == 0) break;
-    pc += len;
   }
 }
 
