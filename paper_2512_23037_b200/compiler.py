@@ -237,6 +237,43 @@ class _XZTableau:
             raise CompileError("stabilizer decomposition failed")
         return beta, delta, (r[2] - m[2]) & 3, beta | (gamma << n)
 
+    def actions_1q(self, qmask: int):
+        """``action`` of X_q and Z_q for every q in ``qmask`` (noise tables),
+        from one conversion of the rows to Python ints: the anticommutation
+        masks are column reads, and in a symplectic tableau the stabilizer
+        coefficients of P are its anticommutations with the destabilizers
+        (gamma = delta), checked below by rebuilding P.  Same results as
+        ``action`` (tests/test_compiler_flags.py)."""
+        n = self.n
+        xr = [int(v) for v in self.x]
+        zr = [int(v) for v in self.z]
+        # column q of x / z as a 2n-bit row mask, for all 64 columns at once
+        sh = np.arange(64, dtype=np.uint64)
+        cols = []
+        for a in (self.x, self.z):
+            bits = ((a[None, :] >> sh[:, None]) & np.uint64(1)).astype(np.uint8)
+            packed = np.packbits(bits, axis=1, bitorder="little")
+            cols.append([int.from_bytes(row.tobytes(), "little") for row in packed])
+        mask = (1 << n) - 1
+        out = {}
+        for q in _iter_bits(qmask):
+            colx, colz = cols[0][q], cols[1][q]
+            for lx, lz in ((1, 0), (0, 1)):
+                qx, qz = lx << q, lz << q
+                anti = colz if lx else colx          # rows anticommuting with X_q / Z_q
+                beta, delta = anti >> n, anti & mask
+                d = (0, 0, 0)
+                for k in _iter_bits(beta):
+                    d = _pmul(d, (xr[k], zr[k], 0))
+                r = _pmul((d[0], d[1], (-d[2]) & 3), (qx, qz, 0))
+                m = (0, 0, 0)
+                for k in _iter_bits(delta):
+                    m = _pmul(m, (xr[n + k], zr[n + k], 0))
+                if (m[0], m[1]) != (r[0], r[1]):
+                    raise CompileError("stabilizer decomposition failed")
+                out[(q, lx)] = (beta, delta, (r[2] - m[2]) & 3, beta | (delta << n))
+        return out
+
     def pivot(self, px: int, pz: int):
         """Measurement pivot (ref tableau.py:165-200).  Returns (t, sel, K):
         per shot, rows j in ``sel`` get sigma_j ^= sigma_{n+t} ^ K_j, then
@@ -556,9 +593,10 @@ def compile_program(prog, *, max_dim: int = DEFAULT_MAX_DIM,
         for q in targets:
             qmask |= 1 << q
         words = []
+        acts = tab.actions_1q(qmask)
         for q in _iter_bits(qmask):
-            for lx, lz in ((1, 0), (0, 1)):
-                beta, delta, xis, msig = tab.action(lx << q, lz << q, 0)
+            for lx in (1, 0):
+                beta, delta, xis, msig = acts[(q, lx)]
                 # sign flips still pending at this point are absorbed into the
                 # static phase: par((sigma^P) & M) = par(sigma&M) ^ par(P&M)
                 xis = (xis + 2 * ((pending & msig).bit_count() & 1)) & 3

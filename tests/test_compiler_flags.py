@@ -130,3 +130,21 @@ def test_static_span_keeps_cancelled_t_coordinates():
     assert flat[cut.truncated_at].name == "T" and flat[cut.truncated_at].targets[0] == 20
     whole = compile_program(prog, max_dim=24)
     assert whole.truncated_at is None and whole.max_dim == 24
+
+
+def test_actions_1q_equals_action_on_random_tableaux():
+    """The noise tables' batched single-qubit actions (column reads, gamma =
+    delta) equal the general pauli_action restatement row by row."""
+    import random
+    from paper_2512_23037_b200.compiler import _XZTableau
+    rng = random.Random(5)
+    for n in (3, 9, 30, 64):
+        tab = _XZTableau(n)
+        for _ in range(6 * n):
+            g = rng.choice(("H", "S", "S_DAG", "H_XY", "X", "CX", "CZ", "SWAP"))
+            qs = rng.sample(range(n), 2) if g in ("CX", "CZ", "SWAP") else [rng.randrange(n)]
+            tab.gate(g, qs)
+        qmask = sum(1 << q for q in rng.sample(range(n), min(n, 12)))
+        got = tab.actions_1q(qmask)
+        for (q, lx), act in got.items():
+            assert act == tab.action(lx << q, (1 - lx) << q, 0), (n, q, lx)
