@@ -45,7 +45,7 @@ class Program:
         self.handle = h
 
     # probe size of the narrow-limit tuning (narrow_flag)
-    TUNE_SHOTS = 1 << 20
+    TUNE_SHOTS = 1 << 19
 
     def narrow_flag(self, engine: "Engine", flags: int, capacity: int) -> int:
         """``GS_NARROW_K5`` or 0: the narrow (lane-per-shot) chi dimension
