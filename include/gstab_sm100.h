@@ -50,15 +50,18 @@ extern "C" {
 #define GS_CHI_GLOBAL 4u   /* force chi buffers into global memory (test) */
 #define GS_CHI_SMEM 16u    /* force chi buffers into shared memory (test) */
 #define GS_WIDE_ONLY 32u   /* run every op warp-per-shot (A/B, test)     */
-#define GS_CHI_BLOCK 64u   /* wide sections: one block of warps per shot
-                              (the default when chi exceeds 32 KB)       */
+#define GS_CHI_BLOCK 64u   /* wide sections: one block of 16 warps per
+                              shot, chi in shared memory when it fits (the
+                              default from chi dimension 13: 8 warps at
+                              13-14, 16 from 15, on global memory)       */
 #define GS_SECTION_STATS 128u /* per-section device time (CUDA events on
                               the launch stream) and model bytes / shots
                               (a small reduction launch after each
                               section); read with gs_engine_section_stats */
 #define GS_NARROW_K5 256u  /* lane-per-shot sections up to chi dimension 5
-                              (default 4): a pure performance choice, the
-                              results are identical either way */
+                              (default 4; only sections holding a k = 5 op
+                              use the 2^5-row layout): a pure performance
+                              choice, the results are identical either way */
 #define GS_BLOCK8 512u     /* with GS_CHI_BLOCK: 8 warps per shot (test)   */
 
 /* per-shot status codes (gs_run_records) */

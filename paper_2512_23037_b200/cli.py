@@ -5,7 +5,7 @@ sampling commands, running on the B200.
         [--postselect] [--seed S] [--rng splitmix|philox] [--witnesses K]
     python -m paper_2512_23037_b200 stats CIRCUIT
     python -m paper_2512_23037_b200 bench CIRCUIT --sweep batch-size|noise --values ...
-    python -m paper_2512_23037_b200 msc --d 5 [--noise p]      # proxy circuit text
+    python -m paper_2512_23037_b200 msc --d 5 [--variant table2|grown|proxy] [--noise p]
 
 Exit codes as the reference: 0 success, 2 usage error, 3 parse error
 (ref cli.py:24-27).  ``sample`` writes the reference ``RunStats.as_dict``
@@ -111,8 +111,14 @@ def cmd_bench(a):
 
 
 def cmd_msc(a):
-    from .msc import msc_circuit
-    prog = msc_circuit(a.d)
+    from . import msc
+    make = {("table2", 5): msc.msc_d5_circuit, ("table2", 3): msc.msc_d3_circuit,
+            ("grown", 5): lambda: msc.msc_grown_circuit(5),
+            ("proxy", 5): lambda: msc.msc_circuit(5), ("proxy", 3): lambda: msc.msc_circuit(3)}
+    if (a.variant, a.d) not in make:
+        print("error: no %s circuit at d=%d" % (a.variant, a.d), file=sys.stderr)
+        return EXIT_USAGE
+    prog = make[(a.variant, a.d)]()
     if a.noise:
         prog = apply_noise_model(prog, a.noise)
     _emit(prog.serialize(), a.out)
@@ -155,8 +161,10 @@ def build_parser():
     b.add_argument("--rng", choices=("splitmix", "philox"), default="splitmix")
     b.add_argument("--out", default=None)
     b.set_defaults(fn=cmd_bench)
-    m = sub.add_parser("msc", help="emit the MSC proxy circuit text")
+    m = sub.add_parser("msc", help="emit a magic-state-cultivation circuit text")
     m.add_argument("--d", type=int, default=5, choices=(3, 5))
+    m.add_argument("--variant", default="table2", choices=("table2", "grown", "proxy"),
+                   help="table2: the paper's Table 2 shape (msc_d5_circuit / msc_d3_circuit)")
     m.add_argument("--noise", type=float, default=None)
     m.add_argument("--out", default=None)
     m.set_defaults(fn=cmd_msc)

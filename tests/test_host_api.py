@@ -222,6 +222,13 @@ def test_cli_stats_and_msc(tmp_path):
     import json
     d = json.loads(out.read_text())
     assert d["total_qubits"] == 15 and d["t_count"] == 22
+    # the default d=5 circuit is the Table-2-shaped one; the proxies stay reachable
+    assert main(["msc", "--d", "5", "--out", str(path)]) == 0
+    assert main(["stats", str(path), "--out", str(out)]) == 0
+    d = json.loads(out.read_text())
+    assert (d["total_qubits"], d["total_gates"], d["measurements"], d["t_count"]) == (42, 741, 93, 72)
+    assert main(["msc", "--d", "5", "--variant", "grown", "--out", str(path)]) == 0
+    assert main(["msc", "--d", "3", "--variant", "grown"]) == 2
 
 
 def test_cli_parse_error_exit_code(tmp_path):
