@@ -562,7 +562,7 @@ def main():
     # e2e through the public Python API, as a user calls it: a fresh
     # CircuitProgram (so the host compile to device bytecode is inside the
     # timed region, once), then run_batch over this rank's shots in waves of
-    # 2^24 (each wave: gs_run_counters with host buffers -- the op stream
+    # cfg.wave_shots (each wave: gs_run_counters with host buffers -- the op stream
     # uploaded host->device, counters read back device->host); N > 1:
     # run_batch_distributed (the same per rank + one all-reduce of the
     # counters).  Wall time between barriers, max over ranks.
@@ -588,7 +588,7 @@ def main():
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    waves = -(-e2e_shots // S)
+    waves = -(-e2e_shots // cfg_e.wave_shots)
     e2e = {"value": st_e.total_shots / e2e_s, "unit": "shots/s",
            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * waves * world,
            "shots": st_e.total_shots, "wall_s": e2e_s,

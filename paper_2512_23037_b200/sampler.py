@@ -36,7 +36,7 @@ from . import _lib
 from .engine import Engine, Program, get_engine
 
 _M64 = (1 << 64) - 1
-_WAVE = 1 << 24         # default shots resident per launch (batch_size=None)
+_WAVE = 1 << 22         # default shots resident per launch (batch_size=None)
 
 
 class CorruptStateError(RuntimeError):
@@ -106,7 +106,9 @@ class SamplerConfig:
     master_seed: int = 0
     # shots resident per launch (one wave = one gs_run_counters call, the
     # GPU analogue of the reference's waves, ref sampler.py:348-382);
-    # None = 2^24, which saturates a B200 (Fig. 4 analogue: bench --sweep)
+    # None = 2^22: saturates a B200 (Fig. 4 analogue, profiles/
+    # fig4_batch_size_r02u.csv: 36.6 M shots/s at 2^20, 37.0 M at 2^22 on the
+    # d=5 workload) with 1/4 of the section-queue memory of 2^24
     batch_size: int | None = None
     entry_capacity: int = 4096
     threads: int = 1
