@@ -1,6 +1,6 @@
-"""Large-sample statistical parity (opt-in: GS_LONG_STATS=1, ~6 min on one
-B200 + 16 host cores): the headline workload (grown d=5 MSC proxy, p=1e-3)
-and BASELINE configs 2 and 3, post-selected, sampled with billions of
+"""Large-sample statistical parity (opt-in: GS_LONG_STATS=1, ~8 min on one
+B200 + 16 host cores): the Table-2 d=5 and d=3 cultivation circuits, the
+grown d=5 proxy, the d=3 proxy and BASELINE config 3, post-selected, sampled with billions of
 Philox shots on the GPU against reference-stream (SplitMix) shots of the
 CPU oracle (GS_LONG_SCALE scales both sample sizes).  Discard rate and
 logical-error rate must agree (Bayes-factor-1000 intervals overlap and
@@ -23,13 +23,17 @@ pytestmark = [pytest.mark.gpu,
 
 from oracle import gstab_oracle as orc
 from paper_2512_23037_b200 import SamplerConfig, run_batch
-from paper_2512_23037_b200.msc import injection_circuit, msc_circuit, msc_grown_circuit
+from paper_2512_23037_b200.msc import (injection_circuit, msc_circuit, msc_d3_circuit,
+                                       msc_d5_circuit, msc_grown_circuit)
 from paper_2512_23037_b200.noise import apply_noise_model
 from stats_check import assert_rates_agree, z_score as _z
 
 
 WORKLOADS = {
     # name: (builder, p, default GPU shots, default CPU shots)
+    # the round-2 headline (BASELINE config 5) and config 2 with Table 2's shape
+    "msc_d5_table2": (msc_d5_circuit, 1e-3, 2 * 10 ** 9, 60000),
+    "msc_d3_table2": (msc_d3_circuit, 1e-3, 10 ** 9, 200000),
     "msc_d5_grown_proxy": (lambda: msc_grown_circuit(5), 1e-3, 4 * 10 ** 9, 60000),
     # BASELINE config 2: MSC d=3, 1e8 shots on one B200
     "msc_d3_proxy": (lambda: msc_circuit(3), 1e-3, 10 ** 8, 200000),
