@@ -492,7 +492,11 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     if (rc) return rc;
   }
   if (any_wide && !block) {
-    size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_in_smem ? ((wrec_b + 15) & ~(size_t)15) : 0);
+    // warp form: counters and up to 32 record words in registers
+    // (rec_in_smem = 1 means "in registers" here), the SplitMix fire-bit
+    // ring in shared memory, then chi
+    KW.rec_in_smem = P.rec_words32 <= 32;
+    size_t base = philox ? 0 : gs::kWinBytes;
     KW.chi_off = (u32)base;
     const u32 wb = (u32)(base + (smem_chi ? chi : 0));
     rc = occupancy(e, wb, r->warps_per_block, GS_WIDE_WARPS,

@@ -31,13 +31,13 @@
 #define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
 #endif
 #ifndef GS_WIDE_BLOCKS
-// launch bound only: <= 128 registers, no spills, so 13 one-warp blocks fit
-// per SM at d=5 (shared memory bound; 12 at 146 registers).  A/B (r01bl):
-// 55.2M vs 54.0M, 53.3M / 52.2M with __maxnreg__ 120 / 112
-#define GS_WIDE_BLOCKS 4
+// launch bound only: blocks of up to GS_WIDE_WARPS warps, 1 resident ->
+// <= 146 registers, which 14 warps of the warp form can hold (round 1 held
+// the wide kernel to 128 registers for 13 one-warp blocks: r01bl)
+#define GS_WIDE_BLOCKS 1
 #endif
 #ifndef GS_WIDE_WARPS
-#define GS_WIDE_WARPS 4    // most warps per wide block (13 in one block: 53.5M)
+#define GS_WIDE_WARPS 14   // most warps per wide block (warp form: 14 x 16 KB of chi fit an SM)
 #endif
 #ifndef GS_BLOCK_WARPS
 #define GS_BLOCK_WARPS 16  // warps sharing one shot's chi (block form)
@@ -160,6 +160,15 @@ __device__ __forceinline__ void flush_counters(const DevOut &O, unsigned long lo
     const int dst[WC_N] = {GS_C_TOTAL, GS_C_PRESERVED, GS_C_DISCARDED, GS_C_OVERFLOW,
                            GS_C_CORRUPT, GS_C_UNSUPPORTED, GS_C_ERROR_SHOTS, GS_C_MODEL_BYTES};
     atomicAdd((unsigned long long *)O.counters + dst[lane], wcnt[lane]);
+  }
+}
+
+// the warp form's counters: lane i holds counter i (WC_* order)
+__device__ __forceinline__ void flush_counter_regs(const DevOut &O, u64 cntl, u32 lane) {
+  if (lane < WC_N && cntl) {
+    const int dst[WC_N] = {GS_C_TOTAL, GS_C_PRESERVED, GS_C_DISCARDED, GS_C_OVERFLOW,
+                           GS_C_CORRUPT, GS_C_UNSUPPORTED, GS_C_ERROR_SHOTS, GS_C_MODEL_BYTES};
+    atomicAdd((unsigned long long *)O.counters + dst[lane], (unsigned long long)cntl);
   }
 }
 
@@ -712,10 +721,21 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   const u32 wpb = blockDim.x >> 5;
   const u64 gw = (u64)blockIdx.x * wpb + wib;
   u8 *mine = smem + (size_t)wib * O.warp_bytes;
-  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
-  u32 *win = reinterpret_cast<u32 *>(mine + kCntBytes);
-  u32 *recw = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kWinBytes)
-                            : O.grec + gw * (u64)P.rec_words32;
+  // warp form (kReg): the shot counters and (up to 32) record words live in
+  // registers -- lane i holds counter i and record word i -- so a warp's
+  // shared-memory slice is chi alone (plus the SplitMix fire-bit ring) and
+  // 14 warps fit an SM at 16 KB of chi instead of 13 (host: rec_in_smem = 1
+  // means "record words in registers" for this form); the block form keeps
+  // both in its per-warp slices
+  constexpr bool kReg = kG == 1;
+  const bool rec_reg = kReg && O.rec_in_smem;
+  u64 cntl = 0;   // kReg: counter WC_[lane]
+  u32 rwl = 0;    // rec_reg: record word [lane]
+  unsigned long long *wcnt = kReg ? nullptr : reinterpret_cast<unsigned long long *>(mine);
+  u32 *win = reinterpret_cast<u32 *>(mine + (kReg ? 0u : kCntBytes));
+  u32 *recw = rec_reg ? nullptr
+              : (O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kWinBytes)
+                               : O.grec + gw * (u64)P.rec_words32);
   // block form: per-warp slices, then the group scratch, then chi
   const u32 gl = glane<kG>();
   constexpr u32 NT = 32u * kG;
@@ -747,9 +767,14 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   const u32 SU = slot_u64(P);
   (void)n;
 
-  if (lane < WC_N) wcnt[lane] = 0;
+  if (!kReg && lane < WC_N) wcnt[lane] = 0;
   __syncwarp();
   const u64 total = S.q_in ? (u64)*S.n_in : S.count;
+  // record-bit access (registers or memory), warp-uniform / per-lane index
+  auto rec_bit = [&](u32 idx) -> u32 {
+    if (rec_reg) return (__shfl_sync(FULL, rwl, idx >> 5) >> (idx & 31)) & 1u;
+    return (recw[idx >> 5] >> (idx & 31)) & 1u;
+  };
 
 #pragma unroll 1
   for (;;) {
@@ -778,8 +803,11 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       rng.shot = R.shot_begin + sl;
       rng.seed = 0;
       if (!philox) rng.seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, rng.shot);
+      if (rec_reg) rwl = 0;
+      else {
 #pragma unroll 1
-      for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
+        for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
+      }
       if (gl == 0) A[0] = make_double2(1.0, 0.0);
       nrm_l = gl == 0 ? 1.0 : 0.0;
       nrm_lane0 = true;
@@ -802,8 +830,11 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       gj = (u32)q[Q_GEO]; gpos = (u32)(q[Q_GEO] >> 32);
       fire_pc = (u32)q[Q_FIRE];
       const u32 *qr = reinterpret_cast<const u32 *>(q + Q_HDR);
+      if (rec_reg) rwl = lane < P.rec_words32 ? qr[lane] : 0u;
+      else {
 #pragma unroll 1
-      for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = qr[w];
+        for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = qr[w];
+      }
       // chi in, and its norm (same per-lane order + tree as a sum pass)
       const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
 #pragma unroll 1
@@ -1221,7 +1252,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         u32 rb = bout;
         if ((wfl & MF_FLIP) && rng.m53(udraw + 1) < __ldg(op + 14)) rb ^= 1u;
         if (wfl & MF_RECORD) {
-          if (lane == 0 && rb) recw[slot >> 5] |= 1u << (slot & 31);
+          if (rec_reg) {
+            if (rb && lane == (slot >> 5)) rwl |= 1u << (slot & 31);
+          } else if (lane == 0 && rb) recw[slot >> 5] |= 1u << (slot & 31);
           __syncwarp();
         }
         if ((wfl & MF_RESET) && bout) { sig_lo ^= __ldg(op + 15); sig_hi ^= __ldg(op + 16); }
@@ -1231,7 +1264,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       // @region wide: feedback/detector/end
       if (wkind == OP_FEEDBACK) {
         const u32 idx = (u32)__ldg(op + 1);
-        if ((recw[idx >> 5] >> (idx & 31)) & 1u) {
+        if (rec_bit(idx)) {
           sig_lo ^= __ldg(op + 2);
           sig_hi ^= __ldg(op + 3);
           mbytes += __ldg(op + 4);
@@ -1244,9 +1277,11 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         const u64 off = __ldg(op + 2);
         u32 bb = 0;
 #pragma unroll 1
-        for (u32 i = lane; i < nidx; i += 32) {
-          const u32 idx = (u32)__ldg(tables + off + i);
-          bb ^= (recw[idx >> 5] >> (idx & 31)) & 1u;
+        for (u32 i0 = 0; i0 < nidx; i0 += 32) {   // warp-uniform trips (shuffles)
+          const u32 i = i0 + lane;
+          const u32 idx = i < nidx ? (u32)__ldg(tables + off + i) : 0u;
+          const u32 b = rec_bit(idx);
+          if (i < nidx) bb ^= b;
         }
         const u32 parity = __popc(__ballot_sync(FULL, bb)) & 1u;
         if (wkind == OP_DETECTOR) {
@@ -1282,20 +1317,42 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         q[Q_FIRE] = fire_pc;
       }
       u32 *qr = reinterpret_cast<u32 *>(q + Q_HDR);
+      if (rec_reg) {
+        if (lane < P.rec_words32) qr[lane] = rwl;
+      } else {
 #pragma unroll 1
-      for (u32 w = lane; leader && w < P.rec_words32; w += 32) qr[w] = recw[w];
+        for (u32 w = lane; leader && w < P.rec_words32; w += 32) qr[w] = recw[w];
+      }
       double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
 #pragma unroll 1
       for (u32 j = gl; j < (1u << kcur); j += NT) qc[j] = ldps(A, j, ps);
       (void)exit_pc;
     } else {
+      if (kReg) {
+        // lane i accumulates counter i (status, obs, mbytes are warp-uniform)
+        const bool pres = status == ST_PRESERVED;
+        u64 add = 0;
+        switch (lane) {
+          case WC_TOT: add = 1; break;
+          case WC_MB: add = mbytes; break;
+          case WC_PRES: add = pres; break;
+          case WC_ERR: add = pres && obs; break;
+          case WC_DISC: add = status == ST_DISCARDED; break;
+          case WC_OVF: add = status == ST_OVERFLOW; break;
+          case WC_COR: add = status == ST_CORRUPT; break;
+          case WC_UNS: add = !pres && status != ST_DISCARDED && status != ST_OVERFLOW &&
+                             status != ST_CORRUPT; break;
+          default: break;
+        }
+        cntl += add;
+      }
       if (gl == 0) {
-        wcnt[WC_TOT] += 1;
-        wcnt[WC_MB] += mbytes;
+        if (!kReg) wcnt[WC_TOT] += 1;
+        if (!kReg) wcnt[WC_MB] += mbytes;
         if (status == ST_PRESERVED) {
-          wcnt[WC_PRES] += 1;
+          if (!kReg) wcnt[WC_PRES] += 1;
           if (obs) {
-            wcnt[WC_ERR] += 1;
+            if (!kReg) wcnt[WC_ERR] += 1;
 #pragma unroll 1
             for (u64 o = obs; o; o &= o - 1)
               atomicAdd((unsigned long long *)&O.counters[GS_C_PER_OBS + (__ffsll((long long)o) - 1)], 1ull);
@@ -1304,6 +1361,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
               if (wi < O.witness_cap) O.witness[wi] = rng.shot;
             }
           }
+        } else if (kReg) {
         } else if (status == ST_DISCARDED) wcnt[WC_DISC] += 1;
         else if (status == ST_OVERFLOW) wcnt[WC_OVF] += 1;
         else if (status == ST_CORRUPT) wcnt[WC_COR] += 1;
@@ -1316,11 +1374,17 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           O.obs[sl] = obs;
         }
         const u32 rw64 = (P.nmeas + 63) / 64;
+        if (rec_reg) {   // <= 32 words: rw64 <= 16, one round
+          const u32 lo = __shfl_sync(FULL, rwl, (2 * lane) & 31);
+          const u32 hi = __shfl_sync(FULL, rwl, (2 * lane + 1) & 31);
+          if (lane < rw64) O.rec[sl * rw64 + lane] = ((u64)(2 * lane + 1 < P.rec_words32 ? hi : 0u) << 32) | lo;
+        } else {
 #pragma unroll 1
-        for (u32 w = lane; w < rw64; w += 32) {
-          const u32 lo = recw[2 * w];
-          const u32 hi = (2 * w + 1 < P.rec_words32) ? recw[2 * w + 1] : 0u;
-          O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
+          for (u32 w = lane; w < rw64; w += 32) {
+            const u32 lo = recw[2 * w];
+            const u32 hi = (2 * w + 1 < P.rec_words32) ? recw[2 * w + 1] : 0u;
+            O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
+          }
         }
         if (O.mode == MODE_DUMP) {
           if (lane == 0) {
@@ -1338,7 +1402,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     }
     gsync<kG>();
   }
-  flush_counters(O, wcnt, lane);
+  if (kReg) flush_counter_regs(O, cntl, lane);
+  else flush_counters(O, wcnt, lane);
 }
 
 // ---------------------------------------------------------------- section stats
