@@ -481,13 +481,19 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   KernelCfg KN4, KN5, KW;   // narrow launch shapes for sections needing 4 / 5 chi dims
   KN4.rec_in_smem = KN5.rec_in_smem = nrec_b <= 4096;
   KW.rec_in_smem = wrec_b <= 4096;
+  // the kn=5 build keeps counters and up to gs::kNarrowRecRegs record words
+  // in registers (rec_in_smem = 1 means "in registers" there): its slice is
+  // the 16 KB of chi rows alone, in blocks of up to GS_NARROW_WARPS_K5 warps
+  KN5.rec_in_smem = P.rec_words32 <= gs::kNarrowRecRegs;
   for (u32 kn : {4u, 5u}) {
     bool used = false;
     for (const Section &sc : secs) used |= !sc.wide && sc.kn == kn;
     if (!used) continue;
     KernelCfg &KN = kn == 5 ? KN5 : KN4;
-    const u32 wb = (u32)((gs::kCntBytes + gs::narrow_bytes(kn) + (KN.rec_in_smem ? nrec_b : 0) + 15) & ~(size_t)15);
-    rc = occupancy(e, wb, r->warps_per_block, 4,
+    const u32 wb = kn == 5 ? gs::narrow_bytes(5)
+                           : (u32)((gs::kCntBytes + gs::narrow_bytes(kn) + (KN.rec_in_smem ? nrec_b : 0) + 15) &
+                                   ~(size_t)15);
+    rc = occupancy(e, wb, r->warps_per_block, kn == 5 ? GS_NARROW_WARPS_K5 : 4,
                    [&](auto f) { return with_narrow_kernel(philox, kn == 5, f); }, KN);
     if (rc) return rc;
   }
@@ -536,7 +542,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 3 : KW.wpb) * chi);
     if (rc) return rc;
   }
-  if (!KN4.rec_in_smem || !KW.rec_in_smem) {
+  if (!KN4.rec_in_smem || !KN5.rec_in_smem || !KW.rec_in_smem) {
     rc = ensure_buf(&e->d_rec, &e->rec_bytes, (size_t)nwarps * nrec_b);
     if (rc) return rc;
   }

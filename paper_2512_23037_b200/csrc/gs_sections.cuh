@@ -24,8 +24,8 @@
 // what the instruction cache needs (B200: 32 KB L1.5).
 // GS_WIDE_ONLY runs the whole program as one wide section (A/B, tests).
 
-#ifndef GS_NARROW_BLOCKS_K5
-#define GS_NARROW_BLOCKS_K5 3
+#ifndef GS_NARROW_WARPS_K5
+#define GS_NARROW_WARPS_K5 14   // kn=5 narrow build: most warps per block (14 x 16 KB of chi rows)
 #endif
 #ifndef GS_NARROW_BLOCKS
 #define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
@@ -186,8 +186,16 @@ __device__ __noinline__ void narrow_dump_phase(double2 *amps, u32 n, u32 pn) {
 // shared memory the occupancy limit (3 blocks = 12 warps/SM), so it is
 // compiled for 3 resident blocks (more registers: no spills in the queue
 // reads); kn = 4 keeps 5 blocks = 20 warps/SM
+//
+// The kn = 5 build also keeps the warp's counters (lane i: counter i) and a
+// shot's record words (up to kNarrowRecRegs, one register each; indices are
+// warp-uniform, so the unrolled selects stay in registers) out of shared
+// memory: a warp's slice is its 16 KB of chi rows alone and 14 warps fit
+// an SM in 7-warp blocks instead of 12 (host: rec_in_smem = 1 means "record
+// words in registers" for this build)
+constexpr u32 kNarrowRecRegs = 4;   // 128 measurements
 template <bool kPhilox, bool kK5>
-__global__ void __launch_bounds__(128, kK5 ? GS_NARROW_BLOCKS_K5 : GS_NARROW_BLOCKS)
+__global__ void __launch_bounds__(kK5 ? 32 * GS_NARROW_WARPS_K5 : 128, kK5 ? 1 : GS_NARROW_BLOCKS)
 narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   extern __shared__ __align__(16) u8 smem[];
   const u32 lane = threadIdx.x & 31u;
@@ -195,11 +203,31 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   const u32 wpb = blockDim.x >> 5;
   const u64 gw = (u64)blockIdx.x * wpb + wib;
   u8 *mine = smem + (size_t)wib * O.warp_bytes;
-  unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(mine);
-  double2 *An = reinterpret_cast<double2 *>(mine + kCntBytes);
+  constexpr bool kReg = kK5;
+  const bool rec_reg = kReg && O.rec_in_smem;
+  u64 cntl = 0;                   // kReg: counter WC_[lane]
+  u32 rr[kNarrowRecRegs] = {};    // rec_reg: this lane's record words
+  unsigned long long *wcnt = kReg ? nullptr : reinterpret_cast<unsigned long long *>(mine);
+  double2 *An = reinterpret_cast<double2 *>(mine + (kReg ? 0u : kCntBytes));
   // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
-  u32 *recb = O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + narrow_bytes(S.kn))
-                            : O.grec + gw * (u64)P.rec_words32 * 32u;
+  u32 *recb = rec_reg ? nullptr
+              : (O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + narrow_bytes(S.kn))
+                               : O.grec + gw * (u64)P.rec_words32 * 32u);
+  // record word w (warp-uniform) of this lane's shot
+  auto rec_get = [&](u32 w) -> u32 {
+    if (!rec_reg) return recb[w * 32u + lane];
+    u32 v = 0;
+#pragma unroll
+    for (u32 i = 0; i < kNarrowRecRegs; ++i)
+      if (i == w) v = rr[i];
+    return v;
+  };
+  auto rec_set = [&](u32 w, u32 v) {
+    if (!rec_reg) { recb[w * 32u + lane] = v; return; }
+#pragma unroll
+    for (u32 i = 0; i < kNarrowRecRegs; ++i)
+      if (i == w) rr[i] = v;
+  };
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
   const u64 *__restrict__ tables = P.tables;
@@ -210,7 +238,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   const u32 SU = slot_u64(P);
 #define AN(j) An[(j) * 32u + lane]
 
-  if (lane < WC_N) wcnt[lane] = 0;
+  if (!kReg && lane < WC_N) wcnt[lane] = 0;
   __syncwarp();
   const u64 total = S.q_in ? (u64)*S.n_in : S.count;
 
@@ -240,7 +268,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       shot = R.shot_begin + sl;
       if (valid && !philox) seed = R.seeds ? R.seeds[sl] : sha1_seed(R.master, shot);
 #pragma unroll 1
-      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = 0;
+      for (u32 w = 0; w < P.rec_words32; ++w) rec_set(w, 0u);
       AN(0) = make_double2(1.0, 0.0);
       sone = true;
       if (philox && valid && P.geo_len > 1 && P.nlocs) {
@@ -261,7 +289,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       sfire = (u32)q[Q_FIRE];
       const u32 *qr = reinterpret_cast<const u32 *>(q + Q_HDR);
 #pragma unroll 1
-      for (u32 w = 0; w < P.rec_words32; ++w) recb[w * 32u + lane] = __ldg(qr + w);
+      for (u32 w = 0; w < P.rec_words32; ++w) rec_set(w, __ldg(qr + w));
       // chi rows: every lane reads its own slot (a strided gather across
       // the warp), so keep several loads in flight per lane instead of one
       const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
@@ -572,7 +600,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         const u32 bout = plus ? 0u : 1u;
         u32 rb = bout;
         if ((fl & MF_FLIP) && draw53(seed, R.master, shot, udraw + 1, philox) < __ldg(op + 14)) rb ^= 1u;
-        if ((fl & MF_RECORD) && rb) recb[(slot >> 5) * 32u + lane] |= 1u << (slot & 31);
+        if ((fl & MF_RECORD) && rb) rec_set(slot >> 5, rec_get(slot >> 5) | (1u << (slot & 31)));
         if ((fl & MF_RESET) && bout) { s_lo ^= __ldg(op + 15); s_hi ^= __ldg(op + 16); }
         continue;
       }
@@ -580,7 +608,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       // @region narrow: feedback/detector/end
       if (kind == OP_FEEDBACK) {
         const u32 idx = (u32)__ldg(op + 1);
-        if ((recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u) {
+        if ((rec_get(idx >> 5) >> (idx & 31)) & 1u) {
           s_lo ^= __ldg(op + 2);
           s_hi ^= __ldg(op + 3);
           smb += __ldg(op + 4);
@@ -596,7 +624,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 #pragma unroll 1
         for (u32 i = 0; i < nidx; ++i) {
           const u32 idx = (u32)__ldg(tables + off + i);
-          parity ^= (recb[(idx >> 5) * 32u + lane] >> (idx & 31)) & 1u;
+          parity ^= (rec_get(idx >> 5) >> (idx & 31)) & 1u;
         }
         if (kind == OP_DETECTOR) {
           if ((R.flags & GS_POSTSELECT) && parity) { sst = ST_DISCARDED; saux = (int)id; }
@@ -634,7 +662,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         q[Q_FIRE] = sfire;
         u32 *qr = reinterpret_cast<u32 *>(q + Q_HDR);
 #pragma unroll 1
-        for (u32 w = 0; w < P.rec_words32; ++w) qr[w] = recb[w * 32u + lane];
+        for (u32 w = 0; w < P.rec_words32; ++w) qr[w] = rec_get(w);
         double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
 #pragma unroll 1
         for (u32 j = 0; j < (1u << exit_k); ++j) qc[j] = AN(j);
@@ -652,7 +680,20 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       u64 mb = fin ? smb : 0ull;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mb += __shfl_xor_sync(FULL, mb, o);
-      if (lane == 0) {
+      if (kReg) {   // lane i accumulates counter i
+        u32 m = 0;
+        switch (lane) {
+          case WC_TOT: m = val; break;
+          case WC_PRES: m = pres; break;
+          case WC_DISC: m = disc; break;
+          case WC_OVF: m = ovf; break;
+          case WC_COR: m = cor; break;
+          case WC_UNS: m = uns; break;
+          case WC_ERR: m = errb; break;
+          default: break;
+        }
+        cntl += lane == WC_MB ? mb : (u64)__popc(m);
+      } else if (lane == 0) {
         wcnt[WC_TOT] += __popc(val);
         wcnt[WC_PRES] += __popc(pres);
         wcnt[WC_DISC] += __popc(disc);
@@ -680,8 +721,8 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         const u32 rw64 = (P.nmeas + 63) / 64;
 #pragma unroll 1
         for (u32 w = 0; w < rw64; ++w) {
-          const u32 lo = recb[(2 * w) * 32u + lane];
-          const u32 hi = (2 * w + 1 < P.rec_words32) ? recb[(2 * w + 1) * 32u + lane] : 0u;
+          const u32 lo = rec_get(2 * w);
+          const u32 hi = (2 * w + 1 < P.rec_words32) ? rec_get(2 * w + 1) : 0u;
           O.rec[sl * rw64 + w] = ((u64)hi << 32) | lo;
         }
         if (O.mode == MODE_DUMP) {
@@ -699,7 +740,8 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     __syncwarp();
   }
 #undef AN
-  flush_counters(O, wcnt, lane);
+  if (kReg) flush_counter_regs(O, cntl, lane);
+  else flush_counters(O, wcnt, lane);
 }
 
 // ---------------------------------------------------------------- wide

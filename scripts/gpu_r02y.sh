@@ -1,4 +1,4 @@
-# r02y: warp form with counters / record words in registers (14 warps/SM at k=10): GPU tests + A/B vs HEAD
+# r02y/r02z: register-resident shot state (A/B vs HEAD) + GPU tests
 set -x
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_r02y.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_r02y.log

@@ -1,0 +1,11 @@
+# r02z/r02z: register-resident shot state (A/B vs HEAD) + GPU tests
+set -x
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_r02z.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_r02z.log
+TAG=r02z bash scripts/gpu_ab_tree.sh
+for w in msc_d3 msc_d5_grown msc_d5_2check; do
+  (cd _ab_base && timeout 300 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --e2e-waves 1 > ../gpurun_out/ab_r02z_base_$w.json 2>/dev/null)
+  timeout 300 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --e2e-waves 1 > gpurun_out/ab_r02z_new_$w.json 2>/dev/null
+  echo "$w base $(python -c "import json;print(json.load(open('gpurun_out/ab_r02z_base_$w.json'))['value'])") new $(python -c "import json;print(json.load(open('gpurun_out/ab_r02z_new_$w.json'))['value'])")" >> gpurun_out/ab_r02z.txt
+done
+cat gpurun_out/ab_r02z.txt
