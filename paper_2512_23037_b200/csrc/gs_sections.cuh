@@ -1259,27 +1259,26 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
               sweep_pivot_part<kSmemChi, kG>(A, g, xpp, plus, size);
               gsync<kG>();
               defer_scale(inv_sqrt_norm(nrm0), nrm0);
-              goto pivot_signs;
-            }
-            const SumNz w = sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
-            ps = 1.0;
-            gsync<kG>();
-            const double sk = group_sum<kG>(w.sum, grp);
-            cnt = group_sum_u32<kG>(w.nz, grp);
-            if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
-            const double rs = inv_sqrt_norm(sk);
-            if (g.span) {
-              const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
-              gsync<kG>();
-              cnt = group_sum_u32<kG>(r.nz, grp);
-              nrm_l = r.sum;
-              nrm_lane0 = false;
-              kcur = wk - 1;
             } else {
-              defer_scale(rs, sk);
+              const SumNz w = sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
+              ps = 1.0;
+              gsync<kG>();
+              const double sk = group_sum<kG>(w.sum, grp);
+              cnt = group_sum_u32<kG>(w.nz, grp);
+              if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
+              const double rs = inv_sqrt_norm(sk);
+              if (g.span) {
+                const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
+                gsync<kG>();
+                cnt = group_sum_u32<kG>(r.nz, grp);
+                nrm_l = r.sum;
+                nrm_lane0 = false;
+                kcur = wk - 1;
+              } else {
+                defer_scale(rs, sk);
+              }
             }
           }
-        pivot_signs:
           if (g.ct) c ^= vec;
           // tableau sign update of the pivot (ref tableau.py:176-200)
           const u32 v = (u32)(sig_hi >> t) & 1u;
