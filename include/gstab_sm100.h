@@ -203,7 +203,8 @@ int gs_engine_trim(gs_engine *eng);
    on the caller's.  Launches are ordered across streams by the engine (an
    event recorded after each run is waited on by the next run's stream), so
    mixing the two is safe; concurrent calls from several host threads on
-   one engine are not supported. */
+   one engine are not supported (the Python Engine serialises its calls
+   with a lock, so its process-wide engines are thread-safe). */
 
 /* diagnostics */
 const char *gs_last_error(void);

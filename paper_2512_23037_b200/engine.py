@@ -66,11 +66,12 @@ class Program:
             cache[key] = 0          # every op is narrow at either limit
             return 0
         times = {}
-        for extra in (0, _lib.GS_NARROW_K5):
-            par = Engine.params(0x7E57, 1 << 40, self.TUNE_SHOTS, capacity, flags | extra)
-            engine.run_counters(self, par)            # warm-up (queues, occupancy)
-            engine.run_counters(self, par)
-            times[extra] = engine.last_kernel_ms
+        with engine.lock:
+            for extra in (0, _lib.GS_NARROW_K5):
+                par = Engine.params(0x7E57, 1 << 40, self.TUNE_SHOTS, capacity, flags | extra)
+                engine.run_counters(self, par)            # warm-up (queues, occupancy)
+                engine.run_counters(self, par)
+                times[extra] = engine.last_kernel_ms
         best = min(times, key=times.get)
         cache[key] = best
         self.narrow_tuning = {"k4_ms": times[0], "k5_ms": times[_lib.GS_NARROW_K5],
@@ -109,7 +110,13 @@ class Program:
 
 
 class Engine:
-    """A device context of the sampler (streams, scratch, counters)."""
+    """A device context of the sampler (streams, scratch, counters).
+
+    The C engine's scratch is shared by its runs and the C ABI does not
+    support concurrent calls on one engine (include/gstab_sm100.h); ctypes
+    releases the GIL during a call, so every entry point here holds the
+    engine's lock -- ``get_engine``'s process-wide engines are safe to use
+    from several Python threads (their runs are serialised)."""
 
     def __init__(self, device: int = 0):
         lib = _lib.load()
@@ -117,6 +124,7 @@ class Engine:
         _lib.check(lib.gs_engine_create(int(device), ct.byref(h)))
         self.handle = h
         self.device = device
+        self.lock = threading.RLock()
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -150,9 +158,10 @@ class Engine:
 
     def run_counters(self, prog: Program, params) -> np.ndarray:
         out = np.zeros(prog.num_counters, dtype=np.int64)
-        _lib.check(_lib.load().gs_run_counters(
-            self.handle, prog.handle, ct.byref(params),
-            out.ctypes.data_as(ct.POINTER(ct.c_int64))))
+        with self.lock:
+            _lib.check(_lib.load().gs_run_counters(
+                self.handle, prog.handle, ct.byref(params),
+                out.ctypes.data_as(ct.POINTER(ct.c_int64))))
         return out
 
     def run_counters_witness(self, prog: Program, params, cap: int):
@@ -161,17 +170,19 @@ class Engine:
         out = np.zeros(prog.num_counters, dtype=np.int64)
         wit = np.zeros(max(cap, 1), dtype=np.uint64)
         found = ct.c_uint32(0)
-        _lib.check(_lib.load().gs_run_counters_witness(
-            self.handle, prog.handle, ct.byref(params),
-            out.ctypes.data_as(ct.POINTER(ct.c_int64)), wit.ctypes.data, cap,
-            ct.byref(found)))
+        with self.lock:
+            _lib.check(_lib.load().gs_run_counters_witness(
+                self.handle, prog.handle, ct.byref(params),
+                out.ctypes.data_as(ct.POINTER(ct.c_int64)), wit.ctypes.data, cap,
+                ct.byref(found)))
         return out, np.sort(wit[:min(cap, found.value)]), int(found.value)
 
     def run_counters_async(self, prog: Program, params, counters_dev_ptr: int,
                            stream_ptr: int) -> None:
-        _lib.check(_lib.load().gs_run_counters_async(
-            self.handle, prog.handle, ct.byref(params),
-            ct.c_void_p(counters_dev_ptr), ct.c_void_p(stream_ptr)))
+        with self.lock:
+            _lib.check(_lib.load().gs_run_counters_async(
+                self.handle, prog.handle, ct.byref(params),
+                ct.c_void_p(counters_dev_ptr), ct.c_void_p(stream_ptr)))
 
     def run_records(self, prog: Program, params):
         S = params.shot_count
@@ -180,9 +191,10 @@ class Engine:
         aux = np.zeros(max(S, 1), dtype=np.int32)
         rec = np.zeros((max(S, 1), max(rw, 1)), dtype=np.uint64)
         obs = np.zeros(max(S, 1), dtype=np.uint64)
-        _lib.check(_lib.load().gs_run_records(
-            self.handle, prog.handle, ct.byref(params), status.ctypes.data,
-            aux.ctypes.data, rec.ctypes.data, obs.ctypes.data))
+        with self.lock:
+            _lib.check(_lib.load().gs_run_records(
+                self.handle, prog.handle, ct.byref(params), status.ctypes.data,
+                aux.ctypes.data, rec.ctypes.data, obs.ctypes.data))
         return status[:S], aux[:S], rec[:S, :rw], obs[:S]
 
     def dump(self, prog: Program, params):
@@ -197,10 +209,11 @@ class Engine:
         cv = np.zeros(max(S, 1), dtype=np.uint64)
         amps = np.zeros((max(S, 1), stride, 2), dtype=np.float64)
         dim = np.zeros(max(S, 1), dtype=np.uint32)
-        _lib.check(_lib.load().gs_dump_shots(
-            self.handle, prog.handle, ct.byref(params), status.ctypes.data,
-            aux.ctypes.data, rec.ctypes.data, obs.ctypes.data, sig.ctypes.data,
-            cv.ctypes.data, amps.ctypes.data, dim.ctypes.data))
+        with self.lock:
+            _lib.check(_lib.load().gs_dump_shots(
+                self.handle, prog.handle, ct.byref(params), status.ctypes.data,
+                aux.ctypes.data, rec.ctypes.data, obs.ctypes.data, sig.ctypes.data,
+                cv.ctypes.data, amps.ctypes.data, dim.ctypes.data))
         return {"status": status[:S], "aux": aux[:S], "rec": rec[:S, :rw],
                 "obs": obs[:S], "sig": sig[:S], "c": cv[:S],
                 "amps": amps[:S, :, 0] + 1j * amps[:S, :, 1], "dim": dim[:S]}
@@ -210,11 +223,13 @@ class Engine:
     def set_queue_budget(self, bytes_per_queue: int) -> None:
         """Inter-section queue budget per queue (0 = auto: min(8 GiB, 1/16
         of free device memory)); larger runs are chunked, same results."""
-        _lib.check(_lib.load().gs_engine_set_queue_budget(self.handle, int(bytes_per_queue)))
+        with self.lock:
+            _lib.check(_lib.load().gs_engine_set_queue_budget(self.handle, int(bytes_per_queue)))
 
     def trim(self) -> None:
         """Free the engine's scratch buffers (re-allocated on demand)."""
-        _lib.check(_lib.load().gs_engine_trim(self.handle))
+        with self.lock:
+            _lib.check(_lib.load().gs_engine_trim(self.handle))
 
     # -- diagnostics --------------------------------------------------
 
@@ -225,8 +240,9 @@ class Engine:
         cap = 256
         out = np.zeros(cap * _lib.GS_SEC_FIELDS, dtype=np.uint64)
         n = ct.c_uint32(0)
-        _lib.check(_lib.load().gs_engine_section_stats(
-            self.handle, out.ctypes.data, cap, ct.byref(n), int(reset)))
+        with self.lock:
+            _lib.check(_lib.load().gs_engine_section_stats(
+                self.handle, out.ctypes.data, cap, ct.byref(n), int(reset)))
         rows = out[:min(n.value, cap) * _lib.GS_SEC_FIELDS].reshape(-1, _lib.GS_SEC_FIELDS)
         return [{"shots_in": int(r[_lib.GS_SEC_SHOTS_IN]),
                  "shots_out": int(r[_lib.GS_SEC_SHOTS_OUT]),

@@ -293,6 +293,11 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     t0 = time.perf_counter()
     p = _program_for(prog, cfg.dim_limit)
     eng = engine or get_engine(cfg.device)
+    with eng.lock:   # the waves and their device times, not interleaved with other threads
+        return _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0)
+
+
+def _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0):
     flags = cfg.run_flags() | tuned_flags(p, eng, cfg)
     total = np.zeros(p.num_counters, dtype=np.int64)
     wit: list = []

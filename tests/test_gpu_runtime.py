@@ -176,3 +176,29 @@ def test_narrow_limit_tuning_is_cached_and_result_neutral():
     assert (got[0] == got[1]).all()
     st = run_batch(prog, cfg)
     assert st.total_shots == cfg.shots and st.preserved_shots == int(got[0][_lib.GS_C_PRESERVED])
+
+
+def test_shared_engine_is_safe_across_python_threads():
+    """get_engine's process-wide engine is shared: runs from several Python
+    threads are serialised by its lock (ctypes releases the GIL) and every
+    thread gets the counters a lone run gives."""
+    import threading
+    from paper_2512_23037_b200 import SamplerConfig, parse_circuit, run_batch
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(parse_circuit("H 0 1 2\nT 0 1\nCX 0 2\nT_DAG 2\nM 0 1 2\n"
+                                           "DETECTOR rec[-1] rec[-3]\n"), 0.01)
+    cfg = SamplerConfig(shots=300_000, master_seed=8, postselect=True, rng="philox")
+    want = run_batch(prog, cfg).as_dict()
+    got = [None] * 6
+
+    def work(i):
+        got[i] = run_batch(prog, cfg).as_dict()
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for g in got:
+        for k in ("total_shots", "preserved_shots", "discarded_shots", "logical_error_shots"):
+            assert g[k] == want[k], (k, g[k], want[k])
