@@ -51,7 +51,9 @@ struct DevOut {
   u32 *grec;            // global record scratch (per warp) when not in smem
   u32 mode;
   u32 warp_bytes;       // dynamic smem bytes per warp
-  u32 rec_in_smem;
+  u32 rec_local;        // record words kept warp-locally: in the slice's shared memory
+                        // (narrow kn=4, block form) or in registers (warp form, narrow
+                        // kn=5); else in the global O.grec buffer
   u32 chi_off;          // wide kernel: byte offset of chi in the warp's smem slice
   u64 *witness;         // optional: global indices of preserved shots with a
   u32 *witness_count;   //   flipped observable (paper §V-B witnesses)

@@ -341,7 +341,7 @@ static cudaError_t with_wide_kernel(bool smem_chi, bool philox, u32 gw, F f) {
 }
 
 struct KernelCfg {
-  u32 wpb = 1, blocks = 1, warp_bytes = 0, chi_off = 0, rec_in_smem = 0;
+  u32 wpb = 1, blocks = 1, warp_bytes = 0, chi_off = 0, rec_local = 0;
   size_t smem = 0;
 };
 
@@ -479,19 +479,19 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   else smem_chi = chi <= 32 * 1024;
   const size_t nrec_b = (size_t)P.rec_words32 * 4 * 32, wrec_b = (size_t)P.rec_words32 * 4;
   KernelCfg KN4, KN5, KW;   // narrow launch shapes for sections needing 4 / 5 chi dims
-  KN4.rec_in_smem = KN5.rec_in_smem = nrec_b <= 4096;
-  KW.rec_in_smem = wrec_b <= 4096;
+  KN4.rec_local = KN5.rec_local = nrec_b <= 4096;
+  KW.rec_local = wrec_b <= 4096;
   // the kn=5 build keeps counters and up to gs::kNarrowRecRegs record words
-  // in registers (rec_in_smem = 1 means "in registers" there): its slice is
+  // in registers (rec_local = 1 means "in registers" there): its slice is
   // the 16 KB of chi rows alone, in blocks of up to GS_NARROW_WARPS_K5 warps
-  KN5.rec_in_smem = P.rec_words32 <= gs::kNarrowRecRegs;
+  KN5.rec_local = P.rec_words32 <= gs::kNarrowRecRegs;
   for (u32 kn : {4u, 5u}) {
     bool used = false;
     for (const Section &sc : secs) used |= !sc.wide && sc.kn == kn;
     if (!used) continue;
     KernelCfg &KN = kn == 5 ? KN5 : KN4;
     const u32 wb = kn == 5 ? gs::narrow_bytes(5)
-                           : (u32)((gs::kCntBytes + gs::narrow_bytes(kn) + (KN.rec_in_smem ? nrec_b : 0) + 15) &
+                           : (u32)((gs::kCntBytes + gs::narrow_bytes(kn) + (KN.rec_local ? nrec_b : 0) + 15) &
                                    ~(size_t)15);
     rc = occupancy(e, wb, r->warps_per_block, kn == 5 ? GS_NARROW_WARPS_K5 : 4,
                    [&](auto f) { return with_narrow_kernel(philox, kn == 5, f); }, KN);
@@ -499,9 +499,9 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   }
   if (any_wide && !block) {
     // warp form: counters and up to 32 record words in registers
-    // (rec_in_smem = 1 means "in registers" here), the SplitMix fire-bit
+    // (rec_local = 1 means "in registers" here), the SplitMix fire-bit
     // ring in shared memory, then chi
-    KW.rec_in_smem = P.rec_words32 <= 32;
+    KW.rec_local = P.rec_words32 <= 32;
     size_t base = philox ? 0 : gs::kWinBytes;
     KW.chi_off = (u32)base;
     const u32 wb = (u32)(base + (smem_chi ? chi : 0));
@@ -515,7 +515,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   }
   if (any_wide && block) {
     // [per-warp slices][group scratch: 2 x 32 u64][chi]
-    const size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_in_smem ? ((wrec_b + 15) & ~(size_t)15) : 0);
+    const size_t base = gs::kCntBytes + gs::kWinBytes + (KW.rec_local ? ((wrec_b + 15) & ~(size_t)15) : 0);
     const size_t head = (size_t)gwarps * base + 64 * sizeof(u64);
     if (smem_chi && head + chi > e->smem_optin) smem_chi = false;
     KW.wpb = gwarps;
@@ -542,7 +542,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 3 : KW.wpb) * chi);
     if (rc) return rc;
   }
-  if (!KN4.rec_in_smem || !KN5.rec_in_smem || !KW.rec_in_smem) {
+  if (!KN4.rec_local || !KN5.rec_local || !KW.rec_local) {
     rc = ensure_buf(&e->d_rec, &e->rec_bytes, (size_t)nwarps * nrec_b);
     if (rc) return rc;
   }
@@ -636,7 +636,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
         if (secs[i].wide) {
           gs::DevOut Ow = O;
           Ow.warp_bytes = KW.warp_bytes;
-          Ow.rec_in_smem = KW.rec_in_smem;
+          Ow.rec_local = KW.rec_local;
           Ow.chi_off = KW.chi_off;
           CUDA_TRY(with_wide_kernel(smem_chi, philox, gwarps, [&](auto kern) {
             kern<<<KW.blocks, KW.wpb * 32, KW.smem, st>>>(P, R, Ow, S);
@@ -646,7 +646,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
           const KernelCfg &KN = secs[i].kn == 5 ? KN5 : KN4;
           gs::DevOut On = O;
           On.warp_bytes = KN.warp_bytes;
-          On.rec_in_smem = KN.rec_in_smem;
+          On.rec_local = KN.rec_local;
           On.chi_off = 0;
           CUDA_TRY(with_narrow_kernel(philox, secs[i].kn == 5, [&](auto kern) {
             kern<<<KN.blocks, KN.wpb * 32, KN.smem, st>>>(P, R, On, S);

@@ -191,7 +191,7 @@ __device__ __noinline__ void narrow_dump_phase(double2 *amps, u32 n, u32 pn) {
 // shot's record words (up to kNarrowRecRegs, one register each; indices are
 // warp-uniform, so the unrolled selects stay in registers) out of shared
 // memory: a warp's slice is its 16 KB of chi rows alone and 14 warps fit
-// an SM in 7-warp blocks instead of 12 (host: rec_in_smem = 1 means "record
+// an SM in 7-warp blocks instead of 12 (host: rec_local = 1 means "record
 // words in registers" for this build)
 constexpr u32 kNarrowRecRegs = 4;   // 128 measurements
 template <bool kPhilox, bool kK5>
@@ -204,14 +204,14 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   const u64 gw = (u64)blockIdx.x * wpb + wib;
   u8 *mine = smem + (size_t)wib * O.warp_bytes;
   constexpr bool kReg = kK5;
-  const bool rec_reg = kReg && O.rec_in_smem;
+  const bool rec_reg = kReg && O.rec_local;
   u64 cntl = 0;                   // kReg: counter WC_[lane]
   u32 rr[kNarrowRecRegs] = {};    // rec_reg: this lane's record words
   unsigned long long *wcnt = kReg ? nullptr : reinterpret_cast<unsigned long long *>(mine);
   double2 *An = reinterpret_cast<double2 *>(mine + (kReg ? 0u : kCntBytes));
   // record bits, one column per lane: word w of lane l at recb[w * 32 + l]
   u32 *recb = rec_reg ? nullptr
-              : (O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + narrow_bytes(S.kn))
+              : (O.rec_local ? reinterpret_cast<u32 *>(mine + kCntBytes + narrow_bytes(S.kn))
                                : O.grec + gw * (u64)P.rec_words32 * 32u);
   // record word w (warp-uniform) of this lane's shot
   auto rec_get = [&](u32 w) -> u32 {
@@ -766,17 +766,17 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   // warp form (kReg): the shot counters and (up to 32) record words live in
   // registers -- lane i holds counter i and record word i -- so a warp's
   // shared-memory slice is chi alone (plus the SplitMix fire-bit ring) and
-  // 14 warps fit an SM at 16 KB of chi instead of 13 (host: rec_in_smem = 1
+  // 14 warps fit an SM at 16 KB of chi instead of 13 (host: rec_local = 1
   // means "record words in registers" for this form); the block form keeps
   // both in its per-warp slices
   constexpr bool kReg = kG == 1;
-  const bool rec_reg = kReg && O.rec_in_smem;
+  const bool rec_reg = kReg && O.rec_local;
   u64 cntl = 0;   // kReg: counter WC_[lane]
   u32 rwl = 0;    // rec_reg: record word [lane]
   unsigned long long *wcnt = kReg ? nullptr : reinterpret_cast<unsigned long long *>(mine);
   u32 *win = reinterpret_cast<u32 *>(mine + (kReg ? 0u : kCntBytes));
   u32 *recw = rec_reg ? nullptr
-              : (O.rec_in_smem ? reinterpret_cast<u32 *>(mine + kCntBytes + kWinBytes)
+              : (O.rec_local ? reinterpret_cast<u32 *>(mine + kCntBytes + kWinBytes)
                                : O.grec + gw * (u64)P.rec_words32);
   // block form: per-warp slices, then the group scratch, then chi
   const u32 gl = glane<kG>();
