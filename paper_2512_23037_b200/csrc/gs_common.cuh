@@ -237,12 +237,16 @@ __device__ __noinline__ u64 sha1_seed(u64 master, u64 shot) {
   return ((u64)bswap32(h1) << 32) | bswap32(h0);
 }
 
-__device__ __forceinline__ u64 splitmix(u64 seed, u32 k) {
-  u64 z = seed + (u64)(k + 1ull) * 0x9E3779B97F4A7C15ull;
+constexpr u64 kSplitGamma = 0x9E3779B97F4A7C15ull;
+// SplitMix64 draw k = mix(seed + (k + 1) gamma), split so a run of draws can
+// step the pre-mix counter by additions
+__device__ __forceinline__ u64 splitmix_pre(u64 seed, u32 k) { return seed + (u64)(k + 1ull) * kSplitGamma; }
+__device__ __forceinline__ u64 splitmix_mix(u64 z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+__device__ __forceinline__ u64 splitmix(u64 seed, u32 k) { return splitmix_mix(splitmix_pre(seed, k)); }
 
 // Philox4x32-10, key = master seed, counter = (c0, c1, shot lo, shot hi)
 __device__ __forceinline__ uint4 philox4(u32 c0, u32 c1, u64 shot, u64 master) {

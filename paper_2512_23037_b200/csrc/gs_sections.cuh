@@ -345,14 +345,24 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           if (sst != ST_RUNNING) continue;
           const u32 nloc = (u32)(nw0 >> 32), loc0 = (u32)__ldg(nrec + 1);
           u64 ex = 0, ez = 0;
+          // one instruction's locations share their kind and threshold and
+          // draw at d0, d0 + step, ... (compiler.py emit_noise; DEPOLARIZE
+          // draws twice per location), so the fire test walks SplitMix's
+          // pre-mix counter z = seed + (d + 1) gamma by additions and loads a
+          // location word only when it fires (same draws, same bits)
+          if (nloc) {
+            const u64 lw0 = __ldg(locs + 2ull * loc0), thr = __ldg(locs + 2ull * loc0 + 1);
+            const u32 step = (((u32)(lw0 >> 48) & 3) <= NK_DEP2) ? 2u : 1u;
+            u64 z = splitmix_pre(seed, (u32)lw0);
+            const u64 dz = (u64)step * kSplitGamma;
 #pragma unroll 1
-          for (u32 l = loc0; l < loc0 + nloc; ++l) {
-            const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
-            const u32 d = (u32)lw;
-            if ((splitmix(seed, d) >> 11) < thr) {
-              const u32 nk = (u32)(lw >> 48) & 3;
-              const double u = nk <= NK_DEP2 ? (double)(splitmix(seed, d + 1) >> 11) * 0x1.0p-53 : 0.0;
-              noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+            for (u32 l = loc0; l < loc0 + nloc; ++l, z += dz) {
+              if ((splitmix_mix(z) >> 11) < thr) {
+                const u64 lw = __ldg(locs + 2ull * l);
+                const u32 nk = (u32)(lw >> 48) & 3;
+                const double u = nk <= NK_DEP2 ? (double)(splitmix_mix(z + kSplitGamma) >> 11) * 0x1.0p-53 : 0.0;
+                noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+              }
             }
           }
           if (ex | ez) lane_error(ex, ez, nrec, size);
