@@ -446,7 +446,7 @@ def main():
     import torch.distributed as dist
     from paper_2512_23037_b200 import _lib
     from paper_2512_23037_b200.compiler import compile_program
-    from paper_2512_23037_b200.engine import Engine, Program
+    from paper_2512_23037_b200.engine import Engine, Program, get_engine
 
     dev = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(dev)
@@ -462,7 +462,7 @@ def main():
         print(P.sections((_lib.GS_WIDE_ONLY if args.wide_only else 0) |
                          (_lib.GS_NARROW_K5 if args.narrow_k == "5" else 0)))
         return 0
-    eng = Engine(dev)
+    eng = get_engine(dev)   # the process-wide engine run_batch (e2e) also uses
     flags = _lib.GS_POSTSELECT | (_lib.GS_RNG_PHILOX if args.rng == "philox" else 0)
     if args.chi_global:
         flags |= _lib.GS_CHI_GLOBAL
