@@ -957,52 +957,67 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             apply_error(ex, ez, nrec);
           }
         } else {
-          // SplitMix: one fire draw per location, 32 locations per ballot
-          while (scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= wpc) {
-            const u32 l = scanned * 32u + lane;
-            bool fire = false;
-            if (l < P.nlocs) {
-              const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
-              fire = rng.m53((u32)lw) < thr;
-            }
-            const u32 bits = __ballot_sync(FULL, fire);
-            if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
-            ++scanned;
-          }
-          __syncwarp();
-          next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
-          fire_pc = 0xFFFFFFFFu;
-#pragma unroll 1
+          // SplitMix: one fire draw per location, 32 locations per ballot,
+          // into a ring of kWinWords fire-bit words.  A stretch of more than
+          // kWinWords words inserted before one op is scanned in bounded
+          // steps: the words still to be read lie at or above `low` (the
+          // search resumes at max(search_w, cursor / 32), and the owner of a
+          // fire found there starts at most 33 words earlier -- <= 1024
+          // locations per instruction, compiler.py), and an instruction is
+          // applied only once all its words are scanned
           for (;;) {
-            // next fired location >= cursor among the scanned words
-            u32 fl_loc = 0xFFFFFFFFu;
-            u32 w = max(search_w, cursor >> 5);
-#pragma unroll 1
-            for (; w < scanned; ++w) {
-              u32 bits = win[w & (kWinWords - 1)];
-              if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
-              if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+            const u32 low = max(cursor >> 5, search_w > 33u ? search_w - 33u : 0u);
+            while (scanned < P.nwords && scanned - low < (u32)kWinWords &&
+                   __ldg(tables + P.wordpc_off + scanned) <= wpc) {
+              const u32 l = scanned * 32u + lane;
+              bool fire = false;
+              if (l < P.nlocs) {
+                const u64 lw = __ldg(locs + 2ull * l), thr = __ldg(locs + 2ull * l + 1);
+                fire = rng.m53((u32)lw) < thr;
+              }
+              const u32 bits = __ballot_sync(FULL, fire);
+              if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+              ++scanned;
             }
-            search_w = w;
-            if (fl_loc == 0xFFFFFFFFu) break;
-            const u64 *nrec = noise_owner(P, fl_loc);
-            const u64 nw0 = __ldg(nrec);
-            const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
-            if (ipc > wpc) { fire_pc = ipc; break; }
-            const u32 loc0 = (u32)__ldg(nrec + 1);
-            cursor = loc0 + nloc;
-            u64 ex = 0, ez = 0;
+            __syncwarp();
+            fire_pc = 0xFFFFFFFFu;
+            bool need_scan = false;
 #pragma unroll 1
-            for (u32 i = lane; i < nloc; i += 32) {
-              const u32 l = loc0 + i;
-              if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
-              const u64 lw = __ldg(locs + 2ull * l);
-              const u32 nk = (u32)(lw >> 48) & 3;
-              const double u = nk <= NK_DEP2 ? rng.uniform((u32)lw + 1) : 0.0;
-              noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+            for (;;) {
+              // next fired location >= cursor among the scanned words
+              u32 fl_loc = 0xFFFFFFFFu;
+              u32 w = max(search_w, cursor >> 5);
+#pragma unroll 1
+              for (; w < scanned; ++w) {
+                u32 bits = win[w & (kWinWords - 1)];
+                if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
+                if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
+              }
+              search_w = w;
+              if (fl_loc == 0xFFFFFFFFu) break;
+              const u64 *nrec = noise_owner(P, fl_loc);
+              const u64 nw0 = __ldg(nrec);
+              const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
+              if (ipc > wpc) { fire_pc = ipc; break; }
+              const u32 loc0 = (u32)__ldg(nrec + 1);
+              if (((loc0 + nloc + 31u) >> 5) > scanned) { need_scan = true; break; }
+              cursor = loc0 + nloc;
+              u64 ex = 0, ez = 0;
+#pragma unroll 1
+              for (u32 i = lane; i < nloc; i += 32) {
+                const u32 l = loc0 + i;
+                if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+                const u64 lw = __ldg(locs + 2ull * l);
+                const u32 nk = (u32)(lw >> 48) & 3;
+                const double u = nk <= NK_DEP2 ? rng.uniform((u32)lw + 1) : 0.0;
+                noise_letter(nk, (u32)(lw >> 32) & 0xff, (u32)(lw >> 40) & 0xff, u, ex, ez);
+              }
+              apply_error(warp_or64(ex), warp_or64(ez), nrec);
             }
-            apply_error(warp_or64(ex), warp_or64(ez), nrec);
+            const bool more = scanned < P.nwords && __ldg(tables + P.wordpc_off + scanned) <= wpc;
+            if (!more && !need_scan) break;
           }
+          next_word_pc = scanned < P.nwords ? (u32)__ldg(tables + P.wordpc_off + scanned) : 0xFFFFFFFFu;
         }
       }
 

@@ -127,3 +127,46 @@ def test_cancelled_t_span_beyond_dim_limit_is_loud_then_runs():
     _check(prog, 5, 8, dict(max_dim=22, postselect=True), 32768)
     st = run_batch(prog, SamplerConfig(shots=8, master_seed=5, max_dim=22))
     assert st.total_shots == 8 and st.overflow_count == 0
+
+
+def test_long_noise_stretch_inside_a_wide_section_splitmix():
+    """More than 2,048 noise locations (the wide kernel's SplitMix fire-bit
+    ring) inserted before one op of a warp-per-shot section: every location
+    must still be tested and applied in order (records equal the oracle's)."""
+    body = ["H 0 1 2 3 4 5", "T 0 1 2 3 4 5"]                 # chi dimension 6: wide
+    body += ["REPEAT 350 {", "  H 6 7", "  DEPOLARIZE1(0.004) 0 1 2 3 4 5 6 7", "}"]
+    body += ["CX 0 6 1 7", "M 0 1 2 3 4 5 6 7", "DETECTOR rec[-1] rec[-2]",
+             "OBSERVABLE_INCLUDE(0) rec[-3]"]
+    prog = parse_circuit("\n".join(body) + "\n")
+    from paper_2512_23037_b200.compiler import compile_program
+    dp = compile_program(prog)
+    assert dp.num_locations > 2048
+    for post in (False, True):
+        _check(prog, 12, 48, dict(postselect=post), 4096)
+
+
+def test_narrow_limit5_records_beyond_register_words():
+    """The kn=5 narrow build keeps up to 4 record words per lane in
+    registers; a program with more measurements inside a k=5 narrow section
+    takes the global record buffer -- same records as the oracle's."""
+    from paper_2512_23037_b200 import _lib
+    from paper_2512_23037_b200.engine import Engine, Program, get_engine
+    from paper_2512_23037_b200.compiler import compile_program
+    from paper_2512_23037_b200.sampler import ShotBatch
+    text = ("H 0 1 2 3 4\nT 0 1 2 3 4\nREPEAT 140 {\n  X_ERROR(0.2) 5\n  M 5\n}\n"
+            "M 0 1 2 3 4\nDETECTOR rec[-1] rec[-6]\nOBSERVABLE_INCLUDE(0) rec[-2]\n")
+    prog = parse_circuit(text)
+    dp = compile_program(prog)
+    assert dp.num_measurements > 128 and dp.max_dim == 5
+    p = Program(dp)
+    assert p.sections(_lib.GS_NARROW_K5) == 1   # all lane-per-shot at limit 5
+    eng = get_engine(0)
+    for mode, extra in (("splitmix", 0), ("philox", _lib.GS_RNG_PHILOX)):
+        par = Engine.params(21, 0, 64, 32768, _lib.GS_POSTSELECT | _lib.GS_NARROW_K5 | extra)
+        status, aux, rec, obs = eng.run_records(p, par)
+        b = ShotBatch(status, aux, rec, obs, list(dp.obs_keys), dp.num_measurements)
+        ref = _oracle(prog, 21, 64, 32768, True, mode)
+        for s in range(64):
+            got = b.result(s, measured=_records_before(prog, b, s))
+            assert got.status.value == ref[s]["status"], (mode, s)
+            assert got.record == ref[s]["record"], (mode, s)
