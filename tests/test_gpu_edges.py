@@ -50,6 +50,13 @@ def test_records_beyond_shared_memory_slot():
     _check(prog, 2, 8, dict(postselect=False), 4096)
     b = sample(prog, SamplerConfig(shots=16, master_seed=3, postselect=True))
     assert b.records.shape[1] == (prog.num_measurements + 63) // 64
+    # the same in every kernel form (warp per shot: record words beyond the
+    # 32 register slots go to the global buffer; block per shot)
+    from paper_2512_23037_b200 import _lib
+    for extra in (_lib.GS_WIDE_ONLY, _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK):
+        got = sample(prog, SamplerConfig(shots=8, master_seed=2), extra_flags=extra)
+        ref = sample(prog, SamplerConfig(shots=8, master_seed=2))
+        assert np.array_equal(got.status, ref.status) and np.array_equal(got.records, ref.records)
 
 
 def test_dimension_limit_overflow_and_unsupported():
