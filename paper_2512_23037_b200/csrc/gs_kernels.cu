@@ -304,7 +304,7 @@ static void sections_of(const gs_program *p, bool wide_only, u32 kn, std::vector
     ++nops;
     // the wide kernel runs TF_RED ops in the reduced form (gs_sweeps.cuh
     // t_mix); every shot entering a later section executed all of them
-    if (wide && kind == gs::OP_T && (fl & gs::TF_RED) && len > 12)
+    if ((wide || GS_NARROW_RED) && kind == gs::OP_T && (fl & gs::TF_RED) && len > 12)
       pn = (pn + ((ops[pc + 12] & 2u) ? 15u : 1u)) & 15u;
   }
 }

@@ -27,6 +27,9 @@
 #ifndef GS_NARROW_WARPS_K5
 #define GS_NARROW_WARPS_K5 14   // kn=5 narrow build: most warps per block (14 x 16 KB of chi rows)
 #endif
+#ifndef GS_NARROW_RED
+#define GS_NARROW_RED 1   // reduced T form in the narrow kernel too (A/B r02ff)
+#endif
 #ifndef GS_NARROW_BLOCKS
 #define GS_NARROW_BLOCKS 5   // <= 102 registers: 20 warps/SM (A/B: 47.4M vs 46.4M at 4)
 #endif
@@ -262,6 +265,9 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
     int sst = valid ? ST_RUNNING : ST_PRESERVED, saux = -1;
     // Philox fire schedule of this shot
     u32 sgj = 0, sgpos = 0xFFFFFFFFu, sfire = 0xFFFFFFFFu;
+    // GS_NARROW_RED: chi = e^{i pi spn / 8} * An (reduced T ops, as the wide
+    // kernel's pn; static per op, per lane only because lanes stop apart)
+    u32 spn = S.pn0;
     u64 sgpick = 0;
     if (!S.q_in) {
       sl = S.first + idx;
@@ -427,7 +433,42 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
         const u32 cin = scnt;
         u32 nz = 0;
-        if (tcase == T_BUTTERFLY) {
+        if (GS_NARROW_RED && (fl & TF_RED)) {
+          // reduced form (gs_sweeps.cuh t_mix): c v + (-1)^s i ss w, the
+          // global phase counted in spn -- 4 FP64 operations per entry
+          const u64 w12 = __ldg(op + 12);
+          const double ssr = neg_if1(kTs, ((u32)w12 & 1u) ^ flip);
+          spn = (spn + ((w12 & 2u) ? 15u : 1u)) & 15u;
+          if (tcase == T_BUTTERFLY) {
+            const u32 hb = 31 - __clz(cb);
+#pragma unroll 1
+            for (u32 m = 0; m < (size >> 1); ++m) {
+              const u32 j0 = ins_bit(m, hb, 0), j1 = j0 ^ cb;
+              const double2 v0 = AN(j0), v1 = AN(j1);
+              const double sx0 = neg_if1(ssr, dc ^ par32(j1 & dmask));
+              const double sx1 = neg_if1(ssr, dc ^ par32(j0 & dmask));
+              const double2 n0 = prune(make_double2(__fma_rn(kTc, v0.x, -__dmul_rn(sx0, v1.y)),
+                                                    __fma_rn(kTc, v0.y, __dmul_rn(sx0, v1.x))));
+              const double2 n1 = prune(make_double2(__fma_rn(kTc, v1.x, -__dmul_rn(sx1, v0.y)),
+                                                    __fma_rn(kTc, v1.y, __dmul_rn(sx1, v0.x))));
+              AN(j0) = n0;
+              AN(j1) = n1;
+              nz += nonzero(n0) + nonzero(n1);
+            }
+          } else {
+#pragma unroll 1
+            for (u32 j = 0; j < size; ++j) {
+              const double2 v = AN(j);
+              const double sx = neg_if1(ssr, dc ^ par32(j & dmask));
+              const double2 n0 = prune(make_double2(__dmul_rn(kTc, v.x), __dmul_rn(kTc, v.y)));
+              const double2 n1 = prune(make_double2(-__dmul_rn(sx, v.y), __dmul_rn(sx, v.x)));
+              AN(j) = n0;
+              AN(size + j) = n1;
+              nz += nonzero(n0) + nonzero(n1);
+            }
+            sk = k + 1;
+          }
+        } else if (tcase == T_BUTTERFLY) {
           const u32 hb = 31 - __clz(cb);
 #pragma unroll 1
           for (u32 m = 0; m < (size >> 1); ++m) {
@@ -743,7 +784,7 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const u64 stride = 1ull << P.max_dim;
 #pragma unroll 1
           for (u32 j = 0; j < (1u << sk); ++j) O.amps[sl * stride + j] = AN(j);
-          if (S.pn0) narrow_dump_phase(O.amps + sl * stride, 1u << sk, S.pn0);
+          if (spn) narrow_dump_phase(O.amps + sl * stride, 1u << sk, spn);
         }
       }
     }
