@@ -27,6 +27,9 @@
 #ifndef GS_NARROW_WARPS_K5
 #define GS_NARROW_WARPS_K5 14   // kn=5 narrow build: most warps per block (14 x 16 KB of chi rows)
 #endif
+#ifndef GS_COMPACT_DEFER
+#define GS_COMPACT_DEFER 1   // beta = 0 compactions move only, renormalisation deferred (A/B r02gg)
+#endif
 #ifndef GS_NARROW_RED
 #define GS_NARROW_RED 1   // reduced T form in the narrow kernel too (A/B r02ff)
 #endif
@@ -1254,20 +1257,30 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const double rs = inv_sqrt_norm(plus ? sp : sm);
           if (wfl & MF_COMPACT) {
             const u32 tau = want_neg ^ neg0;
-            SumNz r;
-            if (kPP) {
-              double2 *D = cur ? b0 : b1;
-              r = sweep_compact_to<kG>(A, D, size >> 1, isq, dmask, tau, rs, ps);
-              A = D;
-              cur ^= 1u;
+            if (!kPP && GS_COMPACT_DEFER) {
+              // move only; the renormalisation rs is deferred (ldps), as the
+              // ping-pong form's compactions of span pivots do
+              const u32 nzm = sweep_compact_move<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, ps);
+              ps = 1.0;
+              gsync<kG>();
+              cnt = group_sum_u32<kG>(nzm, grp);
+              defer_scale(rs, plus ? sp : sm);
             } else {
-              r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, rs, ps);
+              SumNz r;
+              if (kPP) {
+                double2 *D = cur ? b0 : b1;
+                r = sweep_compact_to<kG>(A, D, size >> 1, isq, dmask, tau, rs, ps);
+                A = D;
+                cur ^= 1u;
+              } else {
+                r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, rs, ps);
+              }
+              ps = 1.0;
+              gsync<kG>();
+              cnt = group_sum_u32<kG>(r.nz, grp);
+              nrm_l = r.sum;
+              nrm_lane0 = false;
             }
-            ps = 1.0;
-            gsync<kG>();
-            cnt = group_sum_u32<kG>(r.nz, grp);
-            nrm_l = r.sum;
-            nrm_lane0 = false;
             if (tau) c ^= vec;
             kcur = wk - 1;
           } else if ((plus ? sm : sp) == 0.0) {

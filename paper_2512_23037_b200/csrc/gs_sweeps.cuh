@@ -345,6 +345,39 @@ __device__ __forceinline__ SumNz sweep_compact_impl(double2 *A_, u32 half, u32 i
   }
   return r;
 }
+// compaction that only moves (the renormalisation is deferred by the
+// caller into the next pass's loads, ldps): A[jp] = ps * A[src(jp)], same
+// round structure as sweep_compact; returns the nonzero count
+template <bool kS, int kG, bool kPS>
+__device__ __forceinline__ u32 sweep_compact_move_impl(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
+                                                    double ps) {
+  double2 *__restrict__ A = chi_ptr<kS>(A_);
+  const u32 lane = glane<kG>();
+  gbar_in<kG>();
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 b0 = 0; b0 < half; b0 += 32u * kG) {
+    const u32 jp = b0 + lane;
+    double2 v = make_double2(0.0, 0.0);
+    if (jp < half) {
+      const u32 j0 = ins_bit(jp, isq, 0);
+      v = ldp<kPS>(A, j0 | ((tau ^ par32(j0 & mask)) << isq), ps);
+    }
+    gsync<kG>();
+    if (jp < half) {
+      A[jp] = v;
+      nz += nonzero(v);
+    }
+    gsync<kG>();
+  }
+  return nz;
+}
+template <bool kS, int kG = 1>
+__device__ __forceinline__ u32 sweep_compact_move(double2 *A_, u32 half, u32 isq, u32 mask, u32 tau,
+                                               double ps) {
+  if (ps == 1.0) return sweep_compact_move_impl<kS, kG, false>(A_, half, isq, mask, tau, ps);
+  return sweep_compact_move_impl<kS, kG, true>(A_, half, isq, mask, tau, ps);
+}
 // out of place (ping-pong buffers, global chi): D[jp] = rs * A[src(jp)] in
 // one pass, no per-round barriers
 template <int kG>
