@@ -15,7 +15,9 @@ enum { ST_RUNNING = 0, ST_PRESERVED = 1, ST_DISCARDED = 2, ST_OVERFLOW = 3,
        ST_CORRUPT = 4, ST_UNSUPPORTED = 5 };
 enum { MODE_COUNTERS = 0, MODE_RECORDS = 1, MODE_DUMP = 2 };
 
-constexpr int kWinWords = 64;          // noise fire window: 2048 locations
+constexpr int kWinWords = 48;          // SplitMix fire-bit ring: 1536 locations (>= one
+                                       // instruction's 33 words + lookahead; 48 so 14
+                                       // warp-form slices of 16 KB chi + ring fit an SM)
 constexpr int kWinBytes = kWinWords * 4;
 constexpr double kPrune2 = 1e-24;   // (1e-12)^2, ref state.py:24
 constexpr int kEntryBytes = 24;        // SURVEY §8(d) state-touch model

@@ -1008,9 +1008,12 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           // search resumes at max(search_w, cursor / 32), and the owner of a
           // fire found there starts at most 33 words earlier -- <= 1024
           // locations per instruction, compiler.py), and an instruction is
-          // applied only once all its words are scanned
+          // applied only once all its words are scanned (the scan then keeps
+          // its first word live: <= 33 words per instruction < kWinWords)
+          u32 pend_lo = 0xFFFFFFFFu;   // first word of an instruction waiting for its last words
           for (;;) {
-            const u32 low = max(cursor >> 5, search_w > 33u ? search_w - 33u : 0u);
+            const u32 low = pend_lo != 0xFFFFFFFFu ? max(cursor >> 5, pend_lo)
+                                                   : max(cursor >> 5, search_w > 33u ? search_w - 33u : 0u);
             while (scanned < P.nwords && scanned - low < (u32)kWinWords &&
                    __ldg(tables + P.wordpc_off + scanned) <= wpc) {
               const u32 l = scanned * 32u + lane;
@@ -1020,7 +1023,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
                 fire = rng.m53((u32)lw) < thr;
               }
               const u32 bits = __ballot_sync(FULL, fire);
-              if (lane == 0) win[scanned & (kWinWords - 1)] = bits;
+              if (lane == 0) win[scanned % (u32)kWinWords] = bits;
               ++scanned;
             }
             __syncwarp();
@@ -1033,7 +1036,7 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
               u32 w = max(search_w, cursor >> 5);
 #pragma unroll 1
               for (; w < scanned; ++w) {
-                u32 bits = win[w & (kWinWords - 1)];
+                u32 bits = win[w % (u32)kWinWords];
                 if (w == (cursor >> 5)) bits &= ~0u << (cursor & 31);
                 if (bits) { fl_loc = w * 32u + (__ffs(bits) - 1); break; }
               }
@@ -1044,13 +1047,14 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
               const u32 ipc = (u32)nw0, nloc = (u32)(nw0 >> 32);
               if (ipc > wpc) { fire_pc = ipc; break; }
               const u32 loc0 = (u32)__ldg(nrec + 1);
-              if (((loc0 + nloc + 31u) >> 5) > scanned) { need_scan = true; break; }
+              if (((loc0 + nloc + 31u) >> 5) > scanned) { need_scan = true; pend_lo = loc0 >> 5; break; }
+              pend_lo = 0xFFFFFFFFu;
               cursor = loc0 + nloc;
               u64 ex = 0, ez = 0;
 #pragma unroll 1
               for (u32 i = lane; i < nloc; i += 32) {
                 const u32 l = loc0 + i;
-                if (!((win[(l >> 5) & (kWinWords - 1)] >> (l & 31)) & 1u)) continue;
+                if (!((win[(l >> 5) % (u32)kWinWords] >> (l & 31)) & 1u)) continue;
                 const u64 lw = __ldg(locs + 2ull * l);
                 const u32 nk = (u32)(lw >> 48) & 3;
                 const double u = nk <= NK_DEP2 ? rng.uniform((u32)lw + 1) : 0.0;

@@ -176,3 +176,19 @@ def test_narrow_limit5_records_beyond_register_words():
             got = b.result(s, measured=_records_before(prog, b, s))
             assert got.status.value == ref[s]["status"], (mode, s)
             assert got.record == ref[s]["record"], (mode, s)
+
+
+def test_thousand_location_instruction_across_the_ring_splitmix():
+    """One noise instruction of 1,000 locations (repeated targets: 32-33
+    fire-bit words) behind a long stretch of small ones, inserted before one
+    op of a wide section: the ring keeps the whole instruction live until it
+    is complete (records equal the oracle's)."""
+    rep = " ".join(["7"] * 1000)
+    body = ["H 0 1 2 3 4 5", "T 0 1 2 3 4 5",
+            "REPEAT 90 {", "  H 6", "  DEPOLARIZE1(0.003) 0 1 2 3 4 5 6", "}",
+            "X_ERROR(0.003) " + rep, "DEPOLARIZE1(0.01) 6",
+            "REPEAT 40 {", "  DEPOLARIZE1(0.003) 0 1 2 3 4 5 6", "}",
+            "M 0 1 2 3 4 5 6 7", "DETECTOR rec[-1] rec[-2]", "OBSERVABLE_INCLUDE(0) rec[-3]"]
+    prog = parse_circuit("\n".join(body) + "\n")
+    for post in (False, True):
+        _check(prog, 31, 48, dict(postselect=post), 4096)
