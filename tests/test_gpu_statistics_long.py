@@ -80,3 +80,36 @@ def test_discard_and_logical_error_rates_large_sample(name):
     assert_rates_agree(gpu.discarded_shots, gpu.total_shots, cpu["discarded"], cpu["total"])
     assert_rates_agree(gpu.logical_error_shots, gpu.preserved_shots,
                        cpu["error_shots"], cpu["preserved"])
+
+
+def test_philox_production_stream_vs_the_reference_stream_at_scale():
+    """The benchmarked Philox stream against the reference's own SplitMix
+    stream at scale: the GPU's SplitMix records are bit-identical to the
+    reference's (tests/test_gpu_configs.py goldens), so a billion-shot
+    SplitMix run on the GPU is a reference-equivalent sample of the same
+    law.  Discard and logical-error rates of the two streams on the Table-2
+    d=5 circuit must agree (Bayes-factor-1000 intervals, z < 4.5)."""
+    from paper_2512_23037_b200.msc import msc_d5_circuit
+    scale = float(os.environ.get("GS_LONG_SCALE", "1"))
+    shots = int(2 * 10 ** 9 * scale)
+    prog = apply_noise_model(msc_d5_circuit(), 1e-3)
+    out = {}
+    for rng in ("philox", "splitmix"):
+        t0 = time.perf_counter()
+        st = run_batch(prog, SamplerConfig(shots=shots, master_seed=4242 if rng == "philox" else 99,
+                                           postselect=True, rng=rng))
+        out[rng] = (st, time.perf_counter() - t0)
+    (a, ta), (b, tb) = out["philox"], out["splitmix"]
+    summary = {"workload": "msc_d5_table2", "p": 1e-3, "shots_each": shots,
+               "philox": {"discard_rate": a.discard_rate, "logical_error_rate": a.logical_error_rate,
+                          "logical_error_shots": a.logical_error_shots, "wall_s": ta},
+               "splitmix_reference_stream": {"discard_rate": b.discard_rate,
+                                             "logical_error_rate": b.logical_error_rate,
+                                             "logical_error_shots": b.logical_error_shots, "wall_s": tb},
+               "z_discard": _z(a.discarded_shots, a.total_shots, b.discarded_shots, b.total_shots),
+               "z_logical_error": _z(a.logical_error_shots, a.preserved_shots,
+                                     b.logical_error_shots, b.preserved_shots)}
+    print("LONG_STATS " + json.dumps(summary))
+    assert_rates_agree(a.discarded_shots, a.total_shots, b.discarded_shots, b.total_shots)
+    assert_rates_agree(a.logical_error_shots, a.preserved_shots,
+                       b.logical_error_shots, b.preserved_shots)
