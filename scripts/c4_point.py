@@ -21,6 +21,7 @@ ap.add_argument("t", type=int)
 ap.add_argument("--shots", type=int, default=20000)
 ap.add_argument("--warm", type=int, default=2048)
 ap.add_argument("--flags", default="", help="extra run flags, e.g. CHI_BLOCK,CHI_GLOBAL")
+ap.add_argument("--blocks", type=int, default=0, help="resident blocks of the launches (0 = auto)")
 args = ap.parse_args()
 from paper_2512_23037_b200 import _lib  # noqa: E402
 EXTRA = 0
@@ -34,6 +35,15 @@ class Cfg(SamplerConfig):
 
 
 SamplerConfig = Cfg  # noqa: F811
+if args.blocks:
+    from paper_2512_23037_b200.engine import Engine
+    _params = Engine.params
+
+    def _with_blocks(*a, **kw):
+        kw["blocks"] = args.blocks
+        return _params(*a, **kw)
+
+    Engine.params = staticmethod(_with_blocks)
 prog = apply_noise_model(config4_circuit(args.n, args.t, seed=args.n + args.t), 1e-3)
 if args.warm:
     run_batch(prog, SamplerConfig(shots=args.warm, master_seed=1, rng="philox"))
@@ -44,4 +54,4 @@ p = _program_for(prog, cfg.dim_limit)
 print(json.dumps({"n": args.n, "t": args.t, "shots": st.total_shots,
                   "device_shots_per_s": st.device_dict()["device_shots_per_s"],
                   "overflow": st.overflow_count, "max_dim": p.dp.max_dim,
-                  "sections": p.sections(), "flags": args.flags}))
+                  "sections": p.sections(), "flags": args.flags, "blocks": args.blocks}))
