@@ -63,6 +63,11 @@ extern "C" {
                               use the 2^5-row layout): a pure performance
                               choice, the results are identical either way */
 #define GS_BLOCK8 512u     /* with GS_CHI_BLOCK: 8 warps per shot (test)   */
+#define GS_SPARSE 1024u    /* sparse chi: the whole program warp per shot
+                              on a list of the nonzero entries (program
+                              max_dim <= 30, capacity <= 65536) -- for
+                              supports far below 2^k, e.g. T gates that
+                              cancel; results as the dense forms'        */
 
 /* per-shot status codes (gs_run_records) */
 #define GS_ST_PRESERVED 1

@@ -24,6 +24,7 @@ GS_WIDE_ONLY = 32
 GS_SECTION_STATS = 128
 GS_NARROW_K5 = 256
 GS_BLOCK8 = 512
+GS_SPARSE = 1024
 
 # gs_engine_section_stats fields
 GS_SEC_SHOTS_IN = 0

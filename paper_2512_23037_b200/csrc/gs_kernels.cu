@@ -52,6 +52,7 @@ namespace gs {
 
 #include "gs_common.cuh"
 #include "gs_sweeps.cuh"
+#include "gs_sparse.cuh"
 #include "gs_sections.cuh"
 #include "gs_plugin.cuh"
 
@@ -312,7 +313,7 @@ static void sections_of(const gs_program *p, bool wide_only, u32 kn, std::vector
 int gs_program_sections(const gs_program *p, uint32_t flags) {
   if (!p) return fail(GS_ERR_ARG, "null argument");
   std::vector<Section> secs;
-  sections_of(p, (flags & GS_WIDE_ONLY) != 0, gs::narrow_kn(flags), secs);
+  sections_of(p, (flags & (GS_WIDE_ONLY | GS_SPARSE)) != 0, gs::narrow_kn(flags), secs);
   return (int)secs.size();
 }
 
@@ -338,6 +339,12 @@ static cudaError_t with_wide_kernel(bool smem_chi, bool philox, u32 gw, F f) {
   }
   if (smem_chi) return philox ? f(gs::wide_kernel<true, true, 1>) : f(gs::wide_kernel<true, false, 1>);
   return philox ? f(gs::wide_kernel<false, true, 1>) : f(gs::wide_kernel<false, false, 1>);
+}
+
+// the sparse-chi warp-per-shot kernel (GS_SPARSE)
+template <typename F>
+static cudaError_t with_sparse_kernel(bool philox, F f) {
+  return philox ? f(gs::wide_kernel<false, true, 1, true>) : f(gs::wide_kernel<false, false, 1, true>);
 }
 
 struct KernelCfg {
@@ -417,7 +424,10 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
                        cudaStream_t st, bool timed) {
   int rc = GS_OK;
   const bool philox = (r->flags & GS_RNG_PHILOX) != 0;
-  const bool wide_only = (r->flags & GS_WIDE_ONLY) != 0;
+  const bool sparse = (r->flags & GS_SPARSE) != 0;
+  const bool wide_only = sparse || (r->flags & GS_WIDE_ONLY) != 0;
+  if (sparse && r->capacity > 65536)
+    return fail(GS_ERR_UNSUPPORTED, "GS_SPARSE: capacity above 65536 entries");
   gs::DevProg P;
   P.ops = p->d_ops;
   P.tables = p->d_tables;
@@ -467,13 +477,13 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   // shared memory when it fits, GS_CHI_BLOCK | GS_CHI_GLOBAL on global memory
   const size_t chi = (size_t)16 << P.max_dim;
   const bool forced_block = (r->flags & GS_CHI_BLOCK) != 0;
-  const bool block = forced_block ||
-                     (!(r->flags & (GS_CHI_GLOBAL | GS_CHI_SMEM)) && P.max_dim >= GS_BLOCK_MIN_DIM);
+  const bool block = !sparse && (forced_block ||
+                     (!(r->flags & (GS_CHI_GLOBAL | GS_CHI_SMEM)) && P.max_dim >= GS_BLOCK_MIN_DIM));
   const u32 gwarps = !block ? 1u
                      : forced_block ? ((r->flags & GS_BLOCK8) ? 8u : (u32)GS_BLOCK_WARPS)
                      : (P.max_dim < 15 ? 8u : (u32)GS_BLOCK_WARPS);
   bool smem_chi;
-  if (r->flags & GS_CHI_GLOBAL) smem_chi = false;
+  if (sparse || (r->flags & GS_CHI_GLOBAL)) smem_chi = false;
   else if (block) smem_chi = forced_block;   // decided below against the opt-in limit
   else if (r->flags & GS_CHI_SMEM) smem_chi = chi <= 64 * 1024;
   else smem_chi = chi <= 32 * 1024;
@@ -497,7 +507,19 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
                    [&](auto f) { return with_narrow_kernel(philox, kn == 5, f); }, KN);
     if (rc) return rc;
   }
-  if (any_wide && !block) {
+  const u64 sp_stride = gs::sp_geometry(r->capacity).stride;   // sparse workspace per warp
+  if (sparse) {
+    // warp form layout without chi: counters and records in registers,
+    // the SplitMix fire-bit ring in shared memory
+    KW.rec_local = P.rec_words32 <= 32;
+    KW.chi_off = 0;
+    rc = occupancy(e, philox ? 0u : (u32)gs::kWinBytes, r->warps_per_block, GS_WIDE_WARPS,
+                   [&](auto f) { return with_sparse_kernel(philox, f); }, KW);
+    if (rc) return rc;
+    const u64 max_warps = ((u64)8 << 30) / sp_stride;
+    if ((u64)KW.blocks * KW.wpb > max_warps) KW.blocks = (u32)std::max<u64>(1, max_warps / KW.wpb);
+  }
+  if (any_wide && !block && !sparse) {
     // warp form: counters and up to 32 record words in registers
     // (rec_local = 1 means "in registers" here), the SplitMix fire-bit
     // ring in shared memory, then chi
@@ -538,7 +560,10 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
   if (r->blocks) { KN4.blocks = KN5.blocks = r->blocks; KW.blocks = r->blocks; }
   const u64 nwarps = std::max({(u64)KN4.blocks * KN4.wpb, (u64)KN5.blocks * KN5.wpb,
                                (u64)KW.blocks * KW.wpb});
-  if (!smem_chi && any_wide) {
+  if (sparse) {
+    rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * KW.wpb * sp_stride);
+    if (rc) return rc;
+  } else if (!smem_chi && any_wide) {
     rc = ensure_buf(&e->d_chi, &e->chi_bytes, (size_t)KW.blocks * (block ? 3 : KW.wpb) * chi);
     if (rc) return rc;
   }
@@ -638,10 +663,12 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
           Ow.warp_bytes = KW.warp_bytes;
           Ow.rec_local = KW.rec_local;
           Ow.chi_off = KW.chi_off;
-          CUDA_TRY(with_wide_kernel(smem_chi, philox, gwarps, [&](auto kern) {
+          auto go = [&](auto kern) {
             kern<<<KW.blocks, KW.wpb * 32, KW.smem, st>>>(P, R, Ow, S);
             return cudaGetLastError();
-          }));
+          };
+          if (sparse) CUDA_TRY(with_sparse_kernel(philox, go));
+          else CUDA_TRY(with_wide_kernel(smem_chi, philox, gwarps, go));
         } else {
           const KernelCfg &KN = secs[i].kn == 5 ? KN5 : KN4;
           gs::DevOut On = O;

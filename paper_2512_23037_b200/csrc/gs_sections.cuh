@@ -802,8 +802,9 @@ narrow_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 
 // @region wide: prologue
 // kG = 1: warp per shot, kG > 1: block of kG warps per shot (large chi,
-// see GroupScratch)
-template <bool kSmemChi, bool kPhilox, int kG>
+// see GroupScratch); kSp: warp per shot on the sparse chi of gs_sparse.cuh
+// (one section, the whole program)
+template <bool kSmemChi, bool kPhilox, int kG, bool kSp = false>
 #ifdef GS_WIDE_MAXREG
 __global__ void __maxnreg__(GS_WIDE_MAXREG)
 #else
@@ -853,6 +854,12 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   double2 *const b0 = A;
   double2 *const b1 = kPP ? A + pp_stride : nullptr;
   u32 cur = 0;   // kPP: the buffer A lies in
+  static_assert(!kSp || (kG == 1 && !kSmemChi), "sparse chi: warp per shot, global buffers");
+  SpChi spc;
+  if (kSp) {
+    const SpGeo sg = sp_geometry(R.cap);
+    sp_init(spc, reinterpret_cast<u8 *>(O.gchi) + gw * sg.stride, sg.cap2, sg.hbits);
+  }
   const u32 n = P.n;
   const u64 *__restrict__ ops = P.ops;
   const u64 *__restrict__ tables = P.tables;
@@ -904,7 +911,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
 #pragma unroll 1
         for (u32 w = lane; w < P.rec_words32; w += 32) recw[w] = 0;
       }
-      if (gl == 0) A[0] = make_double2(1.0, 0.0);
+      if constexpr (kSp) sp_reset(spc, lane);
+      else if (gl == 0) A[0] = make_double2(1.0, 0.0);
       nrm_l = gl == 0 ? 1.0 : 0.0;
       nrm_lane0 = true;
       nrm_u = 1.0;
@@ -933,11 +941,13 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
       }
       // chi in, and its norm (same per-lane order + tree as a sum pass)
       const double2 *qc = reinterpret_cast<const double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+      if constexpr (!kSp) {   // (the sparse form runs as one section)
 #pragma unroll 1
-      for (u32 j = gl; j < (1u << k); j += NT) {
-        const double2 v = qc[j];
-        A[j] = v;
-        nrm_l = __dadd_rn(nrm_l, abs2(v));
+        for (u32 j = gl; j < (1u << k); j += NT) {
+          const double2 v = qc[j];
+          A[j] = v;
+          nrm_l = __dadd_rn(nrm_l, abs2(v));
+        }
       }
     }
     if (!philox) fire_pc = 0xFFFFFFFFu;
@@ -968,7 +978,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const ErrAct e = compose_error(tables, ex, ez, __ldg(nrec + 2), __ldg(nrec + 3),
                                          sig_lo, sig_hi);
           const double2 php = ipow(e.xi);
-          sweep_phase<kSmemChi, kG>(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
+          if constexpr (kSp) sp_phase(spc, par64(e.delt & c), e.dm, php, cneg(php), ps, lane);
+          else sweep_phase<kSmemChi, kG>(A, 1u << kcur, par64(e.delt & c), e.dm, php, cneg(php), ps);
           ps = 1.0;
           gsync<kG>();
           c ^= e.beta;
@@ -1102,7 +1113,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         if (tcase == T_DIAG) {
           // beta == 0: pure phase per entry (ref state.py:120-126); the
           // factors have modulus 1, the norm is kept
-          sweep_phase<kSmemChi, kG>(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
+          if constexpr (kSp) sp_phase(spc, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps, lane);
+          else sweep_phase<kSmemChi, kG>(A, size, dc, dmask, cadd(a, bx0), cadd(a, cneg(bx0)), ps);
           ps = 1.0;
           gsync<kG>();
           mbytes += 32ull * cnt;
@@ -1113,12 +1125,15 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           u32 nz = 0;
           const double2 bx1 = cneg(bx0);
           gbar_in<kG>();
+          if constexpr (kSp) nz = sp_grow_count(spc, a, bx0, dc, dmask, ps, lane);
+          else {
 #pragma unroll 1
-          for (u32 j = gl; j < size; j += NT) {
-            const double2 v = ldps(A, j, ps);
-            const u32 s_ = dc ^ par32(j & dmask);
-            nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
-            nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
+            for (u32 j = gl; j < size; j += NT) {
+              const double2 v = ldps(A, j, ps);
+              const u32 s_ = dc ^ par32(j & dmask);
+              nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
+              nz += abs2(cadd(Z, cmul(s_ ? bx1 : bx0, v))) > kPrune2;
+            }
           }
           nz = group_sum_u32<kG>(nz, grp);
           status = (u64)nz > R.cap ? ST_OVERFLOW : ST_UNSUPPORTED;
@@ -1126,7 +1141,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           break;
         }
         // beta != 0: pair merge + prune (ref state.py:127-129, 294-306)
-        if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);   // rare: right after a deferral
+        if (ps != 1.0) {   // rare: right after a deferral
+          if constexpr (kSp) sp_scale(spc, ps, lane);
+          else sweep_scale<kSmemChi, kG>(A, size, ps);
+        }
         ps = 1.0;
         // TF_FUSEQ: the partner follows a noise insertion; fusable when no
         // location there fires for this shot: Philox -- its schedule has no
@@ -1162,8 +1180,24 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           mbytes += __ldg(op2 + 11);
           wpc += (u32)((h2 >> 8) & 0xff);
           hnext = __ldg(ops + wpc);
-          const SumNz2 r2 = red ? sweep_butterfly2<kSmemChi, kG, true>(A, size >> 2, g1, g2)
-                                : sweep_butterfly2<kSmemChi, kG, false>(A, size >> 2, g1, g2);
+          SumNz2 r2;
+          if constexpr (kSp) {
+            // two single-gate passes (the fused pass's arithmetic); the
+            // second only while the first stayed within the capacity
+            const SumNz s1 = red ? sp_butterfly<true>(spc, g1, lane) : sp_butterfly<false>(spc, g1, lane);
+            r2.nz1 = s1.nz;
+            r2.nz = 0;
+            r2.sum = 0.0;
+            const u32 c1 = warp_sum_u32(s1.nz);
+            if ((u64)c1 <= R.cap && c1 > 0) {
+              const SumNz s2 = red ? sp_butterfly<true>(spc, g2, lane) : sp_butterfly<false>(spc, g2, lane);
+              r2.nz = s2.nz;
+              r2.sum = s2.sum;
+            }
+          } else {
+            r2 = red ? sweep_butterfly2<kSmemChi, kG, true>(A, size >> 2, g1, g2)
+                     : sweep_butterfly2<kSmemChi, kG, false>(A, size >> 2, g1, g2);
+          }
           gsync<kG>();
           const u32 cnt1 = group_sum_u32<kG>(r2.nz1, grp);
           mbytes += (u64)kEntryBytes * (cin + cnt1);
@@ -1186,7 +1220,14 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           pn = (pn + ((w12 & 2u) ? 15u : 1u)) & 15u;
         }
         SumNz r;
-        if (tcase == T_BUTTERFLY) {
+        if constexpr (kSp) {
+          if (tcase == T_BUTTERFLY) {
+            r = red ? sp_butterfly<true>(spc, g, lane) : sp_butterfly<false>(spc, g, lane);
+          } else {
+            r = red ? sp_grow<true>(spc, g, wk, lane) : sp_grow<false>(spc, g, wk, lane);
+            kcur = wk + 1;
+          }
+        } else if (tcase == T_BUTTERFLY) {
           r = red ? sweep_butterfly<kSmemChi, kG, true>(A, size >> 1, g)
                   : sweep_butterfly<kSmemChi, kG, false>(A, size >> 1, g);
         } else {
@@ -1231,7 +1272,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           // a factor of exactly 1 changes no entry: any pending scale stays
           // pending instead of being applied by a pass now
           if (rs != 1.0) {
-            if (ps != 1.0) sweep_scale<kSmemChi, kG>(A, size, ps);
+            if (ps != 1.0) {
+              if constexpr (kSp) sp_scale(spc, ps, lane);
+              else sweep_scale<kSmemChi, kG>(A, size, ps);
+            }
             ps = rs;
           }
           nrm_u = __dmul_rn(__dmul_rn(kept, rs), rs);
@@ -1250,7 +1294,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             sp = neg0 ? 0.0 : nrm;
             sm = neg0 ? nrm : 0.0;
           } else {
-            const double2 part = sweep_det_sums<kSmemChi, kG>(A, size, dmask, neg0, ps);
+            double2 part;
+            if constexpr (kSp) part = sp_det_sums(spc, dmask, neg0, ps, lane);
+            else part = sweep_det_sums<kSmemChi, kG>(A, size, dmask, neg0, ps);
             sp = group_sum<kG>(part.x, grp);
             sm = group_sum<kG>(part.y, grp);
           }
@@ -1261,7 +1307,11 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           const double rs = inv_sqrt_norm(plus ? sp : sm);
           if (wfl & MF_COMPACT) {
             const u32 tau = want_neg ^ neg0;
-            if (!kPP && GS_COMPACT_DEFER) {
+            if constexpr (kSp) {
+              cnt = sp_compact_move(spc, isq, dmask, tau, ps, lane);   // (warp total)
+              ps = 1.0;
+              defer_scale(rs, plus ? sp : sm);
+            } else if (!kPP && GS_COMPACT_DEFER) {
               // move only; the renormalisation rs is deferred (ldps), as the
               // ping-pong form's compactions of span pivots do
               const u32 nzm = sweep_compact_move<kSmemChi, kG>(A, size >> 1, isq, dmask, tau, ps);
@@ -1292,7 +1342,9 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             // renormalisation
             defer_scale(rs, plus ? sp : sm);
           } else {
-            const SumNz r = sweep_filter<kSmemChi, kG>(A, size, dmask, neg0, want_neg, rs, ps);
+            SumNz r;
+            if constexpr (kSp) r = sp_filter(spc, dmask, neg0, want_neg, rs, ps, lane);
+            else r = sweep_filter<kSmemChi, kG>(A, size, dmask, neg0, want_neg, rs, ps);
             ps = 1.0;
             gsync<kG>();
             cnt = group_sum_u32<kG>(r.nz, grp);
@@ -1307,13 +1359,16 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
           g.isq = isq; g.tmask = tmask; g.ct = (u32)(c >> t) & 1u; g.cb = cb;
           g.dc = dc; g.dmask = dmask;
           const double2 xpp = ipow(xi0);   // i^xi0, exact
-          if (kPP && g.span) {
+          if ((kPP || kSp) && g.span) {
             // one pass: P+ and both outcomes' merged, pruned, compacted
             // pairs (sweep_pivot_both), then chi continues at the chosen
             // half with the renormalisation deferred
             double2 *D = cur ? b0 : b1;
             const u32 half = size >> 1;
-            const PivotBoth pb = sweep_pivot_both<kG>(A, D, g, xpp, ps);
+            u32 spn_p = 0, spn_m = 0;
+            PivotBoth pb;
+            if constexpr (kSp) pb = sp_pivot_both(spc, g, xpp, ps, spn_p, spn_m, lane);
+            else pb = sweep_pivot_both<kG>(A, D, g, xpp, ps);
             gsync<kG>();
             const double pp = __dmul_rn(0.5, group_sum<kG>(pb.pp, grp));
             plus = pick_plus(pp);
@@ -1323,7 +1378,8 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             cnt = group_sum_u32<kG>(plus ? pb.nzp : pb.nzm, grp);
             if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
             ps = 1.0;
-            A = D + (plus ? 0u : half);
+            if constexpr (kSp) sp_take(spc, spc.cur ^ 1u, plus ? 0u : spc.cap2 >> 1, plus ? spn_p : spn_m);
+            else A = D + (plus ? 0u : half);
             cur ^= 1u;
             kcur = wk - 1;
             defer_scale(inv_sqrt_norm(sk), sk);
@@ -1339,18 +1395,21 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             if (chosen < 1e-12) { status = ST_CORRUPT; aux = (int)winstr; break; }
             if (!g.span && ps == 1.0) {
               // rotate the part entries only; norm and count carry over
-              sweep_pivot_part<kSmemChi, kG>(A, g, xpp, plus, size);
+              if constexpr (kSp) sp_pivot_part(spc, g, xpp, plus, lane);
+              else sweep_pivot_part<kSmemChi, kG>(A, g, xpp, plus, size);
               gsync<kG>();
               defer_scale(inv_sqrt_norm(nrm0), nrm0);
             } else {
-              const SumNz w = sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
+              SumNz w;
+              if constexpr (kSp) w = sp_pivot_w(spc, g, xpp, plus, ps, lane);
+              else w = sweep_pivot_w<kSmemChi, kG>(A, g, xpp, plus, ps);
               ps = 1.0;
               gsync<kG>();
               const double sk = group_sum<kG>(w.sum, grp);
               cnt = group_sum_u32<kG>(w.nz, grp);
               if (cnt == 0) { status = ST_CORRUPT; aux = (int)winstr; break; }
               const double rs = inv_sqrt_norm(sk);
-              if (g.span) {
+              if (!kSp && g.span) {   // (sparse span pivots take the one-pass branch)
                 const SumNz r = sweep_compact<kSmemChi, kG>(A, size >> 1, isq, tmask, g.ct, rs, 1.0);
                 gsync<kG>();
                 cnt = group_sum_u32<kG>(r.nz, grp);
@@ -1448,8 +1507,10 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
         for (u32 w = lane; leader && w < P.rec_words32; w += 32) qr[w] = recw[w];
       }
       double2 *qc = reinterpret_cast<double2 *>(q + Q_HDR + rec_u64(P.rec_words32));
+      if constexpr (!kSp) {
 #pragma unroll 1
-      for (u32 j = gl; j < (1u << kcur); j += NT) qc[j] = ldps(A, j, ps);
+        for (u32 j = gl; j < (1u << kcur); j += NT) qc[j] = ldps(A, j, ps);
+      }
       (void)exit_pc;
     } else {
       if (kReg) {
@@ -1518,9 +1579,18 @@ wide_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
             O.dim[sl] = kcur;
           }
           const u64 stride = 1ull << P.max_dim;
+          if constexpr (kSp) {   // zero, then scatter the entries
 #pragma unroll 1
-          for (u32 j = lane; j < (1u << kcur); j += 32)   // leader warp
-            O.amps[sl * stride + j] = with_phase(pn, ldps(A, j, ps));
+            for (u32 j = lane; j < (1u << kcur); j += 32) O.amps[sl * stride + j] = make_double2(0.0, 0.0);
+            __syncwarp();
+#pragma unroll 1
+            for (u32 i = lane; i < spc.n; i += 32)
+              O.amps[sl * stride + spc.key[i]] = with_phase(pn, ldps(spc.amp, i, ps));
+          } else {
+#pragma unroll 1
+            for (u32 j = lane; j < (1u << kcur); j += 32)   // leader warp
+              O.amps[sl * stride + j] = with_phase(pn, ldps(A, j, ps));
+          }
         }
       }
     }

@@ -1,0 +1,434 @@
+// gs_sparse.cuh -- sparse chi for the warp-per-shot kernel (run flag GS_SPARSE).
+// Part of gs_kernels.cu (one translation unit; included inside namespace gs).
+//
+// The dense forms hold chi over all 2^k coordinates of the static span.  A
+// circuit whose T gates cancel (or whose support stays far below 2^k) keeps
+// k growing while the reference's map holds a handful of entries (ref
+// state.py:294-306) -- past the dense dimension limit such shots would end
+// UNSUPPORTED.  The sparse form stores the nonzero entries alone, as an
+// unordered list of (coordinate, amplitude) pairs in two global buffers
+// (ping-pong, 2 x capacity entries each), with a per-warp open-addressing
+// hash table (coordinate -> list index) rebuilt for the two passes that need
+// a partner's value (T butterflies, span pivots).  Every entry's arithmetic
+// is the dense passes' (gs_sweeps.cuh) with an absent partner read as the
+// zero the dense array would hold, so amplitudes agree bit for bit with the
+// warp form; only the order of the norm sums differs (a few ulps, as between
+// the reference and the dense forms).  Coordinates are u32 (k <= 30,
+// compiler.py); list indices fit the table's 16-bit field (capacity <= 2^16).
+#pragma once
+
+// @region sparse
+struct SpChi {
+  u32 *key;        // current list: coordinates
+  double2 *amp;    //               amplitudes
+  u32 n;           // entries (all nonzero)
+  u32 cur;         // buffer holding the list
+  u32 *kb[2];      // ping-pong buffers of `cap2` entries
+  double2 *ab[2];
+  u32 cap2;
+  u64 *tab;        // hash table, 2^hbits slots: gen << 48 | key << 16 | index
+  u32 hbits;
+  u32 gen;         // current table generation (0: table not yet cleared)
+};
+
+// workspace geometry for a capacity (host and device): per warp [hash
+// table: 2^hbits u64][2 x cap2 keys][2 x cap2 amplitudes], cap2 = 2 x
+// capacity (a T at most doubles the <= capacity entries it starts from),
+// 2^hbits >= 2 x capacity slots (load <= 1/2)
+struct SpGeo {
+  u32 cap2, hbits;
+  u64 stride;   // bytes per warp
+};
+__host__ __device__ __forceinline__ SpGeo sp_geometry(u64 cap) {
+  SpGeo g;
+  g.hbits = 6;
+  while ((1ull << g.hbits) < 2ull * cap) ++g.hbits;
+  g.cap2 = (u32)(2 * cap);
+  g.stride = (8ull << g.hbits) + 40ull * g.cap2;
+  return g;
+}
+
+__device__ __forceinline__ void sp_init(SpChi &s, u8 *ws, u32 cap2, u32 hbits) {
+  s.tab = reinterpret_cast<u64 *>(ws);
+  s.hbits = hbits;
+  u8 *p = ws + (8ull << hbits);
+  s.kb[0] = reinterpret_cast<u32 *>(p);
+  s.kb[1] = s.kb[0] + cap2;
+  s.ab[0] = reinterpret_cast<double2 *>(p + 8ull * cap2);
+  s.ab[1] = s.ab[0] + cap2;
+  s.cap2 = cap2;
+  s.gen = 0;
+  s.cur = 0;
+  s.key = s.kb[0];
+  s.amp = s.ab[0];
+  s.n = 0;
+}
+
+// a new shot: chi = |0>
+__device__ __forceinline__ void sp_reset(SpChi &s, u32 lane) {
+  s.cur = 0;
+  s.key = s.kb[0];
+  s.amp = s.ab[0];
+  s.n = 1;
+  if (lane == 0) {
+    s.key[0] = 0;
+    s.amp[0] = make_double2(1.0, 0.0);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ u32 sp_hash(u32 key, u32 hbits) { return (key * 0x9E3779B1u) >> (32 - hbits); }
+
+// index the current list (every key is distinct)
+__device__ __forceinline__ void sp_build(SpChi &s, u32 lane) {
+  const u32 hm = (1u << s.hbits) - 1u;
+  if (s.gen == 0 || s.gen == 0xFFFFu) {   // first use in this launch / generations exhausted
+#pragma unroll 1
+    for (u32 i = lane; i <= hm; i += 32) s.tab[i] = 0;
+    __syncwarp();
+    s.gen = 0;
+  }
+  ++s.gen;
+  const u64 g = (u64)s.gen << 48;
+#pragma unroll 1
+  for (u32 i = lane; i < s.n; i += 32) {
+    const u32 key = s.key[i];
+    const u64 ent = g | ((u64)key << 16) | i;
+    u32 h = sp_hash(key, s.hbits);
+#pragma unroll 1
+    for (;;) {
+      const u64 old = __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
+      // slots of older generations are free; only this warp writes the
+      // table, so a failed swap means another lane took the slot just now
+      if ((u32)(old >> 48) != s.gen &&
+          atomicCAS(reinterpret_cast<unsigned long long *>(s.tab + h), old, ent) == old)
+        break;
+      h = (h + 1u) & hm;
+    }
+  }
+  __syncwarp();
+}
+
+// list index of `key`, or -1
+__device__ __forceinline__ int sp_find(const SpChi &s, u32 key) {
+  const u32 hm = (1u << s.hbits) - 1u;
+  u32 h = sp_hash(key, s.hbits);
+#pragma unroll 1
+  for (;;) {
+    const u64 e = __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
+    if ((u32)(e >> 48) != s.gen) return -1;
+    if ((u32)(e >> 16) == key) return (int)(e & 0xFFFFu);
+    h = (h + 1u) & hm;
+  }
+}
+
+// warp-aggregated append of the lanes with `has` at out[base + rank]
+__device__ __forceinline__ u32 sp_put(u32 *ok, double2 *oa, u32 base, bool has, u32 key, double2 v,
+                                      u32 lane) {
+  const u32 m = __ballot_sync(FULL, has);
+  if (has) {
+    const u32 p = base + __popc(m & ((1u << lane) - 1u));
+    ok[p] = key;
+    oa[p] = v;
+  }
+  return base + __popc(m);
+}
+// prune test with the dense passes' accounting (prune_acc)
+__device__ __forceinline__ bool sp_keep(double2 v, double &sum, u32 &nz) {
+  const double q = abs2(v);
+  if (q > kPrune2) {
+    sum = __dadd_rn(sum, q);
+    nz += 1;
+    return true;
+  }
+  return false;
+}
+// the finished output list (in buffer `b` at `off`) becomes the current one
+__device__ __forceinline__ void sp_take(SpChi &s, u32 b, u32 off, u32 n) {
+  __syncwarp();
+  s.cur = b;
+  s.key = s.kb[b] + off;
+  s.amp = s.ab[b] + off;
+  s.n = n;
+}
+
+// T with beta in span (sweep_butterfly): new[j] = a v_j + b_j v_{j^cb}; an
+// entry whose partner is absent also creates the partner
+template <bool kR>
+__device__ __forceinline__ SumNz sp_butterfly(SpChi &s, const Gate &g, u32 lane) {
+  sp_build(s, lane);
+  const u32 ob = s.cur ^ 1u;
+  u32 *ok = s.kb[ob];
+  double2 *oa = s.ab[ob];
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+  u32 base = 0;
+  const double2 Z = make_double2(0.0, 0.0);
+#pragma unroll 1
+  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
+    const u32 i = i0 + lane;
+    const bool act = i < s.n;
+    u32 j = 0, p = 0;
+    double2 v = Z, w = Z;
+    int ip = 0;
+    if (act) {
+      j = s.key[i];
+      v = s.amp[i];
+      p = j ^ g.cb;
+      ip = sp_find(s, p);
+      if (ip >= 0) w = s.amp[ip];
+    }
+    const u32 mj = (g.dc ^ par32(j & g.dmask)) << 31, mp = (g.dc ^ par32(p & g.dmask)) << 31;
+    const double2 nj = t_mix<kR>(g, v, w, mp);
+    const bool k1 = act && sp_keep(nj, r.sum, r.nz);
+    base = sp_put(ok, oa, base, k1, j, nj, lane);
+    const bool add = act && ip < 0;
+    const double2 np = t_mix<kR>(g, Z, v, mj);
+    const bool k2 = add && sp_keep(np, r.sum, r.nz);
+    base = sp_put(ok, oa, base, k2, p, np, lane);
+  }
+  sp_take(s, ob, 0, base);
+  return r;
+}
+
+// T with a new basis vector k (sweep_grow): (j, a v_j), (j | 2^k, b_j v_j)
+template <bool kR>
+__device__ __forceinline__ SumNz sp_grow(SpChi &s, const Gate &g, u32 k, u32 lane) {
+  const u32 ob = s.cur ^ 1u;
+  u32 *ok = s.kb[ob];
+  double2 *oa = s.ab[ob];
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+  u32 base = 0;
+#pragma unroll 1
+  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
+    const u32 i = i0 + lane;
+    const bool act = i < s.n;
+    u32 j = 0;
+    double2 v = make_double2(0.0, 0.0);
+    if (act) {
+      j = s.key[i];
+      v = s.amp[i];
+    }
+    const u32 sg = g.dc ^ par32(j & g.dmask);
+    double2 lo, hi;
+    if (kR) {
+      const double sx = neg_if1(g.ss, sg);
+      lo = make_double2(__dmul_rn(kTc, v.x), __dmul_rn(kTc, v.y));
+      hi = make_double2(-__dmul_rn(sx, v.y), __dmul_rn(sx, v.x));
+    } else {
+      lo = cmul(g.a, v);
+      hi = neg_if(cmul(g.bx0, v), sg);
+    }
+    const bool k1 = act && sp_keep(lo, r.sum, r.nz);
+    base = sp_put(ok, oa, base, k1, j, lo, lane);
+    const bool k2 = act && sp_keep(hi, r.sum, r.nz);
+    base = sp_put(ok, oa, base, k2, j | (1u << k), hi, lane);
+  }
+  sp_take(s, ob, 0, base);
+  return r;
+}
+
+// nonzeros a T would leave at the dimension limit (OP_GROW_LIMIT)
+__device__ __forceinline__ u32 sp_grow_count(const SpChi &s, double2 a, double2 bx0, u32 dc, u32 dmask,
+                                             double ps, u32 lane) {
+  const double2 Z = make_double2(0.0, 0.0), bx1 = cneg(bx0);
+  u32 nz = 0;
+#pragma unroll 1
+  for (u32 i = lane; i < s.n; i += 32) {
+    const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+    const u32 sg = dc ^ par32(s.key[i] & dmask);
+    nz += abs2(cadd(Z, cmul(a, v))) > kPrune2;
+    nz += abs2(cadd(Z, cmul(sg ? bx1 : bx0, v))) > kPrune2;
+  }
+  return nz;
+}
+
+// diagonal phase (sweep_phase), in place
+__device__ __forceinline__ void sp_phase(SpChi &s, u32 dc, u32 mask, double2 f0, double2 f1, double ps,
+                                         u32 lane) {
+#pragma unroll 1
+  for (u32 i = lane; i < s.n; i += 32) {
+    const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+    s.amp[i] = cmul(v, (dc ^ par32(s.key[i] & mask)) ? f1 : f0);
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void sp_scale(SpChi &s, double ps, u32 lane) {
+#pragma unroll 1
+  for (u32 i = lane; i < s.n; i += 32) s.amp[i] = cscale(s.amp[i], ps);
+  __syncwarp();
+}
+
+// beta = 0 measurement weights (sweep_det_sums)
+__device__ __forceinline__ double2 sp_det_sums(const SpChi &s, u32 dmask, u32 neg0, double ps, u32 lane) {
+  double sp = 0.0, sm = 0.0;
+#pragma unroll 1
+  for (u32 i = lane; i < s.n; i += 32) {
+    const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+    const double a2 = abs2(v);
+    if (neg0 ^ par32(s.key[i] & dmask)) sm = __dadd_rn(sm, a2); else sp = __dadd_rn(sp, a2);
+  }
+  return make_double2(sp, sm);
+}
+
+// keep the chosen eigen-entries scaled by rs (sweep_filter)
+__device__ __forceinline__ SumNz sp_filter(SpChi &s, u32 dmask, u32 neg0, u32 want_neg, double rs,
+                                           double ps, u32 lane) {
+  const u32 ob = s.cur ^ 1u;
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+  u32 base = 0;
+#pragma unroll 1
+  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
+    const u32 i = i0 + lane;
+    bool has = false;
+    u32 j = 0;
+    double2 w = make_double2(0.0, 0.0);
+    if (i < s.n) {
+      j = s.key[i];
+      if ((neg0 ^ par32(j & dmask)) == want_neg) {
+        const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+        w = cscale(v, rs);
+        has = nonzero(w);
+        if (has) {
+          r.sum = __dadd_rn(r.sum, abs2(w));
+          r.nz += 1;
+        }
+      }
+    }
+    base = sp_put(s.kb[ob], s.ab[ob], base, has, j, w, lane);
+  }
+  sp_take(s, ob, 0, base);
+  return r;
+}
+
+// drop coordinate isq keeping the entries j = src(del(j)) (sweep_compact_move):
+// moved with the pending scale applied; returns the nonzero count
+__device__ __forceinline__ u32 sp_compact_move(SpChi &s, u32 isq, u32 mask, u32 tau, double ps, u32 lane) {
+  const u32 ob = s.cur ^ 1u;
+  const u32 lo = (1u << isq) - 1u;
+  u32 base = 0;
+#pragma unroll 1
+  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
+    const u32 i = i0 + lane;
+    bool has = false;
+    u32 jp = 0;
+    double2 v = make_double2(0.0, 0.0);
+    if (i < s.n) {
+      const u32 j = s.key[i];
+      const u32 j0 = j & ~(1u << isq);
+      if (((j >> isq) & 1u) == (tau ^ par32(j0 & mask))) {
+        v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+        has = nonzero(v);
+        jp = (j & lo) | ((j >> 1) & ~lo);
+      }
+    }
+    base = sp_put(s.kb[ob], s.ab[ob], base, has, jp, v, lane);
+  }
+  sp_take(s, ob, 0, base);
+  return base;
+}
+
+// span pivot in one pass (sweep_pivot_both): pairs (rep, rep ^ cb), rep =
+// j0 | ((ct ^ par(j0 & tmask)) << isq); a pair is handled by its rep entry,
+// or by its part entry when the rep is absent; w+ goes to the other buffer
+// at 0, w- at cap2 / 2, both keyed by the rep with coordinate isq removed
+__device__ __forceinline__ PivotBoth sp_pivot_both(SpChi &s, const PivotGeo &g, double2 xpp, double ps,
+                                                   u32 &np, u32 &nm, u32 lane) {
+  sp_build(s, lane);
+  const u32 ob = s.cur ^ 1u;
+  const u32 half = s.cap2 >> 1;
+  const u32 lo = (1u << g.isq) - 1u;
+  const double2 xpm = cneg(xpp), Z = make_double2(0.0, 0.0);
+  PivotBoth r;
+  r.pp = 0.0; r.sump = 0.0; r.summ = 0.0;
+  r.nzp = 0; r.nzm = 0;
+  u32 bp = 0, bm = 0;
+#pragma unroll 1
+  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
+    const u32 i = i0 + lane;
+    bool act = i < s.n;
+    u32 rep = 0, part = 0;
+    double2 vr = Z, vp = Z;
+    if (act) {
+      const u32 j = s.key[i];
+      const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+      const u32 j0 = j & ~(1u << g.isq);
+      if (((j >> g.isq) & 1u) == (g.ct ^ par32(j0 & g.tmask))) {
+        rep = j;
+        part = j ^ g.cb;
+        vr = v;
+        const int ip = sp_find(s, part);
+        if (ip >= 0) vp = ps != 1.0 ? cscale(s.amp[ip], ps) : s.amp[ip];
+      } else {
+        part = j;
+        rep = j ^ g.cb;
+        vp = v;
+        act = sp_find(s, rep) < 0;   // else the rep entry handles the pair
+      }
+    }
+    const double2 pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, vp);
+    const double2 wp = cadd(vr, pr), wm = csub(vr, pr);
+    if (act) r.pp = __dadd_rn(r.pp, abs2(wp));
+    const u32 key = (rep & lo) | ((rep >> 1) & ~lo);
+    const bool kp = act && sp_keep(wp, r.sump, r.nzp);
+    bp = sp_put(s.kb[ob], s.ab[ob], bp, kp, key, wp, lane);
+    const bool km = act && sp_keep(wm, r.summ, r.nzm);
+    bm = sp_put(s.kb[ob] + half, s.ab[ob] + half, bm, km, key, wm, lane);
+  }
+  __syncwarp();
+  np = bp;
+  nm = bm;
+  return r;
+}
+
+// no-span pivot (pivot_terms, span = false): rep entries keep v, part
+// entries -- ct ^ par(j & tmask) = 1 -- become +-(+-i^xi0) v.  Without a
+// pending scale an in-place rotation (sweep_pivot_part); with one, the
+// pruned rewrite of sweep_pivot_w
+__device__ __forceinline__ void sp_pivot_part(SpChi &s, const PivotGeo &g, double2 xpp, bool plus, u32 lane) {
+  const double2 xp = plus ? xpp : cneg(xpp), xm = cneg(xp);
+#pragma unroll 1
+  for (u32 i = lane; i < s.n; i += 32) {
+    const u32 m = s.key[i];
+    if (g.ct ^ par32(m & g.tmask)) s.amp[i] = cmul((g.dc ^ par32(m & g.dmask)) ? xm : xp, s.amp[i]);
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ SumNz sp_pivot_w(SpChi &s, const PivotGeo &g, double2 xpp, bool plus, double ps,
+                                            u32 lane) {
+  const u32 ob = s.cur ^ 1u;
+  const double2 xpm = cneg(xpp);
+  SumNz r;
+  r.sum = 0.0;
+  r.nz = 0;
+  u32 base = 0;
+#pragma unroll 1
+  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
+    const u32 i = i0 + lane;
+    const bool act = i < s.n;
+    u32 m = 0;
+    double2 w = make_double2(0.0, 0.0);
+    if (act) {
+      m = s.key[i];
+      const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+      double2 vr, pr;
+      if (g.ct ^ par32(m & g.tmask)) {
+        vr = make_double2(0.0, 0.0);
+        pr = cmul((g.dc ^ par32(m & g.dmask)) ? xpm : xpp, v);
+      } else {
+        vr = v;
+        pr = make_double2(-0.0, -0.0);
+      }
+      w = plus ? cadd(vr, pr) : csub(vr, pr);
+    }
+    const bool k = act && sp_keep(w, r.sum, r.nz);
+    base = sp_put(s.kb[ob], s.ab[ob], base, k, m, w, lane);
+  }
+  sp_take(s, ob, 0, base);
+  return r;
+}

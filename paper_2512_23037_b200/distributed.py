@@ -18,7 +18,7 @@ import time
 import numpy as np
 
 from . import _lib
-from .sampler import SamplerConfig, counters_to_stats, _program_for, tuned_flags
+from .sampler import SamplerConfig, counters_to_stats, _plan, tuned_flags
 
 
 def shard_range(total: int, rank: int, world: int):
@@ -44,14 +44,14 @@ def _gpu_shard_counters(prog, cfg: SamplerConfig, begin: int, count: int):
     the caller's current device); counters stay on that device."""
     import torch
     from .engine import Engine, get_engine
-    p = _program_for(prog, cfg.dim_limit)
+    p, form = _plan(prog, cfg)
     dev = rank_device(cfg)
     with torch.cuda.device(dev):
         eng = get_engine(dev)
         counters = torch.zeros(p.num_counters, dtype=torch.int64, device=dev)
         stream = torch.cuda.current_stream(dev)
         chunk = cfg.wave_shots
-        flags = cfg.run_flags() | tuned_flags(p, eng, cfg)
+        flags = cfg.run_flags() | (form or tuned_flags(p, eng, cfg))
         done = 0
         while done < count:
             n = min(chunk, count - done)

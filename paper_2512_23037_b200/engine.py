@@ -200,6 +200,8 @@ class Engine:
     def dump(self, prog: Program, params):
         S = params.shot_count
         rw = (prog.dp.num_measurements + 63) // 64
+        if prog.dp.max_dim > 24:
+            raise ValueError("dumps hold 2^max_dim amplitudes per shot: compile with max_dim <= 24")
         stride = 1 << prog.dp.max_dim
         status = np.zeros(max(S, 1), dtype=np.uint8)
         aux = np.zeros(max(S, 1), dtype=np.int32)

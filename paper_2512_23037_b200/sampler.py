@@ -118,6 +118,10 @@ class SamplerConfig:
     rng: str = "splitmix"
     device: int = 0
     max_dim: int | None = None   # chi dimension limit (auto from capacity)
+    # chi form: "dense" (lane / warp / block per shot over 2^k coordinates),
+    # "sparse" (warp per shot over the nonzero entries, GS_SPARSE), "auto"
+    # (dense; sparse when the dense program would hit its dimension limit)
+    chi: str = "auto"
 
     def __post_init__(self):
         if self.shots < 0:
@@ -130,6 +134,8 @@ class SamplerConfig:
             raise ValueError("threads must be >= 1")
         if self.rng not in ("splitmix", "philox"):
             raise ValueError("rng must be 'splitmix' or 'philox'")
+        if self.chi not in ("auto", "dense", "sparse"):
+            raise ValueError("chi must be 'auto', 'dense' or 'sparse'")
 
     @property
     def dim_limit(self) -> int:
@@ -237,6 +243,32 @@ def _program_for(prog, max_dim: int) -> Program:
     return p
 
 
+# the sparse form's limits (gs_sparse.cuh): u32 coordinates of a <= 30-dim
+# span, list indices in 16 bits
+SPARSE_MAX_DIM = 30
+SPARSE_MAX_CAPACITY = 1 << 16
+
+
+def _plan(prog, cfg: SamplerConfig) -> tuple[Program, int]:
+    """The program and chi-form run flag for ``cfg.chi``.  "auto" keeps the
+    dense forms unless the program compiled at ``cfg.dim_limit`` is truncated
+    (a shot can reach a dimension the dense buffers cannot hold while within
+    the capacity -- the advisor's cancelling-T case); then the whole program
+    runs on the sparse form, like the reference's map (ref state.py:294-306)."""
+    if cfg.chi == "dense":
+        return _program_for(prog, cfg.dim_limit), 0
+    sparse_ok = cfg.effective_capacity <= SPARSE_MAX_CAPACITY
+    if cfg.chi == "sparse":
+        if not sparse_ok:
+            raise ValueError("chi='sparse' needs an effective capacity <= %d" % SPARSE_MAX_CAPACITY)
+        lim = SPARSE_MAX_DIM if cfg.max_dim is None else min(cfg.max_dim, SPARSE_MAX_DIM)
+        return _program_for(prog, lim), _lib.GS_SPARSE
+    p = _program_for(prog, cfg.dim_limit)
+    if p.dp.truncated_at is not None and sparse_ok and cfg.max_dim is None:
+        return _program_for(prog, SPARSE_MAX_DIM), _lib.GS_SPARSE
+    return p, 0
+
+
 # runs at least this long (shots) tune the narrow limit first (the probe
 # costs 4 x Program.TUNE_SHOTS shots, once per program)
 TUNE_MIN_SHOTS = 1 << 23
@@ -291,14 +323,14 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     ``ShotContext.reset(derive_seed(master_seed, index))``.
     """
     t0 = time.perf_counter()
-    p = _program_for(prog, cfg.dim_limit)
+    p, form = _plan(prog, cfg)
     eng = engine or get_engine(cfg.device)
     with eng.lock:   # the waves and their device times, not interleaved with other threads
-        return _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0)
+        return _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form)
 
 
-def _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0):
-    flags = cfg.run_flags() | tuned_flags(p, eng, cfg)
+def _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form=0):
+    flags = cfg.run_flags() | (form or tuned_flags(p, eng, cfg))
     total = np.zeros(p.num_counters, dtype=np.int64)
     wit: list = []
     dev_s = 0.0
@@ -366,10 +398,10 @@ def sample(prog, cfg: SamplerConfig, *, shot_begin: int = 0, seeds=None,
            engine: Engine | None = None, extra_flags: int = 0) -> ShotBatch:
     """Per-shot statuses, measurement records and observables.
     ``extra_flags``: performance-only run flags (e.g. ``GS_NARROW_K5``)."""
-    p = _program_for(prog, cfg.dim_limit)
+    p, form = _plan(prog, cfg)
     eng = engine or get_engine(cfg.device)
     par = Engine.params(cfg.master_seed, shot_begin, cfg.shots,
-                        cfg.effective_capacity, cfg.run_flags() | extra_flags, seeds=seeds)
+                        cfg.effective_capacity, cfg.run_flags() | form | extra_flags, seeds=seeds)
     status, aux, rec, obs = eng.run_records(p, par)
     if np.any(status == 4):
         raise CorruptStateError("a shot selected a ~zero-weight branch")

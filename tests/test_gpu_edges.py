@@ -121,19 +121,30 @@ def _cancelled_t(nq: int, noise: bool) -> str:
     return body + "M " + " ".join(map(str, range(nq))) + "\nDETECTOR rec[-1]\n"
 
 
-def test_cancelled_t_span_beyond_dim_limit_is_loud_then_runs():
+def test_cancelled_t_span_beyond_dim_limit_runs_sparse():
+    """Past the dense dimension limit the default (chi="auto") runs the
+    whole program on the sparse form, like the reference's map; forcing the
+    dense forms stays loud; a raised dense limit runs too."""
     from paper_2512_23037_b200 import UnsupportedCircuitError
     prog = parse_circuit(_cancelled_t(22, True))
-    cfg = SamplerConfig(shots=8, master_seed=5)
+    cfg = SamplerConfig(shots=8, master_seed=5, chi="dense")
     assert cfg.dim_limit == 20
     with pytest.raises(UnsupportedCircuitError) as ei:
         run_batch(prog, cfg)
     assert ei.value.limit == 20 and ei.value.instruction is not None
-    # with the limit raised to the span the records equal the reference
-    # restatement's (sparse map, one or two entries per shot)
+    # auto -> sparse: the records equal the reference restatement's (sparse
+    # map, one or two entries per shot), in both random streams
+    for rng in ("splitmix", "philox"):
+        _check(prog, 5, 8, dict(postselect=True, rng=rng), 32768)
+        st = run_batch(prog, SamplerConfig(shots=4096, master_seed=5, rng=rng))
+        assert st.total_shots == 4096 and st.overflow_count == 0
+    # the dense block form with the limit raised to the span agrees
     _check(prog, 5, 8, dict(max_dim=22, postselect=True), 32768)
-    st = run_batch(prog, SamplerConfig(shots=8, master_seed=5, max_dim=22))
-    assert st.total_shots == 8 and st.overflow_count == 0
+    # the advisor's noiseless repro: 24 blocks, every shot preserved
+    prog24 = parse_circuit(_cancelled_t(24, False))
+    st = run_batch(prog24, SamplerConfig(shots=5, master_seed=1))
+    assert st.preserved_shots == 5 and st.overflow_count == 0
+    _check(prog24, 1, 5, dict(), 32768)
 
 
 def test_long_noise_stretch_inside_a_wide_section_splitmix():

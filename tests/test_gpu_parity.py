@@ -74,7 +74,8 @@ def test_golden_shot_results_bit_exact(golden_shots):
 @pytest.mark.parametrize("flag", [_lib.GS_CHI_GLOBAL, _lib.GS_CHI_SMEM,
                                   _lib.GS_WIDE_ONLY,
                                   _lib.GS_WIDE_ONLY | _lib.GS_CHI_SMEM,
-                                  _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK])
+                                  _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK,
+                                  _lib.GS_SPARSE])
 def test_golden_shot_results_storage_variants(golden_shots, flag):
     for fx in golden_shots[::3]:
         prog = parse_circuit(fx["text"])
@@ -83,7 +84,8 @@ def test_golden_shot_results_storage_variants(golden_shots, flag):
         assert got == fx["shots"], fx["name"]
 
 
-def test_golden_state_snapshots(golden_states):
+@pytest.mark.parametrize("flag", [0, _lib.GS_SPARSE])
+def test_golden_state_snapshots(golden_states, flag):
     eng = get_engine(0)
     for fx in golden_states:
         prog = parse_circuit(fx["text"])
@@ -91,7 +93,7 @@ def test_golden_state_snapshots(golden_states):
             dp = compile_program(prog, stop_after=snap["i"], keep_frames=True)
             p = Program(dp)
             seeds = np.array([derive_seed(fx["master"], fx["shot"])], dtype=np.uint64)
-            d = eng.dump(p, Engine.params(fx["master"], 0, 1, 4096, 0, seeds=seeds))
+            d = eng.dump(p, Engine.params(fx["master"], 0, 1, 4096, flag, seeds=seeds))
             assert int(d["status"][0]) == 1
             st = reconstruct_state(dp, snap["i"], int(d["sig"][0][0]) |
                                    (int(d["sig"][0][1]) << prog.num_qubits),
@@ -208,7 +210,7 @@ def test_large_chi_block_per_shot_matches_oracle(n, t):
         outs = []
         for extra in (0, _lib.GS_CHI_GLOBAL, _lib.GS_CHI_BLOCK,
                       _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8,
-                      _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8 | _lib.GS_CHI_GLOBAL):
+                      _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8 | _lib.GS_CHI_GLOBAL, _lib.GS_SPARSE):
             par = Engine.params(9, 0, shots, 32768, flags | extra)
             outs.append(eng.run_records(p, par))
         for other in outs[1:]:
@@ -262,7 +264,7 @@ def test_msc_noiseless_is_deterministic(d):
 @pytest.mark.parametrize("variant", ["default", "wide_only", "chi_global",
                                      "chi_smem", "wide_only_chi_smem", "chi_block",
                                      "chi_block_global", "wide_only_chi_block", "narrow_k5",
-                                     "chi_block8", "chi_block8_global"])
+                                     "chi_block8", "chi_block8_global", "sparse"])
 def test_chi_storage_modes_match_oracle(variant, mode):
     """Lane-per-shot / warp-per-shot / block-per-shot execution and shared- /
     global-memory chi buffers must all give the oracle's results, in both
@@ -277,7 +279,8 @@ def test_chi_storage_modes_match_oracle(variant, mode):
                    "wide_only_chi_block": _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK,
                    "narrow_k5": _lib.GS_NARROW_K5,
                    "chi_block8": _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8,
-                   "chi_block8_global": _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8 | _lib.GS_CHI_GLOBAL}[variant]
+                   "chi_block8_global": _lib.GS_CHI_BLOCK | _lib.GS_BLOCK8 | _lib.GS_CHI_GLOBAL,
+                   "sparse": _lib.GS_SPARSE}[variant]
     eng = get_engine(0)
     for it in range(25):
         n = rng.choice((4, 9, 20))
@@ -298,7 +301,7 @@ def test_chi_storage_modes_match_oracle(variant, mode):
             assert r.record == ref[i]["record"], (variant, it, i)
 
 
-@pytest.mark.parametrize("flag", [0, _lib.GS_CHI_BLOCK])
+@pytest.mark.parametrize("flag", [0, _lib.GS_CHI_BLOCK, _lib.GS_SPARSE])
 def test_msc_d5_dumps_match_oracle_through_t_layer(flag):
     """Full-size state check: the d=5 proxy with chi peaking at 1024
     entries, dumped after the first T layer and after the undo layer
@@ -314,9 +317,10 @@ def test_msc_d5_dumps_match_oracle_through_t_layer(flag):
         p = Program(dp)
         for shot in range(3):
             seeds = np.array([derive_seed(4, shot)], dtype=np.uint64)
-            d = eng.dump(p, Engine.params(4, 0, 1, 1 << 20, flag, seeds=seeds))
+            cap = 1 << 16 if flag & _lib.GS_SPARSE else 1 << 20   # (sparse: <= 2^16)
+            d = eng.dump(p, Engine.params(4, 0, 1, cap, flag, seeds=seeds))
             ref = orc.run_one_shot(flat, prog.num_qubits,
-                                   orc.DrawStream("splitmix", 4, shot), 1 << 20,
+                                   orc.DrawStream("splitmix", 4, shot), cap,
                                    False, stop_after=stop, snapshot=True)
             assert int(d["status"][0]) == 1
             st = reconstruct_state(dp, stop, int(d["sig"][0][0]) |
@@ -379,7 +383,7 @@ def test_section_chunking_invariance(rng):
     assert np.array_equal(c0, c1)
 
 
-@pytest.mark.parametrize("flag", [0, _lib.GS_CHI_BLOCK])
+@pytest.mark.parametrize("flag", [0, _lib.GS_CHI_BLOCK, _lib.GS_SPARSE])
 def test_dumps_restore_the_reduced_t_phase(flag):
     """Reduced-form T ops leave their global phase e^{+-i pi/8} out of chi
     and count it; dumps must restore it both inside the wide section that
@@ -409,7 +413,7 @@ def test_dumps_restore_the_reduced_t_phase(flag):
             assert_chi_close(st["amp"], rs["amp"], context=(stop, shot))
 
 
-@pytest.mark.parametrize("flag", [0, _lib.GS_WIDE_ONLY, _lib.GS_CHI_BLOCK])
+@pytest.mark.parametrize("flag", [0, _lib.GS_WIDE_ONLY, _lib.GS_CHI_BLOCK, _lib.GS_SPARSE])
 def test_conditional_pair_fusion_matches_oracle(flag):
     """TF_FUSEQ pairs (T gates with a noise insertion between them) are fused
     only for shots whose Philox schedule has no candidate there: with noise

@@ -1,0 +1,93 @@
+"""The sparse chi form (run flag GS_SPARSE, gs_sparse.cuh): the whole program
+warp per shot on a list of the nonzero entries.  Parity with the oracle and
+with the dense forms is also covered by the storage-variant parametrisations
+of test_gpu_parity.py (goldens, snapshots, dumps, random programs)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import gstab_oracle as orc
+from paper_2512_23037_b200 import SamplerConfig, compile_program, parse_circuit, run_batch
+from paper_2512_23037_b200 import _lib
+from paper_2512_23037_b200.engine import Engine, Program, get_engine
+
+
+def _config4(n, t):
+    from paper_2512_23037_b200.msc import config4_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    return apply_noise_model(config4_circuit(n, t, seed=n + t), 1e-3)
+
+
+@pytest.mark.parametrize("n,t", [(24, 24), (40, 32), (56, 16)])
+def test_sparse_equals_dense_on_config4(n, t):
+    """Records, statuses (overflow points included) and observables of the
+    sparse form equal the dense forms' shot for shot (the same per-entry
+    arithmetic; only norm-sum orders differ), at capacity 32768."""
+    prog = _config4(n, t)
+    dp = compile_program(prog, max_dim=20)
+    p = Program(dp)
+    eng = get_engine(0)
+    for flags in (_lib.GS_RNG_PHILOX, 0):
+        par = Engine.params(17, 0, 512, 32768, flags | _lib.GS_POSTSELECT)
+        dense = eng.run_records(p, par)
+        par = Engine.params(17, 0, 512, 32768, flags | _lib.GS_POSTSELECT | _lib.GS_SPARSE)
+        sp = eng.run_records(p, par)
+        for x, y in zip(dense, sp):
+            assert np.array_equal(x, y), (n, t, flags)
+
+
+def test_sparse_counters_and_model_bytes_equal_dense():
+    """Counters -- model bytes included (the same per-entry accounting) --
+    of a mixed run equal the dense forms'."""
+    from paper_2512_23037_b200.msc import msc_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(msc_circuit(3), 2e-3)
+    p = Program(compile_program(prog))
+    eng = get_engine(0)
+    base = _lib.GS_RNG_PHILOX | _lib.GS_POSTSELECT
+    c0 = eng.run_counters(p, Engine.params(3, 0, 1 << 16, 32768, base))
+    c1 = eng.run_counters(p, Engine.params(3, 0, 1 << 16, 32768, base | _lib.GS_SPARSE))
+    assert np.array_equal(c0, c1)
+
+
+def test_sparse_overflow_at_the_capacity_matches_oracle():
+    """A small capacity makes shots overflow inside T layers: the overflow
+    instruction and every record before it equal the oracle's."""
+    prog = _config4(24, 16)
+    flat = list(prog.flat())
+    p = Program(compile_program(prog))
+    eng = get_engine(0)
+    cap = 64
+    status, aux, rec, obs = eng.run_records(p, Engine.params(5, 0, 24, cap, _lib.GS_SPARSE))
+    n_ovf = 0
+    for s in range(24):
+        ref = orc.run_one_shot(flat, prog.num_qubits, orc.DrawStream("splitmix", 5, s), cap, False)
+        want = {orc.PRESERVED: 1, orc.DISCARDED: 2, orc.OVERFLOW: 3}[ref["status"]]
+        assert int(status[s]) == want, s
+        if want == 3:
+            n_ovf += 1
+            assert int(aux[s]) == ref["overflow_instruction"], s
+    assert n_ovf > 0
+
+
+def test_sparse_rejects_capacities_beyond_its_index_field():
+    p = Program(compile_program(parse_circuit("H 0\nT 0\nM 0\n")))
+    with pytest.raises(RuntimeError):
+        get_engine(0).run_counters(p, Engine.params(1, 0, 8, 1 << 17, _lib.GS_SPARSE))
+
+
+def test_sparse_hash_table_survives_many_builds():
+    """532 butterflies per shot and one block of warps (blocks=1): each warp
+    rebuilds its hash table ~150,000 times, so the 16-bit generation counter
+    wraps (table cleared) twice; results still equal the dense form's."""
+    text = "H 0 1 2 3\n" + "REPEAT 400 {\n  T 0\n  H 0\n  CX 0 1\n  T 1\n  H 1\n  CX 1 2\n}\n" + \
+        "M 0 1 2 3\n"
+    prog = parse_circuit(text)
+    p = Program(compile_program(prog))
+    eng = get_engine(0)
+    a = eng.run_records(p, Engine.params(2, 0, 4096, 4096, _lib.GS_RNG_PHILOX))
+    b = eng.run_records(p, Engine.params(2, 0, 4096, 4096, _lib.GS_RNG_PHILOX | _lib.GS_SPARSE, blocks=1))
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
