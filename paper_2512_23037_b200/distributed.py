@@ -44,7 +44,9 @@ def _gpu_shard_counters(prog, cfg: SamplerConfig, begin: int, count: int):
     the caller's current device); counters stay on that device."""
     import torch
     from .engine import Engine, get_engine
-    p, form = _plan(prog, cfg)
+    p, form, fallback = _plan(prog, cfg)
+    if fallback is not None:   # (counters stay on the device here: no dense probe)
+        p, form = fallback
     dev = rank_device(cfg)
     with torch.cuda.device(dev):
         eng = get_engine(dev)

@@ -45,15 +45,16 @@ class CorruptStateError(RuntimeError):
 
 class UnsupportedCircuitError(RuntimeError):
     """A shot reached an op whose static chi dimension exceeds the program's
-    dimension limit (``SamplerConfig.dim_limit``) while its support still
-    fit the entry capacity.  The static frame keeps every T
-    coordinate of the shot-invariant span until a measurement removes it, so
-    a circuit whose T gates cancel back to a small support (e.g. many
-    ``H q; T q; T_DAG q; H q`` blocks on distinct qubits) needs a dense chi
-    over the whole span where the reference's sparse map holds one entry
-    (ref state.py:294-306).  Raising ``SamplerConfig(max_dim=...)`` runs it
-    (block form, chi in global memory, up to 2^24 entries per shot); the
-    error is never silent."""
+    dimension limit while its support still fit the entry capacity.  The
+    static frame keeps every T coordinate of the
+    shot-invariant span until a measurement removes it, so a circuit whose T
+    gates cancel back to a small support (e.g. many ``H q; T q; T_DAG q; H q``
+    blocks on distinct qubits) needs a dense chi over the whole span where
+    the reference's sparse map holds one entry (ref state.py:294-306).  With
+    ``chi="auto"`` (default) such runs switch to the sparse form (GS_SPARSE,
+    up to 30 span dimensions, effective capacity <= 2^16), so this is raised
+    only with ``chi="dense"``, beyond those limits, or with an explicit
+    ``max_dim`` -- never silently."""
 
     def __init__(self, shots: int, instruction: int | None, limit: int | None):
         self.shots = shots
@@ -64,7 +65,7 @@ class UnsupportedCircuitError(RuntimeError):
         super().__init__(
             "%d shot(s) reached a chi dimension above the limit%s%s while within the entry "
             "capacity (the static frame keeps cancelled T coordinates until a measurement "
-            "drops them; raise SamplerConfig(max_dim=...))" % (shots, lim, at))
+            "drops them; use SamplerConfig(chi='sparse') or raise max_dim)" % (shots, lim, at))
 
 
 class CapacityError(RuntimeError):
@@ -249,24 +250,30 @@ SPARSE_MAX_DIM = 30
 SPARSE_MAX_CAPACITY = 1 << 16
 
 
-def _plan(prog, cfg: SamplerConfig) -> tuple[Program, int]:
-    """The program and chi-form run flag for ``cfg.chi``.  "auto" keeps the
-    dense forms unless the program compiled at ``cfg.dim_limit`` is truncated
-    (a shot can reach a dimension the dense buffers cannot hold while within
-    the capacity -- the advisor's cancelling-T case); then the whole program
-    runs on the sparse form, like the reference's map (ref state.py:294-306)."""
+def _plan(prog, cfg: SamplerConfig):
+    """(program, chi-form run flag, fallback) for ``cfg.chi``.  "auto" runs
+    the dense forms; when the program compiled at ``cfg.dim_limit`` is
+    truncated (a shot can reach a dimension the dense buffers cannot hold
+    while within the capacity -- the advisor's cancelling-T case) the
+    fallback is the same program on the sparse form (max_dim 30), like the
+    reference's map (ref state.py:294-306).  Callers run a wave dense and
+    switch to the fallback -- rerunning that wave -- once a wave reports an
+    UNSUPPORTED shot: the forms give identical per-shot results, so the
+    counters stay exact, and truncated programs whose shots all overflow
+    before the limit (config-4's largest points) keep the faster dense
+    forms."""
     if cfg.chi == "dense":
-        return _program_for(prog, cfg.dim_limit), 0
+        return _program_for(prog, cfg.dim_limit), 0, None
     sparse_ok = cfg.effective_capacity <= SPARSE_MAX_CAPACITY
     if cfg.chi == "sparse":
         if not sparse_ok:
             raise ValueError("chi='sparse' needs an effective capacity <= %d" % SPARSE_MAX_CAPACITY)
         lim = SPARSE_MAX_DIM if cfg.max_dim is None else min(cfg.max_dim, SPARSE_MAX_DIM)
-        return _program_for(prog, lim), _lib.GS_SPARSE
+        return _program_for(prog, lim), _lib.GS_SPARSE, None
     p = _program_for(prog, cfg.dim_limit)
     if p.dp.truncated_at is not None and sparse_ok and cfg.max_dim is None:
-        return _program_for(prog, SPARSE_MAX_DIM), _lib.GS_SPARSE
-    return p, 0
+        return p, 0, (_program_for(prog, SPARSE_MAX_DIM), _lib.GS_SPARSE)
+    return p, 0, None
 
 
 # runs at least this long (shots) tune the narrow limit first (the probe
@@ -323,13 +330,13 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     ``ShotContext.reset(derive_seed(master_seed, index))``.
     """
     t0 = time.perf_counter()
-    p, form = _plan(prog, cfg)
+    p, form, fallback = _plan(prog, cfg)
     eng = engine or get_engine(cfg.device)
     with eng.lock:   # the waves and their device times, not interleaved with other threads
-        return _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form)
+        return _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form, fallback)
 
 
-def _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form=0):
+def _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form=0, fallback=None):
     flags = cfg.run_flags() | (form or tuned_flags(p, eng, cfg))
     total = np.zeros(p.num_counters, dtype=np.int64)
     wit: list = []
@@ -341,11 +348,17 @@ def _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form=0):
                             cfg.effective_capacity, flags)
         if witnesses > len(wit):
             c, w, _ = eng.run_counters_witness(p, par, witnesses - len(wit))
-            total += c
-            wit.extend(int(x) for x in w)
         else:
-            total += eng.run_counters(p, par)
+            c, w = eng.run_counters(p, par), []
         dev_s += eng.last_kernel_ms * 1e-3
+        if fallback is not None and c[_lib.GS_C_UNSUPPORTED]:
+            # past the dense dimension limit: this wave and the rest sparse
+            p, form = fallback
+            fallback = None
+            flags = cfg.run_flags() | form
+            continue
+        total += c
+        wit.extend(int(x) for x in w)
         done += cnt
     st = counters_to_stats(total, p.dp.obs_keys, time.perf_counter() - t0,
                            dev_s, dp=p.dp)
@@ -398,11 +411,16 @@ def sample(prog, cfg: SamplerConfig, *, shot_begin: int = 0, seeds=None,
            engine: Engine | None = None, extra_flags: int = 0) -> ShotBatch:
     """Per-shot statuses, measurement records and observables.
     ``extra_flags``: performance-only run flags (e.g. ``GS_NARROW_K5``)."""
-    p, form = _plan(prog, cfg)
+    p, form, fallback = _plan(prog, cfg)
     eng = engine or get_engine(cfg.device)
     par = Engine.params(cfg.master_seed, shot_begin, cfg.shots,
                         cfg.effective_capacity, cfg.run_flags() | form | extra_flags, seeds=seeds)
     status, aux, rec, obs = eng.run_records(p, par)
+    if fallback is not None and np.any(status == 5):   # (see _plan)
+        p, form = fallback
+        par = Engine.params(cfg.master_seed, shot_begin, cfg.shots, cfg.effective_capacity,
+                            cfg.run_flags() | form | extra_flags, seeds=seeds)
+        status, aux, rec, obs = eng.run_records(p, par)
     if np.any(status == 4):
         raise CorruptStateError("a shot selected a ~zero-weight branch")
     if np.any(status == 5):

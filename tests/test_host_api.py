@@ -241,24 +241,27 @@ def test_cli_parse_error_exit_code(tmp_path):
 
 
 def test_chi_form_plan():
-    """chi="auto" keeps the dense forms unless the program compiled at the
-    dense dimension limit is truncated (the advisor's cancelling-T case);
-    then the whole program runs on the sparse form (GS_SPARSE, max_dim 30)."""
+    """chi="auto" runs the dense forms; a program truncated at the dense
+    dimension limit (the advisor's cancelling-T case) carries the sparse
+    fallback (GS_SPARSE, max_dim 30) that run_batch / sample switch to once
+    a wave reports an UNSUPPORTED shot."""
     from paper_2512_23037_b200 import _lib
     from paper_2512_23037_b200.sampler import _plan
     body = "".join("H %d\nT %d\nT_DAG %d\nH %d\n" % (q, q, q, q) for q in range(24))
     prog = parse_circuit(body + "M " + " ".join(map(str, range(24))) + "\n")
-    p, f = _plan(prog, SamplerConfig(shots=5))
-    assert f == _lib.GS_SPARSE and p.dp.max_dim == 24 and p.dp.truncated_at is None
-    p, f = _plan(prog, SamplerConfig(shots=5, chi="dense"))
+    p, f, fb = _plan(prog, SamplerConfig(shots=5))
     assert f == 0 and p.dp.max_dim == 20 and p.dp.truncated_at is not None
+    ps, fs = fb
+    assert fs == _lib.GS_SPARSE and ps.dp.max_dim == 24 and ps.dp.truncated_at is None
+    p, f, fb = _plan(prog, SamplerConfig(shots=5, chi="dense"))
+    assert f == 0 and p.dp.truncated_at is not None and fb is None
     # beyond the sparse index field (capacity > 2^16): dense, loud at run time
-    p, f = _plan(prog, SamplerConfig(shots=5, entry_capacity=1 << 15))
-    assert f == 0
+    p, f, fb = _plan(prog, SamplerConfig(shots=5, entry_capacity=1 << 15))
+    assert f == 0 and fb is None
     with pytest.raises(ValueError):
         _plan(prog, SamplerConfig(shots=5, entry_capacity=1 << 15, chi="sparse"))
     small = parse_circuit("H 0\nT 0\nM 0\n")
-    assert _plan(small, SamplerConfig(shots=5))[1] == 0
+    assert _plan(small, SamplerConfig(shots=5))[1:] == (0, None)
     assert _plan(small, SamplerConfig(shots=5, chi="sparse"))[1] == _lib.GS_SPARSE
     with pytest.raises(ValueError):
         SamplerConfig(shots=1, chi="list")
