@@ -36,6 +36,7 @@ class Program:
         self._tables = np.ascontiguousarray(dp.tables, dtype=np.uint64)
         self._locs = np.ascontiguousarray(dp.locs, dtype=np.uint64)
         self._narrow = {}            # (device, flags) -> tuned narrow flag
+        self._chi_form = {}          # (device, flags, capacity) -> 0 dense / 1 sparse (sampler)
         self.narrow_tuning = None    # probe times of the last tuning
         h = ct.c_void_p()
         _lib.check(lib.gs_program_create(ct.byref(info), _u64p(self._ops),

@@ -259,9 +259,7 @@ def _plan(prog, cfg: SamplerConfig):
     reference's map (ref state.py:294-306).  Callers run a wave dense and
     switch to the fallback -- rerunning that wave -- once a wave reports an
     UNSUPPORTED shot: the forms give identical per-shot results, so the
-    counters stay exact, and truncated programs whose shots all overflow
-    before the limit (config-4's largest points) keep the faster dense
-    forms."""
+    counters stay exact.  ``_choose_form`` decides up front on a probe."""
     if cfg.chi == "dense":
         return _program_for(prog, cfg.dim_limit), 0, None
     sparse_ok = cfg.effective_capacity <= SPARSE_MAX_CAPACITY
@@ -274,6 +272,36 @@ def _plan(prog, cfg: SamplerConfig):
     if p.dp.truncated_at is not None and sparse_ok and cfg.max_dim is None:
         return p, 0, (_program_for(prog, SPARSE_MAX_DIM), _lib.GS_SPARSE)
     return p, 0, None
+
+
+PROBE_SHOTS = 4096
+
+
+def _choose_form(p, eng, cfg, fallback, shot_begin):
+    """For a truncated program (``_plan``'s fallback): run a probe of the
+    run's first <= PROBE_SHOTS shots dense; an UNSUPPORTED shot there picks
+    the sparse form (a dense wave would stall on 2^limit-entry passes for
+    shots the sparse form runs on a few entries: 34 K vs 25 M shots/s on
+    24 cancelled T blocks, profiles/sparse_r02.jsonl); otherwise the faster
+    of the two on the same probe (config-4 n=64, T=32: sparse 1.5x; the
+    results are identical either way).  Cached per program and run flags."""
+    key = (eng.device, cfg.run_flags(), cfg.effective_capacity)
+    hit = p._chi_form.get(key)
+    if hit is not None:
+        return (p, 0) if hit == 0 else fallback
+    n = max(1, min(PROBE_SHOTS, cfg.shots))
+    par = Engine.params(cfg.master_seed, shot_begin, n, cfg.effective_capacity, cfg.run_flags())
+    c = eng.run_counters(p, par)
+    t_dense = eng.last_kernel_ms
+    choice = 1
+    if not c[_lib.GS_C_UNSUPPORTED]:
+        ps, fs = fallback
+        par = Engine.params(cfg.master_seed, shot_begin, n, cfg.effective_capacity,
+                            cfg.run_flags() | fs)
+        eng.run_counters(ps, par)
+        choice = 1 if eng.last_kernel_ms < t_dense else 0
+    p._chi_form[key] = choice
+    return (p, 0) if choice == 0 else fallback
 
 
 # runs at least this long (shots) tune the narrow limit first (the probe
@@ -333,6 +361,10 @@ def run_batch(prog, cfg: SamplerConfig, *, shot_begin: int = 0,
     p, form, fallback = _plan(prog, cfg)
     eng = engine or get_engine(cfg.device)
     with eng.lock:   # the waves and their device times, not interleaved with other threads
+        if fallback is not None and cfg.shots:
+            p, form = _choose_form(p, eng, cfg, fallback, shot_begin)
+            if form:
+                fallback = None
         return _run_batch_locked(p, eng, cfg, shot_begin, witnesses, t0, form, fallback)
 
 
@@ -413,6 +445,11 @@ def sample(prog, cfg: SamplerConfig, *, shot_begin: int = 0, seeds=None,
     ``extra_flags``: performance-only run flags (e.g. ``GS_NARROW_K5``)."""
     p, form, fallback = _plan(prog, cfg)
     eng = engine or get_engine(cfg.device)
+    if fallback is not None and cfg.shots:
+        with eng.lock:
+            p, form = _choose_form(p, eng, cfg, fallback, shot_begin)
+        if form:
+            fallback = None
     par = Engine.params(cfg.master_seed, shot_begin, cfg.shots,
                         cfg.effective_capacity, cfg.run_flags() | form | extra_flags, seeds=seeds)
     status, aux, rec, obs = eng.run_records(p, par)

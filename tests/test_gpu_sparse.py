@@ -95,13 +95,16 @@ def test_sparse_hash_table_survives_many_builds():
 
 def test_auto_form_on_a_truncated_program_whose_shots_overflow():
     """Config-4 n=64, T=24 is truncated at the dense limit (k 20) but every
-    shot overflows before reaching it: chi="auto" keeps the dense forms (no
-    UNSUPPORTED wave) and its counters equal the sparse form's."""
+    shot overflows before reaching it: chi="auto" probes both forms (no
+    UNSUPPORTED shot), keeps the faster, and its counters equal the sparse
+    form's and the dense form's."""
     prog = _config4(64, 24)
     kw = dict(shots=2048, master_seed=3, rng="philox", postselect=True)
     a = run_batch(prog, SamplerConfig(**kw))
     s = run_batch(prog, SamplerConfig(chi="sparse", **kw))
+    d = run_batch(prog, SamplerConfig(chi="dense", **kw))
     assert a.overflow_count == 2048
-    assert (a.total_shots, a.preserved_shots, a.discarded_shots, a.overflow_count,
-            a.model_bytes) == (s.total_shots, s.preserved_shots, s.discarded_shots,
-                               s.overflow_count, s.model_bytes)
+    for o in (s, d):
+        assert (a.total_shots, a.preserved_shots, a.discarded_shots, a.overflow_count,
+                a.model_bytes) == (o.total_shots, o.preserved_shots, o.discarded_shots,
+                                   o.overflow_count, o.model_bytes)
