@@ -7,14 +7,17 @@
 // state.py:294-306) -- past the dense dimension limit such shots would end
 // UNSUPPORTED.  The sparse form stores the nonzero entries alone, as an
 // unordered list of (coordinate, amplitude) pairs in two global buffers
-// (ping-pong, 2 x capacity entries each), with a per-warp open-addressing
-// hash table (coordinate -> list index) rebuilt for the two passes that need
-// a partner's value (T butterflies, span pivots).  Every entry's arithmetic
+// (ping-pong, 2 x capacity entries each).  The two passes that need a
+// partner's value (T butterflies, span pivots; partner = key ^ cb) find it
+// by a warp match on the pair's id when the list fits one warp round (<= 32
+// entries), else through a per-warp open-addressing hash table (coordinate
+// -> list index; generation-tagged, so filling it for a pass never clears
+// it).  Every entry's arithmetic
 // is the dense passes' (gs_sweeps.cuh) with an absent partner read as the
 // zero the dense array would hold, so amplitudes agree bit for bit with the
 // warp form; only the order of the norm sums differs (a few ulps, as between
 // the reference and the dense forms).  Coordinates are u32 (k <= 30,
-// compiler.py); list indices fit the table's 16-bit field (capacity <= 2^16).
+// compiler.py); the capacity is bounded (<= 2^16) by the workspace per warp.
 #pragma once
 
 // @region sparse
@@ -28,7 +31,7 @@ struct SpChi {
   u32 cap2;
   u64 *tab;        // hash table, 2^hbits slots: gen << 48 | key << 16 | index
   u32 hbits;
-  u32 gen;         // current table generation (0: table not yet cleared)
+  u32 gen;         // generation of the current fill (0: table not yet cleared)
 };
 
 // workspace geometry for a capacity (host and device): per warp [hash
@@ -79,7 +82,12 @@ __device__ __forceinline__ void sp_reset(SpChi &s, u32 lane) {
 
 __device__ __forceinline__ u32 sp_hash(u32 key, u32 hbits) { return (key * 0x9E3779B1u) >> (32 - hbits); }
 
-// index the current list (every key is distinct)
+// index the current list (every key is distinct; n <= capacity <= 2^16):
+// slots of older generations count as empty, and one atomicMax per entry
+// claims a slot -- a newer generation always wins; within a generation the
+// larger entry wins and the displaced one continues along its own probe
+// sequence (it only moves forward past occupied slots, so lookups still
+// reach it).  No table read before the swap, no clearing after the pass.
 __device__ __forceinline__ void sp_build(SpChi &s, u32 lane) {
   const u32 hm = (1u << s.hbits) - 1u;
   if (s.gen == 0 || s.gen == 0xFFFFu) {   // first use in this launch / generations exhausted
@@ -92,24 +100,26 @@ __device__ __forceinline__ void sp_build(SpChi &s, u32 lane) {
   const u64 g = (u64)s.gen << 48;
 #pragma unroll 1
   for (u32 i = lane; i < s.n; i += 32) {
-    const u32 key = s.key[i];
-    const u64 ent = g | ((u64)key << 16) | i;
-    u32 h = sp_hash(key, s.hbits);
+    u64 ent = g | ((u64)s.key[i] << 16) | i;
+    u32 h = sp_hash((u32)(ent >> 16), s.hbits);
 #pragma unroll 1
     for (;;) {
-      const u64 old = __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
-      // slots of older generations are free; only this warp writes the
-      // table, so a failed swap means another lane took the slot just now
-      if ((u32)(old >> 48) != s.gen &&
-          atomicCAS(reinterpret_cast<unsigned long long *>(s.tab + h), old, ent) == old)
-        break;
+      const u64 old = atomicMax(reinterpret_cast<unsigned long long *>(s.tab + h), ent);
+      if ((old >> 48) != s.gen) break;        // an empty (older) slot: claimed
+      if (old > ent) {                        // taken in this fill: probe on
+        h = (h + 1u) & hm;
+        continue;
+      }
+      ent = old;                              // displaced it: re-home the old entry
       h = (h + 1u) & hm;
     }
   }
   __syncwarp();
 }
+// (kept for symmetry with the pass structure: generation tags need no clear)
+__device__ __forceinline__ void sp_unbuild(SpChi &, u32) {}
 
-// list index of `key`, or -1
+// list index of `key`, or -1 (table reads bypass L1: the swaps ran in L2)
 __device__ __forceinline__ int sp_find(const SpChi &s, u32 key) {
   const u32 hm = (1u << s.hbits) - 1u;
   u32 h = sp_hash(key, s.hbits);
@@ -117,9 +127,22 @@ __device__ __forceinline__ int sp_find(const SpChi &s, u32 key) {
   for (;;) {
     const u64 e = __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
     if ((u32)(e >> 48) != s.gen) return -1;
-    if ((u32)(e >> 16) == key) return (int)(e & 0xFFFFu);
+    if ((u32)((e >> 16) & 0xFFFFFFFFull) == key) return (int)(e & 0xFFFFu);
     h = (h + 1u) & hm;
   }
+}
+
+// the list index of entry (lane, key j)'s partner j ^ cb, or -1: a warp
+// match on the pair id (the member with cb's top bit clear) for lists of
+// <= 32 entries (list index = lane), else the hash table
+__device__ __forceinline__ int sp_partner(const SpChi &s, bool small, bool act, u32 j, u32 cb, u32 lane) {
+  if (small) {
+    const u32 hb = 31 - __clz(cb);
+    const u32 pid = act ? (((j >> hb) & 1u) ? j ^ cb : j) : (0x80000000u | lane);   // keys < 2^30
+    const u32 pl = __match_any_sync(FULL, pid) & ~(1u << lane);
+    return pl ? __ffs(pl) - 1 : -1;
+  }
+  return act ? sp_find(s, j ^ cb) : -1;
 }
 
 // warp-aggregated append of the lanes with `has` at out[base + rank]
@@ -156,7 +179,8 @@ __device__ __forceinline__ void sp_take(SpChi &s, u32 b, u32 off, u32 n) {
 // entry whose partner is absent also creates the partner
 template <bool kR>
 __device__ __forceinline__ SumNz sp_butterfly(SpChi &s, const Gate &g, u32 lane) {
-  sp_build(s, lane);
+  const bool small = s.n <= 32;
+  if (!small) sp_build(s, lane);
   const u32 ob = s.cur ^ 1u;
   u32 *ok = s.kb[ob];
   double2 *oa = s.ab[ob];
@@ -176,9 +200,9 @@ __device__ __forceinline__ SumNz sp_butterfly(SpChi &s, const Gate &g, u32 lane)
       j = s.key[i];
       v = s.amp[i];
       p = j ^ g.cb;
-      ip = sp_find(s, p);
-      if (ip >= 0) w = s.amp[ip];
     }
+    ip = sp_partner(s, small, act, j, g.cb, lane);
+    if (ip >= 0) w = s.amp[ip];
     const u32 mj = (g.dc ^ par32(j & g.dmask)) << 31, mp = (g.dc ^ par32(p & g.dmask)) << 31;
     const double2 nj = t_mix<kR>(g, v, w, mp);
     const bool k1 = act && sp_keep(nj, r.sum, r.nz);
@@ -188,6 +212,7 @@ __device__ __forceinline__ SumNz sp_butterfly(SpChi &s, const Gate &g, u32 lane)
     const bool k2 = add && sp_keep(np, r.sum, r.nz);
     base = sp_put(ok, oa, base, k2, p, np, lane);
   }
+  if (!small) sp_unbuild(s, lane);
   sp_take(s, ob, 0, base);
   return r;
 }
@@ -339,7 +364,8 @@ __device__ __forceinline__ u32 sp_compact_move(SpChi &s, u32 isq, u32 mask, u32 
 // at 0, w- at cap2 / 2, both keyed by the rep with coordinate isq removed
 __device__ __forceinline__ PivotBoth sp_pivot_both(SpChi &s, const PivotGeo &g, double2 xpp, double ps,
                                                    u32 &np, u32 &nm, u32 lane) {
-  sp_build(s, lane);
+  const bool small = s.n <= 32;
+  if (!small) sp_build(s, lane);
   const u32 ob = s.cur ^ 1u;
   const u32 half = s.cap2 >> 1;
   const u32 lo = (1u << g.isq) - 1u;
@@ -352,23 +378,23 @@ __device__ __forceinline__ PivotBoth sp_pivot_both(SpChi &s, const PivotGeo &g, 
   for (u32 i0 = 0; i0 < s.n; i0 += 32) {
     const u32 i = i0 + lane;
     bool act = i < s.n;
-    u32 rep = 0, part = 0;
+    u32 rep = 0, part = 0, j = 0;
     double2 vr = Z, vp = Z;
+    if (act) j = s.key[i];
+    const int ip = sp_partner(s, small, act, j, g.cb, lane);
     if (act) {
-      const u32 j = s.key[i];
       const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
       const u32 j0 = j & ~(1u << g.isq);
       if (((j >> g.isq) & 1u) == (g.ct ^ par32(j0 & g.tmask))) {
         rep = j;
         part = j ^ g.cb;
         vr = v;
-        const int ip = sp_find(s, part);
         if (ip >= 0) vp = ps != 1.0 ? cscale(s.amp[ip], ps) : s.amp[ip];
       } else {
         part = j;
         rep = j ^ g.cb;
         vp = v;
-        act = sp_find(s, rep) < 0;   // else the rep entry handles the pair
+        act = ip < 0;   // else the rep entry handles the pair
       }
     }
     const double2 pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, vp);
@@ -380,6 +406,7 @@ __device__ __forceinline__ PivotBoth sp_pivot_both(SpChi &s, const PivotGeo &g, 
     const bool km = act && sp_keep(wm, r.summ, r.nzm);
     bm = sp_put(s.kb[ob] + half, s.ab[ob] + half, bm, km, key, wm, lane);
   }
+  if (!small) sp_unbuild(s, lane);
   __syncwarp();
   np = bp;
   nm = bm;

@@ -281,9 +281,9 @@ def _choose_form(p, eng, cfg, fallback, shot_begin):
     """For a truncated program (``_plan``'s fallback): run a probe of the
     run's first <= PROBE_SHOTS shots dense; an UNSUPPORTED shot there picks
     the sparse form (a dense wave would stall on 2^limit-entry passes for
-    shots the sparse form runs on a few entries: 34 K vs 25 M shots/s on
+    shots the sparse form runs on a few entries: 34 K vs 30 M shots/s on
     24 cancelled T blocks, profiles/sparse_r02.jsonl); otherwise the faster
-    of the two on the same probe (config-4 n=64, T=32: sparse 1.5x; the
+    of the two on the same probe (config-4 n=64, T=32: sparse 1.6x; the
     results are identical either way).  Cached per program and run flags."""
     key = (eng.device, cfg.run_flags(), cfg.effective_capacity)
     hit = p._chi_form.get(key)

@@ -79,13 +79,15 @@ def test_sparse_rejects_capacities_beyond_its_index_field():
 
 
 def test_sparse_hash_table_survives_many_builds():
-    """532 butterflies per shot and one block of warps (blocks=1): each warp
-    rebuilds its hash table ~150,000 times, so the 16-bit generation counter
-    wraps (table cleared) twice; results still equal the dense form's."""
-    text = "H 0 1 2 3\n" + "REPEAT 400 {\n  T 0\n  H 0\n  CX 0 1\n  T 1\n  H 1\n  CX 1 2\n}\n" + \
-        "M 0 1 2 3\n"
+    """Lists of up to 256 entries (k = 8; > 32 entries take the hash-table
+    path, <= 32 the warp-match path) through 240 butterflies per shot, on
+    one block of warps (blocks=1): every warp fills and clears its table
+    ~70,000 times; results equal the dense form's."""
+    text = ("H 0 1 2 3 4 5 6 7\nT 0 1 2 3 4 5 6 7\nREPEAT 60 {\n  H 0 1 2 3 4 5 6 7\n"
+            "  T 0 1 2 3 4 5 6 7\n  CX 0 1 2 3 4 5 6 7\n}\nM 0 1 2 3 4 5 6 7\n")
     prog = parse_circuit(text)
     p = Program(compile_program(prog))
+    assert p.dp.max_dim == 8
     eng = get_engine(0)
     a = eng.run_records(p, Engine.params(2, 0, 4096, 4096, _lib.GS_RNG_PHILOX))
     b = eng.run_records(p, Engine.params(2, 0, 4096, 4096, _lib.GS_RNG_PHILOX | _lib.GS_SPARSE, blocks=1))
