@@ -344,7 +344,7 @@ static cudaError_t with_wide_kernel(bool smem_chi, bool philox, u32 gw, F f) {
 // the sparse-chi warp-per-shot kernel (GS_SPARSE)
 template <typename F>
 static cudaError_t with_sparse_kernel(bool philox, F f) {
-  return philox ? f(gs::wide_kernel<false, true, 1, true>) : f(gs::wide_kernel<false, false, 1, true>);
+  return philox ? f(gs::sparse_kernel<true>) : f(gs::sparse_kernel<false>);
 }
 
 struct KernelCfg {
