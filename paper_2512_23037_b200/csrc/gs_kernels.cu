@@ -4,7 +4,10 @@
 //   gs_common.cuh   enums, device program/run/output structs, RNG (SplitMix,
 //                   Philox4x32-10, geometric gap search), SHA-1 seeding
 //   gs_sweeps.cuh   warp-cooperative sweeps over the dense chi vector
-//   gs_sections.cuh the two section kernels and their slot queues
+//   gs_sparse.cuh   the sparse chi form: nonzero-entry list passes (GS_SPARSE)
+//   gs_sections.cuh the lane-per-shot section kernel, slot queues, and
+//   gs_wide.cuh     the warp/block-per-shot body, instantiated twice: dense
+//                   wide_kernel and sparse_kernel
 //   gs_plugin.cuh   the Pauli/tableau plugin kernels (ops.py boundary)
 //   this file       host side: program upload, section plan, launch loop, C ABI
 //
