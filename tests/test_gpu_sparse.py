@@ -110,3 +110,22 @@ def test_auto_form_on_a_truncated_program_whose_shots_overflow():
         assert (a.total_shots, a.preserved_shots, a.discarded_shots, a.overflow_count,
                 a.model_bytes) == (o.total_shots, o.preserved_shots, o.discarded_shots,
                                    o.overflow_count, o.model_bytes)
+
+
+def _cancelled(nq):
+    body = "".join("H %d\nT %d\nT_DAG %d\nH %d\n" % (q, q, q, q) for q in range(nq))
+    return parse_circuit(body + "M " + " ".join(map(str, range(nq))) + "\n")
+
+
+def test_sparse_span_limits():
+    """k = 30 (the u32-coordinate limit) runs sparse; a 31-dimensional span
+    is truncated even for the sparse form and stays loud; the largest
+    capacity the index field allows (2^16) runs."""
+    from paper_2512_23037_b200 import UnsupportedCircuitError
+    st = run_batch(_cancelled(30), SamplerConfig(shots=256, master_seed=2))
+    assert st.preserved_shots == 256
+    with pytest.raises(UnsupportedCircuitError):
+        run_batch(_cancelled(31), SamplerConfig(shots=8, master_seed=2))
+    st = run_batch(_cancelled(24), SamplerConfig(shots=256, master_seed=2, chi="sparse",
+                                                entry_capacity=1 << 13))
+    assert st.preserved_shots == 256
