@@ -116,9 +116,6 @@ __device__ __forceinline__ void sp_build(SpChi &s, u32 lane) {
   }
   __syncwarp();
 }
-// (kept for symmetry with the pass structure: generation tags need no clear)
-__device__ __forceinline__ void sp_unbuild(SpChi &, u32) {}
-
 // list index of `key`, or -1 (table reads bypass L1: the swaps ran in L2)
 __device__ __forceinline__ int sp_find(const SpChi &s, u32 key) {
   const u32 hm = (1u << s.hbits) - 1u;
@@ -212,7 +209,6 @@ __device__ __forceinline__ SumNz sp_butterfly(SpChi &s, const Gate &g, u32 lane)
     const bool k2 = add && sp_keep(np, r.sum, r.nz);
     base = sp_put(ok, oa, base, k2, p, np, lane);
   }
-  if (!small) sp_unbuild(s, lane);
   sp_take(s, ob, 0, base);
   return r;
 }
@@ -406,7 +402,6 @@ __device__ __forceinline__ PivotBoth sp_pivot_both(SpChi &s, const PivotGeo &g, 
     const bool km = act && sp_keep(wm, r.summ, r.nzm);
     bm = sp_put(s.kb[ob] + half, s.ab[ob] + half, bm, km, key, wm, lane);
   }
-  if (!small) sp_unbuild(s, lane);
   __syncwarp();
   np = bp;
   nm = bm;
