@@ -31,6 +31,8 @@ struct SpChi {
   u32 cap2;
   u64 *tab;        // hash table, 2^hbits slots: gen << 48 | key << 16 | index
   u32 hbits;
+  u32 hcur;        // slots in use by the current fill: the 2^hcur >= 2n prefix
+                   // (a compact region for short lists: better L2 locality)
   u32 gen;         // generation of the current fill (0: table not yet cleared)
 };
 
@@ -54,6 +56,7 @@ __host__ __device__ __forceinline__ SpGeo sp_geometry(u64 cap) {
 __device__ __forceinline__ void sp_init(SpChi &s, u8 *ws, u32 cap2, u32 hbits) {
   s.tab = reinterpret_cast<u64 *>(ws);
   s.hbits = hbits;
+  s.hcur = hbits;
   u8 *p = ws + (8ull << hbits);
   s.kb[0] = reinterpret_cast<u32 *>(p);
   s.kb[1] = s.kb[0] + cap2;
@@ -89,19 +92,21 @@ __device__ __forceinline__ u32 sp_hash(u32 key, u32 hbits) { return (key * 0x9E3
 // sequence (it only moves forward past occupied slots, so lookups still
 // reach it).  No table read before the swap, no clearing after the pass.
 __device__ __forceinline__ void sp_build(SpChi &s, u32 lane) {
-  const u32 hm = (1u << s.hbits) - 1u;
-  if (s.gen == 0 || s.gen == 0xFFFFu) {   // first use in this launch / generations exhausted
+  if (s.gen == 0 || s.gen == 0xFFFFu) {
+    const u32 hm = (1u << s.hbits) - 1u;   // first use in this launch / generations exhausted
 #pragma unroll 1
     for (u32 i = lane; i <= hm; i += 32) s.tab[i] = 0;
     __syncwarp();
     s.gen = 0;
   }
   ++s.gen;
+  s.hcur = max(6u, min(s.hbits, 32u - __clz(2u * s.n - 1u)));   // 2^hcur >= 2n
+  const u32 hm = (1u << s.hcur) - 1u;
   const u64 g = (u64)s.gen << 48;
 #pragma unroll 1
   for (u32 i = lane; i < s.n; i += 32) {
     u64 ent = g | ((u64)s.key[i] << 16) | i;
-    u32 h = sp_hash((u32)(ent >> 16), s.hbits);
+    u32 h = sp_hash((u32)(ent >> 16), s.hcur);
 #pragma unroll 1
     for (;;) {
       const u64 old = atomicMax(reinterpret_cast<unsigned long long *>(s.tab + h), ent);
@@ -118,8 +123,8 @@ __device__ __forceinline__ void sp_build(SpChi &s, u32 lane) {
 }
 // list index of `key`, or -1 (table reads bypass L1: the swaps ran in L2)
 __device__ __forceinline__ int sp_find(const SpChi &s, u32 key) {
-  const u32 hm = (1u << s.hbits) - 1u;
-  u32 h = sp_hash(key, s.hbits);
+  const u32 hm = (1u << s.hcur) - 1u;
+  u32 h = sp_hash(key, s.hcur);
 #pragma unroll 1
   for (;;) {
     const u64 e = __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
