@@ -3,6 +3,7 @@ sampling commands, running on the B200.
 
     python -m paper_2512_23037_b200 sample CIRCUIT --shots N [--noise p]
         [--postselect] [--seed S] [--rng splitmix|philox] [--witnesses K]
+        [--chi auto|dense|sparse]
     python -m paper_2512_23037_b200 stats CIRCUIT
     python -m paper_2512_23037_b200 bench CIRCUIT --sweep batch-size|noise --values ...
     python -m paper_2512_23037_b200 msc --d 5 [--variant table2|grown|proxy] [--noise p]
@@ -58,7 +59,7 @@ def cmd_sample(a):
         cfg = SamplerConfig(shots=a.shots, master_seed=a.seed, batch_size=a.batch_size,
                             entry_capacity=a.entry_capacity,
                             threads=a.threads or int(os.environ.get("SOFT_THREADS", "1")),
-                            postselect=a.postselect, rng=a.rng, device=a.device)
+                            postselect=a.postselect, rng=a.rng, device=a.device, chi=a.chi)
     except ValueError as exc:
         print("error: %s" % exc, file=sys.stderr)
         return EXIT_USAGE
@@ -99,7 +100,7 @@ def cmd_bench(a):
         cfg = SamplerConfig(shots=a.shots, master_seed=a.seed,
                             entry_capacity=a.entry_capacity,
                             postselect=a.postselect, rng=a.rng,
-                            batch_size=a.batch_size)
+                            batch_size=a.batch_size, chi=a.chi)
         try:
             rows = throughput_bench(prog, cfg, a.sweep, vals)
         except NoiseModelError as exc:
@@ -135,13 +136,15 @@ def build_parser():
     s.add_argument("--seed", type=int, default=0)
     s.add_argument("--threads", type=int, default=None, help="accepted, ignored")
     s.add_argument("--batch-size", type=int, default=None,
-                   help="shots resident per launch (default 2^24)")
+                   help="shots resident per launch (default 2^22)")
     s.add_argument("--noise", type=float, default=None)
     s.add_argument("--postselect", action=argparse.BooleanOptionalAction, default=False)
     s.add_argument("--entry-capacity", type=int, default=4096)
     s.add_argument("--rng", choices=("splitmix", "philox"), default="splitmix")
     s.add_argument("--device", type=int, default=0)
     s.add_argument("--witnesses", type=int, default=0)
+    s.add_argument("--chi", choices=("auto", "dense", "sparse"), default="auto",
+                   help="chi form (DESIGN.md §3): sparse for supports far below 2^k")
     s.add_argument("--out", default=None)
     s.set_defaults(fn=cmd_sample)
     t = sub.add_parser("stats", help="circuit statistics")
@@ -154,11 +157,12 @@ def build_parser():
     b.add_argument("--values", required=True)
     b.add_argument("--shots", type=int, default=10000)
     b.add_argument("--batch-size", type=int, default=None,
-                   help="wave size for --sweep noise (default 2^24)")
+                   help="wave size for --sweep noise (default 2^22)")
     b.add_argument("--seed", type=int, default=0)
     b.add_argument("--postselect", action=argparse.BooleanOptionalAction, default=False)
     b.add_argument("--entry-capacity", type=int, default=4096)
     b.add_argument("--rng", choices=("splitmix", "philox"), default="splitmix")
+    b.add_argument("--chi", choices=("auto", "dense", "sparse"), default="auto")
     b.add_argument("--out", default=None)
     b.set_defaults(fn=cmd_bench)
     m = sub.add_parser("msc", help="emit a magic-state-cultivation circuit text")

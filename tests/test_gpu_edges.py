@@ -109,6 +109,13 @@ def test_cli_sample_json_schema(tmp_path):
     d = json.loads(out.read_text())
     assert d["total_shots"] == 1000
     assert set(d) >= {"preserved_shots", "discard_rate", "bayes_lo", "throughput"}
+    # the sparse chi form through the CLI: the same counters
+    out2 = tmp_path / "o2.json"
+    assert main(["sample", str(path), "--shots", "1000", "--noise", "0.01",
+                 "--postselect", "--chi", "sparse", "--out", str(out2)]) == 0
+    d2 = json.loads(out2.read_text())
+    for k in ("total_shots", "preserved_shots", "discarded_shots", "logical_error_shots"):
+        assert d2[k] == d[k], k
 
 
 def _cancelled_t(nq: int, noise: bool) -> str:

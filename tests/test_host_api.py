@@ -265,3 +265,13 @@ def test_chi_form_plan():
     assert _plan(small, SamplerConfig(shots=5, chi="sparse"))[1] == _lib.GS_SPARSE
     with pytest.raises(ValueError):
         SamplerConfig(shots=1, chi="list")
+
+
+def test_cli_chi_option_parses():
+    from paper_2512_23037_b200.cli import build_parser
+    a = build_parser().parse_args(["sample", "x.stim", "--shots", "4", "--chi", "sparse"])
+    assert a.chi == "sparse"
+    a = build_parser().parse_args(["bench", "x.stim", "--sweep", "noise", "--values", "1e-3"])
+    assert a.chi == "auto"
+    with pytest.raises(SystemExit):
+        build_parser().parse_args(["sample", "x.stim", "--shots", "4", "--chi", "list"])
