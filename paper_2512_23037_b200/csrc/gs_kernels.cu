@@ -519,7 +519,7 @@ static int launch_body(gs_engine *e, gs_program *p, const gs_run_params *r, gs::
     rc = occupancy(e, philox ? 0u : (u32)gs::kWinBytes, r->warps_per_block, GS_WIDE_WARPS,
                    [&](auto f) { return with_sparse_kernel(philox, f); }, KW);
     if (rc) return rc;
-    const u64 max_warps = ((u64)8 << 30) / sp_stride;
+    const u64 max_warps = ((u64)GS_SPARSE_GB << 30) / sp_stride;
     if ((u64)KW.blocks * KW.wpb > max_warps) KW.blocks = (u32)std::max<u64>(1, max_warps / KW.wpb);
   }
   if (any_wide && !block && !sparse) {

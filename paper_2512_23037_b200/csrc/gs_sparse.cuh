@@ -20,6 +20,13 @@
 // compiler.py); the capacity is bounded (<= 2^16) by the workspace per warp.
 #pragma once
 
+#ifndef GS_SPARSE_MINB
+#define GS_SPARSE_MINB 1   // resident 14-warp blocks per SM the register budget targets
+#endif
+#ifndef GS_SPARSE_GB
+#define GS_SPARSE_GB 8     // workspace budget (GB) bounding the resident warps
+#endif
+
 // @region sparse
 struct SpChi {
   u32 *key;        // current list: coordinates

@@ -11,7 +11,7 @@
 // section, the whole program); the dense forms' body with the chi passes
 // swapped for the sp_* list passes
 template <bool kPhilox>
-__global__ void __launch_bounds__(32 * GS_WIDE_WARPS, GS_WIDE_BLOCKS)
+__global__ void __launch_bounds__(32 * GS_WIDE_WARPS, GS_SPARSE_MINB)
 sparse_kernel(DevProg P, DevRun R, DevOut O, DevSec S) {
   constexpr bool kSmemChi = false;
   constexpr int kG = 1;
