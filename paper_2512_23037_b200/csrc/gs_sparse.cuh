@@ -12,12 +12,12 @@
 // by a warp match on the pair's id when the list fits one warp round (<= 32
 // entries), else through a per-warp open-addressing hash table (coordinate
 // -> list index; generation-tagged, so filling it for a pass never clears
-// it).  Every entry's arithmetic
-// is the dense passes' (gs_sweeps.cuh) with an absent partner read as the
-// zero the dense array would hold, so amplitudes agree bit for bit with the
-// warp form; only the order of the norm sums differs (a few ulps, as between
-// the reference and the dense forms).  Coordinates are u32 (k <= 30,
-// compiler.py); the capacity is bounded (<= 2^16) by the workspace per warp.
+// it).  Every entry's arithmetic is the dense passes' (gs_sweeps.cuh) with
+// an absent partner read as the zero the dense array would hold, so
+// amplitudes agree bit for bit with the warp form; only the order of the
+// norm sums differs (a few ulps, as between the reference and the dense
+// forms).  Coordinates are u32 (k <= 30, compiler.py); list indices fit the
+// table entries' 16-bit field (capacity <= 2^16, checked on the host).
 #pragma once
 
 #ifndef GS_SPARSE_MINB
