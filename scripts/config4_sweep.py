@@ -50,6 +50,8 @@ def main():
                    "preserved": st.preserved_shots,
                    "logical_error_shots": st.logical_error_shots,
                    "max_dim": p.dp.max_dim, "sections": p.sections(),
+                   # chi="auto": truncated programs may run on the sparse form
+                   "form": "sparse" if 1 in p._chi_form.values() else "dense",
                    "model_bytes_per_shot": st.model_bytes / max(st.total_shots, 1),
                    "rng": args.rng, "p": args.p}
             rows.append(row)
