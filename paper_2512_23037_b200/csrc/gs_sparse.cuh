@@ -110,35 +110,55 @@ __device__ __forceinline__ void sp_build(SpChi &s, u32 lane) {
   s.hcur = max(6u, min(s.hbits, 32u - __clz(2u * s.n - 1u)));   // 2^hcur >= 2n
   const u32 hm = (1u << s.hcur) - 1u;
   const u64 g = (u64)s.gen << 48;
+  // two rounds per iteration: both first swaps in flight before either
+  // resolves (the swaps are L2 round trips)
 #pragma unroll 1
-  for (u32 i = lane; i < s.n; i += 32) {
-    u64 ent = g | ((u64)s.key[i] << 16) | i;
-    u32 h = sp_hash((u32)(ent >> 16), s.hcur);
+  for (u32 i0 = 0; i0 < s.n; i0 += 64) {
+    u64 ent[2], old[2];
+    u32 h[2];
+    bool live[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const u32 i = i0 + 32u * u + lane;
+      live[u] = i < s.n;
+      ent[u] = live[u] ? (g | ((u64)s.key[i] << 16) | i) : 0ull;
+      h[u] = sp_hash((u32)(ent[u] >> 16), s.hcur);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      old[u] = live[u] ? atomicMax(reinterpret_cast<unsigned long long *>(s.tab + h[u]), ent[u]) : 0ull;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!live[u]) continue;
 #pragma unroll 1
-    for (;;) {
-      const u64 old = atomicMax(reinterpret_cast<unsigned long long *>(s.tab + h), ent);
-      if ((old >> 48) != s.gen) break;        // an empty (older) slot: claimed
-      if (old > ent) {                        // taken in this fill: probe on
-        h = (h + 1u) & hm;
-        continue;
+      for (;;) {
+        if ((old[u] >> 48) != s.gen) break;   // an empty (older) slot: claimed
+        if (old[u] < ent[u]) ent[u] = old[u]; // displaced it: re-home the old entry
+        h[u] = (h[u] + 1u) & hm;              // (else taken in this fill: probe on)
+        old[u] = atomicMax(reinterpret_cast<unsigned long long *>(s.tab + h[u]), ent[u]);
       }
-      ent = old;                              // displaced it: re-home the old entry
-      h = (h + 1u) & hm;
     }
   }
   __syncwarp();
 }
-// list index of `key`, or -1 (table reads bypass L1: the swaps ran in L2)
-__device__ __forceinline__ int sp_find(const SpChi &s, u32 key) {
+// list index of `key`, or -1, from its first probe (slot h, entry e);
+// table reads bypass L1 (the swaps ran in L2)
+__device__ __forceinline__ int sp_resolve(const SpChi &s, u32 key, u32 h, u64 e) {
   const u32 hm = (1u << s.hcur) - 1u;
-  u32 h = sp_hash(key, s.hcur);
 #pragma unroll 1
   for (;;) {
-    const u64 e = __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
     if ((u32)(e >> 48) != s.gen) return -1;
     if ((u32)((e >> 16) & 0xFFFFFFFFull) == key) return (int)(e & 0xFFFFu);
     h = (h + 1u) & hm;
+    e = __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
   }
+}
+__device__ __forceinline__ u64 sp_probe(const SpChi &s, u32 h) {
+  return __ldcg(reinterpret_cast<const unsigned long long *>(s.tab + h));
+}
+__device__ __forceinline__ int sp_find(const SpChi &s, u32 key) {
+  const u32 h = sp_hash(key, s.hcur);
+  return sp_resolve(s, key, h, sp_probe(s, h));
 }
 
 // the list index of entry (lane, key j)'s partner j ^ cb, or -1: a warp
@@ -198,28 +218,51 @@ __device__ __forceinline__ SumNz sp_butterfly(SpChi &s, const Gate &g, u32 lane)
   r.nz = 0;
   u32 base = 0;
   const double2 Z = make_double2(0.0, 0.0);
+  // two rounds per iteration: both rounds' loads and first probes in
+  // flight before either resolves
 #pragma unroll 1
-  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
-    const u32 i = i0 + lane;
-    const bool act = i < s.n;
-    u32 j = 0, p = 0;
-    double2 v = Z, w = Z;
-    int ip = 0;
-    if (act) {
-      j = s.key[i];
-      v = s.amp[i];
-      p = j ^ g.cb;
+  for (u32 i0 = 0; i0 < s.n; i0 += 64) {
+    u32 j[2], p[2];
+    double2 v[2], w[2];
+    int ip[2];
+    bool act[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const u32 i = i0 + 32u * u + lane;
+      act[u] = i < s.n;
+      j[u] = act[u] ? s.key[i] : 0u;
+      v[u] = act[u] ? s.amp[i] : Z;
+      p[u] = j[u] ^ g.cb;
+      w[u] = Z;
     }
-    ip = sp_partner(s, small, act, j, g.cb, lane);
-    if (ip >= 0) w = s.amp[ip];
-    const u32 mj = (g.dc ^ par32(j & g.dmask)) << 31, mp = (g.dc ^ par32(p & g.dmask)) << 31;
-    const double2 nj = t_mix<kR>(g, v, w, mp);
-    const bool k1 = act && sp_keep(nj, r.sum, r.nz);
-    base = sp_put(ok, oa, base, k1, j, nj, lane);
-    const bool add = act && ip < 0;
-    const double2 np = t_mix<kR>(g, Z, v, mj);
-    const bool k2 = add && sp_keep(np, r.sum, r.nz);
-    base = sp_put(ok, oa, base, k2, p, np, lane);
+    if (small) {   // one round (n <= 32)
+      ip[0] = sp_partner(s, true, act[0], j[0], g.cb, lane);
+      ip[1] = -1;
+    } else {
+      u32 h[2];
+      u64 e[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        h[u] = sp_hash(p[u], s.hcur);
+        e[u] = act[u] ? sp_probe(s, h[u]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) ip[u] = act[u] ? sp_resolve(s, p[u], h[u], e[u]) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (ip[u] >= 0) w[u] = s.amp[ip[u]];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const u32 mj = (g.dc ^ par32(j[u] & g.dmask)) << 31, mp = (g.dc ^ par32(p[u] & g.dmask)) << 31;
+      const double2 nj = t_mix<kR>(g, v[u], w[u], mp);
+      const bool k1 = act[u] && sp_keep(nj, r.sum, r.nz);
+      base = sp_put(ok, oa, base, k1, j[u], nj, lane);
+      const bool add = act[u] && ip[u] < 0;
+      const double2 np = t_mix<kR>(g, Z, v[u], mj);
+      const bool k2 = add && sp_keep(np, r.sum, r.nz);
+      base = sp_put(ok, oa, base, k2, p[u], np, lane);
+    }
   }
   sp_take(s, ob, 0, base);
   return r;
