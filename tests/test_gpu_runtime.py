@@ -52,6 +52,23 @@ def test_section_stats_partition_the_run(d5):
                for s in eng.section_stats(reset=True))
 
 
+def test_section_stats_of_the_sparse_form(d5):
+    """GS_SPARSE runs one section (the whole program): its stats hold every
+    shot and the run's model bytes, and the counters equal the dense run's."""
+    p = _program_for(d5, 13)
+    eng = Engine(0)
+    S = 1 << 15
+    c0 = eng.run_counters(p, Engine.params(4, 0, S, 4096, _flags()))
+    eng.section_stats(reset=True)
+    c1 = eng.run_counters(p, Engine.params(4, 0, S, 4096, _flags(True) | _lib.GS_SPARSE))
+    secs = eng.section_stats(reset=True)
+    assert np.array_equal(c0, c1)
+    assert len(secs) == 1 and p.sections(_lib.GS_SPARSE) == 1
+    assert secs[0]["shots_in"] == S and secs[0]["shots_out"] == 0
+    assert secs[0]["model_bytes"] == int(c1[_lib.GS_C_MODEL_BYTES])
+    assert secs[0]["kernel"] == "wide" and secs[0]["launches"] == 1
+
+
 def test_section_stats_accumulate_over_chunks_and_async(d5):
     import torch
     p = _program_for(d5, 13)
