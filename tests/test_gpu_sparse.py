@@ -129,3 +129,17 @@ def test_sparse_span_limits():
     st = run_batch(_cancelled(24), SamplerConfig(shots=256, master_seed=2, chi="sparse",
                                                 entry_capacity=1 << 13))
     assert st.preserved_shots == 256
+
+
+def test_sparse_witnesses_equal_dense():
+    """Rare-failure witnesses (preserved shots with a flipped observable)
+    are the same shot indices on both forms."""
+    from paper_2512_23037_b200.msc import msc_d3_circuit
+    from paper_2512_23037_b200.noise import apply_noise_model
+    prog = apply_noise_model(msc_d3_circuit(), 5e-3)
+    kw = dict(shots=1 << 16, master_seed=9, rng="philox", postselect=True)
+    a = run_batch(prog, SamplerConfig(**kw), witnesses=64)
+    b = run_batch(prog, SamplerConfig(chi="sparse", **kw), witnesses=64)
+    assert a.logical_error_shots > 0
+    assert a.witnesses == b.witnesses
+    assert a.logical_error_shots == b.logical_error_shots
