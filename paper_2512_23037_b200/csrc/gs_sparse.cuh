@@ -425,37 +425,63 @@ __device__ __forceinline__ PivotBoth sp_pivot_both(SpChi &s, const PivotGeo &g, 
   r.pp = 0.0; r.sump = 0.0; r.summ = 0.0;
   r.nzp = 0; r.nzm = 0;
   u32 bp = 0, bm = 0;
+  // two rounds per iteration, both rounds' partner probes in flight first
+  // (as sp_butterfly)
 #pragma unroll 1
-  for (u32 i0 = 0; i0 < s.n; i0 += 32) {
-    const u32 i = i0 + lane;
-    bool act = i < s.n;
-    u32 rep = 0, part = 0, j = 0;
-    double2 vr = Z, vp = Z;
-    if (act) j = s.key[i];
-    const int ip = sp_partner(s, small, act, j, g.cb, lane);
-    if (act) {
-      const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
-      const u32 j0 = j & ~(1u << g.isq);
-      if (((j >> g.isq) & 1u) == (g.ct ^ par32(j0 & g.tmask))) {
-        rep = j;
-        part = j ^ g.cb;
-        vr = v;
-        if (ip >= 0) vp = ps != 1.0 ? cscale(s.amp[ip], ps) : s.amp[ip];
-      } else {
-        part = j;
-        rep = j ^ g.cb;
-        vp = v;
-        act = ip < 0;   // else the rep entry handles the pair
-      }
+  for (u32 i0 = 0; i0 < s.n; i0 += 64) {
+    u32 j[2];
+    int ip[2];
+    bool in[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const u32 i = i0 + 32u * u + lane;
+      in[u] = i < s.n;
+      j[u] = in[u] ? s.key[i] : 0u;
     }
-    const double2 pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, vp);
-    const double2 wp = cadd(vr, pr), wm = csub(vr, pr);
-    if (act) r.pp = __dadd_rn(r.pp, abs2(wp));
-    const u32 key = (rep & lo) | ((rep >> 1) & ~lo);
-    const bool kp = act && sp_keep(wp, r.sump, r.nzp);
-    bp = sp_put(s.kb[ob], s.ab[ob], bp, kp, key, wp, lane);
-    const bool km = act && sp_keep(wm, r.summ, r.nzm);
-    bm = sp_put(s.kb[ob] + half, s.ab[ob] + half, bm, km, key, wm, lane);
+    if (small) {   // one round (n <= 32)
+      ip[0] = sp_partner(s, true, in[0], j[0], g.cb, lane);
+      ip[1] = -1;
+    } else {
+      u32 h[2];
+      u64 e[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        h[u] = sp_hash(j[u] ^ g.cb, s.hcur);
+        e[u] = in[u] ? sp_probe(s, h[u]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) ip[u] = in[u] ? sp_resolve(s, j[u] ^ g.cb, h[u], e[u]) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const u32 i = i0 + 32u * u + lane;
+      bool act = in[u];
+      u32 rep = 0, part = 0;
+      double2 vr = Z, vp = Z;
+      if (act) {
+        const double2 v = ps != 1.0 ? cscale(s.amp[i], ps) : s.amp[i];
+        const u32 j0 = j[u] & ~(1u << g.isq);
+        if (((j[u] >> g.isq) & 1u) == (g.ct ^ par32(j0 & g.tmask))) {
+          rep = j[u];
+          part = j[u] ^ g.cb;
+          vr = v;
+          if (ip[u] >= 0) vp = ps != 1.0 ? cscale(s.amp[ip[u]], ps) : s.amp[ip[u]];
+        } else {
+          part = j[u];
+          rep = j[u] ^ g.cb;
+          vp = v;
+          act = ip[u] < 0;   // else the rep entry handles the pair
+        }
+      }
+      const double2 pr = cmul((g.dc ^ par32(part & g.dmask)) ? xpm : xpp, vp);
+      const double2 wp = cadd(vr, pr), wm = csub(vr, pr);
+      if (act) r.pp = __dadd_rn(r.pp, abs2(wp));
+      const u32 key = (rep & lo) | ((rep >> 1) & ~lo);
+      const bool kp = act && sp_keep(wp, r.sump, r.nzp);
+      bp = sp_put(s.kb[ob], s.ab[ob], bp, kp, key, wp, lane);
+      const bool km = act && sp_keep(wm, r.summ, r.nzm);
+      bm = sp_put(s.kb[ob] + half, s.ab[ob] + half, bm, km, key, wm, lane);
+    }
   }
   __syncwarp();
   np = bp;
