@@ -51,9 +51,9 @@ def test_records_beyond_shared_memory_slot():
     b = sample(prog, SamplerConfig(shots=16, master_seed=3, postselect=True))
     assert b.records.shape[1] == (prog.num_measurements + 63) // 64
     # the same in every kernel form (warp per shot: record words beyond the
-    # 32 register slots go to the global buffer; block per shot)
+    # 32 register slots go to the global buffer; block per shot; sparse)
     from paper_2512_23037_b200 import _lib
-    for extra in (_lib.GS_WIDE_ONLY, _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK):
+    for extra in (_lib.GS_WIDE_ONLY, _lib.GS_WIDE_ONLY | _lib.GS_CHI_BLOCK, _lib.GS_SPARSE):
         got = sample(prog, SamplerConfig(shots=8, master_seed=2), extra_flags=extra)
         ref = sample(prog, SamplerConfig(shots=8, master_seed=2))
         assert np.array_equal(got.status, ref.status) and np.array_equal(got.records, ref.records)
@@ -79,6 +79,7 @@ def test_64_qubit_masks():
     prog = parse_circuit("\n".join(lines) + "\n")
     assert prog.num_qubits == 64
     _check(prog, 9, 48, dict(postselect=True), 4096)
+    _check(prog, 9, 48, dict(postselect=True, chi="sparse"), 4096)
 
 
 def test_witnesses_replay_to_logical_errors():
@@ -168,6 +169,7 @@ def test_long_noise_stretch_inside_a_wide_section_splitmix():
     assert dp.num_locations > 2048
     for post in (False, True):
         _check(prog, 12, 48, dict(postselect=post), 4096)
+        _check(prog, 12, 48, dict(postselect=post, chi="sparse"), 4096)   # same noise scan
 
 
 def test_narrow_limit5_records_beyond_register_words():
@@ -210,3 +212,4 @@ def test_thousand_location_instruction_across_the_ring_splitmix():
     prog = parse_circuit("\n".join(body) + "\n")
     for post in (False, True):
         _check(prog, 31, 48, dict(postselect=post), 4096)
+        _check(prog, 31, 48, dict(postselect=post, chi="sparse"), 4096)
