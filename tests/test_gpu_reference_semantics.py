@@ -3,7 +3,8 @@ the CUDA path (ref tests/test_sampler.py:100-199, tests/test_state.py:72-106,
 tests/test_noise.py:62-80).  Single shots go through ``run_shot`` with an
 explicit SplitMix seed exactly like the reference's ``run_text`` helper;
 batch properties through ``run_batch`` / ``sample``; rates against the
-closed forms the reference checks (binomial z < 5)."""
+closed forms the reference checks (binomial z < 5).  Every test runs on the
+default chi form and again forced onto the sparse form (GS_SPARSE)."""
 
 import math
 
@@ -16,6 +17,25 @@ from oracle import gstab_oracle as orc
 from paper_2512_23037_b200 import (SamplerConfig, ShotContext, derive_seed,
                                    parse_circuit, run_batch, run_shot, sample)
 from paper_2512_23037_b200.sampler import ShotStatus, _records_before
+
+
+@pytest.fixture(autouse=True, params=["auto", "sparse"])
+def chi_form(request, monkeypatch):
+    """Run the test on the default form, then with every run_batch / sample /
+    run_shot planned onto the sparse form (where its capacity limit allows)."""
+    if request.param == "sparse" and "criterion_9" in request.node.name:
+        pytest.skip("throughput criteria are measured on the default form")
+    if request.param == "sparse":
+        from dataclasses import replace
+        from paper_2512_23037_b200 import sampler as smp
+        orig = smp._plan
+
+        def sparse_plan(prog, cfg):
+            if cfg.effective_capacity <= smp.SPARSE_MAX_CAPACITY:
+                cfg = replace(cfg, chi="sparse")
+            return orig(prog, cfg)
+        monkeypatch.setattr(smp, "_plan", sparse_plan)
+    return request.param
 
 
 def run_text(text, seed=0, shot=0, **kw):
