@@ -24,13 +24,14 @@ from stats_check import assert_rates_agree
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "config1_records.npz")
 
 
-def test_config1_all_1e5_shots_bit_exact():
+@pytest.mark.parametrize("chi", ["auto", "sparse"])
+def test_config1_all_1e5_shots_bit_exact(chi):
     g = np.load(GOLDEN)
     prog = parse_circuit(str(g["text"]))
     shots = len(g["status"])
     assert shots == 100_000
     b = sample(prog, SamplerConfig(shots=shots, master_seed=int(g["master"]),
-                                   postselect=True))
+                                   postselect=True, chi=chi))
     assert np.array_equal(b.status, g["status"])
     m = int(g["num_measurements"])
     want = np.unpackbits(g["records"], axis=1, bitorder="little")[:, :m]
@@ -39,10 +40,11 @@ def test_config1_all_1e5_shots_bit_exact():
 
 @pytest.mark.parametrize("n,t", [(20, 8), (24, 16), (32, 24), (64, 32)])
 @pytest.mark.parametrize("cap,rerun", [(64, False), (256, True), (4096, True)])
-def test_config4_overflow_parity(n, t, cap, rerun):
+@pytest.mark.parametrize("chi", ["auto", "sparse"])
+def test_config4_overflow_parity(n, t, cap, rerun, chi):
     prog = apply_noise_model(config4_circuit(n, t, seed=n + t), 2e-3)
     cfg = SamplerConfig(shots=6, master_seed=n * t, entry_capacity=cap,
-                        rerun_on_overflow=rerun, postselect=False)
+                        rerun_on_overflow=rerun, postselect=False, chi=chi)
     b = sample(prog, cfg)
     flat = list(prog.flat())
     for s in range(6):
@@ -98,13 +100,14 @@ def test_d5_full_size_properties():
     assert int(c[_lib.GS_C_ERROR_SHOTS]) == a.logical_error_shots
 
 
-@pytest.mark.parametrize("narrow", [0, _lib.GS_NARROW_K5])
+@pytest.mark.parametrize("narrow", [0, _lib.GS_NARROW_K5, _lib.GS_SPARSE])
 @pytest.mark.parametrize("name", ["msc_d5_table2_records.npz", "msc_d3_table2_records.npz",
                                   "msc_d5_records.npz", "msc_d3_records.npz"])
 def test_msc_golden_records_bit_exact(name, narrow):
     """Headline workloads: every one of the 20,000 reference-generated shots
     (statuses, discarding detector, observable, record bits) bit-exact, at
-    either narrow chi limit (4, or 5 with GS_NARROW_K5)."""
+    either narrow chi limit (4, or 5 with GS_NARROW_K5), and on the sparse
+    chi form (GS_SPARSE)."""
     g = np.load(os.path.join(os.path.dirname(__file__), "golden", name))
     prog = parse_circuit(str(g["text"]))
     shots = len(g["status"])
