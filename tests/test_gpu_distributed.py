@@ -22,7 +22,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _cancelled_t(nq):
+    from paper_2512_23037_b200 import parse_circuit
+    body = "".join("H %d\nT %d\nDEPOLARIZE1(0.01) %d\nT_DAG %d\nH %d\n" % (q, q, q, q, q)
+                   for q in range(nq))
+    return parse_circuit(body + "M " + " ".join(map(str, range(nq))) + "\nDETECTOR rec[-1]\n")
+
+
+def _worker(rank, world, port, out, which="grown"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -32,7 +39,10 @@ def _worker(rank, world, port, out):
         from paper_2512_23037_b200.distributed import run_batch_distributed
         from paper_2512_23037_b200.msc import msc_grown_circuit
         from paper_2512_23037_b200.noise import apply_noise_model
-        prog = apply_noise_model(msc_grown_circuit(5), 1e-3)
+        if which == "grown":
+            prog = apply_noise_model(msc_grown_circuit(5), 1e-3)
+        else:   # past the dense dimension limit: the shards run the sparse form
+            prog = _cancelled_t(22)
         cfg = SamplerConfig(shots=200_001, master_seed=5, postselect=True, rng="philox")
         st = run_batch_distributed(prog, cfg)
         out[rank] = st.as_dict()
@@ -55,4 +65,20 @@ def test_two_ranks_equal_one_process():
             "overflow_count")
     for r in (0, 1):
         for k in keys:
+            assert out[r][k] == one[k], (r, k)
+
+
+def test_two_ranks_on_the_sparse_form():
+    """A program past the dense dimension limit (22 cancelled T blocks):
+    the shards take the sparse form; the reduced counters equal a
+    one-process run_batch (which probes, then runs sparse)."""
+    from paper_2512_23037_b200 import SamplerConfig, run_batch
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker, args=(2, _free_port(), out, "sparse"), nprocs=2, join=True,
+                       start_method="spawn")
+    one = run_batch(_cancelled_t(22), SamplerConfig(shots=200_001, master_seed=5,
+                                                    postselect=True, rng="philox")).as_dict()
+    for r in (0, 1):
+        for k in ("total_shots", "preserved_shots", "discarded_shots", "overflow_count"):
             assert out[r][k] == one[k], (r, k)
