@@ -867,7 +867,11 @@ int gs_engine_section_stats(gs_engine *e, uint64_t *out, uint32_t cap, uint32_t 
     o[GS_SEC_PC0] = e->sec_meta[2 * i + 1];
   }
   if (reset) {
-    if (e->d_secstats) CUDA_TRY(cudaMemset(e->d_secstats, 0, (e->secstats_cap * 4 + 1) * 8));
+    if (e->d_secstats) {
+      // legacy-stream memset: finish it before a launch on a non-blocking stream
+      CUDA_TRY(cudaMemset(e->d_secstats, 0, (e->secstats_cap * 4 + 1) * 8));
+      CUDA_TRY(cudaDeviceSynchronize());
+    }
     for (auto &t : e->timed) { e->spare_ev.push_back(t.a); e->spare_ev.push_back(t.b); }
     e->timed.clear();
   }
