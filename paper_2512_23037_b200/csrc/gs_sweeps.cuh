@@ -102,6 +102,35 @@ __device__ __forceinline__ double2 t_mix(const Gate &g, double2 v, double2 w, u3
   return cadd(cmul(g.a, v), neg_if(cmul(g.bx0, w), m >> 31));
 }
 
+#ifndef GS_SGN_OPERAND
+#define GS_SGN_OPERAND 1   // A/B r02sgn: +2.0 % headline, +2.0 % grown proxy
+#endif
+// t_mix with the sign already in the b operand: (-ss) w == -(ss w) and
+// cmul(-b, w) == -cmul(b, w) bit for bit, so flipping the operand once per
+// sign class (4 per gate and group) replaces flipping each product, and the
+// flip leaves the FP64 dependency chain
+// (reduced form only: the full form's two-word operand flip measured more
+// instructions than the product flips)
+struct SgnOp {
+  double ss;
+  u32 m;
+};
+template <bool kR>
+__device__ __forceinline__ SgnOp sgn_op(const Gate &g, u32 m) {
+  SgnOp o;
+  o.ss = kR ? flip_hi(g.ss, m) : 0.0;
+  o.m = m;
+  return o;
+}
+template <bool kR>
+__device__ __forceinline__ double2 t_mix_s(const Gate &g, double2 v, double2 w, const SgnOp &o) {
+  if (kR) {
+    const double px = __dmul_rn(o.ss, w.y), py = __dmul_rn(o.ss, w.x);
+    return make_double2(__fma_rn(kTc, v.x, -px), __fma_rn(kTc, v.y, py));
+  }
+  return t_mix<false>(g, v, w, o.m);
+}
+
 // T with beta in span: new[j] = a v_j + b_j v_{j^cb} (ref state.py:127-129,
 // 294-306: a-term then b-term); no renormalisation pending (caller)
 template <bool kS, int kG = 1, bool kR = false>
@@ -122,8 +151,13 @@ __device__ __forceinline__ SumNz sweep_butterfly(double2 *A_, u32 half, const Ga
     const u32 j0 = jr | jl, j1 = j0 ^ cb;
     const double2 v0 = A[j0], v1 = A[j1];
     const u32 m0 = (pl ^ par32(jr & dmask)) << 31, m1 = m0 ^ pcb;
+#if GS_SGN_OPERAND
+    A[j0] = prune_acc(t_mix_s<kR>(g, v0, v1, sgn_op<kR>(g, m1)), r.sum, r.nz);
+    A[j1] = prune_acc(t_mix_s<kR>(g, v1, v0, sgn_op<kR>(g, m0)), r.sum, r.nz);
+#else
     A[j0] = prune_acc(t_mix<kR>(g, v0, v1, m1), r.sum, r.nz);
     A[j1] = prune_acc(t_mix<kR>(g, v1, v0, m0), r.sum, r.nz);
+#endif
   }
   return r;
 }
@@ -170,16 +204,31 @@ __device__ __forceinline__ SumNz2 sweep_butterfly2(double2 *A_, u32 quarter, con
     const u32 p1 = (l1 ^ par32(jr & g1.dmask)) << 31, p2 = (l2 ^ par32(jr & g2.dmask)) << 31;
     // gate 1: pairs (x0, x1), (x2, x3)
     const u32 s0 = p1, s1 = p1 ^ a1, s2 = p1 ^ b1, s3 = p1 ^ a1 ^ b1;
+    // gate 2: pairs (x0, x2), (x1, x3)
+    const u32 t0 = p2, t1 = p2 ^ a2, t2 = p2 ^ b2, t3 = p2 ^ a2 ^ b2;
+#if GS_SGN_OPERAND
+    const SgnOp o0 = sgn_op<kR>(g1, s0), o1 = sgn_op<kR>(g1, s1), o2 = sgn_op<kR>(g1, s2),
+                o3 = sgn_op<kR>(g1, s3);
+    const double2 u0 = prune_acc(t_mix_s<kR>(g1, v0, v1, o1), dummy, r.nz1);
+    const double2 u1 = prune_acc(t_mix_s<kR>(g1, v1, v0, o0), dummy, r.nz1);
+    const double2 u2 = prune_acc(t_mix_s<kR>(g1, v2, v3, o3), dummy, r.nz1);
+    const double2 u3 = prune_acc(t_mix_s<kR>(g1, v3, v2, o2), dummy, r.nz1);
+    const SgnOp q0 = sgn_op<kR>(g2, t0), q1 = sgn_op<kR>(g2, t1), q2 = sgn_op<kR>(g2, t2),
+                q3 = sgn_op<kR>(g2, t3);
+    A[x0] = prune_acc(t_mix_s<kR>(g2, u0, u2, q2), r.sum, r.nz);
+    A[x2] = prune_acc(t_mix_s<kR>(g2, u2, u0, q0), r.sum, r.nz);
+    A[x1] = prune_acc(t_mix_s<kR>(g2, u1, u3, q3), r.sum, r.nz);
+    A[x3] = prune_acc(t_mix_s<kR>(g2, u3, u1, q1), r.sum, r.nz);
+#else
     const double2 u0 = prune_acc(t_mix<kR>(g1, v0, v1, s1), dummy, r.nz1);
     const double2 u1 = prune_acc(t_mix<kR>(g1, v1, v0, s0), dummy, r.nz1);
     const double2 u2 = prune_acc(t_mix<kR>(g1, v2, v3, s3), dummy, r.nz1);
     const double2 u3 = prune_acc(t_mix<kR>(g1, v3, v2, s2), dummy, r.nz1);
-    // gate 2: pairs (x0, x2), (x1, x3)
-    const u32 t0 = p2, t1 = p2 ^ a2, t2 = p2 ^ b2, t3 = p2 ^ a2 ^ b2;
     A[x0] = prune_acc(t_mix<kR>(g2, u0, u2, t2), r.sum, r.nz);
     A[x2] = prune_acc(t_mix<kR>(g2, u2, u0, t0), r.sum, r.nz);
     A[x1] = prune_acc(t_mix<kR>(g2, u1, u3, t3), r.sum, r.nz);
     A[x3] = prune_acc(t_mix<kR>(g2, u3, u1, t1), r.sum, r.nz);
+#endif
   }
   (void)dummy;
   return r;
